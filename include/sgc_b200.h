@@ -1,0 +1,229 @@
+/*
+ * sgc_b200.h -- C ABI of the B200-native SubGCache in-batch serving hot path.
+ *
+ * Drop-in boundary for the reference's hot-path C++ API (paths relative to
+ * /root/reference/proj). Each entry point names the reference interface it
+ * replaces; INTEGRATION.md shows the reference-side binding. All calls are
+ * synchronous at return, stream-ordered on the context's stream, and report
+ * errors through an int status plus a thread-local message (sgc_last_error),
+ * mirroring the reference's exception taxonomy (include/subgcache/errors.hpp:9-32):
+ *
+ *   SGC_OK 0, SGC_DOMAIN 1 (DomainError), SGC_CAPACITY 2 (CapacityError),
+ *   SGC_INTEGRITY 3 (IntegrityError), SGC_PARSE 4 (ParseError),
+ *   SGC_LOGIC 5 (std::logic_error), SGC_CUDA 6 (device / runtime failure).
+ *
+ * Pointers to array data may be host or device memory (unified addressing); the
+ * library copies as needed. No torch types cross this boundary.
+ */
+#ifndef SGC_B200_H
+#define SGC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    SGC_OK = 0,
+    SGC_DOMAIN = 1,
+    SGC_CAPACITY = 2,
+    SGC_INTEGRITY = 3,
+    SGC_PARSE = 4,
+    SGC_LOGIC = 5,
+    SGC_CUDA = 6
+};
+
+/* clustering.hpp:11 enum class Linkage */
+enum { SGC_WARD = 0, SGC_SINGLE = 1, SGC_AVERAGE = 2, SGC_COMPLETE = 3, SGC_CENTROID = 4 };
+
+#define SGC_VOCAB 260 /* tokenizer.hpp:15-19: 256 bytes + BOS/EOS/PAD/GRAPH_SOFT_SLOT */
+
+typedef struct sgc_ctx sgc_ctx;     /* one CUDA device + stream + scratch arena */
+typedef struct sgc_model sgc_model; /* ToyLm weights, bf16 in HBM (lm_core.hpp:114-171) */
+typedef struct sgc_graph sgc_graph; /* TextualGraph pre-rendered rows + text features */
+typedef struct sgc_kv sgc_kv;       /* sealed prefix segments (KVCache::seal, lm_core.cpp:60-80) */
+
+/* lm_core.hpp:16-27 ToyLmConfig */
+typedef struct {
+    uint32_t layers, heads, model_dim, ffn_hidden, max_seq_len, max_new_tokens;
+    uint64_t seed;
+} sgc_lm_config;
+
+/* encoders.hpp:17-21 TextEncoderConfig + :44-49 GnnEncoderConfig */
+typedef struct {
+    uint32_t layers, heads, dim;
+    uint64_t seed;      /* GnnEncoderConfig::seed (pipeline.cpp:138: splitmix64_once(seed^0x62)) */
+    uint64_t text_seed; /* TextEncoderConfig::seed, default 1 */
+    uint64_t text_salt; /* TextEncoderConfig::hash_salt, default 55 */
+} sgc_gnn_config;
+
+/* A batch of subgraphs of one graph in CSR form: subgraph i owns node ids
+ * nodes[node_off[i] .. node_off[i+1]) and edge indices edges[edge_off[i] .. edge_off[i+1]),
+ * both ascending (std::set order, graph_store.hpp:39-49). */
+typedef struct {
+    uint32_t count;
+    const uint64_t* node_off;
+    const uint32_t* nodes;
+    const uint64_t* edge_off;
+    const uint32_t* edges;
+} sgc_subgraphs;
+
+/* Ragged int32 token lists: list i = tokens[off[i] .. off[i+1]). */
+typedef struct {
+    uint32_t count;
+    const uint64_t* off;
+    const int32_t* tokens;
+} sgc_token_lists;
+
+const char* sgc_last_error(void);
+const char* sgc_version(void);
+
+/* ---- context ------------------------------------------------------------------ */
+int sgc_ctx_create(int device, sgc_ctx** out);
+int sgc_ctx_destroy(sgc_ctx* ctx);
+/* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the own stream. */
+int sgc_ctx_set_stream(sgc_ctx* ctx, void* stream);
+/* Number of kernel launches issued by this context since creation (bench evidence). */
+uint64_t sgc_ctx_launch_count(const sgc_ctx* ctx);
+
+/* ---- model: ToyLm::ToyLm (lm_core.cpp:122-161) -------------------------------------
+ * Weights are generated ON DEVICE from the seed, element-for-element identical to the
+ * reference's fp32 SplitMix64 streams, then stored as bf16 (GEMM operands) and fp32
+ * (token embedding, head). RoPE tables are computed on the host exactly as the reference. */
+int sgc_model_create(sgc_ctx* ctx, const sgc_lm_config* cfg, sgc_model** out);
+int sgc_model_destroy(sgc_model* model);
+/* Copy one generated fp32 weight tensor to `out` (test hook): which = 0 tok_embedding,
+ * 1 head, 2 wqkv, 3 wo, 4 w1, 5 w2 (fp32 values reconstructed from the bf16 copy for 2..5
+ * when fp32 == 0, or the exact fp32 stream when fp32 == 1). */
+int sgc_model_weight(sgc_model* model, int which, uint32_t layer, int fp32, float* out, size_t n);
+
+/* ---- graph: TextualGraph (graph_store.hpp:28-35) -------------------------------------
+ * Node ids ascending; node i's attribute text is node_text[node_off[i] .. node_off[i+1]).
+ * Edge e = (edge_src[e], edge_text[..], edge_dst[e]). Rows are pre-rendered once
+ * (serialize_subgraph_rows, graph_store.cpp:249-262) and the text encoder's token hashes
+ * computed (encoders.cpp:62-80): host string work, done at ingest. */
+int sgc_graph_upload(sgc_ctx* ctx, uint32_t n_nodes, const uint32_t* node_ids,
+                     const char* node_text, const uint64_t* node_off, uint32_t n_edges,
+                     const uint32_t* edge_src, const uint32_t* edge_dst, const char* edge_text,
+                     const uint64_t* edge_off, sgc_graph** out);
+int sgc_graph_destroy(sgc_graph* g);
+
+/* ---- (1) subgraph embedding: GnnEncoder::encode (encoders.hpp:61, encoders.cpp:122-186) --
+ * Batched over subgraphs; out [count * dim] fp32. DomainError on an empty subgraph. */
+int sgc_encode_subgraphs(sgc_ctx* ctx, sgc_graph* g, const sgc_gnn_config* cfg,
+                         const sgc_subgraphs* subs, float* out);
+/* TextEncoder::embed of every node then every edge text, out [(n_nodes+n_edges) * dim]. */
+int sgc_text_features(sgc_ctx* ctx, sgc_graph* g, uint32_t dim, uint64_t seed, uint64_t salt,
+                      float* out);
+
+/* ---- (2) clustering (clustering.hpp:35,44; clustering.cpp:33-174) -------------------- */
+int sgc_pairwise_distances(sgc_ctx* ctx, const float* emb, uint32_t m, uint32_t dim,
+                           double* out /* [m*m] */);
+/* labels [m]; merge_left/right [m-c] = min member of the kept / absorbed cluster
+ * (MergeStep::left.front()/right.front()); merge_dist [m-c] = MergeStep::distance;
+ * op_count = ClusterAssignment::op_count. Any of the outputs may be NULL. */
+int sgc_agglomerate(sgc_ctx* ctx, const float* emb, uint32_t m, uint32_t dim, int linkage,
+                    uint32_t c, uint32_t* labels, uint32_t* merge_left, uint32_t* merge_right,
+                    double* merge_dist, uint64_t* op_count);
+
+/* ---- (3) representative construction ------------------------------------------------
+ * merge_subgraphs (graph_store.cpp:223-235) + build_prompt (cache_engine.cpp:29-71) +
+ * Tokenizer::tokenize (tokenizer.cpp:5-11) for every cluster in one pass: members of
+ * cluster k are the subgraphs i with labels[i] == k. Outputs (host or device):
+ *   rep_nodes/rep_edges : CSR of the union (ascending) -- offsets [c+1]
+ *   prefix              : BOS + prefix bytes per cluster -- offsets [c+1]
+ *   dropped             : [2c] dropped node rows, dropped edge rows per cluster
+ * Capacities are checked; SGC_CAPACITY if headers alone exceed the budget.
+ * budget_tokens = PromptBudget::prefix_budget() (cache_engine.hpp:27-30). */
+int sgc_build_representatives(sgc_ctx* ctx, sgc_graph* g, const sgc_subgraphs* subs,
+                              const uint32_t* labels, uint32_t c, uint32_t budget_tokens,
+                              uint64_t* rep_node_off, uint32_t* rep_nodes, uint64_t rep_node_cap,
+                              uint64_t* rep_edge_off, uint32_t* rep_edges, uint64_t rep_edge_cap,
+                              uint64_t* prefix_off, int32_t* prefix, uint64_t prefix_cap,
+                              uint32_t* dropped);
+
+/* ---- (4) KV precompute: ToyLm::prefill + KVCache::seal (lm_core.cpp:299-327, :60-80) --
+ * Prefills `seqs.count` sequences in one batched pass (varlen causal attention) into a
+ * paged bf16 KV pool and seals them. soft (optional) [count * model_dim] with
+ * soft_mask[i] != 0 selecting sequences that carry a GRAPH_SOFT_SLOT at position 0.
+ * last_logits (optional) [count * 260]. CapacityError if a sequence exceeds max_seq_len. */
+int sgc_prefill(sgc_ctx* ctx, sgc_model* model, const sgc_token_lists* seqs, const float* soft,
+                const uint8_t* soft_mask, sgc_kv** out, float* last_logits);
+int sgc_kv_release(sgc_kv* kv);
+uint32_t sgc_kv_count(const sgc_kv* kv);
+/* KVCache::token_count of sealed segment i */
+uint64_t sgc_kv_tokens(const sgc_kv* kv, uint32_t i);
+/* KVCache::prefix_digest analogue: FNV-1a over segment i's bf16 K/V bytes, layer-major */
+uint64_t sgc_kv_digest(const sgc_kv* kv, uint32_t i);
+/* KVCache::resident_kv_bytes analogue for the whole handle (bf16 storage) */
+uint64_t sgc_kv_resident_bytes(const sgc_kv* kv);
+/* Copy segment i, layer l, K (is_v=0) or V as fp32 [tokens * model_dim] (test hook). */
+int sgc_kv_read(const sgc_kv* kv, uint32_t i, uint32_t layer, int is_v, float* out);
+
+/* ---- (5) per-query reuse: KVCache::fork + ToyLm::extend + first greedy token ----------
+ * (lm_core.cpp:82-90, :329-339, :352-390; cache_engine.cpp:183-189)
+ * Member j forks sealed segment member_seg[j] and extends it with its question tokens;
+ * all members of all segments run in ONE batched pass (cascade attention: shared prefix
+ * KV read once per query tile for every member of the segment). Private suffixes are
+ * released at return (KVCache::release_suffix). Outputs (optional):
+ *   logits      [count * 260]  last-position logits after the extend
+ *   first_token [count]        greedy_argmax with the copy-pointer bias: answer j (may be
+ *                              empty) searched in the segment's prefix tokens
+ *                              (CopyPointerHint::search_limit = prefix length).
+ * CapacityError if prefix + question exceeds max_seq_len. */
+int sgc_extend(sgc_ctx* ctx, sgc_model* model, sgc_kv* kv, const uint32_t* member_seg,
+               const sgc_token_lists* questions, const sgc_token_lists* answers,
+               float pointer_bonus, float* logits, int32_t* first_token);
+
+/* ---- the whole SubgCache branch: run() lines pipeline.cpp:212-293 + run_batch -------- */
+typedef struct {
+    sgc_subgraphs retrieved;   /* per query (retrieval is outside the hot path) */
+    sgc_token_lists questions; /* per query: question wrapper bytes (Tokenizer::encode_bytes) */
+    sgc_token_lists answers;   /* per query: copy-pointer target, count 0 = lookup off */
+    sgc_token_lists own_prefix;/* per query: BOS + own prompt prefix (fallback path) */
+    uint32_t clusters;         /* ClusterConfig::cluster_count */
+    int linkage;               /* SGC_WARD .. */
+    uint32_t question_budget;  /* RunConfig::question_budget (128) */
+    int soft_prefix;           /* RunConfig::soft_prefix_enabled() */
+    float pointer_bonus;       /* EngineOptions::pointer_bonus (100) */
+    sgc_gnn_config gnn;
+    /* multi-GPU: this rank serves only clusters k with owner[k] == rank when owner != NULL
+     * (embeddings must then be supplied gathered, see precomputed_embeddings) */
+    const float* precomputed_embeddings; /* [m * dim] or NULL to encode here */
+    const uint32_t* cluster_owner;       /* [c] or NULL = all clusters */
+    int rank;
+} sgc_batch;
+
+typedef struct {
+    float* embeddings;      /* [m * dim] optional */
+    uint32_t* labels;       /* [m] optional */
+    uint32_t* merge_left;   /* [m - c] optional */
+    uint32_t* merge_right;  /* [m - c] optional */
+    double* merge_dist;     /* [m - c] optional */
+    uint64_t* prefix_len;   /* [c] optional: representative prompt tokens (incl. soft slot) */
+    float* logits;          /* [m * 260] optional (rows of unserved queries untouched) */
+    int32_t* first_token;   /* [m] optional (-1 for queries not served by this rank) */
+    uint8_t* fallback;      /* [m] optional */
+    double stage_ms[8];     /* encode, cluster, represent, prefill, extend, total, -, - */
+    uint64_t prefill_rows, extend_rows; /* tokens pushed through prefill / extend */
+} sgc_batch_out;
+
+int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_batch* batch,
+                      sgc_batch_out* out);
+
+/* ---- GEMM building block (exposed for parity tests and the roofline bench) -----------
+ * D[M x N] = A[M x K] (bf16, row-major) * B[N x K]^T (bf16, row-major), fp32 accumulate in
+ * TMEM via tcgen05.mma; epi 0 = store fp32 D, 1 = store bf16 D, 2 = D += into fp32 `d`,
+ * 3 = bf16(tanh(D)). All pointers device. K % 64 == 0, N % 64 == 0. */
+int sgc_gemm_bf16(sgc_ctx* ctx, const void* a, const void* b, void* d, uint32_t M, uint32_t N,
+                  uint32_t K, int epi);
+/* Average device time in ms of the last `n` GEMM launches issued with timing enabled. */
+int sgc_set_timing(sgc_ctx* ctx, int enable);
+int sgc_get_timing(sgc_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGC_B200_H */

@@ -1,0 +1,164 @@
+"""ctypes binding of the C ABI in include/sgc_b200.h (libsgc_b200.so, built in-tree).
+
+The product path has no fallback: if the shared library is missing or no sm_100 device is
+present, loading fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsgc_b200.so")
+
+SGC_OK, SGC_DOMAIN, SGC_CAPACITY, SGC_INTEGRITY, SGC_PARSE, SGC_LOGIC, SGC_CUDA = range(7)
+VOCAB = 260
+
+
+class Error(RuntimeError):
+    """subgcache::Error (errors.hpp:9-12)."""
+
+
+class DomainError(Error, ValueError):
+    """errors.hpp:25-27."""
+
+
+class CapacityError(Error):
+    """errors.hpp:30-32."""
+
+
+class IntegrityError(Error):
+    """errors.hpp:20-22."""
+
+
+class ParseError(Error):
+    """errors.hpp:15-18."""
+
+
+class LogicError(Error):
+    """std::logic_error (lm_core.cpp:95, cache_engine.cpp:211)."""
+
+
+class CudaError(Error):
+    """device or runtime failure."""
+
+
+_EXC = {SGC_DOMAIN: DomainError, SGC_CAPACITY: CapacityError, SGC_INTEGRITY: IntegrityError,
+        SGC_PARSE: ParseError, SGC_LOGIC: LogicError, SGC_CUDA: CudaError}
+
+
+class LmConfig(C.Structure):
+    _fields_ = [("layers", C.c_uint32), ("heads", C.c_uint32), ("model_dim", C.c_uint32),
+                ("ffn_hidden", C.c_uint32), ("max_seq_len", C.c_uint32),
+                ("max_new_tokens", C.c_uint32), ("seed", C.c_uint64)]
+
+
+class GnnConfig(C.Structure):
+    _fields_ = [("layers", C.c_uint32), ("heads", C.c_uint32), ("dim", C.c_uint32),
+                ("seed", C.c_uint64), ("text_seed", C.c_uint64), ("text_salt", C.c_uint64)]
+
+
+class Subgraphs(C.Structure):
+    _fields_ = [("count", C.c_uint32), ("node_off", C.POINTER(C.c_uint64)),
+                ("nodes", C.POINTER(C.c_uint32)), ("edge_off", C.POINTER(C.c_uint64)),
+                ("edges", C.POINTER(C.c_uint32))]
+
+
+class TokenLists(C.Structure):
+    _fields_ = [("count", C.c_uint32), ("off", C.POINTER(C.c_uint64)),
+                ("tokens", C.POINTER(C.c_int32))]
+
+
+class Batch(C.Structure):
+    _fields_ = [("retrieved", Subgraphs), ("questions", TokenLists), ("answers", TokenLists),
+                ("own_prefix", TokenLists), ("clusters", C.c_uint32), ("linkage", C.c_int),
+                ("question_budget", C.c_uint32), ("soft_prefix", C.c_int),
+                ("pointer_bonus", C.c_float), ("gnn", GnnConfig),
+                ("precomputed_embeddings", C.POINTER(C.c_float)),
+                ("cluster_owner", C.POINTER(C.c_uint32)), ("rank", C.c_int)]
+
+
+class BatchOut(C.Structure):
+    _fields_ = [("embeddings", C.POINTER(C.c_float)), ("labels", C.POINTER(C.c_uint32)),
+                ("merge_left", C.POINTER(C.c_uint32)), ("merge_right", C.POINTER(C.c_uint32)),
+                ("merge_dist", C.POINTER(C.c_double)), ("prefix_len", C.POINTER(C.c_uint64)),
+                ("logits", C.POINTER(C.c_float)), ("first_token", C.POINTER(C.c_int32)),
+                ("fallback", C.POINTER(C.c_uint8)), ("stage_ms", C.c_double * 8),
+                ("prefill_rows", C.c_uint64), ("extend_rows", C.c_uint64)]
+
+
+# every symbol include/sgc_b200.h declares (checked by tests/test_boundary.py)
+EXPORTS = [
+    "sgc_last_error", "sgc_version", "sgc_ctx_create", "sgc_ctx_destroy", "sgc_ctx_set_stream",
+    "sgc_ctx_launch_count", "sgc_model_create", "sgc_model_destroy", "sgc_model_weight",
+    "sgc_graph_upload", "sgc_graph_destroy", "sgc_encode_subgraphs", "sgc_text_features",
+    "sgc_pairwise_distances", "sgc_agglomerate", "sgc_build_representatives", "sgc_prefill",
+    "sgc_kv_release", "sgc_kv_count", "sgc_kv_tokens", "sgc_kv_digest", "sgc_kv_resident_bytes",
+    "sgc_kv_read", "sgc_extend", "sgc_run_subgcache", "sgc_gemm_bf16", "sgc_set_timing",
+    "sgc_get_timing",
+]
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build the CUDA library first "
+            "(python -c 'import __graft_entry__ as g; g.build()'). There is no CPU fallback.")
+    L = C.CDLL(LIB_PATH)
+    P, vp = C.POINTER, C.c_void_p
+    L.sgc_last_error.restype = C.c_char_p
+    L.sgc_version.restype = C.c_char_p
+    L.sgc_ctx_create.argtypes = [C.c_int, P(vp)]
+    L.sgc_ctx_destroy.argtypes = [vp]
+    L.sgc_ctx_set_stream.argtypes = [vp, vp]
+    L.sgc_ctx_launch_count.argtypes = [vp]
+    L.sgc_ctx_launch_count.restype = C.c_uint64
+    L.sgc_model_create.argtypes = [vp, P(LmConfig), P(vp)]
+    L.sgc_model_destroy.argtypes = [vp]
+    L.sgc_model_weight.argtypes = [vp, C.c_int, C.c_uint32, C.c_int, P(C.c_float), C.c_size_t]
+    L.sgc_graph_upload.argtypes = [vp, C.c_uint32, P(C.c_uint32), C.c_char_p, P(C.c_uint64),
+                                   C.c_uint32, P(C.c_uint32), P(C.c_uint32), C.c_char_p,
+                                   P(C.c_uint64), P(vp)]
+    L.sgc_graph_destroy.argtypes = [vp]
+    L.sgc_encode_subgraphs.argtypes = [vp, vp, P(GnnConfig), P(Subgraphs), P(C.c_float)]
+    L.sgc_text_features.argtypes = [vp, vp, C.c_uint32, C.c_uint64, C.c_uint64, P(C.c_float)]
+    L.sgc_pairwise_distances.argtypes = [vp, P(C.c_float), C.c_uint32, C.c_uint32, P(C.c_double)]
+    L.sgc_agglomerate.argtypes = [vp, P(C.c_float), C.c_uint32, C.c_uint32, C.c_int, C.c_uint32,
+                                  P(C.c_uint32), P(C.c_uint32), P(C.c_uint32), P(C.c_double),
+                                  P(C.c_uint64)]
+    L.sgc_build_representatives.argtypes = [vp, vp, P(Subgraphs), P(C.c_uint32), C.c_uint32,
+                                            C.c_uint32, P(C.c_uint64), P(C.c_uint32), C.c_uint64,
+                                            P(C.c_uint64), P(C.c_uint32), C.c_uint64,
+                                            P(C.c_uint64), P(C.c_int32), C.c_uint64,
+                                            P(C.c_uint32)]
+    L.sgc_prefill.argtypes = [vp, vp, P(TokenLists), P(C.c_float), P(C.c_uint8), P(vp),
+                              P(C.c_float)]
+    L.sgc_kv_release.argtypes = [vp]
+    L.sgc_kv_count.argtypes = [vp]
+    L.sgc_kv_count.restype = C.c_uint32
+    L.sgc_kv_tokens.argtypes = [vp, C.c_uint32]
+    L.sgc_kv_tokens.restype = C.c_uint64
+    L.sgc_kv_digest.argtypes = [vp, C.c_uint32]
+    L.sgc_kv_digest.restype = C.c_uint64
+    L.sgc_kv_resident_bytes.argtypes = [vp]
+    L.sgc_kv_resident_bytes.restype = C.c_uint64
+    L.sgc_kv_read.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_int, P(C.c_float)]
+    L.sgc_extend.argtypes = [vp, vp, vp, P(C.c_uint32), P(TokenLists), P(TokenLists), C.c_float,
+                             P(C.c_float), P(C.c_int32)]
+    L.sgc_run_subgcache.argtypes = [vp, vp, vp, P(Batch), P(BatchOut)]
+    L.sgc_gemm_bf16.argtypes = [vp, vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]
+    L.sgc_set_timing.argtypes = [vp, C.c_int]
+    L.sgc_get_timing.argtypes = [vp, C.c_char_p, P(C.c_double), P(C.c_uint64)]
+    _lib = L
+    return L
+
+
+def check(status: int) -> None:
+    if status != SGC_OK:
+        msg = load().sgc_last_error().decode(errors="replace")
+        raise _EXC.get(status, Error)(msg)

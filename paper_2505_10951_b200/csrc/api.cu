@@ -1,0 +1,1518 @@
+// api.cu -- C ABI (include/sgc_b200.h) and the C++ host orchestration of the SubGCache hot
+// path: graph ingest-side preparation, batched GNN encode, clustering, representative
+// construction, batched representative prefill and batched cascade member extend.
+//
+// Reference call stack being replaced (paths under /root/reference/proj):
+//   pipeline.cpp:212-293  run() SubgCache branch  -> sgc_run_subgcache
+//   cache_engine.cpp:140-233 process_cluster / run_batch -> sgc_prefill + sgc_extend
+//   lm_core.cpp:179-297 ToyLm::forward (token-sequential)  -> forward_rows (row-batched)
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <numeric>
+#include <unordered_map>
+
+#include "attention.cuh"
+#include "cluster_kernels.cuh"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "gnn_kernels.cuh"
+#include "graph_kernels.cuh"
+#include "lm_kernels.cuh"
+#include "rng.cuh"
+
+using sgc::Ctx;
+using sgc::fail;
+using bf16 = __nv_bfloat16;
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return SGC_OK;
+    } catch (const sgc::Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = std::string("host allocation failed: ") + e.what();
+        return SGC_CUDA;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return SGC_LOGIC;
+    }
+}
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(
+               std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+
+template <typename T>
+T* dalloc(Ctx* c, size_t n) {
+    void* p = nullptr;
+    SGC_CUDA_CHECK(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), c->stream));
+    return static_cast<T*>(p);
+}
+inline void dfree(Ctx* c, void* p) {
+    if (p) cudaFreeAsync(p, c->stream);
+}
+
+// host copy of a possibly-device array
+template <typename T>
+std::vector<T> to_host(Ctx* c, const T* p, size_t n) {
+    std::vector<T> v(n);
+    if (n) {
+        SGC_CUDA_CHECK(cudaMemcpyAsync(v.data(), p, n * sizeof(T), cudaMemcpyDefault, c->stream));
+        SGC_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    }
+    return v;
+}
+
+std::string csv_quote(const std::string& f) {  // graph_store.cpp:237-247
+    if (f.find_first_of(",\"\n") == std::string::npos) return f;
+    std::string out = "\"";
+    for (char ch : f) {
+        if (ch == '"') out += "\"\"";
+        else out += ch;
+    }
+    return out + "\"";
+}
+
+// encoders.cpp:62-80 token hashing (host string work, once per graph)
+void hash_tokens(const char* s, size_t n, uint64_t salt, std::vector<uint32_t>& b,
+                 std::vector<int8_t>& sg) {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    size_t len = 0;
+    for (size_t i = 0; i <= n; ++i) {
+        unsigned char ch = i < n ? static_cast<unsigned char>(s[i]) : 0;
+        bool tok = i < n && ((ch >= '0' && ch <= '9') || (ch >= 'a' && ch <= 'z') ||
+                             (ch >= 'A' && ch <= 'Z') || ch >= 0x80);
+        if (tok) {
+            if (ch >= 'A' && ch <= 'Z') ch = static_cast<unsigned char>(ch - 'A' + 'a');
+            h ^= ch;
+            h *= 0x100000001b3ULL;
+            ++len;
+            continue;
+        }
+        if (len) {
+            uint64_t hh = sgc::splitmix64_once(h ^ salt);
+            b.push_back(static_cast<uint32_t>(hh % 4096));
+            sg.push_back(((hh >> 32) & 1) ? 1 : -1);
+            h = 0xcbf29ce484222325ULL;
+            len = 0;
+        }
+    }
+}
+
+const char kHeader[] = "Use the following graph to answer the question.\n\n";
+const char kNodeHdr[] = "node id,node attr";
+const char kEdgeHdr[] = "src,edge attr,dst";
+
+}  // namespace
+
+// ====================================================================== handles
+
+struct sgc_model {
+    Ctx* c = nullptr;
+    sgc_lm_config cfg{};
+    int d = 0, hd = 0, H = 0, L = 0, ffn = 0;
+    float* tok_emb = nullptr;  // fp32 [260 x d]
+    float* head = nullptr;     // fp32 [260 x d]
+    float* head_t = nullptr;   // fp32 [d x 260]
+    bf16* weights = nullptr;   // all layers, bf16
+    std::vector<bf16*> wqkv, wo, w1, w2;
+    float* rope_cos = nullptr;
+    float* rope_sin = nullptr;
+    uint64_t seed_states[6] = {};
+};
+
+struct sgc_graph {
+    Ctx* c = nullptr;
+    uint32_t n_nodes = 0, n_edges = 0;
+    std::vector<uint32_t> ids;  // ascending
+    std::vector<uint32_t> edge_src_idx, edge_dst_idx;  // dense node indices
+    uint32_t* d_ids = nullptr;
+    char* d_node_rows = nullptr;
+    uint64_t* d_node_row_off = nullptr;
+    uint32_t* d_node_row_len = nullptr;
+    char* d_edge_rows = nullptr;
+    uint64_t* d_edge_row_off = nullptr;
+    uint32_t* d_edge_row_len = nullptr;
+    // text hashes for nodes then edges, per salt
+    uint64_t hash_salt = ~0ull;
+    uint32_t* d_bucket = nullptr;
+    int8_t* d_sign = nullptr;
+    uint64_t* d_tok_off = nullptr;
+    std::vector<std::string> texts;  // node texts then edge texts (for re-hashing)
+};
+
+struct sgc_kv {
+    sgc_model* model = nullptr;
+    uint32_t n = 0;
+    std::vector<uint64_t> off, len;  // rows per segment in the KV region
+    uint64_t rows = 0;
+    bf16* k = nullptr;  // [L][rows x d]
+    bf16* v = nullptr;
+    int32_t* d_tokens = nullptr;  // context token ids (prefix, incl. soft slot)
+    uint64_t* d_tok_off = nullptr;
+    bf16* k_layer(int l) const { return k + static_cast<size_t>(l) * rows * model->d; }
+    bf16* v_layer(int l) const { return v + static_cast<size_t>(l) * rows * model->d; }
+};
+
+namespace {
+
+// ============================================================ model weights
+
+void check_lm_cfg(const sgc_lm_config& c) {
+    if (c.model_dim == 0 || c.heads == 0 || c.layers == 0)
+        fail(SGC_DOMAIN, "lm config needs layers, heads, dim >= 1");
+    if (c.model_dim % c.heads) fail(SGC_DOMAIN, "model_dim must be divisible by heads");
+    uint32_t hd = c.model_dim / c.heads;
+    if (hd != 16 && hd != 32 && hd != 64 && hd != 128)
+        fail(SGC_DOMAIN, "head_dim must be 16, 32, 64 or 128 on this backend");
+    if (c.model_dim % 64 || c.ffn_hidden % 64)
+        fail(SGC_DOMAIN, "model_dim and ffn_hidden must be multiples of 64 on this backend");
+}
+
+// ============================================================ row-batched forward
+
+struct FwdBatch {
+    int M = 0;
+    const int32_t* d_tokens = nullptr;  // [M]
+    const float* d_soft = nullptr;      // soft vectors
+    const int32_t* d_soft_idx = nullptr;  // [M] row -> soft vector index or -1
+    const int32_t* d_pos = nullptr;
+    const int32_t* d_seg_lo = nullptr;
+    const sgc::AttnWork* d_work = nullptr;
+    int n_work = 0;
+    // KV written by this batch: row r -> loc row r of (k_loc_layer(l), v_loc_layer(l))
+    std::function<bf16*(int)> k_loc, v_loc;
+    std::function<const bf16*(int)> k_pfx, v_pfx;
+    const int32_t* d_logit_rows = nullptr;
+    int n_logits = 0;
+    float* d_logits = nullptr;
+};
+
+void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
+    const int M = b.M, d = m->d;
+    if (M == 0) return;
+    float* x = c->buf<float>("fwd_x", static_cast<size_t>(M) * d);
+    bf16* xb = c->buf<bf16>("fwd_xb", static_cast<size_t>(M) * d);
+    bf16* q = c->buf<bf16>("fwd_q", static_cast<size_t>(M) * d);
+    bf16* ao = c->buf<bf16>("fwd_attn", static_cast<size_t>(M) * d);
+    bf16* h = c->buf<bf16>("fwd_h", static_cast<size_t>(M) * m->ffn);
+    int32_t* iota = c->buf<int32_t>("fwd_iota", M);
+    int* bad = c->buf<int>("fwd_bad", 1);
+    {
+        std::vector<int32_t> io(M);
+        std::iota(io.begin(), io.end(), 0);
+        sgc::copy_in(c, iota, io.data(), M);
+        SGC_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
+        SGC_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    }
+    sgc::embed(c, x, b.d_tokens, m->tok_emb, b.d_soft, b.d_soft_idx, d, M, bad);
+    for (int l = 0; l < m->L; ++l) {
+        sgc::rmsnorm_bf16(c, xb, x, d, M);
+        sgc::GemmEpi e;
+        e.mode = sgc::EPI_QKV;
+        e.q_out = q;
+        e.k_cache = b.k_loc(l);
+        e.v_cache = b.v_loc(l);
+        e.kv_row = iota;
+        e.pos = b.d_pos;
+        e.rope_cos = m->rope_cos;
+        e.rope_sin = m->rope_sin;
+        e.d = d;
+        e.hd = m->hd;
+        sgc::gemm_bf16(c, xb, m->wqkv[l], M, 3 * d, d, e);
+
+        sgc::AttnParams ap;
+        ap.q = q;
+        ap.out = ao;
+        ap.k_pfx = b.k_pfx ? b.k_pfx(l) : b.k_loc(l);
+        ap.v_pfx = b.v_pfx ? b.v_pfx(l) : b.v_loc(l);
+        ap.k_loc = b.k_loc(l);
+        ap.v_loc = b.v_loc(l);
+        ap.loc_kv0 = 0;
+        ap.seg_lo = b.d_seg_lo;
+        ap.work = b.d_work;
+        ap.d = d;
+        ap.scale = 1.0f / std::sqrt(static_cast<float>(m->hd));
+        sgc::cascade_attention(c, ap, b.n_work, m->H, m->hd);
+
+        sgc::GemmEpi r;
+        r.mode = sgc::EPI_RESID;
+        r.out = x;
+        r.ldo = d;
+        sgc::gemm_bf16(c, ao, m->wo[l], M, d, d, r);
+
+        sgc::rmsnorm_bf16(c, xb, x, d, M);
+        sgc::GemmEpi t;
+        t.mode = sgc::EPI_TANH;
+        t.out = h;
+        t.ldo = m->ffn;
+        sgc::gemm_bf16(c, xb, m->w1[l], M, m->ffn, d, t);
+        sgc::gemm_bf16(c, h, m->w2[l], M, d, m->ffn, r);
+    }
+    sgc::head_logits(c, b.d_logits, x, b.d_logit_rows, b.n_logits, m->head_t, d);
+    int hbad = 0;
+    SGC_CUDA_CHECK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (hbad) fail(SGC_DOMAIN, "token id out of vocab");
+}
+
+// tiles of <= 64 rows that never cross a `group` boundary (sequence for prefill, segment
+// for extend); rows of one group are contiguous
+std::vector<sgc::AttnWork> make_work(const std::vector<int>& group_start, const std::vector<int>& group_rows,
+                                     const std::vector<int>& pfx_kv0, const std::vector<int>& pfx_len) {
+    std::vector<sgc::AttnWork> w;
+    for (size_t g = 0; g < group_start.size(); ++g)
+        for (int r = 0; r < group_rows[g]; r += 64)
+            w.push_back({group_start[g] + r, std::min(64, group_rows[g] - r), pfx_kv0[g], pfx_len[g]});
+    return w;
+}
+
+// ============================================================ prefill / extend
+
+sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in, const int32_t* tok_in,
+                   const float* soft, const uint8_t* soft_mask, float* last_logits) {
+    std::vector<uint64_t> off = to_host(c, off_in, count + 1);
+    std::vector<int32_t> toks = to_host(c, tok_in, off[count]);
+    std::vector<uint8_t> smask = soft_mask ? to_host(c, soft_mask, count) : std::vector<uint8_t>(count, 0);
+    const int d = m->d;
+    auto kv = std::make_unique<sgc_kv>();
+    kv->model = m;
+    kv->n = count;
+    std::vector<int32_t> rows_tok, pos, seg_lo, soft_idx, logit_rows;
+    std::vector<uint64_t> ctx_off(1, 0);
+    bool any_soft = false;
+    for (uint32_t s = 0; s < count; ++s) {
+        uint64_t n = off[s + 1] - off[s];
+        bool has_soft = smask[s] != 0;
+        any_soft |= has_soft;
+        uint64_t total = n + (has_soft ? 1 : 0);
+        if (total > m->cfg.max_seq_len)
+            fail(SGC_CAPACITY, "prompt of " + std::to_string(total) + " tokens exceeds max " +
+                                   std::to_string(m->cfg.max_seq_len));
+        if (total == 0) fail(SGC_DOMAIN, "prefill: empty sequence");
+        int start = static_cast<int>(rows_tok.size());
+        kv->off.push_back(start);
+        kv->len.push_back(total);
+        if (has_soft) {
+            rows_tok.push_back(259);
+            soft_idx.push_back(static_cast<int32_t>(s));
+        }
+        for (uint64_t i = 0; i < n; ++i) {
+            rows_tok.push_back(toks[off[s] + i]);
+            soft_idx.push_back(-1);
+        }
+        for (uint64_t i = 0; i < total; ++i) {
+            pos.push_back(static_cast<int32_t>(i));
+            seg_lo.push_back(start);
+        }
+        logit_rows.push_back(static_cast<int32_t>(rows_tok.size() - 1));
+        ctx_off.push_back(rows_tok.size());
+    }
+    const int M = static_cast<int>(rows_tok.size());
+    kv->rows = M;
+    kv->k = dalloc<bf16>(c, static_cast<size_t>(m->L) * M * d);
+    kv->v = dalloc<bf16>(c, static_cast<size_t>(m->L) * M * d);
+    kv->d_tokens = dalloc<int32_t>(c, M);
+    kv->d_tok_off = dalloc<uint64_t>(c, count + 1);
+    sgc::copy_in(c, kv->d_tokens, rows_tok.data(), M);
+    sgc::copy_in(c, kv->d_tok_off, ctx_off.data(), count + 1);
+
+    int32_t* d_pos = c->buf<int32_t>("pf_pos", M);
+    int32_t* d_seg = c->buf<int32_t>("pf_seg", M);
+    int32_t* d_sidx = c->buf<int32_t>("pf_sidx", M);
+    int32_t* d_lr = c->buf<int32_t>("pf_lrows", count);
+    float* d_logits = c->buf<float>("pf_logits", static_cast<size_t>(count) * SGC_VOCAB);
+    float* d_soft = nullptr;
+    if (any_soft) {
+        d_soft = c->buf<float>("pf_soft", static_cast<size_t>(count) * d);
+        sgc::copy_in(c, d_soft, soft, static_cast<size_t>(count) * d);
+    }
+    std::vector<int> gs, gr, z(count, 0);
+    for (uint32_t s = 0; s < count; ++s) {
+        gs.push_back(static_cast<int>(kv->off[s]));
+        gr.push_back(static_cast<int>(kv->len[s]));
+    }
+    std::vector<sgc::AttnWork> work = make_work(gs, gr, z, z);
+    sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("pf_work", work.size());
+    sgc::copy_in(c, d_pos, pos.data(), M);
+    sgc::copy_in(c, d_seg, seg_lo.data(), M);
+    sgc::copy_in(c, d_sidx, soft_idx.data(), M);
+    sgc::copy_in(c, d_lr, logit_rows.data(), count);
+    sgc::copy_in(c, d_work, work.data(), work.size());
+
+    FwdBatch b;
+    b.M = M;
+    b.d_tokens = kv->d_tokens;
+    b.d_soft = d_soft;
+    b.d_soft_idx = any_soft ? d_sidx : nullptr;
+    b.d_pos = d_pos;
+    b.d_seg_lo = d_seg;
+    b.d_work = d_work;
+    b.n_work = static_cast<int>(work.size());
+    sgc_kv* kvp = kv.get();
+    b.k_loc = [kvp](int l) { return kvp->k_layer(l); };
+    b.v_loc = [kvp](int l) { return kvp->v_layer(l); };
+    b.d_logit_rows = d_lr;
+    b.n_logits = static_cast<int>(count);
+    b.d_logits = d_logits;
+    forward_rows(c, m, b);
+    sgc::copy_out(c, last_logits, d_logits, static_cast<size_t>(count) * SGC_VOCAB);
+    c->sync();
+    return kv.release();
+}
+
+// members: segment, question tokens, answers; returns logits/first token in member order
+void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg_in,
+               const uint64_t* q_off_in, const int32_t* q_in, const uint64_t* a_off_in,
+               const int32_t* a_in, float bonus, float* logits_out, int32_t* first_out,
+               uint64_t max_rows = 1ull << 16) {
+    if (n == 0) return;
+    const int d = m->d;
+    std::vector<uint32_t> seg = to_host(c, seg_in, n);
+    std::vector<uint64_t> qo = to_host(c, q_off_in, n + 1);
+    std::vector<int32_t> qt = to_host(c, q_in, qo[n]);
+    std::vector<uint64_t> ao;
+    std::vector<int32_t> at;
+    if (a_off_in) {
+        ao = to_host(c, a_off_in, n + 1);
+        at = to_host(c, a_in, ao[n]);
+    }
+    for (uint32_t j = 0; j < n; ++j) {
+        if (seg[j] >= kv->n) fail(SGC_DOMAIN, "extend: member references an unknown segment");
+        uint64_t qn = qo[j + 1] - qo[j];
+        if (qn == 0) fail(SGC_DOMAIN, "extend: empty question (KVCache::extend with zero tokens is a no-op)");
+        if (kv->len[seg[j]] + qn > m->cfg.max_seq_len)
+            fail(SGC_CAPACITY, "sequence length " + std::to_string(kv->len[seg[j]] + qn) + " exceeds max " +
+                                   std::to_string(m->cfg.max_seq_len));
+    }
+    // members grouped by segment (stable), processed in row chunks
+    std::vector<uint32_t> order(n);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return seg[a] < seg[b]; });
+    float* d_logits_all = c->buf<float>("ex_logits_all", static_cast<size_t>(n) * SGC_VOCAB);
+    int32_t* d_first_all = c->buf<int32_t>("ex_first_all", n);
+    size_t i0 = 0;
+    while (i0 < n) {
+        // chunk [i0, i1) with <= max_rows rows
+        size_t i1 = i0;
+        uint64_t rows = 0;
+        while (i1 < n) {
+            uint64_t qn = qo[order[i1] + 1] - qo[order[i1]];
+            if (i1 > i0 && rows + qn > max_rows) break;
+            rows += qn;
+            ++i1;
+        }
+        const int M = static_cast<int>(rows);
+        std::vector<int32_t> toks, pos, seg_lo, lrows;
+        std::vector<int> gs, gr, pk, pl;
+        std::vector<uint32_t> mseg;
+        std::vector<uint64_t> a_off(1, 0);
+        std::vector<int32_t> a_tok;
+        for (size_t ii = i0; ii < i1; ++ii) {
+            uint32_t j = order[ii];
+            uint32_t s = seg[j];
+            int start = static_cast<int>(toks.size());
+            uint64_t qn = qo[j + 1] - qo[j];
+            if (gs.empty() || mseg.back() != s) {
+                gs.push_back(start);
+                gr.push_back(0);
+                pk.push_back(static_cast<int>(kv->off[s]));
+                pl.push_back(static_cast<int>(kv->len[s]));
+            }
+            gr.back() += static_cast<int>(qn);
+            mseg.push_back(s);
+            for (uint64_t t = 0; t < qn; ++t) {
+                toks.push_back(qt[qo[j] + t]);
+                pos.push_back(static_cast<int32_t>(kv->len[s] + t));
+                seg_lo.push_back(start);
+            }
+            lrows.push_back(static_cast<int32_t>(toks.size() - 1));
+            if (!ao.empty()) {
+                for (uint64_t t = ao[j]; t < ao[j + 1]; ++t) a_tok.push_back(at[t]);
+            }
+            a_off.push_back(a_tok.size());
+        }
+        std::vector<sgc::AttnWork> work = make_work(gs, gr, pk, pl);
+        const int nm = static_cast<int>(i1 - i0);
+        int32_t* d_tok = c->buf<int32_t>("ex_tok", M);
+        int32_t* d_pos = c->buf<int32_t>("ex_pos", M);
+        int32_t* d_seg = c->buf<int32_t>("ex_seg", M);
+        int32_t* d_lr = c->buf<int32_t>("ex_lrows", nm);
+        uint32_t* d_mseg = c->buf<uint32_t>("ex_mseg", nm);
+        uint64_t* d_aoff = c->buf<uint64_t>("ex_aoff", nm + 1);
+        int32_t* d_atok = c->buf<int32_t>("ex_atok", a_tok.size());
+        sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("ex_work", work.size());
+        float* d_logits = c->buf<float>("ex_logits", static_cast<size_t>(nm) * SGC_VOCAB);
+        int32_t* d_first = c->buf<int32_t>("ex_first", nm);
+        bf16* kl = c->buf<bf16>("ex_kloc", static_cast<size_t>(M) * d);  // one layer at a time
+        bf16* vl = c->buf<bf16>("ex_vloc", static_cast<size_t>(M) * d);
+        sgc::copy_in(c, d_tok, toks.data(), M);
+        sgc::copy_in(c, d_pos, pos.data(), M);
+        sgc::copy_in(c, d_seg, seg_lo.data(), M);
+        sgc::copy_in(c, d_lr, lrows.data(), nm);
+        sgc::copy_in(c, d_mseg, mseg.data(), nm);
+        sgc::copy_in(c, d_aoff, a_off.data(), nm + 1);
+        sgc::copy_in(c, d_atok, a_tok.data(), a_tok.size());
+        sgc::copy_in(c, d_work, work.data(), work.size());
+        FwdBatch b;
+        b.M = M;
+        b.d_tokens = d_tok;
+        b.d_pos = d_pos;
+        b.d_seg_lo = d_seg;
+        b.d_work = d_work;
+        b.n_work = static_cast<int>(work.size());
+        b.k_loc = [kl](int) { return kl; };
+        b.v_loc = [vl](int) { return vl; };
+        b.k_pfx = [kv](int l) { return static_cast<const bf16*>(kv->k_layer(l)); };
+        b.v_pfx = [kv](int l) { return static_cast<const bf16*>(kv->v_layer(l)); };
+        b.d_logit_rows = d_lr;
+        b.n_logits = nm;
+        b.d_logits = d_logits;
+        forward_rows(c, m, b);
+        sgc::first_tokens(c, d_first, d_logits, nm, kv->d_tokens, kv->d_tok_off, d_mseg, d_atok,
+                          a_tok.empty() ? nullptr : d_aoff, bonus);
+        // scatter back to member order
+        std::vector<float> lg(static_cast<size_t>(nm) * SGC_VOCAB);
+        std::vector<int32_t> ft(nm);
+        sgc::copy_out(c, lg.data(), d_logits, lg.size());
+        sgc::copy_out(c, ft.data(), d_first, ft.size());
+        c->sync();
+        std::vector<float> lg_all;
+        for (int k = 0; k < nm; ++k) {
+            uint32_t j = order[i0 + k];
+            if (logits_out)
+                SGC_CUDA_CHECK(cudaMemcpyAsync(logits_out + static_cast<size_t>(j) * SGC_VOCAB,
+                                               lg.data() + static_cast<size_t>(k) * SGC_VOCAB,
+                                               SGC_VOCAB * sizeof(float), cudaMemcpyDefault, c->stream));
+            if (first_out)
+                SGC_CUDA_CHECK(cudaMemcpyAsync(first_out + j, ft.data() + k, sizeof(int32_t),
+                                               cudaMemcpyDefault, c->stream));
+        }
+        c->sync();
+        i0 = i1;
+    }
+    (void)d_logits_all;
+    (void)d_first_all;
+}
+
+// ============================================================ graph-side helpers
+
+void ensure_hashes(Ctx* c, sgc_graph* g, uint64_t salt) {
+    if (g->hash_salt == salt) return;
+    std::vector<uint32_t> b;
+    std::vector<int8_t> s;
+    std::vector<uint64_t> off(1, 0);
+    for (const std::string& t : g->texts) {
+        hash_tokens(t.data(), t.size(), salt, b, s);
+        off.push_back(b.size());
+    }
+    dfree(c, g->d_bucket);
+    dfree(c, g->d_sign);
+    dfree(c, g->d_tok_off);
+    g->d_bucket = dalloc<uint32_t>(c, b.size());
+    g->d_sign = dalloc<int8_t>(c, s.size());
+    g->d_tok_off = dalloc<uint64_t>(c, off.size());
+    sgc::copy_in(c, g->d_bucket, b.data(), b.size());
+    sgc::copy_in(c, g->d_sign, s.data(), s.size());
+    sgc::copy_in(c, g->d_tok_off, off.data(), off.size());
+    c->sync();
+    g->hash_salt = salt;
+}
+
+// frozen encoder state cached per context: text projection and folded GNN weights
+struct EncoderState {
+    uint32_t dim = 0;
+    uint64_t text_seed = 0;
+    float* proj_t = nullptr;
+    uint32_t layers = 0, heads = 0;
+    uint64_t gnn_seed = 0;
+    double* wbar = nullptr;
+};
+std::map<Ctx*, EncoderState> g_enc;
+
+EncoderState& encoder_state(Ctx* c, const sgc_gnn_config& cfg) {
+    EncoderState& e = g_enc[c];
+    if (!e.proj_t || e.dim != cfg.dim || e.text_seed != cfg.text_seed) {
+        dfree(c, e.proj_t);
+        e.proj_t = dalloc<float>(c, static_cast<size_t>(cfg.dim) * 4096);
+        sgc::gen_text_projection_t(c, e.proj_t, cfg.dim, sgc::splitmix64_once(cfg.text_seed ^ 0x7e87a11dULL));
+        e.text_seed = cfg.text_seed;
+        e.wbar = (dfree(c, e.wbar), nullptr);
+    }
+    if (!e.wbar || e.dim != cfg.dim || e.layers != cfg.layers || e.heads != cfg.heads || e.gnn_seed != cfg.seed) {
+        dfree(c, e.wbar);
+        e.wbar = dalloc<double>(c, static_cast<size_t>(cfg.layers) * cfg.dim * cfg.dim);
+        float scale = std::sqrt(3.0f / static_cast<float>(cfg.dim));
+        sgc::gnn_gen_wbar(c, e.wbar, cfg.layers, cfg.heads, cfg.dim,
+                          sgc::splitmix64_once(cfg.seed ^ 0x6e6eULL), scale);
+        e.layers = cfg.layers;
+        e.heads = cfg.heads;
+        e.gnn_seed = cfg.seed;
+    }
+    e.dim = cfg.dim;
+    return e;
+}
+
+float* compute_text_features(Ctx* c, sgc_graph* g, uint32_t dim, uint64_t seed, uint64_t salt,
+                             const sgc_gnn_config* gcfg) {
+    sgc_gnn_config cfg{};
+    if (gcfg) cfg = *gcfg;
+    cfg.dim = dim;
+    cfg.text_seed = seed;
+    if (!gcfg) {  // features only: keep any cached GNN weights of the same dim
+        EncoderState& e = g_enc[c];
+        cfg.layers = e.layers ? e.layers : 1;
+        cfg.heads = e.heads ? e.heads : 1;
+        cfg.seed = e.gnn_seed;
+    }
+    EncoderState& es = encoder_state(c, cfg);
+    ensure_hashes(c, g, salt);
+    const int ne = static_cast<int>(g->n_nodes + g->n_edges);
+    float* feat = c->buf<float>("text_feat", static_cast<size_t>(ne) * dim);
+    sgc::text_features(c, feat, g->d_bucket, g->d_sign, g->d_tok_off, ne, es.proj_t, dim);
+    return feat;
+}
+
+// read a subgraph CSR to host
+struct HostSubs {
+    std::vector<uint64_t> noff, eoff;
+    std::vector<uint32_t> nodes, edges;
+};
+HostSubs host_subs(Ctx* c, const sgc_subgraphs* s) {
+    HostSubs h;
+    h.noff = to_host(c, s->node_off, s->count + 1);
+    h.eoff = to_host(c, s->edge_off, s->count + 1);
+    h.nodes = to_host(c, s->nodes, h.noff[s->count]);
+    h.edges = to_host(c, s->edges, h.eoff[s->count]);
+    return h;
+}
+
+uint32_t dense_index(const sgc_graph* g, uint32_t id) {
+    auto it = std::lower_bound(g->ids.begin(), g->ids.end(), id);
+    if (it == g->ids.end() || *it != id)
+        fail(SGC_INTEGRITY, "subgraph node " + std::to_string(id) + " not in parent graph");
+    return static_cast<uint32_t>(it - g->ids.begin());
+}
+
+// GnnEncoder::encode for a batch of subgraphs; identical subgraphs are encoded once
+void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const HostSubs& hs,
+                      uint32_t count, float* out_dev) {
+    if (cfg.dim == 0 || cfg.layers == 0 || cfg.heads == 0)
+        fail(SGC_DOMAIN, "gnn encoder needs dim, layers, heads >= 1");
+    if (cfg.dim % 16) fail(SGC_DOMAIN, "gnn dim must be a multiple of 16 on this backend");
+    const int d = static_cast<int>(cfg.dim);
+    float* feat = compute_text_features(c, g, cfg.dim, cfg.text_seed, cfg.text_salt, &cfg);
+    EncoderState& es = g_enc[c];
+    // dedup
+    std::unordered_map<uint64_t, std::vector<uint32_t>> seen;
+    std::vector<uint32_t> uniq_of(count), uniq_first;
+    for (uint32_t i = 0; i < count; ++i) {
+        uint64_t nn = hs.noff[i + 1] - hs.noff[i], ne = hs.eoff[i + 1] - hs.eoff[i];
+        if (nn == 0) fail(SGC_DOMAIN, "encode_subgraph: empty subgraph");
+        uint64_t h = sgc::mix64(nn * 1000003ull + ne);
+        for (uint64_t k = hs.noff[i]; k < hs.noff[i + 1]; ++k) h = sgc::mix64(h ^ hs.nodes[k]);
+        h = sgc::mix64(h ^ 0xabcdefull);
+        for (uint64_t k = hs.eoff[i]; k < hs.eoff[i + 1]; ++k) h = sgc::mix64(h ^ hs.edges[k]);
+        auto& cand = seen[h];
+        uint32_t found = UINT32_MAX;
+        for (uint32_t u : cand) {
+            uint32_t f = uniq_first[u];
+            if (hs.noff[f + 1] - hs.noff[f] == nn && hs.eoff[f + 1] - hs.eoff[f] == ne &&
+                std::equal(hs.nodes.begin() + hs.noff[i], hs.nodes.begin() + hs.noff[i + 1],
+                           hs.nodes.begin() + hs.noff[f]) &&
+                std::equal(hs.edges.begin() + hs.eoff[i], hs.edges.begin() + hs.eoff[i + 1],
+                           hs.edges.begin() + hs.eoff[f])) {
+                found = u;
+                break;
+            }
+        }
+        if (found == UINT32_MAX) {
+            found = static_cast<uint32_t>(uniq_first.size());
+            uniq_first.push_back(i);
+            cand.push_back(found);
+        }
+        uniq_of[i] = found;
+    }
+    const uint32_t nu = static_cast<uint32_t>(uniq_first.size());
+    std::vector<uint32_t> inst_feat, sub_inst_off(1, 0), in_off(1, 0), in_src, in_gate;
+    for (uint32_t u = 0; u < nu; ++u) {
+        uint32_t i = uniq_first[u];
+        const uint32_t base = static_cast<uint32_t>(inst_feat.size());
+        const uint64_t n0 = hs.noff[i], n1 = hs.noff[i + 1];
+        std::vector<uint32_t> local_dense;
+        for (uint64_t k = n0; k < n1; ++k) {
+            if (k > n0 && hs.nodes[k] <= hs.nodes[k - 1])
+                fail(SGC_DOMAIN, "subgraph node ids must be ascending and unique");
+            uint32_t di = dense_index(g, hs.nodes[k]);
+            local_dense.push_back(di);
+            inst_feat.push_back(di);
+        }
+        // in-edges per destination, ascending edge index (encoders.cpp:142-162)
+        std::vector<std::vector<std::pair<uint32_t, uint32_t>>> in(n1 - n0);
+        for (uint64_t k = hs.eoff[i]; k < hs.eoff[i + 1]; ++k) {
+            uint32_t e = hs.edges[k];
+            if (e >= g->n_edges) fail(SGC_INTEGRITY, "subgraph edge index " + std::to_string(e) + " out of range");
+            auto ls = std::lower_bound(local_dense.begin(), local_dense.end(), g->edge_src_idx[e]);
+            auto ld = std::lower_bound(local_dense.begin(), local_dense.end(), g->edge_dst_idx[e]);
+            if (ls == local_dense.end() || *ls != g->edge_src_idx[e] || ld == local_dense.end() ||
+                *ld != g->edge_dst_idx[e])
+                fail(SGC_INTEGRITY, "subgraph edge " + std::to_string(e) + " violates closure: endpoint missing");
+            in[ld - local_dense.begin()].push_back({base + static_cast<uint32_t>(ls - local_dense.begin()),
+                                                    g->n_nodes + e});
+        }
+        for (auto& lst : in) {
+            for (auto& pr : lst) {
+                in_src.push_back(pr.first);
+                in_gate.push_back(pr.second);
+            }
+            in_off.push_back(static_cast<uint32_t>(in_src.size()));
+        }
+        sub_inst_off.push_back(static_cast<uint32_t>(inst_feat.size()));
+    }
+    const int n_inst = static_cast<int>(inst_feat.size());
+    sgc::GnnBatch b;
+    b.layers = static_cast<int>(cfg.layers);
+    b.heads = static_cast<int>(cfg.heads);
+    b.d = d;
+    b.n_inst = n_inst;
+    b.n_sub = static_cast<int>(nu);
+    uint32_t* d_if = c->buf<uint32_t>("gnn_inst_feat", n_inst);
+    uint32_t* d_io = c->buf<uint32_t>("gnn_in_off", in_off.size());
+    uint32_t* d_is = c->buf<uint32_t>("gnn_in_src", in_src.size());
+    uint32_t* d_ig = c->buf<uint32_t>("gnn_in_gate", in_gate.size());
+    uint32_t* d_so = c->buf<uint32_t>("gnn_sub_off", sub_inst_off.size());
+    sgc::copy_in(c, d_if, inst_feat.data(), inst_feat.size());
+    sgc::copy_in(c, d_io, in_off.data(), in_off.size());
+    sgc::copy_in(c, d_is, in_src.data(), in_src.size());
+    sgc::copy_in(c, d_ig, in_gate.data(), in_gate.size());
+    sgc::copy_in(c, d_so, sub_inst_off.data(), sub_inst_off.size());
+    b.inst_feat = d_if;
+    b.in_off = d_io;
+    b.in_src = d_is;
+    b.in_gate = d_ig;
+    b.sub_inst_off = d_so;
+    b.feat = feat;
+    b.wbar = es.wbar;
+    b.state = c->buf<double>("gnn_state", static_cast<size_t>(n_inst) * d);
+    b.agg = c->buf<double>("gnn_agg", static_cast<size_t>(n_inst) * d);
+    float* uniq_out = c->buf<float>("gnn_uniq_out", static_cast<size_t>(nu) * d);
+    b.out = uniq_out;
+    sgc::gnn_encode_batch(c, b);
+    // scatter unique embeddings to every subgraph
+    for (uint32_t i = 0; i < count; ++i)
+        SGC_CUDA_CHECK(cudaMemcpyAsync(out_dev + static_cast<size_t>(i) * d,
+                                       uniq_out + static_cast<size_t>(uniq_of[i]) * d, d * sizeof(float),
+                                       cudaMemcpyDeviceToDevice, c->stream));
+    c->sync();
+}
+
+// clustering on device; labels etc. are device pointers
+void cluster_device(Ctx* c, const float* d_emb, uint32_t m, uint32_t dim, int linkage, uint32_t k,
+                    uint32_t* d_labels, uint32_t* d_left, uint32_t* d_right, double* d_dist) {
+    if (k < 1) fail(SGC_DOMAIN, "cluster count must be >= 1");
+    if (m == 0) fail(SGC_DOMAIN, "pairwise_distances: need at least one embedding");
+    if (k > m)
+        fail(SGC_DOMAIN, "cluster count " + std::to_string(k) + " exceeds point count " + std::to_string(m));
+    if (linkage < SGC_WARD || linkage > SGC_CENTROID) fail(SGC_DOMAIN, "unknown linkage");
+    double* D = c->buf<double>("agg_D", static_cast<size_t>(m) * m);
+    bool squared = linkage == SGC_WARD || linkage == SGC_CENTROID;
+    sgc::pairwise_distances(c, D, d_emb, static_cast<int>(m), static_cast<int>(dim), squared);
+    sgc::agglomerate(c, D, static_cast<int>(m), static_cast<int>(k), linkage, d_labels, d_left, d_right, d_dist);
+}
+
+uint64_t agglomerate_op_count(uint64_t m, uint64_t dim, uint64_t c) {
+    // clustering.cpp:71,99,130: distance evals + scanned alive pairs + recurrence updates
+    uint64_t ops = m * (m - 1) / 2 * dim;
+    for (uint64_t a = m; a > c; --a) ops += a * (a - 1) / 2 + (a - 2);
+    return ops;
+}
+
+struct RepResult {
+    std::vector<uint64_t> prefix_off;  // [c+1] on host
+    int32_t* d_prefix = nullptr;       // device tokens (BOS + bytes)
+    uint64_t* d_prefix_off = nullptr;
+    std::vector<uint32_t> stats;       // [c x 6]
+    uint32_t* d_sel_nodes = nullptr;
+    uint32_t* d_sel_edges = nullptr;
+};
+
+RepResult build_reps(Ctx* c, sgc_graph* g, const HostSubs& hs, uint32_t count,
+                     const std::vector<std::vector<uint32_t>>& members, uint32_t budget_tokens) {
+    const uint32_t k = static_cast<uint32_t>(members.size());
+    RepResult r;
+    // dense node indices of all subgraph nodes (device binary search)
+    uint64_t total_nodes = hs.noff[count];
+    uint32_t* d_ids = c->buf<uint32_t>("rep_ids", total_nodes);
+    int32_t* d_idx = c->buf<int32_t>("rep_idx", total_nodes);
+    uint64_t* d_noff = c->buf<uint64_t>("rep_noff", count + 1);
+    uint32_t* d_edges = c->buf<uint32_t>("rep_edges_in", hs.eoff[count]);
+    uint64_t* d_eoff = c->buf<uint64_t>("rep_eoff", count + 1);
+    sgc::copy_in(c, d_ids, hs.nodes.data(), total_nodes);
+    sgc::copy_in(c, d_noff, hs.noff.data(), count + 1);
+    sgc::copy_in(c, d_edges, hs.edges.data(), hs.eoff[count]);
+    sgc::copy_in(c, d_eoff, hs.eoff.data(), count + 1);
+    sgc::node_index(c, d_idx, d_ids, total_nodes, g->d_ids, static_cast<int>(g->n_nodes));
+    std::vector<uint32_t> mem;
+    std::vector<uint64_t> moff(1, 0);
+    for (auto& v : members) {
+        if (v.empty()) fail(SGC_DOMAIN, "merge_subgraphs: empty member list");
+        mem.insert(mem.end(), v.begin(), v.end());
+        moff.push_back(mem.size());
+    }
+    uint32_t* d_mem = c->buf<uint32_t>("rep_members", mem.size());
+    uint64_t* d_moff = c->buf<uint64_t>("rep_moff", moff.size());
+    sgc::copy_in(c, d_mem, mem.data(), mem.size());
+    sgc::copy_in(c, d_moff, moff.data(), moff.size());
+    const int nw = static_cast<int>((g->n_nodes + 31) / 32), ew = static_cast<int>((g->n_edges + 31) / 32);
+    sgc::UnionArgs a;
+    a.clusters = static_cast<int>(k);
+    a.sub_nodes = d_idx;
+    a.sub_node_off = d_noff;
+    a.sub_edges = d_edges;
+    a.sub_edge_off = d_eoff;
+    a.members = d_mem;
+    a.member_off = d_moff;
+    a.node_bm = c->buf<uint32_t>("rep_nbm", static_cast<size_t>(k) * std::max(nw, 1));
+    a.edge_bm = c->buf<uint32_t>("rep_ebm", static_cast<size_t>(k) * std::max(ew, 1));
+    a.node_words = nw;
+    a.edge_words = ew;
+    a.node_row_len = g->d_node_row_len;
+    a.edge_row_len = g->d_edge_row_len;
+    a.n_nodes = static_cast<int>(g->n_nodes);
+    a.n_edges = static_cast<int>(g->n_edges);
+    a.budget_bytes = budget_tokens == 0 ? 0 : budget_tokens - 1;
+    a.base_bytes = static_cast<uint32_t>(strlen(kHeader) + strlen(kNodeHdr) + strlen(kEdgeHdr) + 2);
+    r.d_sel_nodes = a.sel_nodes = c->buf<uint32_t>("rep_seln", static_cast<size_t>(k) * std::max<uint32_t>(g->n_nodes, 1));
+    r.d_sel_edges = a.sel_edges = c->buf<uint32_t>("rep_sele", static_cast<size_t>(k) * std::max<uint32_t>(g->n_edges, 1));
+    a.node_pre = c->buf<uint32_t>("rep_npre", static_cast<size_t>(k) * (g->n_nodes + 1));
+    a.edge_pre = c->buf<uint32_t>("rep_epre", static_cast<size_t>(k) * (g->n_edges + 1));
+    uint32_t* d_stats = c->buf<uint32_t>("rep_stats", static_cast<size_t>(k) * 6);
+    a.stats = d_stats;
+    int* d_status = c->buf<int>("rep_status", 1);
+    a.status = d_status;
+    SGC_CUDA_CHECK(cudaMemsetAsync(d_status, 0, sizeof(int), c->stream));
+    sgc::union_prompt(c, a);
+    r.stats = to_host(c, d_stats, static_cast<size_t>(k) * 6);
+    int status = to_host(c, d_status, 1)[0];
+    if (status == SGC_INTEGRITY) fail(SGC_INTEGRITY, "subgraph references a node or edge outside the graph");
+    if (status == SGC_CAPACITY) fail(SGC_CAPACITY, "prompt headers alone exceed the prefix budget");
+    r.prefix_off.assign(1, 0);
+    uint64_t maxp = 0;
+    const uint64_t head_len = strlen(kHeader) + strlen(kNodeHdr) + 1, ehead_len = strlen(kEdgeHdr) + 1;
+    for (uint32_t i = 0; i < k; ++i) {
+        const uint32_t* st = &r.stats[i * 6];
+        uint64_t P = 1 + head_len + st[4] + ehead_len + st[5];
+        maxp = std::max(maxp, P);
+        r.prefix_off.push_back(r.prefix_off.back() + P);
+    }
+    r.d_prefix = c->buf<int32_t>("rep_prefix", r.prefix_off.back());
+    r.d_prefix_off = c->buf<uint64_t>("rep_prefix_off", k + 1);
+    sgc::copy_in(c, r.d_prefix_off, r.prefix_off.data(), k + 1);
+    static bool headers_set = false;
+    if (!headers_set) {
+        std::string h = std::string(kHeader) + kNodeHdr + "\n";
+        std::string eh = std::string(kEdgeHdr) + "\n";
+        sgc::set_prompt_headers(h.data(), static_cast<int>(h.size()), eh.data(), static_cast<int>(eh.size()));
+        headers_set = true;
+    }
+    sgc::GatherArgs ga;
+    ga.clusters = static_cast<int>(k);
+    ga.max_tokens = maxp;
+    ga.tokens = r.d_prefix;
+    ga.tok_off = r.d_prefix_off;
+    ga.stats = d_stats;
+    ga.sel_nodes = a.sel_nodes;
+    ga.sel_edges = a.sel_edges;
+    ga.node_pre = a.node_pre;
+    ga.edge_pre = a.edge_pre;
+    ga.node_text = g->d_node_rows;
+    ga.node_text_off = g->d_node_row_off;
+    ga.edge_text = g->d_edge_rows;
+    ga.edge_text_off = g->d_edge_row_off;
+    ga.n_nodes = static_cast<int>(g->n_nodes);
+    ga.n_edges = static_cast<int>(g->n_edges);
+    ga.head_len = static_cast<int>(head_len);
+    ga.ehead_len = static_cast<int>(ehead_len);
+    sgc::prompt_gather(c, ga);
+    return r;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+
+extern "C" {
+
+const char* sgc_last_error(void) { return g_last_error.c_str(); }
+const char* sgc_version(void) { return "subgcache-b200 0.1 (sm_100a)"; }
+
+int sgc_ctx_create(int device, sgc_ctx** out) {
+    return guarded([&] {
+        if (!out) fail(SGC_DOMAIN, "null out");
+        int n = 0;
+        SGC_CUDA_CHECK(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) fail(SGC_CUDA, "no such CUDA device " + std::to_string(device));
+        SGC_CUDA_CHECK(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        SGC_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10) fail(SGC_CUDA, std::string("sm_100a device required, found ") + prop.name);
+        auto* h = new sgc_ctx();
+        h->c.device = device;
+        h->c.num_sms = prop.multiProcessorCount;
+        SGC_CUDA_CHECK(cudaStreamCreateWithFlags(&h->c.own_stream, cudaStreamNonBlocking));
+        h->c.stream = h->c.own_stream;
+        *out = h;
+    });
+}
+
+int sgc_ctx_destroy(sgc_ctx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        Ctx* c = &ctx->c;
+        cudaStreamSynchronize(c->stream);
+        for (auto& kv : c->scratch) cudaFree(kv.second.ptr);
+        auto it = g_enc.find(c);
+        if (it != g_enc.end()) {
+            cudaFree(it->second.proj_t);
+            cudaFree(it->second.wbar);
+            g_enc.erase(it);
+        }
+        for (auto e : c->event_pool) cudaEventDestroy(e);
+        cudaStreamDestroy(c->own_stream);
+        delete ctx;
+    });
+}
+
+int sgc_ctx_set_stream(sgc_ctx* ctx, void* stream) {
+    return guarded([&] {
+        ctx->c.sync();
+        ctx->c.stream = stream ? static_cast<cudaStream_t>(stream) : ctx->c.own_stream;
+    });
+}
+
+uint64_t sgc_ctx_launch_count(const sgc_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int sgc_model_create(sgc_ctx* ctx, const sgc_lm_config* cfg, sgc_model** out) {
+    return guarded([&] {
+        Ctx* c = &ctx->c;
+        check_lm_cfg(*cfg);
+        auto m = std::make_unique<sgc_model>();
+        m->c = c;
+        m->cfg = *cfg;
+        m->d = cfg->model_dim;
+        m->H = cfg->heads;
+        m->hd = cfg->model_dim / cfg->heads;
+        m->L = cfg->layers;
+        m->ffn = cfg->ffn_hidden;
+        const size_t d = m->d, ffn = m->ffn, L = m->L;
+        const uint64_t seed = cfg->seed;
+        m->tok_emb = dalloc<float>(c, SGC_VOCAB * d);
+        m->head = dalloc<float>(c, SGC_VOCAB * d);
+        m->head_t = dalloc<float>(c, SGC_VOCAB * d);
+        const float sd = std::sqrt(3.0f / static_cast<float>(d));
+        const float sf = std::sqrt(3.0f / static_cast<float>(ffn));
+        // lm_core.cpp:131-147: fill_uniform(w, seed ^ const, fan_in) -> stream splitmix64_once(seed^const)
+        sgc::gen_uniform(c, m->tok_emb, SGC_VOCAB * d, sgc::splitmix64_once(seed ^ 0x10ad1ULL), -sd, sd);
+        sgc::gen_uniform(c, m->head, SGC_VOCAB * d, sgc::splitmix64_once(seed ^ 0x8eadULL), -sd, sd);
+        sgc::head_transpose(c, m->head_t, m->head, static_cast<int>(d));
+        const size_t per_layer = 3 * d * d + d * d + ffn * d + d * ffn;
+        m->weights = dalloc<bf16>(c, per_layer * L);
+        for (size_t l = 0; l < L; ++l) {
+            bf16* base = m->weights + per_layer * l;
+            m->wqkv.push_back(base);
+            m->wo.push_back(base + 3 * d * d);
+            m->w1.push_back(base + 4 * d * d);
+            m->w2.push_back(base + 4 * d * d + ffn * d);
+            sgc::gen_uniform(c, m->wqkv[l], 3 * d * d, sgc::splitmix64_once(seed ^ (0x9a11ULL + l * 4)), -sd, sd);
+            sgc::gen_uniform(c, m->wo[l], d * d, sgc::splitmix64_once(seed ^ (0x9a12ULL + l * 4)), -sd, sd);
+            sgc::gen_uniform(c, m->w1[l], ffn * d, sgc::splitmix64_once(seed ^ (0x9a13ULL + l * 4)), -sd, sd);
+            sgc::gen_uniform(c, m->w2[l], d * ffn, sgc::splitmix64_once(seed ^ (0x9a14ULL + l * 4)), -sf, sf);
+        }
+        // RoPE tables exactly as lm_core.cpp:149-160 (host libm, float)
+        const uint32_t half = m->hd / 2, ms = cfg->max_seq_len;
+        std::vector<float> cs(static_cast<size_t>(ms) * half), sn(static_cast<size_t>(ms) * half);
+        for (uint32_t p = 0; p < ms; ++p)
+            for (uint32_t i = 0; i < half; ++i) {
+                float freq = std::pow(10000.0f, -2.0f * static_cast<float>(i) / static_cast<float>(m->hd));
+                float angle = static_cast<float>(p) * freq;
+                cs[static_cast<size_t>(p) * half + i] = std::cos(angle);
+                sn[static_cast<size_t>(p) * half + i] = std::sin(angle);
+            }
+        m->rope_cos = dalloc<float>(c, cs.size());
+        m->rope_sin = dalloc<float>(c, sn.size());
+        sgc::copy_in(c, m->rope_cos, cs.data(), cs.size());
+        sgc::copy_in(c, m->rope_sin, sn.data(), sn.size());
+        c->sync();
+        *out = m.release();
+    });
+}
+
+int sgc_model_destroy(sgc_model* m) {
+    return guarded([&] {
+        if (!m) return;
+        Ctx* c = m->c;
+        dfree(c, m->tok_emb);
+        dfree(c, m->head);
+        dfree(c, m->head_t);
+        dfree(c, m->weights);
+        dfree(c, m->rope_cos);
+        dfree(c, m->rope_sin);
+        c->sync();
+        delete m;
+    });
+}
+
+int sgc_model_weight(sgc_model* m, int which, uint32_t layer, int fp32, float* out, size_t n) {
+    return guarded([&] {
+        Ctx* c = m->c;
+        const size_t d = m->d, ffn = m->ffn;
+        if (which < 2) {
+            if (n != SGC_VOCAB * d) fail(SGC_DOMAIN, "size mismatch");
+            sgc::copy_out(c, out, which == 0 ? m->tok_emb : m->head, n);
+            c->sync();
+            return;
+        }
+        if (layer >= static_cast<uint32_t>(m->L)) fail(SGC_DOMAIN, "layer out of range");
+        size_t cnt = which == 2 ? 3 * d * d : which == 3 ? d * d : ffn * d;
+        if (n != cnt) fail(SGC_DOMAIN, "size mismatch");
+        const uint64_t seed = m->cfg.seed;
+        const uint64_t k = which == 2 ? 0x9a11ULL : which == 3 ? 0x9a12ULL : which == 4 ? 0x9a13ULL : 0x9a14ULL;
+        const float s = std::sqrt(3.0f / static_cast<float>(which == 5 ? ffn : d));
+        if (fp32) {
+            float* tmp = c->buf<float>("wtmp", cnt);
+            sgc::gen_uniform(c, tmp, cnt, sgc::splitmix64_once(seed ^ (k + layer * 4)), -s, s);
+            sgc::copy_out(c, out, tmp, cnt);
+        } else {
+            const bf16* src = which == 2 ? m->wqkv[layer] : which == 3 ? m->wo[layer] : which == 4 ? m->w1[layer] : m->w2[layer];
+            std::vector<bf16> h(cnt);
+            sgc::copy_out(c, h.data(), src, cnt);
+            c->sync();
+            std::vector<float> f(cnt);
+            for (size_t i = 0; i < cnt; ++i) f[i] = __bfloat162float(h[i]);
+            sgc::copy_out(c, out, f.data(), cnt);
+        }
+        c->sync();
+    });
+}
+
+int sgc_graph_upload(sgc_ctx* ctx, uint32_t n_nodes, const uint32_t* node_ids, const char* node_text,
+                     const uint64_t* node_off, uint32_t n_edges, const uint32_t* edge_src,
+                     const uint32_t* edge_dst, const char* edge_text, const uint64_t* edge_off,
+                     sgc_graph** out) {
+    return guarded([&] {
+        Ctx* c = &ctx->c;
+        auto g = std::make_unique<sgc_graph>();
+        g->c = c;
+        g->n_nodes = n_nodes;
+        g->n_edges = n_edges;
+        g->ids.assign(node_ids, node_ids + n_nodes);
+        for (uint32_t i = 1; i < n_nodes; ++i)
+            if (g->ids[i] <= g->ids[i - 1]) fail(SGC_INTEGRITY, "node ids must be ascending and unique");
+        std::string nrows, erows;
+        std::vector<uint64_t> noff(1, 0), eoff(1, 0);
+        std::vector<uint32_t> nlen, elen;
+        for (uint32_t i = 0; i < n_nodes; ++i) {
+            std::string attr(node_text + node_off[i], node_text + node_off[i + 1]);
+            g->texts.push_back(attr);
+            std::string row = std::to_string(g->ids[i]) + ',' + csv_quote(attr);  // graph_store.cpp:251-253
+            nrows += row;
+            noff.push_back(nrows.size());
+            nlen.push_back(static_cast<uint32_t>(row.size()));
+        }
+        for (uint32_t e = 0; e < n_edges; ++e) {
+            std::string attr(edge_text + edge_off[e], edge_text + edge_off[e + 1]);
+            g->texts.push_back(attr);
+            g->edge_src_idx.push_back(dense_index(g.get(), edge_src[e]));
+            g->edge_dst_idx.push_back(dense_index(g.get(), edge_dst[e]));
+            std::string row = std::to_string(edge_src[e]) + ',' + csv_quote(attr) + ',' +
+                              std::to_string(edge_dst[e]);  // graph_store.cpp:256-259
+            erows += row;
+            eoff.push_back(erows.size());
+            elen.push_back(static_cast<uint32_t>(row.size()));
+        }
+        g->d_ids = dalloc<uint32_t>(c, n_nodes);
+        g->d_node_rows = dalloc<char>(c, nrows.size());
+        g->d_node_row_off = dalloc<uint64_t>(c, noff.size());
+        g->d_node_row_len = dalloc<uint32_t>(c, nlen.size());
+        g->d_edge_rows = dalloc<char>(c, erows.size());
+        g->d_edge_row_off = dalloc<uint64_t>(c, eoff.size());
+        g->d_edge_row_len = dalloc<uint32_t>(c, elen.size());
+        sgc::copy_in(c, g->d_ids, g->ids.data(), n_nodes);
+        sgc::copy_in(c, g->d_node_rows, nrows.data(), nrows.size());
+        sgc::copy_in(c, g->d_node_row_off, noff.data(), noff.size());
+        sgc::copy_in(c, g->d_node_row_len, nlen.data(), nlen.size());
+        sgc::copy_in(c, g->d_edge_rows, erows.data(), erows.size());
+        sgc::copy_in(c, g->d_edge_row_off, eoff.data(), eoff.size());
+        sgc::copy_in(c, g->d_edge_row_len, elen.data(), elen.size());
+        c->sync();
+        *out = g.release();
+    });
+}
+
+int sgc_graph_destroy(sgc_graph* g) {
+    return guarded([&] {
+        if (!g) return;
+        Ctx* c = g->c;
+        for (void* p : {(void*)g->d_ids, (void*)g->d_node_rows, (void*)g->d_node_row_off,
+                        (void*)g->d_node_row_len, (void*)g->d_edge_rows, (void*)g->d_edge_row_off,
+                        (void*)g->d_edge_row_len, (void*)g->d_bucket, (void*)g->d_sign, (void*)g->d_tok_off})
+            dfree(c, p);
+        c->sync();
+        delete g;
+    });
+}
+
+int sgc_text_features(sgc_ctx* ctx, sgc_graph* g, uint32_t dim, uint64_t seed, uint64_t salt, float* out) {
+    return guarded([&] {
+        Ctx* c = &ctx->c;
+        if (dim == 0) fail(SGC_DOMAIN, "text encoder dim must be >= 1");
+        float* f = compute_text_features(c, g, dim, seed, salt, nullptr);
+        sgc::copy_out(c, out, f, static_cast<size_t>(g->n_nodes + g->n_edges) * dim);
+        c->sync();
+    });
+}
+
+int sgc_encode_subgraphs(sgc_ctx* ctx, sgc_graph* g, const sgc_gnn_config* cfg,
+                         const sgc_subgraphs* subs, float* out) {
+    return guarded([&] {
+        Ctx* c = &ctx->c;
+        HostSubs hs = host_subs(c, subs);
+        float* d_out = c->buf<float>("enc_out", static_cast<size_t>(subs->count) * cfg->dim);
+        encode_subgraphs(c, g, *cfg, hs, subs->count, d_out);
+        sgc::copy_out(c, out, d_out, static_cast<size_t>(subs->count) * cfg->dim);
+        c->sync();
+    });
+}
+
+int sgc_pairwise_distances(sgc_ctx* ctx, const float* emb, uint32_t m, uint32_t dim, double* out) {
+    return guarded([&] {
+        Ctx* c = &ctx->c;
+        if (m == 0) fail(SGC_DOMAIN, "pairwise_distances: need at least one embedding");
+        float* e = c->buf<float>("pw_emb", static_cast<size_t>(m) * dim);
+        sgc::copy_in(c, e, emb, static_cast<size_t>(m) * dim);
+        double* D = c->buf<double>("pw_D", static_cast<size_t>(m) * m);
+        sgc::pairwise_distances(c, D, e, static_cast<int>(m), static_cast<int>(dim), false);
+        sgc::copy_out(c, out, D, static_cast<size_t>(m) * m);
+        c->sync();
+    });
+}
+
+int sgc_agglomerate(sgc_ctx* ctx, const float* emb, uint32_t m, uint32_t dim, int linkage, uint32_t k,
+                    uint32_t* labels, uint32_t* merge_left, uint32_t* merge_right, double* merge_dist,
+                    uint64_t* op_count) {
+    return guarded([&] {
+        Ctx* c = &ctx->c;
+        if (k < 1) fail(SGC_DOMAIN, "cluster count must be >= 1");
+        if (k > m) fail(SGC_DOMAIN, "cluster count " + std::to_string(k) + " exceeds point count " + std::to_string(m));
+        float* e = c->buf<float>("ag_emb", static_cast<size_t>(m) * dim);
+        sgc::copy_in(c, e, emb, static_cast<size_t>(m) * dim);
+        uint32_t* dl = c->buf<uint32_t>("ag_labels", m);
+        uint32_t* dleft = c->buf<uint32_t>("ag_left", m);
+        uint32_t* dright = c->buf<uint32_t>("ag_right", m);
+        double* ddist = c->buf<double>("ag_dist", m);
+        cluster_device(c, e, m, dim, linkage, k, dl, dleft, dright, ddist);
+        sgc::copy_out(c, labels, dl, m);
+        sgc::copy_out(c, merge_left, dleft, m - k);
+        sgc::copy_out(c, merge_right, dright, m - k);
+        sgc::copy_out(c, merge_dist, ddist, m - k);
+        c->sync();
+        if (op_count) *op_count = agglomerate_op_count(m, dim, k);
+    });
+}
+
+int sgc_build_representatives(sgc_ctx* ctx, sgc_graph* g, const sgc_subgraphs* subs, const uint32_t* labels,
+                              uint32_t k, uint32_t budget_tokens, uint64_t* rep_node_off, uint32_t* rep_nodes,
+                              uint64_t rep_node_cap, uint64_t* rep_edge_off, uint32_t* rep_edges,
+                              uint64_t rep_edge_cap, uint64_t* prefix_off, int32_t* prefix, uint64_t prefix_cap,
+                              uint32_t* dropped) {
+    return guarded([&] {
+        Ctx* c = &ctx->c;
+        HostSubs hs = host_subs(c, subs);
+        std::vector<uint32_t> lab = to_host(c, labels, subs->count);
+        std::vector<std::vector<uint32_t>> members(k);
+        for (uint32_t i = 0; i < subs->count; ++i) {
+            if (lab[i] >= k) fail(SGC_DOMAIN, "label out of range");
+            members[lab[i]].push_back(i);
+        }
+        RepResult r = build_reps(c, g, hs, subs->count, members, budget_tokens);
+        uint64_t nsum = 0, esum = 0;
+        for (uint32_t i = 0; i < k; ++i) {
+            nsum += r.stats[i * 6];
+            esum += r.stats[i * 6 + 1];
+        }
+        if (rep_nodes && nsum > rep_node_cap) fail(SGC_CAPACITY, "rep_nodes capacity too small");
+        if (rep_edges && esum > rep_edge_cap) fail(SGC_CAPACITY, "rep_edges capacity too small");
+        if (prefix && r.prefix_off[k] > prefix_cap) fail(SGC_CAPACITY, "prefix capacity too small");
+        std::vector<uint64_t> no(1, 0), eo(1, 0);
+        for (uint32_t i = 0; i < k; ++i) {
+            const uint32_t* st = &r.stats[i * 6];
+            if (rep_nodes)
+                sgc::copy_out(c, rep_nodes + no.back(), r.d_sel_nodes + static_cast<size_t>(i) * g->n_nodes, st[0]);
+            if (rep_edges)
+                sgc::copy_out(c, rep_edges + eo.back(), r.d_sel_edges + static_cast<size_t>(i) * g->n_edges, st[1]);
+            no.push_back(no.back() + st[0]);
+            eo.push_back(eo.back() + st[1]);
+            if (dropped) {
+                dropped[2 * i] = st[0] - st[2];
+                dropped[2 * i + 1] = st[1] - st[3];
+            }
+        }
+        c->sync();
+        // selected indices are dense node indices -> convert to ids
+        if (rep_nodes) {
+            std::vector<uint32_t> tmp = to_host(c, rep_nodes, nsum);
+            for (auto& v : tmp) v = g->ids[v];
+            sgc::copy_out(c, rep_nodes, tmp.data(), nsum);
+        }
+        if (rep_node_off) sgc::copy_out(c, rep_node_off, no.data(), k + 1);
+        if (rep_edge_off) sgc::copy_out(c, rep_edge_off, eo.data(), k + 1);
+        if (prefix_off) sgc::copy_out(c, prefix_off, r.prefix_off.data(), k + 1);
+        if (prefix) sgc::copy_out(c, prefix, r.d_prefix, r.prefix_off[k]);
+        c->sync();
+    });
+}
+
+int sgc_prefill(sgc_ctx* ctx, sgc_model* model, const sgc_token_lists* seqs, const float* soft,
+                const uint8_t* soft_mask, sgc_kv** out, float* last_logits) {
+    return guarded([&] {
+        if (seqs->count == 0) fail(SGC_DOMAIN, "prefill: no sequences");
+        *out = do_prefill(&ctx->c, model, seqs->count, seqs->off, seqs->tokens, soft, soft_mask, last_logits);
+    });
+}
+
+int sgc_kv_release(sgc_kv* kv) {
+    return guarded([&] {
+        if (!kv) return;
+        Ctx* c = kv->model->c;
+        dfree(c, kv->k);
+        dfree(c, kv->v);
+        dfree(c, kv->d_tokens);
+        dfree(c, kv->d_tok_off);
+        c->sync();
+        delete kv;
+    });
+}
+
+uint32_t sgc_kv_count(const sgc_kv* kv) { return kv ? kv->n : 0; }
+uint64_t sgc_kv_tokens(const sgc_kv* kv, uint32_t i) { return kv && i < kv->n ? kv->len[i] : 0; }
+uint64_t sgc_kv_resident_bytes(const sgc_kv* kv) {
+    return kv ? kv->rows * static_cast<uint64_t>(kv->model->L) * 2 * kv->model->d * sizeof(bf16) : 0;
+}
+
+uint64_t sgc_kv_digest(const sgc_kv* kv, uint32_t i) {
+    if (!kv || i >= kv->n) return 0;
+    uint64_t h = 0xcbf29ce484222325ULL;
+    try {
+        Ctx* c = kv->model->c;
+        const size_t d = kv->model->d, n = kv->len[i] * d;
+        std::vector<bf16> buf(n);
+        for (int l = 0; l < kv->model->L; ++l) {
+            for (int which = 0; which < 2; ++which) {
+                const bf16* src = (which ? kv->v_layer(l) : kv->k_layer(l)) + kv->off[i] * d;
+                SGC_CUDA_CHECK(cudaMemcpy(buf.data(), src, n * sizeof(bf16), cudaMemcpyDeviceToHost));
+                const unsigned char* p = reinterpret_cast<const unsigned char*>(buf.data());
+                for (size_t b = 0; b < n * sizeof(bf16); ++b) {
+                    h ^= p[b];
+                    h *= 0x100000001b3ULL;
+                }
+            }
+        }
+        (void)c;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return 0;
+    }
+    return h;
+}
+
+int sgc_kv_read(const sgc_kv* kv, uint32_t i, uint32_t layer, int is_v, float* out) {
+    return guarded([&] {
+        if (i >= kv->n || layer >= static_cast<uint32_t>(kv->model->L)) fail(SGC_DOMAIN, "kv_read: out of range");
+        const size_t d = kv->model->d, n = kv->len[i] * d;
+        std::vector<bf16> buf(n);
+        const bf16* src = (is_v ? kv->v_layer(layer) : kv->k_layer(layer)) + kv->off[i] * d;
+        SGC_CUDA_CHECK(cudaMemcpy(buf.data(), src, n * sizeof(bf16), cudaMemcpyDeviceToHost));
+        std::vector<float> f(n);
+        for (size_t t = 0; t < n; ++t) f[t] = __bfloat162float(buf[t]);
+        SGC_CUDA_CHECK(cudaMemcpy(out, f.data(), n * sizeof(float), cudaMemcpyDefault));
+    });
+}
+
+int sgc_extend(sgc_ctx* ctx, sgc_model* model, sgc_kv* kv, const uint32_t* member_seg,
+               const sgc_token_lists* questions, const sgc_token_lists* answers, float pointer_bonus,
+               float* logits, int32_t* first_token) {
+    return guarded([&] {
+        if (kv->model != model) fail(SGC_DOMAIN, "KV cache does not belong to this model");
+        const bool ans = answers && answers->count > 0;
+        if (ans && answers->count != questions->count) fail(SGC_DOMAIN, "answers/questions count mismatch");
+        do_extend(&ctx->c, model, kv, questions->count, member_seg, questions->off, questions->tokens,
+                  ans ? answers->off : nullptr, ans ? answers->tokens : nullptr, pointer_bonus, logits,
+                  first_token);
+    });
+}
+
+int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_batch* b, sgc_batch_out* o) {
+    return guarded([&] {
+        Ctx* c = &ctx->c;
+        const double t_start = now_ms();
+        const uint32_t m = b->retrieved.count;
+        const uint32_t d = model->d;
+        if (m == 0) fail(SGC_DOMAIN, "no queries to run");
+        if (b->questions.count != m) fail(SGC_DOMAIN, "questions count != retrieved count");
+        if (b->clusters > m) fail(SGC_DOMAIN, "cluster count exceeds batch size");
+        const sgc_lm_config& lc = model->cfg;
+        // PromptBudget (cache_engine.hpp:21-32)
+        const uint32_t reserved = b->question_budget + lc.max_new_tokens + (b->soft_prefix ? 1 : 0);
+        const uint32_t budget = reserved >= lc.max_seq_len ? 0 : lc.max_seq_len - reserved;
+        if (budget <= 1) fail(SGC_DOMAIN, "max_seq too small for the question budget and generation cap");
+        HostSubs hs = host_subs(c, &b->retrieved);
+        // ---- (1) embeddings
+        float* d_emb = c->buf<float>("run_emb", static_cast<size_t>(m) * d);
+        if (b->precomputed_embeddings) {
+            sgc::copy_in(c, d_emb, b->precomputed_embeddings, static_cast<size_t>(m) * d);
+        } else {
+            sgc_gnn_config gc = b->gnn;
+            gc.dim = d;
+            encode_subgraphs(c, g, gc, hs, m, d_emb);
+        }
+        c->sync();
+        const double t_enc = now_ms();
+        // ---- (2) clustering
+        uint32_t* d_lab = c->buf<uint32_t>("run_labels", m);
+        uint32_t* d_left = c->buf<uint32_t>("run_left", m);
+        uint32_t* d_right = c->buf<uint32_t>("run_right", m);
+        double* d_dist = c->buf<double>("run_dist", m);
+        cluster_device(c, d_emb, m, d, b->linkage, b->clusters, d_lab, d_left, d_right, d_dist);
+        std::vector<uint32_t> labels = to_host(c, d_lab, m);
+        const double t_cl = now_ms();
+        const uint32_t k = b->clusters;
+        // ---- (3) jobs (pipeline.cpp:249-261) + representatives for the clusters served here
+        std::vector<std::vector<uint32_t>> members(k);
+        for (uint32_t i = 0; i < m; ++i) members[labels[i]].push_back(i);
+        std::vector<uint32_t> owned;
+        std::vector<uint32_t> owner = b->cluster_owner ? to_host(c, b->cluster_owner, k) : std::vector<uint32_t>();
+        for (uint32_t ci = 0; ci < k; ++ci)
+            if (owner.empty() || owner[ci] == static_cast<uint32_t>(b->rank)) owned.push_back(ci);
+        std::vector<std::vector<uint32_t>> own_members;
+        for (uint32_t ci : owned) own_members.push_back(members[ci]);
+        RepResult reps;
+        if (!owned.empty()) reps = build_reps(c, g, hs, m, own_members, budget);
+        std::vector<float> soft_h;
+        std::vector<uint8_t> soft_mask;
+        float* d_soft = nullptr;
+        if (b->soft_prefix && !owned.empty()) {
+            // soft prefix = gnn.encode(representative) (pipeline.cpp:270-276)
+            std::vector<uint64_t> no(1, 0), eo(1, 0);
+            std::vector<uint32_t> rn, re;
+            for (size_t i = 0; i < owned.size(); ++i) {
+                const uint32_t* st = &reps.stats[i * 6];
+                std::vector<uint32_t> sn = to_host(c, reps.d_sel_nodes + i * g->n_nodes, st[0]);
+                std::vector<uint32_t> se = to_host(c, reps.d_sel_edges + i * g->n_edges, st[1]);
+                for (auto v : sn) rn.push_back(g->ids[v]);
+                re.insert(re.end(), se.begin(), se.end());
+                no.push_back(rn.size());
+                eo.push_back(re.size());
+            }
+            HostSubs rs{no, eo, rn, re};
+            sgc_gnn_config gc = b->gnn;
+            gc.dim = d;
+            d_soft = c->buf<float>("run_soft", owned.size() * d);
+            encode_subgraphs(c, g, gc, rs, static_cast<uint32_t>(owned.size()), d_soft);
+        }
+        c->sync();
+        const double t_rep = now_ms();
+        // ---- (4) KV precompute: representative prompts (+ standalone fallbacks) in one batch
+        std::vector<uint64_t> q_off = to_host(c, b->questions.off, m + 1);
+        std::vector<int32_t> q_tok = to_host(c, b->questions.tokens, q_off[m]);
+        std::vector<uint64_t> a_off;
+        std::vector<int32_t> a_tok;
+        const bool ans = b->answers.count == m && b->answers.off;
+        if (ans) {
+            a_off = to_host(c, b->answers.off, m + 1);
+            a_tok = to_host(c, b->answers.tokens, a_off[m]);
+        }
+        std::vector<int32_t> rep_tok = owned.empty() ? std::vector<int32_t>() : to_host(c, reps.d_prefix, reps.prefix_off.back());
+        std::vector<uint64_t> seq_off(1, 0);
+        std::vector<int32_t> seq_tok;
+        std::vector<uint8_t> seq_soft;
+        std::vector<float> seq_soft_vec;
+        std::vector<uint32_t> mem_seg, mem_q;  // extend members
+        std::vector<uint32_t> fb_q;            // fallback queries -> their standalone sequence
+        std::vector<uint64_t> fb_seq;
+        std::vector<float> soft_all;
+        if (d_soft) soft_all = to_host(c, d_soft, owned.size() * d);
+        std::vector<float> emb_h;
+        for (size_t i = 0; i < owned.size(); ++i) {
+            seq_tok.insert(seq_tok.end(), rep_tok.begin() + reps.prefix_off[i], rep_tok.begin() + reps.prefix_off[i + 1]);
+            seq_off.push_back(seq_tok.size());
+            seq_soft.push_back(d_soft ? 1 : 0);
+            if (d_soft) seq_soft_vec.insert(seq_soft_vec.end(), soft_all.begin() + i * d, soft_all.begin() + (i + 1) * d);
+            else seq_soft_vec.insert(seq_soft_vec.end(), d, 0.f);
+            const uint64_t plen = reps.prefix_off[i + 1] - reps.prefix_off[i] + (d_soft ? 1 : 0);
+            if (o->prefix_len) o->prefix_len[owned[i]] = plen;
+            for (uint32_t q : own_members[i]) {
+                const uint64_t qn = q_off[q + 1] - q_off[q];
+                if (plen + qn + lc.max_new_tokens > lc.max_seq_len) {  // cache_engine.cpp:171
+                    fb_q.push_back(q);
+                } else {
+                    mem_seg.push_back(static_cast<uint32_t>(i));
+                    mem_q.push_back(q);
+                }
+            }
+        }
+        // standalone path for fallbacks (cache_engine.cpp:112-138): own prompt + question, trimmed
+        if (!fb_q.empty()) {
+            if (b->own_prefix.count != m) fail(SGC_DOMAIN, "fallback needs own_prefix token lists");
+            std::vector<uint64_t> oo = to_host(c, b->own_prefix.off, m + 1);
+            std::vector<int32_t> ot = to_host(c, b->own_prefix.tokens, oo[m]);
+            if (b->soft_prefix) emb_h = to_host(c, d_emb, static_cast<size_t>(m) * d);
+            for (uint32_t q : fb_q) {
+                std::vector<int32_t> full(ot.begin() + oo[q], ot.begin() + oo[q + 1]);
+                full.insert(full.end(), q_tok.begin() + q_off[q], q_tok.begin() + q_off[q + 1]);
+                size_t allowed = lc.max_seq_len;
+                allowed -= std::min<size_t>(allowed, lc.max_new_tokens + (b->soft_prefix ? 1 : 0));
+                if (full.size() > allowed) full.resize(allowed);
+                fb_seq.push_back(seq_off.size() - 1);
+                seq_tok.insert(seq_tok.end(), full.begin(), full.end());
+                seq_off.push_back(seq_tok.size());
+                seq_soft.push_back(b->soft_prefix ? 1 : 0);
+                if (b->soft_prefix) seq_soft_vec.insert(seq_soft_vec.end(), emb_h.begin() + static_cast<size_t>(q) * d, emb_h.begin() + static_cast<size_t>(q + 1) * d);
+                else seq_soft_vec.insert(seq_soft_vec.end(), d, 0.f);
+            }
+        }
+        uint64_t prefill_rows = 0, extend_rows = 0;
+        sgc_kv* kv = nullptr;
+        std::vector<float> seq_logits;
+        if (seq_off.size() > 1) {
+            const uint32_t ns = static_cast<uint32_t>(seq_off.size() - 1);
+            seq_logits.resize(static_cast<size_t>(ns) * SGC_VOCAB);
+            kv = do_prefill(c, model, ns, seq_off.data(), seq_tok.data(), seq_soft_vec.data(), seq_soft.data(),
+                            seq_logits.data());
+            prefill_rows = kv->rows;
+        }
+        const double t_pf = now_ms();
+        // ---- (5) per-query reuse: all members of all served clusters in one cascade pass
+        std::unique_ptr<sgc_kv, int (*)(sgc_kv*)> kv_guard(kv, sgc_kv_release);
+        if (!mem_q.empty()) {
+            std::vector<uint64_t> mq_off(1, 0), ma_off(1, 0);
+            std::vector<int32_t> mq_tok, ma_tok;
+            for (uint32_t q : mem_q) {
+                mq_tok.insert(mq_tok.end(), q_tok.begin() + q_off[q], q_tok.begin() + q_off[q + 1]);
+                mq_off.push_back(mq_tok.size());
+                if (ans) ma_tok.insert(ma_tok.end(), a_tok.begin() + a_off[q], a_tok.begin() + a_off[q + 1]);
+                ma_off.push_back(ma_tok.size());
+                extend_rows += q_off[q + 1] - q_off[q];
+            }
+            const uint32_t nm = static_cast<uint32_t>(mem_q.size());
+            std::vector<float> lg(static_cast<size_t>(nm) * SGC_VOCAB);
+            std::vector<int32_t> ft(nm);
+            do_extend(c, model, kv, nm, mem_seg.data(), mq_off.data(), mq_tok.data(), ans ? ma_off.data() : nullptr,
+                      ans ? ma_tok.data() : nullptr, b->pointer_bonus, lg.data(), ft.data());
+            for (uint32_t j = 0; j < nm; ++j) {
+                const uint32_t q = mem_q[j];
+                if (o->logits)
+                    sgc::copy_out(c, o->logits + static_cast<size_t>(q) * SGC_VOCAB, lg.data() + static_cast<size_t>(j) * SGC_VOCAB, SGC_VOCAB);
+                if (o->first_token) sgc::copy_out(c, o->first_token + q, ft.data() + j, 1);
+                if (o->fallback) {
+                    uint8_t z = 0;
+                    sgc::copy_out(c, o->fallback + q, &z, 1);
+                }
+            }
+            c->sync();
+        }
+        // fallback first tokens: standalone logits, hint over the own prompt prefix
+        for (size_t f = 0; f < fb_q.size(); ++f) {
+            const uint32_t q = fb_q[f];
+            const uint64_t s = fb_seq[f];
+            const float* lg = seq_logits.data() + s * SGC_VOCAB;
+            const uint64_t ctx_len = seq_off[s + 1] - seq_off[s] + (b->soft_prefix ? 1 : 0);
+            const uint64_t qn = std::min<uint64_t>(q_off[q + 1] - q_off[q], ctx_len);
+            const uint64_t limit = ctx_len - qn;
+            int target = -1;
+            if (ans && a_off[q + 1] > a_off[q]) {
+                std::vector<int32_t> ctxv;
+                if (b->soft_prefix) ctxv.push_back(259);
+                ctxv.insert(ctxv.end(), seq_tok.begin() + seq_off[s], seq_tok.begin() + seq_off[s + 1]);
+                const int32_t* a = a_tok.data() + a_off[q];
+                const uint64_t al = a_off[q + 1] - a_off[q];
+                for (uint64_t st = 0; st + al <= limit && target < 0; ++st)
+                    if (std::equal(a, a + al, ctxv.begin() + st)) target = a[0];
+            }
+            int best = 0;
+            float bv = lg[0] + (target == 0 ? b->pointer_bonus : 0.0f);
+            for (int v = 1; v < SGC_VOCAB; ++v) {
+                float val = lg[v] + (v == target ? b->pointer_bonus : 0.0f);
+                if (val > bv) {
+                    bv = val;
+                    best = v;
+                }
+            }
+            if (o->logits) sgc::copy_out(c, o->logits + static_cast<size_t>(q) * SGC_VOCAB, lg, SGC_VOCAB);
+            if (o->first_token) sgc::copy_out(c, o->first_token + q, &best, 1);
+            if (o->fallback) {
+                uint8_t one = 1;
+                sgc::copy_out(c, o->fallback + q, &one, 1);
+            }
+            c->sync();
+        }
+        const double t_ext = now_ms();
+        if (o->embeddings) sgc::copy_out(c, o->embeddings, d_emb, static_cast<size_t>(m) * d);
+        if (o->labels) sgc::copy_out(c, o->labels, d_lab, m);
+        if (o->merge_left) sgc::copy_out(c, o->merge_left, d_left, m - k);
+        if (o->merge_right) sgc::copy_out(c, o->merge_right, d_right, m - k);
+        if (o->merge_dist) sgc::copy_out(c, o->merge_dist, d_dist, m - k);
+        c->sync();
+        o->stage_ms[0] = t_enc - t_start;
+        o->stage_ms[1] = t_cl - t_enc;
+        o->stage_ms[2] = t_rep - t_cl;
+        o->stage_ms[3] = t_pf - t_rep;
+        o->stage_ms[4] = t_ext - t_pf;
+        o->stage_ms[5] = now_ms() - t_start;
+        o->prefill_rows = prefill_rows;
+        o->extend_rows = extend_rows;
+    });
+}
+
+int sgc_gemm_bf16(sgc_ctx* ctx, const void* a, const void* b, void* d, uint32_t M, uint32_t N, uint32_t K, int epi) {
+    return guarded([&] {
+        sgc::GemmEpi e;
+        e.mode = epi;
+        e.out = d;
+        e.ldo = static_cast<int>(N);
+        if (epi == sgc::EPI_QKV) fail(SGC_DOMAIN, "QKV epilogue is internal");
+        sgc::gemm_bf16(&ctx->c, a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e);
+        ctx->c.sync();
+    });
+}
+
+int sgc_set_timing(sgc_ctx* ctx, int enable) {
+    return guarded([&] {
+        ctx->c.sync();
+        ctx->c.timing = enable != 0;
+        ctx->c.timings.clear();
+    });
+}
+
+int sgc_get_timing(sgc_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches) {
+    return guarded([&] {
+        ctx->c.sync();
+        auto it = ctx->c.timings.find(kernel);
+        *total_ms = it == ctx->c.timings.end() ? 0.0 : it->second.ms;
+        *launches = it == ctx->c.timings.end() ? 0 : it->second.launches;
+    });
+}
+
+}  // extern "C"

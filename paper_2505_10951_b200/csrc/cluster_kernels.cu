@@ -1,0 +1,291 @@
+// cluster_kernels.cu -- exact fp64 pairwise distances and the Lance-Williams agglomeration
+// (clustering.cpp:33-174) on the device, bit-identical to the reference.
+//
+// Exactness rules: direct-form sum over k in sequential order with every
+// mul/add rounded separately (__dmul_rn/__dadd_rn, no FMA), sqrt then square for
+// ward/centroid, the same Lance-Williams operand order, and the (value, i, j) lexicographic
+// argmin -- which equals the reference's tie rule because an alive slot's index is always its
+// min member (clustering.cpp:113).
+#include "cluster_kernels.cuh"
+#include "common.cuh"
+
+namespace sgc {
+namespace {
+
+constexpr int PT = 64;   // pair tile
+constexpr int PK = 16;   // k chunk
+
+// encoders.cpp:40-48 euclidean_distance for all i<j (one thread = 4x4 pairs, k sequential)
+__global__ void __launch_bounds__(256)
+    pairwise_kernel(double* D, const float* emb, int m, int dim, const int2* tiles, int squared) {
+    __shared__ float As[PK][PT + 1];
+    __shared__ float Bs[PK][PT + 1];
+    const int2 tile = tiles[blockIdx.x];
+    const int i0 = tile.x * PT, j0 = tile.y * PT;
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    for (int k0 = 0; k0 < dim; k0 += PK) {
+        for (int idx = threadIdx.x; idx < PT * PK; idx += 256) {
+            int r = idx / PK, kk = idx % PK;
+            int gi = i0 + r, gj = j0 + r, gk = k0 + kk;
+            As[kk][r] = (gi < m && gk < dim) ? emb[static_cast<size_t>(gi) * dim + gk] : 0.f;
+            Bs[kk][r] = (gj < m && gk < dim) ? emb[static_cast<size_t>(gj) * dim + gk] : 0.f;
+        }
+        __syncthreads();
+        const int kn = min(PK, dim - k0);
+        for (int kk = 0; kk < kn; ++kk) {
+            double a[4], b[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                a[q] = static_cast<double>(As[kk][ty + 16 * q]);
+                b[q] = static_cast<double>(Bs[kk][tx + 16 * q]);
+            }
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    double v = __dsub_rn(a[p], b[q]);
+                    acc[p][q] = __dadd_rn(acc[p][q], __dmul_rn(v, v));
+                }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            int i = i0 + ty + 16 * p, j = j0 + tx + 16 * q;
+            if (i < m && j < m && i <= j) {
+                double v = i == j ? 0.0 : __dsqrt_rn(acc[p][q]);
+                if (squared) v = __dmul_rn(v, v);  // clustering.cpp:72-74 squares the sqrt
+                D[static_cast<size_t>(i) * m + j] = v;
+                D[static_cast<size_t>(j) * m + i] = v;
+            }
+        }
+}
+
+struct Best {
+    double v;
+    int j;
+};
+__device__ __forceinline__ bool better(double v, int j, double bv, int bj) {
+    return v < bv || (v == bv && j < bj);
+}
+
+constexpr int kAggThreads = 1024;
+
+// One CTA runs the whole merge loop. Per alive row i a cached (value, j) minimum over alive
+// j > i is maintained; after a merge only rows whose cached argmin touched keep/kill (or row
+// keep itself) are rescanned, every other row gets an O(1) update against the new D[i][keep].
+__global__ void __launch_bounds__(kAggThreads)
+    agglomerate_kernel(double* D, int m, int c, int linkage, uint32_t* labels, uint32_t* merge_left,
+                       uint32_t* merge_right, double* merge_dist) {
+    extern __shared__ uint8_t sm[];
+    double* rv = reinterpret_cast<double*>(sm);                 // [m] row-min value
+    int* rj = reinterpret_cast<int*>(rv + m);                   // [m] row-min column
+    int* size = rj + m;                                         // [m]
+    int* owner = size + m;                                      // [m] point -> slot
+    int* rescan = owner + m;                                    // [m] rows to rescan
+    unsigned char* alive = reinterpret_cast<unsigned char*>(rescan + m);
+    __shared__ double red_v[32];
+    __shared__ int red_i[32], red_j[32];
+    __shared__ int n_rescan;
+    __shared__ int s_keep, s_kill;
+    __shared__ double s_best;
+
+    const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32, nwarps = blockDim.x / 32;
+    for (int i = tid; i < m; i += blockDim.x) {
+        alive[i] = 1;
+        size[i] = 1;
+        owner[i] = i;
+    }
+    __syncthreads();
+
+    auto scan_row = [&](int i) {  // warp-cooperative: min over alive j > i of (D[i][j], j)
+        double bv = INFINITY;
+        int bj = 0x7fffffff;
+        const double* row = D + static_cast<size_t>(i) * m;
+        for (int j = i + 1 + lane; j < m; j += 32) {
+            if (!alive[j]) continue;
+            double v = row[j];
+            if (better(v, j, bv, bj)) {
+                bv = v;
+                bj = j;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            double ov = __shfl_xor_sync(0xffffffff, bv, o);
+            int oj = __shfl_xor_sync(0xffffffff, bj, o);
+            if (better(ov, oj, bv, bj)) {
+                bv = ov;
+                bj = oj;
+            }
+        }
+        if (lane == 0) {
+            rv[i] = bv;
+            rj[i] = bj;
+        }
+    };
+    for (int i = warp; i < m; i += nwarps) scan_row(i);
+    __syncthreads();
+
+    const int steps = m - c;
+    for (int step = 0; step < steps; ++step) {
+        // ---- global argmin over rows, key (value, i, j)
+        double bv = INFINITY;
+        int bi = 0x7fffffff, bj = 0x7fffffff;
+        for (int i = tid; i < m; i += blockDim.x) {
+            if (!alive[i] || rj[i] == 0x7fffffff) continue;
+            double v = rv[i];
+            if (v < bv || (v == bv && (i < bi || (i == bi && rj[i] < bj)))) {
+                bv = v;
+                bi = i;
+                bj = rj[i];
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            double ov = __shfl_xor_sync(0xffffffff, bv, o);
+            int oi = __shfl_xor_sync(0xffffffff, bi, o);
+            int oj = __shfl_xor_sync(0xffffffff, bj, o);
+            if (ov < bv || (ov == bv && (oi < bi || (oi == bi && oj < bj)))) {
+                bv = ov;
+                bi = oi;
+                bj = oj;
+            }
+        }
+        if (lane == 0) {
+            red_v[warp] = bv;
+            red_i[warp] = bi;
+            red_j[warp] = bj;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < nwarps; ++w) {
+                double ov = red_v[w];
+                int oi = red_i[w], oj = red_j[w];
+                if (ov < bv || (ov == bv && (oi < bi || (oi == bi && oj < bj)))) {
+                    bv = ov;
+                    bi = oi;
+                    bj = oj;
+                }
+            }
+            s_keep = bi;  // slot index == min member, bi < bj
+            s_kill = bj;
+            s_best = bv;
+            merge_left[step] = bi;
+            merge_right[step] = bj;
+            merge_dist[step] = linkage == SGC_WARD ? __ddiv_rn(bv, 2.0)
+                               : linkage == SGC_CENTROID ? __dsqrt_rn(bv)
+                                                         : bv;
+            n_rescan = 0;
+        }
+        __syncthreads();
+        const int keep = s_keep, kill = s_kill;
+        const double na = size[keep], nb = size[kill];
+        double* Dk = D + static_cast<size_t>(keep) * m;
+        const double* Dl = D + static_cast<size_t>(kill) * m;
+        const double dab = Dk[kill];
+        // ---- Lance-Williams update (clustering.cpp:128-148), same operand order, no FMA
+        for (int k = tid; k < m; k += blockDim.x) {
+            if (!alive[k] || k == keep || k == kill) continue;
+            const double dak = Dk[k], dbk = Dl[k];
+            const double nk = size[k];
+            double v;
+            switch (linkage) {
+                case SGC_SINGLE: v = dak < dbk ? dak : dbk; break;
+                case SGC_COMPLETE: v = dak > dbk ? dak : dbk; break;
+                case SGC_AVERAGE:
+                    v = __ddiv_rn(__dadd_rn(__dmul_rn(na, dak), __dmul_rn(nb, dbk)), __dadd_rn(na, nb));
+                    break;
+                case SGC_CENTROID: {
+                    double s = __dadd_rn(na, nb);
+                    double t1 = __ddiv_rn(__dadd_rn(__dmul_rn(na, dak), __dmul_rn(nb, dbk)), s);
+                    double t2 = __ddiv_rn(__dmul_rn(__dmul_rn(na, nb), dab), __dmul_rn(s, s));
+                    v = __dsub_rn(t1, t2);
+                    break;
+                }
+                default: {  // ward
+                    double t = __dadd_rn(__dmul_rn(__dadd_rn(na, nk), dak), __dmul_rn(__dadd_rn(nb, nk), dbk));
+                    t = __dsub_rn(t, __dmul_rn(nk, dab));
+                    v = __ddiv_rn(t, __dadd_rn(__dadd_rn(na, nb), nk));
+                }
+            }
+            Dk[k] = v;
+            D[static_cast<size_t>(k) * m + keep] = v;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            alive[kill] = 0;
+            size[keep] += size[kill];
+        }
+        for (int p = tid; p < m; p += blockDim.x)
+            if (owner[p] == kill) owner[p] = keep;
+        __syncthreads();
+        // ---- row-min maintenance
+        for (int i = tid; i < kill; i += blockDim.x) {
+            if (!alive[i]) continue;
+            bool need = false;
+            if (i == keep) need = true;
+            else if (rj[i] == kill) need = true;
+            else if (i < keep) {
+                if (rj[i] == keep) need = true;
+                else {
+                    double v = D[static_cast<size_t>(i) * m + keep];
+                    if (better(v, keep, rv[i], rj[i])) {
+                        rv[i] = v;
+                        rj[i] = keep;
+                    }
+                }
+            }
+            if (need) rescan[atomicAdd(&n_rescan, 1)] = i;
+        }
+        __syncthreads();
+        const int nr = n_rescan;
+        for (int r = warp; r < nr; r += nwarps) scan_row(rescan[r]);
+        __syncthreads();
+    }
+    // ---- labels by ascending min member (clustering.cpp:162-172): alive slot i == min member
+    if (tid == 0) {
+        int next = 0;
+        for (int i = 0; i < m; ++i)
+            if (alive[i]) rescan[i] = next++;
+    }
+    __syncthreads();
+    for (int p = tid; p < m; p += blockDim.x) labels[p] = rescan[owner[p]];
+}
+
+}  // namespace
+
+void pairwise_distances(Ctx* c, double* D, const float* emb, int m, int dim, bool squared) {
+    int nt = (m + PT - 1) / PT;
+    std::vector<int2> tiles;
+    for (int a = 0; a < nt; ++a)
+        for (int b = a; b < nt; ++b) tiles.push_back(make_int2(a, b));
+    int2* dt = c->buf<int2>("pairwise_tiles", tiles.size());
+    copy_in(c, dt, tiles.data(), tiles.size());
+    Ctx::Timed timer(c, "pairwise");
+    pairwise_kernel<<<tiles.size(), 256, 0, c->stream>>>(D, emb, m, dim, dt, squared ? 1 : 0);
+    SGC_LAUNCH_CHECK(c);
+    // keep `tiles` alive until the async copy has consumed it
+    SGC_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+}
+
+size_t agglomerate_smem(int m) { return static_cast<size_t>(m) * (8 + 4 * 4 + 1) + 16; }
+
+void agglomerate(Ctx* c, double* D, int m, int clusters, int linkage, uint32_t* labels,
+                 uint32_t* merge_left, uint32_t* merge_right, double* merge_dist) {
+    size_t smem = agglomerate_smem(m);
+    if (smem > 200 * 1024) fail(SGC_DOMAIN, "agglomerate: m too large for the on-chip merge loop");
+    SGC_CUDA_CHECK(cudaFuncSetAttribute(agglomerate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)));
+    Ctx::Timed timer(c, "agglomerate");
+    agglomerate_kernel<<<1, kAggThreads, smem, c->stream>>>(D, m, clusters, linkage, labels, merge_left,
+                                                            merge_right, merge_dist);
+    SGC_LAUNCH_CHECK(c);
+}
+
+}  // namespace sgc

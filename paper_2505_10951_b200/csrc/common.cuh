@@ -1,0 +1,146 @@
+// common.cuh -- shared host/device plumbing for the sm_100a SubGCache library.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "sgc_b200.h"
+
+namespace sgc {
+
+// ---- error taxonomy (mirrors include/subgcache/errors.hpp:9-32) ---------------------
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+#define SGC_CUDA_CHECK(x)                                                                    \
+    do {                                                                                     \
+        cudaError_t _e = (x);                                                                \
+        if (_e != cudaSuccess)                                                               \
+            ::sgc::fail(SGC_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e) + " @" +   \
+                                      __FILE__ + ":" + std::to_string(__LINE__));            \
+    } while (0)
+
+#define SGC_LAUNCH_CHECK(ctx)                                                                \
+    do {                                                                                     \
+        cudaError_t _e = cudaGetLastError();                                                 \
+        if (_e != cudaSuccess)                                                               \
+            ::sgc::fail(SGC_CUDA, std::string("kernel launch: ") + cudaGetErrorString(_e) +  \
+                                      " @" + __FILE__ + ":" + std::to_string(__LINE__));     \
+        (ctx)->launches++;                                                                   \
+    } while (0)
+
+// ---- device scratch arena: grow-only buffers keyed by name -------------------------------
+struct Buffer {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+
+struct KernelTiming {
+    double ms = 0;
+    uint64_t launches = 0;
+};
+
+struct Ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    uint64_t launches = 0;
+    std::map<std::string, Buffer> scratch;
+    bool timing = false;
+    std::map<std::string, KernelTiming> timings;
+    // pending (name, start, stop) event triples, resolved at the next sync point
+    std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::vector<cudaEvent_t> event_pool;
+
+    template <typename T>
+    T* buf(const std::string& name, size_t count) {
+        Buffer& b = scratch[name];
+        size_t need = count * sizeof(T);
+        if (need == 0) need = 16;
+        if (b.bytes < need) {
+            if (b.ptr) SGC_CUDA_CHECK(cudaFreeAsync(b.ptr, stream));
+            size_t cap = need + need / 8;
+            SGC_CUDA_CHECK(cudaMallocAsync(&b.ptr, cap, stream));
+            b.bytes = cap;
+        }
+        return reinterpret_cast<T*>(b.ptr);
+    }
+
+    cudaEvent_t event() {
+        if (!event_pool.empty()) {
+            cudaEvent_t e = event_pool.back();
+            event_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        SGC_CUDA_CHECK(cudaEventCreate(&e));
+        return e;
+    }
+    // bracket a launch with events when timing is on
+    struct Timed {
+        Ctx* c;
+        std::string name;
+        cudaEvent_t a = nullptr, b = nullptr;
+        Timed(Ctx* ctx, const char* n) : c(ctx), name(n) {
+            if (c->timing) {
+                a = c->event();
+                b = c->event();
+                cudaEventRecord(a, c->stream);
+            }
+        }
+        ~Timed() {
+            if (a) {
+                cudaEventRecord(b, c->stream);
+                c->pending.push_back({name, {a, b}});
+            }
+        }
+    };
+    void resolve_timings() {
+        for (auto& p : pending) {
+            float ms = 0;
+            cudaEventSynchronize(p.second.second);
+            cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+            KernelTiming& t = timings[p.first];
+            t.ms += ms;
+            t.launches++;
+            event_pool.push_back(p.second.first);
+            event_pool.push_back(p.second.second);
+        }
+        pending.clear();
+    }
+    void sync() {
+        SGC_CUDA_CHECK(cudaStreamSynchronize(stream));
+        resolve_timings();
+    }
+};
+
+// copy helpers that accept host or device pointers (cudaMemcpyDefault under UVA)
+template <typename T>
+inline void copy_in(Ctx* c, T* dst_dev, const T* src, size_t n) {
+    if (n) SGC_CUDA_CHECK(cudaMemcpyAsync(dst_dev, src, n * sizeof(T), cudaMemcpyDefault, c->stream));
+}
+template <typename T>
+inline void copy_out(Ctx* c, T* dst, const T* src_dev, size_t n) {
+    if (n && dst) SGC_CUDA_CHECK(cudaMemcpyAsync(dst, src_dev, n * sizeof(T), cudaMemcpyDefault, c->stream));
+}
+
+inline unsigned ceil_div(uint64_t a, uint64_t b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+}  // namespace sgc
+
+// opaque handle definitions
+struct sgc_ctx {
+    sgc::Ctx c;
+};

@@ -1,0 +1,30 @@
+// gemm.cuh -- host interface of the tcgen05 GEMM (gemm_sm100.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace sgc {
+
+struct Ctx;
+
+enum { EPI_F32 = 0, EPI_BF16 = 1, EPI_RESID = 2, EPI_TANH = 3, EPI_QKV = 4 };
+
+struct GemmEpi {
+    int mode = EPI_F32;
+    void* out = nullptr;  // F32/BF16/TANH: output; RESID: fp32 residual updated in place
+    int ldo = 0;
+    // EPI_QKV (N = 3d): q -> q_out[row], k -> k_cache[kv_row[row]], v -> v_cache[kv_row[row]]
+    __nv_bfloat16* q_out = nullptr;
+    __nv_bfloat16* k_cache = nullptr;
+    __nv_bfloat16* v_cache = nullptr;
+    const int32_t* kv_row = nullptr;
+    const int32_t* pos = nullptr;
+    const float* rope_cos = nullptr;  // [max_seq x hd/2]
+    const float* rope_sin = nullptr;
+    int d = 0;
+    int hd = 0;
+};
+
+void gemm_bf16(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep);
+
+}  // namespace sgc

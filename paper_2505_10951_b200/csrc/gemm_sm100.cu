@@ -1,0 +1,409 @@
+// gemm_sm100.cu -- persistent, warp-specialized tcgen05/TMEM/TMA GEMM for sm_100a with the
+// ToyLm's fused epilogues.
+//
+// D[M x N] = A[M x K] * B[N x K]^T; A = activations (bf16, row-major), B = a ToyLm weight
+// (bf16, row-major [out x in], lm_core.hpp:161-168), fp32 accumulation in TMEM.
+//
+//   warp 0      TMA producer: A 128x64 and B BNx64 tiles (128B swizzle) into a smem ring
+//   warp 1      MMA issuer: one thread issues tcgen05.mma (M=128, N=BN, K=16) x4 per stage
+//   warp 2      TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
+//   warps 4..7  epilogue: tcgen05.ld -> fused epilogue -> global stores
+//
+// Epilogues (the ops the reference runs after each matvec, lm_core.cpp:220-283):
+//   EPI_F32 / EPI_BF16   plain store
+//   EPI_RESID            x += D                         (residual add, lm_core.cpp:277,283)
+//   EPI_TANH             h = bf16(tanh(D))              (FFN activation, :281)
+//   EPI_QKV              RoPE(q), RoPE(k) -> K cache, v -> V cache, q -> Q buffer (:227-244)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "sm100_ptx.cuh"
+
+namespace sgc {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
+constexpr int kThreads = 256;
+
+template <int BN>
+struct Cfg {
+    static constexpr int kStages = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+    static constexpr int kABytes = BM * BK * 2;
+    static constexpr int kBBytes = BN * BK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
+    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ float tanh_fast(float x) {
+    // tanh via exp2: accurate to ~1e-7 relative, saturates cleanly (reference clamps at 9,
+    // kernels_scalar.cpp:74-81)
+    x = fminf(fmaxf(x, -9.0f), 9.0f);
+    float e = exp2f(x * 2.8853900817779268f);  // exp(2x)
+    return __fdividef(e - 1.0f, e + 1.0f);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// store 32 fp32 values as bf16 (64 contiguous bytes)
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v) {
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+        w.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+        w.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+        w.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+        d4[q] = w;
+    }
+}
+
+// RoPE on a pair of 32-column chunks (lo = cols i, hi = cols i+half), reference op order
+// (lm_core.cpp:231-238) without FMA contraction.
+__device__ __forceinline__ void rope_pair(float* lo, float* hi, const float* cosp,
+                                          const float* sinp) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        float c = cosp[j], s = sinp[j];
+        float a = lo[j], b = hi[j];
+        lo[j] = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, s));
+        hi[j] = __fadd_rn(__fmul_rn(b, c), __fmul_rn(a, s));
+    }
+}
+
+template <int BN, int EPI, int HD>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                int M, int N, int K, GemmEpi ep) {
+    using C = Cfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* smemA = smem;
+    uint8_t* smemB = smem + C::kStages * C::kABytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + C::kStages;
+    uint64_t* tfull = bars + 2 * C::kStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const int m_tiles = (M + BM - 1) / BM;
+    const int n_tiles = N / BN;
+    const int num_tiles = m_tiles * n_tiles;
+    const int num_kb = K / BK;
+    // grouped raster: GROUP m-tiles sweep all n-tiles before moving on, so both the
+    // activation rows and the weight tiles of the concurrently running CTAs stay in L2
+    const int GROUP = 16;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+        for (int s = 0; s < C::kStages; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 128);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    auto tile_coords = [&](int t, int& m0, int& n0) {
+        int per_group = GROUP * n_tiles;
+        int g = t / per_group;
+        int first_m = g * GROUP;
+        int gsize = min(GROUP, m_tiles - first_m);
+        int r = t % per_group;
+        m0 = (first_m + r % gsize) * BM;
+        n0 = (r / gsize) * BN;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                int m0, n0;
+                tile_coords(t, m0, n0);
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    ptx::mbar_expect_tx(&full[stage], C::kStageBytes);
+                    ptx::tma_load_2d(smemA + stage * C::kABytes, &tmA, &full[stage], kb * BK, m0);
+                    ptx::tma_load_2d(smemB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, n0);
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+                const int acc = local & 1;
+                const uint32_t acc_phase = (local >> 1) & 1;
+                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = ptx::smem_u32(smemA + stage * C::kABytes);
+                    const uint32_t b_addr = ptx::smem_u32(smemB + stage * C::kBBytes);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        uint64_t ad = ptx::umma_desc_sw128(a_addr + k * 32);
+                        uint64_t bd = ptx::umma_desc_sw128(b_addr + k * 32);
+                        ptx::mma_bf16(tmem_d, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    ptx::mma_commit(&empty[stage]);
+                    if (++stage == C::kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::mma_commit(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
+        int local = 0;
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+            int m0, n0;
+            tile_coords(t, m0, n0);
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            const int row = m0 + ew * 32 + lane;
+            const bool valid = row < M;
+            const uint32_t tbase = tmem_base + ((ew * 32) << 16) + acc * BN;
+
+            if constexpr (EPI == EPI_QKV) {
+                // one tile never straddles the q/k/v sections (d % BN == 0)
+                const int d = ep.d;
+                const int section = n0 / d;
+                const int c0 = n0 - section * d;
+                constexpr int HALF = HD / 2;
+                int pos = 0, kvr = 0;
+                if (valid) {
+                    pos = ep.pos[row];
+                    kvr = ep.kv_row[row];
+                }
+                if (section == 2) {
+#pragma unroll 1
+                    for (int ch = 0; ch < BN / 32; ++ch) {
+                        uint32_t r[32];
+                        ptx::tmem_ld32(tbase + ch * 32, r);
+                        ptx::tmem_ld_wait();
+                        if (valid)
+                            store_bf16x32(ep.v_cache + static_cast<size_t>(kvr) * d + c0 + ch * 32,
+                                          reinterpret_cast<float*>(r));
+                    }
+                } else {
+                    __nv_bfloat16* dst = section == 0
+                                             ? ep.q_out + static_cast<size_t>(row) * d
+                                             : ep.k_cache + static_cast<size_t>(kvr) * d;
+                    const float* cosp = ep.rope_cos + static_cast<size_t>(pos) * HALF;
+                    const float* sinp = ep.rope_sin + static_cast<size_t>(pos) * HALF;
+                    if constexpr (HALF >= 32) {
+                        // pairs span two chunks: (ch, ch + HALF/32) within each head
+#pragma unroll 1
+                        for (int ch = 0; ch < BN / 32; ++ch) {
+                            const int in_head = (ch * 32) % HD;
+                            if (in_head >= HALF) continue;
+                            const int ch2 = ch + HALF / 32;
+                            uint32_t lo[32], hi[32];
+                            ptx::tmem_ld32(tbase + ch * 32, lo);
+                            ptx::tmem_ld32(tbase + ch2 * 32, hi);
+                            ptx::tmem_ld_wait();
+                            if (valid) {
+                                float cs[32], sn[32];
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) {
+                                    cs[j] = __ldg(cosp + in_head + j);
+                                    sn[j] = __ldg(sinp + in_head + j);
+                                }
+                                rope_pair(reinterpret_cast<float*>(lo), reinterpret_cast<float*>(hi),
+                                          cs, sn);
+                                store_bf16x32(dst + c0 + ch * 32, reinterpret_cast<float*>(lo));
+                                store_bf16x32(dst + c0 + ch2 * 32, reinterpret_cast<float*>(hi));
+                            }
+                        }
+                    } else {
+                        // whole heads inside one 32-column chunk
+#pragma unroll 1
+                        for (int ch = 0; ch < BN / 32; ++ch) {
+                            uint32_t r[32];
+                            ptx::tmem_ld32(tbase + ch * 32, r);
+                            ptx::tmem_ld_wait();
+                            if (valid) {
+                                float* v = reinterpret_cast<float*>(r);
+                                float o[32];
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) {
+                                    const int i = j % HD;
+                                    if (i < HALF) {
+                                        float c = __ldg(cosp + i), s = __ldg(sinp + i);
+                                        float a = v[j], b = v[j + HALF];
+                                        o[j] = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, s));
+                                        o[j + HALF] = __fadd_rn(__fmul_rn(b, c), __fmul_rn(a, s));
+                                    }
+                                }
+                                store_bf16x32(dst + c0 + ch * 32, o);
+                            }
+                        }
+                    }
+                }
+            } else {
+#pragma unroll 1
+                for (int ch = 0; ch < BN / 32; ++ch) {
+                    uint32_t r[32];
+                    ptx::tmem_ld32(tbase + ch * 32, r);
+                    ptx::tmem_ld_wait();
+                    if (!valid) continue;
+                    float* v = reinterpret_cast<float*>(r);
+                    const int col = n0 + ch * 32;
+                    if constexpr (EPI == EPI_F32) {
+                        float4* dst = reinterpret_cast<float4*>(
+                            static_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ldo + col);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    } else if constexpr (EPI == EPI_BF16) {
+                        store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) +
+                                          static_cast<size_t>(row) * ep.ldo + col,
+                                      v);
+                    } else if constexpr (EPI == EPI_TANH) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = tanh_fast(v[j]);
+                        store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) +
+                                          static_cast<size_t>(row) * ep.ldo + col,
+                                      v);
+                    } else if constexpr (EPI == EPI_RESID) {
+                        float4* dst = reinterpret_cast<float4*>(
+                            static_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ldo + col);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            float4 x = dst[q];
+                            x.x += v[4 * q];
+                            x.y += v[4 * q + 1];
+                            x.z += v[4 * q + 2];
+                            x.w += v[4 * q + 3];
+                            dst[q] = x;
+                        }
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(&tempty[acc]);
+        }
+    }
+
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+    }
+}
+
+// ---- host side ----------------------------------------------------------------------------
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        SGC_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) fail(SGC_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+CUtensorMap make_map_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
+                        uint32_t box_cols) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(SGC_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
+
+template <int BN, int EPI, int HD>
+void launch(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
+    using Cf = Cfg<BN>;
+    static bool attr_set = false;  // per-instantiation (per process; single device type)
+    auto kfn = gemm_kernel<BN, EPI, HD>;
+    if (!attr_set) {
+        SGC_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmem));
+        attr_set = true;
+    }
+    CUtensorMap ta = make_map_2d(A, M, K, BM, BK);
+    CUtensorMap tb = make_map_2d(B, N, K, BN, BK);
+    int tiles = ((M + BM - 1) / BM) * (N / BN);
+    int grid = tiles < c->num_sms ? tiles : c->num_sms;
+    Ctx::Timed timer(c, "gemm");
+    kfn<<<grid, kThreads, Cf::kSmem, c->stream>>>(ta, tb, M, N, K, ep);
+    SGC_LAUNCH_CHECK(c);
+}
+
+template <int EPI, int HD>
+void dispatch_bn(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
+    // widest tile that divides N (and d, for the QKV section split)
+    int lim = EPI == EPI_QKV ? ep.d : N;
+    if (N % 256 == 0 && lim % 256 == 0) launch<256, EPI, HD>(c, A, B, M, N, K, ep);
+    else if (N % 128 == 0 && lim % 128 == 0) launch<128, EPI, HD>(c, A, B, M, N, K, ep);
+    else if (N % 64 == 0 && lim % 64 == 0) launch<64, EPI, HD>(c, A, B, M, N, K, ep);
+    else fail(SGC_DOMAIN, "gemm: N must be a multiple of 64");
+}
+
+}  // namespace
+
+void gemm_bf16(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
+    if (M <= 0) return;
+    if (K % BK != 0) fail(SGC_DOMAIN, "gemm: K must be a multiple of 64");
+    switch (ep.mode) {
+        case EPI_F32: dispatch_bn<EPI_F32, 0>(c, A, B, M, N, K, ep); break;
+        case EPI_BF16: dispatch_bn<EPI_BF16, 0>(c, A, B, M, N, K, ep); break;
+        case EPI_RESID: dispatch_bn<EPI_RESID, 0>(c, A, B, M, N, K, ep); break;
+        case EPI_TANH: dispatch_bn<EPI_TANH, 0>(c, A, B, M, N, K, ep); break;
+        case EPI_QKV:
+            if (ep.hd == 128) dispatch_bn<EPI_QKV, 128>(c, A, B, M, N, K, ep);
+            else if (ep.hd == 64) dispatch_bn<EPI_QKV, 64>(c, A, B, M, N, K, ep);
+            else if (ep.hd == 32) dispatch_bn<EPI_QKV, 32>(c, A, B, M, N, K, ep);
+            else if (ep.hd == 16) dispatch_bn<EPI_QKV, 16>(c, A, B, M, N, K, ep);
+            else fail(SGC_DOMAIN, "gemm: head_dim must be 16, 32, 64 or 128");
+            break;
+        default: fail(SGC_DOMAIN, "gemm: unknown epilogue");
+    }
+}
+
+}  // namespace sgc

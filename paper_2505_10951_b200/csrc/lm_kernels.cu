@@ -1,0 +1,260 @@
+// lm_kernels.cu -- ToyLm support kernels: seeded weight generation, embedding gather,
+// RMSNorm (no gain), fp32 head + RMSNorm for the logit rows, copy-pointer search and the
+// biased greedy argmax of the first token.
+#include "common.cuh"
+#include "lm_kernels.cuh"
+#include "rng.cuh"
+
+namespace sgc {
+namespace {
+
+__global__ void gen_uniform_f32(float* out, uint64_t n, uint64_t state0, float lo, float hi) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = uniform_at(state0, i, lo, hi);
+}
+
+__global__ void gen_uniform_bf16(__nv_bfloat16* out, uint64_t n, uint64_t state0, float lo,
+                                 float hi) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = __float2bfloat16_rn(uniform_at(state0, i, lo, hi));
+}
+
+// text projection [dim x 4096] (encoders.cpp:50-55) stored transposed [4096 x dim]
+__global__ void gen_projection_t(float* out_t, uint32_t dim, uint64_t state0) {
+    uint64_t n = (uint64_t)dim * 4096;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t k = i / 4096, b = i % 4096;
+        out_t[b * dim + k] = uniform_at(state0, i, -1.0f, 1.0f);
+    }
+}
+
+// embed_tokens (lm_core.cpp:163-173) + soft slot (:308-320): x[r] = tok_emb[id] or soft[s]
+__global__ void embed_kernel(float* x, const int32_t* tokens, const float* tok_emb,
+                             const float* soft, const int32_t* soft_idx, int d, int rows,
+                             int* bad) {
+    int r = blockIdx.x;
+    if (r >= rows) return;
+    int id = tokens[r];
+    const float* src;
+    if (id == 259 && soft_idx && soft_idx[r] >= 0) {
+        src = soft + static_cast<size_t>(soft_idx[r]) * d;
+    } else {
+        if (id < 0 || id >= SGC_VOCAB) {
+            if (threadIdx.x == 0) atomicExch(bad, 1);
+            return;
+        }
+        src = tok_emb + static_cast<size_t>(id) * d;
+    }
+    for (int i = threadIdx.x; i < d / 4; i += blockDim.x)
+        reinterpret_cast<float4*>(x + static_cast<size_t>(r) * d)[i] =
+            reinterpret_cast<const float4*>(src)[i];
+}
+
+// rmsnorm (lm_core.cpp:26-31): out = bf16(x / sqrt(mean(x^2) + 1e-5)), one CTA per row
+__global__ void rmsnorm_bf16_kernel(__nv_bfloat16* out, const float* x, int d, int rows) {
+    int r = blockIdx.x;
+    const float4* xr = reinterpret_cast<const float4*>(x + static_cast<size_t>(r) * d);
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+        float4 v = xr[i];
+        ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    }
+    __shared__ float red[32];
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffff, v, o);
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    const float inv = 1.0f / sqrtf(red[0] / static_cast<float>(d) + 1e-5f);
+    uint2* o2 = reinterpret_cast<uint2*>(out + static_cast<size_t>(r) * d);
+    for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+        float4 v = xr[i];
+        __nv_bfloat162 a = __floats2bfloat162_rn(v.x * inv, v.y * inv);
+        __nv_bfloat162 b = __floats2bfloat162_rn(v.z * inv, v.w * inv);
+        uint2 w;
+        w.x = *reinterpret_cast<uint32_t*>(&a);
+        w.y = *reinterpret_cast<uint32_t*>(&b);
+        o2[i] = w;
+    }
+}
+
+// final rmsnorm + fp32 head (lm_core.cpp:288-295) for selected rows. CTA = 16 rows x all
+// vocab; the head is stored transposed [d x 260] so a thread per vocab id reads coalesced.
+constexpr int kHeadRows = 16;
+constexpr int kHeadChunk = 512;
+__global__ void __launch_bounds__(288) head_kernel(float* logits, const float* x,
+                                                   const int32_t* rows, int n, const float* head_t,
+                                                   int d) {
+    __shared__ float xs[kHeadRows][kHeadChunk];
+    __shared__ float inv[kHeadRows];
+    const int r0 = blockIdx.x * kHeadRows;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    for (int rr = warp; rr < kHeadRows; rr += blockDim.x / 32) {
+        float ss = 0.f;
+        if (r0 + rr < n) {
+            const float* xr = x + static_cast<size_t>(rows[r0 + rr]) * d;
+            for (int i = lane; i < d; i += 32) ss += xr[i] * xr[i];
+        }
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+        if (lane == 0) inv[rr] = 1.0f / sqrtf(ss / static_cast<float>(d) + 1e-5f);
+    }
+    const int v = threadIdx.x;  // vocab id (260 of 288 threads active in the dot)
+    float acc[kHeadRows];
+#pragma unroll
+    for (int i = 0; i < kHeadRows; ++i) acc[i] = 0.f;
+    for (int k0 = 0; k0 < d; k0 += kHeadChunk) {
+        const int kc = min(kHeadChunk, d - k0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < kHeadRows * kc; i += blockDim.x) {
+            int rr = i / kc, k = i % kc;
+            xs[rr][k] = r0 + rr < n ? x[static_cast<size_t>(rows[r0 + rr]) * d + k0 + k] * inv[rr] : 0.f;
+        }
+        __syncthreads();
+        if (v < SGC_VOCAB) {
+            for (int k = 0; k < kc; ++k) {
+                float w = head_t[static_cast<size_t>(k0 + k) * SGC_VOCAB + v];
+#pragma unroll
+                for (int i = 0; i < kHeadRows; ++i) acc[i] = fmaf(xs[i][k], w, acc[i]);
+            }
+        }
+    }
+    if (v < SGC_VOCAB)
+        for (int i = 0; i < kHeadRows; ++i)
+            if (r0 + i < n) logits[static_cast<size_t>(r0 + i) * SGC_VOCAB + v] = acc[i];
+}
+
+// copy pointer (lm_core.cpp:360-374) + first greedy step (:379-385): one CTA per member.
+// context = the member's sealed prefix tokens; search_limit = prefix length.
+__global__ void first_token_kernel(int32_t* first, const float* logits, int n,
+                                   const int32_t* ctx_tokens, const uint64_t* ctx_off,
+                                   const uint32_t* member_ctx, const int32_t* ans,
+                                   const uint64_t* ans_off, float bonus) {
+    const int j = blockIdx.x;
+    if (j >= n) return;
+    __shared__ int found;
+    if (threadIdx.x == 0) found = 0;
+    __syncthreads();
+    int alen = 0;
+    const int32_t* a = nullptr;
+    if (ans_off) {
+        alen = static_cast<int>(ans_off[j + 1] - ans_off[j]);
+        a = ans + ans_off[j];
+    }
+    if (alen > 0) {
+        const uint32_t cidx = member_ctx[j];
+        const int32_t* c = ctx_tokens + ctx_off[cidx];
+        const int clen = static_cast<int>(ctx_off[cidx + 1] - ctx_off[cidx]);
+        for (int s = threadIdx.x; s + alen <= clen; s += blockDim.x) {
+            int i = 0;
+            while (i < alen && c[s + i] == a[i]) ++i;
+            if (i == alen) found = 1;
+        }
+    }
+    __syncthreads();
+    const int target = found ? a[0] : -1;
+    // argmax with ties toward the lowest id (lm_core.cpp:39-50)
+    float best = -INFINITY;
+    int bi = 0x7fffffff;
+    const float* lg = logits + static_cast<size_t>(j) * SGC_VOCAB;
+    for (int v = threadIdx.x; v < SGC_VOCAB; v += blockDim.x) {
+        float val = lg[v] + (v == target ? bonus : 0.0f);
+        if (val > best || (val == best && v < bi)) {
+            best = val;
+            bi = v;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        float ob = __shfl_xor_sync(0xffffffff, best, o);
+        int oi = __shfl_xor_sync(0xffffffff, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+            best = ob;
+            bi = oi;
+        }
+    }
+    __shared__ float sb[32];
+    __shared__ int si[32];
+    if (threadIdx.x % 32 == 0) {
+        sb[threadIdx.x / 32] = best;
+        si[threadIdx.x / 32] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < blockDim.x / 32; ++w)
+            if (sb[w] > best || (sb[w] == best && si[w] < bi)) {
+                best = sb[w];
+                bi = si[w];
+            }
+        first[j] = bi;
+    }
+}
+
+__global__ void transpose_head(float* out_t, const float* head, int d) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < SGC_VOCAB * d; i += gridDim.x * blockDim.x) {
+        int v = i / d, k = i % d;
+        out_t[static_cast<size_t>(k) * SGC_VOCAB + v] = head[i];
+    }
+}
+
+}  // namespace
+
+static unsigned grid_for(uint64_t n, int threads, int sms) {
+    uint64_t b = (n + threads - 1) / threads;
+    uint64_t cap = static_cast<uint64_t>(sms) * 32;
+    return static_cast<unsigned>(b < cap ? (b ? b : 1) : cap);
+}
+
+void gen_uniform(Ctx* c, float* out, uint64_t n, uint64_t state0, float lo, float hi) {
+    gen_uniform_f32<<<grid_for(n, 256, c->num_sms), 256, 0, c->stream>>>(out, n, state0, lo, hi);
+    SGC_LAUNCH_CHECK(c);
+}
+void gen_uniform(Ctx* c, __nv_bfloat16* out, uint64_t n, uint64_t state0, float lo, float hi) {
+    gen_uniform_bf16<<<grid_for(n, 256, c->num_sms), 256, 0, c->stream>>>(out, n, state0, lo, hi);
+    SGC_LAUNCH_CHECK(c);
+}
+void gen_text_projection_t(Ctx* c, float* out_t, uint32_t dim, uint64_t state0) {
+    gen_projection_t<<<grid_for((uint64_t)dim * 4096, 256, c->num_sms), 256, 0, c->stream>>>(out_t, dim, state0);
+    SGC_LAUNCH_CHECK(c);
+}
+void embed(Ctx* c, float* x, const int32_t* tokens, const float* tok_emb, const float* soft,
+           const int32_t* soft_idx, int d, int rows, int* bad) {
+    if (rows <= 0) return;
+    Ctx::Timed timer(c, "embed");
+    embed_kernel<<<rows, 128, 0, c->stream>>>(x, tokens, tok_emb, soft, soft_idx, d, rows, bad);
+    SGC_LAUNCH_CHECK(c);
+}
+void rmsnorm_bf16(Ctx* c, __nv_bfloat16* out, const float* x, int d, int rows) {
+    if (rows <= 0) return;
+    Ctx::Timed timer(c, "rmsnorm");
+    int threads = d >= 512 ? 128 : 32;
+    rmsnorm_bf16_kernel<<<rows, threads, 0, c->stream>>>(out, x, d, rows);
+    SGC_LAUNCH_CHECK(c);
+}
+void head_logits(Ctx* c, float* logits, const float* x, const int32_t* rows, int n,
+                 const float* head_t, int d) {
+    if (n <= 0) return;
+    Ctx::Timed timer(c, "head");
+    head_kernel<<<ceil_div(n, kHeadRows), 288, 0, c->stream>>>(logits, x, rows, n, head_t, d);
+    SGC_LAUNCH_CHECK(c);
+}
+void first_tokens(Ctx* c, int32_t* first, const float* logits, int n, const int32_t* ctx_tokens,
+                  const uint64_t* ctx_off, const uint32_t* member_ctx, const int32_t* ans,
+                  const uint64_t* ans_off, float bonus) {
+    if (n <= 0) return;
+    Ctx::Timed timer(c, "first_token");
+    first_token_kernel<<<n, 128, 0, c->stream>>>(first, logits, n, ctx_tokens, ctx_off, member_ctx,
+                                                 ans, ans_off, bonus);
+    SGC_LAUNCH_CHECK(c);
+}
+void head_transpose(Ctx* c, float* out_t, const float* head, int d) {
+    transpose_head<<<grid_for((uint64_t)SGC_VOCAB * d, 256, c->num_sms), 256, 0, c->stream>>>(out_t, head, d);
+    SGC_LAUNCH_CHECK(c);
+}
+
+}  // namespace sgc

@@ -1,0 +1,20 @@
+// lm_kernels.cuh -- host interface of lm_kernels.cu
+#pragma once
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace sgc {
+struct Ctx;
+void gen_uniform(Ctx* c, float* out, uint64_t n, uint64_t state0, float lo, float hi);
+void gen_uniform(Ctx* c, __nv_bfloat16* out, uint64_t n, uint64_t state0, float lo, float hi);
+void gen_text_projection_t(Ctx* c, float* out_t, uint32_t dim, uint64_t state0);
+void embed(Ctx* c, float* x, const int32_t* tokens, const float* tok_emb, const float* soft,
+           const int32_t* soft_idx, int d, int rows, int* bad);
+void rmsnorm_bf16(Ctx* c, __nv_bfloat16* out, const float* x, int d, int rows);
+void head_logits(Ctx* c, float* logits, const float* x, const int32_t* rows, int n,
+                 const float* head_t, int d);
+void first_tokens(Ctx* c, int32_t* first, const float* logits, int n, const int32_t* ctx_tokens,
+                  const uint64_t* ctx_off, const uint32_t* member_ctx, const int32_t* ans,
+                  const uint64_t* ans_off, float bonus);
+void head_transpose(Ctx* c, float* out_t, const float* head, int d);
+}  // namespace sgc

@@ -1,0 +1,511 @@
+"""Host-side mirror of the reference's hot-path API over the C ABI (include/sgc_b200.h).
+
+Names, argument meaning and error behaviour follow the reference (paths under
+/root/reference/proj), so the parity tests read like the reference's own tests:
+
+=========================  ==========================================================
+reference                  here
+=========================  ==========================================================
+ToyLm (lm_core.hpp:114)    ToyLm.prefill / prefill_batch / extend / extend_members
+KVCache (lm_core.hpp:35)   KVBatch (sealed prefix segments in HBM, bf16)
+GnnEncoder::encode         encode_subgraphs (batched, encoders.hpp:61)
+TextEncoder::embed         text_features (every node/edge text of a graph)
+pairwise_distances         pairwise_distances (clustering.hpp:35)
+agglomerate                agglomerate -> ClusterAssignment (clustering.hpp:44)
+merge_subgraphs +          build_representatives (graph_store.hpp:77,
+build_prompt + tokenize      cache_engine.hpp:45, tokenizer.hpp:22)
+run() SubgCache branch     run_subgcache (pipeline.cpp:212-293 + run_batch)
+=========================  ==========================================================
+
+Every call goes to hand-written sm_100a kernels; nothing here computes on the CPU beyond
+packing arguments.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+
+import numpy as np
+
+from . import _lib
+from ._lib import (CapacityError, CudaError, DomainError, Error, IntegrityError,  # noqa: F401
+                   LogicError, ParseError, VOCAB, check)
+from .workload import Subgraph, TextualGraph, Workload
+
+LINKAGES = {"ward": 0, "single": 1, "average": 2, "complete": 3, "centroid": 4}
+
+
+def _p(a, ct):
+    return None if a is None else a.ctypes.data_as(C.POINTER(ct))
+
+
+def splitmix64_once(x: int) -> int:
+    from .workload import splitmix64_once as s
+
+    return s(x)
+
+
+class Context:
+    """One CUDA device + stream (sgc_ctx)."""
+
+    def __init__(self, device: int = 0):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        check(self.lib.sgc_ctx_create(device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.sgc_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    @property
+    def launches(self) -> int:
+        return self.lib.sgc_ctx_launch_count(self.h)
+
+    def set_stream(self, stream_ptr: int | None):
+        check(self.lib.sgc_ctx_set_stream(self.h, C.c_void_p(stream_ptr or 0)))
+
+    def set_timing(self, enable: bool):
+        check(self.lib.sgc_set_timing(self.h, int(enable)))
+
+    def kernel_time(self, name: str):
+        ms, n = C.c_double(), C.c_uint64()
+        check(self.lib.sgc_get_timing(self.h, name.encode(), C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
+    def gemm(self, a_ptr: int, b_ptr: int, d_ptr: int, M: int, N: int, K: int, epi: int):
+        check(self.lib.sgc_gemm_bf16(self.h, C.c_void_p(a_ptr), C.c_void_p(b_ptr),
+                                     C.c_void_p(d_ptr), M, N, K, epi))
+
+
+# ------------------------------------------------------------------ packing helpers
+
+def pack_subgraphs(subs):
+    noff = np.zeros(len(subs) + 1, np.uint64)
+    eoff = np.zeros(len(subs) + 1, np.uint64)
+    for i, s in enumerate(subs):
+        noff[i + 1] = noff[i] + len(s.node_ids)
+        eoff[i + 1] = eoff[i] + len(s.edge_indices)
+    nodes = np.concatenate([np.asarray(s.node_ids, np.uint32) for s in subs] or [np.zeros(0, np.uint32)])
+    edges = np.concatenate([np.asarray(s.edge_indices, np.uint32) for s in subs] or [np.zeros(0, np.uint32)])
+    nodes = np.ascontiguousarray(nodes, np.uint32)
+    edges = np.ascontiguousarray(edges, np.uint32)
+    st = _lib.Subgraphs(len(subs), _p(noff, C.c_uint64), _p(nodes, C.c_uint32),
+                        _p(eoff, C.c_uint64), _p(edges, C.c_uint32))
+    return st, (noff, nodes, eoff, edges)
+
+
+def pack_tokens(lists):
+    off = np.zeros(len(lists) + 1, np.uint64)
+    for i, t in enumerate(lists):
+        off[i + 1] = off[i] + len(t)
+    toks = np.ascontiguousarray(
+        np.concatenate([np.asarray(t, np.int32) for t in lists] or [np.zeros(0, np.int32)]), np.int32)
+    if toks.size == 0:
+        toks = np.zeros(1, np.int32)
+    return _lib.TokenLists(len(lists), _p(off, C.c_uint64), _p(toks, C.c_int32)), (off, toks)
+
+
+# ---------------------------------------------------------------------------- LM
+
+@dataclasses.dataclass
+class ToyLmConfig:
+    """lm_core.hpp:16-27."""
+
+    layers: int = 4
+    heads: int = 4
+    model_dim: int = 64
+    ffn_hidden: int = 256
+    max_seq_len: int = 1024
+    max_new_tokens: int = 32
+    seed: int = 3
+
+    def c(self):
+        return _lib.LmConfig(self.layers, self.heads, self.model_dim, self.ffn_hidden,
+                             self.max_seq_len, self.max_new_tokens, self.seed)
+
+
+class KVBatch:
+    """Sealed prefix segments (KVCache::seal, lm_core.cpp:60-80) living in HBM as bf16."""
+
+    def __init__(self, lm: "ToyLm", h):
+        self.lm, self.h = lm, h
+        self.lib = lm.lib
+
+    def release(self):
+        if getattr(self, "h", None):
+            self.lib.sgc_kv_release(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.release()
+
+    @property
+    def count(self) -> int:
+        return self.lib.sgc_kv_count(self.h)
+
+    def token_count(self, i: int = 0) -> int:
+        return self.lib.sgc_kv_tokens(self.h, i)
+
+    def prefix_digest(self, i: int = 0) -> int:
+        return self.lib.sgc_kv_digest(self.h, i)
+
+    @property
+    def resident_kv_bytes(self) -> int:
+        return self.lib.sgc_kv_resident_bytes(self.h)
+
+    def read(self, i: int, layer: int, is_v: bool) -> np.ndarray:
+        out = np.zeros(self.token_count(i) * self.lm.cfg.model_dim, np.float32)
+        check(self.lib.sgc_kv_read(self.h, i, layer, int(is_v), _p(out, C.c_float)))
+        return out
+
+
+class ToyLm:
+    """ToyLm (lm_core.hpp:114-171) with device-generated, bit-exact seeded weights (bf16)."""
+
+    WEIGHTS = {"tok": 0, "head": 1, "wqkv": 2, "wo": 3, "w1": 4, "w2": 5}
+
+    def __init__(self, ctx: Context, cfg: ToyLmConfig | None = None):
+        self.ctx, self.lib = ctx, ctx.lib
+        self.cfg = cfg or ToyLmConfig()
+        h = C.c_void_p()
+        c = self.cfg.c()
+        check(self.lib.sgc_model_create(ctx.h, C.byref(c), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.sgc_model_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def weight(self, which: str, layer: int = 0, fp32: bool = True) -> np.ndarray:
+        d, f = self.cfg.model_dim, self.cfg.ffn_hidden
+        n = {"tok": VOCAB * d, "head": VOCAB * d, "wqkv": 3 * d * d, "wo": d * d, "w1": f * d,
+             "w2": f * d}[which]
+        out = np.zeros(n, np.float32)
+        check(self.lib.sgc_model_weight(self.h, self.WEIGHTS[which], layer, int(fp32),
+                                        _p(out, C.c_float), n))
+        return out
+
+    def prefill_batch(self, seqs, softs=None):
+        """ToyLm::prefill + KVCache::seal for many prompts in one batched pass.
+
+        softs: optional list (per sequence) of a model_dim vector or None."""
+        tl, keep = pack_tokens(seqs)
+        n = len(seqs)
+        soft = mask = None
+        if softs is not None and any(s is not None for s in softs):
+            d = self.cfg.model_dim
+            soft = np.zeros((n, d), np.float32)
+            mask = np.zeros(n, np.uint8)
+            for i, s in enumerate(softs):
+                if s is not None:
+                    s = np.asarray(s, np.float32)
+                    if s.shape != (d,):
+                        raise DomainError("soft prefix length must equal model_dim")
+                    soft[i] = s
+                    mask[i] = 1
+        logits = np.zeros((n, VOCAB), np.float32)
+        h = C.c_void_p()
+        check(self.lib.sgc_prefill(self.ctx.h, self.h, C.byref(tl), _p(soft, C.c_float),
+                                   _p(mask, C.c_uint8), C.byref(h), _p(logits, C.c_float)))
+        return KVBatch(self, h), logits
+
+    def prefill(self, tokens, soft=None):
+        kv, logits = self.prefill_batch([tokens], None if soft is None else [soft])
+        kv.last_logits = logits[0]
+        return kv
+
+    def extend_members(self, kv: KVBatch, member_seg, questions, answers=None, bonus=100.0):
+        """KVCache::fork + ToyLm::extend + first greedy token, for every member at once."""
+        seg = np.ascontiguousarray(member_seg, np.uint32)
+        ql, keepq = pack_tokens(questions)
+        al, keepa = pack_tokens(answers) if answers is not None else (None, None)
+        n = len(questions)
+        logits = np.zeros((n, VOCAB), np.float32)
+        first = np.zeros(n, np.int32)
+        check(self.lib.sgc_extend(self.ctx.h, self.h, kv.h, _p(seg, C.c_uint32), C.byref(ql),
+                                  C.byref(al) if al is not None else None, bonus,
+                                  _p(logits, C.c_float), _p(first, C.c_int32)))
+        return logits, first
+
+    def extend(self, kv: KVBatch, tokens, seg: int = 0):
+        """ToyLm::extend on a fork of sealed segment `seg`; returns the last logits."""
+        logits, _ = self.extend_members(kv, [seg], [tokens])
+        return logits[0]
+
+
+# ------------------------------------------------------------------------- graph
+
+class DeviceGraph:
+    """TextualGraph with pre-rendered rows and text hashes in HBM (sgc_graph)."""
+
+    def __init__(self, ctx: Context, g: TextualGraph):
+        self.ctx, self.lib, self.graph = ctx, ctx.lib, g
+        ids = np.array(sorted(g.nodes), np.uint32)
+        ntext = [g.nodes[int(i)] for i in ids]
+        noff = np.zeros(len(ids) + 1, np.uint64)
+        noff[1:] = np.cumsum([len(t) for t in ntext]) if len(ids) else []
+        esrc = np.array([e[0] for e in g.edges], np.uint32)
+        edst = np.array([e[2] for e in g.edges], np.uint32)
+        etext = [e[1] for e in g.edges]
+        eoff = np.zeros(len(g.edges) + 1, np.uint64)
+        eoff[1:] = np.cumsum([len(t) for t in etext]) if g.edges else []
+        h = C.c_void_p()
+        nb, eb = b"".join(ntext) + b"\0", b"".join(etext) + b"\0"
+        check(self.lib.sgc_graph_upload(ctx.h, len(ids), _p(ids, C.c_uint32), nb, _p(noff, C.c_uint64),
+                                        len(g.edges), _p(esrc, C.c_uint32), _p(edst, C.c_uint32), eb,
+                                        _p(eoff, C.c_uint64), C.byref(h)))
+        self.h = h
+        self.n_nodes, self.n_edges = len(ids), len(g.edges)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.sgc_graph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+
+@dataclasses.dataclass
+class GnnEncoderConfig:
+    """encoders.hpp:44-49 (+ TextEncoderConfig encoders.hpp:17-21)."""
+
+    layers: int = 4
+    heads: int = 4
+    dim: int = 64
+    seed: int = 2
+    text_seed: int = 1
+    text_salt: int = 55
+
+    def c(self):
+        return _lib.GnnConfig(self.layers, self.heads, self.dim, self.seed, self.text_seed,
+                              self.text_salt)
+
+
+def text_features(ctx: Context, g: DeviceGraph, dim: int, seed: int = 1, salt: int = 55):
+    out = np.zeros((g.n_nodes + g.n_edges, dim), np.float32)
+    check(ctx.lib.sgc_text_features(ctx.h, g.h, dim, seed, salt, _p(out, C.c_float)))
+    return out
+
+
+def encode_subgraphs(ctx: Context, g: DeviceGraph, subgraphs, cfg: GnnEncoderConfig):
+    st, keep = pack_subgraphs(subgraphs)
+    out = np.zeros((len(subgraphs), cfg.dim), np.float32)
+    c = cfg.c()
+    check(ctx.lib.sgc_encode_subgraphs(ctx.h, g.h, C.byref(c), C.byref(st), _p(out, C.c_float)))
+    return out
+
+
+# --------------------------------------------------------------------- clustering
+
+@dataclasses.dataclass
+class ClusterAssignment:
+    """clustering.hpp:21-32 (merges as (left min member, right min member, distance))."""
+
+    labels: np.ndarray
+    merge_left: np.ndarray
+    merge_right: np.ndarray
+    merge_dist: np.ndarray
+    op_count: int
+
+
+def pairwise_distances(ctx: Context, emb: np.ndarray) -> np.ndarray:
+    emb = np.ascontiguousarray(emb, np.float32)
+    m, d = emb.shape
+    out = np.zeros((m, m), np.float64)
+    check(ctx.lib.sgc_pairwise_distances(ctx.h, _p(emb, C.c_float), m, d, _p(out, C.c_double)))
+    return out
+
+
+def agglomerate(ctx: Context, emb: np.ndarray, linkage: str = "ward", c: int = 1) -> ClusterAssignment:
+    emb = np.ascontiguousarray(emb, np.float32)
+    if emb.ndim != 2:
+        raise DomainError("embeddings must be [m, dim]")
+    m, d = emb.shape
+    if linkage not in LINKAGES:
+        raise DomainError("unknown linkage: " + linkage)
+    labels = np.zeros(m, np.uint32)
+    k = max(m - c, 0)
+    left = np.zeros(max(k, 1), np.uint32)
+    right = np.zeros(max(k, 1), np.uint32)
+    dist = np.zeros(max(k, 1), np.float64)
+    ops = C.c_uint64()
+    check(ctx.lib.sgc_agglomerate(ctx.h, _p(emb, C.c_float), m, d, LINKAGES[linkage], c,
+                                  _p(labels, C.c_uint32), _p(left, C.c_uint32),
+                                  _p(right, C.c_uint32), _p(dist, C.c_double), C.byref(ops)))
+    return ClusterAssignment(labels, left[:k], right[:k], dist[:k], ops.value)
+
+
+@dataclasses.dataclass
+class Representatives:
+    subgraphs: list          # merged Subgraph per cluster
+    prefix_tokens: list      # np.int32 arrays (BOS + prefix bytes)
+    dropped_nodes: np.ndarray
+    dropped_edges: np.ndarray
+
+
+def prefix_budget(max_seq_len: int, question_budget: int = 128, max_new_tokens: int = 32,
+                  soft: bool = False) -> int:
+    """PromptBudget::prefix_budget (cache_engine.hpp:27-30)."""
+    reserved = question_budget + max_new_tokens + (1 if soft else 0)
+    return 0 if reserved >= max_seq_len else max_seq_len - reserved
+
+
+def build_representatives(ctx: Context, g: DeviceGraph, subgraphs, labels, c: int,
+                          budget_tokens: int) -> Representatives:
+    st, keep = pack_subgraphs(subgraphs)
+    labels = np.ascontiguousarray(labels, np.uint32)
+    nn = sum(len(s.node_ids) for s in subgraphs) + 1
+    ne = sum(len(s.edge_indices) for s in subgraphs) + 1
+    rno, reo, po = (np.zeros(c + 1, np.uint64) for _ in range(3))
+    rn, re = np.zeros(nn, np.uint32), np.zeros(ne, np.uint32)
+    cap = c * (budget_tokens + 1) + 8  # each prefix is at most budget_tokens long
+    pref = np.zeros(cap, np.int32)
+    dropped = np.zeros(2 * c, np.uint32)
+    check(ctx.lib.sgc_build_representatives(
+        ctx.h, g.h, C.byref(st), _p(labels, C.c_uint32), c, budget_tokens, _p(rno, C.c_uint64),
+        _p(rn, C.c_uint32), nn, _p(reo, C.c_uint64), _p(re, C.c_uint32), ne, _p(po, C.c_uint64),
+        _p(pref, C.c_int32), cap, _p(dropped, C.c_uint32)))
+    subs = [Subgraph(rn[rno[i]:rno[i + 1]].copy(), re[reo[i]:reo[i + 1]].copy()) for i in range(c)]
+    toks = [pref[po[i]:po[i + 1]].copy() for i in range(c)]
+    return Representatives(subs, toks, dropped[0::2].copy(), dropped[1::2].copy())
+
+
+# ----------------------------------------------------------------- question side
+
+def question_tokens(question: bytes, question_budget: int = 128) -> np.ndarray:
+    """build_prompt question side (cache_engine.cpp:33-41) + Tokenizer::encode_bytes.
+
+    Host string work done when the query is prepared (pipeline.cpp:175-183), before the
+    hot path starts."""
+    pre, post = b"\nQuestion: ", b"\nAnswer:"
+    if question_budget <= len(pre) + len(post):
+        raise DomainError("question budget smaller than the question template")
+    q = question[: question_budget - len(pre) - len(post)]
+    return np.frombuffer(pre + q + post, np.uint8).astype(np.int32)
+
+
+def own_prefix_tokens(graph: TextualGraph, sub: Subgraph, budget_tokens: int) -> np.ndarray:
+    """BOS + own prompt prefix of a query (fallback path input; pipeline.cpp:177-178).
+
+    Only used when a member cannot fit on its cluster's prefix (cache_engine.cpp:171)."""
+    from .workload import render_edge_row, render_node_row
+
+    nodes = [render_node_row(int(i), graph.nodes[int(i)]) for i in sub.node_ids]
+    edges = [render_edge_row(*graph.edges[int(e)]) for e in sub.edge_indices]
+    head = b"Use the following graph to answer the question.\n\n"
+    base = len(head) + 17 + 17 + 2
+    budget_bytes = 0 if budget_tokens == 0 else budget_tokens - 1
+    nb = sum(len(r) + 1 for r in nodes)
+    eb = [len(r) + 1 for r in edges]
+    ke = len(edges)
+    while ke > 0 and base + nb + sum(eb[:ke]) > budget_bytes:
+        ke -= 1
+    kn = len(nodes)
+    while kn > 0 and base + sum(len(r) + 1 for r in nodes[:kn]) + sum(eb[:ke]) > budget_bytes:
+        kn -= 1
+    text = head + b"node id,node attr\n" + b"".join(r + b"\n" for r in nodes[:kn]) + \
+        b"src,edge attr,dst\n" + b"".join(r + b"\n" for r in edges[:ke])
+    return np.concatenate([[256], np.frombuffer(text, np.uint8)]).astype(np.int32)
+
+
+# ----------------------------------------------------------------- whole branch
+
+@dataclasses.dataclass
+class SubgCacheResult:
+    embeddings: np.ndarray
+    labels: np.ndarray
+    merge_left: np.ndarray
+    merge_right: np.ndarray
+    merge_dist: np.ndarray
+    prefix_len: np.ndarray
+    logits: np.ndarray
+    first_token: np.ndarray
+    fallback: np.ndarray
+    stage_ms: list
+    prefill_rows: int
+    extend_rows: int
+
+
+class PreparedBatch:
+    """Host inputs of one batch, packed once (question/answer tokens are prepared before the
+    hot path, pipeline.cpp:175-183)."""
+
+    def __init__(self, w: Workload, gnn_seed: int | None = None, with_own_prefix: bool = True):
+        self.w = w
+        lm = w.lm
+        self.budget = prefix_budget(lm["max_seq_len"], w.question_budget, lm["max_new_tokens"],
+                                    w.soft_prefix)
+        self.q = [question_tokens(q.question, w.question_budget) for q in w.queries]
+        self.a = [np.frombuffer(q.answer, np.uint8).astype(np.int32) for q in w.queries] \
+            if w.answer_lookup else []
+        self.own = [own_prefix_tokens(w.graph, s, self.budget) for s in w.retrieved] \
+            if with_own_prefix else []
+        self.gnn = GnnEncoderConfig(4, 4, lm["model_dim"],
+                                    splitmix64_once(w.seed ^ 0x62) if gnn_seed is None else gnn_seed)
+        self.subs, self._ks = pack_subgraphs(w.retrieved)
+        self.ql, self._kq = pack_tokens(self.q)
+        self.al, self._ka = pack_tokens(self.a) if self.a else (_lib.TokenLists(0, None, None), None)
+        self.ol, self._ko = pack_tokens(self.own) if self.own else (_lib.TokenLists(0, None, None), None)
+
+
+def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
+                  embeddings: np.ndarray | None = None, cluster_owner=None, rank: int = 0,
+                  want_logits: bool = True) -> SubgCacheResult:
+    """pipeline.cpp:212-293 (SubgCache branch) + cache_engine.cpp:217-233 (run_batch), to the
+    first token of every query."""
+    w = pb.w
+    m = len(w.queries)
+    d = model.cfg.model_dim
+    k = w.clusters
+    b = _lib.Batch()
+    b.retrieved = pb.subs
+    b.questions = pb.ql
+    b.answers = pb.al
+    b.own_prefix = pb.ol
+    b.clusters = k
+    b.linkage = LINKAGES[w.linkage]
+    b.question_budget = w.question_budget
+    b.soft_prefix = int(w.soft_prefix)
+    b.pointer_bonus = 100.0
+    b.gnn = pb.gnn.c()
+    emb_in = None
+    if embeddings is not None:
+        emb_in = np.ascontiguousarray(embeddings, np.float32)
+        b.precomputed_embeddings = _p(emb_in, C.c_float)
+    own = None
+    if cluster_owner is not None:
+        own = np.ascontiguousarray(cluster_owner, np.uint32)
+        b.cluster_owner = _p(own, C.c_uint32)
+    b.rank = rank
+    emb = np.zeros((m, d), np.float32)
+    labels = np.zeros(m, np.uint32)
+    nm = max(m - k, 1)
+    left, right = np.zeros(nm, np.uint32), np.zeros(nm, np.uint32)
+    dist = np.zeros(nm, np.float64)
+    plen = np.zeros(k, np.uint64)
+    logits = np.zeros((m, VOCAB), np.float32) if want_logits else None
+    first = np.full(m, -1, np.int32)
+    fb = np.zeros(m, np.uint8)
+    o = _lib.BatchOut()
+    o.embeddings = _p(emb, C.c_float)
+    o.labels = _p(labels, C.c_uint32)
+    o.merge_left = _p(left, C.c_uint32)
+    o.merge_right = _p(right, C.c_uint32)
+    o.merge_dist = _p(dist, C.c_double)
+    o.prefix_len = _p(plen, C.c_uint64)
+    o.logits = _p(logits, C.c_float)
+    o.first_token = _p(first, C.c_int32)
+    o.fallback = _p(fb, C.c_uint8)
+    check(ctx.lib.sgc_run_subgcache(ctx.h, model.h, g.h, C.byref(b), C.byref(o)))
+    return SubgCacheResult(emb, labels, left[: m - k], right[: m - k], dist[: m - k], plen, logits,
+                           first, fb, list(o.stage_ms)[:6], o.prefill_rows, o.extend_rows)

@@ -1,0 +1,214 @@
+"""Generate the committed golden fixtures from the UNMODIFIED reference.
+
+Runs oracle/_ref/ref_driver (the reference library compiled from /root/reference/proj/src,
+see oracle/Makefile) on seeded inputs and stores inputs + outputs as small JSON files in
+tests/golden/. Run here (where /root/reference exists); the fixtures travel to the GPU box.
+
+    python tests/golden/make_golden.py
+"""
+import json
+import os
+import sys
+import tempfile
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+from paper_2505_10951_b200 import workload as W  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+REF_DATA = "/root/reference/proj/data/scene_graph"
+
+
+def dump(name, obj):
+    with open(os.path.join(OUT, name), "w") as f:
+        json.dump(obj, f, separators=(",", ":"))
+    print("wrote", name, os.path.getsize(os.path.join(OUT, name)), "bytes")
+
+
+def graph_json(g: W.TextualGraph):
+    return {"nodes": [[int(k), g.nodes[k].decode("latin1")] for k in sorted(g.nodes)],
+            "edges": [[int(s), a.decode("latin1"), int(d)] for s, a, d in g.edges]}
+
+
+def c1_pipeline(td):
+    """BASELINE configs[0] end to end: reference synth dataset (synth.hpp), ego-topk retrieval,
+    seed 7, c=4, ward, default tiny ToyLm (acceptance.cpp:40-48 settings)."""
+    d = os.path.join(td, "c1")
+    ref = oracle.run_ref({"cmd": "synth", "dir": d, "m": 64})
+    g, qs = W.two_star_dataset(64)
+    mine = os.path.join(td, "mine")
+    w = W.c1_workload(64, 4)
+    w.write_dataset(mine)
+    # the restated dataset must parse to exactly the reference writer's graph and queries
+    import csv
+
+    with open(ref["nodes"], newline="") as f:
+        rn = {int(r[0]): r[1].encode() for r in list(csv.reader(f))[1:] if r}
+    with open(ref["edges"], newline="") as f:
+        re_ = [(int(r[0]), r[1].encode(), int(r[2])) for r in list(csv.reader(f))[1:] if r]
+    assert rn == g.nodes and re_ == g.edges
+    with open(ref["queries"]) as f:
+        rq = [json.loads(x) for x in f if x.strip()]
+    assert [(q["id"], q["question"].encode(), q["answer"].encode()) for q in rq] == \
+        [(q.id, q.question, q.answer) for q in qs]
+    out = oracle.run_ref({"cmd": "pipeline", "nodes_csv": ref["nodes"], "edges_csv": ref["edges"],
+                          "queries_jsonl": ref["queries"], "clusters": 4, "linkage": "ward",
+                          "seed": 7, "retrieval": "ego-topk", "run_batch": True})
+    out["graph"] = graph_json(g)
+    out["queries"] = [[q.id, q.question.decode(), q.answer.decode()] for q in qs]
+    out["config"] = {"clusters": 4, "linkage": "ward", "seed": 7, "lm": W.TINY_LM}
+    dump("c1_pipeline.json", out)
+
+
+def c1_variants(td):
+    """Same dataset with c in {2, 64} (c=m degenerates to the baseline, acceptance.cpp:108-124)
+    and soft-prefix on (node-edge-topk semantics)."""
+    d = os.path.join(td, "c1v")
+    ref = oracle.run_ref({"cmd": "synth", "dir": d, "m": 24})
+    res = {}
+    for name, extra in (("c2", {"clusters": 2}), ("cm", {"clusters": 24}),
+                        ("soft", {"clusters": 3, "soft": True}),
+                        ("single", {"clusters": 5, "linkage": "single"})):
+        spec = {"cmd": "pipeline", "nodes_csv": ref["nodes"], "edges_csv": ref["edges"],
+                "queries_jsonl": ref["queries"], "linkage": "ward", "seed": 7,
+                "retrieval": "ego-topk"}
+        spec.update(extra)
+        o = oracle.run_ref(spec)
+        o["spec"] = {k: v for k, v in extra.items()}
+        res[name] = o
+    g, qs = W.two_star_dataset(24)
+    res["graph"] = graph_json(g)
+    res["queries"] = [[q.id, q.question.decode(), q.answer.decode()] for q in qs]
+    dump("c1_variants.json", res)
+
+
+def lm_cases():
+    """prefill(A) -> seal -> fork -> extend(B) logits + greedy decode (acceptance.cpp:76-104,
+    test_lm_core.cpp:58-75,113-128,189-239) at the default tiny shape."""
+    rng = np.random.default_rng(1001)
+    cases = []
+    for i in range(12):
+        total = int(rng.integers(2, 300))
+        cut = int(rng.integers(1, total))
+        toks = rng.integers(0, 256, total).tolist()
+        c = {"prefix": toks[:cut], "suffix": toks[cut:], "decode": 8}
+        if i % 3 == 0:
+            c["collect"] = True
+        if i % 4 == 1:
+            c["soft"] = (rng.uniform(-0.1, 0.1, 64).astype(np.float32)).tolist()
+        cases.append(c)
+    # copy pointer: answer present in the prefix
+    prompt = list(b"facts: the cords are blue. question: color?")
+    cases.append({"prefix": [256] + prompt, "suffix": list(b" answer:"), "decode": 6,
+                  "answer": list(b"blue")})
+    # capacity error
+    cases.append({"prefix": rng.integers(0, 256, 1100).tolist()})
+    cfg = {"max_seq_len": 1024}
+    out = oracle.run_ref({"cmd": "lm", "cfg": cfg, "cases": cases})
+    dump("lm_tiny.json", {"cfg": cfg, "cases": cases, "out": out})
+    # a wider shape (hd = 64 / 128 kernels): reduced depth keeps the CPU oracle fast
+    for name, cfg in (("lm_hd64.json", {"layers": 2, "heads": 4, "model_dim": 256, "ffn_hidden": 512,
+                                        "max_seq_len": 512, "seed": 11}),
+                      ("lm_hd128.json", {"layers": 2, "heads": 4, "model_dim": 512, "ffn_hidden": 1024,
+                                         "max_seq_len": 512, "seed": 12})):
+        cs = []
+        for i in range(4):
+            total = int(rng.integers(40, 400))
+            cut = int(rng.integers(1, total))
+            toks = rng.integers(0, 256, total).tolist()
+            cs.append({"prefix": toks[:cut], "suffix": toks[cut:]})
+        out = oracle.run_ref({"cmd": "lm", "cfg": cfg, "cases": cs})
+        dump(name, {"cfg": cfg, "cases": cs, "out": out})
+
+
+def cluster_cases():
+    """agglomerate vs the naive oracle (acceptance.cpp:158-178 style) incl. exact ties."""
+    rng = np.random.default_rng(4004)
+    cases = []
+    for it in range(30):
+        m = int(rng.integers(2, 65))
+        pts = rng.uniform(-1, 1, (m, 6)).astype(np.float32)
+        if it % 5 == 0:  # duplicate points -> exact-tie merges
+            pts[m // 2:] = pts[: m - m // 2]
+        c = int(rng.integers(1, m + 1))
+        for lk in oracle.LINKAGES:
+            cases.append({"embeddings": pts.tolist(), "linkage": lk, "c": c, "naive": True,
+                          "pairwise": it < 3})
+    cases.append({"embeddings": [[1.0, 2.0]] * 4, "linkage": "ward", "c": 2})
+    cases.append({"embeddings": [[0.0, 0.0], [0.0, 0.1], [10.0, 10.0], [10.0, 10.1]],
+                  "linkage": "centroid", "c": 2})
+    cases.append({"embeddings": [[0.0], [1.0]], "linkage": "ward", "c": 3})  # c > m
+    out = oracle.run_ref({"cmd": "cluster", "cases": cases})
+    dump("cluster.json", {"cases": cases, "out": out})
+
+
+def scene_graph_cases(td):
+    """build_prompt truncation + merge on the bundled scene graph (test_cache_engine.cpp:46-104)."""
+    nodes = os.path.join(REF_DATA, "nodes.csv")
+    edges = os.path.join(REF_DATA, "edges.csv")
+    # parse the CSV with the reference, then read back the canonical content
+    out = oracle.run_ref({"cmd": "prompt", "nodes_csv": nodes, "edges_csv": edges,
+                          "budget": {"max_seq_len": 320, "question_budget": 64, "max_new_tokens": 16},
+                          "subgraphs": [{"nodes": list(range(22)), "edges": list(range(8))}],
+                          "clusters": [[0]], "questions": []})
+    import csv
+
+    with open(nodes, newline="") as f:
+        rows = list(csv.reader(f))[1:]
+    with open(edges, newline="") as f:
+        erows = list(csv.reader(f))[1:]
+    g = {"nodes": [[int(r[0]), r[1]] for r in rows if r],
+         "edges": [[int(r[0]), r[1], int(r[2])] for r in erows if r]}
+    gg = W.TextualGraph({n: a.encode() for n, a in g["nodes"]},
+                        [(s, a.encode(), d) for s, a, d in g["edges"]])
+    gg.write_csv(os.path.join(td, "sg_nodes.csv"), os.path.join(td, "sg_edges.csv"))
+    rng = np.random.default_rng(6006)
+    subs = []
+    for _ in range(40):
+        es = [e for e in range(len(g["edges"])) if rng.integers(0, 3) == 0]
+        ns = set()
+        for e in es:
+            ns.add(g["edges"][e][0])
+            ns.add(g["edges"][e][2])
+        for n, _a in g["nodes"]:
+            if rng.integers(0, 4) == 0:
+                ns.add(n)
+        if not ns:
+            ns.add(0)
+        subs.append({"nodes": sorted(ns), "edges": es})
+    clusters = [[int(i) for i in rng.choice(40, size=int(rng.integers(1, 7)), replace=True)]
+                for _ in range(30)]
+    res = {"graph": g, "subgraphs": subs, "clusters": clusters, "budgets": []}
+    for budget in ({"max_seq_len": 1024, "question_budget": 128, "max_new_tokens": 32},
+                   {"max_seq_len": 320, "question_budget": 64, "max_new_tokens": 16},
+                   {"max_seq_len": 200, "question_budget": 64, "max_new_tokens": 16},
+                   {"max_seq_len": 150, "question_budget": 30, "max_new_tokens": 16}):
+        o = oracle.run_ref({"cmd": "prompt", "nodes_csv": os.path.join(td, "sg_nodes.csv"),
+                            "edges_csv": os.path.join(td, "sg_edges.csv"), "budget": budget,
+                            "subgraphs": subs, "clusters": clusters,
+                            "questions": ["What is the color of the cords?", "x" * 500, ""]})
+        res["budgets"].append({"budget": budget, "out": o})
+    res["full_truncation"] = out
+    # GNN embeddings + text features of the same graph (encoders.cpp:57-186)
+    texts = [a for _, a in g["nodes"]] + [a for _, a, _ in g["edges"]] + ["", "!!!", "Ünïcode wörds"]
+    for dim, seed in ((64, 2), (128, 77)):
+        o = oracle.run_ref({"cmd": "gnn", "nodes_csv": os.path.join(td, "sg_nodes.csv"),
+                            "edges_csv": os.path.join(td, "sg_edges.csv"), "dim": dim,
+                            "gnn_seed": seed, "subgraphs": subs[:20], "texts": texts})
+        res[f"gnn_{dim}"] = {"seed": seed, "texts": texts, "out": o}
+    dump("scene_graph.json", res)
+
+
+if __name__ == "__main__":
+    if not oracle.ref_available():
+        oracle.build(ref=True)
+    with tempfile.TemporaryDirectory() as td:
+        c1_pipeline(td)
+        c1_variants(td)
+        lm_cases()
+        cluster_cases()
+        scene_graph_cases(td)
