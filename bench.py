@@ -1,0 +1,422 @@
+#!/usr/bin/env python
+"""bench.py -- SubGCache in-batch serving hot path on B200 (driver contract).
+
+One step = one whole batch through the hot path (pipeline.cpp:212-293 + run_batch):
+GNN subgraph embedding -> agglomerative clustering -> representative union/prompt ->
+batched representative prefill (KV precompute) -> batched cascade extend of every member
+-> first token of every query. Default workload: BASELINE configs[2] (Llama-3-8B-shaped
+ToyLm, 1024 synthetic graph-RAG queries, 16 clusters, ~2k-token representative prompts),
+which fits one B200; --config c1/c2/c4/c5 select the other configs.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+N > 1 runs under torchrun: each rank encodes its shard of subgraphs, embeddings are
+all-gathered over NCCL, every rank clusters redundantly (bit-identical labels), whole
+clusters are assigned to ranks by LPT, and first tokens are all-reduced to rank 0.
+Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "per-query TTFT (p50) and queries/s vs CPU ref; fraction of tensor/HBM roofline"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            j = json.load(f)
+        return j, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+# ----------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            self.p.wait()
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for n, v in zip(names, r[5:9]):
+                    if "Active" in v and "Not" not in v:
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        load = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": float(np.median(load)) if load else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+
+def build_workload(args):
+    from paper_2505_10951_b200 import workload as W
+
+    kw = {}
+    if args.m:
+        kw["m"] = args.m
+    if args.clusters:
+        kw["clusters"] = args.clusters
+    if args.config == "c2" and "clusters" in kw:
+        kw.pop("clusters")
+    w = W.WORKLOADS[args.config](**kw)
+    if args.layers:
+        raise SystemExit("--layers changes the model: not a valid bench configuration")
+    return w
+
+
+def lm_flops(w, prefix_lens, members_q, labels):
+    """Algorithmic FLOPs of one batch: F_tok = 2 L (4 d^2 + 2 d ffn);
+    prefill P F_tok + 2 d L P (P+1); member S F_tok + 4 d L (S P + S (S+1)/2); + heads."""
+    L, d, f = w.lm["layers"], w.lm["model_dim"], w.lm["ffn_hidden"]
+    ftok = 2.0 * L * (4 * d * d + 2 * d * f)
+    gemm = attn = 0.0
+    for P in prefix_lens:
+        gemm += P * ftok
+        attn += 2.0 * d * L * P * (P + 1)
+    for S, c in zip(members_q, labels):
+        P = prefix_lens[c]
+        gemm += S * ftok
+        attn += 4.0 * d * L * (S * P + S * (S + 1) / 2)
+    head = 2.0 * 260 * d * (len(prefix_lens) + len(members_q))
+    return gemm, attn, head
+
+
+# ---------------------------------------------------------------- our arm
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2505_10951_b200 import host
+
+    torch.cuda.set_device(local_rank)
+    w = build_workload(args)
+    m = len(w.queries)
+    ctx = host.Context(local_rank)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+    t0 = time.time()
+    lm = host.ToyLm(ctx, host.ToyLmConfig(**w.lm, seed=w.seed))
+    dg = host.DeviceGraph(ctx, w.graph)
+    pb = host.PreparedBatch(w, with_own_prefix=True)
+    setup_s = time.time() - t0
+    d = w.lm["model_dim"]
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        pg = dist
+    # this rank's encode shard (contiguous query ranges)
+    lo, hi = (rank * m) // world, ((rank + 1) * m) // world
+
+    def step():
+        emb = None
+        if world > 1:
+            shard = host.encode_subgraphs(ctx, dg, w.retrieved[lo:hi], pb.gnn)
+            counts = [((r + 1) * m) // world - (r * m) // world for r in range(world)]
+            mx = max(counts)
+            buf = torch.zeros(mx, d, device="cuda")
+            buf[: hi - lo] = torch.from_numpy(shard).cuda()
+            gathered = [torch.zeros(mx, d, device="cuda") for _ in range(world)]
+            pg.all_gather(gathered, buf)
+            emb = torch.cat([g[:c] for g, c in zip(gathered, counts)]).cpu().numpy()
+        res = host.run_subgcache(ctx, lm, dg, pb, embeddings=emb, rank=rank, world_size=world,
+                                 want_logits=False, device_inputs=True)
+        if world > 1:
+            ft = torch.from_numpy(res.first_token.astype(np.int64)).cuda()
+            pg.all_reduce(ft, op=pg.ReduceOp.MAX)
+            res.first_token = ft.cpu().numpy().astype(np.int32)
+        return res
+
+    for _ in range(args.warmup):
+        res = step()
+    if world > 1:
+        pg.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launches
+    ctx.set_timing(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stage = np.zeros(6)
+    with ClockSampler(local_rank) as clk:
+        if world > 1:
+            pg.barrier()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = step()
+            stage += np.array(res.stage_ms)
+        ev1.record(stream)
+        if world > 1:
+            pg.barrier()
+        torch.cuda.synchronize()
+    total_ms = ev0.elapsed_time(ev1)
+    launches = ctx.launches - launches0
+    gemm_ms, gemm_n = ctx.kernel_time("gemm")
+    attn_ms, attn_n = ctx.kernel_time("attention")
+    gnn_ms, _ = ctx.kernel_time("gnn_encode")
+    agg_ms, _ = ctx.kernel_time("agglomerate")
+    ctx.set_timing(False)
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = m / (ms_per_step / 1000.0)
+
+    # ---- e2e: same batch through the C ABI with host buffers, rank-local inputs copied in and
+    # first tokens copied out every step (run_subgcache takes host numpy arrays)
+    e2e = None
+    if not args.no_e2e and world == 1:
+        ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev2.record(stream)
+        for _ in range(args.steps):
+            r2 = host.run_subgcache(ctx, lm, dg, pb, want_logits=True)
+        ev3.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = ev2.elapsed_time(ev3) / args.steps
+        h2d = int(sum(a.nbytes for a in pb._ks) + sum(a.nbytes for a in pb._kq) +
+                  (sum(a.nbytes for a in pb._ka) if pb._ka else 0) +
+                  (sum(a.nbytes for a in pb._ko) if pb._ko else 0))
+        d2h = int(r2.first_token.nbytes + r2.logits.nbytes + r2.labels.nbytes + r2.embeddings.nbytes)
+        e2e = {"value": m / (e2e_ms / 1000.0), "unit": "queries/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    if rank != 0:
+        return None
+    # ---- roofline of the dominant kernel (the tcgen05 GEMM, tensor-bound)
+    labels = res.labels
+    prefix_lens = [int(x) for x in res.prefix_len]
+    members_q = [len(q) for q in pb.q]
+    gemm_f, attn_f, head_f = lm_flops(w, prefix_lens, members_q, labels)
+    peaks, pk_kind = load_peaks()
+    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    gemm_tf = (gemm_f * args.steps) / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0.0
+    prof = None
+    prof_path = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
+    if os.path.exists(prof_path):
+        with open(prof_path) as f:
+            prof = json.load(f).get(args.config)
+    roofline = {"bound": "tensor", "kernel": "gemm_kernel (tcgen05)", "achieved": round(gemm_tf, 2),
+                "peak": peak, "unit": "TFLOP/s", "frac": round(gemm_tf / peak, 4),
+                "peak_kind": f"{pk_kind} bf16 sustained",
+                "traffic": prof,
+                "flops_per_launch": gemm_f / max(1, gemm_n / args.steps),
+                "avg_launch_ms": gemm_ms / max(1, gemm_n)}
+    step_tf = (gemm_f + attn_f + head_f) / (ms_per_step / 1e3) / 1e12
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": "queries/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded community graph, injected retrieval, random-init seeded ToyLm weights)",
+        "config": {"workload": w.name, "model": "ToyLm Llama-3-8B-shaped" if w.lm["model_dim"] == 4096
+                   else f"ToyLm d{w.lm['model_dim']} L{w.lm['layers']}",
+                   "queries": m, "clusters": w.clusters, "layers": w.lm["layers"],
+                   "model_dim": w.lm["model_dim"], "ffn_hidden": w.lm["ffn_hidden"],
+                   "prefix_tokens_mean": float(np.mean(prefix_lens)),
+                   "question_tokens_mean": float(np.mean(members_q)),
+                   "parallelism": f"clusters sharded over {world} GPU(s)" if world > 1 else "1 GPU",
+                   "l2": "inputs larger than L2 (11 GiB bf16 weights + prefix KV streamed every step)"},
+        "ttft_p50_ms": round(ms_per_step, 3),
+        "ttft_semantics": "submission -> first token of every query (whole batch served in one pass)",
+        "stage_ms": {k: round(v / args.steps, 3) for k, v in
+                     zip(["encode", "cluster", "represent", "prefill", "extend", "total"], stage)},
+        "kernel_ms_per_step": {"gemm": gemm_ms / args.steps, "attention": attn_ms / args.steps,
+                               "gnn_encode": gnn_ms / args.steps, "agglomerate": agg_ms / args.steps},
+        "step_tflops": round(step_tf, 2), "step_tensor_frac": round(step_tf / peak, 4),
+        "roofline": roofline,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "setup_s": round(setup_s, 2),
+    }
+    out["clocks"] = clk.summary()
+    if not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(w, res, pb, threads=1)
+    return out
+
+
+# ------------------------------------------------------------- CPU reference
+
+def cpu_baseline(w, res, pb, threads: int = 1, samples: int = 1):
+    """The reference's CPU path (oracle/_ref, compiled from the reference sources) timed on
+    this host on a BOUNDED sample, extrapolated to the whole batch:
+      T = sum_i T_gnn(|V_i|) + T_agglomerate(m) + sum_c P_c t_tok(P_c/2) + sum_q S_q t_tok(P_c)
+    t_tok is measured at full width with 1 layer and scaled by the layer count (per-token
+    cost is linear in layers); attention at context ctx adds 4 d ctx per layer-token."""
+    import oracle
+
+    L, d, f = w.lm["layers"], w.lm["model_dim"], w.lm["ffn_hidden"]
+    spec = {"cmd": "bench", "lm": {"layers": 1, "heads": w.lm["heads"], "model_dim": d,
+                                   "ffn_hidden": f, "max_seq_len": w.lm["max_seq_len"]},
+            "prefill_tokens": 4, "extend_tokens": 2, "threads": threads,
+            "gnn_nodes": 4, "agglomerate_m": len(w.queries), "agglomerate_d": d,
+            "agglomerate_c": w.clusters}
+    kind = "reference"
+    t0 = time.time()
+    if oracle.ref_available():
+        r = oracle.run_ref(spec, timeout=900)
+    else:
+        raise RuntimeError("oracle/_ref/ref_driver missing (build() compiles it from the reference)")
+    sample_s = time.time() - t0
+    matvec = 2.0 * (4 * d * d + 2 * d * f)
+    tok_key = "parallel_extend_ms_per_token" if threads > 1 else "extend_ms_per_token"
+    t_ext = r[tok_key] * L
+    t_pre = r["prefill_ms_per_token"] * L
+    gnn_per_node = r["gnn_encode_ms"] / 4.0
+    plen = [int(x) for x in res.prefix_len]
+    T = sum(len(s.node_ids) for s in w.retrieved) * gnn_per_node + r["agglomerate_ms"]
+    for P in plen:
+        T += P * t_pre * (1 + 4 * d * (P / 2) / matvec)
+    for q, c in zip(pb.q, res.labels):
+        P = plen[c]
+        T += len(q) * t_ext * (1 + 4 * d * P / matvec)
+    m = len(w.queries)
+    return {"value": round(m / (T / 1000.0), 6), "unit": "queries/s", "cores": threads, "kind": kind,
+            "ttft_p50_ms_extrapolated": round(T / 2, 1),
+            "batch_ms_extrapolated": round(T, 1),
+            "sample": (f"ref_driver at full width, 1 layer (x{L}): prefill 4 tok, extend 2 tok"
+                       f"{' x%d threads' % threads if threads > 1 else ''}, GNN encode of a 4-node "
+                       f"subgraph, agglomerate at full m={m}; {sample_s:.1f}s of CPU work; "
+                       f"extrapolated to the whole batch"),
+            "measured": {k: v for k, v in r.items() if k.endswith("_ms") or "per_token" in k}}
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation (oracle/_ref) on the host cores,
+    all threads (std::async per member as --parallel-queries), bounded sample per step."""
+    import torch  # noqa: F401  (only for parity of the environment)
+
+    from paper_2505_10951_b200 import host
+
+    w = build_workload(args)
+    # representatives' prompt lengths and labels come from the reference's own algorithm on
+    # this workload; we use the restated pipeline pieces (bit-identical, tests/test_oracle_pin)
+    import oracle
+
+    pb = host.PreparedBatch(w, with_own_prefix=False)
+    threads = os.cpu_count() or 1
+
+    class R:  # minimal result holder for the extrapolation
+        pass
+
+    res = R()
+    # labels / prefix lengths: restated clustering on restated embeddings would need a full CPU
+    # GNN run; the prompt sizes only enter the cost model, so use the workload's community
+    # structure (query j -> community j % clusters) and the union prompt length of each.
+    from paper_2505_10951_b200 import workload as W
+
+    k = w.clusters
+    res.labels = np.array([j % k for j in range(len(w.queries))])
+    plen = []
+    for c in range(k):
+        idx = [j for j in range(len(w.queries)) if j % k == c]
+        u = W.Subgraph.of(set().union(*[set(w.retrieved[j].node_ids.tolist()) for j in idx]),
+                          set().union(*[set(w.retrieved[j].edge_indices.tolist()) for j in idx]))
+        plen.append(min(W.prompt_tokens_estimate(w.graph, u), pb.budget))
+    res.prefix_len = np.array(plen)
+    vals = []
+    t_start = time.time()
+    for s in range(args.warmup + args.steps):
+        cb = cpu_baseline(w, res, pb, threads=threads)
+        if s >= args.warmup:
+            vals.append(cb)
+    v = float(np.median([c["value"] for c in vals]))
+    ms = float(np.median([c["batch_ms_extrapolated"] for c in vals]))
+    cb = vals[-1]
+    cb["value"] = v
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "queries/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "fp32 (reference CPU)",
+           "data": "synthetic", "config": {"workload": w.name, "queries": len(w.queries),
+                                           "clusters": k},
+           "ttft_p50_ms": cb["ttft_p50_ms_extrapolated"],
+           "cpu_baseline": cb,
+           "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "wall_s": round(time.time() - t_start, 1)}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--m", type=int, default=0)
+    ap.add_argument("--clusters", type=int, default=0)
+    ap.add_argument("--layers", type=int, default=0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours" and not os.environ.get("SGC_PROFILE"):
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)))
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    out = run_ours(args, rank, world, local_rank)
+    if rank == 0 and out is not None:
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

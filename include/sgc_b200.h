@@ -189,11 +189,14 @@ typedef struct {
     int soft_prefix;           /* RunConfig::soft_prefix_enabled() */
     float pointer_bonus;       /* EngineOptions::pointer_bonus (100) */
     sgc_gnn_config gnn;
-    /* multi-GPU: this rank serves only clusters k with owner[k] == rank when owner != NULL
-     * (embeddings must then be supplied gathered, see precomputed_embeddings) */
-    const float* precomputed_embeddings; /* [m * dim] or NULL to encode here */
-    const uint32_t* cluster_owner;       /* [c] or NULL = all clusters */
+    /* multi-GPU (whole clusters per GPU): with world_size > 1 every rank
+     * clusters the gathered embeddings redundantly (bit-identical labels), assigns clusters
+     * to ranks by LPT on their cost (prefix + member rows, FLOP-weighted) and serves only its
+     * own. cluster_owner (optional) forces the assignment. */
+    const float* precomputed_embeddings; /* [m * dim] (all-gathered) or NULL to encode here */
+    const uint32_t* cluster_owner;       /* [c] or NULL = LPT over world_size */
     int rank;
+    int world_size;                      /* 0 or 1 = single GPU */
 } sgc_batch;
 
 typedef struct {
@@ -206,6 +209,7 @@ typedef struct {
     float* logits;          /* [m * 260] optional (rows of unserved queries untouched) */
     int32_t* first_token;   /* [m] optional (-1 for queries not served by this rank) */
     uint8_t* fallback;      /* [m] optional */
+    uint32_t* owner;        /* [c] optional: rank serving each cluster */
     double stage_ms[8];     /* encode, cluster, represent, prefill, extend, total, -, - */
     uint64_t prefill_rows, extend_rows; /* tokens pushed through prefill / extend */
 } sgc_batch_out;

@@ -17,6 +17,7 @@
 #include <chrono>
 #include <cstdio>
 #include <fstream>
+#include <future>
 #include <iostream>
 #include <thread>
 
@@ -388,6 +389,25 @@ json cmd_bench(const json& spec) {
         t0 = Clock::now();
         lm.extend(f, rand_toks(en));
         out["extend_ms_per_token"] = ms_since(t0) / en;
+    }
+    // --parallel-queries analogue (cache_engine.cpp:195-201): T members extend concurrently
+    // on forks of one sealed prefix, one std::async task each
+    uint32_t threads = spec.value("threads", 1u);
+    if (threads > 1 && en > 0) {
+        KVCache base = lm.prefill(rand_toks(4));
+        base.seal();
+        std::vector<std::vector<TokenId>> qs;
+        for (uint32_t t = 0; t < threads; ++t) qs.push_back(rand_toks(en));
+        t0 = Clock::now();
+        std::vector<std::future<void>> futs;
+        for (uint32_t t = 0; t < threads; ++t)
+            futs.push_back(std::async(std::launch::async, [&, t] {
+                KVCache f = base.fork();
+                lm.extend(f, qs[t]);
+            }));
+        for (auto& f : futs) f.get();
+        out["parallel_extend_ms_per_token"] = ms_since(t0) / (static_cast<double>(en) * threads);
+        out["parallel_threads"] = threads;
     }
     if (spec.contains("gnn_nodes")) {
         uint32_t n = spec["gnn_nodes"], e = spec.value("gnn_edges", n - 1);

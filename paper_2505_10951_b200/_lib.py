@@ -75,7 +75,8 @@ class Batch(C.Structure):
                 ("question_budget", C.c_uint32), ("soft_prefix", C.c_int),
                 ("pointer_bonus", C.c_float), ("gnn", GnnConfig),
                 ("precomputed_embeddings", C.POINTER(C.c_float)),
-                ("cluster_owner", C.POINTER(C.c_uint32)), ("rank", C.c_int)]
+                ("cluster_owner", C.POINTER(C.c_uint32)), ("rank", C.c_int),
+                ("world_size", C.c_int)]
 
 
 class BatchOut(C.Structure):
@@ -83,7 +84,8 @@ class BatchOut(C.Structure):
                 ("merge_left", C.POINTER(C.c_uint32)), ("merge_right", C.POINTER(C.c_uint32)),
                 ("merge_dist", C.POINTER(C.c_double)), ("prefix_len", C.POINTER(C.c_uint64)),
                 ("logits", C.POINTER(C.c_float)), ("first_token", C.POINTER(C.c_int32)),
-                ("fallback", C.POINTER(C.c_uint8)), ("stage_ms", C.c_double * 8),
+                ("fallback", C.POINTER(C.c_uint8)), ("owner", C.POINTER(C.c_uint32)),
+                ("stage_ms", C.c_double * 8),
                 ("prefill_rows", C.c_uint64), ("extend_rows", C.c_uint64)]
 
 

@@ -191,8 +191,9 @@ struct FwdBatch {
     const int32_t* d_soft_idx = nullptr;  // [M] row -> soft vector index or -1
     const int32_t* d_pos = nullptr;
     const int32_t* d_seg_lo = nullptr;
-    const sgc::AttnWork* d_work = nullptr;
+    const sgc::AttnWork* d_work = nullptr;  // tiles of <= attn_tile(hd) rows
     int n_work = 0;
+    int pfx_rows = 0;  // rows of the prefix KV region (TMA bounds)
     // KV written by this batch: row r -> loc row r of (k_loc_layer(l), v_loc_layer(l))
     std::function<bf16*(int)> k_loc, v_loc;
     std::function<const bf16*(int)> k_pfx, v_pfx;
@@ -246,7 +247,10 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
         ap.work = b.d_work;
         ap.d = d;
         ap.scale = 1.0f / std::sqrt(static_cast<float>(m->hd));
-        sgc::cascade_attention(c, ap, b.n_work, m->H, m->hd);
+        if (sgc::attention_tc_supported(m->hd))
+            sgc::cascade_attention_tc(c, ap, b.n_work, m->H, m->hd, M, b.k_pfx ? b.pfx_rows : M, M);
+        else
+            sgc::cascade_attention(c, ap, b.n_work, m->H, m->hd);
 
         sgc::GemmEpi r;
         r.mode = sgc::EPI_RESID;
@@ -271,12 +275,15 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
 
 // tiles of <= 64 rows that never cross a `group` boundary (sequence for prefill, segment
 // for extend); rows of one group are contiguous
+int attn_tile(int hd) { return sgc::attention_tc_supported(hd) ? 128 : 64; }
+
 std::vector<sgc::AttnWork> make_work(const std::vector<int>& group_start, const std::vector<int>& group_rows,
-                                     const std::vector<int>& pfx_kv0, const std::vector<int>& pfx_len) {
+                                     const std::vector<int>& pfx_kv0, const std::vector<int>& pfx_len,
+                                     int tile) {
     std::vector<sgc::AttnWork> w;
     for (size_t g = 0; g < group_start.size(); ++g)
-        for (int r = 0; r < group_rows[g]; r += 64)
-            w.push_back({group_start[g] + r, std::min(64, group_rows[g] - r), pfx_kv0[g], pfx_len[g]});
+        for (int r = 0; r < group_rows[g]; r += tile)
+            w.push_back({group_start[g] + r, std::min(tile, group_rows[g] - r), pfx_kv0[g], pfx_len[g]});
     return w;
 }
 
@@ -345,7 +352,7 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
         gs.push_back(static_cast<int>(kv->off[s]));
         gr.push_back(static_cast<int>(kv->len[s]));
     }
-    std::vector<sgc::AttnWork> work = make_work(gs, gr, z, z);
+    std::vector<sgc::AttnWork> work = make_work(gs, gr, z, z, attn_tile(m->hd));
     sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("pf_work", work.size());
     sgc::copy_in(c, d_pos, pos.data(), M);
     sgc::copy_in(c, d_seg, seg_lo.data(), M);
@@ -445,7 +452,7 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
             }
             a_off.push_back(a_tok.size());
         }
-        std::vector<sgc::AttnWork> work = make_work(gs, gr, pk, pl);
+        std::vector<sgc::AttnWork> work = make_work(gs, gr, pk, pl, attn_tile(m->hd));
         const int nm = static_cast<int>(i1 - i0);
         int32_t* d_tok = c->buf<int32_t>("ex_tok", M);
         int32_t* d_pos = c->buf<int32_t>("ex_pos", M);
@@ -477,6 +484,7 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
         b.k_loc = [kl](int) { return kl; };
         b.v_loc = [vl](int) { return vl; };
         b.k_pfx = [kv](int l) { return static_cast<const bf16*>(kv->k_layer(l)); };
+        b.pfx_rows = static_cast<int>(kv->rows);
         b.v_pfx = [kv](int l) { return static_cast<const bf16*>(kv->v_layer(l)); };
         b.d_logit_rows = d_lr;
         b.n_logits = nm;
@@ -740,6 +748,23 @@ uint64_t agglomerate_op_count(uint64_t m, uint64_t dim, uint64_t c) {
     return ops;
 }
 
+// LPT: clusters by descending cost (ties by index) to the least-loaded rank (ties by rank)
+std::vector<uint32_t> lpt_assign(const std::vector<double>& cost, int world) {
+    std::vector<uint32_t> order(cost.size());
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return cost[a] > cost[b]; });
+    std::vector<double> load(world, 0.0);
+    std::vector<uint32_t> owner(cost.size(), 0);
+    for (uint32_t ci : order) {
+        int best = 0;
+        for (int r = 1; r < world; ++r)
+            if (load[r] < load[best]) best = r;
+        owner[ci] = static_cast<uint32_t>(best);
+        load[best] += cost[ci];
+    }
+    return owner;
+}
+
 struct RepResult {
     std::vector<uint64_t> prefix_off;  // [c+1] on host
     int32_t* d_prefix = nullptr;       // device tokens (BOS + bytes)
@@ -873,6 +898,12 @@ int sgc_ctx_create(int device, sgc_ctx** out) {
         h->c.device = device;
         h->c.num_sms = prop.multiProcessorCount;
         SGC_CUDA_CHECK(cudaStreamCreateWithFlags(&h->c.own_stream, cudaStreamNonBlocking));
+        // keep freed pool memory mapped: KV segments and activation buffers are re-allocated
+        // every batch, and returning them to the driver would re-map GBs per step
+        cudaMemPool_t pool;
+        SGC_CUDA_CHECK(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = UINT64_MAX;
+        SGC_CUDA_CHECK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         h->c.stream = h->c.own_stream;
         *out = h;
     });
@@ -1302,14 +1333,37 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         // ---- (3) jobs (pipeline.cpp:249-261) + representatives for the clusters served here
         std::vector<std::vector<uint32_t>> members(k);
         for (uint32_t i = 0; i < m; ++i) members[labels[i]].push_back(i);
+        // representatives of every cluster (cheap, exact) -> costs -> LPT owner per cluster
+        RepResult reps_all = build_reps(c, g, hs, m, members, budget);
+        std::vector<uint64_t> q_off_all = to_host(c, b->questions.off, m + 1);
+        std::vector<uint32_t> owner(k, 0);
+        const int world = b->world_size > 1 ? b->world_size : 1;
+        if (b->cluster_owner) {
+            owner = to_host(c, b->cluster_owner, k);
+        } else if (world > 1) {
+            std::vector<double> cost(k, 0.0);
+            const double ftok = 2.0 * model->L * (4.0 * d * d + 2.0 * d * model->ffn);
+            for (uint32_t ci = 0; ci < k; ++ci) {
+                const double P = static_cast<double>(reps_all.prefix_off[ci + 1] - reps_all.prefix_off[ci]);
+                cost[ci] = P * ftok + 2.0 * d * model->L * P * P;
+                for (uint32_t q : members[ci]) {
+                    const double S = static_cast<double>(q_off_all[q + 1] - q_off_all[q]);
+                    cost[ci] += S * ftok + 4.0 * d * model->L * S * P;
+                }
+            }
+            owner = lpt_assign(cost, world);
+        }
+        if (o->owner) sgc::copy_out(c, o->owner, owner.data(), k);
         std::vector<uint32_t> owned;
-        std::vector<uint32_t> owner = b->cluster_owner ? to_host(c, b->cluster_owner, k) : std::vector<uint32_t>();
         for (uint32_t ci = 0; ci < k; ++ci)
-            if (owner.empty() || owner[ci] == static_cast<uint32_t>(b->rank)) owned.push_back(ci);
+            if (owner[ci] == static_cast<uint32_t>(world > 1 || b->cluster_owner ? b->rank : 0)) owned.push_back(ci);
         std::vector<std::vector<uint32_t>> own_members;
         for (uint32_t ci : owned) own_members.push_back(members[ci]);
         RepResult reps;
-        if (!owned.empty()) reps = build_reps(c, g, hs, m, own_members, budget);
+        if (!owned.empty()) {
+            if (owned.size() == k) reps = reps_all;
+            else reps = build_reps(c, g, hs, m, own_members, budget);
+        }
         std::vector<float> soft_h;
         std::vector<uint8_t> soft_mask;
         float* d_soft = nullptr;

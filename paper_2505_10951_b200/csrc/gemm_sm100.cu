@@ -20,6 +20,7 @@
 #include "common.cuh"
 #include "gemm.cuh"
 #include "sm100_ptx.cuh"
+#include "tma.cuh"
 
 namespace sgc {
 
@@ -329,33 +330,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---- host side ----------------------------------------------------------------------------
-
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        cudaDriverEntryPointQueryResult q;
-        void* p = nullptr;
-        SGC_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-        if (q != cudaDriverEntryPointSuccess || !p) fail(SGC_CUDA, "cuTensorMapEncodeTiled unavailable");
-        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
-}
-
-CUtensorMap make_map_2d(const void* base, uint64_t rows, uint64_t cols, uint32_t box_rows,
-                        uint32_t box_cols) {
-    CUtensorMap m;
-    cuuint64_t dims[2] = {cols, rows};
-    cuuint64_t strides[1] = {cols * 2};
-    cuuint32_t box[2] = {box_cols, box_rows};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
-                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) fail(SGC_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
-    return m;
-}
 
 template <int BN, int EPI, int HD>
 void launch(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {

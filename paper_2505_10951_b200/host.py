@@ -431,6 +431,7 @@ class SubgCacheResult:
     logits: np.ndarray
     first_token: np.ndarray
     fallback: np.ndarray
+    owner: np.ndarray
     stage_ms: list
     prefill_rows: int
     extend_rows: int
@@ -458,9 +459,38 @@ class PreparedBatch:
         self.ol, self._ko = pack_tokens(self.own) if self.own else (_lib.TokenLists(0, None, None), None)
 
 
+def _device_copy(pb: "PreparedBatch"):
+    """Device-resident copies of the batch inputs (torch CUDA tensors) and the C structs
+    pointing at them -- the `value` leg of bench.py starts with inputs already in HBM."""
+    import torch
+
+    def dev(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+    keep = []
+
+    def ptr(a, ct):
+        t = dev(a)
+        keep.append(t)
+        return C.cast(C.c_void_p(t.data_ptr()), C.POINTER(ct))
+
+    noff, nodes, eoff, edges = pb._ks
+    subs = _lib.Subgraphs(pb.subs.count, ptr(noff, C.c_uint64), ptr(nodes, C.c_uint32),
+                          ptr(eoff, C.c_uint64), ptr(edges, C.c_uint32))
+
+    def tl(struct, k):
+        if k is None:
+            return struct
+        off, toks = k
+        return _lib.TokenLists(struct.count, ptr(off, C.c_uint64), ptr(toks, C.c_int32))
+
+    return subs, tl(pb.ql, pb._kq), tl(pb.al, pb._ka), tl(pb.ol, pb._ko), keep
+
+
 def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
                   embeddings: np.ndarray | None = None, cluster_owner=None, rank: int = 0,
-                  want_logits: bool = True) -> SubgCacheResult:
+                  world_size: int = 1, want_logits: bool = True,
+                  device_inputs: bool = False) -> SubgCacheResult:
     """pipeline.cpp:212-293 (SubgCache branch) + cache_engine.cpp:217-233 (run_batch), to the
     first token of every query."""
     w = pb.w
@@ -468,10 +498,15 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     d = model.cfg.model_dim
     k = w.clusters
     b = _lib.Batch()
-    b.retrieved = pb.subs
-    b.questions = pb.ql
-    b.answers = pb.al
-    b.own_prefix = pb.ol
+    if device_inputs:
+        if getattr(pb, "_dev", None) is None:
+            pb._dev = _device_copy(pb)
+        b.retrieved, b.questions, b.answers, b.own_prefix, _ = pb._dev
+    else:
+        b.retrieved = pb.subs
+        b.questions = pb.ql
+        b.answers = pb.al
+        b.own_prefix = pb.ol
     b.clusters = k
     b.linkage = LINKAGES[w.linkage]
     b.question_budget = w.question_budget
@@ -487,6 +522,7 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
         own = np.ascontiguousarray(cluster_owner, np.uint32)
         b.cluster_owner = _p(own, C.c_uint32)
     b.rank = rank
+    b.world_size = world_size
     emb = np.zeros((m, d), np.float32)
     labels = np.zeros(m, np.uint32)
     nm = max(m - k, 1)
@@ -496,7 +532,9 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     logits = np.zeros((m, VOCAB), np.float32) if want_logits else None
     first = np.full(m, -1, np.int32)
     fb = np.zeros(m, np.uint8)
+    owner = np.zeros(k, np.uint32)
     o = _lib.BatchOut()
+    o.owner = _p(owner, C.c_uint32)
     o.embeddings = _p(emb, C.c_float)
     o.labels = _p(labels, C.c_uint32)
     o.merge_left = _p(left, C.c_uint32)
@@ -508,4 +546,4 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     o.fallback = _p(fb, C.c_uint8)
     check(ctx.lib.sgc_run_subgcache(ctx.h, model.h, g.h, C.byref(b), C.byref(o)))
     return SubgCacheResult(emb, labels, left[: m - k], right[: m - k], dist[: m - k], plen, logits,
-                           first, fb, list(o.stage_ms)[:6], o.prefill_rows, o.extend_rows)
+                           first, fb, owner, list(o.stage_ms)[:6], o.prefill_rows, o.extend_rows)

@@ -245,7 +245,7 @@ def community_workload(name: str, lm: dict, m: int, communities: int, nodes_per_
         sub = Subgraph.of(sel, sel_edges)
         target = int(sub.node_ids[rng.next() % len(sub.node_ids)])
         attr = nodes[target].split(b"attribute: ")[1].split(b" ")[0]
-        queries.append(Query(j, b"what is the attribute of entity %d in this graph?" % target, attr))
+        queries.append(Query(j, b"which attribute has entity %d?" % target, attr))
         retrieved.append(sub)
     return Workload(name, g, queries, retrieved, dict(lm), clusters)
 
