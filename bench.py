@@ -150,26 +150,21 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist
 
         pg = dist
+    from paper_2505_10951_b200 import dist as D
+
     # this rank's encode shard (contiguous query ranges)
-    lo, hi = (rank * m) // world, ((rank + 1) * m) // world
+    lo, hi = D.shard_range(m, world, rank)
 
     def step():
         emb = None
         if world > 1:
             shard = host.encode_subgraphs(ctx, dg, w.retrieved[lo:hi], pb.gnn)
-            counts = [((r + 1) * m) // world - (r * m) // world for r in range(world)]
-            mx = max(counts)
-            buf = torch.zeros(mx, d, device="cuda")
-            buf[: hi - lo] = torch.from_numpy(shard).cuda()
-            gathered = [torch.zeros(mx, d, device="cuda") for _ in range(world)]
-            pg.all_gather(gathered, buf)
-            emb = torch.cat([g[:c] for g, c in zip(gathered, counts)]).cpu().numpy()
+            emb = D.gather_rows(torch.from_numpy(shard).cuda(), m, world, pg).cpu().numpy()
         res = host.run_subgcache(ctx, lm, dg, pb, embeddings=emb, rank=rank, world_size=world,
                                  want_logits=False, device_inputs=True)
         if world > 1:
-            ft = torch.from_numpy(res.first_token.astype(np.int64)).cuda()
-            pg.all_reduce(ft, op=pg.ReduceOp.MAX)
-            res.first_token = ft.cpu().numpy().astype(np.int32)
+            res.first_token = D.combine_first_tokens(
+                torch.from_numpy(res.first_token.astype(np.int64)).cuda(), pg)
         return res
 
     for _ in range(args.warmup):

@@ -217,6 +217,11 @@ typedef struct {
 int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_batch* batch,
                       sgc_batch_out* out);
 
+/* Cluster -> rank assignment used by sgc_run_subgcache when world_size > 1: longest
+ * processing time first (descending cost, ties by cluster index) onto the least-loaded rank
+ * (ties by rank). Host-only (no device needed). */
+int sgc_lpt_assign(const double* cost, uint32_t clusters, int world_size, uint32_t* owner);
+
 /* ---- GEMM building block (exposed for parity tests and the roofline bench) -----------
  * D[M x N] = A[M x K] (bf16, row-major) * B[N x K]^T (bf16, row-major), fp32 accumulate in
  * TMEM via tcgen05.mma; epi 0 = store fp32 D, 1 = store bf16 D, 2 = D += into fp32 `d`,

@@ -1540,6 +1540,14 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
     });
 }
 
+int sgc_lpt_assign(const double* cost, uint32_t clusters, int world_size, uint32_t* owner) {
+    return guarded([&] {
+        if (world_size < 1) fail(SGC_DOMAIN, "world_size must be >= 1");
+        std::vector<uint32_t> o = lpt_assign(std::vector<double>(cost, cost + clusters), world_size);
+        std::copy(o.begin(), o.end(), owner);
+    });
+}
+
 int sgc_gemm_bf16(sgc_ctx* ctx, const void* a, const void* b, void* d, uint32_t M, uint32_t N, uint32_t K, int epi) {
     return guarded([&] {
         sgc::GemmEpi e;

@@ -3,15 +3,19 @@
 // Same semantics as attention.cu (lm_core.cpp:246-274: one softmax over the sealed prefix keys
 // followed by the row's own causal suffix keys), re-laid out for the 5th-gen tensor cores:
 //
-//   warp 0      TMA loader: Q tile (128 rows) once per item; K and V blocks (128 keys) of the
-//               cluster's prefix (phase A) then of the batch's own rows (phase B), 2-stage ring
+//   warp 0      TMA loader: Q tile (128 rows) once per item and K blocks (128 keys) of the
+//               cluster's prefix (phase A) then of the batch's own rows (phase B), 3-stage ring
+//               released as soon as S = Q K^T has consumed a slot
+//   warp 3      TMA loader for the V blocks, 2-stage ring released after O += P V
 //   warp 1      MMA issuer (one thread): S_b = Q K_b^T into a double-buffered TMEM S, and
 //               O += P_{b-1} V_{b-1} into TMEM O (P from smem, V as an MN-major operand)
 //   warp 2      TMEM allocator (512 columns: S0 | S1 | O)
-//   warps 4..7  softmax: thread r owns query row r (TMEM lane r). Reads its S row from TMEM,
-//               masks, online softmax in base 2 with lazy O rescale (only when the running max
-//               grows by > 2^8), writes its P row (bf16, 128B-swizzled) for the PV MMA, and at
-//               the end normalizes its O row and stores it.
+//   warps 4..11 softmax, two warpgroups: thread (r, half) owns keys [64 half, 64 half + 64) of
+//               query row r (TMEM lane r) and O columns [HD/2 half, ...). Reads its S half-row
+//               from TMEM, masks, agrees on the row max with its partner through smem, online
+//               softmax in base 2 with lazy O rescale (only when the running max grows by > 2^8),
+//               writes its P half-row (bf16, 128B-swizzled) for the PV MMA, and at the end
+//               normalizes and stores its half of the O row.
 //
 // The kernel is persistent: CTAs loop over (tile, head) items; a tile is <= 128 query rows of
 // one cluster, so the prefix K/V blocks are fetched once per tile for every member row in it.
@@ -25,7 +29,7 @@ namespace {
 
 constexpr int BQ = 128;   // query rows per item
 constexpr int BKV = 128;  // keys per block
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // 4 control warps + 2 softmax warpgroups
 
 template <int HD>
 struct TcCfg {
@@ -34,8 +38,11 @@ struct TcCfg {
     static constexpr int kKBytes = BKV * HD * 2;
     static constexpr int kVBytes = BKV * HD * 2;
     static constexpr int kPBytes = BQ * BKV * 2;
-    static constexpr int kStageBytes = kKBytes + kVBytes;
-    static constexpr int kSmem = 1024 + kQBytes + kPBytes + 2 * kStageBytes + 256;
+    static constexpr int kKStages = 3;  // K slots are freed as soon as S = Q K^T completes
+    static constexpr int kVStages = 2;  // V slots are freed after O += P V
+    static constexpr int kRedBytes = 2 * 2 * BQ * 4;
+    static constexpr int kSmem = kQBytes + kPBytes + kKStages * kKBytes + kVStages * kVBytes +
+                                 kRedBytes + 256;
     static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kO = 256;             // TMEM column of the O accumulator
 };
@@ -48,6 +55,17 @@ struct TcParams {
     int d;
     float scale_log2;
 };
+
+// MUFU.EX2 without the denormal-range fixups of exp2f (inputs are <= 8; ex2(-inf) = +0)
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 __device__ __forceinline__ void item_blocks(const AttnWork& w, const int32_t* seg_lo, int& nA,
                                             int& nB, int& loc_first) {
@@ -63,23 +81,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap tmVp, const __grid_constant__ CUtensorMap tmKl,
                    const __grid_constant__ CUtensorMap tmVl, TcParams p) {
     using C = TcCfg<HD>;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    // all shared memory is dynamic (no static arrays), so the base is 1024-byte aligned
+    extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sQ = smem;
     uint8_t* sP = sQ + C::kQBytes;
-    uint8_t* sKV = sP + C::kPBytes;  // stage s: K at sKV + s*kStageBytes, V right after K
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + 2 * C::kStageBytes);
+    uint8_t* sK = sP + C::kPBytes;                       // [kKStages][BKV x HD]
+    uint8_t* sV = sK + C::kKStages * C::kKBytes;         // [kVStages][BKV x HD]
+    float (*red_max)[2][BQ] = reinterpret_cast<float (*)[2][BQ]>(sV + C::kVStages * C::kVBytes);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(red_max) + C::kRedBytes);
     uint64_t* q_full = bars + 0;
     uint64_t* q_empty = bars + 1;
-    uint64_t* kv_full = bars + 2;   // [2]
-    uint64_t* kv_empty = bars + 4;  // [2]
-    uint64_t* s_full = bars + 6;    // [2]
-    uint64_t* s_empty = bars + 8;   // [2]
-    uint64_t* p_full = bars + 10;
-    uint64_t* p_empty = bars + 11;
-    uint64_t* o_full = bars + 12;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+    uint64_t* k_full = bars + 2;    // [3]
+    uint64_t* k_empty = bars + 5;   // [3]
+    uint64_t* v_full = bars + 8;    // [2]
+    uint64_t* v_empty = bars + 10;  // [2]
+    uint64_t* s_full = bars + 12;   // [2]
+    uint64_t* s_empty = bars + 14;  // [2]
+    uint64_t* p_full = bars + 16;
+    uint64_t* p_empty = bars + 17;
+    uint64_t* o_full = bars + 18;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int n_items = p.n_work * p.heads;
@@ -92,13 +113,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch_desc(&tmVl);
         ptx::mbar_init(q_full, 1);
         ptx::mbar_init(q_empty, 1);
-        for (int i = 0; i < 2; ++i) {
-            ptx::mbar_init(&kv_full[i], 1);
-            ptx::mbar_init(&kv_empty[i], 1);
-            ptx::mbar_init(&s_full[i], 1);
-            ptx::mbar_init(&s_empty[i], 128);
+        for (int i = 0; i < C::kKStages; ++i) {
+            ptx::mbar_init(&k_full[i], 1);
+            ptx::mbar_init(&k_empty[i], 1);
         }
-        ptx::mbar_init(p_full, 128);
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&v_full[i], 1);
+            ptx::mbar_init(&v_empty[i], 1);
+            ptx::mbar_init(&s_full[i], 1);
+            ptx::mbar_init(&s_empty[i], 256);
+        }
+        ptx::mbar_init(p_full, 256);
         ptx::mbar_init(p_empty, 1);
         ptx::mbar_init(o_full, 1);
         ptx::fence_barrier_init();
@@ -109,33 +134,44 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0) {
+    if (warp == 0 || warp == 3) {
+        // warp 0: Q + K loader (3-stage ring), warp 3: V loader (2-stage ring)
         if (lane == 0) {
+            const bool kload = warp == 0;
             uint32_t g = 0, it = 0;
             for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
                 const int h = item / p.n_work;
                 const AttnWork w = p.work[item % p.n_work];
                 int nA, nB, loc_first;
                 item_blocks(w, p.seg_lo, nA, nB, loc_first);
-                ptx::mbar_wait(q_empty, (it & 1) ^ 1);
-                ptx::mbar_expect_tx(q_full, C::kQBytes);
+                if (kload) {
+                    ptx::mbar_wait(q_empty, (it & 1) ^ 1);
+                    ptx::mbar_expect_tx(q_full, C::kQBytes);
 #pragma unroll
-                for (int s = 0; s < C::kSub; ++s)
-                    ptx::tma_load_2d(sQ + s * (BQ * 128), &tmQ, q_full, h * HD + s * 64, w.row0);
+                    for (int s = 0; s < C::kSub; ++s)
+                        ptx::tma_load_2d(sQ + s * (BQ * 128), &tmQ, q_full, h * HD + s * 64, w.row0);
+                }
                 for (int b = 0; b < nA + nB; ++b, ++g) {
-                    const int st = g & 1;
-                    ptx::mbar_wait(&kv_empty[st], ((g >> 1) & 1) ^ 1);
-                    ptx::mbar_expect_tx(&kv_full[st], C::kStageBytes);
-                    uint8_t* sK = sKV + st * C::kStageBytes;
-                    uint8_t* sV = sK + C::kKBytes;
                     const bool pfx = b < nA;
                     const int row = pfx ? w.pfx_kv0 + b * BKV : loc_first + (b - nA) * BKV;
-                    const CUtensorMap* mk = pfx ? &tmKp : &tmKl;
-                    const CUtensorMap* mv = pfx ? &tmVp : &tmVl;
+                    if (kload) {
+                        const int st = g % C::kKStages;
+                        ptx::mbar_wait(&k_empty[st], ((g / C::kKStages) & 1) ^ 1);
+                        ptx::mbar_expect_tx(&k_full[st], C::kKBytes);
+                        uint8_t* dst = sK + st * C::kKBytes;
 #pragma unroll
-                    for (int s = 0; s < C::kSub; ++s) {
-                        ptx::tma_load_2d(sK + s * (BKV * 128), mk, &kv_full[st], h * HD + s * 64, row);
-                        ptx::tma_load_2d(sV + s * (BKV * 128), mv, &kv_full[st], h * HD + s * 64, row);
+                        for (int s = 0; s < C::kSub; ++s)
+                            ptx::tma_load_2d(dst + s * (BKV * 128), pfx ? &tmKp : &tmKl, &k_full[st],
+                                             h * HD + s * 64, row);
+                    } else {
+                        const int st = g & 1;
+                        ptx::mbar_wait(&v_empty[st], ((g >> 1) & 1) ^ 1);
+                        ptx::mbar_expect_tx(&v_full[st], C::kVBytes);
+                        uint8_t* dst = sV + st * C::kVBytes;
+#pragma unroll
+                        for (int s = 0; s < C::kSub; ++s)
+                            ptx::tma_load_2d(dst + s * (BKV * 128), pfx ? &tmVp : &tmVl, &v_full[st],
+                                             h * HD + s * 64, row);
                     }
                 }
             }
@@ -147,16 +183,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t q_addr = ptx::smem_u32(sQ), p_addr = ptx::smem_u32(sP);
             uint32_t g = 0, it = 0;
             auto issue_pv = [&](uint32_t gb, bool first) {
+                ptx::mbar_wait(&v_full[gb & 1], (gb >> 1) & 1);
                 ptx::mbar_wait(p_full, gb & 1);
                 ptx::tc_fence_after();
-                const uint32_t v_addr = ptx::smem_u32(sKV + (gb & 1) * C::kStageBytes + C::kKBytes);
+                const uint32_t v_addr = ptx::smem_u32(sV + (gb & 1) * C::kVBytes);
 #pragma unroll
                 for (int kk = 0; kk < BKV / 16; ++kk) {
                     uint64_t ad = ptx::umma_desc_sw128(p_addr + (kk / 4) * (BQ * 128) + (kk % 4) * 32);
                     uint64_t bd = ptx::umma_desc_sw128_lbo(v_addr + kk * 16 * 128, BKV * 128, 1024);
                     ptx::mma_bf16(tmem_base + C::kO, ad, bd, idO, (!first || kk > 0) ? 1u : 0u);
                 }
-                ptx::mma_commit(&kv_empty[gb & 1]);
+                ptx::mma_commit(&v_empty[gb & 1]);
                 ptx::mma_commit(p_empty);
             };
             for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
@@ -167,10 +204,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::mbar_wait(q_full, it & 1);
                 for (int b = 0; b < nb; ++b, ++g) {
                     const int st = g & 1;
-                    ptx::mbar_wait(&kv_full[st], (g >> 1) & 1);
+                    const int ks = g % C::kKStages;
+                    ptx::mbar_wait(&k_full[ks], (g / C::kKStages) & 1);
                     ptx::mbar_wait(&s_empty[st], ((g >> 1) & 1) ^ 1);
                     ptx::tc_fence_after();
-                    const uint32_t k_addr = ptx::smem_u32(sKV + st * C::kStageBytes);
+                    const uint32_t k_addr = ptx::smem_u32(sK + ks * C::kKBytes);
 #pragma unroll
                     for (int kc = 0; kc < HD / 16; ++kc) {
                         uint64_t ad = ptx::umma_desc_sw128(q_addr + (kc / 4) * (BQ * 128) + (kc % 4) * 32);
@@ -178,6 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::mma_bf16(tmem_base + st * BKV, ad, bd, idS, kc > 0 ? 1u : 0u);
                     }
                     ptx::mma_commit(&s_full[st]);
+                    ptx::mma_commit(&k_empty[ks]);
                     if (b == nb - 1) ptx::mma_commit(q_empty);
                     if (b >= 1) issue_pv(g - 1, b - 1 == 0);
                 }
@@ -186,11 +225,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const int r = threadIdx.x - 128;  // query row within the tile == TMEM lane
-        const uint32_t lane_base = static_cast<uint32_t>((warp - 4) * 32) << 16;
+        // two softmax warpgroups split each row's 128 keys (and O's HD columns) in halves;
+        // thread pairs (r, half 0/1) agree on the row max through smem once per block
+        const int half = (warp - 4) >> 2;
+        const int r = (threadIdx.x - 128) & (BQ - 1);  // query row within the tile == TMEM lane
+        const uint32_t lane_base = static_cast<uint32_t>(((warp - 4) & 3) * 32) << 16;
+        constexpr int KH = BKV / 2;  // keys per thread
+        constexpr int OH = HD / 2;   // O columns per thread
         uint32_t g = 0, it = 0;
-        // P row r inside the swizzled [128 x 128] bf16 tile (two 64-key sub-tiles)
-        uint8_t* prow = sP + (r >> 3) * 1024 + (r & 7) * 128;
+        // P row r inside the swizzled [128 x 128] bf16 tile: this half = one 64-key sub-tile
+        uint8_t* prow = sP + half * (BQ * 128) + (r >> 3) * 1024 + (r & 7) * 128;
         for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
             const int h = item / p.n_work;
             const AttnWork w = p.work[item % p.n_work];
@@ -205,32 +249,45 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int st = g & 1;
                 ptx::mbar_wait(&s_full[st], (g >> 1) & 1);
                 ptx::tc_fence_after();
-                float s[BKV];
+                float s[KH];
 #pragma unroll
-                for (int c = 0; c < BKV / 32; ++c)
-                    ptx::tmem_ld32(tmem_base + lane_base + st * BKV + c * 32,
+                for (int c = 0; c < KH / 32; ++c)
+                    ptx::tmem_ld32(tmem_base + lane_base + st * BKV + half * KH + c * 32,
                                    *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
                 ptx::tmem_ld_wait();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&s_empty[st]);
-                // mask + scale (base-2 logits)
-                float mx = -INFINITY;
+                // visible key window [klo, khi] of this row, in block-local key index
+                int k0, klo, khi;
                 if (b < nA) {
-                    const int kend = w.pfx_len - b * BKV;
-#pragma unroll
-                    for (int j = 0; j < BKV; ++j) {
-                        s[j] = (valid && j < kend) ? s[j] * p.scale_log2 : -INFINITY;
-                        mx = fmaxf(mx, s[j]);
-                    }
+                    k0 = b * BKV;
+                    klo = 0;
+                    khi = valid ? min(BKV, w.pfx_len - k0) - 1 : -1;
                 } else {
-                    const int k0 = loc_first + (b - nA) * BKV;
+                    k0 = loc_first + (b - nA) * BKV;
+                    klo = max(0, seg - k0);
+                    khi = valid ? min(BKV - 1, row - k0) : -1;
+                }
+                const int cb = half * KH;
+                // fast path (interior prefix blocks): no masking, scale folded into the FFMA
+                const bool full = klo <= cb && khi >= cb + KH - 1;
+                float mx;
+                if (full) {
+                    mx = s[0];
 #pragma unroll
-                    for (int j = 0; j < BKV; ++j) {
-                        const int key = k0 + j;
-                        s[j] = (key >= seg && key <= row) ? s[j] * p.scale_log2 : -INFINITY;
+                    for (int j = 1; j < KH; ++j) mx = fmaxf(mx, s[j]);
+                    mx *= p.scale_log2;
+                } else {
+                    mx = -INFINITY;
+#pragma unroll
+                    for (int j = 0; j < KH; ++j) {
+                        s[j] = (cb + j >= klo && cb + j <= khi) ? s[j] * p.scale_log2 : -INFINITY;
                         mx = fmaxf(mx, s[j]);
                     }
                 }
+                red_max[st][half][r] = mx;
+                named_bar_sync(1, 256);
+                mx = fmaxf(mx, red_max[st][half ^ 1][r]);
                 // lazy rescale: keep the running max unless it grows by more than 8 (2^8)
                 float alpha = 1.f;
                 bool rescale = false;
@@ -238,34 +295,44 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (m == -INFINITY) {
                         m = mx;  // O and l are still zero
                     } else if (mx > m + 8.f) {
-                        alpha = exp2f(m - mx);
+                        alpha = ex2_approx(m - mx);
                         m = mx;
                         rescale = true;
                     }
                 }
                 float rs = 0.f;
-                uint32_t pk[BKV / 2];
+                uint32_t pk[KH / 2];
                 if (m == -INFINITY) {
 #pragma unroll
-                    for (int j = 0; j < BKV / 2; ++j) pk[j] = 0u;
+                    for (int j = 0; j < KH / 2; ++j) pk[j] = 0u;
+                } else if (full) {
+                    const float sc = p.scale_log2, nm = -m;
+#pragma unroll
+                    for (int j = 0; j < KH / 2; ++j) {
+                        float a = ex2_approx(fmaf(s[2 * j], sc, nm));
+                        float c = ex2_approx(fmaf(s[2 * j + 1], sc, nm));
+                        rs += a + c;
+                        __nv_bfloat162 v = __floats2bfloat162_rn(a, c);
+                        pk[j] = *reinterpret_cast<uint32_t*>(&v);
+                    }
                 } else {
 #pragma unroll
-                    for (int j = 0; j < BKV / 2; ++j) {
-                        float a = exp2f(s[2 * j] - m), c = exp2f(s[2 * j + 1] - m);
+                    for (int j = 0; j < KH / 2; ++j) {
+                        float a = ex2_approx(s[2 * j] - m), c = ex2_approx(s[2 * j + 1] - m);
                         rs += a + c;
                         __nv_bfloat162 v = __floats2bfloat162_rn(a, c);
                         pk[j] = *reinterpret_cast<uint32_t*>(&v);
                     }
                 }
-                l = l * alpha + rs;
+                l = l * alpha + rs;  // this half's share of the row sum
                 // P buffer free and O stable once PV of the previous block completed
                 ptx::mbar_wait(p_empty, (g & 1) ^ 1);
                 ptx::tc_fence_after();
                 if (rescale && b > 0) {
 #pragma unroll 1
-                    for (int c = 0; c < HD / 32; ++c) {
+                    for (int c = 0; c < OH / 32; ++c) {
                         uint32_t o[32];
-                        const uint32_t ta = tmem_base + lane_base + C::kO + c * 32;
+                        const uint32_t ta = tmem_base + lane_base + C::kO + half * OH + c * 32;
                         ptx::tmem_ld32(ta, o);
                         ptx::tmem_ld_wait();
 #pragma unroll
@@ -274,28 +341,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     ptx::tmem_st_wait();
                 }
-                // P row: 16 chunks of 8 keys (16 B), sub-tile = chunk / 8, 128B XOR swizzle
+                // P half-row: 8 chunks of 8 keys (16 B) with the 128B XOR swizzle
 #pragma unroll
-                for (int q = 0; q < BKV / 8; ++q) {
-                    const int sub = q >> 3, cc = q & 7;
-                    uint4 v = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-                    *reinterpret_cast<uint4*>(prow + sub * (BQ * 128) + ((cc ^ (r & 7)) << 4)) = v;
+                for (int cc = 0; cc < 8; ++cc) {
+                    uint4 v = make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
+                    *reinterpret_cast<uint4*>(prow + ((cc ^ (r & 7)) << 4)) = v;
                 }
                 ptx::fence_proxy_async_smem();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(p_full);
             }
-            // epilogue: O / l -> bf16
+            // epilogue: O / l -> bf16 (each half stores HD/2 columns); the row sums are
+            // exchanged through red_max[0] once both halves are past their last max exchange
+            named_bar_sync(1, 256);
+            red_max[0][half][r] = l;
+            named_bar_sync(1, 256);
+            const float lt = l + red_max[0][half ^ 1][r];
             ptx::mbar_wait(o_full, it & 1);
             ptx::tc_fence_after();
-            const float il = l > 0.f ? 1.f / l : 0.f;
+            const float il = lt > 0.f ? 1.f / lt : 0.f;
 #pragma unroll 1
-            for (int c = 0; c < HD / 32; ++c) {
+            for (int c = 0; c < OH / 32; ++c) {
                 uint32_t o[32];
-                ptx::tmem_ld32(tmem_base + lane_base + C::kO + c * 32, o);
+                ptx::tmem_ld32(tmem_base + lane_base + C::kO + half * OH + c * 32, o);
                 ptx::tmem_ld_wait();
                 if (valid) {
-                    uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(row) * p.d + h * HD + c * 32);
+                    uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(row) * p.d + h * HD +
+                                                          half * OH + c * 32);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         uint32_t wv[4];
@@ -310,6 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             ptx::tc_fence_before();
+            named_bar_sync(1, 256);  // red_max[0] is reused by the next item
         }
     }
     __syncthreads();

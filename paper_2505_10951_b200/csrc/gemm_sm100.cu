@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int num_kb = K / BK;
     // grouped raster: GROUP m-tiles sweep all n-tiles before moving on, so both the
     // activation rows and the weight tiles of the concurrently running CTAs stay in L2
-    const int GROUP = 16;
+    const int GROUP = 64;
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);
