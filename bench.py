@@ -303,7 +303,8 @@ def cpu_baseline(w, res, pb, threads: int = 1, samples: int = 1):
     t_pre = r["prefill_ms_per_token"] * L
     gnn_per_node = r["gnn_encode_ms"] / 4.0
     plen = [int(x) for x in res.prefix_len]
-    T = sum(len(s.node_ids) for s in w.retrieved) * gnn_per_node + r["agglomerate_ms"]
+    # --parallel-queries also runs the per-subgraph encodes concurrently (pipeline.cpp:217-223)
+    T = sum(len(s.node_ids) for s in w.retrieved) * gnn_per_node / threads + r["agglomerate_ms"]
     for P in plen:
         T += P * t_pre * (1 + 4 * d * (P / 2) / matvec)
     for q, c in zip(pb.q, res.labels):
