@@ -161,7 +161,7 @@ def run_ours(args, rank, world, local_rank):
             shard = host.encode_subgraphs(ctx, dg, w.retrieved[lo:hi], pb.gnn)
             emb = D.gather_rows(torch.from_numpy(shard).cuda(), m, world, pg).cpu().numpy()
         res = host.run_subgcache(ctx, lm, dg, pb, embeddings=emb, rank=rank, world_size=world,
-                                 want_logits=False, device_inputs=True)
+                                 want_logits=False, device_inputs=True, waves=args.waves)
         if world > 1:
             res.first_token = D.combine_first_tokens(
                 torch.from_numpy(res.first_token.astype(np.int64)).cuda(), pg)
@@ -176,6 +176,7 @@ def run_ours(args, rank, world, local_rank):
     ctx.set_timing(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stage = np.zeros(6)
+    ttfts = []
     with ClockSampler(local_rank) as clk:
         if world > 1:
             pg.barrier()
@@ -184,6 +185,7 @@ def run_ours(args, rank, world, local_rank):
         for _ in range(args.steps):
             res = step()
             stage += np.array(res.stage_ms)
+            ttfts.append(res.ttft_ms.copy())
         ev1.record(stream)
         if world > 1:
             pg.barrier()
@@ -210,7 +212,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         ev2.record(stream)
         for _ in range(args.steps):
-            r2 = host.run_subgcache(ctx, lm, dg, pb, want_logits=True)
+            r2 = host.run_subgcache(ctx, lm, dg, pb, want_logits=True, waves=args.waves)
         ev3.record(stream)
         torch.cuda.synchronize()
         e2e_ms = ev2.elapsed_time(ev3) / args.steps
@@ -221,6 +223,14 @@ def run_ours(args, rank, world, local_rank):
         e2e = {"value": m / (e2e_ms / 1000.0), "unit": "queries/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
+    if world > 1:
+        # every query is served by one rank: its TTFT is that rank's value (others report -1)
+        tt = torch.from_numpy(np.stack(ttfts)).cuda()
+        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
+        ttfts = list(tt.cpu().numpy())
+    allt = np.concatenate(ttfts)
+    allt = allt[allt >= 0]
+    ttft_p50, ttft_p90 = float(np.percentile(allt, 50)), float(np.percentile(allt, 90))
     if rank != 0:
         return None
     # ---- roofline of the dominant kernel (the tcgen05 GEMM, tensor-bound)
@@ -256,8 +266,10 @@ def run_ours(args, rank, world, local_rank):
                    "question_tokens_mean": float(np.mean(members_q)),
                    "parallelism": f"clusters sharded over {world} GPU(s)" if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (11 GiB bf16 weights + prefix KV streamed every step)"},
-        "ttft_p50_ms": round(ms_per_step, 3),
-        "ttft_semantics": "submission -> first token of every query (whole batch served in one pass)",
+        "ttft_p50_ms": round(ttft_p50, 3),
+        "ttft_p90_ms": round(ttft_p90, 3),
+        "ttft_semantics": ("submission -> first token, per query, device events at the end of the "
+                           f"query's cluster wave ({res.waves} waves); median over queries and steps"),
         "stage_ms": {k: round(v / args.steps, 3) for k, v in
                      zip(["encode", "cluster", "represent", "prefill", "extend", "total"], stage)},
         "kernel_ms_per_step": {"gemm": gemm_ms / args.steps, "attention": attn_ms / args.steps,
@@ -388,6 +400,8 @@ def main():
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--waves", type=int, default=4,
+                    help="serve clusters in this many waves (lower TTFT p50); 1 = one pass")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours" and not os.environ.get("SGC_PROFILE"):
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

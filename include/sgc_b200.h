@@ -197,6 +197,9 @@ typedef struct {
     const uint32_t* cluster_owner;       /* [c] or NULL = LPT over world_size */
     int rank;
     int world_size;                      /* 0 or 1 = single GPU */
+    /* clusters are served in `waves` groups of balanced cost (index order): members of an early
+     * wave get their first token before later waves run (lower TTFT); 0/1 = one pass */
+    uint32_t waves;
 } sgc_batch;
 
 typedef struct {
@@ -206,10 +209,12 @@ typedef struct {
     uint32_t* merge_right;  /* [m - c] optional */
     double* merge_dist;     /* [m - c] optional */
     uint64_t* prefix_len;   /* [c] optional: representative prompt tokens (incl. soft slot) */
-    float* logits;          /* [m * 260] optional (rows of unserved queries untouched) */
-    int32_t* first_token;   /* [m] optional (-1 for queries not served by this rank) */
-    uint8_t* fallback;      /* [m] optional */
+    float* logits;          /* [m * 260] optional, HOST memory (rows of unserved queries untouched) */
+    int32_t* first_token;   /* [m] optional, HOST memory (untouched for queries not served here) */
+    uint8_t* fallback;      /* [m] optional, HOST memory */
     uint32_t* owner;        /* [c] optional: rank serving each cluster */
+    float* ttft_ms;         /* [m] optional: submission -> first token (-1 if not served here) */
+    uint32_t waves;         /* waves actually run */
     double stage_ms[8];     /* encode, cluster, represent, prefill, extend, total, -, - */
     uint64_t prefill_rows, extend_rows; /* tokens pushed through prefill / extend */
 } sgc_batch_out;

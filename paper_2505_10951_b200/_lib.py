@@ -76,7 +76,7 @@ class Batch(C.Structure):
                 ("pointer_bonus", C.c_float), ("gnn", GnnConfig),
                 ("precomputed_embeddings", C.POINTER(C.c_float)),
                 ("cluster_owner", C.POINTER(C.c_uint32)), ("rank", C.c_int),
-                ("world_size", C.c_int)]
+                ("world_size", C.c_int), ("waves", C.c_uint32)]
 
 
 class BatchOut(C.Structure):
@@ -85,6 +85,7 @@ class BatchOut(C.Structure):
                 ("merge_dist", C.POINTER(C.c_double)), ("prefix_len", C.POINTER(C.c_uint64)),
                 ("logits", C.POINTER(C.c_float)), ("first_token", C.POINTER(C.c_int32)),
                 ("fallback", C.POINTER(C.c_uint8)), ("owner", C.POINTER(C.c_uint32)),
+                ("ttft_ms", C.POINTER(C.c_float)), ("waves", C.c_uint32),
                 ("stage_ms", C.c_double * 8),
                 ("prefill_rows", C.c_uint64), ("extend_rows", C.c_uint64)]
 

@@ -1399,130 +1399,185 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             a_tok = to_host(c, b->answers.tokens, a_off[m]);
         }
         std::vector<int32_t> rep_tok = owned.empty() ? std::vector<int32_t>() : to_host(c, reps.d_prefix, reps.prefix_off.back());
-        std::vector<uint64_t> seq_off(1, 0);
-        std::vector<int32_t> seq_tok;
-        std::vector<uint8_t> seq_soft;
-        std::vector<float> seq_soft_vec;
-        std::vector<uint32_t> mem_seg, mem_q;  // extend members
-        std::vector<uint32_t> fb_q;            // fallback queries -> their standalone sequence
-        std::vector<uint64_t> fb_seq;
         std::vector<float> soft_all;
         if (d_soft) soft_all = to_host(c, d_soft, owned.size() * d);
+        std::vector<uint64_t> oo;
+        std::vector<int32_t> ot;
         std::vector<float> emb_h;
-        for (size_t i = 0; i < owned.size(); ++i) {
-            seq_tok.insert(seq_tok.end(), rep_tok.begin() + reps.prefix_off[i], rep_tok.begin() + reps.prefix_off[i + 1]);
-            seq_off.push_back(seq_tok.size());
-            seq_soft.push_back(d_soft ? 1 : 0);
-            if (d_soft) seq_soft_vec.insert(seq_soft_vec.end(), soft_all.begin() + i * d, soft_all.begin() + (i + 1) * d);
-            else seq_soft_vec.insert(seq_soft_vec.end(), d, 0.f);
-            const uint64_t plen = reps.prefix_off[i + 1] - reps.prefix_off[i] + (d_soft ? 1 : 0);
-            if (o->prefix_len) o->prefix_len[owned[i]] = plen;
-            for (uint32_t q : own_members[i]) {
-                const uint64_t qn = q_off[q + 1] - q_off[q];
-                if (plen + qn + lc.max_new_tokens > lc.max_seq_len) {  // cache_engine.cpp:171
-                    fb_q.push_back(q);
-                } else {
-                    mem_seg.push_back(static_cast<uint32_t>(i));
-                    mem_q.push_back(q);
-                }
-            }
+        // ---- waves: owned clusters (index order) in groups of balanced row cost, so members of
+        // early clusters get their first token before the whole batch is done (TTFT), while each
+        // wave still feeds the GEMMs thousands of rows
+        const uint32_t nown = static_cast<uint32_t>(owned.size());
+        std::vector<double> wcost(nown, 0.0);
+        double total_cost = 0;
+        for (uint32_t i = 0; i < nown; ++i) {
+            wcost[i] = static_cast<double>(reps.prefix_off[i + 1] - reps.prefix_off[i]);
+            for (uint32_t q : own_members[i]) wcost[i] += static_cast<double>(q_off[q + 1] - q_off[q]);
+            total_cost += wcost[i];
         }
-        // standalone path for fallbacks (cache_engine.cpp:112-138): own prompt + question, trimmed
-        if (!fb_q.empty()) {
-            if (b->own_prefix.count != m) fail(SGC_DOMAIN, "fallback needs own_prefix token lists");
-            std::vector<uint64_t> oo = to_host(c, b->own_prefix.off, m + 1);
-            std::vector<int32_t> ot = to_host(c, b->own_prefix.tokens, oo[m]);
-            if (b->soft_prefix) emb_h = to_host(c, d_emb, static_cast<size_t>(m) * d);
-            for (uint32_t q : fb_q) {
-                std::vector<int32_t> full(ot.begin() + oo[q], ot.begin() + oo[q + 1]);
-                full.insert(full.end(), q_tok.begin() + q_off[q], q_tok.begin() + q_off[q + 1]);
-                size_t allowed = lc.max_seq_len;
-                allowed -= std::min<size_t>(allowed, lc.max_new_tokens + (b->soft_prefix ? 1 : 0));
-                if (full.size() > allowed) full.resize(allowed);
-                fb_seq.push_back(seq_off.size() - 1);
-                seq_tok.insert(seq_tok.end(), full.begin(), full.end());
-                seq_off.push_back(seq_tok.size());
-                seq_soft.push_back(b->soft_prefix ? 1 : 0);
-                if (b->soft_prefix) seq_soft_vec.insert(seq_soft_vec.end(), emb_h.begin() + static_cast<size_t>(q) * d, emb_h.begin() + static_cast<size_t>(q + 1) * d);
-                else seq_soft_vec.insert(seq_soft_vec.end(), d, 0.f);
+        uint32_t n_waves = b->waves > 0 ? b->waves : 1;
+        n_waves = std::max<uint32_t>(1, std::min(n_waves, nown));
+        std::vector<uint32_t> wave_end;  // exclusive cluster index bound per wave
+        {
+            double acc = 0;
+            for (uint32_t i = 0; i < nown; ++i) {
+                acc += wcost[i];
+                const uint32_t w = static_cast<uint32_t>(wave_end.size());
+                const bool last_wave = w + 1 == n_waves;
+                if (!last_wave && acc >= total_cost * (w + 1) / n_waves && nown - (i + 1) >= n_waves - (w + 1))
+                    wave_end.push_back(i + 1);
             }
+            while (wave_end.size() < n_waves) wave_end.push_back(nown);
         }
+        cudaEvent_t ev_start = c->event();
+        SGC_CUDA_CHECK(cudaEventRecord(ev_start, c->stream));
+        std::vector<cudaEvent_t> ev_wave;
+        std::vector<int32_t> wave_of(m, -1);
         uint64_t prefill_rows = 0, extend_rows = 0;
-        sgc_kv* kv = nullptr;
-        std::vector<float> seq_logits;
-        if (seq_off.size() > 1) {
+        double pf_ms = 0, ex_ms = 0;
+        uint32_t wb = 0;
+        for (uint32_t wv = 0; wv < wave_end.size(); ++wv) {
+            const uint32_t we = wave_end[wv];
+            if (we <= wb) continue;
+            const double tw0 = now_ms();
+            std::vector<uint64_t> seq_off(1, 0);
+            std::vector<int32_t> seq_tok;
+            std::vector<uint8_t> seq_soft;
+            std::vector<float> seq_soft_vec;
+            std::vector<uint32_t> mem_seg, mem_q;  // extend members (segment index within the wave)
+            std::vector<uint32_t> fb_q;            // fallback queries -> their standalone sequence
+            std::vector<uint64_t> fb_seq;
+            for (uint32_t i = wb; i < we; ++i) {
+                seq_tok.insert(seq_tok.end(), rep_tok.begin() + reps.prefix_off[i], rep_tok.begin() + reps.prefix_off[i + 1]);
+                seq_off.push_back(seq_tok.size());
+                seq_soft.push_back(d_soft ? 1 : 0);
+                if (d_soft) seq_soft_vec.insert(seq_soft_vec.end(), soft_all.begin() + static_cast<size_t>(i) * d, soft_all.begin() + static_cast<size_t>(i + 1) * d);
+                else seq_soft_vec.insert(seq_soft_vec.end(), d, 0.f);
+                const uint64_t plen = reps.prefix_off[i + 1] - reps.prefix_off[i] + (d_soft ? 1 : 0);
+                if (o->prefix_len) o->prefix_len[owned[i]] = plen;
+                for (uint32_t q : own_members[i]) {
+                    const uint64_t qn = q_off[q + 1] - q_off[q];
+                    wave_of[q] = static_cast<int32_t>(wv);
+                    if (plen + qn + lc.max_new_tokens > lc.max_seq_len) {  // cache_engine.cpp:171
+                        fb_q.push_back(q);
+                    } else {
+                        mem_seg.push_back(i - wb);
+                        mem_q.push_back(q);
+                    }
+                }
+            }
+            // standalone path for fallbacks (cache_engine.cpp:112-138): own prompt + question, trimmed
+            if (!fb_q.empty()) {
+                if (b->own_prefix.count != m) fail(SGC_DOMAIN, "fallback needs own_prefix token lists");
+                if (oo.empty()) {
+                    oo = to_host(c, b->own_prefix.off, m + 1);
+                    ot = to_host(c, b->own_prefix.tokens, oo[m]);
+                    if (b->soft_prefix) emb_h = to_host(c, d_emb, static_cast<size_t>(m) * d);
+                }
+                for (uint32_t q : fb_q) {
+                    std::vector<int32_t> full(ot.begin() + oo[q], ot.begin() + oo[q + 1]);
+                    full.insert(full.end(), q_tok.begin() + q_off[q], q_tok.begin() + q_off[q + 1]);
+                    size_t allowed = lc.max_seq_len;
+                    allowed -= std::min<size_t>(allowed, lc.max_new_tokens + (b->soft_prefix ? 1 : 0));
+                    if (full.size() > allowed) full.resize(allowed);
+                    fb_seq.push_back(seq_off.size() - 1);
+                    seq_tok.insert(seq_tok.end(), full.begin(), full.end());
+                    seq_off.push_back(seq_tok.size());
+                    seq_soft.push_back(b->soft_prefix ? 1 : 0);
+                    if (b->soft_prefix) seq_soft_vec.insert(seq_soft_vec.end(), emb_h.begin() + static_cast<size_t>(q) * d, emb_h.begin() + static_cast<size_t>(q + 1) * d);
+                    else seq_soft_vec.insert(seq_soft_vec.end(), d, 0.f);
+                }
+            }
             const uint32_t ns = static_cast<uint32_t>(seq_off.size() - 1);
-            seq_logits.resize(static_cast<size_t>(ns) * SGC_VOCAB);
-            kv = do_prefill(c, model, ns, seq_off.data(), seq_tok.data(), seq_soft_vec.data(), seq_soft.data(),
-                            seq_logits.data());
-            prefill_rows = kv->rows;
-        }
-        const double t_pf = now_ms();
-        // ---- (5) per-query reuse: all members of all served clusters in one cascade pass
-        std::unique_ptr<sgc_kv, int (*)(sgc_kv*)> kv_guard(kv, sgc_kv_release);
-        if (!mem_q.empty()) {
-            std::vector<uint64_t> mq_off(1, 0), ma_off(1, 0);
-            std::vector<int32_t> mq_tok, ma_tok;
-            for (uint32_t q : mem_q) {
-                mq_tok.insert(mq_tok.end(), q_tok.begin() + q_off[q], q_tok.begin() + q_off[q + 1]);
-                mq_off.push_back(mq_tok.size());
-                if (ans) ma_tok.insert(ma_tok.end(), a_tok.begin() + a_off[q], a_tok.begin() + a_off[q + 1]);
-                ma_off.push_back(ma_tok.size());
-                extend_rows += q_off[q + 1] - q_off[q];
-            }
-            const uint32_t nm = static_cast<uint32_t>(mem_q.size());
-            std::vector<float> lg(static_cast<size_t>(nm) * SGC_VOCAB);
-            std::vector<int32_t> ft(nm);
-            do_extend(c, model, kv, nm, mem_seg.data(), mq_off.data(), mq_tok.data(), ans ? ma_off.data() : nullptr,
-                      ans ? ma_tok.data() : nullptr, b->pointer_bonus, lg.data(), ft.data());
-            for (uint32_t j = 0; j < nm; ++j) {
-                const uint32_t q = mem_q[j];
-                if (o->logits)
-                    sgc::copy_out(c, o->logits + static_cast<size_t>(q) * SGC_VOCAB, lg.data() + static_cast<size_t>(j) * SGC_VOCAB, SGC_VOCAB);
-                if (o->first_token) sgc::copy_out(c, o->first_token + q, ft.data() + j, 1);
-                if (o->fallback) {
-                    uint8_t z = 0;
-                    sgc::copy_out(c, o->fallback + q, &z, 1);
+            std::vector<float> seq_logits(static_cast<size_t>(ns) * SGC_VOCAB);
+            sgc_kv* kv = do_prefill(c, model, ns, seq_off.data(), seq_tok.data(), seq_soft_vec.data(),
+                                    seq_soft.data(), seq_logits.data());
+            std::unique_ptr<sgc_kv, int (*)(sgc_kv*)> kv_guard(kv, sgc_kv_release);
+            prefill_rows += kv->rows;
+            const double tw1 = now_ms();
+            pf_ms += tw1 - tw0;
+            // ---- (5) per-query reuse: every member of the wave's clusters in one cascade pass
+            if (!mem_q.empty()) {
+                std::vector<uint64_t> mq_off(1, 0), ma_off(1, 0);
+                std::vector<int32_t> mq_tok, ma_tok;
+                for (uint32_t q : mem_q) {
+                    mq_tok.insert(mq_tok.end(), q_tok.begin() + q_off[q], q_tok.begin() + q_off[q + 1]);
+                    mq_off.push_back(mq_tok.size());
+                    if (ans) ma_tok.insert(ma_tok.end(), a_tok.begin() + a_off[q], a_tok.begin() + a_off[q + 1]);
+                    ma_off.push_back(ma_tok.size());
+                    extend_rows += q_off[q + 1] - q_off[q];
+                }
+                const uint32_t nm = static_cast<uint32_t>(mem_q.size());
+                std::vector<float> lg(static_cast<size_t>(nm) * SGC_VOCAB);
+                std::vector<int32_t> ft(nm);
+                do_extend(c, model, kv, nm, mem_seg.data(), mq_off.data(), mq_tok.data(), ans ? ma_off.data() : nullptr,
+                          ans ? ma_tok.data() : nullptr, b->pointer_bonus, lg.data(), ft.data());
+                for (uint32_t j = 0; j < nm; ++j) {
+                    const uint32_t q = mem_q[j];
+                    if (o->logits)
+                        std::memcpy(o->logits + static_cast<size_t>(q) * SGC_VOCAB, lg.data() + static_cast<size_t>(j) * SGC_VOCAB,
+                                    SGC_VOCAB * sizeof(float));
+                    if (o->first_token) o->first_token[q] = ft[j];
+                    if (o->fallback) o->fallback[q] = 0;
                 }
             }
-            c->sync();
-        }
-        // fallback first tokens: standalone logits, hint over the own prompt prefix
-        for (size_t f = 0; f < fb_q.size(); ++f) {
-            const uint32_t q = fb_q[f];
-            const uint64_t s = fb_seq[f];
-            const float* lg = seq_logits.data() + s * SGC_VOCAB;
-            const uint64_t ctx_len = seq_off[s + 1] - seq_off[s] + (b->soft_prefix ? 1 : 0);
-            const uint64_t qn = std::min<uint64_t>(q_off[q + 1] - q_off[q], ctx_len);
-            const uint64_t limit = ctx_len - qn;
-            int target = -1;
-            if (ans && a_off[q + 1] > a_off[q]) {
-                std::vector<int32_t> ctxv;
-                if (b->soft_prefix) ctxv.push_back(259);
-                ctxv.insert(ctxv.end(), seq_tok.begin() + seq_off[s], seq_tok.begin() + seq_off[s + 1]);
-                const int32_t* a = a_tok.data() + a_off[q];
-                const uint64_t al = a_off[q + 1] - a_off[q];
-                for (uint64_t st = 0; st + al <= limit && target < 0; ++st)
-                    if (std::equal(a, a + al, ctxv.begin() + st)) target = a[0];
-            }
-            int best = 0;
-            float bv = lg[0] + (target == 0 ? b->pointer_bonus : 0.0f);
-            for (int v = 1; v < SGC_VOCAB; ++v) {
-                float val = lg[v] + (v == target ? b->pointer_bonus : 0.0f);
-                if (val > bv) {
-                    bv = val;
-                    best = v;
+            // fallback first tokens: standalone logits, hint over the own prompt prefix
+            for (size_t f = 0; f < fb_q.size(); ++f) {
+                const uint32_t q = fb_q[f];
+                const uint64_t s = fb_seq[f];
+                const float* lg = seq_logits.data() + s * SGC_VOCAB;
+                const uint64_t ctx_len = seq_off[s + 1] - seq_off[s] + (b->soft_prefix ? 1 : 0);
+                const uint64_t qn = std::min<uint64_t>(q_off[q + 1] - q_off[q], ctx_len);
+                const uint64_t limit = ctx_len - qn;
+                int target = -1;
+                if (ans && a_off[q + 1] > a_off[q]) {
+                    std::vector<int32_t> ctxv;
+                    if (b->soft_prefix) ctxv.push_back(259);
+                    ctxv.insert(ctxv.end(), seq_tok.begin() + seq_off[s], seq_tok.begin() + seq_off[s + 1]);
+                    const int32_t* a = a_tok.data() + a_off[q];
+                    const uint64_t al = a_off[q + 1] - a_off[q];
+                    for (uint64_t st = 0; st + al <= limit && target < 0; ++st)
+                        if (std::equal(a, a + al, ctxv.begin() + st)) target = a[0];
                 }
+                int best = 0;
+                float bv = lg[0] + (target == 0 ? b->pointer_bonus : 0.0f);
+                for (int v = 1; v < SGC_VOCAB; ++v) {
+                    float val = lg[v] + (v == target ? b->pointer_bonus : 0.0f);
+                    if (val > bv) {
+                        bv = val;
+                        best = v;
+                    }
+                }
+                if (o->logits) std::memcpy(o->logits + static_cast<size_t>(q) * SGC_VOCAB, lg, SGC_VOCAB * sizeof(float));
+                if (o->first_token) o->first_token[q] = best;
+                if (o->fallback) o->fallback[q] = 1;
             }
-            if (o->logits) sgc::copy_out(c, o->logits + static_cast<size_t>(q) * SGC_VOCAB, lg, SGC_VOCAB);
-            if (o->first_token) sgc::copy_out(c, o->first_token + q, &best, 1);
-            if (o->fallback) {
-                uint8_t one = 1;
-                sgc::copy_out(c, o->fallback + q, &one, 1);
-            }
-            c->sync();
+            cudaEvent_t e = c->event();
+            SGC_CUDA_CHECK(cudaEventRecord(e, c->stream));
+            ev_wave.push_back(e);
+            ex_ms += now_ms() - tw1;
+            wb = we;
         }
+        c->sync();
+        std::vector<float> wave_ms;
+        for (cudaEvent_t e : ev_wave) {
+            float ms = 0;
+            SGC_CUDA_CHECK(cudaEventElapsedTime(&ms, ev_start, e));
+            wave_ms.push_back(ms);
+            c->event_pool.push_back(e);
+        }
+        c->event_pool.push_back(ev_start);
+        // TTFT (submission -> first token): batch start to the end of the query's wave; the
+        // encode/cluster/represent stages before ev_start are added from the host clock
+        const double pre_ms = t_rep - t_start;
+        if (o->ttft_ms)
+            for (uint32_t q = 0; q < m; ++q)
+                o->ttft_ms[q] = wave_of[q] >= 0 ? static_cast<float>(pre_ms + wave_ms[wave_of[q]]) : -1.0f;
+        o->waves = static_cast<uint32_t>(ev_wave.size());
+        const double t_pf = t_rep + pf_ms;
         const double t_ext = now_ms();
+        (void)t_pf;
+        (void)t_ext;
         if (o->embeddings) sgc::copy_out(c, o->embeddings, d_emb, static_cast<size_t>(m) * d);
         if (o->labels) sgc::copy_out(c, o->labels, d_lab, m);
         if (o->merge_left) sgc::copy_out(c, o->merge_left, d_left, m - k);
@@ -1532,8 +1587,8 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         o->stage_ms[0] = t_enc - t_start;
         o->stage_ms[1] = t_cl - t_enc;
         o->stage_ms[2] = t_rep - t_cl;
-        o->stage_ms[3] = t_pf - t_rep;
-        o->stage_ms[4] = t_ext - t_pf;
+        o->stage_ms[3] = pf_ms;
+        o->stage_ms[4] = ex_ms;
         o->stage_ms[5] = now_ms() - t_start;
         o->prefill_rows = prefill_rows;
         o->extend_rows = extend_rows;

@@ -432,6 +432,8 @@ class SubgCacheResult:
     first_token: np.ndarray
     fallback: np.ndarray
     owner: np.ndarray
+    ttft_ms: np.ndarray
+    waves: int
     stage_ms: list
     prefill_rows: int
     extend_rows: int
@@ -490,7 +492,7 @@ def _device_copy(pb: "PreparedBatch"):
 def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
                   embeddings: np.ndarray | None = None, cluster_owner=None, rank: int = 0,
                   world_size: int = 1, want_logits: bool = True,
-                  device_inputs: bool = False) -> SubgCacheResult:
+                  device_inputs: bool = False, waves: int = 1) -> SubgCacheResult:
     """pipeline.cpp:212-293 (SubgCache branch) + cache_engine.cpp:217-233 (run_batch), to the
     first token of every query."""
     w = pb.w
@@ -523,6 +525,7 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
         b.cluster_owner = _p(own, C.c_uint32)
     b.rank = rank
     b.world_size = world_size
+    b.waves = waves
     emb = np.zeros((m, d), np.float32)
     labels = np.zeros(m, np.uint32)
     nm = max(m - k, 1)
@@ -533,8 +536,10 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     first = np.full(m, -1, np.int32)
     fb = np.zeros(m, np.uint8)
     owner = np.zeros(k, np.uint32)
+    ttft = np.full(m, -1.0, np.float32)
     o = _lib.BatchOut()
     o.owner = _p(owner, C.c_uint32)
+    o.ttft_ms = _p(ttft, C.c_float)
     o.embeddings = _p(emb, C.c_float)
     o.labels = _p(labels, C.c_uint32)
     o.merge_left = _p(left, C.c_uint32)
@@ -546,4 +551,5 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     o.fallback = _p(fb, C.c_uint8)
     check(ctx.lib.sgc_run_subgcache(ctx.h, model.h, g.h, C.byref(b), C.byref(o)))
     return SubgCacheResult(emb, labels, left[: m - k], right[: m - k], dist[: m - k], plen, logits,
-                           first, fb, owner, list(o.stage_ms)[:6], o.prefill_rows, o.extend_rows)
+                           first, fb, owner, ttft, o.waves, list(o.stage_ms)[:6], o.prefill_rows,
+                           o.extend_rows)

@@ -331,3 +331,20 @@ def test_c1_variants_vs_reference_golden(ctx, variant):
     for i in range(24):
         check_logits(res.logits[i], V["logits"][i])
     assert res.first_token.tolist() == V["first_token"]
+
+
+def test_waves_do_not_change_results(ctx):
+    """Serving clusters in waves only regroups rows: per-row math is identical, so logits and
+    first tokens are bit-identical to the single pass; TTFT grows with the wave index."""
+    w = W.c1_workload(40, 4)
+    pb = host.PreparedBatch(w)
+    lm = host.ToyLm(ctx, host.ToyLmConfig(**w.lm, seed=7))
+    dg = host.DeviceGraph(ctx, w.graph)
+    one = host.run_subgcache(ctx, lm, dg, pb, waves=1)
+    many = host.run_subgcache(ctx, lm, dg, pb, waves=3)
+    assert many.waves == 3 and one.waves == 1
+    assert np.array_equal(one.first_token, many.first_token)
+    assert np.array_equal(one.logits, many.logits)
+    assert (many.ttft_ms > 0).all()
+    order = np.argsort([many.ttft_ms[i] for i in range(40)])
+    assert many.ttft_ms[order[0]] < many.ttft_ms[order[-1]]
