@@ -139,6 +139,7 @@ def run_ours(args, rank, world, local_rank):
     ctx = host.Context(local_rank)
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
+    ctx.set_option("gemm_pairs", 0 if args.no_pairs else 1)
     t0 = time.time()
     lm = host.ToyLm(ctx, host.ToyLmConfig(**w.lm, seed=w.seed))
     dg = host.DeviceGraph(ctx, w.graph)
@@ -400,6 +401,7 @@ def main():
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-pairs", action="store_true", help="1-CTA GEMM instead of CTA pairs")
     ap.add_argument("--waves", type=int, default=4,
                     help="serve clusters in this many waves (lower TTFT p50); 1 = one pass")
     args = ap.parse_args()

@@ -235,6 +235,8 @@ int sgc_gemm_bf16(sgc_ctx* ctx, const void* a, const void* b, void* d, uint32_t 
                   uint32_t K, int epi);
 /* Average device time in ms of the last `n` GEMM launches issued with timing enabled. */
 int sgc_set_timing(sgc_ctx* ctx, int enable);
+/* Tuning knobs: "gemm_pairs" (1 = CTA-pair tcgen05 GEMM for 256-wide tiles, default; 0 = 1-CTA). */
+int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value);
 int sgc_get_timing(sgc_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches);
 
 #ifdef __cplusplus

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsgc_b200.so")
+LIB_PATH = os.environ.get("SGC_LIB", os.path.join(HERE, "libsgc_b200.so"))
 
 SGC_OK, SGC_DOMAIN, SGC_CAPACITY, SGC_INTEGRITY, SGC_PARSE, SGC_LOGIC, SGC_CUDA = range(7)
 VOCAB = 260
@@ -98,7 +98,7 @@ EXPORTS = [
     "sgc_pairwise_distances", "sgc_agglomerate", "sgc_build_representatives", "sgc_prefill",
     "sgc_kv_release", "sgc_kv_count", "sgc_kv_tokens", "sgc_kv_digest", "sgc_kv_resident_bytes",
     "sgc_kv_read", "sgc_extend", "sgc_run_subgcache", "sgc_gemm_bf16", "sgc_set_timing",
-    "sgc_get_timing", "sgc_lpt_assign",
+    "sgc_get_timing", "sgc_lpt_assign", "sgc_set_option",
 ]
 
 _lib = None
@@ -157,6 +157,7 @@ def load() -> C.CDLL:
     L.sgc_gemm_bf16.argtypes = [vp, vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]
     L.sgc_set_timing.argtypes = [vp, C.c_int]
     L.sgc_get_timing.argtypes = [vp, C.c_char_p, P(C.c_double), P(C.c_uint64)]
+    L.sgc_set_option.argtypes = [vp, C.c_char_p, C.c_int64]
     L.sgc_lpt_assign.argtypes = [P(C.c_double), C.c_uint32, C.c_int, P(C.c_uint32)]
     _lib = L
     return L

@@ -163,6 +163,7 @@ struct sgc_kv {
     bf16* v = nullptr;
     int32_t* d_tokens = nullptr;  // context token ids (prefix, incl. soft slot)
     uint64_t* d_tok_off = nullptr;
+    bool owns_kv = true;          // false: K/V live in the context's reusable KV arena
     bf16* k_layer(int l) const { return k + static_cast<size_t>(l) * rows * model->d; }
     bf16* v_layer(int l) const { return v + static_cast<size_t>(l) * rows * model->d; }
 };
@@ -290,7 +291,7 @@ std::vector<sgc::AttnWork> make_work(const std::vector<int>& group_start, const 
 // ============================================================ prefill / extend
 
 sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in, const int32_t* tok_in,
-                   const float* soft, const uint8_t* soft_mask, float* last_logits) {
+                   const float* soft, const uint8_t* soft_mask, float* last_logits, bool arena = false) {
     std::vector<uint64_t> off = to_host(c, off_in, count + 1);
     std::vector<int32_t> toks = to_host(c, tok_in, off[count]);
     std::vector<uint8_t> smask = soft_mask ? to_host(c, soft_mask, count) : std::vector<uint8_t>(count, 0);
@@ -330,8 +331,14 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
     }
     const int M = static_cast<int>(rows_tok.size());
     kv->rows = M;
-    kv->k = dalloc<bf16>(c, static_cast<size_t>(m->L) * M * d);
-    kv->v = dalloc<bf16>(c, static_cast<size_t>(m->L) * M * d);
+    if (arena) {  // batch-internal sealed prefixes: grow-only arena, no per-wave (re)mapping
+        kv->k = c->buf<bf16>("kv_arena_k", static_cast<size_t>(m->L) * M * d);
+        kv->v = c->buf<bf16>("kv_arena_v", static_cast<size_t>(m->L) * M * d);
+        kv->owns_kv = false;
+    } else {
+        kv->k = dalloc<bf16>(c, static_cast<size_t>(m->L) * M * d);
+        kv->v = dalloc<bf16>(c, static_cast<size_t>(m->L) * M * d);
+    }
     kv->d_tokens = dalloc<int32_t>(c, M);
     kv->d_tok_off = dalloc<uint64_t>(c, count + 1);
     sgc::copy_in(c, kv->d_tokens, rows_tok.data(), M);
@@ -1228,8 +1235,10 @@ int sgc_kv_release(sgc_kv* kv) {
     return guarded([&] {
         if (!kv) return;
         Ctx* c = kv->model->c;
-        dfree(c, kv->k);
-        dfree(c, kv->v);
+        if (kv->owns_kv) {
+            dfree(c, kv->k);
+            dfree(c, kv->v);
+        }
         dfree(c, kv->d_tokens);
         dfree(c, kv->d_tok_off);
         c->sync();
@@ -1491,7 +1500,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             const uint32_t ns = static_cast<uint32_t>(seq_off.size() - 1);
             std::vector<float> seq_logits(static_cast<size_t>(ns) * SGC_VOCAB);
             sgc_kv* kv = do_prefill(c, model, ns, seq_off.data(), seq_tok.data(), seq_soft_vec.data(),
-                                    seq_soft.data(), seq_logits.data());
+                                    seq_soft.data(), seq_logits.data(), /*arena=*/true);
             std::unique_ptr<sgc_kv, int (*)(sgc_kv*)> kv_guard(kv, sgc_kv_release);
             prefill_rows += kv->rows;
             const double tw1 = now_ms();
@@ -1595,6 +1604,21 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
     });
 }
 
+#ifdef SGC_ATTN_PROF
+}  // extern "C"
+namespace sgc {
+void attn_prof_read(unsigned long long* out);
+void attn_prof_reset();
+}
+extern "C" {
+// debug builds only (make prof): per-CTA phase cycle counters of the tcgen05 attention kernel
+int sgc_debug_attn_prof(unsigned long long* out, int reset) {
+    if (reset) sgc::attn_prof_reset();
+    else sgc::attn_prof_read(out);
+    return 0;
+}
+#endif
+
 int sgc_lpt_assign(const double* cost, uint32_t clusters, int world_size, uint32_t* owner) {
     return guarded([&] {
         if (world_size < 1) fail(SGC_DOMAIN, "world_size must be >= 1");
@@ -1612,6 +1636,14 @@ int sgc_gemm_bf16(sgc_ctx* ctx, const void* a, const void* b, void* d, uint32_t 
         if (epi == sgc::EPI_QKV) fail(SGC_DOMAIN, "QKV epilogue is internal");
         sgc::gemm_bf16(&ctx->c, a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e);
         ctx->c.sync();
+    });
+}
+
+int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value) {
+    return guarded([&] {
+        (void)ctx;
+        if (std::string(name) == "gemm_pairs") sgc::gemm_set_pairs(value != 0);
+        else fail(SGC_DOMAIN, std::string("unknown option ") + name);
     });
 }
 

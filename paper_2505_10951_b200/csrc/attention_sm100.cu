@@ -47,6 +47,22 @@ struct TcCfg {
     static constexpr uint32_t kO = 256;             // TMEM column of the O accumulator
 };
 
+// Compile with -DSGC_ATTN_PROF to accumulate per-phase clock64() cycles into a global
+// [148][16] counter array (debug builds only; see scripts/attn_prof.py).
+#ifdef SGC_ATTN_PROF
+__device__ unsigned long long g_attn_prof[148 * 16];
+#define PROF_T0() long long _pt = clock64()
+#define PROF_ACC(slot)                                                             \
+    do {                                                                           \
+        long long _n = clock64();                                                  \
+        atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 16 + (slot)], (unsigned long long)(_n - _pt)); \
+        _pt = _n;                                                                  \
+    } while (0)
+#else
+#define PROF_T0()
+#define PROF_ACC(slot)
+#endif
+
 struct TcParams {
     const AttnWork* work;
     int n_work, heads;
@@ -61,6 +77,18 @@ __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// 2^x on the FMA/ALU pipes (FA4-style MUFU offload): round-to-nearest split x = i + f,
+// f in [-0.5, 0.5], degree-3 fit of 2^f (max rel. error 7.7e-5, far below the bf16 rounding
+// of P), exponent added in the integer domain. Inputs are clamped at -125 (result ~1e-38).
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -125.0f);
+    const float t = x + 12582912.0f;  // 1.5 * 2^23: rounds x to the nearest integer
+    const float f = x - (t - 12582912.0f);
+    const float p = fmaf(fmaf(fmaf(0.05508868f, f, 0.24260405f), f, 0.69327623f), f, 0.99992895f);
+    const int e = __float_as_int(t) - 0x4B400000;
+    return __int_as_float(__float_as_int(p) + (e << 23));
 }
 
 __device__ __forceinline__ void named_bar_sync(int id, int n) {
@@ -183,8 +211,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t q_addr = ptx::smem_u32(sQ), p_addr = ptx::smem_u32(sP);
             uint32_t g = 0, it = 0;
             auto issue_pv = [&](uint32_t gb, bool first) {
+                PROF_T0();
                 ptx::mbar_wait(&v_full[gb & 1], (gb >> 1) & 1);
+                PROF_ACC(0);
                 ptx::mbar_wait(p_full, gb & 1);
+                PROF_ACC(1);
                 ptx::tc_fence_after();
                 const uint32_t v_addr = ptx::smem_u32(sV + (gb & 1) * C::kVBytes);
 #pragma unroll
@@ -205,8 +236,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int b = 0; b < nb; ++b, ++g) {
                     const int st = g & 1;
                     const int ks = g % C::kKStages;
+                    PROF_T0();
                     ptx::mbar_wait(&k_full[ks], (g / C::kKStages) & 1);
+                    PROF_ACC(2);
                     ptx::mbar_wait(&s_empty[st], ((g >> 1) & 1) ^ 1);
+                    PROF_ACC(3);
                     ptx::tc_fence_after();
                     const uint32_t k_addr = ptx::smem_u32(sK + ks * C::kKBytes);
 #pragma unroll
@@ -247,7 +281,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             float m = -INFINITY, l = 0.f;
             for (int b = 0; b < nb; ++b, ++g) {
                 const int st = g & 1;
+#ifdef SGC_ATTN_PROF
+                const bool prof_thr = threadIdx.x == 128;
+                long long _pt = clock64();
+#define SPROF(slot)                                                                            \
+    if (prof_thr) {                                                                            \
+        long long _n = clock64();                                                              \
+        atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 16 + (slot)], (unsigned long long)(_n - _pt)); \
+        _pt = _n;                                                                              \
+    }
+#else
+#define SPROF(slot)
+#endif
                 ptx::mbar_wait(&s_full[st], (g >> 1) & 1);
+                SPROF(4);
                 ptx::tc_fence_after();
                 float s[KH];
 #pragma unroll
@@ -257,6 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tmem_ld_wait();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&s_empty[st]);
+                SPROF(5);
                 // visible key window [klo, khi] of this row, in block-local key index
                 int k0, klo, khi;
                 if (b < nA) {
@@ -273,21 +321,24 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool full = klo <= cb && khi >= cb + KH - 1;
                 float mx;
                 if (full) {
-                    mx = s[0];
+                    float m4[4] = {s[0], s[1], s[2], s[3]};  // 4 independent chains
 #pragma unroll
-                    for (int j = 1; j < KH; ++j) mx = fmaxf(mx, s[j]);
-                    mx *= p.scale_log2;
+                    for (int j = 4; j < KH; ++j) m4[j & 3] = fmaxf(m4[j & 3], s[j]);
+                    mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * p.scale_log2;
                 } else {
-                    mx = -INFINITY;
+                    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
                     for (int j = 0; j < KH; ++j) {
                         s[j] = (cb + j >= klo && cb + j <= khi) ? s[j] * p.scale_log2 : -INFINITY;
-                        mx = fmaxf(mx, s[j]);
+                        m4[j & 3] = fmaxf(m4[j & 3], s[j]);
                     }
+                    mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
                 }
+                SPROF(6);
                 red_max[st][half][r] = mx;
                 named_bar_sync(1, 256);
                 mx = fmaxf(mx, red_max[st][half ^ 1][r]);
+                SPROF(7);
                 // lazy rescale: keep the running max unless it grows by more than 8 (2^8)
                 float alpha = 1.f;
                 bool rescale = false;
@@ -307,14 +358,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < KH / 2; ++j) pk[j] = 0u;
                 } else if (full) {
                     const float sc = p.scale_log2, nm = -m;
+                    float rs2[2] = {0.f, 0.f};
 #pragma unroll
                     for (int j = 0; j < KH / 2; ++j) {
-                        float a = ex2_approx(fmaf(s[2 * j], sc, nm));
-                        float c = ex2_approx(fmaf(s[2 * j + 1], sc, nm));
-                        rs += a + c;
+                        const float xa = fmaf(s[2 * j], sc, nm), xc = fmaf(s[2 * j + 1], sc, nm);
+                        // ~30% of the exponentials on the FMA pipe, the rest on MUFU
+                        const bool emu = (j % 3) == 2;
+                        float a = emu ? ex2_poly(xa) : ex2_approx(xa);
+                        float c = emu ? ex2_poly(xc) : ex2_approx(xc);
+                        rs2[j & 1] += a + c;
                         __nv_bfloat162 v = __floats2bfloat162_rn(a, c);
                         pk[j] = *reinterpret_cast<uint32_t*>(&v);
                     }
+                    rs = rs2[0] + rs2[1];
                 } else {
 #pragma unroll
                     for (int j = 0; j < KH / 2; ++j) {
@@ -325,8 +381,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 l = l * alpha + rs;  // this half's share of the row sum
+                SPROF(8);
                 // P buffer free and O stable once PV of the previous block completed
                 ptx::mbar_wait(p_empty, (g & 1) ^ 1);
+                SPROF(9);
                 ptx::tc_fence_after();
                 if (rescale && b > 0) {
 #pragma unroll 1
@@ -347,9 +405,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint4 v = make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
                     *reinterpret_cast<uint4*>(prow + ((cc ^ (r & 7)) << 4)) = v;
                 }
+                SPROF(10);
                 ptx::fence_proxy_async_smem();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(p_full);
+                SPROF(11);
+
             }
             // epilogue: O / l -> bf16 (each half stores HD/2 columns); the row sums are
             // exchanged through red_max[0] once both halves are past their last max exchange
@@ -416,6 +477,16 @@ void launch_tc(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, i
 }
 
 }  // namespace
+
+#ifdef SGC_ATTN_PROF
+void attn_prof_read(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, g_attn_prof, sizeof(unsigned long long) * 148 * 16);
+}
+void attn_prof_reset() {
+    static unsigned long long z[148 * 16] = {};
+    cudaMemcpyToSymbol(g_attn_prof, z, sizeof(z));
+}
+#endif
 
 bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, int hd, int q_rows,
                           int pfx_rows, int loc_rows) {

@@ -26,5 +26,7 @@ struct GemmEpi {
 };
 
 void gemm_bf16(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep);
+// use the CTA-pair (cta_group::2) kernel for 256-wide tiles when M >= 256 (default on)
+void gemm_set_pairs(bool on);
 
 }  // namespace sgc

@@ -80,6 +80,129 @@ __device__ __forceinline__ void rope_pair(float* lo, float* hi, const float* cos
     }
 }
 
+// Epilogue of one 128 x BN accumulator tile held in TMEM (lanes = rows): `tbase` addresses
+// this warp's 32 lanes at the tile's first column, `row` is this thread's output row.
+template <int BN, int EPI, int HD>
+__device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool valid, int n0,
+                                              const GemmEpi& ep) {
+            if constexpr (EPI == EPI_QKV) {
+        // one tile never straddles the q/k/v sections (d % BN == 0)
+        const int d = ep.d;
+        const int section = n0 / d;
+        const int c0 = n0 - section * d;
+        constexpr int HALF = HD / 2;
+        int pos = 0, kvr = 0;
+        if (valid) {
+            pos = ep.pos[row];
+            kvr = ep.kv_row[row];
+        }
+        if (section == 2) {
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 32; ++ch) {
+                uint32_t r[32];
+                ptx::tmem_ld32(tbase + ch * 32, r);
+                ptx::tmem_ld_wait();
+                if (valid)
+                    store_bf16x32(ep.v_cache + static_cast<size_t>(kvr) * d + c0 + ch * 32,
+                                  reinterpret_cast<float*>(r));
+            }
+        } else {
+            __nv_bfloat16* dst = section == 0
+                                     ? ep.q_out + static_cast<size_t>(row) * d
+                                     : ep.k_cache + static_cast<size_t>(kvr) * d;
+            const float* cosp = ep.rope_cos + static_cast<size_t>(pos) * HALF;
+            const float* sinp = ep.rope_sin + static_cast<size_t>(pos) * HALF;
+            if constexpr (HALF >= 32) {
+                // pairs span two chunks: (ch, ch + HALF/32) within each head
+#pragma unroll 1
+                for (int ch = 0; ch < BN / 32; ++ch) {
+                    const int in_head = (ch * 32) % HD;
+                    if (in_head >= HALF) continue;
+                    const int ch2 = ch + HALF / 32;
+                    uint32_t lo[32], hi[32];
+                    ptx::tmem_ld32(tbase + ch * 32, lo);
+                    ptx::tmem_ld32(tbase + ch2 * 32, hi);
+                    ptx::tmem_ld_wait();
+                    if (valid) {
+                        float cs[32], sn[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            cs[j] = __ldg(cosp + in_head + j);
+                            sn[j] = __ldg(sinp + in_head + j);
+                        }
+                        rope_pair(reinterpret_cast<float*>(lo), reinterpret_cast<float*>(hi),
+                                  cs, sn);
+                        store_bf16x32(dst + c0 + ch * 32, reinterpret_cast<float*>(lo));
+                        store_bf16x32(dst + c0 + ch2 * 32, reinterpret_cast<float*>(hi));
+                    }
+                }
+            } else {
+                // whole heads inside one 32-column chunk
+#pragma unroll 1
+                for (int ch = 0; ch < BN / 32; ++ch) {
+                    uint32_t r[32];
+                    ptx::tmem_ld32(tbase + ch * 32, r);
+                    ptx::tmem_ld_wait();
+                    if (valid) {
+                        float* v = reinterpret_cast<float*>(r);
+                        float o[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const int i = j % HD;
+                            if (i < HALF) {
+                                float c = __ldg(cosp + i), s = __ldg(sinp + i);
+                                float a = v[j], b = v[j + HALF];
+                                o[j] = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, s));
+                                o[j + HALF] = __fadd_rn(__fmul_rn(b, c), __fmul_rn(a, s));
+                            }
+                        }
+                        store_bf16x32(dst + c0 + ch * 32, o);
+                    }
+                }
+            }
+        }
+    } else {
+#pragma unroll 1
+        for (int ch = 0; ch < BN / 32; ++ch) {
+            uint32_t r[32];
+            ptx::tmem_ld32(tbase + ch * 32, r);
+            ptx::tmem_ld_wait();
+            if (!valid) continue;
+            float* v = reinterpret_cast<float*>(r);
+            const int col = n0 + ch * 32;
+            if constexpr (EPI == EPI_F32) {
+                float4* dst = reinterpret_cast<float4*>(
+                    static_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ldo + col);
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            } else if constexpr (EPI == EPI_BF16) {
+                store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) +
+                                  static_cast<size_t>(row) * ep.ldo + col,
+                              v);
+            } else if constexpr (EPI == EPI_TANH) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = tanh_fast(v[j]);
+                store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) +
+                                  static_cast<size_t>(row) * ep.ldo + col,
+                              v);
+            } else if constexpr (EPI == EPI_RESID) {
+                float4* dst = reinterpret_cast<float4*>(
+                    static_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ldo + col);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    float4 x = dst[q];
+                    x.x += v[4 * q];
+                    x.y += v[4 * q + 1];
+                    x.z += v[4 * q + 2];
+                    x.w += v[4 * q + 3];
+                    dst[q] = x;
+                }
+            }
+        }
+    }
+}
+
 template <int BN, int EPI, int HD>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -201,122 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool valid = row < M;
             const uint32_t tbase = tmem_base + ((ew * 32) << 16) + acc * BN;
 
-            if constexpr (EPI == EPI_QKV) {
-                // one tile never straddles the q/k/v sections (d % BN == 0)
-                const int d = ep.d;
-                const int section = n0 / d;
-                const int c0 = n0 - section * d;
-                constexpr int HALF = HD / 2;
-                int pos = 0, kvr = 0;
-                if (valid) {
-                    pos = ep.pos[row];
-                    kvr = ep.kv_row[row];
-                }
-                if (section == 2) {
-#pragma unroll 1
-                    for (int ch = 0; ch < BN / 32; ++ch) {
-                        uint32_t r[32];
-                        ptx::tmem_ld32(tbase + ch * 32, r);
-                        ptx::tmem_ld_wait();
-                        if (valid)
-                            store_bf16x32(ep.v_cache + static_cast<size_t>(kvr) * d + c0 + ch * 32,
-                                          reinterpret_cast<float*>(r));
-                    }
-                } else {
-                    __nv_bfloat16* dst = section == 0
-                                             ? ep.q_out + static_cast<size_t>(row) * d
-                                             : ep.k_cache + static_cast<size_t>(kvr) * d;
-                    const float* cosp = ep.rope_cos + static_cast<size_t>(pos) * HALF;
-                    const float* sinp = ep.rope_sin + static_cast<size_t>(pos) * HALF;
-                    if constexpr (HALF >= 32) {
-                        // pairs span two chunks: (ch, ch + HALF/32) within each head
-#pragma unroll 1
-                        for (int ch = 0; ch < BN / 32; ++ch) {
-                            const int in_head = (ch * 32) % HD;
-                            if (in_head >= HALF) continue;
-                            const int ch2 = ch + HALF / 32;
-                            uint32_t lo[32], hi[32];
-                            ptx::tmem_ld32(tbase + ch * 32, lo);
-                            ptx::tmem_ld32(tbase + ch2 * 32, hi);
-                            ptx::tmem_ld_wait();
-                            if (valid) {
-                                float cs[32], sn[32];
-#pragma unroll
-                                for (int j = 0; j < 32; ++j) {
-                                    cs[j] = __ldg(cosp + in_head + j);
-                                    sn[j] = __ldg(sinp + in_head + j);
-                                }
-                                rope_pair(reinterpret_cast<float*>(lo), reinterpret_cast<float*>(hi),
-                                          cs, sn);
-                                store_bf16x32(dst + c0 + ch * 32, reinterpret_cast<float*>(lo));
-                                store_bf16x32(dst + c0 + ch2 * 32, reinterpret_cast<float*>(hi));
-                            }
-                        }
-                    } else {
-                        // whole heads inside one 32-column chunk
-#pragma unroll 1
-                        for (int ch = 0; ch < BN / 32; ++ch) {
-                            uint32_t r[32];
-                            ptx::tmem_ld32(tbase + ch * 32, r);
-                            ptx::tmem_ld_wait();
-                            if (valid) {
-                                float* v = reinterpret_cast<float*>(r);
-                                float o[32];
-#pragma unroll
-                                for (int j = 0; j < 32; ++j) {
-                                    const int i = j % HD;
-                                    if (i < HALF) {
-                                        float c = __ldg(cosp + i), s = __ldg(sinp + i);
-                                        float a = v[j], b = v[j + HALF];
-                                        o[j] = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, s));
-                                        o[j + HALF] = __fadd_rn(__fmul_rn(b, c), __fmul_rn(a, s));
-                                    }
-                                }
-                                store_bf16x32(dst + c0 + ch * 32, o);
-                            }
-                        }
-                    }
-                }
-            } else {
-#pragma unroll 1
-                for (int ch = 0; ch < BN / 32; ++ch) {
-                    uint32_t r[32];
-                    ptx::tmem_ld32(tbase + ch * 32, r);
-                    ptx::tmem_ld_wait();
-                    if (!valid) continue;
-                    float* v = reinterpret_cast<float*>(r);
-                    const int col = n0 + ch * 32;
-                    if constexpr (EPI == EPI_F32) {
-                        float4* dst = reinterpret_cast<float4*>(
-                            static_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ldo + col);
-#pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                    } else if constexpr (EPI == EPI_BF16) {
-                        store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) +
-                                          static_cast<size_t>(row) * ep.ldo + col,
-                                      v);
-                    } else if constexpr (EPI == EPI_TANH) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] = tanh_fast(v[j]);
-                        store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) +
-                                          static_cast<size_t>(row) * ep.ldo + col,
-                                      v);
-                    } else if constexpr (EPI == EPI_RESID) {
-                        float4* dst = reinterpret_cast<float4*>(
-                            static_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ldo + col);
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            float4 x = dst[q];
-                            x.x += v[4 * q];
-                            x.y += v[4 * q + 1];
-                            x.z += v[4 * q + 2];
-                            x.w += v[4 * q + 3];
-                            dst[q] = x;
-                        }
-                    }
-                }
-            }
+            epilogue_tile<BN, EPI, HD>(tbase, row, valid, n0, ep);
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);
         }
@@ -326,6 +334,153 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+    }
+}
+
+// ---- CTA-pair variant (tcgen05.mma.cta_group::2) -------------------------------------------
+// A cluster of 2 CTAs computes a 256 x 256 tile: each CTA TMA-loads its 128 rows of A and its
+// 128 rows of B (half of N) into its own smem, the leader issues M=256 x N=256 MMAs that read
+// both CTAs' operands, and each CTA's TMEM receives its own 128 x 256 accumulator rows. Per CTA
+// this halves the B traffic of the 1-CTA 128 x 256 tile (32 KB instead of 48 KB per k-block).
+constexpr int kStages2 = 6;
+struct Cfg2 {
+    static constexpr int kABytes = BM * BK * 2;  // this CTA's 128 rows of A
+    static constexpr int kBBytes = BM * BK * 2;  // this CTA's 128 rows of B
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kSmem = kStages2 * kStageBytes + 1024 + 256;
+};
+
+template <int EPI, int HD>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 int M, int N, int K, GemmEpi ep) {
+    constexpr int BN = 256;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* smemA = smem;
+    uint8_t* smemB = smem + kStages2 * Cfg2::kABytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages2 * Cfg2::kStageBytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages2;
+    uint64_t* tfull = bars + 2 * kStages2;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int m_tiles = (M + 2 * BM - 1) / (2 * BM);
+    const int n_tiles = N / BN;
+    const int num_tiles = m_tiles * n_tiles;
+    const int num_kb = K / BK;
+    const int GROUP = 32;  // pair-tiles of 256 rows per raster group
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+        for (int s = 0; s < kStages2; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 2 * 128);  // both CTAs' epilogue threads release
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc_2sm<512>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();  // peer barriers initialized before any remote arrive / TMA signal
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    auto tile_coords = [&](int t, int& m0, int& n0) {
+        int per_group = GROUP * n_tiles;
+        int g = t / per_group;
+        int first_m = g * GROUP;
+        int gsize = min(GROUP, m_tiles - first_m);
+        int r = t % per_group;
+        m0 = (first_m + r % gsize) * 2 * BM;
+        n0 = (r / gsize) * BN;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = pair; t < num_tiles; t += npairs) {
+                int m0, n0;
+                tile_coords(t, m0, n0);
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) ptx::mbar_expect_tx(&full[stage], 2 * Cfg2::kStageBytes);
+                    ptx::tma_load_2d_2sm(smemA + stage * Cfg2::kABytes, &tmA, &full[stage], kb * BK,
+                                         m0 + rank * BM);
+                    ptx::tma_load_2d_2sm(smemB + stage * Cfg2::kBBytes, &tmB, &full[stage], kb * BK,
+                                         n0 + rank * BM);
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int t = pair; t < num_tiles; t += npairs, ++local) {
+                const int acc = local & 1;
+                const uint32_t acc_phase = (local >> 1) & 1;
+                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                for (int kb = 0; kb < num_kb; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = ptx::smem_u32(smemA + stage * Cfg2::kABytes);
+                    const uint32_t b_addr = ptx::smem_u32(smemB + stage * Cfg2::kBBytes);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        ptx::mma_bf16_2sm(tmem_d, ptx::umma_desc_sw128(a_addr + k * 32),
+                                          ptx::umma_desc_sw128(b_addr + k * 32), idesc, (kb | k) != 0);
+                    ptx::mma_commit_2sm(&empty[stage], 0x3);
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::mma_commit_2sm(&tfull[acc], 0x3);
+            }
+        }
+    } else if (warp >= 4) {
+        const int ew = warp - 4;
+        int local = 0;
+        for (int t = pair; t < num_tiles; t += npairs, ++local) {
+            int m0, n0;
+            tile_coords(t, m0, n0);
+            const int acc = local & 1;
+            const uint32_t acc_phase = (local >> 1) & 1;
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            const int row = m0 + static_cast<int>(rank) * BM + ew * 32 + lane;
+            const uint32_t tbase = tmem_base + ((ew * 32) << 16) + acc * BN;
+            epilogue_tile<BN, EPI, HD>(tbase, row, row < M, n0, ep);
+            ptx::tc_fence_before();
+            ptx::mbar_arrive_cluster(&tempty[acc], 0);
+        }
+    }
+
+    __syncthreads();
+    ptx::cluster_sync();  // neither CTA frees TMEM while the pair may still use it
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_2sm<512>(tmem_base);
     }
 }
 
@@ -350,16 +505,38 @@ void launch(Ctx* c, const void* A, const void* B, int M, int N, int K, const Gem
 }
 
 template <int EPI, int HD>
+void launch2(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
+    static bool attr_set = false;
+    auto kfn = gemm2_kernel<EPI, HD>;
+    if (!attr_set) {
+        SGC_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::kSmem));
+        attr_set = true;
+    }
+    CUtensorMap ta = make_map_2d(A, M, K, BM, BK);
+    CUtensorMap tb = make_map_2d(B, N, K, BM, BK);
+    int tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / 256);
+    int grid = 2 * tiles < c->num_sms ? 2 * tiles : (c->num_sms & ~1);
+    Ctx::Timed timer(c, "gemm");
+    kfn<<<grid, kThreads, Cfg2::kSmem, c->stream>>>(ta, tb, M, N, K, ep);
+    SGC_LAUNCH_CHECK(c);
+}
+
+bool g_gemm_pairs = true;  // CTA-pair kernel for large tiles (sgc_set_gemm_pairs toggles)
+
+template <int EPI, int HD>
 void dispatch_bn(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
     // widest tile that divides N (and d, for the QKV section split)
     int lim = EPI == EPI_QKV ? ep.d : N;
-    if (N % 256 == 0 && lim % 256 == 0) launch<256, EPI, HD>(c, A, B, M, N, K, ep);
+    if (g_gemm_pairs && M >= 2 * BM && N % 256 == 0 && lim % 256 == 0) launch2<EPI, HD>(c, A, B, M, N, K, ep);
+    else if (N % 256 == 0 && lim % 256 == 0) launch<256, EPI, HD>(c, A, B, M, N, K, ep);
     else if (N % 128 == 0 && lim % 128 == 0) launch<128, EPI, HD>(c, A, B, M, N, K, ep);
     else if (N % 64 == 0 && lim % 64 == 0) launch<64, EPI, HD>(c, A, B, M, N, K, ep);
     else fail(SGC_DOMAIN, "gemm: N must be a multiple of 64");
 }
 
 }  // namespace
+
+void gemm_set_pairs(bool on) { g_gemm_pairs = on; }
 
 void gemm_bf16(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
     if (M <= 0) return;

@@ -72,6 +72,9 @@ class Context:
     def set_timing(self, enable: bool):
         check(self.lib.sgc_set_timing(self.h, int(enable)))
 
+    def set_option(self, name: str, value: int):
+        check(self.lib.sgc_set_option(self.h, name.encode(), int(value)))
+
     def kernel_time(self, name: str):
         ms, n = C.c_double(), C.c_uint64()
         check(self.lib.sgc_get_timing(self.h, name.encode(), C.byref(ms), C.byref(n)))

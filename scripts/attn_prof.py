@@ -1,0 +1,43 @@
+"""Phase breakdown of the tcgen05 attention kernel (debug library built with `make prof`).
+
+    SGC_LIB=paper_2505_10951_b200/libsgc_b200_prof.so python scripts/attn_prof.py
+"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2505_10951_b200 import _lib, host, workload as W  # noqa: E402
+
+NAMES = ["mma: wait v_full", "mma: wait p_full", "mma: wait k_full", "mma: wait s_empty",
+         "smx: wait s_full", "smx: tmem ld S", "smx: mask+max", "smx: max exchange",
+         "smx: exp+sum+pack", "smx: wait p_empty", "smx: rescale+P store", "smx: fence+arrive"]
+
+
+def main():
+    L = _lib.load()
+    L.sgc_debug_attn_prof.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
+    w = W.c3_workload()
+    ctx = host.Context(0)
+    lm = host.ToyLm(ctx, host.ToyLmConfig(**w.lm, seed=w.seed))
+    dg = host.DeviceGraph(ctx, w.graph)
+    pb = host.PreparedBatch(w)
+    host.run_subgcache(ctx, lm, dg, pb, waves=1, want_logits=False)
+    buf = np.zeros(148 * 16, np.uint64)
+    L.sgc_debug_attn_prof(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), 1)
+    ctx.set_timing(True)
+    host.run_subgcache(ctx, lm, dg, pb, waves=1, want_logits=False)
+    L.sgc_debug_attn_prof(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), 0)
+    ms, n = ctx.kernel_time("attention")
+    per = buf.reshape(148, 16).astype(np.float64).mean(0)
+    tot_mma = per[:4].sum()
+    print(f"attention {ms:.1f} ms over {n} launches; mean cycles per CTA (all launches):")
+    for i, nm in enumerate(NAMES):
+        print(f"  {nm:26s} {per[i] / 1e6:10.2f} Mcyc")
+    print(f"  sum softmax phases         {per[4:12].sum() / 1e6:10.2f} Mcyc; mma waits {tot_mma / 1e6:.2f} Mcyc")
+
+
+if __name__ == "__main__":
+    main()

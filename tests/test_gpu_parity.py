@@ -52,7 +52,8 @@ def check_logits(got, ref, tol=LOGIT_TOL):
 @pytest.mark.parametrize("M,N,K", [(1, 64, 64), (100, 128, 128), (128, 256, 256), (300, 768, 512),
                                    (1000, 256, 4096), (129, 192, 64), (2048, 1024, 1024)])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
-def test_gemm_tcgen05_vs_torch(ctx, M, N, K, epi):
+@pytest.mark.parametrize("pairs", [1, 0])
+def test_gemm_tcgen05_vs_torch(ctx, M, N, K, epi, pairs):
     torch = pytest.importorskip("torch")
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
     a = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
@@ -69,7 +70,9 @@ def test_gemm_tcgen05_vs_torch(ctx, M, N, K, epi):
         d = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
     if epi == 3:
         ref = torch.tanh(ref)
+    ctx.set_option("gemm_pairs", pairs)
     ctx.gemm(a.data_ptr(), b.data_ptr(), d.data_ptr(), M, N, K, epi)
+    ctx.set_option("gemm_pairs", 1)
     got = d.float()
     tol = 2e-2 if epi in (1, 3) else 1e-3 * max(1.0, (K / 64) ** 0.5)
     rel = (got - ref).abs().max().item() / max(1.0, ref.abs().max().item())
