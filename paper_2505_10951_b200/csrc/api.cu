@@ -662,10 +662,15 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
         uniq_of[i] = found;
     }
     const uint32_t nu = static_cast<uint32_t>(uniq_first.size());
-    std::vector<uint32_t> inst_feat, sub_inst_off(1, 0), in_off(1, 0), in_src, in_gate;
+    // node instances of the unique subgraphs with their in-edges (ascending edge index,
+    // encoders.cpp:142-162), then per-layer signature dedup: an instance's state after layer
+    // l+1 is a function of (its state after l, [(edge, source state after l)] in ascending edge
+    // order), so instances with equal signatures share one computed state -- bit-identically
+    std::vector<uint32_t> inst_node, sub_off(1, 0);
+    std::vector<std::vector<std::pair<uint32_t, uint32_t>>> inst_in;  // (edge, src instance)
     for (uint32_t u = 0; u < nu; ++u) {
         uint32_t i = uniq_first[u];
-        const uint32_t base = static_cast<uint32_t>(inst_feat.size());
+        const uint32_t base = static_cast<uint32_t>(inst_node.size());
         const uint64_t n0 = hs.noff[i], n1 = hs.noff[i + 1];
         std::vector<uint32_t> local_dense;
         for (uint64_t k = n0; k < n1; ++k) {
@@ -673,10 +678,9 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
                 fail(SGC_DOMAIN, "subgraph node ids must be ascending and unique");
             uint32_t di = dense_index(g, hs.nodes[k]);
             local_dense.push_back(di);
-            inst_feat.push_back(di);
+            inst_node.push_back(di);
         }
-        // in-edges per destination, ascending edge index (encoders.cpp:142-162)
-        std::vector<std::vector<std::pair<uint32_t, uint32_t>>> in(n1 - n0);
+        inst_in.resize(inst_node.size());
         for (uint64_t k = hs.eoff[i]; k < hs.eoff[i + 1]; ++k) {
             uint32_t e = hs.edges[k];
             if (e >= g->n_edges) fail(SGC_INTEGRITY, "subgraph edge index " + std::to_string(e) + " out of range");
@@ -685,52 +689,104 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
             if (ls == local_dense.end() || *ls != g->edge_src_idx[e] || ld == local_dense.end() ||
                 *ld != g->edge_dst_idx[e])
                 fail(SGC_INTEGRITY, "subgraph edge " + std::to_string(e) + " violates closure: endpoint missing");
-            in[ld - local_dense.begin()].push_back({base + static_cast<uint32_t>(ls - local_dense.begin()),
-                                                    g->n_nodes + e});
+            inst_in[base + (ld - local_dense.begin())].push_back({e, base + static_cast<uint32_t>(ls - local_dense.begin())});
         }
-        for (auto& lst : in) {
-            for (auto& pr : lst) {
-                in_src.push_back(pr.first);
-                in_gate.push_back(pr.second);
-            }
-            in_off.push_back(static_cast<uint32_t>(in_src.size()));
-        }
-        sub_inst_off.push_back(static_cast<uint32_t>(inst_feat.size()));
+        sub_off.push_back(static_cast<uint32_t>(inst_node.size()));
     }
-    const int n_inst = static_cast<int>(inst_feat.size());
-    sgc::GnnBatch b;
-    b.layers = static_cast<int>(cfg.layers);
-    b.heads = static_cast<int>(cfg.heads);
-    b.d = d;
-    b.n_inst = n_inst;
-    b.n_sub = static_cast<int>(nu);
-    uint32_t* d_if = c->buf<uint32_t>("gnn_inst_feat", n_inst);
-    uint32_t* d_io = c->buf<uint32_t>("gnn_in_off", in_off.size());
-    uint32_t* d_is = c->buf<uint32_t>("gnn_in_src", in_src.size());
-    uint32_t* d_ig = c->buf<uint32_t>("gnn_in_gate", in_gate.size());
-    uint32_t* d_so = c->buf<uint32_t>("gnn_sub_off", sub_inst_off.size());
-    sgc::copy_in(c, d_if, inst_feat.data(), inst_feat.size());
-    sgc::copy_in(c, d_io, in_off.data(), in_off.size());
-    sgc::copy_in(c, d_is, in_src.data(), in_src.size());
-    sgc::copy_in(c, d_ig, in_gate.data(), in_gate.size());
-    sgc::copy_in(c, d_so, sub_inst_off.data(), sub_inst_off.size());
-    b.inst_feat = d_if;
-    b.in_off = d_io;
-    b.in_src = d_is;
-    b.in_gate = d_ig;
-    b.sub_inst_off = d_so;
-    b.feat = feat;
-    b.wbar = es.wbar;
-    b.state = c->buf<double>("gnn_state", static_cast<size_t>(n_inst) * d);
-    b.agg = c->buf<double>("gnn_agg", static_cast<size_t>(n_inst) * d);
+    const size_t n_inst = inst_node.size();
+    struct KeyHash {
+        size_t operator()(const std::vector<uint32_t>& v) const {
+            uint64_t h = 0x9e3779b97f4a7c15ULL;
+            for (uint32_t x : v) h = sgc::mix64(h ^ x);
+            return static_cast<size_t>(h);
+        }
+    };
+    // layer 0 groups = distinct nodes
+    std::vector<uint32_t> gid(n_inst), g0_node;
+    {
+        std::unordered_map<uint32_t, uint32_t> m0;
+        for (size_t v = 0; v < n_inst; ++v) {
+            auto it = m0.find(inst_node[v]);
+            if (it == m0.end()) {
+                it = m0.emplace(inst_node[v], static_cast<uint32_t>(g0_node.size())).first;
+                g0_node.push_back(inst_node[v]);
+            }
+            gid[v] = it->second;
+        }
+    }
+    struct LayerHost {
+        std::vector<uint32_t> self_row, in_off{0}, in_src, in_gate;
+    };
+    std::vector<LayerHost> lh(cfg.layers);
+    size_t max_groups = g0_node.size();
+    for (uint32_t l = 0; l < cfg.layers; ++l) {
+        std::unordered_map<std::vector<uint32_t>, uint32_t, KeyHash> groups;
+        std::vector<uint32_t> next(n_inst);
+        LayerHost& L = lh[l];
+        std::vector<uint32_t> key;
+        for (size_t v = 0; v < n_inst; ++v) {
+            key.assign(1, gid[v]);
+            for (auto& pr : inst_in[v]) {
+                key.push_back(pr.first);
+                key.push_back(gid[pr.second]);
+            }
+            auto it = groups.find(key);
+            if (it == groups.end()) {
+                uint32_t ng = static_cast<uint32_t>(L.self_row.size());
+                it = groups.emplace(key, ng).first;
+                L.self_row.push_back(gid[v]);
+                for (auto& pr : inst_in[v]) {
+                    L.in_src.push_back(gid[pr.second]);
+                    L.in_gate.push_back(g->n_nodes + pr.first);
+                }
+                L.in_off.push_back(static_cast<uint32_t>(L.in_src.size()));
+            }
+            next[v] = it->second;
+        }
+        gid.swap(next);
+        max_groups = std::max(max_groups, L.self_row.size());
+    }
+    sgc::GnnPlan p{};
+    p.layers = static_cast<int>(cfg.layers);
+    p.heads = static_cast<int>(cfg.heads);
+    p.d = d;
+    p.n0 = static_cast<int>(g0_node.size());
+    uint32_t* d_g0 = c->buf<uint32_t>("gnn_g0", g0_node.size());
+    sgc::copy_in(c, d_g0, g0_node.data(), g0_node.size());
+    p.g0_node = d_g0;
+    if (cfg.layers > 8) fail(SGC_DOMAIN, "gnn encoder supports at most 8 layers on this backend");
+    for (uint32_t l = 0; l < cfg.layers; ++l) {
+        LayerHost& L = lh[l];
+        const std::string t = "gnn_l" + std::to_string(l);
+        uint32_t* sr = c->buf<uint32_t>(t + "_self", L.self_row.size());
+        uint32_t* io = c->buf<uint32_t>(t + "_off", L.in_off.size());
+        uint32_t* is = c->buf<uint32_t>(t + "_src", L.in_src.size());
+        uint32_t* ig = c->buf<uint32_t>(t + "_gate", L.in_gate.size());
+        sgc::copy_in(c, sr, L.self_row.data(), L.self_row.size());
+        sgc::copy_in(c, io, L.in_off.data(), L.in_off.size());
+        sgc::copy_in(c, is, L.in_src.data(), L.in_src.size());
+        sgc::copy_in(c, ig, L.in_gate.data(), L.in_gate.size());
+        p.layer[l] = {static_cast<int>(L.self_row.size()), sr, io, is, ig};
+    }
+    p.n_sub = static_cast<int>(nu);
+    uint32_t* d_so = c->buf<uint32_t>("gnn_sub_off", sub_off.size());
+    uint32_t* d_sr = c->buf<uint32_t>("gnn_sub_rows", gid.size());
+    sgc::copy_in(c, d_so, sub_off.data(), sub_off.size());
+    sgc::copy_in(c, d_sr, gid.data(), gid.size());
+    p.sub_off = d_so;
+    p.sub_rows = d_sr;
+    p.feat = feat;
+    p.wbar = es.wbar;
+    p.state[0] = c->buf<double>("gnn_state0", max_groups * d);
+    p.state[1] = c->buf<double>("gnn_state1", max_groups * d);
+    p.agg = c->buf<double>("gnn_agg", max_groups * d);
     float* uniq_out = c->buf<float>("gnn_uniq_out", static_cast<size_t>(nu) * d);
-    b.out = uniq_out;
-    sgc::gnn_encode_batch(c, b);
-    // scatter unique embeddings to every subgraph
-    for (uint32_t i = 0; i < count; ++i)
-        SGC_CUDA_CHECK(cudaMemcpyAsync(out_dev + static_cast<size_t>(i) * d,
-                                       uniq_out + static_cast<size_t>(uniq_of[i]) * d, d * sizeof(float),
-                                       cudaMemcpyDeviceToDevice, c->stream));
+    p.out = uniq_out;
+    sgc::gnn_encode_layers(c, p);
+    // unique subgraph embeddings -> every subgraph
+    uint32_t* d_uo = c->buf<uint32_t>("gnn_uniq_of", count);
+    sgc::copy_in(c, d_uo, uniq_of.data(), count);
+    sgc::gather_rows(c, out_dev, uniq_out, d_uo, static_cast<int>(count), d);
     c->sync();
 }
 

@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int num_kb = K / BK;
     // grouped raster: GROUP m-tiles sweep all n-tiles before moving on, so both the
     // activation rows and the weight tiles of the concurrently running CTAs stay in L2
-    const int GROUP = 64;
+    const int GROUP = max(4, min(64, (48 << 20) / (BM * K * 2)));
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);
@@ -375,7 +375,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int n_tiles = N / BN;
     const int num_tiles = m_tiles * n_tiles;
     const int num_kb = K / BK;
-    const int GROUP = 32;  // pair-tiles of 256 rows per raster group
+    // pair-tiles of 256 rows per raster group: the group's A rows (GROUP x 256 x K bf16) stay
+    // L2-resident (~48 MB) while the group sweeps every n-tile; larger K -> smaller group
+    const int GROUP = max(2, min(32, (48 << 20) / (2 * BM * K * 2)));
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);

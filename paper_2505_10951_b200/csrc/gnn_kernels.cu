@@ -1,7 +1,9 @@
-// gnn_kernels.cu -- GnnEncoder::encode (encoders.cpp:106-186) batched over all node instances
-// of all (deduplicated) subgraphs, in fp64.
+// gnn_kernels.cu -- GnnEncoder::encode (encoders.cpp:106-186) batched over all subgraphs of a
+// batch, in fp64, over UNIQUE node states: the host plan (api.cu encode_subgraphs) groups node
+// instances whose layer-l in-neighbourhood signatures agree, so each distinct state is computed
+// once (C3: 18.5k instances -> 0.9k..2.3k states per layer) and results stay bit-identical.
 //
-//   aggregate : agg[v] = (s[v] + sum_{e: src->v, ascending e} s[src] * gate_e) * (1/fanin)
+//   aggregate : agg[g] = (s[self] + sum_{e: src->v, ascending e} s[src] * gate_e) * (1/fanin)
 //               -- same operand order as the reference, mul/add rounded separately
 //   layer map : s'[v] = tanh((Wbar . agg[v]) / heads), Wbar = sum_h W_h folded once in fp64
 //               (register-tiled DFMA GEMM over [instances x dim] . [dim x dim]^T)
@@ -29,15 +31,17 @@ __global__ void gen_wbar_kernel(double* wbar, int layers, int heads, int d, uint
     }
 }
 
-// one CTA per node instance; threads over the feature dim
-__global__ void gnn_aggregate_kernel(double* agg, const double* state, const uint32_t* in_off,
-                                     const uint32_t* in_src, const uint32_t* in_gate,
-                                     const float* feat, int d) {
+// one CTA per output group; threads over the feature dim. The group's self row and in-edge
+// list (ascending edge index) index the previous layer's unique states.
+__global__ void gnn_aggregate_kernel(double* agg, const double* state, const uint32_t* self_row,
+                                     const uint32_t* in_off, const uint32_t* in_src,
+                                     const uint32_t* in_gate, const float* feat, int d) {
     const int v = blockIdx.x;
     const uint32_t e0 = in_off[v], e1 = in_off[v + 1];
     const double inv = __ddiv_rn(1.0, static_cast<double>(1 + (e1 - e0)));
+    const size_t self = self_row[v];
     for (int k = threadIdx.x; k < d; k += blockDim.x) {
-        double a = state[static_cast<size_t>(v) * d + k];
+        double a = state[self * d + k];
         for (uint32_t e = e0; e < e1; ++e) {
             double s = state[static_cast<size_t>(in_src[e]) * d + k];
             double g = static_cast<double>(feat[static_cast<size_t>(in_gate[e]) * d + k]);
@@ -99,17 +103,18 @@ __global__ void __launch_bounds__(256)
         }
 }
 
-// mean-pool (ascending instance order), sequential L2 norm, cast (encoders.cpp:170-185)
-__global__ void gnn_pool_kernel(float* out, const double* state, const uint32_t* sub_inst_off,
-                                int d) {
+// mean-pool over the subgraph's node states (ascending node id), sequential L2 norm, cast
+// (encoders.cpp:170-185); rows index the last layer's unique states
+__global__ void gnn_pool_kernel(float* out, const double* state, const uint32_t* sub_off,
+                                const uint32_t* rows, int d) {
     extern __shared__ double pooled[];
     __shared__ double norm_s;
     const int u = blockIdx.x;
-    const uint32_t v0 = sub_inst_off[u], v1 = sub_inst_off[u + 1];
+    const uint32_t v0 = sub_off[u], v1 = sub_off[u + 1];
     const double inv_n = __ddiv_rn(1.0, static_cast<double>(v1 - v0));
     for (int k = threadIdx.x; k < d; k += blockDim.x) {
         double p = 0.0;
-        for (uint32_t v = v0; v < v1; ++v) p = __dadd_rn(p, state[static_cast<size_t>(v) * d + k]);
+        for (uint32_t v = v0; v < v1; ++v) p = __dadd_rn(p, state[static_cast<size_t>(rows[v]) * d + k]);
         pooled[k] = __dmul_rn(p, inv_n);
     }
     __syncthreads();
@@ -124,6 +129,12 @@ __global__ void gnn_pool_kernel(float* out, const double* state, const uint32_t*
         out[static_cast<size_t>(u) * d + k] = nrm > 0.0 ? static_cast<float>(__ddiv_rn(pooled[k], nrm)) : 0.0f;
 }
 
+__global__ void gather_rows_kernel(float* out, const float* src, const uint32_t* idx, int d) {
+    const int i = blockIdx.x;
+    const float* s = src + static_cast<size_t>(idx[i]) * d;
+    for (int k = threadIdx.x; k < d; k += blockDim.x) out[static_cast<size_t>(i) * d + k] = s[k];
+}
+
 }  // namespace
 
 void gnn_gen_wbar(Ctx* c, double* wbar, int layers, int heads, int d, uint64_t state0, float scale) {
@@ -133,31 +144,40 @@ void gnn_gen_wbar(Ctx* c, double* wbar, int layers, int heads, int d, uint64_t s
     SGC_LAUNCH_CHECK(c);
 }
 
-void gnn_encode_batch(Ctx* c, const GnnBatch& b) {
-    const int d = b.d;
+void gnn_encode_layers(Ctx* c, const GnnPlan& p) {
+    const int d = p.d;
+    const int threads = d >= 256 ? 256 : 64;
     Ctx::Timed timer(c, "gnn_encode");
     {
-        uint64_t n = static_cast<uint64_t>(b.n_inst) * d;
+        uint64_t n = static_cast<uint64_t>(p.n0) * d;
         unsigned g = ceil_div(n, 256);
-        gnn_init_kernel<<<g < 8192 ? g : 8192, 256, 0, c->stream>>>(b.state, b.inst_feat, b.feat, b.n_inst, d);
+        gnn_init_kernel<<<g < 8192 ? g : 8192, 256, 0, c->stream>>>(p.state[0], p.g0_node, p.feat, p.n0, d);
         SGC_LAUNCH_CHECK(c);
     }
-    const int threads = d >= 256 ? 256 : 64;
-    for (int l = 0; l < b.layers; ++l) {
-        gnn_aggregate_kernel<<<b.n_inst, threads, 0, c->stream>>>(b.agg, b.state, b.in_off, b.in_src,
-                                                                  b.in_gate, b.feat, d);
+    for (int l = 0; l < p.layers; ++l) {
+        const GnnLayerPlan& L = p.layer[l];
+        double* prev = p.state[l & 1];
+        double* next = p.state[(l + 1) & 1];
+        gnn_aggregate_kernel<<<L.n_out, threads, 0, c->stream>>>(p.agg, prev, L.self_row, L.in_off, L.in_src,
+                                                                 L.in_gate, p.feat, d);
         SGC_LAUNCH_CHECK(c);
-        dim3 grid(ceil_div(b.n_inst, GM), ceil_div(d, GN));
-        gnn_layer_gemm<<<grid, 256, 0, c->stream>>>(b.state, b.agg,
-                                                     b.wbar + static_cast<size_t>(l) * d * d, b.n_inst,
-                                                     d, 1.0 / b.heads);
+        dim3 grid(ceil_div(L.n_out, GM), ceil_div(d, GN));
+        gnn_layer_gemm<<<grid, 256, 0, c->stream>>>(next, p.agg, p.wbar + static_cast<size_t>(l) * d * d,
+                                                     L.n_out, d, 1.0 / p.heads);
         SGC_LAUNCH_CHECK(c);
     }
     size_t smem = static_cast<size_t>(d) * sizeof(double);
     if (smem > 48 * 1024)
         SGC_CUDA_CHECK(cudaFuncSetAttribute(gnn_pool_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             static_cast<int>(smem)));
-    gnn_pool_kernel<<<b.n_sub, threads, smem, c->stream>>>(b.out, b.state, b.sub_inst_off, d);
+    gnn_pool_kernel<<<p.n_sub, threads, smem, c->stream>>>(p.out, p.state[p.layers & 1], p.sub_off,
+                                                          p.sub_rows, d);
+    SGC_LAUNCH_CHECK(c);
+}
+
+void gather_rows(Ctx* c, float* out, const float* src, const uint32_t* idx, int n, int d) {
+    if (n <= 0) return;
+    gather_rows_kernel<<<n, d >= 256 ? 256 : 64, 0, c->stream>>>(out, src, idx, d);
     SGC_LAUNCH_CHECK(c);
 }
 
