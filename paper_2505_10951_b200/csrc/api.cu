@@ -276,7 +276,7 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
 
 // tiles of <= 64 rows that never cross a `group` boundary (sequence for prefill, segment
 // for extend); rows of one group are contiguous
-int attn_tile(int hd) { return sgc::attention_tc_supported(hd) ? 128 : 64; }
+int attn_tile(int hd) { return sgc::attention_tc_supported(hd) ? 256 : 64; }
 
 std::vector<sgc::AttnWork> make_work(const std::vector<int>& group_start, const std::vector<int>& group_rows,
                                      const std::vector<int>& pfx_kv0, const std::vector<int>& pfx_len,

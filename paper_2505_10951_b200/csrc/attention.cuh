@@ -29,7 +29,8 @@ struct AttnParams {
 };
 
 void cascade_attention(Ctx* c, const AttnParams& p, int n_work, int heads, int hd);
-// tcgen05 version (attention_sm100.cu): tiles of <= 128 rows; head_dim 64 or 128. Returns
+// tcgen05 version (attention_sm100.cu): units of <= 256 rows (two 128-row tiles); head_dim 64
+// or 128. Returns
 // false when the shape is not supported by it.
 bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, int hd, int q_rows,
                           int pfx_rows, int loc_rows);

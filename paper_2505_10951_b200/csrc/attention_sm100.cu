@@ -1,24 +1,29 @@
 // attention_sm100.cu -- tcgen05/TMEM/TMA cascade attention for sm_100a (head_dim 64 / 128).
 //
 // Same semantics as attention.cu (lm_core.cpp:246-274: one softmax over the sealed prefix keys
-// followed by the row's own causal suffix keys), re-laid out for the 5th-gen tensor cores:
+// followed by the row's own causal suffix keys), laid out for the 5th-gen tensor cores in the
+// FlashAttention-4 style: one work unit = two 128-row query tiles (A, B) of ONE cluster and one
+// head, so every K/V block fetched serves 256 member rows, and the two tiles ping-pong on the
+// tensor core while the other tile's softmax runs:
 //
-//   warp 0      TMA loader: Q tile (128 rows) once per item and K blocks (128 keys) of the
-//               cluster's prefix (phase A) then of the batch's own rows (phase B), 3-stage ring
-//               released as soon as S = Q K^T has consumed a slot
-//   warp 3      TMA loader for the V blocks, 2-stage ring released after O += P V
-//   warp 1      MMA issuer (one thread): S_b = Q K_b^T into a double-buffered TMEM S, and
-//               O += P_{b-1} V_{b-1} into TMEM O (P from smem, V as an MN-major operand)
-//   warp 2      TMEM allocator (512 columns: S0 | S1 | O)
-//   warps 4..11 softmax, two warpgroups: thread (r, half) owns keys [64 half, 64 half + 64) of
-//               query row r (TMEM lane r) and O columns [HD/2 half, ...). Reads its S half-row
-//               from TMEM, masks, agrees on the row max with its partner through smem, online
-//               softmax in base 2 with lazy O rescale (only when the running max grows by > 2^8),
-//               writes its P half-row (bf16, 128B-swizzled) for the PV MMA, and at the end
-//               normalizes and stores its half of the O row.
+//   warp 0      TMA: Q tiles (once per unit) and K blocks (128 keys) -- 3-stage ring released
+//               once both tiles' S = Q K^T have consumed a slot
+//   warp 3      TMA: V blocks -- 2-stage ring released after both O += P V
+//   warp 1      MMA issuer (one thread), per block j:
+//                 O_A += P_A(j) V_j ; S_A(j+1) = Q_A K_{j+1} ; O_B += P_B(j) V_j ; S_B(j+1) = ...
+//               S_X lives in TMEM; P_X (bf16) is written back over S_X's first 64 columns and
+//               consumed straight from TMEM by the PV MMA (A operand in TMEM, V MN-major in smem).
+//               tcgen05 ops of one thread execute in order, so S_X(j+1) never overwrites P_X(j)
+//               before PV_X(j) read it, and s_full_X(j+1) also certifies PV_X(j) completed.
+//   warp 2      TMEM allocator (512 columns: S_A | S_B | O_A | O_B)
+//   warps 4-7   softmax of tile A, warps 8-11 softmax of tile B: thread r owns query row r
+//               (TMEM lane r) -- two passes over its S row (max, then exp + pack + store P),
+//               online softmax in base 2 with lazy O rescale (only when the running max grows
+//               by > 2^8; done in place in TMEM, O is stable whenever S is ready), ~30% of the
+//               exponentials on the FMA pipe (MUFU offload), and the final O / l epilogue.
 //
-// The kernel is persistent: CTAs loop over (tile, head) items; a tile is <= 128 query rows of
-// one cluster, so the prefix K/V blocks are fetched once per tile for every member row in it.
+// Persistent: CTAs loop over (unit, head) items; units never straddle clusters (members) or
+// sequences (representative prefill).
 #include "attention.cuh"
 #include "common.cuh"
 #include "sm100_ptx.cuh"
@@ -27,40 +32,28 @@
 namespace sgc {
 namespace {
 
-constexpr int BQ = 128;   // query rows per item
+constexpr int BQ = 128;   // rows per query tile (two tiles per unit)
 constexpr int BKV = 128;  // keys per block
-constexpr int kThreads = 384;  // 4 control warps + 2 softmax warpgroups
+constexpr int kThreads = 384;
+constexpr int kKStages = 3;
+constexpr int kVStages = 2;
 
 template <int HD>
 struct TcCfg {
-    static constexpr int kSub = HD / 64;            // 64-element (128 B) swizzle sub-tiles
+    static constexpr int kSub = HD / 64;  // 64-element (128 B) swizzle sub-tiles
     static constexpr int kQBytes = BQ * HD * 2;
     static constexpr int kKBytes = BKV * HD * 2;
     static constexpr int kVBytes = BKV * HD * 2;
-    static constexpr int kPBytes = BQ * BKV * 2;
-    static constexpr int kKStages = 3;  // K slots are freed as soon as S = Q K^T completes
-    static constexpr int kVStages = 2;  // V slots are freed after O += P V
-    static constexpr int kRedBytes = 2 * 2 * BQ * 4;
-    static constexpr int kSmem = kQBytes + kPBytes + kKStages * kKBytes + kVStages * kVBytes +
-                                 kRedBytes + 256;
+    static constexpr int kSmem = 2 * kQBytes + kKStages * kKBytes + kVStages * kVBytes + 256;
     static constexpr uint32_t kTmemCols = 512;
-    static constexpr uint32_t kO = 256;             // TMEM column of the O accumulator
+    static constexpr uint32_t kS = 0;    // S_X at column X * 128
+    static constexpr uint32_t kO = 256;  // O_X at column 256 + X * 128
 };
 
 // Compile with -DSGC_ATTN_PROF to accumulate per-phase clock64() cycles into a global
 // [148][16] counter array (debug builds only; see scripts/attn_prof.py).
 #ifdef SGC_ATTN_PROF
 __device__ unsigned long long g_attn_prof[148 * 16];
-#define PROF_T0() long long _pt = clock64()
-#define PROF_ACC(slot)                                                             \
-    do {                                                                           \
-        long long _n = clock64();                                                  \
-        atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 16 + (slot)], (unsigned long long)(_n - _pt)); \
-        _pt = _n;                                                                  \
-    } while (0)
-#else
-#define PROF_T0()
-#define PROF_ACC(slot)
 #endif
 
 struct TcParams {
@@ -72,7 +65,6 @@ struct TcParams {
     float scale_log2;
 };
 
-// MUFU.EX2 without the denormal-range fixups of exp2f (inputs are <= 8; ex2(-inf) = +0)
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -91,16 +83,21 @@ __device__ __forceinline__ float ex2_poly(float x) {
     return __int_as_float(__float_as_int(p) + (e << 23));
 }
 
-__device__ __forceinline__ void named_bar_sync(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-__device__ __forceinline__ void item_blocks(const AttnWork& w, const int32_t* seg_lo, int& nA,
-                                            int& nB, int& loc_first) {
-    nA = (w.pfx_len + BKV - 1) / BKV;
-    loc_first = seg_lo[w.row0];
-    const int loc_last = w.row0 + w.nrows - 1;
-    nB = (loc_last - loc_first + BKV) / BKV;
+// blocks of one unit: prefix blocks nA (shared), total blocks per tile, first local key row
+struct UnitPlan {
+    int nA, nb[2], nrows[2], loc_first;
+};
+__device__ __forceinline__ UnitPlan plan_unit(const AttnWork& w, const int32_t* seg_lo) {
+    UnitPlan u;
+    u.nA = (w.pfx_len + BKV - 1) / BKV;
+    u.loc_first = seg_lo[w.row0];
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+        u.nrows[x] = min(BQ, max(0, w.nrows - x * BQ));
+        const int last = w.row0 + x * BQ + u.nrows[x] - 1;
+        u.nb[x] = u.nrows[x] > 0 ? u.nA + (last - u.loc_first + BKV) / BKV : 0;
+    }
+    return u;
 }
 
 template <int HD>
@@ -111,23 +108,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     using C = TcCfg<HD>;
     // all shared memory is dynamic (no static arrays), so the base is 1024-byte aligned
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* sQ = smem;
-    uint8_t* sP = sQ + C::kQBytes;
-    uint8_t* sK = sP + C::kPBytes;                       // [kKStages][BKV x HD]
-    uint8_t* sV = sK + C::kKStages * C::kKBytes;         // [kVStages][BKV x HD]
-    float (*red_max)[2][BQ] = reinterpret_cast<float (*)[2][BQ]>(sV + C::kVStages * C::kVBytes);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(red_max) + C::kRedBytes);
-    uint64_t* q_full = bars + 0;
-    uint64_t* q_empty = bars + 1;
-    uint64_t* k_full = bars + 2;    // [3]
-    uint64_t* k_empty = bars + 5;   // [3]
-    uint64_t* v_full = bars + 8;    // [2]
-    uint64_t* v_empty = bars + 10;  // [2]
-    uint64_t* s_full = bars + 12;   // [2]
-    uint64_t* s_empty = bars + 14;  // [2]
-    uint64_t* p_full = bars + 16;
-    uint64_t* p_empty = bars + 17;
-    uint64_t* o_full = bars + 18;
+    uint8_t* sQ = smem;                                  // [2][BQ x HD]
+    uint8_t* sK = sQ + 2 * C::kQBytes;                   // [kKStages][BKV x HD]
+    uint8_t* sV = sK + kKStages * C::kKBytes;            // [kVStages][BKV x HD]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVStages * C::kVBytes);
+    uint64_t* q_full = bars + 0;    // [2]
+    uint64_t* q_empty = bars + 2;   // [2]
+    uint64_t* k_full = bars + 4;    // [3]
+    uint64_t* k_empty = bars + 7;   // [3]
+    uint64_t* v_full = bars + 10;   // [2]
+    uint64_t* v_empty = bars + 12;  // [2]
+    uint64_t* s_full = bars + 14;   // [2] per tile
+    uint64_t* p_full = bars + 16;   // [2] per tile
+    uint64_t* o_full = bars + 18;   // [2] per tile
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -139,21 +132,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch_desc(&tmVp);
         ptx::tma_prefetch_desc(&tmKl);
         ptx::tma_prefetch_desc(&tmVl);
-        ptx::mbar_init(q_full, 1);
-        ptx::mbar_init(q_empty, 1);
-        for (int i = 0; i < C::kKStages; ++i) {
+        for (int i = 0; i < kKStages; ++i) {
             ptx::mbar_init(&k_full[i], 1);
             ptx::mbar_init(&k_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&q_full[i], 1);
+            ptx::mbar_init(&q_empty[i], 1);
             ptx::mbar_init(&v_full[i], 1);
             ptx::mbar_init(&v_empty[i], 1);
             ptx::mbar_init(&s_full[i], 1);
-            ptx::mbar_init(&s_empty[i], 256);
+            ptx::mbar_init(&p_full[i], 128);
+            ptx::mbar_init(&o_full[i], 1);
         }
-        ptx::mbar_init(p_full, 256);
-        ptx::mbar_init(p_empty, 1);
-        ptx::mbar_init(o_full, 1);
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -163,43 +154,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0 || warp == 3) {
-        // warp 0: Q + K loader (3-stage ring), warp 3: V loader (2-stage ring)
+        // warp 0: Q + K loader, warp 3: V loader
         if (lane == 0) {
             const bool kload = warp == 0;
-            uint32_t g = 0, it = 0;
-            for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+            uint32_t g = 0, qit[2] = {0, 0};
+            for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
                 const int h = item / p.n_work;
                 const AttnWork w = p.work[item % p.n_work];
-                int nA, nB, loc_first;
-                item_blocks(w, p.seg_lo, nA, nB, loc_first);
+                const UnitPlan u = plan_unit(w, p.seg_lo);
                 if (kload) {
-                    ptx::mbar_wait(q_empty, (it & 1) ^ 1);
-                    ptx::mbar_expect_tx(q_full, C::kQBytes);
 #pragma unroll
-                    for (int s = 0; s < C::kSub; ++s)
-                        ptx::tma_load_2d(sQ + s * (BQ * 128), &tmQ, q_full, h * HD + s * 64, w.row0);
-                }
-                for (int b = 0; b < nA + nB; ++b, ++g) {
-                    const bool pfx = b < nA;
-                    const int row = pfx ? w.pfx_kv0 + b * BKV : loc_first + (b - nA) * BKV;
-                    if (kload) {
-                        const int st = g % C::kKStages;
-                        ptx::mbar_wait(&k_empty[st], ((g / C::kKStages) & 1) ^ 1);
-                        ptx::mbar_expect_tx(&k_full[st], C::kKBytes);
-                        uint8_t* dst = sK + st * C::kKBytes;
+                    for (int x = 0; x < 2; ++x) {
+                        if (!u.nb[x]) continue;
+                        ptx::mbar_wait(&q_empty[x], (qit[x] & 1) ^ 1);
+                        ptx::mbar_expect_tx(&q_full[x], C::kQBytes);
 #pragma unroll
                         for (int s = 0; s < C::kSub; ++s)
-                            ptx::tma_load_2d(dst + s * (BKV * 128), pfx ? &tmKp : &tmKl, &k_full[st],
-                                             h * HD + s * 64, row);
+                            ptx::tma_load_2d(sQ + x * C::kQBytes + s * (BQ * 128), &tmQ, &q_full[x],
+                                             h * HD + s * 64, w.row0 + x * BQ);
+                        ++qit[x];
+                    }
+                }
+                const int nbu = max(u.nb[0], u.nb[1]);
+                for (int b = 0; b < nbu; ++b, ++g) {
+                    const bool pfx = b < u.nA;
+                    const int row = pfx ? w.pfx_kv0 + b * BKV : u.loc_first + (b - u.nA) * BKV;
+                    if (kload) {
+                        const int st = g % kKStages;
+                        ptx::mbar_wait(&k_empty[st], ((g / kKStages) & 1) ^ 1);
+                        ptx::mbar_expect_tx(&k_full[st], C::kKBytes);
+#pragma unroll
+                        for (int s = 0; s < C::kSub; ++s)
+                            ptx::tma_load_2d(sK + st * C::kKBytes + s * (BKV * 128), pfx ? &tmKp : &tmKl,
+                                             &k_full[st], h * HD + s * 64, row);
                     } else {
                         const int st = g & 1;
                         ptx::mbar_wait(&v_empty[st], ((g >> 1) & 1) ^ 1);
                         ptx::mbar_expect_tx(&v_full[st], C::kVBytes);
-                        uint8_t* dst = sV + st * C::kVBytes;
 #pragma unroll
                         for (int s = 0; s < C::kSub; ++s)
-                            ptx::tma_load_2d(dst + s * (BKV * 128), pfx ? &tmVp : &tmVl, &v_full[st],
-                                             h * HD + s * 64, row);
+                            ptx::tma_load_2d(sV + st * C::kVBytes + s * (BKV * 128), pfx ? &tmVp : &tmVl,
+                                             &v_full[st], h * HD + s * 64, row);
                     }
                 }
             }
@@ -208,82 +203,79 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             constexpr uint32_t idS = ptx::idesc_bf16_f32(BQ, BKV);
             constexpr uint32_t idO = ptx::idesc_bf16_f32_bmn(BQ, HD);
-            const uint32_t q_addr = ptx::smem_u32(sQ), p_addr = ptx::smem_u32(sP);
-            uint32_t g = 0, it = 0;
-            auto issue_pv = [&](uint32_t gb, bool first) {
-                PROF_T0();
-                ptx::mbar_wait(&v_full[gb & 1], (gb >> 1) & 1);
-                PROF_ACC(0);
-                ptx::mbar_wait(p_full, gb & 1);
-                PROF_ACC(1);
+            uint32_t g = 0, gx[2] = {0, 0}, qit[2] = {0, 0};
+            auto issue_s = [&](int x, uint32_t kg) {  // S_X = Q_X K^T
+                const uint32_t q_addr = ptx::smem_u32(sQ + x * C::kQBytes);
+                const uint32_t k_addr = ptx::smem_u32(sK + (kg % kKStages) * C::kKBytes);
+#pragma unroll
+                for (int kc = 0; kc < HD / 16; ++kc) {
+                    uint64_t ad = ptx::umma_desc_sw128(q_addr + (kc / 4) * (BQ * 128) + (kc % 4) * 32);
+                    uint64_t bd = ptx::umma_desc_sw128(k_addr + (kc / 4) * (BKV * 128) + (kc % 4) * 32);
+                    ptx::mma_bf16(tmem_base + C::kS + x * BQ, ad, bd, idS, kc > 0 ? 1u : 0u);
+                }
+                ptx::mma_commit(&s_full[x]);
+            };
+            auto issue_pv = [&](int x, uint32_t kg, bool first) {  // O_X += P_X V
+                ptx::mbar_wait(&p_full[x], gx[x] & 1);
                 ptx::tc_fence_after();
-                const uint32_t v_addr = ptx::smem_u32(sV + (gb & 1) * C::kVBytes);
+                const uint32_t v_addr = ptx::smem_u32(sV + (kg & 1) * C::kVBytes);
 #pragma unroll
                 for (int kk = 0; kk < BKV / 16; ++kk) {
-                    uint64_t ad = ptx::umma_desc_sw128(p_addr + (kk / 4) * (BQ * 128) + (kk % 4) * 32);
                     uint64_t bd = ptx::umma_desc_sw128_lbo(v_addr + kk * 16 * 128, BKV * 128, 1024);
-                    ptx::mma_bf16(tmem_base + C::kO, ad, bd, idO, (!first || kk > 0) ? 1u : 0u);
+                    ptx::mma_bf16_ts(tmem_base + C::kO + x * 128, tmem_base + C::kS + x * BQ + kk * 8, bd,
+                                     idO, (!first || kk > 0) ? 1u : 0u);
                 }
-                ptx::mma_commit(&v_empty[gb & 1]);
-                ptx::mma_commit(p_empty);
+                ++gx[x];
             };
-            for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
+            for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
                 const AttnWork w = p.work[item % p.n_work];
-                int nA, nB, loc_first;
-                item_blocks(w, p.seg_lo, nA, nB, loc_first);
-                const int nb = nA + nB;
-                ptx::mbar_wait(q_full, it & 1);
-                for (int b = 0; b < nb; ++b, ++g) {
-                    const int st = g & 1;
-                    const int ks = g % C::kKStages;
-                    PROF_T0();
-                    ptx::mbar_wait(&k_full[ks], (g / C::kKStages) & 1);
-                    PROF_ACC(2);
-                    ptx::mbar_wait(&s_empty[st], ((g >> 1) & 1) ^ 1);
-                    PROF_ACC(3);
-                    ptx::tc_fence_after();
-                    const uint32_t k_addr = ptx::smem_u32(sK + ks * C::kKBytes);
-#pragma unroll
-                    for (int kc = 0; kc < HD / 16; ++kc) {
-                        uint64_t ad = ptx::umma_desc_sw128(q_addr + (kc / 4) * (BQ * 128) + (kc % 4) * 32);
-                        uint64_t bd = ptx::umma_desc_sw128(k_addr + (kc / 4) * (BKV * 128) + (kc % 4) * 32);
-                        ptx::mma_bf16(tmem_base + st * BKV, ad, bd, idS, kc > 0 ? 1u : 0u);
+                const UnitPlan u = plan_unit(w, p.seg_lo);
+                const int nbu = max(u.nb[0], u.nb[1]);
+                for (int x = 0; x < 2; ++x)
+                    if (u.nb[x]) ptx::mbar_wait(&q_full[x], qit[x] & 1);
+                // prologue: S(0) of both tiles
+                ptx::mbar_wait(&k_full[g % kKStages], (g / kKStages) & 1);
+                ptx::tc_fence_after();
+                for (int x = 0; x < 2; ++x)
+                    if (u.nb[x]) issue_s(x, g);
+                ptx::mma_commit(&k_empty[g % kKStages]);
+                for (int j = 0; j < nbu; ++j) {
+                    const uint32_t kg = g + j;
+                    ptx::mbar_wait(&v_full[kg & 1], (kg >> 1) & 1);
+                    bool waited_next_k = false;
+                    for (int x = 0; x < 2; ++x) {
+                        if (j >= u.nb[x]) continue;
+                        issue_pv(x, kg, j == 0);
+                        if (j + 1 < u.nb[x]) {
+                            if (!waited_next_k) {
+                                ptx::mbar_wait(&k_full[(kg + 1) % kKStages], ((kg + 1) / kKStages) & 1);
+                                ptx::tc_fence_after();
+                                waited_next_k = true;
+                            }
+                            issue_s(x, kg + 1);
+                        } else {
+                            ptx::mma_commit(&o_full[x]);
+                            ptx::mma_commit(&q_empty[x]);
+                        }
                     }
-                    ptx::mma_commit(&s_full[st]);
-                    ptx::mma_commit(&k_empty[ks]);
-                    if (b == nb - 1) ptx::mma_commit(q_empty);
-                    if (b >= 1) issue_pv(g - 1, b - 1 == 0);
+                    ptx::mma_commit(&v_empty[kg & 1]);
+                    if (j + 1 < nbu) ptx::mma_commit(&k_empty[(kg + 1) % kKStages]);
                 }
-                issue_pv(g - 1, nb == 1);
-                ptx::mma_commit(o_full);
+                g += nbu;
+                for (int x = 0; x < 2; ++x)
+                    if (u.nb[x]) ++qit[x];
             }
         }
     } else if (warp >= 4) {
-        // two softmax warpgroups split each row's 128 keys (and O's HD columns) in halves;
-        // thread pairs (r, half 0/1) agree on the row max through smem once per block
-        const int half = (warp - 4) >> 2;
-        const int r = (threadIdx.x - 128) & (BQ - 1);  // query row within the tile == TMEM lane
+        const int x = (warp - 4) >> 2;                  // query tile handled by this warpgroup
+        const int r = (threadIdx.x - 128) & (BQ - 1);   // row within the tile == TMEM lane
         const uint32_t lane_base = static_cast<uint32_t>(((warp - 4) & 3) * 32) << 16;
-        constexpr int KH = BKV / 2;  // keys per thread
-        constexpr int OH = HD / 2;   // O columns per thread
-        uint32_t g = 0, it = 0;
-        // P row r inside the swizzled [128 x 128] bf16 tile: this half = one 64-key sub-tile
-        uint8_t* prow = sP + half * (BQ * 128) + (r >> 3) * 1024 + (r & 7) * 128;
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x, ++it) {
-            const int h = item / p.n_work;
-            const AttnWork w = p.work[item % p.n_work];
-            int nA, nB, loc_first;
-            item_blocks(w, p.seg_lo, nA, nB, loc_first);
-            const int nb = nA + nB;
-            const bool valid = r < w.nrows;
-            const int row = w.row0 + r;
-            const int seg = valid ? p.seg_lo[row] : 0x7fffffff;
-            float m = -INFINITY, l = 0.f;
-            for (int b = 0; b < nb; ++b, ++g) {
-                const int st = g & 1;
+        const uint32_t tS = tmem_base + lane_base + C::kS + x * BQ;
+        const uint32_t tO = tmem_base + lane_base + C::kO + x * 128;
+        uint32_t gs = 0, uit = 0;
 #ifdef SGC_ATTN_PROF
-                const bool prof_thr = threadIdx.x == 128;
-                long long _pt = clock64();
+        const bool prof_thr = threadIdx.x == 128;
+        long long _pt = clock64();
 #define SPROF(slot)                                                                            \
     if (prof_thr) {                                                                            \
         long long _n = clock64();                                                              \
@@ -293,158 +285,137 @@ __global__ void __launch_bounds__(kThreads, 1)
 #else
 #define SPROF(slot)
 #endif
-                ptx::mbar_wait(&s_full[st], (g >> 1) & 1);
-                SPROF(4);
+        for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+            const int h = item / p.n_work;
+            const AttnWork w = p.work[item % p.n_work];
+            const UnitPlan u = plan_unit(w, p.seg_lo);
+            const int nb = u.nb[x];
+            if (!nb) continue;
+            const bool valid = r < u.nrows[x];
+            const int row = w.row0 + x * BQ + r;
+            const int seg = valid ? p.seg_lo[row] : 0x7fffffff;
+            float m = -INFINITY, l = 0.f;
+            for (int b = 0; b < nb; ++b, ++gs) {
+                SPROF(0);
+                ptx::mbar_wait(&s_full[x], gs & 1);
                 ptx::tc_fence_after();
-                float s[KH];
-#pragma unroll
-                for (int c = 0; c < KH / 32; ++c)
-                    ptx::tmem_ld32(tmem_base + lane_base + st * BKV + half * KH + c * 32,
-                                   *reinterpret_cast<uint32_t(*)[32]>(&s[c * 32]));
-                ptx::tmem_ld_wait();
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(&s_empty[st]);
-                SPROF(5);
-                // visible key window [klo, khi] of this row, in block-local key index
-                int k0, klo, khi;
-                if (b < nA) {
+                SPROF(1);
+                int k0, klo, khi;  // visible key window [klo, khi] in block-local index
+                if (b < u.nA) {
                     k0 = b * BKV;
                     klo = 0;
                     khi = valid ? min(BKV, w.pfx_len - k0) - 1 : -1;
                 } else {
-                    k0 = loc_first + (b - nA) * BKV;
+                    k0 = u.loc_first + (b - u.nA) * BKV;
                     klo = max(0, seg - k0);
                     khi = valid ? min(BKV - 1, row - k0) : -1;
                 }
-                const int cb = half * KH;
-                // fast path (interior prefix blocks): no masking, scale folded into the FFMA
-                const bool full = klo <= cb && khi >= cb + KH - 1;
-                float mx;
-                if (full) {
-                    float m4[4] = {s[0], s[1], s[2], s[3]};  // 4 independent chains
+                const bool full = klo == 0 && khi == BKV - 1;
+                // pass 1: row max over the visible keys (raw scores; scale > 0)
+                float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-                    for (int j = 4; j < KH; ++j) m4[j & 3] = fmaxf(m4[j & 3], s[j]);
-                    mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * p.scale_log2;
-                } else {
-                    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+                for (int c = 0; c < BKV / 32; ++c) {
+                    uint32_t v[32];
+                    ptx::tmem_ld32(tS + c * 32, v);
+                    ptx::tmem_ld_wait();
+                    if (full) {
 #pragma unroll
-                    for (int j = 0; j < KH; ++j) {
-                        s[j] = (cb + j >= klo && cb + j <= khi) ? s[j] * p.scale_log2 : -INFINITY;
-                        m4[j & 3] = fmaxf(m4[j & 3], s[j]);
+                        for (int j = 0; j < 32; ++j) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(v[j]));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const int key = c * 32 + j;
+                            if (key >= klo && key <= khi) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(v[j]));
+                        }
                     }
-                    mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
                 }
-                SPROF(6);
-                red_max[st][half][r] = mx;
-                named_bar_sync(1, 256);
-                mx = fmaxf(mx, red_max[st][half ^ 1][r]);
-                SPROF(7);
-                // lazy rescale: keep the running max unless it grows by more than 8 (2^8)
+                float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+                mx = mx > -INFINITY ? mx * p.scale_log2 : -INFINITY;
+                SPROF(2);
+                // lazy rescale: keep the running max unless it grows by more than 8 (2^8);
+                // O_X is stable here (s_full certifies the previous PV completed)
                 float alpha = 1.f;
-                bool rescale = false;
                 if (mx > -INFINITY) {
                     if (m == -INFINITY) {
                         m = mx;  // O and l are still zero
                     } else if (mx > m + 8.f) {
                         alpha = ex2_approx(m - mx);
                         m = mx;
-                        rescale = true;
-                    }
-                }
-                float rs = 0.f;
-                uint32_t pk[KH / 2];
-                if (m == -INFINITY) {
-#pragma unroll
-                    for (int j = 0; j < KH / 2; ++j) pk[j] = 0u;
-                } else if (full) {
-                    const float sc = p.scale_log2, nm = -m;
-                    float rs2[2] = {0.f, 0.f};
-#pragma unroll
-                    for (int j = 0; j < KH / 2; ++j) {
-                        const float xa = fmaf(s[2 * j], sc, nm), xc = fmaf(s[2 * j + 1], sc, nm);
-                        // ~30% of the exponentials on the FMA pipe, the rest on MUFU
-                        const bool emu = (j % 3) == 2;
-                        float a = emu ? ex2_poly(xa) : ex2_approx(xa);
-                        float c = emu ? ex2_poly(xc) : ex2_approx(xc);
-                        rs2[j & 1] += a + c;
-                        __nv_bfloat162 v = __floats2bfloat162_rn(a, c);
-                        pk[j] = *reinterpret_cast<uint32_t*>(&v);
-                    }
-                    rs = rs2[0] + rs2[1];
-                } else {
-#pragma unroll
-                    for (int j = 0; j < KH / 2; ++j) {
-                        float a = ex2_approx(s[2 * j] - m), c = ex2_approx(s[2 * j + 1] - m);
-                        rs += a + c;
-                        __nv_bfloat162 v = __floats2bfloat162_rn(a, c);
-                        pk[j] = *reinterpret_cast<uint32_t*>(&v);
-                    }
-                }
-                l = l * alpha + rs;  // this half's share of the row sum
-                SPROF(8);
-                // P buffer free and O stable once PV of the previous block completed
-                ptx::mbar_wait(p_empty, (g & 1) ^ 1);
-                SPROF(9);
-                ptx::tc_fence_after();
-                if (rescale && b > 0) {
 #pragma unroll 1
-                    for (int c = 0; c < OH / 32; ++c) {
-                        uint32_t o[32];
-                        const uint32_t ta = tmem_base + lane_base + C::kO + half * OH + c * 32;
-                        ptx::tmem_ld32(ta, o);
-                        ptx::tmem_ld_wait();
+                        for (int c = 0; c < HD / 32; ++c) {
+                            uint32_t o[32];
+                            ptx::tmem_ld32(tO + c * 32, o);
+                            ptx::tmem_ld_wait();
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-                        ptx::tmem_st32(ta, o);
+                            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+                            ptx::tmem_st32(tO + c * 32, o);
+                        }
                     }
-                    ptx::tmem_st_wait();
                 }
-                // P half-row: 8 chunks of 8 keys (16 B) with the 128B XOR swizzle
+                SPROF(3);
+                // pass 2: p = 2^(s*scale - m) -> bf16 pairs written over S's first 64 columns
+                float rs2[2] = {0.f, 0.f};
+                const float sc = p.scale_log2, nm = m == -INFINITY ? 0.f : -m;
 #pragma unroll
-                for (int cc = 0; cc < 8; ++cc) {
-                    uint4 v = make_uint4(pk[4 * cc], pk[4 * cc + 1], pk[4 * cc + 2], pk[4 * cc + 3]);
-                    *reinterpret_cast<uint4*>(prow + ((cc ^ (r & 7)) << 4)) = v;
+                for (int c = 0; c < BKV / 32; ++c) {
+                    uint32_t v[32], pk[16];
+                    ptx::tmem_ld32(tS + c * 32, v);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int key = c * 32 + 2 * j;
+                        float xa = fmaf(__uint_as_float(v[2 * j]), sc, nm);
+                        float xc = fmaf(__uint_as_float(v[2 * j + 1]), sc, nm);
+                        if (!full) {
+                            xa = (key >= klo && key <= khi && m != -INFINITY) ? xa : -INFINITY;
+                            xc = (key + 1 >= klo && key + 1 <= khi && m != -INFINITY) ? xc : -INFINITY;
+                        }
+                        // ~30% of the exponentials on the FMA pipe (full blocks), rest on MUFU
+                        const bool emu = full && (j % 3) == 2;
+                        const float a = emu ? ex2_poly(xa) : ex2_approx(xa);
+                        const float cc = emu ? ex2_poly(xc) : ex2_approx(xc);
+                        rs2[j & 1] += a + cc;
+                        __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
+                        pk[j] = *reinterpret_cast<uint32_t*>(&bv);
+                    }
+                    ptx::tmem_st16(tS + c * 16, pk);
                 }
-                SPROF(10);
-                ptx::fence_proxy_async_smem();
+                l = l * alpha + (rs2[0] + rs2[1]);
+                ptx::tmem_st_wait();
                 ptx::tc_fence_before();
-                ptx::mbar_arrive(p_full);
-                SPROF(11);
-
+                ptx::mbar_arrive(&p_full[x]);
+                SPROF(4);
             }
-            // epilogue: O / l -> bf16 (each half stores HD/2 columns); the row sums are
-            // exchanged through red_max[0] once both halves are past their last max exchange
-            named_bar_sync(1, 256);
-            red_max[0][half][r] = l;
-            named_bar_sync(1, 256);
-            const float lt = l + red_max[0][half ^ 1][r];
-            ptx::mbar_wait(o_full, it & 1);
+            // epilogue: O / l -> bf16
+            ptx::mbar_wait(&o_full[x], uit & 1);
             ptx::tc_fence_after();
-            const float il = lt > 0.f ? 1.f / lt : 0.f;
+            SPROF(5);
+            const float il = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll 1
-            for (int c = 0; c < OH / 32; ++c) {
+            for (int c = 0; c < HD / 32; ++c) {
                 uint32_t o[32];
-                ptx::tmem_ld32(tmem_base + lane_base + C::kO + half * OH + c * 32, o);
+                ptx::tmem_ld32(tO + c * 32, o);
                 ptx::tmem_ld_wait();
                 if (valid) {
-                    uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(row) * p.d + h * HD +
-                                                          half * OH + c * 32);
+                    uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(row) * p.d + h * HD + c * 32);
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         uint32_t wv[4];
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(o[8 * q + 2 * e]) * il,
-                                                                     __uint_as_float(o[8 * q + 2 * e + 1]) * il);
-                            wv[e] = *reinterpret_cast<uint32_t*>(&v);
+                            __nv_bfloat162 bv = __floats2bfloat162_rn(__uint_as_float(o[8 * q + 2 * e]) * il,
+                                                                      __uint_as_float(o[8 * q + 2 * e + 1]) * il);
+                            wv[e] = *reinterpret_cast<uint32_t*>(&bv);
                         }
                         dst[q] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
                     }
                 }
             }
             ptx::tc_fence_before();
-            named_bar_sync(1, 256);  // red_max[0] is reused by the next item
+            ++uit;
+            SPROF(6);
         }
+#undef SPROF
     }
     __syncthreads();
     if (warp == 2) {

@@ -11,9 +11,8 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2505_10951_b200 import _lib, host, workload as W  # noqa: E402
 
-NAMES = ["mma: wait v_full", "mma: wait p_full", "mma: wait k_full", "mma: wait s_empty",
-         "smx: wait s_full", "smx: tmem ld S", "smx: mask+max", "smx: max exchange",
-         "smx: exp+sum+pack", "smx: wait p_empty", "smx: rescale+P store", "smx: fence+arrive"]
+NAMES = ["smx: loop overhead", "smx: wait s_full", "smx: pass 1 (ld + max)", "smx: rescale O",
+         "smx: pass 2 (ld + exp + P->TMEM)", "smx: wait o_full", "smx: epilogue"]
 
 
 def main():
@@ -32,11 +31,11 @@ def main():
     L.sgc_debug_attn_prof(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), 0)
     ms, n = ctx.kernel_time("attention")
     per = buf.reshape(148, 16).astype(np.float64).mean(0)
-    tot_mma = per[:4].sum()
+    tot = per[:7].sum()
     print(f"attention {ms:.1f} ms over {n} launches; mean cycles per CTA (all launches):")
     for i, nm in enumerate(NAMES):
         print(f"  {nm:26s} {per[i] / 1e6:10.2f} Mcyc")
-    print(f"  sum softmax phases         {per[4:12].sum() / 1e6:10.2f} Mcyc; mma waits {tot_mma / 1e6:.2f} Mcyc")
+    print(f"  sum                         {tot / 1e6:10.2f} Mcyc")
 
 
 if __name__ == "__main__":
