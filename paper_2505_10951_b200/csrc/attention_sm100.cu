@@ -310,22 +310,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                     klo = max(0, seg - k0);
                     khi = valid ? min(BKV - 1, row - k0) : -1;
                 }
-                const bool full = klo == 0 && khi == BKV - 1;
+                // warp-uniform: the tcgen05.ld/st below are .sync.aligned (whole warp, same path)
+                const bool full = __all_sync(0xffffffffu, klo == 0 && khi == BKV - 1);
                 // pass 1: row max over the visible keys (raw scores; scale > 0)
                 float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+                if (full) {
 #pragma unroll
-                for (int c = 0; c < BKV / 32; ++c) {
-                    uint32_t v[32];
-                    ptx::tmem_ld32(tS + c * 32, v);
-                    ptx::tmem_ld_wait();
-                    if (full) {
+                    for (int c = 0; c < BKV / 32; ++c) {
+                        uint32_t v[32];
+                        ptx::tmem_ld32(tS + c * 32, v);
+                        ptx::tmem_ld_wait();
 #pragma unroll
                         for (int j = 0; j < 32; ++j) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(v[j]));
-                    } else {
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < BKV / 32; ++c) {
+                        uint32_t v[32];
+                        ptx::tmem_ld32(tS + c * 32, v);
+                        ptx::tmem_ld_wait();
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
                             const int key = c * 32 + j;
-                            if (key >= klo && key <= khi) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(v[j]));
+                            const float sv = (key >= klo && key <= khi) ? __uint_as_float(v[j]) : -INFINITY;
+                            m4[j & 3] = fmaxf(m4[j & 3], sv);
                         }
                     }
                 }
@@ -356,29 +364,51 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // pass 2: p = 2^(s*scale - m) -> bf16 pairs written over S's first 64 columns
                 float rs2[2] = {0.f, 0.f};
                 const float sc = p.scale_log2, nm = m == -INFINITY ? 0.f : -m;
+                if (full) {
 #pragma unroll
-                for (int c = 0; c < BKV / 32; ++c) {
-                    uint32_t v[32], pk[16];
-                    ptx::tmem_ld32(tS + c * 32, v);
-                    ptx::tmem_ld_wait();
+                    for (int c = 0; c < BKV / 32; ++c) {
+                        uint32_t v[32], pk[16];
+                        ptx::tmem_ld32(tS + c * 32, v);
+                        ptx::tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int key = c * 32 + 2 * j;
-                        float xa = fmaf(__uint_as_float(v[2 * j]), sc, nm);
-                        float xc = fmaf(__uint_as_float(v[2 * j + 1]), sc, nm);
-                        if (!full) {
-                            xa = (key >= klo && key <= khi && m != -INFINITY) ? xa : -INFINITY;
-                            xc = (key + 1 >= klo && key + 1 <= khi && m != -INFINITY) ? xc : -INFINITY;
+                        for (int j = 0; j < 16; ++j) {
+                            const float xa = fmaf(__uint_as_float(v[2 * j]), sc, nm);
+                            const float xc = fmaf(__uint_as_float(v[2 * j + 1]), sc, nm);
+                            // ~30% of the exponentials on the FMA pipe, the rest on MUFU
+                            float a, cc;
+                            if ((j % 3) == 2) {
+                                a = ex2_poly(xa);
+                                cc = ex2_poly(xc);
+                            } else {
+                                a = ex2_approx(xa);
+                                cc = ex2_approx(xc);
+                            }
+                            rs2[j & 1] += a + cc;
+                            __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
+                            pk[j] = *reinterpret_cast<uint32_t*>(&bv);
                         }
-                        // ~30% of the exponentials on the FMA pipe (full blocks), rest on MUFU
-                        const bool emu = full && (j % 3) == 2;
-                        const float a = emu ? ex2_poly(xa) : ex2_approx(xa);
-                        const float cc = emu ? ex2_poly(xc) : ex2_approx(xc);
-                        rs2[j & 1] += a + cc;
-                        __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
-                        pk[j] = *reinterpret_cast<uint32_t*>(&bv);
+                        ptx::tmem_st16(tS + c * 16, pk);
                     }
-                    ptx::tmem_st16(tS + c * 16, pk);
+                } else {
+                    const bool any = m != -INFINITY;
+#pragma unroll
+                    for (int c = 0; c < BKV / 32; ++c) {
+                        uint32_t v[32], pk[16];
+                        ptx::tmem_ld32(tS + c * 32, v);
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const int key = c * 32 + 2 * j;
+                            const bool va = any && key >= klo && key <= khi;
+                            const bool vc = any && key + 1 >= klo && key + 1 <= khi;
+                            const float a = va ? ex2_approx(fmaf(__uint_as_float(v[2 * j]), sc, nm)) : 0.f;
+                            const float cc = vc ? ex2_approx(fmaf(__uint_as_float(v[2 * j + 1]), sc, nm)) : 0.f;
+                            rs2[j & 1] += a + cc;
+                            __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
+                            pk[j] = *reinterpret_cast<uint32_t*>(&bv);
+                        }
+                        ptx::tmem_st16(tS + c * 16, pk);
+                    }
                 }
                 l = l * alpha + (rs2[0] + rs2[1]);
                 ptx::tmem_st_wait();
