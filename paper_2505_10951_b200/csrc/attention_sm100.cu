@@ -6,18 +6,19 @@
 // head, so every K/V block fetched serves 256 member rows, and the two tiles ping-pong on the
 // tensor core while the other tile's softmax runs:
 //
-//   warp 0      TMA: Q tiles (once per unit) and K blocks (128 keys) -- 3-stage ring released
-//               once both tiles' S = Q K^T have consumed a slot
-//   warp 3      TMA: V blocks -- 2-stage ring released after both O += P V
+//   warp 0      TMEM allocator + TMA: Q tiles (once per unit), K blocks (128 keys, 3-stage ring
+//               released once both tiles' S = Q K^T consumed a slot) and V blocks (2-stage
+//               ring released after both O += P V)
 //   warp 1      MMA issuer (one thread), per block j:
 //                 O_A += P_A(j) V_j ; S_A(j+1) = Q_A K_{j+1} ; O_B += P_B(j) V_j ; S_B(j+1) = ...
 //               S_X lives in TMEM; P_X (bf16) is written back over S_X's first 64 columns and
 //               consumed straight from TMEM by the PV MMA (A operand in TMEM, V MN-major in smem).
 //               tcgen05 ops of one thread execute in order, so S_X(j+1) never overwrites P_X(j)
 //               before PV_X(j) read it, and s_full_X(j+1) also certifies PV_X(j) completed.
-//   warp 2      TMEM allocator (512 columns: S_A | S_B | O_A | O_B)
-//   warps 4-7   softmax of tile A, warps 8-11 softmax of tile B: thread r owns query row r
-//               (TMEM lane r) -- two passes over its S row (max, then exp + pack + store P),
+//   TMEM: 512 columns S_A | S_B | O_A | O_B
+//   warps 2-5   softmax of tile A, warps 6-9 softmax of tile B: thread r owns query row r
+//               (TMEM lane r) -- one pass over its S row (4 loads in flight, max, exp, pack,
+//               P stored back to TMEM),
 //               online softmax in base 2 with lazy O rescale (only when the running max grows
 //               by > 2^8; done in place in TMEM, O is stable whenever S is ready), ~30% of the
 //               exponentials on the FMA pipe (MUFU offload), and the final O / l epilogue.
@@ -34,7 +35,7 @@ namespace {
 
 constexpr int BQ = 128;   // rows per query tile (two tiles per unit)
 constexpr int BKV = 128;  // keys per block
-constexpr int kThreads = 384;
+constexpr int kThreads = 320;  // loader, MMA, 2 x 4 softmax warps
 constexpr int kKStages = 3;
 constexpr int kVStages = 2;
 
@@ -101,7 +102,7 @@ __device__ __forceinline__ UnitPlan plan_unit(const AttnWork& w, const int32_t* 
 }
 
 template <int HD>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __maxnreg__(200)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKp,
                    const __grid_constant__ CUtensorMap tmVp, const __grid_constant__ CUtensorMap tmKl,
                    const __grid_constant__ CUtensorMap tmVl, TcParams p) {
@@ -147,55 +148,49 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::fence_barrier_init();
     }
-    if (warp == 2) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
+    if (warp == 0) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    if (warp == 0 || warp == 3) {
-        // warp 0: Q + K loader, warp 3: V loader
+    if (warp == 0) {
+        // TMA loader: Q tiles once per unit, then K_b and V_b per block
         if (lane == 0) {
-            const bool kload = warp == 0;
             uint32_t g = 0, qit[2] = {0, 0};
             for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
                 const int h = item / p.n_work;
                 const AttnWork w = p.work[item % p.n_work];
                 const UnitPlan u = plan_unit(w, p.seg_lo);
-                if (kload) {
 #pragma unroll
-                    for (int x = 0; x < 2; ++x) {
-                        if (!u.nb[x]) continue;
-                        ptx::mbar_wait(&q_empty[x], (qit[x] & 1) ^ 1);
-                        ptx::mbar_expect_tx(&q_full[x], C::kQBytes);
+                for (int x = 0; x < 2; ++x) {
+                    if (!u.nb[x]) continue;
+                    ptx::mbar_wait(&q_empty[x], (qit[x] & 1) ^ 1);
+                    ptx::mbar_expect_tx(&q_full[x], C::kQBytes);
 #pragma unroll
-                        for (int s = 0; s < C::kSub; ++s)
-                            ptx::tma_load_2d(sQ + x * C::kQBytes + s * (BQ * 128), &tmQ, &q_full[x],
-                                             h * HD + s * 64, w.row0 + x * BQ);
-                        ++qit[x];
-                    }
+                    for (int s = 0; s < C::kSub; ++s)
+                        ptx::tma_load_2d(sQ + x * C::kQBytes + s * (BQ * 128), &tmQ, &q_full[x],
+                                         h * HD + s * 64, w.row0 + x * BQ);
+                    ++qit[x];
                 }
                 const int nbu = max(u.nb[0], u.nb[1]);
                 for (int b = 0; b < nbu; ++b, ++g) {
                     const bool pfx = b < u.nA;
                     const int row = pfx ? w.pfx_kv0 + b * BKV : u.loc_first + (b - u.nA) * BKV;
-                    if (kload) {
-                        const int st = g % kKStages;
-                        ptx::mbar_wait(&k_empty[st], ((g / kKStages) & 1) ^ 1);
-                        ptx::mbar_expect_tx(&k_full[st], C::kKBytes);
+                    const int ks = g % kKStages;
+                    ptx::mbar_wait(&k_empty[ks], ((g / kKStages) & 1) ^ 1);
+                    ptx::mbar_expect_tx(&k_full[ks], C::kKBytes);
 #pragma unroll
-                        for (int s = 0; s < C::kSub; ++s)
-                            ptx::tma_load_2d(sK + st * C::kKBytes + s * (BKV * 128), pfx ? &tmKp : &tmKl,
-                                             &k_full[st], h * HD + s * 64, row);
-                    } else {
-                        const int st = g & 1;
-                        ptx::mbar_wait(&v_empty[st], ((g >> 1) & 1) ^ 1);
-                        ptx::mbar_expect_tx(&v_full[st], C::kVBytes);
+                    for (int s = 0; s < C::kSub; ++s)
+                        ptx::tma_load_2d(sK + ks * C::kKBytes + s * (BKV * 128), pfx ? &tmKp : &tmKl,
+                                         &k_full[ks], h * HD + s * 64, row);
+                    const int vs = g & 1;
+                    ptx::mbar_wait(&v_empty[vs], ((g >> 1) & 1) ^ 1);
+                    ptx::mbar_expect_tx(&v_full[vs], C::kVBytes);
 #pragma unroll
-                        for (int s = 0; s < C::kSub; ++s)
-                            ptx::tma_load_2d(sV + st * C::kVBytes + s * (BKV * 128), pfx ? &tmVp : &tmVl,
-                                             &v_full[st], h * HD + s * 64, row);
-                    }
+                    for (int s = 0; s < C::kSub; ++s)
+                        ptx::tma_load_2d(sV + vs * C::kVBytes + s * (BKV * 128), pfx ? &tmVp : &tmVl,
+                                         &v_full[vs], h * HD + s * 64, row);
                 }
             }
         }
@@ -266,15 +261,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (u.nb[x]) ++qit[x];
             }
         }
-    } else if (warp >= 4) {
-        const int x = (warp - 4) >> 2;                  // query tile handled by this warpgroup
-        const int r = (threadIdx.x - 128) & (BQ - 1);   // row within the tile == TMEM lane
-        const uint32_t lane_base = static_cast<uint32_t>(((warp - 4) & 3) * 32) << 16;
+    } else {
+        // warps 2-5: tile A, warps 6-9: tile B; a warp may only touch TMEM lanes
+        // 32 * (warp % 4) .. +31, so row = 32 * (warp % 4) + lane
+        const int x = (warp - 2) >> 2;                  // query tile handled by this warpgroup
+        const int r = (warp & 3) * 32 + lane;           // row within the tile == TMEM lane
+        const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const uint32_t tS = tmem_base + lane_base + C::kS + x * BQ;
         const uint32_t tO = tmem_base + lane_base + C::kO + x * 128;
         uint32_t gs = 0, uit = 0;
 #ifdef SGC_ATTN_PROF
-        const bool prof_thr = threadIdx.x == 128;
+        const bool prof_thr = threadIdx.x == 64;
         long long _pt = clock64();
 #define SPROF(slot)                                                                            \
     if (prof_thr) {                                                                            \
@@ -312,29 +309,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 // warp-uniform: the tcgen05.ld/st below are .sync.aligned (whole warp, same path)
                 const bool full = __all_sync(0xffffffffu, klo == 0 && khi == BKV - 1);
-                // pass 1: row max over the visible keys (raw scores; scale > 0)
+                // one pass over S: all four 32-column loads in flight, one wait (a tcgen05.ld
+                // round trip costs ~160 cycles regardless of width, scripts/micro/tmem_bw.cu)
+                uint32_t v[BKV];
+#pragma unroll
+                for (int c = 0; c < BKV / 32; ++c)
+                    ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[c * 32]));
+                ptx::tmem_ld_wait();
                 float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
                 if (full) {
 #pragma unroll
-                    for (int c = 0; c < BKV / 32; ++c) {
-                        uint32_t v[32];
-                        ptx::tmem_ld32(tS + c * 32, v);
-                        ptx::tmem_ld_wait();
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(v[j]));
-                    }
+                    for (int j = 0; j < BKV; ++j) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(v[j]));
                 } else {
 #pragma unroll
-                    for (int c = 0; c < BKV / 32; ++c) {
-                        uint32_t v[32];
-                        ptx::tmem_ld32(tS + c * 32, v);
-                        ptx::tmem_ld_wait();
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) {
-                            const int key = c * 32 + j;
-                            const float sv = (key >= klo && key <= khi) ? __uint_as_float(v[j]) : -INFINITY;
-                            m4[j & 3] = fmaxf(m4[j & 3], sv);
-                        }
+                    for (int j = 0; j < BKV; ++j) {
+                        const float sv = (j >= klo && j <= khi) ? __uint_as_float(v[j]) : -INFINITY;
+                        m4[j & 3] = fmaxf(m4[j & 3], sv);
                     }
                 }
                 float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
@@ -361,19 +351,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
                 SPROF(3);
-                // pass 2: p = 2^(s*scale - m) -> bf16 pairs written over S's first 64 columns
+                // p = 2^(s*scale - m) -> bf16 pairs written over S's first 64 columns
                 float rs2[2] = {0.f, 0.f};
                 const float sc = p.scale_log2, nm = m == -INFINITY ? 0.f : -m;
                 if (full) {
 #pragma unroll
                     for (int c = 0; c < BKV / 32; ++c) {
-                        uint32_t v[32], pk[16];
-                        ptx::tmem_ld32(tS + c * 32, v);
-                        ptx::tmem_ld_wait();
+                        uint32_t pk[16];
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
-                            const float xa = fmaf(__uint_as_float(v[2 * j]), sc, nm);
-                            const float xc = fmaf(__uint_as_float(v[2 * j + 1]), sc, nm);
+                            const float xa = fmaf(__uint_as_float(v[c * 32 + 2 * j]), sc, nm);
+                            const float xc = fmaf(__uint_as_float(v[c * 32 + 2 * j + 1]), sc, nm);
                             // ~30% of the exponentials on the FMA pipe, the rest on MUFU
                             float a, cc;
                             if ((j % 3) == 2) {
@@ -393,16 +381,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const bool any = m != -INFINITY;
 #pragma unroll
                     for (int c = 0; c < BKV / 32; ++c) {
-                        uint32_t v[32], pk[16];
-                        ptx::tmem_ld32(tS + c * 32, v);
-                        ptx::tmem_ld_wait();
+                        uint32_t pk[16];
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             const int key = c * 32 + 2 * j;
                             const bool va = any && key >= klo && key <= khi;
                             const bool vc = any && key + 1 >= klo && key + 1 <= khi;
-                            const float a = va ? ex2_approx(fmaf(__uint_as_float(v[2 * j]), sc, nm)) : 0.f;
-                            const float cc = vc ? ex2_approx(fmaf(__uint_as_float(v[2 * j + 1]), sc, nm)) : 0.f;
+                            const float a = va ? ex2_approx(fmaf(__uint_as_float(v[key]), sc, nm)) : 0.f;
+                            const float cc = vc ? ex2_approx(fmaf(__uint_as_float(v[key + 1]), sc, nm)) : 0.f;
                             rs2[j & 1] += a + cc;
                             __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
                             pk[j] = *reinterpret_cast<uint32_t*>(&bv);
@@ -421,24 +407,23 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             SPROF(5);
             const float il = l > 0.f ? 1.f / l : 0.f;
-#pragma unroll 1
-            for (int c = 0; c < HD / 32; ++c) {
-                uint32_t o[32];
-                ptx::tmem_ld32(tO + c * 32, o);
-                ptx::tmem_ld_wait();
-                if (valid) {
-                    uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(row) * p.d + h * HD + c * 32);
+            uint32_t o[HD];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        uint32_t wv[4];
+            for (int c = 0; c < HD / 32; ++c)
+                ptx::tmem_ld32(tO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
+            ptx::tmem_ld_wait();
+            if (valid) {
+                uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(row) * p.d + h * HD);
 #pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            __nv_bfloat162 bv = __floats2bfloat162_rn(__uint_as_float(o[8 * q + 2 * e]) * il,
-                                                                      __uint_as_float(o[8 * q + 2 * e + 1]) * il);
-                            wv[e] = *reinterpret_cast<uint32_t*>(&bv);
-                        }
-                        dst[q] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                for (int q = 0; q < HD / 8; ++q) {
+                    uint32_t wv[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        __nv_bfloat162 bv = __floats2bfloat162_rn(__uint_as_float(o[8 * q + 2 * e]) * il,
+                                                                  __uint_as_float(o[8 * q + 2 * e + 1]) * il);
+                        wv[e] = *reinterpret_cast<uint32_t*>(&bv);
                     }
+                    dst[q] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
                 }
             }
             ptx::tc_fence_before();
@@ -448,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #undef SPROF
     }
     __syncthreads();
-    if (warp == 2) {
+    if (warp == 0) {
         ptx::tc_fence_after();
         ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
     }
