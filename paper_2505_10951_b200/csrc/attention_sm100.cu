@@ -17,11 +17,11 @@
 //               before PV_X(j) read it, and s_full_X(j+1) also certifies PV_X(j) completed.
 //   TMEM: 512 columns S_A | S_B | O_A | O_B
 //   warps 2-5   softmax of tile A, warps 6-9 softmax of tile B: thread r owns query row r
-//               (TMEM lane r) -- one pass over its S row (4 loads in flight, max, exp, pack,
-//               P stored back to TMEM),
-//               online softmax in base 2 with lazy O rescale (only when the running max grows
-//               by > 2^8; done in place in TMEM, O is stable whenever S is ready), ~30% of the
-//               exponentials on the FMA pipe (MUFU offload), and the final O / l epilogue.
+//               (TMEM lane r) -- one streaming pass over its S row against the running max
+//               (double-buffered 32-column TMEM loads, P packed in registers, then stored back
+//               to TMEM); the max only moves when a block overshoots it by > 2^8 (block
+//               recomputed, O rescaled in place in TMEM, O is stable whenever S is ready);
+//               ~30% of the exponentials on the FMA pipe (MUFU offload); final O / l epilogue.
 //
 // Persistent: CTAs loop over (unit, head) items; units never straddle clusters (members) or
 // sequences (representative prefill).
@@ -102,7 +102,7 @@ __device__ __forceinline__ UnitPlan plan_unit(const AttnWork& w, const int32_t* 
 }
 
 template <int HD>
-__global__ void __maxnreg__(200)
+__global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKp,
                    const __grid_constant__ CUtensorMap tmVp, const __grid_constant__ CUtensorMap tmKl,
                    const __grid_constant__ CUtensorMap tmVl, TcParams p) {
@@ -309,93 +309,109 @@ __global__ void __maxnreg__(200)
                 }
                 // warp-uniform: the tcgen05.ld/st below are .sync.aligned (whole warp, same path)
                 const bool full = __all_sync(0xffffffffu, klo == 0 && khi == BKV - 1);
-                // one pass over S: all four 32-column loads in flight, one wait (a tcgen05.ld
-                // round trip costs ~160 cycles regardless of width, scripts/micro/tmem_bw.cu)
-                uint32_t v[BKV];
-#pragma unroll
-                for (int c = 0; c < BKV / 32; ++c)
-                    ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&v[c * 32]));
-                ptx::tmem_ld_wait();
-                float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-                if (full) {
-#pragma unroll
-                    for (int j = 0; j < BKV; ++j) m4[j & 3] = fmaxf(m4[j & 3], __uint_as_float(v[j]));
-                } else {
-#pragma unroll
-                    for (int j = 0; j < BKV; ++j) {
-                        const float sv = (j >= klo && j <= khi) ? __uint_as_float(v[j]) : -INFINITY;
-                        m4[j & 3] = fmaxf(m4[j & 3], sv);
-                    }
-                }
-                float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
-                mx = mx > -INFINITY ? mx * p.scale_log2 : -INFINITY;
-                SPROF(2);
-                // lazy rescale: keep the running max unless it grows by more than 8 (2^8);
-                // O_X is stable here (s_full certifies the previous PV completed)
-                float alpha = 1.f;
-                if (mx > -INFINITY) {
-                    if (m == -INFINITY) {
-                        m = mx;  // O and l are still zero
-                    } else if (mx > m + 8.f) {
-                        alpha = ex2_approx(m - mx);
-                        m = mx;
-#pragma unroll 1
-                        for (int c = 0; c < HD / 32; ++c) {
-                            uint32_t o[32];
-                            ptx::tmem_ld32(tO + c * 32, o);
-                            ptx::tmem_ld_wait();
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-                            ptx::tmem_st32(tO + c * 32, o);
-                        }
-                    }
-                }
-                SPROF(3);
-                // p = 2^(s*scale - m) -> bf16 pairs written over S's first 64 columns
-                float rs2[2] = {0.f, 0.f};
-                const float sc = p.scale_log2, nm = m == -INFINITY ? 0.f : -m;
-                if (full) {
+                // Streaming pass over S against the running (lazy) max m: 32-column chunks,
+                // double-buffered so one tcgen05.ld is always in flight (a load round trip costs
+                // ~160 cycles, scripts/micro/tmem_bw.cu); P stays packed in registers until the
+                // block is done. If the block max overshoots m by more than 2^8 the block is
+                // recomputed with the new max (rare) and O rescaled in place.
+                const float sc = p.scale_log2;
+                uint32_t pk[BKV / 2];
+                float rs = 0.f, bmax = -INFINITY;
+                float mref = m;  // -inf until the row has seen a visible key
+                {
+                    uint32_t va[32], vb[32];
+                    ptx::tmem_ld32(tS, va);
 #pragma unroll
                     for (int c = 0; c < BKV / 32; ++c) {
-                        uint32_t pk[16];
+                        uint32_t(&cur)[32] = (c & 1) ? vb : va;
+                        uint32_t(&nxt)[32] = (c & 1) ? va : vb;
+                        ptx::tmem_ld_wait();
+                        if (c + 1 < BKV / 32) ptx::tmem_ld32(tS + (c + 1) * 32, nxt);
+                        float cm4[2] = {-INFINITY, -INFINITY};
+                        if (full) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                cur[j] = __float_as_uint(__uint_as_float(cur[j]) * sc);
+                                cm4[j & 1] = fmaxf(cm4[j & 1], __uint_as_float(cur[j]));
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                const int key = c * 32 + j;
+                                const float sv = (key >= klo && key <= khi) ? __uint_as_float(cur[j]) * sc : -INFINITY;
+                                cur[j] = __float_as_uint(sv);
+                                cm4[j & 1] = fmaxf(cm4[j & 1], sv);
+                            }
+                        }
+                        const float cmax = fmaxf(cm4[0], cm4[1]);
+                        bmax = fmaxf(bmax, cmax);
+                        if (mref == -INFINITY) mref = cmax;  // first visible keys of the row
+                        const float nm = mref == -INFINITY ? 0.f : -mref;
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
-                            const float xa = fmaf(__uint_as_float(v[c * 32 + 2 * j]), sc, nm);
-                            const float xc = fmaf(__uint_as_float(v[c * 32 + 2 * j + 1]), sc, nm);
-                            // ~30% of the exponentials on the FMA pipe, the rest on MUFU
+                            const float xa = __uint_as_float(cur[2 * j]) + nm;
+                            const float xc = __uint_as_float(cur[2 * j + 1]) + nm;
                             float a, cc;
-                            if ((j % 3) == 2) {
+                            if (full && (j % 3) == 2) {  // ~30% on the FMA pipe (MUFU offload)
                                 a = ex2_poly(xa);
                                 cc = ex2_poly(xc);
                             } else {
                                 a = ex2_approx(xa);
                                 cc = ex2_approx(xc);
                             }
-                            rs2[j & 1] += a + cc;
+                            rs += a + cc;
                             __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
-                            pk[j] = *reinterpret_cast<uint32_t*>(&bv);
+                            pk[c * 16 + j] = *reinterpret_cast<uint32_t*>(&bv);
                         }
-                        ptx::tmem_st16(tS + c * 16, pk);
                     }
-                } else {
-                    const bool any = m != -INFINITY;
+                }
+                SPROF(2);
+                float alpha = 1.f;
+                if (bmax > mref + 8.f) {
+                    // overshoot: recompute the block against its true max (rare)
+                    const float nmax = bmax;
+                    const float nm = -nmax;
+                    rs = 0.f;
 #pragma unroll
                     for (int c = 0; c < BKV / 32; ++c) {
-                        uint32_t pk[16];
+                        uint32_t cur[32];
+                        ptx::tmem_ld32(tS + c * 32, cur);
+                        ptx::tmem_ld_wait();
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             const int key = c * 32 + 2 * j;
-                            const bool va = any && key >= klo && key <= khi;
-                            const bool vc = any && key + 1 >= klo && key + 1 <= khi;
-                            const float a = va ? ex2_approx(fmaf(__uint_as_float(v[key]), sc, nm)) : 0.f;
-                            const float cc = vc ? ex2_approx(fmaf(__uint_as_float(v[key + 1]), sc, nm)) : 0.f;
-                            rs2[j & 1] += a + cc;
+                            const bool va = full || (key >= klo && key <= khi);
+                            const bool vc = full || (key + 1 >= klo && key + 1 <= khi);
+                            const float a = va ? ex2_approx(fmaf(__uint_as_float(cur[2 * j]), sc, nm)) : 0.f;
+                            const float cc = vc ? ex2_approx(fmaf(__uint_as_float(cur[2 * j + 1]), sc, nm)) : 0.f;
+                            rs += a + cc;
                             __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
-                            pk[j] = *reinterpret_cast<uint32_t*>(&bv);
+                            pk[c * 16 + j] = *reinterpret_cast<uint32_t*>(&bv);
                         }
-                        ptx::tmem_st16(tS + c * 16, pk);
+                    }
+                    mref = nmax;
+                }
+                if (m != -INFINITY && mref > m) {
+                    // the row's reference max moved: rescale O in place (O is stable here:
+                    // s_full certified the previous PV completed)
+                    alpha = ex2_approx(m - mref);
+#pragma unroll 1
+                    for (int c = 0; c < HD / 32; ++c) {
+                        uint32_t o[32];
+                        ptx::tmem_ld32(tO + c * 32, o);
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+                        ptx::tmem_st32(tO + c * 32, o);
                     }
                 }
+                m = mref;
+                SPROF(3);
+                // P -> TMEM over S's first 64 columns (all of S has been read)
+#pragma unroll
+                for (int c = 0; c < BKV / 32; ++c)
+                    ptx::tmem_st16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[c * 16]));
+                const float rs2[2] = {rs, 0.f};
                 l = l * alpha + (rs2[0] + rs2[1]);
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
