@@ -233,7 +233,18 @@ int sgc_lpt_assign(const double* cost, uint32_t clusters, int world_size, uint32
  * 3 = bf16(tanh(D)). All pointers device. K % 64 == 0, N % 64 == 0. */
 int sgc_gemm_bf16(sgc_ctx* ctx, const void* a, const void* b, void* d, uint32_t M, uint32_t N,
                   uint32_t K, int epi);
-/* Average device time in ms of the last `n` GEMM launches issued with timing enabled. */
+/* ---- cascade attention building block (parity tests at full size; lm_core.cpp:246-274) ----
+ * out[r, h*hd:(h+1)*hd] = softmax over { prefix keys pfx_kv0 .. pfx_kv0+pfx_len-1 of (k_pfx, v_pfx) }
+ * U { own keys seg_lo[r] .. r of (k_loc, v_loc) } with scale 1/sqrt(hd), for every row r of every
+ * work unit. `work` is a HOST array of n_work x {row0, nrows, pfx_kv0, pfx_len}; units hold
+ * <= 256 rows (hd 64/128, tcgen05 kernel) or <= 64 rows (hd 16/32), rows of one unit share
+ * one prefix. q/out/k_loc/v_loc are [rows x d] bf16, k_pfx/v_pfx [pfx_rows x d] bf16, seg_lo
+ * [rows] int32; all device pointers. */
+int sgc_attention_bf16(sgc_ctx* ctx, const void* q, const void* k_pfx, const void* v_pfx,
+                       uint32_t pfx_rows, const void* k_loc, const void* v_loc, const int32_t* seg_lo,
+                       const int32_t* work, uint32_t n_work, uint32_t rows, uint32_t d, uint32_t heads,
+                       void* out);
+/* Enable/disable per-kernel CUDA-event timing; sgc_get_timing reads the accumulated totals. */
 int sgc_set_timing(sgc_ctx* ctx, int enable);
 /* Tuning knobs: "gemm_pairs" (1 = CTA-pair tcgen05 GEMM for 256-wide tiles, default; 0 = 1-CTA). */
 int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value);

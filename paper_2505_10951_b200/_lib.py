@@ -98,7 +98,7 @@ EXPORTS = [
     "sgc_pairwise_distances", "sgc_agglomerate", "sgc_build_representatives", "sgc_prefill",
     "sgc_kv_release", "sgc_kv_count", "sgc_kv_tokens", "sgc_kv_digest", "sgc_kv_resident_bytes",
     "sgc_kv_read", "sgc_extend", "sgc_run_subgcache", "sgc_gemm_bf16", "sgc_set_timing",
-    "sgc_get_timing", "sgc_lpt_assign", "sgc_set_option",
+    "sgc_get_timing", "sgc_lpt_assign", "sgc_set_option", "sgc_attention_bf16",
 ]
 
 _lib = None
@@ -156,6 +156,8 @@ def load() -> C.CDLL:
     L.sgc_run_subgcache.argtypes = [vp, vp, vp, P(Batch), P(BatchOut)]
     L.sgc_gemm_bf16.argtypes = [vp, vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]
     L.sgc_set_timing.argtypes = [vp, C.c_int]
+    L.sgc_attention_bf16.argtypes = [vp, vp, vp, vp, C.c_uint32, vp, vp, vp, P(C.c_int32), C.c_uint32,
+                                     C.c_uint32, C.c_uint32, C.c_uint32, vp]
     L.sgc_get_timing.argtypes = [vp, C.c_char_p, P(C.c_double), P(C.c_uint64)]
     L.sgc_set_option.argtypes = [vp, C.c_char_p, C.c_int64]
     L.sgc_lpt_assign.argtypes = [P(C.c_double), C.c_uint32, C.c_int, P(C.c_uint32)]

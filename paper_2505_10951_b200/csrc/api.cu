@@ -1695,6 +1695,47 @@ int sgc_gemm_bf16(sgc_ctx* ctx, const void* a, const void* b, void* d, uint32_t 
     });
 }
 
+int sgc_attention_bf16(sgc_ctx* ctx, const void* q, const void* k_pfx, const void* v_pfx,
+                       uint32_t pfx_rows, const void* k_loc, const void* v_loc, const int32_t* seg_lo,
+                       const int32_t* work, uint32_t n_work, uint32_t rows, uint32_t d, uint32_t heads,
+                       void* out) {
+    return guarded([&] {
+        if (heads == 0 || d % heads != 0) fail(SGC_DOMAIN, "attention: d must be a multiple of heads");
+        const int hd = static_cast<int>(d / heads);
+        const int tile = attn_tile(hd);
+        Ctx* c = &ctx->c;
+        std::vector<sgc::AttnWork> w(n_work);
+        for (uint32_t i = 0; i < n_work; ++i) {
+            w[i] = {work[4 * i], work[4 * i + 1], work[4 * i + 2], work[4 * i + 3]};
+            if (w[i].nrows < 1 || w[i].nrows > tile || w[i].row0 < 0 ||
+                static_cast<uint32_t>(w[i].row0 + w[i].nrows) > rows ||
+                static_cast<uint32_t>(w[i].pfx_kv0 + w[i].pfx_len) > pfx_rows)
+                fail(SGC_DOMAIN, "attention: work unit out of range");
+        }
+        sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("dbg_attn_work", n_work);
+        sgc::copy_in(c, d_work, w.data(), n_work);
+        sgc::AttnParams ap;
+        ap.q = static_cast<const bf16*>(q);
+        ap.out = static_cast<bf16*>(out);
+        ap.k_pfx = static_cast<const bf16*>(k_pfx);
+        ap.v_pfx = static_cast<const bf16*>(v_pfx);
+        ap.k_loc = static_cast<const bf16*>(k_loc);
+        ap.v_loc = static_cast<const bf16*>(v_loc);
+        ap.loc_kv0 = 0;
+        ap.seg_lo = seg_lo;
+        ap.work = d_work;
+        ap.d = static_cast<int>(d);
+        ap.scale = 1.0f / std::sqrt(static_cast<float>(hd));
+        if (sgc::attention_tc_supported(hd))
+            sgc::cascade_attention_tc(c, ap, static_cast<int>(n_work), static_cast<int>(heads), hd,
+                                      static_cast<int>(rows), static_cast<int>(std::max(1u, pfx_rows)),
+                                      static_cast<int>(rows));
+        else
+            sgc::cascade_attention(c, ap, static_cast<int>(n_work), static_cast<int>(heads), hd);
+        c->sync();
+    });
+}
+
 int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value) {
     return guarded([&] {
         (void)ctx;
@@ -1721,3 +1762,16 @@ int sgc_get_timing(sgc_ctx* ctx, const char* kernel, double* total_ms, uint64_t*
 }
 
 }  // extern "C"
+
+namespace sgc {
+void trace_launch(Ctx* c, const char* file, int line) {
+    std::fprintf(stderr, "[sgc trace] launch #%llu %s:%d ...", static_cast<unsigned long long>(c->launches),
+                 file, line);
+    std::fflush(stderr);
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::fprintf(stderr, " %s %.3f ms\n", cudaGetErrorString(e), ms);
+    std::fflush(stderr);
+}
+}  // namespace sgc

@@ -367,34 +367,44 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 SPROF(2);
                 float alpha = 1.f;
-                if (bmax > mref + 8.f) {
+                // Both fix-ups below are per-row decisions, but tcgen05.ld/st are .sync.aligned:
+                // the whole warp enters when any lane needs one, the others pass through
+                // unchanged (their loaded values are discarded / rescaled by exactly 1).
+                const bool over = bmax > mref + 8.f;
+                if (__any_sync(0xffffffffu, over)) {
                     // overshoot: recompute the block against its true max (rare)
                     const float nmax = bmax;
                     const float nm = -nmax;
-                    rs = 0.f;
+                    float rs_new = 0.f;
 #pragma unroll
                     for (int c = 0; c < BKV / 32; ++c) {
                         uint32_t cur[32];
                         ptx::tmem_ld32(tS + c * 32, cur);
                         ptx::tmem_ld_wait();
+                        if (over) {
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const int key = c * 32 + 2 * j;
-                            const bool va = full || (key >= klo && key <= khi);
-                            const bool vc = full || (key + 1 >= klo && key + 1 <= khi);
-                            const float a = va ? ex2_approx(fmaf(__uint_as_float(cur[2 * j]), sc, nm)) : 0.f;
-                            const float cc = vc ? ex2_approx(fmaf(__uint_as_float(cur[2 * j + 1]), sc, nm)) : 0.f;
-                            rs += a + cc;
-                            __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
-                            pk[c * 16 + j] = *reinterpret_cast<uint32_t*>(&bv);
+                            for (int j = 0; j < 16; ++j) {
+                                const int key = c * 32 + 2 * j;
+                                const bool va = full || (key >= klo && key <= khi);
+                                const bool vc = full || (key + 1 >= klo && key + 1 <= khi);
+                                const float a = va ? ex2_approx(fmaf(__uint_as_float(cur[2 * j]), sc, nm)) : 0.f;
+                                const float cc = vc ? ex2_approx(fmaf(__uint_as_float(cur[2 * j + 1]), sc, nm)) : 0.f;
+                                rs_new += a + cc;
+                                __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
+                                pk[c * 16 + j] = *reinterpret_cast<uint32_t*>(&bv);
+                            }
                         }
                     }
-                    mref = nmax;
+                    if (over) {
+                        rs = rs_new;
+                        mref = nmax;
+                    }
                 }
-                if (m != -INFINITY && mref > m) {
+                const bool resc = m != -INFINITY && mref > m;
+                if (__any_sync(0xffffffffu, resc)) {
                     // the row's reference max moved: rescale O in place (O is stable here:
                     // s_full certified the previous PV completed)
-                    alpha = ex2_approx(m - mref);
+                    alpha = resc ? ex2_approx(m - mref) : 1.f;
 #pragma unroll 1
                     for (int c = 0; c < HD / 32; ++c) {
                         uint32_t o[32];

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -38,7 +39,19 @@ struct Error : std::runtime_error {
             ::sgc::fail(SGC_CUDA, std::string("kernel launch: ") + cudaGetErrorString(_e) +  \
                                       " @" + __FILE__ + ":" + std::to_string(__LINE__));     \
         (ctx)->launches++;                                                                   \
+        if (::sgc::trace_launches()) ::sgc::trace_launch(ctx, __FILE__, __LINE__);           \
     } while (0)
+
+// SGC_TRACE=1: synchronize after every launch and log its site (hang / fault triage)
+inline bool trace_launches() {
+    static const int on = [] {
+        const char* e = std::getenv("SGC_TRACE");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+struct Ctx;
+void trace_launch(Ctx* c, const char* file, int line);
 
 // ---- device scratch arena: grow-only buffers keyed by name -------------------------------
 struct Buffer {

@@ -84,6 +84,16 @@ class Context:
         check(self.lib.sgc_gemm_bf16(self.h, C.c_void_p(a_ptr), C.c_void_p(b_ptr),
                                      C.c_void_p(d_ptr), M, N, K, epi))
 
+    def attention(self, q_ptr: int, k_pfx: int, v_pfx: int, pfx_rows: int, k_loc: int, v_loc: int,
+                  seg_lo_ptr: int, work: np.ndarray, rows: int, d: int, heads: int, out_ptr: int):
+        """Cascade attention over device buffers (sgc_attention_bf16); `work` is [n x 4] int32
+        {row0, nrows, pfx_kv0, pfx_len}."""
+        w = np.ascontiguousarray(work, dtype=np.int32).reshape(-1, 4)
+        vp = C.c_void_p
+        check(self.lib.sgc_attention_bf16(self.h, vp(q_ptr), vp(k_pfx), vp(v_pfx), pfx_rows, vp(k_loc),
+                                          vp(v_loc), vp(seg_lo_ptr), _p(w, C.c_int32), w.shape[0], rows,
+                                          d, heads, vp(out_ptr)))
+
 
 # ------------------------------------------------------------------ packing helpers
 

@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout -s KILL 300 python -m pytest tests/test_gpu_attention.py -q -x --timeout 120 2>&1 | tail -5
+timeout -s KILL 300 python -m pytest tests/test_gpu_parity.py -q -x --timeout 120 -k "gemm" 2>&1 | tail -3
+timeout -s KILL 400 python bench.py --config c3 --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/b_quick.json 2>gpurun_out/b_quick.err; echo "bench rc=$?"; tail -3 gpurun_out/b_quick.err
+python -c "import json;d=json.load(open('gpurun_out/b_quick.json'));print(d['ms_per_step'],d['value'],d['ttft_p50_ms'],d['stage_ms'],d['kernel_ms_per_step'],d['roofline']['achieved'],d['clocks'])"

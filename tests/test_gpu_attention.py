@@ -1,0 +1,124 @@
+"""Cascade attention kernel vs a torch fp32 reference at C3-like sizes (many work units per
+persistent CTA, ~2k-key prefixes, member suffixes of ~50 rows).
+
+Semantics (lm_core.cpp:246-274): query row r of a member attends to the cluster's sealed prefix
+keys, then causally to its own suffix keys seg_lo[r] .. r, one softmax over both, scale
+1/sqrt(hd). Scores are deliberately large and grow along the key axis so the kernel's lazy
+running-max paths (block recompute on overshoot, in-place O rescale) fire on some lanes of a
+warp and not on others.
+
+Bar: bf16 output vs the fp32 reference (bf16-rounded q/k/v): |delta| <= 2e-2 + 2e-2 |ref|
+(P is rounded to bf16 before the PV product, O accumulates in fp32).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def _reference(q, kp, vp, kl, vl, seg_lo, groups, heads):
+    """groups: list of (row0, nrows, pfx_kv0, pfx_len, member_starts)."""
+    rows, d = q.shape
+    hd = d // heads
+    out = torch.zeros(rows, d, device=q.device, dtype=torch.float32)
+    scale = 1.0 / np.sqrt(hd)
+    for row0, nrows, p0, plen, _ in groups:
+        qq = q[row0:row0 + nrows].float().view(nrows, heads, hd).transpose(0, 1)        # H x n x hd
+        kk = torch.cat([kp[p0:p0 + plen], kl[row0:row0 + nrows]]).float().view(-1, heads, hd).transpose(0, 1)
+        vv = torch.cat([vp[p0:p0 + plen], vl[row0:row0 + nrows]]).float().view(-1, heads, hd).transpose(0, 1)
+        s = torch.matmul(qq, kk.transpose(1, 2)) * scale                             # H x n x (plen+n)
+        r = torch.arange(row0, row0 + nrows, device=q.device)
+        own = torch.arange(row0, row0 + nrows, device=q.device)
+        lo = seg_lo[row0:row0 + nrows].long()
+        vis_own = (own[None, :] >= lo[:, None]) & (own[None, :] <= r[:, None])      # n x n
+        vis = torch.cat([torch.ones(nrows, plen, dtype=torch.bool, device=q.device), vis_own], 1)
+        s = s.masked_fill(~vis[None], float("-inf"))
+        o = torch.matmul(torch.softmax(s, -1), vv)                                   # H x n x hd
+        out[row0:row0 + nrows] = o.transpose(0, 1).reshape(nrows, d)
+    return out
+
+
+def _case(seed, heads, hd, clusters, pfx_lens, members_per_cluster, q_len, prefill=False):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    rng = np.random.default_rng(seed)
+    d = heads * hd
+    # members: rows grouped by cluster; prefill mode: each "member" is a whole sequence, no prefix
+    seg_lo, groups, row = [], [], 0
+    for c in range(clusters):
+        g0 = row
+        starts = []
+        for _ in range(members_per_cluster[c]):
+            n = int(rng.integers(q_len[0], q_len[1] + 1))
+            starts.append(row)
+            seg_lo += [row] * n
+            row += n
+        groups.append((g0, row - g0, int(sum(pfx_lens[:c])), 0 if prefill else pfx_lens[c], starts))
+    rows = row
+    pfx_rows = max(1, int(sum(pfx_lens)))
+
+    def rnd(n):
+        return torch.randn(n, d, device="cuda", generator=g)
+
+    # keys drift along a fixed direction so scores grow with key position (max moves late)
+    u = torch.randn(1, d, device="cuda", generator=g)
+    kp = rnd(pfx_rows) + u * torch.linspace(0, 3, pfx_rows, device="cuda")[:, None]
+    kl = rnd(rows) + u * torch.linspace(0, 4, rows, device="cuda")[:, None]
+    qs = torch.from_numpy(rng.uniform(0.2, 3.0, size=(rows, 1)).astype(np.float32)).cuda()
+    q = (rnd(rows) + u) * qs
+    vp, vl = rnd(pfx_rows), rnd(rows)
+    bf = [t.to(torch.bfloat16).contiguous() for t in (q, kp, vp, kl, vl)]
+    seg = torch.tensor(seg_lo, dtype=torch.int32, device="cuda")
+    return bf, seg, groups, rows, pfx_rows, d
+
+
+def _units(groups, tile):
+    w = []
+    for row0, nrows, p0, plen, _ in groups:
+        for r in range(0, nrows, tile):
+            w.append([row0 + r, min(tile, nrows - r), p0, plen])
+    return np.array(w, np.int32)
+
+
+@pytest.mark.parametrize("hd,heads,clusters,prefill", [
+    (128, 8, 6, False),   # C3-like members: ~2k prefix, 30-64 row suffixes, many units per CTA
+    (64, 16, 5, False),   # C2-like head_dim
+    (128, 4, 3, True),    # representative prefill: causal, no prefix, ~2k rows per sequence
+    (32, 4, 4, False),    # mma.sync path (tiny-model head_dim)
+])
+def test_cascade_attention_vs_torch_fp32(ctx, hd, heads, clusters, prefill):
+    rng = np.random.default_rng(hd + clusters)
+    if prefill:
+        pfx = [0] * clusters
+        members = [1] * clusters
+        qlen = (1900, 2100)
+    else:
+        pfx = [int(x) for x in rng.integers(1500, 2200, size=clusters)]
+        members = [int(x) for x in rng.integers(20, 60, size=clusters)]
+        qlen = (30, 64)
+    (q, kp, vp, kl, vl), seg, groups, rows, pfx_rows, d = _case(hd * 7 + clusters, heads, hd, clusters,
+                                                                   pfx, members, qlen, prefill)
+    tile = 256 if hd in (64, 128) else 64
+    work = _units(groups, tile)
+    assert len(work) * heads > 148 or prefill  # more items than persistent CTAs
+    out = torch.zeros(rows, d, device="cuda", dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    ctx.attention(q.data_ptr(), kp.data_ptr(), vp.data_ptr(), pfx_rows, kl.data_ptr(), vl.data_ptr(),
+                  seg.data_ptr(), work, rows, d, heads, out.data_ptr())
+    ref = _reference(q, kp, vp, kl, vl, seg, groups, heads)
+    got = out.float()
+    assert torch.isfinite(got).all()
+    err = (got - ref).abs()
+    bound = 2e-2 + 2e-2 * ref.abs()
+    bad = (err > bound).sum().item()
+    assert bad == 0, f"{bad} elements out of tolerance, max |d| {err.max().item():.4f}"
+
+
+def test_cascade_attention_work_validation(ctx):
+    from paper_2505_10951_b200._lib import DomainError
+
+    t = torch.zeros(64, 128, device="cuda", dtype=torch.bfloat16)
+    s = torch.zeros(64, device="cuda", dtype=torch.int32)
+    with pytest.raises(DomainError):
+        ctx.attention(t.data_ptr(), t.data_ptr(), t.data_ptr(), 64, t.data_ptr(), t.data_ptr(), s.data_ptr(),
+                      np.array([[0, 65, 0, 0]], np.int32), 64, 128, 1, t.data_ptr())

@@ -50,7 +50,8 @@ def check_logits(got, ref, tol=LOGIT_TOL):
 # ------------------------------------------------------------------------------ GEMM
 
 @pytest.mark.parametrize("M,N,K", [(1, 64, 64), (100, 128, 128), (128, 256, 256), (300, 768, 512),
-                                   (1000, 256, 4096), (129, 192, 64), (2048, 1024, 1024)])
+                                   (1000, 256, 4096), (129, 192, 64), (2048, 1024, 1024),
+                                   (4096, 4096, 1024), (5000, 1536, 512)])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
 @pytest.mark.parametrize("pairs", [1, 0])
 def test_gemm_tcgen05_vs_torch(ctx, M, N, K, epi, pairs):
