@@ -38,6 +38,12 @@ constexpr int BKV = 128;  // keys per block
 constexpr int kThreads = 320;  // loader, MMA, 2 x 4 softmax warps
 constexpr int kKStages = 3;
 constexpr int kVStages = 2;
+// SGC_POLY_NUM / SGC_POLY_DEN of the exponential pairs run as a polynomial on the FMA pipe
+// (MUFU.EX2 offload, FA4-style); the rest on MUFU
+#ifndef SGC_POLY_NUM
+#define SGC_POLY_NUM 1
+#define SGC_POLY_DEN 3
+#endif
 
 template <int HD>
 struct TcCfg {
@@ -82,6 +88,49 @@ __device__ __forceinline__ float ex2_poly(float x) {
     const float p = fmaf(fmaf(fmaf(0.05508868f, f, 0.24260405f), f, 0.69327623f), f, 0.99992895f);
     const int e = __float_as_int(t) - 0x4B400000;
     return __int_as_float(__float_as_int(p) + (e << 23));
+}
+
+// ---- packed fp32x2 helpers (FFMA2 / FADD2 / FMNMX3 on sm_100a): the softmax is issue-bound,
+// so every per-element op that has a paired or 3-input form uses it
+__device__ __forceinline__ uint64_t f2pack(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2unpack(uint64_t v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+// two ex2_poly lanes with packed arithmetic: 10 issue slots for 2 exponentials
+__device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& y1) {
+    const uint64_t magic = f2pack(12582912.0f, 12582912.0f), nmagic = f2pack(-12582912.0f, -12582912.0f);
+    const uint64_t x = f2pack(fmaxf(x0, -125.0f), fmaxf(x1, -125.0f));
+    const uint64_t t = fadd2(x, magic);                        // round(x) in the low mantissa bits
+    const uint64_t u = fadd2(t, nmagic);                       // round(x) (exact)
+    const uint64_t f = ffma2(u, f2pack(-1.0f, -1.0f), x);      // x - round(x), exact
+    uint64_t p = ffma2(f2pack(0.05508868f, 0.05508868f), f, f2pack(0.24260405f, 0.24260405f));
+    p = ffma2(p, f, f2pack(0.69327623f, 0.69327623f));
+    p = ffma2(p, f, f2pack(0.99992895f, 0.99992895f));
+    float t0, t1, p0, p1;
+    f2unpack(t, t0, t1);
+    f2unpack(p, p0, p1);
+    // (bits(t) << 23) == round(x) << 23 (mod 2^32): the magic's high bits shift out
+    y0 = __int_as_float((__float_as_int(t0) << 23) + __float_as_int(p0));
+    y1 = __int_as_float((__float_as_int(t1) << 23) + __float_as_int(p1));
 }
 
 // blocks of one unit: prefix blocks nA (shared), total blocks per tile, first local key row
@@ -309,102 +358,89 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 // warp-uniform: the tcgen05.ld/st below are .sync.aligned (whole warp, same path)
                 const bool full = __all_sync(0xffffffffu, klo == 0 && khi == BKV - 1);
-                // Streaming pass over S against the running (lazy) max m: 32-column chunks,
-                // double-buffered so one tcgen05.ld is always in flight (a load round trip costs
-                // ~160 cycles, scripts/micro/tmem_bw.cu); P stays packed in registers until the
-                // block is done. If the block max overshoots m by more than 2^8 the block is
-                // recomputed with the new max (rare) and O rescaled in place.
+                // The whole S row (128 fp32) is loaded into registers with four back-to-back
+                // tcgen05.ld (one wait), reduced to its max, exponentiated in place (P packed as
+                // bf16 pairs over the first 64 registers) and stored over S's first 64 columns.
+                // The row's reference max m is lazy: it only moves when the block max exceeds it
+                // by more than 2^8 (then O is rescaled in place; P <= 2^8 otherwise), so the
+                // common case has no O traffic at all.
                 const float sc = p.scale_log2;
-                uint32_t pk[BKV / 2];
-                float rs = 0.f, bmax = -INFINITY;
-                float mref = m;  // -inf until the row has seen a visible key
+                uint32_t sv[BKV];
+#pragma unroll
+                for (int c = 0; c < BKV / 32; ++c)
+                    ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
+                ptx::tmem_ld_wait();
+                SPROF(7);
+                // visibility bitmap of the block's keys [klo, khi] (4 x 32 bits); masked -> -inf
+                uint32_t vw[BKV / 32];
+#pragma unroll
+                for (int w = 0; w < BKV / 32; ++w) {
+                    const int lo = klo - 32 * w, hi = khi - 32 * w;
+                    const uint32_t mlo = lo <= 0 ? ~0u : (lo >= 32 ? 0u : ~0u << lo);
+                    const uint32_t mhi = hi >= 31 ? ~0u : (hi < 0 ? 0u : ~0u >> (31 - hi));
+                    vw[w] = mlo & mhi;
+                }
+                if (!full) {
+#pragma unroll
+                    for (int j = 0; j < BKV; ++j)
+                        if (!(vw[j / 32] & (1u << (j % 32)))) sv[j] = __float_as_uint(-INFINITY);
+                }
+                float bmax;
                 {
-                    uint32_t va[32], vb[32];
-                    ptx::tmem_ld32(tS, va);
+                    // max over RAW scores (scale > 0): 3-input max, four independent chains
+                    float c0 = -INFINITY, c1 = -INFINITY, c2 = -INFINITY, c3 = -INFINITY;
 #pragma unroll
-                    for (int c = 0; c < BKV / 32; ++c) {
-                        uint32_t(&cur)[32] = (c & 1) ? vb : va;
-                        uint32_t(&nxt)[32] = (c & 1) ? va : vb;
-                        ptx::tmem_ld_wait();
-                        if (c + 1 < BKV / 32) ptx::tmem_ld32(tS + (c + 1) * 32, nxt);
-                        float cm4[2] = {-INFINITY, -INFINITY};
-                        if (full) {
+                    for (int j = 0; j < BKV; j += 8) {
+                        c0 = fmax3(c0, __uint_as_float(sv[j]), __uint_as_float(sv[j + 1]));
+                        c1 = fmax3(c1, __uint_as_float(sv[j + 2]), __uint_as_float(sv[j + 3]));
+                        c2 = fmax3(c2, __uint_as_float(sv[j + 4]), __uint_as_float(sv[j + 5]));
+                        c3 = fmax3(c3, __uint_as_float(sv[j + 6]), __uint_as_float(sv[j + 7]));
+                    }
+                    bmax = fmaxf(fmaxf(c0, c1), fmaxf(c2, c3)) * sc;  // scaled-log2 units
+                }
+                SPROF(8);
+                const float mnew = (m == -INFINITY || bmax > m + 8.f) ? bmax : m;
+                const float nm = mnew == -INFINITY ? 0.f : -mnew;
+                float rs;
+                {
+                    const uint64_t sc2 = f2pack(sc, sc), nm2 = f2pack(nm, nm);
+                    uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;  // packed partial row sums
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                cur[j] = __float_as_uint(__uint_as_float(cur[j]) * sc);
-                                cm4[j & 1] = fmaxf(cm4[j & 1], __uint_as_float(cur[j]));
+                    for (int j = 0; j < BKV / 2; ++j) {
+                        float xa, xc;  // x = raw * scale_log2 - m: one FFMA2 per pair
+                        f2unpack(ffma2(f2pack(__uint_as_float(sv[2 * j]), __uint_as_float(sv[2 * j + 1])), sc2, nm2),
+                                 xa, xc);
+                        float a, cc;
+                        if ((j % SGC_POLY_DEN) < SGC_POLY_NUM) {  // share of exponentials on the FMA pipe
+                            ex2_poly2(xa, xc, a, cc);
+                            if (!full) {  // the polynomial maps -inf to 2^-125: zero masked keys
+                                if (!(vw[(2 * j) / 32] & (1u << ((2 * j) % 32)))) a = 0.f;
+                                if (!(vw[(2 * j + 1) / 32] & (1u << ((2 * j + 1) % 32)))) cc = 0.f;
                             }
                         } else {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                const int key = c * 32 + j;
-                                const float sv = (key >= klo && key <= khi) ? __uint_as_float(cur[j]) * sc : -INFINITY;
-                                cur[j] = __float_as_uint(sv);
-                                cm4[j & 1] = fmaxf(cm4[j & 1], sv);
-                            }
+                            a = ex2_approx(xa);
+                            cc = ex2_approx(xc);
                         }
-                        const float cmax = fmaxf(cm4[0], cm4[1]);
-                        bmax = fmaxf(bmax, cmax);
-                        if (mref == -INFINITY) mref = cmax;  // first visible keys of the row
-                        const float nm = mref == -INFINITY ? 0.f : -mref;
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const float xa = __uint_as_float(cur[2 * j]) + nm;
-                            const float xc = __uint_as_float(cur[2 * j + 1]) + nm;
-                            float a, cc;
-                            if (full && (j % 3) == 2) {  // ~30% on the FMA pipe (MUFU offload)
-                                a = ex2_poly(xa);
-                                cc = ex2_poly(xc);
-                            } else {
-                                a = ex2_approx(xa);
-                                cc = ex2_approx(xc);
-                            }
-                            rs += a + cc;
-                            __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
-                            pk[c * 16 + j] = *reinterpret_cast<uint32_t*>(&bv);
-                        }
+                        const uint64_t pr = f2pack(a, cc);
+                        if ((j & 3) == 0) r0 = fadd2(r0, pr);
+                        else if ((j & 3) == 1) r1 = fadd2(r1, pr);
+                        else if ((j & 3) == 2) r2 = fadd2(r2, pr);
+                        else r3 = fadd2(r3, pr);
+                        __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
+                        sv[j] = *reinterpret_cast<uint32_t*>(&bv);  // P pair j (j <= 2j: in place)
                     }
+                    float x0, x1;
+                    f2unpack(fadd2(fadd2(r0, r1), fadd2(r2, r3)), x0, x1);
+                    rs = x0 + x1;
                 }
                 SPROF(2);
                 float alpha = 1.f;
-                // Both fix-ups below are per-row decisions, but tcgen05.ld/st are .sync.aligned:
-                // the whole warp enters when any lane needs one, the others pass through
-                // unchanged (their loaded values are discarded / rescaled by exactly 1).
-                const bool over = bmax > mref + 8.f;
-                if (__any_sync(0xffffffffu, over)) {
-                    // overshoot: recompute the block against its true max (rare)
-                    const float nmax = bmax;
-                    const float nm = -nmax;
-                    float rs_new = 0.f;
-#pragma unroll
-                    for (int c = 0; c < BKV / 32; ++c) {
-                        uint32_t cur[32];
-                        ptx::tmem_ld32(tS + c * 32, cur);
-                        ptx::tmem_ld_wait();
-                        if (over) {
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                const int key = c * 32 + 2 * j;
-                                const bool va = full || (key >= klo && key <= khi);
-                                const bool vc = full || (key + 1 >= klo && key + 1 <= khi);
-                                const float a = va ? ex2_approx(fmaf(__uint_as_float(cur[2 * j]), sc, nm)) : 0.f;
-                                const float cc = vc ? ex2_approx(fmaf(__uint_as_float(cur[2 * j + 1]), sc, nm)) : 0.f;
-                                rs_new += a + cc;
-                                __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
-                                pk[c * 16 + j] = *reinterpret_cast<uint32_t*>(&bv);
-                            }
-                        }
-                    }
-                    if (over) {
-                        rs = rs_new;
-                        mref = nmax;
-                    }
-                }
-                const bool resc = m != -INFINITY && mref > m;
+                // the rescale is a per-row decision, but tcgen05.ld/st are .sync.aligned: the
+                // whole warp enters when any lane needs it (the others scale by exactly 1)
+                const bool resc = m != -INFINITY && mnew > m;
                 if (__any_sync(0xffffffffu, resc)) {
-                    // the row's reference max moved: rescale O in place (O is stable here:
-                    // s_full certified the previous PV completed)
-                    alpha = resc ? ex2_approx(m - mref) : 1.f;
+                    // O is stable here: s_full certified the previous PV of this tile completed
+                    alpha = resc ? ex2_approx(m - mnew) : 1.f;
 #pragma unroll 1
                     for (int c = 0; c < HD / 32; ++c) {
                         uint32_t o[32];
@@ -415,14 +451,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::tmem_st32(tO + c * 32, o);
                     }
                 }
-                m = mref;
+                m = mnew;
                 SPROF(3);
-                // P -> TMEM over S's first 64 columns (all of S has been read)
+                // P -> TMEM over S's first 64 columns
 #pragma unroll
                 for (int c = 0; c < BKV / 32; ++c)
-                    ptx::tmem_st16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&pk[c * 16]));
-                const float rs2[2] = {rs, 0.f};
-                l = l * alpha + (rs2[0] + rs2[1]);
+                    ptx::tmem_st16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&sv[c * 16]));
+                l = l * alpha + rs;
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 ptx::mbar_arrive(&p_full[x]);

@@ -11,8 +11,9 @@ import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2505_10951_b200 import _lib, host, workload as W  # noqa: E402
 
-NAMES = ["smx: loop overhead", "smx: wait s_full", "smx: pass 1 (ld + max)", "smx: rescale O",
-         "smx: pass 2 (ld + exp + P->TMEM)", "smx: wait o_full", "smx: epilogue"]
+NAMES = ["smx: loop overhead", "smx: wait s_full", "smx: exp + rowsum + pack", "smx: rescale O",
+         "smx: P->TMEM + arrive", "smx: wait o_full", "smx: epilogue", "smx: S tmem ld + wait",
+         "smx: mask + max"]
 
 
 def main():
@@ -31,7 +32,7 @@ def main():
     L.sgc_debug_attn_prof(buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), 0)
     ms, n = ctx.kernel_time("attention")
     per = buf.reshape(148, 16).astype(np.float64).mean(0)
-    tot = per[:7].sum()
+    tot = per[:9].sum()
     print(f"attention {ms:.1f} ms over {n} launches; mean cycles per CTA (all launches):")
     for i, nm in enumerate(NAMES):
         print(f"  {nm:26s} {per[i] / 1e6:10.2f} Mcyc")
