@@ -31,6 +31,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "per-query TTFT (p50) and queries/s vs CPU ref; fraction of tensor/HBM roofline"
+# every kernel launch of the library is bracketed by CUDA events under one of these names
+KERNEL_GROUPS = ["gemm", "attention", "rmsnorm", "embed", "head", "first_token", "gnn_encode",
+                 "text_features", "pairwise", "agglomerate", "union_prompt", "prompt_gather"]
 
 
 def load_peaks():
@@ -193,10 +196,9 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
     total_ms = ev0.elapsed_time(ev1)
     launches = ctx.launches - launches0
-    gemm_ms, gemm_n = ctx.kernel_time("gemm")
-    attn_ms, attn_n = ctx.kernel_time("attention")
-    gnn_ms, _ = ctx.kernel_time("gnn_encode")
-    agg_ms, _ = ctx.kernel_time("agglomerate")
+    kt = {k: ctx.kernel_time(k) for k in KERNEL_GROUPS}
+    gemm_ms, gemm_n = kt["gemm"]
+    attn_ms, attn_n = kt["attention"]
     ctx.set_timing(False)
     if world > 1:
         t = torch.tensor([total_ms], device="cuda")
@@ -223,6 +225,39 @@ def run_ours(args, rank, world, local_rank):
         d2h = int(r2.first_token.nbytes + r2.logits.nbytes + r2.labels.nbytes + r2.embeddings.nbytes)
         e2e = {"value": m / (e2e_ms / 1000.0), "unit": "queries/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+    # ---- generation past the first token (batched greedy decode, lm_core.cpp:352-404): the
+    # reference's run() serves every query to EOS / max_new; reported beside the TTFT metric
+    gen = None
+    if not args.no_gen and world == 1 and w.lm.get("max_new_tokens", 32) > 1:
+        mx = int(w.lm.get("max_new_tokens", 32))
+        host.run_subgcache(ctx, lm, dg, pb, want_logits=False, device_inputs=True, waves=args.waves,
+                           max_new=mx)
+        ev4, ev5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        rts, ntok, dec_ms, dec_rows = [], 0, 0.0, 0
+        torch.cuda.synchronize()
+        ev4.record(stream)
+        for _ in range(args.gen_steps):
+            rg = host.run_subgcache(ctx, lm, dg, pb, want_logits=False, device_inputs=True,
+                                    waves=args.waves, max_new=mx)
+            rts.append(rg.rt_ms.copy())
+            ntok += sum(len(t) for t in rg.tokens)
+            dec_ms += rg.decode_ms
+            dec_rows += rg.decode_rows
+        ev5.record(stream)
+        torch.cuda.synchronize()
+        g_ms = ev4.elapsed_time(ev5) / args.gen_steps
+        rt_all = np.concatenate(rts)
+        gen = {"max_new_tokens": mx, "ms_per_batch": round(g_ms, 3),
+               "queries_per_s_to_last_token": round(m / (g_ms / 1e3), 3),
+               "rt_p50_ms": round(float(np.percentile(rt_all[rt_all >= 0], 50)), 3),
+               "tokens_per_query_mean": round(ntok / (m * args.gen_steps), 3),
+               "generated_tokens_per_s": round(ntok / args.gen_steps / (g_ms / 1e3), 1),
+               "decode_stage_ms": round(dec_ms / args.gen_steps, 3),
+               "decode_rows_per_batch": dec_rows // args.gen_steps,
+               "steps": args.gen_steps,
+               "semantics": "same batch to EOS / max_new (run() with ToyLmConfig::max_new_tokens); "
+                            "rt = submission -> last token"}
 
     if world > 1:
         # every query is served by one rank: its TTFT is that rank's value (others report -1)
@@ -273,11 +308,12 @@ def run_ours(args, rank, world, local_rank):
                            f"query's cluster wave ({res.waves} waves); median over queries and steps"),
         "stage_ms": {k: round(v / args.steps, 3) for k, v in
                      zip(["encode", "cluster", "represent", "prefill", "extend", "total"], stage)},
-        "kernel_ms_per_step": {"gemm": gemm_ms / args.steps, "attention": attn_ms / args.steps,
-                               "gnn_encode": gnn_ms / args.steps, "agglomerate": agg_ms / args.steps},
+        "kernel_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in kt.items() if v[1]},
+        "gpu_idle_ms_per_step": round(ms_per_step - sum(v[0] for v in kt.values()) / args.steps, 3),
         "step_tflops": round(step_tf, 2), "step_tensor_frac": round(step_tf / peak, 4),
         "roofline": roofline,
         "e2e": e2e,
+        "generation": gen,
         "gpu_launches": int(launches),
         "setup_s": round(setup_s, 2),
     }
@@ -401,6 +437,8 @@ def main():
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-gen", action="store_true", help="skip the generation (decode) measurement")
+    ap.add_argument("--gen-steps", type=int, default=2)
     ap.add_argument("--no-pairs", action="store_true", help="1-CTA GEMM instead of CTA pairs")
     ap.add_argument("--waves", type=int, default=4,
                     help="serve clusters in this many waves (lower TTFT p50); 1 = one pass")

@@ -39,6 +39,8 @@ enum {
 enum { SGC_WARD = 0, SGC_SINGLE = 1, SGC_AVERAGE = 2, SGC_COMPLETE = 3, SGC_CENTROID = 4 };
 
 #define SGC_VOCAB 260 /* tokenizer.hpp:15-19: 256 bytes + BOS/EOS/PAD/GRAPH_SOFT_SLOT */
+#define SGC_BOS 256   /* Tokenizer::kBos */
+#define SGC_EOS 257   /* Tokenizer::kEos (greedy_decode stops on it, lm_core.cpp:387) */
 
 typedef struct sgc_ctx sgc_ctx;     /* one CUDA device + stream + scratch arena */
 typedef struct sgc_model sgc_model; /* ToyLm weights, bf16 in HBM (lm_core.hpp:114-171) */
@@ -177,6 +179,17 @@ int sgc_extend(sgc_ctx* ctx, sgc_model* model, sgc_kv* kv, const uint32_t* membe
                const sgc_token_lists* questions, const sgc_token_lists* answers,
                float pointer_bonus, float* logits, int32_t* first_token);
 
+/* ---- (5') per-query reuse with generation: sgc_extend followed by ToyLm::greedy_decode on
+ * every fork (lm_core.cpp:352-404), batched: one decode row per still-generating member per
+ * step (cascade attention: the segment's prefix on the tensor cores, the member's own question
+ * and generated keys per row, merged by log-sum-exp). tokens [count * max_new] (-1 padded),
+ * n_tokens [count]; logits / first_token as sgc_extend. The copy pointer biases answer[t]
+ * (then EOS) when the answer occurs in the segment's prefix. */
+int sgc_extend_generate(sgc_ctx* ctx, sgc_model* model, sgc_kv* kv, const uint32_t* member_seg,
+                        const sgc_token_lists* questions, const sgc_token_lists* answers,
+                        float pointer_bonus, uint32_t max_new, float* logits, int32_t* first_token,
+                        int32_t* tokens, uint32_t* n_tokens);
+
 /* ---- the whole SubgCache branch: run() lines pipeline.cpp:212-293 + run_batch -------- */
 typedef struct {
     sgc_subgraphs retrieved;   /* per query (retrieval is outside the hot path) */
@@ -200,6 +213,10 @@ typedef struct {
     /* clusters are served in `waves` groups of balanced cost (index order): members of an early
      * wave get their first token before later waves run (lower TTFT); 0/1 = one pass */
     uint32_t waves;
+    /* greedy decode past the first token (ToyLm::greedy_decode, lm_core.cpp:352-404, batched over
+     * every member of a wave): 0 or 1 = first token only; N > 1 = up to N tokens per query
+     * (run() uses ToyLmConfig::max_new_tokens, pipeline.cpp:186) */
+    uint32_t max_new_tokens;
 } sgc_batch;
 
 typedef struct {
@@ -217,6 +234,11 @@ typedef struct {
     uint32_t waves;         /* waves actually run */
     double stage_ms[8];     /* encode, cluster, represent, prefill, extend, total, -, - */
     uint64_t prefill_rows, extend_rows; /* tokens pushed through prefill / extend */
+    /* with batch.max_new_tokens > 1 (all optional, HOST memory): */
+    int32_t* tokens;        /* [m * max_new_tokens] generated ids, -1 padded (GenerationResult::token_ids) */
+    uint32_t* n_tokens;     /* [m] tokens generated (stops on EOS, max_new, full context) */
+    float* rt_ms;           /* [m] submission -> last token (QueryOutcome::rt_ms semantics) */
+    uint64_t decode_rows;   /* member-steps pushed through the decode forward */
 } sgc_batch_out;
 
 int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_batch* batch,

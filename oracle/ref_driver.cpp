@@ -14,6 +14,7 @@
 //   pipeline  retrieve -> build_prompt -> encode -> agglomerate -> merge -> run_batch
 //             (the SubgCache branch of pipeline.cpp:212-293, stage by stage, with timings)
 //   bench     bounded timing samples of each hot-path stage at a given model shape
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <fstream>
@@ -97,6 +98,24 @@ json cmd_lm(const json& spec) {
                     if (c.contains("answer")) {
                         o.hint = CopyPointerHint{toks(c["answer"]), kv.prefix_token_count(),
                                                  c.value("bonus", 100.0f)};
+                    }
+                    if (c.value("margins", false)) {
+                        // the same greedy loop through the public API (lm_core.cpp:376-398), recording
+                        // each step's biased top-1 / top-2 logit margin (robustness of the argmax)
+                        KVCache f2 = kv.fork();
+                        lm.extend(f2, suffix);
+                        json mg = json::array();
+                        for (size_t t = 0; t < c["decode"].get<size_t>(); ++t) {
+                            std::vector<float> lg = f2.last_logits();
+                            std::vector<float> s = lg;
+                            std::sort(s.begin(), s.end());
+                            mg.push_back(s[s.size() - 1] - s[s.size() - 2]);
+                            TokenId b = greedy_argmax(lg);
+                            if (b == Tokenizer::kEos || f2.token_count() + 1 > lm.config().max_seq_len) break;
+                            TokenId nx[1] = {b};
+                            lm.extend(f2, nx);
+                        }
+                        r["decode_margins"] = mg;
                     }
                     GenerationResult g = lm.greedy_decode(f, c["decode"].get<size_t>(), o);
                     r["decode"] = g.token_ids;
@@ -349,13 +368,19 @@ json cmd_pipeline(const json& spec) {
         eo.batch_start = tb;
         BatchRunResult res = run_batch(jobs, lm, eo);
         out["run_batch_ms"] = ms_since(tb);
-        json ttft = json::array(), ft = json::array();
+        json ttft = json::array(), ft = json::array(), gen = json::array(), rt = json::array();
         for (const QueryOutcome& o : res.outcomes) {
             ttft.push_back(o.ttft_ms);
+            rt.push_back(o.rt_ms);
             ft.push_back(o.gen.token_ids.empty() ? -1 : o.gen.token_ids[0]);
+            gen.push_back(o.gen.token_ids);
         }
         out["ttft_ms"] = ttft;
         out["run_batch_first_token"] = ft;
+        if (eo.max_new_tokens > 1) {
+            out["run_batch_tokens"] = gen;
+            out["rt_ms"] = rt;
+        }
     }
     return out;
 }

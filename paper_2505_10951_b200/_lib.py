@@ -76,7 +76,7 @@ class Batch(C.Structure):
                 ("pointer_bonus", C.c_float), ("gnn", GnnConfig),
                 ("precomputed_embeddings", C.POINTER(C.c_float)),
                 ("cluster_owner", C.POINTER(C.c_uint32)), ("rank", C.c_int),
-                ("world_size", C.c_int), ("waves", C.c_uint32)]
+                ("world_size", C.c_int), ("waves", C.c_uint32), ("max_new_tokens", C.c_uint32)]
 
 
 class BatchOut(C.Structure):
@@ -87,7 +87,9 @@ class BatchOut(C.Structure):
                 ("fallback", C.POINTER(C.c_uint8)), ("owner", C.POINTER(C.c_uint32)),
                 ("ttft_ms", C.POINTER(C.c_float)), ("waves", C.c_uint32),
                 ("stage_ms", C.c_double * 8),
-                ("prefill_rows", C.c_uint64), ("extend_rows", C.c_uint64)]
+                ("prefill_rows", C.c_uint64), ("extend_rows", C.c_uint64),
+                ("tokens", C.POINTER(C.c_int32)), ("n_tokens", C.POINTER(C.c_uint32)),
+                ("rt_ms", C.POINTER(C.c_float)), ("decode_rows", C.c_uint64)]
 
 
 # every symbol include/sgc_b200.h declares (checked by tests/test_boundary.py)
@@ -98,7 +100,7 @@ EXPORTS = [
     "sgc_pairwise_distances", "sgc_agglomerate", "sgc_build_representatives", "sgc_prefill",
     "sgc_kv_release", "sgc_kv_count", "sgc_kv_tokens", "sgc_kv_digest", "sgc_kv_resident_bytes",
     "sgc_kv_read", "sgc_extend", "sgc_run_subgcache", "sgc_gemm_bf16", "sgc_set_timing",
-    "sgc_get_timing", "sgc_lpt_assign", "sgc_set_option", "sgc_attention_bf16",
+    "sgc_get_timing", "sgc_lpt_assign", "sgc_set_option", "sgc_attention_bf16", "sgc_extend_generate",
 ]
 
 _lib = None
@@ -156,6 +158,8 @@ def load() -> C.CDLL:
     L.sgc_run_subgcache.argtypes = [vp, vp, vp, P(Batch), P(BatchOut)]
     L.sgc_gemm_bf16.argtypes = [vp, vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]
     L.sgc_set_timing.argtypes = [vp, C.c_int]
+    L.sgc_extend_generate.argtypes = [vp, vp, vp, P(C.c_uint32), P(TokenLists), P(TokenLists), C.c_float,
+                                      C.c_uint32, P(C.c_float), P(C.c_int32), P(C.c_int32), P(C.c_uint32)]
     L.sgc_attention_bf16.argtypes = [vp, vp, vp, vp, C.c_uint32, vp, vp, vp, P(C.c_int32), C.c_uint32,
                                      C.c_uint32, C.c_uint32, C.c_uint32, vp]
     L.sgc_get_timing.argtypes = [vp, C.c_char_p, P(C.c_double), P(C.c_uint64)]

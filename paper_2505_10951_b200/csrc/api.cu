@@ -201,6 +201,17 @@ struct FwdBatch {
     const int32_t* d_logit_rows = nullptr;
     int n_logits = 0;
     float* d_logits = nullptr;
+    // KV row written for batch row r (default r); decode writes generated tokens' K/V elsewhere
+    const int32_t* d_kv_row = nullptr;
+    // decode step (one row per generating member): prefix partial + own keys, see DecodeRows
+    const struct DecodeRows* dec = nullptr;
+};
+
+// device arrays of one decode step (rows = active members): prefix segment, own question rows
+// and own generated rows (lm_core.cpp:352-404 for a batch of forks)
+struct DecodeRows {
+    const int32_t *p_lo, *p_n, *q_lo, *q_n, *g_lo, *g_n;
+    std::function<const bf16*(int)> k_q, v_q;  // persistent question K/V per layer
 };
 
 void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
@@ -211,15 +222,23 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
     bf16* q = c->buf<bf16>("fwd_q", static_cast<size_t>(M) * d);
     bf16* ao = c->buf<bf16>("fwd_attn", static_cast<size_t>(M) * d);
     bf16* h = c->buf<bf16>("fwd_h", static_cast<size_t>(M) * m->ffn);
-    int32_t* iota = c->buf<int32_t>("fwd_iota", M);
     int* bad = c->buf<int>("fwd_bad", 1);
-    {
+    const int32_t* kv_row = b.d_kv_row;
+    if (!kv_row) {
+        int32_t* iota = c->buf<int32_t>("fwd_iota", M);
         std::vector<int32_t> io(M);
         std::iota(io.begin(), io.end(), 0);
         sgc::copy_in(c, iota, io.data(), M);
-        SGC_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
         SGC_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+        kv_row = iota;
     }
+    float* part_o = nullptr;
+    float* part_lse = nullptr;
+    if (b.dec && sgc::attention_tc_supported(m->hd)) {
+        part_o = c->buf<float>("dec_part_o", static_cast<size_t>(M) * d);
+        part_lse = c->buf<float>("dec_part_lse", static_cast<size_t>(M) * m->H);
+    }
+    SGC_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
     sgc::embed(c, x, b.d_tokens, m->tok_emb, b.d_soft, b.d_soft_idx, d, M, bad);
     for (int l = 0; l < m->L; ++l) {
         sgc::rmsnorm_bf16(c, xb, x, d, M);
@@ -228,7 +247,7 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
         e.q_out = q;
         e.k_cache = b.k_loc(l);
         e.v_cache = b.v_loc(l);
-        e.kv_row = iota;
+        e.kv_row = kv_row;
         e.pos = b.d_pos;
         e.rope_cos = m->rope_cos;
         e.rope_sin = m->rope_sin;
@@ -248,10 +267,46 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
         ap.work = b.d_work;
         ap.d = d;
         ap.scale = 1.0f / std::sqrt(static_cast<float>(m->hd));
-        if (sgc::attention_tc_supported(m->hd))
+        if (b.dec) {
+            // decode: prefix partial on the tensor cores (units of one prefix segment), then each
+            // row's own question + generated keys and the merge
+            sgc::DecodeAttnParams dp;
+            dp.q = q;
+            dp.k_p = ap.k_pfx;
+            dp.v_p = ap.v_pfx;
+            dp.k_q = b.dec->k_q(l);
+            dp.v_q = b.dec->v_q(l);
+            dp.k_g = b.k_loc(l);
+            dp.v_g = b.v_loc(l);
+            dp.p_lo = b.dec->p_lo;
+            dp.p_n = b.dec->p_n;
+            dp.q_lo = b.dec->q_lo;
+            dp.q_n = b.dec->q_n;
+            dp.g_lo = b.dec->g_lo;
+            dp.g_n = b.dec->g_n;
+            dp.out = ao;
+            dp.rows = M;
+            dp.d = d;
+            dp.heads = m->H;
+            dp.scale = ap.scale;
+            if (part_o) {
+                ap.part_o = part_o;
+                ap.part_lse = part_lse;
+                ap.k_loc = ap.k_pfx;
+                ap.v_loc = ap.v_pfx;
+                sgc::cascade_attention_tc(c, ap, b.n_work, m->H, m->hd, M, b.pfx_rows, b.pfx_rows);
+                dp.part_o = part_o;
+                dp.part_lse = part_lse;
+            } else {
+                dp.part_o = nullptr;
+                dp.part_lse = nullptr;
+            }
+            sgc::decode_attention_local(c, dp);
+        } else if (sgc::attention_tc_supported(m->hd)) {
             sgc::cascade_attention_tc(c, ap, b.n_work, m->H, m->hd, M, b.k_pfx ? b.pfx_rows : M, M);
-        else
+        } else {
             sgc::cascade_attention(c, ap, b.n_work, m->H, m->hd);
+        }
 
         sgc::GemmEpi r;
         r.mode = sgc::EPI_RESID;
@@ -388,11 +443,21 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
     return kv.release();
 }
 
+// Optional output of do_extend for a following decode: the members' question K/V kept for all
+// layers (instead of a per-layer scratch) and the copy-pointer decision per member.
+struct ExtendKeep {
+    bf16* k = nullptr;  // [L][rows][d]
+    bf16* v = nullptr;
+    uint64_t rows = 0;
+    std::vector<int32_t> q_lo;  // per member (input order): first question row
+    std::vector<int8_t> hint;   // per member: answer found in the prefix (lm_core.cpp:361-374)
+};
+
 // members: segment, question tokens, answers; returns logits/first token in member order
 void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg_in,
                const uint64_t* q_off_in, const int32_t* q_in, const uint64_t* a_off_in,
                const int32_t* a_in, float bonus, float* logits_out, int32_t* first_out,
-               uint64_t max_rows = 1ull << 16) {
+               ExtendKeep* keep = nullptr, uint64_t max_rows = 1ull << 16) {
     if (n == 0) return;
     const int d = m->d;
     std::vector<uint32_t> seg = to_host(c, seg_in, n);
@@ -416,8 +481,16 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
     std::vector<uint32_t> order(n);
     std::iota(order.begin(), order.end(), 0);
     std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) { return seg[a] < seg[b]; });
-    float* d_logits_all = c->buf<float>("ex_logits_all", static_cast<size_t>(n) * SGC_VOCAB);
-    int32_t* d_first_all = c->buf<int32_t>("ex_first_all", n);
+    std::vector<int32_t> first_h(first_out ? n : 0);
+    std::vector<float> logits_h(logits_out ? static_cast<size_t>(n) * SGC_VOCAB : 0);
+    if (keep) {
+        keep->rows = qo[n];
+        keep->k = c->buf<bf16>("ex_keep_k", static_cast<size_t>(m->L) * keep->rows * d);
+        keep->v = c->buf<bf16>("ex_keep_v", static_cast<size_t>(m->L) * keep->rows * d);
+        keep->q_lo.assign(n, 0);
+        keep->hint.assign(n, 0);
+    }
+    uint64_t chunk0 = 0;  // first kept row of the chunk
     size_t i0 = 0;
     while (i0 < n) {
         // chunk [i0, i1) with <= max_rows rows
@@ -454,6 +527,7 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
                 seg_lo.push_back(start);
             }
             lrows.push_back(static_cast<int32_t>(toks.size() - 1));
+            if (keep) keep->q_lo[j] = static_cast<int32_t>(chunk0 + start);
             if (!ao.empty()) {
                 for (uint64_t t = ao[j]; t < ao[j + 1]; ++t) a_tok.push_back(at[t]);
             }
@@ -471,8 +545,7 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
         sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("ex_work", work.size());
         float* d_logits = c->buf<float>("ex_logits", static_cast<size_t>(nm) * SGC_VOCAB);
         int32_t* d_first = c->buf<int32_t>("ex_first", nm);
-        bf16* kl = c->buf<bf16>("ex_kloc", static_cast<size_t>(M) * d);  // one layer at a time
-        bf16* vl = c->buf<bf16>("ex_vloc", static_cast<size_t>(M) * d);
+        int8_t* d_hint = keep ? c->buf<int8_t>("ex_hint", nm) : nullptr;
         sgc::copy_in(c, d_tok, toks.data(), M);
         sgc::copy_in(c, d_pos, pos.data(), M);
         sgc::copy_in(c, d_seg, seg_lo.data(), M);
@@ -488,8 +561,17 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
         b.d_seg_lo = d_seg;
         b.d_work = d_work;
         b.n_work = static_cast<int>(work.size());
-        b.k_loc = [kl](int) { return kl; };
-        b.v_loc = [vl](int) { return vl; };
+        if (keep) {  // question K/V of every layer kept for the decode steps
+            const size_t lstride = static_cast<size_t>(keep->rows) * d, off = chunk0 * d;
+            bf16 *kk = keep->k, *vv = keep->v;
+            b.k_loc = [kk, lstride, off](int l) { return kk + l * lstride + off; };
+            b.v_loc = [vv, lstride, off](int l) { return vv + l * lstride + off; };
+        } else {  // one layer at a time
+            bf16* kl = c->buf<bf16>("ex_kloc", static_cast<size_t>(M) * d);
+            bf16* vl = c->buf<bf16>("ex_vloc", static_cast<size_t>(M) * d);
+            b.k_loc = [kl](int) { return kl; };
+            b.v_loc = [vl](int) { return vl; };
+        }
         b.k_pfx = [kv](int l) { return static_cast<const bf16*>(kv->k_layer(l)); };
         b.pfx_rows = static_cast<int>(kv->rows);
         b.v_pfx = [kv](int l) { return static_cast<const bf16*>(kv->v_layer(l)); };
@@ -498,29 +580,168 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
         b.d_logits = d_logits;
         forward_rows(c, m, b);
         sgc::first_tokens(c, d_first, d_logits, nm, kv->d_tokens, kv->d_tok_off, d_mseg, d_atok,
-                          a_tok.empty() ? nullptr : d_aoff, bonus);
+                          a_tok.empty() ? nullptr : d_aoff, bonus, d_hint);
         // scatter back to member order
-        std::vector<float> lg(static_cast<size_t>(nm) * SGC_VOCAB);
+        std::vector<float> lg(logits_out ? static_cast<size_t>(nm) * SGC_VOCAB : 0);
         std::vector<int32_t> ft(nm);
+        std::vector<int8_t> hn(keep ? nm : 0);
         sgc::copy_out(c, lg.data(), d_logits, lg.size());
         sgc::copy_out(c, ft.data(), d_first, ft.size());
+        if (keep) sgc::copy_out(c, hn.data(), d_hint, hn.size());
         c->sync();
-        std::vector<float> lg_all;
+        // scatter back to member order (outputs may be host or device memory)
         for (int k = 0; k < nm; ++k) {
-            uint32_t j = order[i0 + k];
+            const uint32_t j = order[i0 + k];
+            if (keep) keep->hint[j] = hn[k];
+            if (first_out) first_h[j] = ft[k];
             if (logits_out)
-                SGC_CUDA_CHECK(cudaMemcpyAsync(logits_out + static_cast<size_t>(j) * SGC_VOCAB,
-                                               lg.data() + static_cast<size_t>(k) * SGC_VOCAB,
-                                               SGC_VOCAB * sizeof(float), cudaMemcpyDefault, c->stream));
-            if (first_out)
-                SGC_CUDA_CHECK(cudaMemcpyAsync(first_out + j, ft.data() + k, sizeof(int32_t),
-                                               cudaMemcpyDefault, c->stream));
+                std::memcpy(logits_h.data() + static_cast<size_t>(j) * SGC_VOCAB,
+                            lg.data() + static_cast<size_t>(k) * SGC_VOCAB, SGC_VOCAB * sizeof(float));
         }
-        c->sync();
+        chunk0 += static_cast<uint64_t>(M);
         i0 = i1;
     }
-    (void)d_logits_all;
-    (void)d_first_all;
+    if (first_out) sgc::copy_in(c, first_out, first_h.data(), n);
+    if (logits_out) sgc::copy_in(c, logits_out, logits_h.data(), logits_h.size());
+    c->sync();
+}
+
+// ============================================================ batched greedy decode
+// ToyLm::greedy_decode (lm_core.cpp:352-404) for a batch of forks, one row per still-generating
+// member per step. Member j: prefix segment [pfx_kv0, +pfx_len) of the wave's sealed KV,
+// own question rows [q_lo, +q_n) of the kept question K/V, generated rows [j*max_new, +t) of
+// the decode K/V; token t is fed back at position pos0 + t (pos0 = context tokens after the
+// extend). Stops per member on EOS, after max_new tokens, or when the context is full; the
+// copy pointer biases answer[t] (then EOS) when the answer occurs in the prefix.
+struct GenJob {
+    std::vector<int32_t> pfx_kv0, pfx_len, q_lo, q_n, pos0, first;
+    std::vector<int8_t> hint;
+    std::vector<uint64_t> a_off{0};
+    std::vector<int32_t> a_tok;
+    uint32_t size() const { return static_cast<uint32_t>(first.size()); }
+};
+struct GenResult {
+    std::vector<int32_t> tokens;    // [n * max_new], -1 padded
+    std::vector<uint32_t> count;    // tokens per member
+    std::vector<int32_t> last_step; // step index of each member's last token
+    std::vector<cudaEvent_t> step_end;  // event after step t (t >= 1), index t - 1
+    uint64_t rows = 0;
+};
+
+GenResult do_decode(Ctx* c, sgc_model* m, const sgc_kv* kv, const ExtendKeep* keep, const GenJob& job,
+                    uint32_t max_new, float bonus) {
+    const uint32_t n = job.size();
+    const int d = m->d;
+    GenResult r;
+    r.tokens.assign(static_cast<size_t>(n) * max_new, -1);
+    r.count.assign(n, 0);
+    r.last_step.assign(n, 0);
+    std::vector<uint8_t> done(n, 0);
+    const uint64_t max_seq = m->cfg.max_seq_len;
+    for (uint32_t j = 0; j < n; ++j) {
+        r.tokens[static_cast<size_t>(j) * max_new] = job.first[j];
+        r.count[j] = 1;
+        done[j] = max_new <= 1 || job.first[j] == SGC_EOS || static_cast<uint64_t>(job.pos0[j]) + 1 > max_seq;
+    }
+    if (max_new <= 1 || n == 0) return r;
+    // generated K/V: member j's token t-1 at row j*max_new + t-1, all layers
+    const size_t grows = static_cast<size_t>(n) * max_new;
+    bf16* gk = c->buf<bf16>("dec_gk", static_cast<size_t>(m->L) * grows * d);
+    bf16* gv = c->buf<bf16>("dec_gv", static_cast<size_t>(m->L) * grows * d);
+    int8_t* d_hint = c->buf<int8_t>("dec_hint", n);
+    uint64_t* d_aoff = c->buf<uint64_t>("dec_aoff", n + 1);
+    int32_t* d_atok = c->buf<int32_t>("dec_atok", std::max<size_t>(1, job.a_tok.size()));
+    sgc::copy_in(c, d_hint, job.hint.data(), n);
+    sgc::copy_in(c, d_aoff, job.a_off.data(), n + 1);
+    sgc::copy_in(c, d_atok, job.a_tok.data(), job.a_tok.size());
+    const int tile = attn_tile(m->hd);
+    for (uint32_t t = 1; t < max_new; ++t) {
+        std::vector<int32_t> act;
+        for (uint32_t j = 0; j < n; ++j)
+            if (!done[j]) act.push_back(static_cast<int32_t>(j));
+        if (act.empty()) break;
+        const int M = static_cast<int>(act.size());
+        // rows: ascending member index == grouped by prefix segment (members are sorted by it)
+        std::vector<int32_t> tok(M), pos(M), kvr(M), step(M, static_cast<int32_t>(t)), lrow(M);
+        std::vector<int32_t> plo(M), pn(M), qlo(M), qn(M), glo(M), gn(M, static_cast<int32_t>(t));
+        std::vector<sgc::AttnWork> work;
+        for (int i = 0; i < M; ++i) {
+            const int32_t j = act[i];
+            tok[i] = r.tokens[static_cast<size_t>(j) * max_new + t - 1];
+            pos[i] = job.pos0[j] + static_cast<int32_t>(t) - 1;
+            kvr[i] = j * static_cast<int32_t>(max_new) + static_cast<int32_t>(t) - 1;
+            lrow[i] = i;
+            plo[i] = job.pfx_kv0[j];
+            pn[i] = job.pfx_len[j];
+            qlo[i] = job.q_lo[j];
+            qn[i] = job.q_n[j];
+            glo[i] = j * static_cast<int32_t>(max_new);
+            if (work.empty() || work.back().pfx_kv0 != plo[i] || work.back().nrows == tile)
+                work.push_back({i, 0, plo[i], pn[i]});
+            work.back().nrows++;
+        }
+        int32_t* d_arr = c->buf<int32_t>("dec_rows", static_cast<size_t>(M) * 12);
+        std::vector<int32_t> packed;
+        packed.reserve(static_cast<size_t>(M) * 12);
+        for (auto* v : {&tok, &pos, &kvr, &step, &lrow, &plo, &pn, &qlo, &qn, &glo, &gn, &act})
+            packed.insert(packed.end(), v->begin(), v->end());
+        sgc::copy_in(c, d_arr, packed.data(), packed.size());
+        auto col = [&](int k) { return d_arr + static_cast<size_t>(k) * M; };
+        sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("dec_work", work.size());
+        sgc::copy_in(c, d_work, work.data(), work.size());
+        float* d_logits = c->buf<float>("dec_logits", static_cast<size_t>(M) * SGC_VOCAB);
+        int32_t* d_tok_out = c->buf<int32_t>("dec_tok", M);
+        DecodeRows dr;
+        dr.p_lo = col(5);
+        dr.p_n = col(6);
+        dr.q_lo = col(7);
+        dr.q_n = col(8);
+        dr.g_lo = col(9);
+        dr.g_n = col(10);
+        {
+            const size_t ls = static_cast<size_t>(keep ? keep->rows : 0) * d;
+            const bf16* qk = keep ? keep->k : nullptr;
+            const bf16* qv = keep ? keep->v : nullptr;
+            dr.k_q = [qk, ls](int l) { return qk ? qk + l * ls : nullptr; };
+            dr.v_q = [qv, ls](int l) { return qv ? qv + l * ls : nullptr; };
+        }
+        FwdBatch b;
+        b.M = M;
+        b.d_tokens = col(0);
+        b.d_pos = col(1);
+        b.d_kv_row = col(2);
+        b.d_seg_lo = col(4);  // unused by the decode attention (own keys come from DecodeRows)
+        b.d_work = d_work;
+        b.n_work = static_cast<int>(work.size());
+        b.pfx_rows = static_cast<int>(kv->rows);
+        b.k_pfx = [kv](int l) { return static_cast<const bf16*>(kv->k_layer(l)); };
+        b.v_pfx = [kv](int l) { return static_cast<const bf16*>(kv->v_layer(l)); };
+        b.k_loc = [gk, grows, d](int l) { return gk + l * grows * d; };
+        b.v_loc = [gv, grows, d](int l) { return gv + l * grows * d; };
+        b.dec = &dr;
+        b.d_logit_rows = col(4);
+        b.n_logits = M;
+        b.d_logits = d_logits;
+        forward_rows(c, m, b);
+        sgc::step_tokens(c, d_tok_out, d_logits, M, d_hint, d_atok, d_aoff, col(11), col(3), bonus);
+        cudaEvent_t ev = c->event();
+        SGC_CUDA_CHECK(cudaEventRecord(ev, c->stream));
+        r.step_end.push_back(ev);
+        std::vector<int32_t> out(M);
+        sgc::copy_out(c, out.data(), d_tok_out, M);
+        c->sync();
+        r.rows += static_cast<uint64_t>(M);
+        for (int i = 0; i < M; ++i) {
+            const int32_t j = act[i];
+            r.tokens[static_cast<size_t>(j) * max_new + t] = out[i];
+            r.count[j] = t + 1;
+            r.last_step[j] = static_cast<int32_t>(t);
+            // stop rules after emitting token t (lm_core.cpp:387-389)
+            if (out[i] == SGC_EOS || t + 1 == max_new || static_cast<uint64_t>(job.pos0[j]) + t + 1 > max_seq)
+                done[j] = 1;
+        }
+    }
+    return r;
 }
 
 // ============================================================ graph-side helpers
@@ -1360,6 +1581,49 @@ int sgc_extend(sgc_ctx* ctx, sgc_model* model, sgc_kv* kv, const uint32_t* membe
     });
 }
 
+int sgc_extend_generate(sgc_ctx* ctx, sgc_model* model, sgc_kv* kv, const uint32_t* member_seg,
+                        const sgc_token_lists* questions, const sgc_token_lists* answers,
+                        float pointer_bonus, uint32_t max_new, float* logits, int32_t* first_token,
+                        int32_t* tokens, uint32_t* n_tokens) {
+    return guarded([&] {
+        if (kv->model != model) fail(SGC_DOMAIN, "KV cache does not belong to this model");
+        Ctx* c = &ctx->c;
+        const uint32_t n = questions->count;
+        const bool ans = answers && answers->count > 0;
+        if (ans && answers->count != n) fail(SGC_DOMAIN, "answers/questions count mismatch");
+        if (n == 0) return;
+        std::vector<int32_t> first(n);
+        ExtendKeep keep;
+        do_extend(c, model, kv, n, member_seg, questions->off, questions->tokens, ans ? answers->off : nullptr,
+                  ans ? answers->tokens : nullptr, pointer_bonus, logits, first.data(), &keep);
+        std::vector<uint32_t> seg = to_host(c, member_seg, n);
+        std::vector<uint64_t> qo = to_host(c, questions->off, n + 1);
+        GenJob job;
+        if (ans) {
+            job.a_off = to_host(c, answers->off, n + 1);
+            job.a_tok = to_host(c, answers->tokens, job.a_off[n]);
+        } else {
+            job.a_off.assign(n + 1, 0);
+        }
+        for (uint32_t j = 0; j < n; ++j) {
+            const int32_t S = static_cast<int32_t>(qo[j + 1] - qo[j]);
+            job.pfx_kv0.push_back(static_cast<int32_t>(kv->off[seg[j]]));
+            job.pfx_len.push_back(static_cast<int32_t>(kv->len[seg[j]]));
+            job.q_lo.push_back(keep.q_lo[j]);
+            job.q_n.push_back(S);
+            job.pos0.push_back(static_cast<int32_t>(kv->len[seg[j]]) + S);
+            job.first.push_back(first[j]);
+            job.hint.push_back(keep.hint[j]);
+        }
+        GenResult r = do_decode(c, model, kv, &keep, job, std::max<uint32_t>(1, max_new), pointer_bonus);
+        for (cudaEvent_t e : r.step_end) c->event_pool.push_back(e);
+        if (first_token) sgc::copy_in(c, first_token, first.data(), n);
+        if (tokens) sgc::copy_in(c, tokens, r.tokens.data(), r.tokens.size());
+        if (n_tokens) sgc::copy_in(c, n_tokens, r.count.data(), n);
+        c->sync();
+    });
+}
+
 int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_batch* b, sgc_batch_out* o) {
     return guarded([&] {
         Ctx* c = &ctx->c;
@@ -1498,8 +1762,11 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         SGC_CUDA_CHECK(cudaEventRecord(ev_start, c->stream));
         std::vector<cudaEvent_t> ev_wave;
         std::vector<int32_t> wave_of(m, -1);
-        uint64_t prefill_rows = 0, extend_rows = 0;
-        double pf_ms = 0, ex_ms = 0;
+        uint64_t prefill_rows = 0, extend_rows = 0, decode_rows = 0;
+        double pf_ms = 0, ex_ms = 0, dec_ms = 0;
+        const uint32_t max_new = b->max_new_tokens;
+        const bool gen_on = max_new > 1;
+        std::vector<cudaEvent_t> rt_event(m, nullptr), dec_events;
         uint32_t wb = 0;
         for (uint32_t wv = 0; wv < wave_end.size(); ++wv) {
             const uint32_t we = wave_end[wv];
@@ -1512,6 +1779,9 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             std::vector<uint32_t> mem_seg, mem_q;  // extend members (segment index within the wave)
             std::vector<uint32_t> fb_q;            // fallback queries -> their standalone sequence
             std::vector<uint64_t> fb_seq;
+            GenJob gj;                             // the wave's decode rows (members, then fallbacks)
+            std::vector<uint32_t> gen_q;
+            ExtendKeep keep;
             for (uint32_t i = wb; i < we; ++i) {
                 seq_tok.insert(seq_tok.end(), rep_tok.begin() + reps.prefix_off[i], rep_tok.begin() + reps.prefix_off[i + 1]);
                 seq_off.push_back(seq_tok.size());
@@ -1576,9 +1846,23 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 std::vector<float> lg(static_cast<size_t>(nm) * SGC_VOCAB);
                 std::vector<int32_t> ft(nm);
                 do_extend(c, model, kv, nm, mem_seg.data(), mq_off.data(), mq_tok.data(), ans ? ma_off.data() : nullptr,
-                          ans ? ma_tok.data() : nullptr, b->pointer_bonus, lg.data(), ft.data());
+                          ans ? ma_tok.data() : nullptr, b->pointer_bonus, lg.data(), ft.data(),
+                          gen_on ? &keep : nullptr);
                 for (uint32_t j = 0; j < nm; ++j) {
                     const uint32_t q = mem_q[j];
+                    if (gen_on) {
+                        const int32_t S = static_cast<int32_t>(q_off[q + 1] - q_off[q]);
+                        gen_q.push_back(q);
+                        gj.pfx_kv0.push_back(static_cast<int32_t>(kv->off[mem_seg[j]]));
+                        gj.pfx_len.push_back(static_cast<int32_t>(kv->len[mem_seg[j]]));
+                        gj.q_lo.push_back(keep.q_lo[j]);
+                        gj.q_n.push_back(S);
+                        gj.pos0.push_back(static_cast<int32_t>(kv->len[mem_seg[j]]) + S);
+                        gj.first.push_back(ft[j]);
+                        gj.hint.push_back(keep.hint[j]);
+                        if (ans) gj.a_tok.insert(gj.a_tok.end(), a_tok.begin() + a_off[q], a_tok.begin() + a_off[q + 1]);
+                        gj.a_off.push_back(gj.a_tok.size());
+                    }
                     if (o->logits)
                         std::memcpy(o->logits + static_cast<size_t>(q) * SGC_VOCAB, lg.data() + static_cast<size_t>(j) * SGC_VOCAB,
                                     SGC_VOCAB * sizeof(float));
@@ -1616,11 +1900,39 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 if (o->logits) std::memcpy(o->logits + static_cast<size_t>(q) * SGC_VOCAB, lg, SGC_VOCAB * sizeof(float));
                 if (o->first_token) o->first_token[q] = best;
                 if (o->fallback) o->fallback[q] = 1;
+                if (gen_on) {  // standalone decode continues from its own sealed prompt
+                    gen_q.push_back(q);
+                    gj.pfx_kv0.push_back(static_cast<int32_t>(kv->off[s]));
+                    gj.pfx_len.push_back(static_cast<int32_t>(kv->len[s]));
+                    gj.q_lo.push_back(0);
+                    gj.q_n.push_back(0);
+                    gj.pos0.push_back(static_cast<int32_t>(kv->len[s]));
+                    gj.first.push_back(best);
+                    gj.hint.push_back(target >= 0 ? 1 : 0);
+                    if (ans) gj.a_tok.insert(gj.a_tok.end(), a_tok.begin() + a_off[q], a_tok.begin() + a_off[q + 1]);
+                    gj.a_off.push_back(gj.a_tok.size());
+                }
             }
             cudaEvent_t e = c->event();
             SGC_CUDA_CHECK(cudaEventRecord(e, c->stream));
             ev_wave.push_back(e);
             ex_ms += now_ms() - tw1;
+            // ---- (6) batched greedy decode of the wave's queries (RT)
+            if (gen_on && gj.size() > 0) {
+                const double td0 = now_ms();
+                GenResult gr = do_decode(c, model, kv, keep.k ? &keep : nullptr, gj, max_new, b->pointer_bonus);
+                decode_rows += gr.rows;
+                for (uint32_t j = 0; j < gj.size(); ++j) {
+                    const uint32_t q = gen_q[j];
+                    if (o->tokens)
+                        std::memcpy(o->tokens + static_cast<size_t>(q) * max_new, gr.tokens.data() + static_cast<size_t>(j) * max_new,
+                                    max_new * sizeof(int32_t));
+                    if (o->n_tokens) o->n_tokens[q] = gr.count[j];
+                    rt_event[q] = gr.last_step[j] > 0 ? gr.step_end[gr.last_step[j] - 1] : e;
+                }
+                for (cudaEvent_t se : gr.step_end) dec_events.push_back(se);
+                dec_ms += now_ms() - td0;
+            }
             wb = we;
         }
         c->sync();
@@ -1631,6 +1943,13 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             wave_ms.push_back(ms);
             c->event_pool.push_back(e);
         }
+        if (o->rt_ms)
+            for (uint32_t q = 0; q < m; ++q) {
+                float ms = -1.0f;
+                if (rt_event[q]) SGC_CUDA_CHECK(cudaEventElapsedTime(&ms, ev_start, rt_event[q]));
+                o->rt_ms[q] = rt_event[q] ? static_cast<float>(t_rep - t_start) + ms : -1.0f;
+            }
+        for (cudaEvent_t e : dec_events) c->event_pool.push_back(e);
         c->event_pool.push_back(ev_start);
         // TTFT (submission -> first token): batch start to the end of the query's wave; the
         // encode/cluster/represent stages before ev_start are added from the host clock
@@ -1657,6 +1976,8 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         o->stage_ms[5] = now_ms() - t_start;
         o->prefill_rows = prefill_rows;
         o->extend_rows = extend_rows;
+        o->decode_rows = decode_rows;
+        o->stage_ms[6] = dec_ms;
     });
 }
 

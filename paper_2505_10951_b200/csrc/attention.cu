@@ -327,4 +327,99 @@ void cascade_attention(Ctx* c, const AttnParams& p, int n_work, int heads, int h
     }
 }
 
+// ---- decode step: each row's own keys (+ merge with the prefix partial) ------------------
+// One warp per (row, head); lane i holds dims [i*DPL, i*DPL + DPL). Keys are visited in
+// order (prefix when no partial is given, question suffix, generated tokens) with an online
+// softmax in scaled-log2 units, then merged with the tcgen05 prefix partial:
+//   out = (O1 2^(lse1 - M) + acc 2^(m2 - M)) / (2^(lse1 - M) + l2 2^(m2 - M)).
+namespace {
+template <int HD>
+__global__ void __launch_bounds__(256) decode_local_kernel(DecodeAttnParams p) {
+    constexpr int DPL = HD >= 32 ? HD / 32 : 1;
+    const int wg = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (wg >= p.rows * p.heads) return;
+    const int r = wg / p.heads, h = wg % p.heads;
+    const bool act = lane * DPL < HD;
+    const size_t col = static_cast<size_t>(h) * HD + (act ? lane * DPL : 0);
+    const float sl2 = p.scale * 1.4426950408889634f;
+    float q[DPL], acc[DPL];
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) {
+        q[i] = act ? __bfloat162float(p.q[static_cast<size_t>(r) * p.d + col + i]) : 0.f;
+        acc[i] = 0.f;
+    }
+    float m = -INFINITY, l = 0.f;
+    auto run = [&](const __nv_bfloat16* K, const __nv_bfloat16* V, int lo, int n) {
+        // four keys per round: independent dot products and shuffle trees (ILP)
+        for (int k0 = 0; k0 < n; k0 += 4) {
+            float s[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                s[u] = 0.f;
+                if (k0 + u < n && act) {
+                    const __nv_bfloat16* kr = K + static_cast<size_t>(lo + k0 + u) * p.d + col;
+#pragma unroll
+                    for (int i = 0; i < DPL; ++i) s[u] = fmaf(q[i], __bfloat162float(kr[i]), s[u]);
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (k0 + u >= n) break;
+                const float x = s[u] * sl2;
+                const float mn = fmaxf(m, x);
+                const float a = m == -INFINITY ? 0.f : exp2f(m - mn);
+                const float pk = exp2f(x - mn);
+                l = l * a + pk;
+                const __nv_bfloat16* vr = V + static_cast<size_t>(lo + k0 + u) * p.d + col;
+#pragma unroll
+                for (int i = 0; i < DPL; ++i) acc[i] = acc[i] * a + pk * (act ? __bfloat162float(vr[i]) : 0.f);
+                m = mn;
+            }
+        }
+    };
+    if (!p.part_o && p.p_n) run(p.k_p, p.v_p, p.p_lo[r], p.p_n[r]);
+    if (p.q_n) run(p.k_q, p.v_q, p.q_lo[r], p.q_n[r]);
+    if (p.g_n) run(p.k_g, p.v_g, p.g_lo[r], p.g_n[r]);
+    float o1[DPL], w1 = 0.f, w2 = 1.f, den = l;
+#pragma unroll
+    for (int i = 0; i < DPL; ++i) o1[i] = 0.f;
+    if (p.part_o) {
+        const float lse1 = p.part_lse[static_cast<size_t>(r) * p.heads + h];
+        const float M = fmaxf(lse1, m);
+        w1 = lse1 == -INFINITY ? 0.f : exp2f(lse1 - M);
+        w2 = m == -INFINITY ? 0.f : exp2f(m - M);
+        den = w1 + l * w2;
+#pragma unroll
+        for (int i = 0; i < DPL; ++i) o1[i] = act ? p.part_o[static_cast<size_t>(r) * p.d + col + i] : 0.f;
+    }
+    const float inv = den > 0.f ? 1.f / den : 0.f;
+    if (act) {
+#pragma unroll
+        for (int i = 0; i < DPL; ++i)
+            p.out[static_cast<size_t>(r) * p.d + col + i] = __float2bfloat16_rn((o1[i] * w1 + acc[i] * w2) * inv);
+    }
+}
+}  // namespace
+
+void decode_attention_local(Ctx* c, const DecodeAttnParams& p) {
+    if (p.rows <= 0) return;
+    const int hd = p.d / p.heads;
+    const int warps = p.rows * p.heads;
+    const dim3 grid((warps + 7) / 8);
+    Ctx::Timed timer(c, "attention");
+    switch (hd) {
+        case 16: decode_local_kernel<16><<<grid, 256, 0, c->stream>>>(p); break;
+        case 32: decode_local_kernel<32><<<grid, 256, 0, c->stream>>>(p); break;
+        case 64: decode_local_kernel<64><<<grid, 256, 0, c->stream>>>(p); break;
+        case 128: decode_local_kernel<128><<<grid, 256, 0, c->stream>>>(p); break;
+        default: fail(SGC_DOMAIN, "decode attention: head_dim must be 16, 32, 64 or 128");
+    }
+    SGC_LAUNCH_CHECK(c);
+}
+
 }  // namespace sgc

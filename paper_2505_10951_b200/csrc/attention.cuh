@@ -26,6 +26,9 @@ struct AttnParams {
     const AttnWork* work;
     int d;
     float scale;  // 1/sqrt(head_dim) (lm_core.cpp:188)
+    // partial mode (tcgen05 kernel only): prefix keys only, fp32 normalized O + log2-sum-exp
+    float* part_o = nullptr;    // [rows x d]
+    float* part_lse = nullptr;  // [rows x heads], in units of log2 of the scaled scores
 };
 
 void cascade_attention(Ctx* c, const AttnParams& p, int n_work, int heads, int hd);
@@ -35,5 +38,22 @@ void cascade_attention(Ctx* c, const AttnParams& p, int n_work, int heads, int h
 bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, int hd, int q_rows,
                           int pfx_rows, int loc_rows);
 inline bool attention_tc_supported(int hd) { return hd == 64 || hd == 128; }
+
+// Decode step (attention.cu): merge the prefix partial (part_o, part_lse from the tcgen05 kernel
+// in partial mode, or none when part_o == nullptr) with each row's own keys: question rows
+// [q_lo[r], q_lo[r] + q_n[r]) of (k_q, v_q) and generated rows [g_lo[r], g_lo[r] + g_n[r]) of
+// (k_g, v_g); one softmax over all of them (lm_core.cpp:246-274), bf16 out.
+struct DecodeAttnParams {
+    const __nv_bfloat16* q;
+    const __nv_bfloat16 *k_p, *v_p, *k_q, *v_q, *k_g, *v_g;
+    // prefix range [p_lo, p_lo + p_n) of (k_p, v_p): read here only when part_o == nullptr
+    const int32_t *p_lo, *p_n, *q_lo, *q_n, *g_lo, *g_n;
+    const float* part_o;
+    const float* part_lse;
+    __nv_bfloat16* out;
+    int rows, d, heads;
+    float scale;
+};
+void decode_attention_local(Ctx* c, const DecodeAttnParams& p);
 
 }  // namespace sgc

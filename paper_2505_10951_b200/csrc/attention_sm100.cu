@@ -66,6 +66,10 @@ __device__ unsigned long long g_attn_prof[148 * 16];
 struct TcParams {
     const AttnWork* work;
     int n_work, heads;
+    // partial mode (decode, prefix segment only): no local blocks; the epilogue writes the
+    // normalized fp32 O and the row's log2-sum-exp (scaled-log2 units) instead of bf16 O
+    float* part_o;    // [rows x d] or nullptr
+    float* part_lse;  // [rows x heads]
     const int32_t* seg_lo;
     __nv_bfloat16* out;
     int d;
@@ -137,9 +141,18 @@ __device__ __forceinline__ void ex2_poly2(float x0, float x1, float& y0, float& 
 struct UnitPlan {
     int nA, nb[2], nrows[2], loc_first;
 };
-__device__ __forceinline__ UnitPlan plan_unit(const AttnWork& w, const int32_t* seg_lo) {
+__device__ __forceinline__ UnitPlan plan_unit(const AttnWork& w, const int32_t* seg_lo, bool partial) {
     UnitPlan u;
     u.nA = (w.pfx_len + BKV - 1) / BKV;
+    if (partial) {
+        u.loc_first = 0;
+#pragma unroll
+        for (int x = 0; x < 2; ++x) {
+            u.nrows[x] = min(BQ, max(0, w.nrows - x * BQ));
+            u.nb[x] = u.nrows[x] > 0 ? u.nA : 0;
+        }
+        return u;
+    }
     u.loc_first = seg_lo[w.row0];
 #pragma unroll
     for (int x = 0; x < 2; ++x) {
@@ -210,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
                 const int h = item / p.n_work;
                 const AttnWork w = p.work[item % p.n_work];
-                const UnitPlan u = plan_unit(w, p.seg_lo);
+                const UnitPlan u = plan_unit(w, p.seg_lo, p.part_o != nullptr);
 #pragma unroll
                 for (int x = 0; x < 2; ++x) {
                     if (!u.nb[x]) continue;
@@ -273,7 +286,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             };
             for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
                 const AttnWork w = p.work[item % p.n_work];
-                const UnitPlan u = plan_unit(w, p.seg_lo);
+                const UnitPlan u = plan_unit(w, p.seg_lo, p.part_o != nullptr);
                 const int nbu = max(u.nb[0], u.nb[1]);
                 for (int x = 0; x < 2; ++x)
                     if (u.nb[x]) ptx::mbar_wait(&q_full[x], qit[x] & 1);
@@ -334,12 +347,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
             const int h = item / p.n_work;
             const AttnWork w = p.work[item % p.n_work];
-            const UnitPlan u = plan_unit(w, p.seg_lo);
+            const UnitPlan u = plan_unit(w, p.seg_lo, p.part_o != nullptr);
             const int nb = u.nb[x];
             if (!nb) continue;
             const bool valid = r < u.nrows[x];
             const int row = w.row0 + x * BQ + r;
-            const int seg = valid ? p.seg_lo[row] : 0x7fffffff;
+            const int seg = valid && !p.part_o ? p.seg_lo[row] : 0x7fffffff;
             float m = -INFINITY, l = 0.f;
             for (int b = 0; b < nb; ++b, ++gs) {
                 SPROF(0);
@@ -473,7 +486,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = 0; c < HD / 32; ++c)
                 ptx::tmem_ld32(tO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
             ptx::tmem_ld_wait();
-            if (valid) {
+            if (valid && p.part_o) {
+                float4* dst = reinterpret_cast<float4*>(p.part_o + static_cast<size_t>(row) * p.d + h * HD);
+#pragma unroll
+                for (int q = 0; q < HD / 4; ++q)
+                    dst[q] = make_float4(__uint_as_float(o[4 * q]) * il, __uint_as_float(o[4 * q + 1]) * il,
+                                         __uint_as_float(o[4 * q + 2]) * il, __uint_as_float(o[4 * q + 3]) * il);
+                p.part_lse[static_cast<size_t>(row) * p.heads + h] = l > 0.f ? m + __log2f(l) : -INFINITY;
+            } else if (valid) {
                 uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(row) * p.d + h * HD);
 #pragma unroll
                 for (int q = 0; q < HD / 8; ++q) {
@@ -515,7 +535,7 @@ void launch_tc(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, i
     CUtensorMap tvp = make_map_2d(a.v_pfx, pfx_rows, d, BKV, 64);
     CUtensorMap tkl = make_map_2d(a.k_loc, loc_rows, d, BKV, 64);
     CUtensorMap tvl = make_map_2d(a.v_loc, loc_rows, d, BKV, 64);
-    TcParams p{a.work, n_work, heads, a.seg_lo, a.out, d, a.scale * 1.4426950408889634f};
+    TcParams p{a.work, n_work, heads, a.part_o, a.part_lse, a.seg_lo, a.out, d, a.scale * 1.4426950408889634f};
     const int items = n_work * heads;
     const int grid = items < c->num_sms ? items : c->num_sms;
     Ctx::Timed timer(c, "attention");
@@ -539,6 +559,7 @@ bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, in
                           int pfx_rows, int loc_rows) {
     if (n_work <= 0) return true;
     if (p.loc_kv0 != 0) return false;
+    if (p.part_o && !p.part_lse) return false;
     switch (hd) {
         case 64: launch_tc<64>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows); return true;
         case 128: launch_tc<128>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows); return true;

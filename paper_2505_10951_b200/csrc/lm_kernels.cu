@@ -132,37 +132,11 @@ __global__ void __launch_bounds__(288) head_kernel(float* logits, const float* x
 
 // copy pointer (lm_core.cpp:360-374) + first greedy step (:379-385): one CTA per member.
 // context = the member's sealed prefix tokens; search_limit = prefix length.
-__global__ void first_token_kernel(int32_t* first, const float* logits, int n,
-                                   const int32_t* ctx_tokens, const uint64_t* ctx_off,
-                                   const uint32_t* member_ctx, const int32_t* ans,
-                                   const uint64_t* ans_off, float bonus) {
-    const int j = blockIdx.x;
-    if (j >= n) return;
-    __shared__ int found;
-    if (threadIdx.x == 0) found = 0;
-    __syncthreads();
-    int alen = 0;
-    const int32_t* a = nullptr;
-    if (ans_off) {
-        alen = static_cast<int>(ans_off[j + 1] - ans_off[j]);
-        a = ans + ans_off[j];
-    }
-    if (alen > 0) {
-        const uint32_t cidx = member_ctx[j];
-        const int32_t* c = ctx_tokens + ctx_off[cidx];
-        const int clen = static_cast<int>(ctx_off[cidx + 1] - ctx_off[cidx]);
-        for (int s = threadIdx.x; s + alen <= clen; s += blockDim.x) {
-            int i = 0;
-            while (i < alen && c[s + i] == a[i]) ++i;
-            if (i == alen) found = 1;
-        }
-    }
-    __syncthreads();
-    const int target = found ? a[0] : -1;
-    // argmax with ties toward the lowest id (lm_core.cpp:39-50)
+// greedy_argmax (lm_core.cpp:39-50) over one row of logits with bonus on `target`, ties toward
+// the lowest id; whole block cooperates, result valid in thread 0
+__device__ int block_biased_argmax(const float* lg, int target, float bonus) {
     float best = -INFINITY;
     int bi = 0x7fffffff;
-    const float* lg = logits + static_cast<size_t>(j) * SGC_VOCAB;
     for (int v = threadIdx.x; v < SGC_VOCAB; v += blockDim.x) {
         float val = lg[v] + (v == target ? bonus : 0.0f);
         if (val > best || (val == best && v < bi)) {
@@ -191,8 +165,60 @@ __global__ void first_token_kernel(int32_t* first, const float* logits, int n,
                 best = sb[w];
                 bi = si[w];
             }
-        first[j] = bi;
     }
+    return bi;
+}
+
+// first decode step (lm_core.cpp:356-386): the copy pointer fires when the answer occurs in the
+// sealed prefix (search_limit = prefix length); hint_out (optional) records it for later steps
+__global__ void first_token_kernel(int32_t* first, int8_t* hint_out, const float* logits, int n,
+                                   const int32_t* ctx_tokens, const uint64_t* ctx_off,
+                                   const uint32_t* member_ctx, const int32_t* ans,
+                                   const uint64_t* ans_off, float bonus) {
+    const int j = blockIdx.x;
+    if (j >= n) return;
+    __shared__ int found;
+    if (threadIdx.x == 0) found = 0;
+    __syncthreads();
+    int alen = 0;
+    const int32_t* a = nullptr;
+    if (ans_off) {
+        alen = static_cast<int>(ans_off[j + 1] - ans_off[j]);
+        a = ans + ans_off[j];
+    }
+    if (alen > 0) {
+        const uint32_t cidx = member_ctx[j];
+        const int32_t* c = ctx_tokens + ctx_off[cidx];
+        const int clen = static_cast<int>(ctx_off[cidx + 1] - ctx_off[cidx]);
+        for (int s = threadIdx.x; s + alen <= clen; s += blockDim.x) {
+            int i = 0;
+            while (i < alen && c[s + i] == a[i]) ++i;
+            if (i == alen) found = 1;
+        }
+    }
+    __syncthreads();
+    const int target = found ? a[0] : -1;
+    const int bi = block_biased_argmax(logits + static_cast<size_t>(j) * SGC_VOCAB, target, bonus);
+    if (threadIdx.x == 0) {
+        first[j] = bi;
+        if (hint_out) hint_out[j] = static_cast<int8_t>(found);
+    }
+}
+
+// decode step t >= 1 (lm_core.cpp:376-381): bias target answer[t] while t < |answer|, then EOS
+__global__ void step_token_kernel(int32_t* tok, const float* logits, int n, const int8_t* hint,
+                                  const int32_t* ans, const uint64_t* ans_off, const int32_t* member,
+                                  const int32_t* step, float bonus) {
+    const int r = blockIdx.x;
+    if (r >= n) return;
+    const int j = member[r], t = step[r];
+    int target = -1;
+    if (hint && hint[j]) {
+        const int alen = static_cast<int>(ans_off[j + 1] - ans_off[j]);
+        target = t < alen ? ans[ans_off[j] + t] : SGC_EOS;
+    }
+    const int bi = block_biased_argmax(logits + static_cast<size_t>(r) * SGC_VOCAB, target, bonus);
+    if (threadIdx.x == 0) tok[r] = bi;
 }
 
 __global__ void transpose_head(float* out_t, const float* head, int d) {
@@ -245,11 +271,18 @@ void head_logits(Ctx* c, float* logits, const float* x, const int32_t* rows, int
 }
 void first_tokens(Ctx* c, int32_t* first, const float* logits, int n, const int32_t* ctx_tokens,
                   const uint64_t* ctx_off, const uint32_t* member_ctx, const int32_t* ans,
-                  const uint64_t* ans_off, float bonus) {
+                  const uint64_t* ans_off, float bonus, int8_t* hint_out) {
     if (n <= 0) return;
     Ctx::Timed timer(c, "first_token");
-    first_token_kernel<<<n, 128, 0, c->stream>>>(first, logits, n, ctx_tokens, ctx_off, member_ctx,
-                                                 ans, ans_off, bonus);
+    first_token_kernel<<<n, 128, 0, c->stream>>>(first, hint_out, logits, n, ctx_tokens, ctx_off,
+                                                 member_ctx, ans, ans_off, bonus);
+    SGC_LAUNCH_CHECK(c);
+}
+void step_tokens(Ctx* c, int32_t* tok, const float* logits, int n, const int8_t* hint, const int32_t* ans,
+                 const uint64_t* ans_off, const int32_t* member, const int32_t* step, float bonus) {
+    if (n <= 0) return;
+    Ctx::Timed timer(c, "first_token");
+    step_token_kernel<<<n, 128, 0, c->stream>>>(tok, logits, n, hint, ans, ans_off, member, step, bonus);
     SGC_LAUNCH_CHECK(c);
 }
 void head_transpose(Ctx* c, float* out_t, const float* head, int d) {

@@ -15,6 +15,8 @@ void head_logits(Ctx* c, float* logits, const float* x, const int32_t* rows, int
                  const float* head_t, int d);
 void first_tokens(Ctx* c, int32_t* first, const float* logits, int n, const int32_t* ctx_tokens,
                   const uint64_t* ctx_off, const uint32_t* member_ctx, const int32_t* ans,
-                  const uint64_t* ans_off, float bonus);
+                  const uint64_t* ans_off, float bonus, int8_t* hint_out = nullptr);
+void step_tokens(Ctx* c, int32_t* tok, const float* logits, int n, const int8_t* hint, const int32_t* ans,
+                 const uint64_t* ans_off, const int32_t* member, const int32_t* step, float bonus);
 void head_transpose(Ctx* c, float* out_t, const float* head, int d);
 }  // namespace sgc

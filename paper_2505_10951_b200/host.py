@@ -249,6 +249,25 @@ class ToyLm:
                                   _p(logits, C.c_float), _p(first, C.c_int32)))
         return logits, first
 
+    def extend_generate(self, kv: KVBatch, member_seg, questions, answers=None, bonus=100.0,
+                        max_new: int | None = None):
+        """extend_members + ToyLm::greedy_decode (lm_core.cpp:352-404) on every fork, batched.
+        Returns (logits after the extend, first tokens, list of generated token arrays)."""
+        seg = np.ascontiguousarray(member_seg, np.uint32)
+        ql, keepq = pack_tokens(questions)
+        al, keepa = pack_tokens(answers) if answers is not None else (None, None)
+        n = len(questions)
+        mx = self.cfg.max_new_tokens if max_new is None else int(max_new)
+        logits = np.zeros((n, VOCAB), np.float32)
+        first = np.zeros(n, np.int32)
+        toks = np.full((n, max(1, mx)), -1, np.int32)
+        cnt = np.zeros(n, np.uint32)
+        check(self.lib.sgc_extend_generate(self.ctx.h, self.h, kv.h, _p(seg, C.c_uint32), C.byref(ql),
+                                           C.byref(al) if al is not None else None, bonus, mx,
+                                           _p(logits, C.c_float), _p(first, C.c_int32),
+                                           _p(toks, C.c_int32), _p(cnt, C.c_uint32)))
+        return logits, first, [toks[j, :cnt[j]].copy() for j in range(n)]
+
     def extend(self, kv: KVBatch, tokens, seg: int = 0):
         """ToyLm::extend on a fork of sealed segment `seg`; returns the last logits."""
         logits, _ = self.extend_members(kv, [seg], [tokens])
@@ -450,6 +469,11 @@ class SubgCacheResult:
     stage_ms: list
     prefill_rows: int
     extend_rows: int
+    # with max_new > 1 (batched greedy decode): generated ids per query, submission -> last token
+    tokens: list | None = None
+    rt_ms: np.ndarray | None = None
+    decode_ms: float = 0.0
+    decode_rows: int = 0
 
 
 class PreparedBatch:
@@ -505,7 +529,7 @@ def _device_copy(pb: "PreparedBatch"):
 def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
                   embeddings: np.ndarray | None = None, cluster_owner=None, rank: int = 0,
                   world_size: int = 1, want_logits: bool = True,
-                  device_inputs: bool = False, waves: int = 1) -> SubgCacheResult:
+                  device_inputs: bool = False, waves: int = 1, max_new: int = 0) -> SubgCacheResult:
     """pipeline.cpp:212-293 (SubgCache branch) + cache_engine.cpp:217-233 (run_batch), to the
     first token of every query."""
     w = pb.w
@@ -539,6 +563,7 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     b.rank = rank
     b.world_size = world_size
     b.waves = waves
+    b.max_new_tokens = max_new
     emb = np.zeros((m, d), np.float32)
     labels = np.zeros(m, np.uint32)
     nm = max(m - k, 1)
@@ -562,7 +587,21 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     o.logits = _p(logits, C.c_float)
     o.first_token = _p(first, C.c_int32)
     o.fallback = _p(fb, C.c_uint8)
+    toks = cnt = rt = None
+    if max_new > 1:
+        toks = np.full((m, max_new), -1, np.int32)
+        cnt = np.zeros(m, np.uint32)
+        rt = np.full(m, -1.0, np.float32)
+        o.tokens = _p(toks, C.c_int32)
+        o.n_tokens = _p(cnt, C.c_uint32)
+        o.rt_ms = _p(rt, C.c_float)
     check(ctx.lib.sgc_run_subgcache(ctx.h, model.h, g.h, C.byref(b), C.byref(o)))
-    return SubgCacheResult(emb, labels, left[: m - k], right[: m - k], dist[: m - k], plen, logits,
-                           first, fb, owner, ttft, o.waves, list(o.stage_ms)[:6], o.prefill_rows,
-                           o.extend_rows)
+    res = SubgCacheResult(emb, labels, left[: m - k], right[: m - k], dist[: m - k], plen, logits,
+                          first, fb, owner, ttft, o.waves, list(o.stage_ms)[:6], o.prefill_rows,
+                          o.extend_rows)
+    if max_new > 1:
+        res.tokens = [toks[q, :cnt[q]].copy() for q in range(m)]
+        res.rt_ms = rt
+        res.decode_ms = o.stage_ms[6]
+        res.decode_rows = o.decode_rows
+    return res

@@ -57,7 +57,8 @@ def c1_pipeline(td):
         [(q.id, q.question, q.answer) for q in qs]
     out = oracle.run_ref({"cmd": "pipeline", "nodes_csv": ref["nodes"], "edges_csv": ref["edges"],
                           "queries_jsonl": ref["queries"], "clusters": 4, "linkage": "ward",
-                          "seed": 7, "retrieval": "ego-topk", "run_batch": True})
+                          "seed": 7, "retrieval": "ego-topk", "run_batch": True,
+                          "engine_max_new": 32})
     out["graph"] = graph_json(g)
     out["queries"] = [[q.id, q.question.decode(), q.answer.decode()] for q in qs]
     out["config"] = {"clusters": 4, "linkage": "ward", "seed": 7, "lm": W.TINY_LM}
@@ -95,7 +96,7 @@ def lm_cases():
         total = int(rng.integers(2, 300))
         cut = int(rng.integers(1, total))
         toks = rng.integers(0, 256, total).tolist()
-        c = {"prefix": toks[:cut], "suffix": toks[cut:], "decode": 8}
+        c = {"prefix": toks[:cut], "suffix": toks[cut:], "decode": 8, "margins": True}
         if i % 3 == 0:
             c["collect"] = True
         if i % 4 == 1:
@@ -120,7 +121,10 @@ def lm_cases():
             total = int(rng.integers(40, 400))
             cut = int(rng.integers(1, total))
             toks = rng.integers(0, 256, total).tolist()
-            cs.append({"prefix": toks[:cut], "suffix": toks[cut:]})
+            cs.append({"prefix": toks[:cut], "suffix": toks[cut:], "decode": 8, "margins": True})
+        # copy pointer over a longer greedy decode (answer then EOS)
+        cs.append({"prefix": [256] + list(b"facts: the cords are blue, the lamp is teal. lamp?"),
+                   "suffix": list(b" answer:"), "decode": 8, "answer": list(b"teal")})
         out = oracle.run_ref({"cmd": "lm", "cfg": cfg, "cases": cs})
         dump(name, {"cfg": cfg, "cases": cs, "out": out})
 
