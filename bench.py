@@ -235,6 +235,7 @@ def run_ours(args, rank, world, local_rank):
                            max_new=mx)
         ev4, ev5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         rts, ntok, dec_ms, dec_rows = [], 0, 0.0, 0
+        ctx.set_timing(True)
         torch.cuda.synchronize()
         ev4.record(stream)
         for _ in range(args.gen_steps):
@@ -246,6 +247,8 @@ def run_ours(args, rank, world, local_rank):
             dec_rows += rg.decode_rows
         ev5.record(stream)
         torch.cuda.synchronize()
+        gkt = {k: ctx.kernel_time(k) for k in KERNEL_GROUPS}
+        ctx.set_timing(False)
         g_ms = ev4.elapsed_time(ev5) / args.gen_steps
         rt_all = np.concatenate(rts)
         gen = {"max_new_tokens": mx, "ms_per_batch": round(g_ms, 3),
@@ -255,6 +258,7 @@ def run_ours(args, rank, world, local_rank):
                "generated_tokens_per_s": round(ntok / args.gen_steps / (g_ms / 1e3), 1),
                "decode_stage_ms": round(dec_ms / args.gen_steps, 3),
                "decode_rows_per_batch": dec_rows // args.gen_steps,
+               "kernel_ms_per_batch": {k: round(v[0] / args.gen_steps, 3) for k, v in gkt.items() if v[1]},
                "steps": args.gen_steps,
                "semantics": "same batch to EOS / max_new (run() with ToyLmConfig::max_new_tokens); "
                             "rt = submission -> last token"}

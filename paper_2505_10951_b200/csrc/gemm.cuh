@@ -23,6 +23,14 @@ struct GemmEpi {
     const float* rope_sin = nullptr;
     int d = 0;
     int hd = 0;
+    // fused RMSNorm (lm_core.cpp:26-31, no gain): A holds bf16(x) UNnormalized and the epilogue
+    // scales each accumulator row by 1 / sqrt(in_ss[row] / norm_dim + 1e-5) (QKV, TANH, F32, BF16)
+    const float* in_ss = nullptr;
+    int norm_dim = 0;
+    // EPI_RESID producer side: also store bf16(x_new) to out_xb (ld = ldo) and accumulate the
+    // row's sum of squares of x_new into out_ss (zeroed by the caller) for the next GEMM
+    __nv_bfloat16* out_xb = nullptr;
+    float* out_ss = nullptr;
 };
 
 void gemm_bf16(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep);

@@ -85,7 +85,10 @@ __device__ __forceinline__ void rope_pair(float* lo, float* hi, const float* cos
 template <int BN, int EPI, int HD>
 __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool valid, int n0,
                                               const GemmEpi& ep) {
-            if constexpr (EPI == EPI_QKV) {
+    // fused RMSNorm of the A rows: one scale per accumulator row
+    float inv = 1.0f;
+    if (ep.in_ss && valid) inv = 1.0f / sqrtf(ep.in_ss[row] / static_cast<float>(ep.norm_dim) + 1e-5f);
+    if constexpr (EPI == EPI_QKV) {
         // one tile never straddles the q/k/v sections (d % BN == 0)
         const int d = ep.d;
         const int section = n0 / d;
@@ -102,9 +105,12 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                 uint32_t r[32];
                 ptx::tmem_ld32(tbase + ch * 32, r);
                 ptx::tmem_ld_wait();
-                if (valid)
-                    store_bf16x32(ep.v_cache + static_cast<size_t>(kvr) * d + c0 + ch * 32,
-                                  reinterpret_cast<float*>(r));
+                if (valid) {
+                    float* v = reinterpret_cast<float*>(r);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] *= inv;
+                    store_bf16x32(ep.v_cache + static_cast<size_t>(kvr) * d + c0 + ch * 32, v);
+                }
             }
         } else {
             __nv_bfloat16* dst = section == 0
@@ -129,6 +135,8 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                         for (int j = 0; j < 32; ++j) {
                             cs[j] = __ldg(cosp + in_head + j);
                             sn[j] = __ldg(sinp + in_head + j);
+                            reinterpret_cast<float*>(lo)[j] *= inv;
+                            reinterpret_cast<float*>(hi)[j] *= inv;
                         }
                         rope_pair(reinterpret_cast<float*>(lo), reinterpret_cast<float*>(hi),
                                   cs, sn);
@@ -145,6 +153,8 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                     ptx::tmem_ld_wait();
                     if (valid) {
                         float* v = reinterpret_cast<float*>(r);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] *= inv;
                         float o[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
@@ -162,6 +172,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
             }
         }
     } else {
+        float ss = 0.f;  // EPI_RESID with out_ss: this row's partial sum of squares of x_new
 #pragma unroll 1
         for (int ch = 0; ch < BN / 32; ++ch) {
             uint32_t r[32];
@@ -170,6 +181,12 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
             if (!valid) continue;
             float* v = reinterpret_cast<float*>(r);
             const int col = n0 + ch * 32;
+            if constexpr (EPI != EPI_RESID) {
+                if (ep.in_ss) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] *= inv;
+                }
+            }
             if constexpr (EPI == EPI_F32) {
                 float4* dst = reinterpret_cast<float4*>(
                     static_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ldo + col);
@@ -197,8 +214,20 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                     x.z += v[4 * q + 2];
                     x.w += v[4 * q + 3];
                     dst[q] = x;
+                    v[4 * q] = x.x;
+                    v[4 * q + 1] = x.y;
+                    v[4 * q + 2] = x.z;
+                    v[4 * q + 3] = x.w;
+                }
+                if (ep.out_xb) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) ss = fmaf(v[j], v[j], ss);
+                    store_bf16x32(ep.out_xb + static_cast<size_t>(row) * ep.ldo + col, v);
                 }
             }
+        }
+        if constexpr (EPI == EPI_RESID) {
+            if (ep.out_ss && valid) atomicAdd(ep.out_ss + row, ss);
         }
     }
 }

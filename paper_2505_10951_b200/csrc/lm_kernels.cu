@@ -32,9 +32,10 @@ __global__ void gen_projection_t(float* out_t, uint32_t dim, uint64_t state0) {
 }
 
 // embed_tokens (lm_core.cpp:163-173) + soft slot (:308-320): x[r] = tok_emb[id] or soft[s]
+// (+ the first layer's fused RMSNorm inputs: bf16(x) and the row's sum of squares)
 __global__ void embed_kernel(float* x, const int32_t* tokens, const float* tok_emb,
                              const float* soft, const int32_t* soft_idx, int d, int rows,
-                             int* bad) {
+                             int* bad, __nv_bfloat16* xb, float* ss_out) {
     int r = blockIdx.x;
     if (r >= rows) return;
     int id = tokens[r];
@@ -44,13 +45,34 @@ __global__ void embed_kernel(float* x, const int32_t* tokens, const float* tok_e
     } else {
         if (id < 0 || id >= SGC_VOCAB) {
             if (threadIdx.x == 0) atomicExch(bad, 1);
-            return;
+            src = tok_emb;  // keep the block convergent; the batch fails after the forward
+        } else {
+            src = tok_emb + static_cast<size_t>(id) * d;
         }
-        src = tok_emb + static_cast<size_t>(id) * d;
     }
-    for (int i = threadIdx.x; i < d / 4; i += blockDim.x)
-        reinterpret_cast<float4*>(x + static_cast<size_t>(r) * d)[i] =
-            reinterpret_cast<const float4*>(src)[i];
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+        const float4 v = reinterpret_cast<const float4*>(src)[i];
+        reinterpret_cast<float4*>(x + static_cast<size_t>(r) * d)[i] = v;
+        if (xb) {
+            ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+            __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&a);
+            pk.y = *reinterpret_cast<uint32_t*>(&b);
+            reinterpret_cast<uint2*>(xb + static_cast<size_t>(r) * d)[i] = pk;
+        }
+    }
+    if (!xb) return;
+    __shared__ float red[32];
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+    if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) t += red[w];
+        ss_out[r] = t;
+    }
 }
 
 // rmsnorm (lm_core.cpp:26-31): out = bf16(x / sqrt(mean(x^2) + 1e-5)), one CTA per row
@@ -249,10 +271,10 @@ void gen_text_projection_t(Ctx* c, float* out_t, uint32_t dim, uint64_t state0) 
     SGC_LAUNCH_CHECK(c);
 }
 void embed(Ctx* c, float* x, const int32_t* tokens, const float* tok_emb, const float* soft,
-           const int32_t* soft_idx, int d, int rows, int* bad) {
+           const int32_t* soft_idx, int d, int rows, int* bad, __nv_bfloat16* xb, float* ss) {
     if (rows <= 0) return;
     Ctx::Timed timer(c, "embed");
-    embed_kernel<<<rows, 128, 0, c->stream>>>(x, tokens, tok_emb, soft, soft_idx, d, rows, bad);
+    embed_kernel<<<rows, 128, 0, c->stream>>>(x, tokens, tok_emb, soft, soft_idx, d, rows, bad, xb, ss);
     SGC_LAUNCH_CHECK(c);
 }
 void rmsnorm_bf16(Ctx* c, __nv_bfloat16* out, const float* x, int d, int rows) {

@@ -9,7 +9,8 @@ void gen_uniform(Ctx* c, float* out, uint64_t n, uint64_t state0, float lo, floa
 void gen_uniform(Ctx* c, __nv_bfloat16* out, uint64_t n, uint64_t state0, float lo, float hi);
 void gen_text_projection_t(Ctx* c, float* out_t, uint32_t dim, uint64_t state0);
 void embed(Ctx* c, float* x, const int32_t* tokens, const float* tok_emb, const float* soft,
-           const int32_t* soft_idx, int d, int rows, int* bad);
+           const int32_t* soft_idx, int d, int rows, int* bad, __nv_bfloat16* xb = nullptr,
+           float* ss = nullptr);
 void rmsnorm_bf16(Ctx* c, __nv_bfloat16* out, const float* x, int d, int rows);
 void head_logits(Ctx* c, float* logits, const float* x, const int32_t* rows, int n,
                  const float* head_t, int d);
