@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "per-query TTFT (p50) and queries/s vs CPU ref; fraction of tensor/HBM roofline"
 # every kernel launch of the library is bracketed by CUDA events under one of these names
-KERNEL_GROUPS = ["gemm", "attention", "rmsnorm", "embed", "head", "first_token", "gnn_encode",
+KERNEL_GROUPS = ["gemm", "attention", "attn_decode", "rmsnorm", "embed", "head", "first_token", "gnn_encode",
                  "text_features", "pairwise", "agglomerate", "union_prompt", "prompt_gather"]
 
 

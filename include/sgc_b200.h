@@ -268,7 +268,10 @@ int sgc_attention_bf16(sgc_ctx* ctx, const void* q, const void* k_pfx, const voi
                        void* out);
 /* Enable/disable per-kernel CUDA-event timing; sgc_get_timing reads the accumulated totals. */
 int sgc_set_timing(sgc_ctx* ctx, int enable);
-/* Tuning knobs: "gemm_pairs" (1 = CTA-pair tcgen05 GEMM for 256-wide tiles, default; 0 = 1-CTA). */
+/* Tuning knobs: "gemm_pairs" (1 = CTA-pair tcgen05 GEMM for 256-wide tiles, default; 0 = 1-CTA);
+ * "decode_defer_pct" (generation: a wave decodes on its own until fewer than this percentage of
+ * its queries still generate, the stragglers of every wave then finish in one shared loop;
+ * default 25, 0 = each wave to completion, >= 100 = all decoding after the last wave). */
 int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value);
 int sgc_get_timing(sgc_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches);
 

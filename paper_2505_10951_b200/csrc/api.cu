@@ -164,8 +164,10 @@ struct sgc_kv {
     int32_t* d_tokens = nullptr;  // context token ids (prefix, incl. soft slot)
     uint64_t* d_tok_off = nullptr;
     bool owns_kv = true;          // false: K/V live in the context's reusable KV arena
-    bf16* k_layer(int l) const { return k + static_cast<size_t>(l) * rows * model->d; }
-    bf16* v_layer(int l) const { return v + static_cast<size_t>(l) * rows * model->d; }
+    uint64_t lstride = 0;         // rows per layer of the underlying buffer (0: rows)
+    size_t layer_elems() const { return static_cast<size_t>(lstride ? lstride : rows) * model->d; }
+    bf16* k_layer(int l) const { return k + l * layer_elems(); }
+    bf16* v_layer(int l) const { return v + l * layer_elems(); }
 };
 
 namespace {
@@ -357,7 +359,8 @@ std::vector<sgc::AttnWork> make_work(const std::vector<int>& group_start, const 
 // ============================================================ prefill / extend
 
 sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in, const int32_t* tok_in,
-                   const float* soft, const uint8_t* soft_mask, float* last_logits, bool arena = false) {
+                   const float* soft, const uint8_t* soft_mask, float* last_logits, bool arena = false,
+                   uint64_t arena_row0 = 0, uint64_t arena_rows = 0) {
     std::vector<uint64_t> off = to_host(c, off_in, count + 1);
     std::vector<int32_t> toks = to_host(c, tok_in, off[count]);
     std::vector<uint8_t> smask = soft_mask ? to_host(c, soft_mask, count) : std::vector<uint8_t>(count, 0);
@@ -397,9 +400,16 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
     }
     const int M = static_cast<int>(rows_tok.size());
     kv->rows = M;
-    if (arena) {  // batch-internal sealed prefixes: grow-only arena, no per-wave (re)mapping
-        kv->k = c->buf<bf16>("kv_arena_k", static_cast<size_t>(m->L) * M * d);
-        kv->v = c->buf<bf16>("kv_arena_v", static_cast<size_t>(m->L) * M * d);
+    if (arena) {
+        // batch-internal sealed prefixes: one grow-only arena [L][arena_rows][d] holding every
+        // wave's prefixes at row offsets (arena_rows == 0: just this call's rows)
+        const uint64_t total = arena_rows ? arena_rows : static_cast<uint64_t>(M);
+        if (arena_row0 + static_cast<uint64_t>(M) > total) fail(SGC_LOGIC, "KV arena overflow");
+        bf16* ak = c->buf<bf16>("kv_arena_k", static_cast<size_t>(m->L) * total * d);
+        bf16* av = c->buf<bf16>("kv_arena_v", static_cast<size_t>(m->L) * total * d);
+        kv->k = ak + arena_row0 * d;
+        kv->v = av + arena_row0 * d;
+        kv->lstride = total;
         kv->owns_kv = false;
     } else {
         kv->k = dalloc<bf16>(c, static_cast<size_t>(m->L) * M * d);
@@ -457,10 +467,11 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
 // Optional output of do_extend for a following decode: the members' question K/V kept for all
 // layers (instead of a per-layer scratch) and the copy-pointer decision per member.
 struct ExtendKeep {
-    bf16* k = nullptr;  // [L][rows][d]
+    bf16* k = nullptr;  // [L][rows][d]; preset by the caller to share one buffer across calls
     bf16* v = nullptr;
-    uint64_t rows = 0;
-    std::vector<int32_t> q_lo;  // per member (input order): first question row
+    uint64_t rows = 0;  // rows per layer of the buffer
+    uint64_t base = 0;  // first row used by this call
+    std::vector<int32_t> q_lo;  // per member (input order): first question row (absolute)
     std::vector<int8_t> hint;   // per member: answer found in the prefix (lm_core.cpp:361-374)
 };
 
@@ -495,13 +506,18 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
     std::vector<int32_t> first_h(first_out ? n : 0);
     std::vector<float> logits_h(logits_out ? static_cast<size_t>(n) * SGC_VOCAB : 0);
     if (keep) {
-        keep->rows = qo[n];
-        keep->k = c->buf<bf16>("ex_keep_k", static_cast<size_t>(m->L) * keep->rows * d);
-        keep->v = c->buf<bf16>("ex_keep_v", static_cast<size_t>(m->L) * keep->rows * d);
+        if (!keep->k) {
+            keep->rows = qo[n];
+            keep->base = 0;
+            keep->k = c->buf<bf16>("ex_keep_k", static_cast<size_t>(m->L) * keep->rows * d);
+            keep->v = c->buf<bf16>("ex_keep_v", static_cast<size_t>(m->L) * keep->rows * d);
+        } else if (keep->base + qo[n] > keep->rows) {
+            fail(SGC_LOGIC, "question KV buffer overflow");
+        }
         keep->q_lo.assign(n, 0);
         keep->hint.assign(n, 0);
     }
-    uint64_t chunk0 = 0;  // first kept row of the chunk
+    uint64_t chunk0 = keep ? keep->base : 0;  // first kept row of the chunk
     size_t i0 = 0;
     while (i0 < n) {
         // chunk [i0, i1) with <= max_rows rows
@@ -625,68 +641,97 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
 // extend). Stops per member on EOS, after max_new tokens, or when the context is full; the
 // copy pointer biases answer[t] (then EOS) when the answer occurs in the prefix.
 struct GenJob {
-    std::vector<int32_t> pfx_kv0, pfx_len, q_lo, q_n, pos0, first;
+    std::vector<int32_t> pfx_kv0, pfx_len, q_lo, q_n, pos0, first, gen_row0;
     std::vector<int8_t> hint;
     std::vector<uint64_t> a_off{0};
     std::vector<int32_t> a_tok;
     uint32_t size() const { return static_cast<uint32_t>(first.size()); }
 };
-struct GenResult {
-    std::vector<int32_t> tokens;    // [n * max_new], -1 padded
-    std::vector<uint32_t> count;    // tokens per member
-    std::vector<int32_t> last_step; // step index of each member's last token
-    std::vector<cudaEvent_t> step_end;  // event after step t (t >= 1), index t - 1
+// progress of every member of a GenJob (resumable: a wave may defer its stragglers)
+struct GenState {
+    uint32_t max_new = 1;
+    std::vector<int32_t> tokens;  // [n * max_new], -1 padded
+    std::vector<uint32_t> count;  // tokens so far
+    std::vector<uint8_t> done;
+    std::vector<int32_t> last_ev;  // event index of the member's last token (-1: the first token)
+    std::vector<cudaEvent_t> events;  // one per decode step
     uint64_t rows = 0;
+    void init(const GenJob& job, uint32_t mx, uint64_t max_seq) {
+        const uint32_t n = job.size();
+        max_new = std::max<uint32_t>(1, mx);
+        tokens.assign(static_cast<size_t>(n) * max_new, -1);
+        count.assign(n, 1);
+        done.assign(n, 0);
+        last_ev.assign(n, -1);
+        for (uint32_t j = 0; j < n; ++j) {
+            tokens[static_cast<size_t>(j) * max_new] = job.first[j];
+            done[j] = max_new <= 1 || job.first[j] == SGC_EOS || static_cast<uint64_t>(job.pos0[j]) + 1 > max_seq;
+        }
+    }
+};
+// Decode buffers shared by every step of a batch: the prefix KV view (all sealed prefixes the
+// job's pfx_kv0 index), the kept question K/V and the generated-token K/V, each [L][rows][d].
+struct GenBuffers {
+    const sgc_kv* pfx = nullptr;
+    const ExtendKeep* keep = nullptr;
+    bf16 *gk = nullptr, *gv = nullptr;
+    size_t grows = 0;
+    int8_t* d_hint = nullptr;
+    uint64_t* d_aoff = nullptr;
+    int32_t* d_atok = nullptr;
 };
 
-GenResult do_decode(Ctx* c, sgc_model* m, const sgc_kv* kv, const ExtendKeep* keep, const GenJob& job,
-                    uint32_t max_new, float bonus) {
+GenBuffers gen_buffers(Ctx* c, sgc_model* m, const sgc_kv* pfx, const ExtendKeep* keep, const GenJob& job,
+                       size_t gen_rows) {
+    GenBuffers g;
+    g.pfx = pfx;
+    g.keep = keep;
+    g.grows = std::max<size_t>(1, gen_rows);
+    g.gk = c->buf<bf16>("dec_gk", static_cast<size_t>(m->L) * g.grows * m->d);
+    g.gv = c->buf<bf16>("dec_gv", static_cast<size_t>(m->L) * g.grows * m->d);
     const uint32_t n = job.size();
+    g.d_hint = c->buf<int8_t>("dec_hint", n);
+    g.d_aoff = c->buf<uint64_t>("dec_aoff", n + 1);
+    g.d_atok = c->buf<int32_t>("dec_atok", std::max<size_t>(1, job.a_tok.size()));
+    sgc::copy_in(c, g.d_hint, job.hint.data(), n);
+    sgc::copy_in(c, g.d_aoff, job.a_off.data(), n + 1);
+    sgc::copy_in(c, g.d_atok, job.a_tok.data(), job.a_tok.size());
+    return g;
+}
+
+// Runs decode steps for members `sel` of the job until all are done, or until fewer than
+// `min_active` of them are still generating (the rest stay pending in `st`).
+void decode_steps(Ctx* c, sgc_model* m, const GenBuffers& g, const GenJob& job, GenState& st,
+                  const std::vector<uint32_t>& sel, uint32_t min_active, float bonus) {
     const int d = m->d;
-    GenResult r;
-    r.tokens.assign(static_cast<size_t>(n) * max_new, -1);
-    r.count.assign(n, 0);
-    r.last_step.assign(n, 0);
-    std::vector<uint8_t> done(n, 0);
+    const uint32_t max_new = st.max_new;
     const uint64_t max_seq = m->cfg.max_seq_len;
-    for (uint32_t j = 0; j < n; ++j) {
-        r.tokens[static_cast<size_t>(j) * max_new] = job.first[j];
-        r.count[j] = 1;
-        done[j] = max_new <= 1 || job.first[j] == SGC_EOS || static_cast<uint64_t>(job.pos0[j]) + 1 > max_seq;
-    }
-    if (max_new <= 1 || n == 0) return r;
-    // generated K/V: member j's token t-1 at row j*max_new + t-1, all layers
-    const size_t grows = static_cast<size_t>(n) * max_new;
-    bf16* gk = c->buf<bf16>("dec_gk", static_cast<size_t>(m->L) * grows * d);
-    bf16* gv = c->buf<bf16>("dec_gv", static_cast<size_t>(m->L) * grows * d);
-    int8_t* d_hint = c->buf<int8_t>("dec_hint", n);
-    uint64_t* d_aoff = c->buf<uint64_t>("dec_aoff", n + 1);
-    int32_t* d_atok = c->buf<int32_t>("dec_atok", std::max<size_t>(1, job.a_tok.size()));
-    sgc::copy_in(c, d_hint, job.hint.data(), n);
-    sgc::copy_in(c, d_aoff, job.a_off.data(), n + 1);
-    sgc::copy_in(c, d_atok, job.a_tok.data(), job.a_tok.size());
     const int tile = attn_tile(m->hd);
-    for (uint32_t t = 1; t < max_new; ++t) {
+    const sgc_kv* kv = g.pfx;
+    for (;;) {
         std::vector<int32_t> act;
-        for (uint32_t j = 0; j < n; ++j)
-            if (!done[j]) act.push_back(static_cast<int32_t>(j));
-        if (act.empty()) break;
+        for (uint32_t j : sel)
+            if (!st.done[j]) act.push_back(static_cast<int32_t>(j));
+        if (act.empty() || act.size() < min_active) break;
         const int M = static_cast<int>(act.size());
-        // rows: ascending member index == grouped by prefix segment (members are sorted by it)
-        std::vector<int32_t> tok(M), pos(M), kvr(M), step(M, static_cast<int32_t>(t)), lrow(M);
-        std::vector<int32_t> plo(M), pn(M), qlo(M), qn(M), glo(M), gn(M, static_cast<int32_t>(t));
+        // rows follow `sel` order == grouped by prefix segment
+        std::vector<int32_t> tok(M), pos(M), kvr(M), step(M), lrow(M);
+        std::vector<int32_t> plo(M), pn(M), qlo(M), qn(M), glo(M), gn(M);
         std::vector<sgc::AttnWork> work;
         for (int i = 0; i < M; ++i) {
             const int32_t j = act[i];
-            tok[i] = r.tokens[static_cast<size_t>(j) * max_new + t - 1];
-            pos[i] = job.pos0[j] + static_cast<int32_t>(t) - 1;
-            kvr[i] = j * static_cast<int32_t>(max_new) + static_cast<int32_t>(t) - 1;
+            const int32_t t = static_cast<int32_t>(st.count[j]);  // index of the token produced now
+            tok[i] = st.tokens[static_cast<size_t>(j) * max_new + t - 1];
+            pos[i] = job.pos0[j] + t - 1;
+            kvr[i] = job.gen_row0[j] + t - 1;
+            step[i] = t;
             lrow[i] = i;
             plo[i] = job.pfx_kv0[j];
             pn[i] = job.pfx_len[j];
             qlo[i] = job.q_lo[j];
             qn[i] = job.q_n[j];
-            glo[i] = j * static_cast<int32_t>(max_new);
+            glo[i] = job.gen_row0[j];
+            gn[i] = t;
             if (work.empty() || work.back().pfx_kv0 != plo[i] || work.back().nrows == tile)
                 work.push_back({i, 0, plo[i], pn[i]});
             work.back().nrows++;
@@ -710,9 +755,9 @@ GenResult do_decode(Ctx* c, sgc_model* m, const sgc_kv* kv, const ExtendKeep* ke
         dr.g_lo = col(9);
         dr.g_n = col(10);
         {
-            const size_t ls = static_cast<size_t>(keep ? keep->rows : 0) * d;
-            const bf16* qk = keep ? keep->k : nullptr;
-            const bf16* qv = keep ? keep->v : nullptr;
+            const size_t ls = static_cast<size_t>(g.keep ? g.keep->rows : 0) * d;
+            const bf16* qk = g.keep ? g.keep->k : nullptr;
+            const bf16* qv = g.keep ? g.keep->v : nullptr;
             dr.k_q = [qk, ls](int l) { return qk ? qk + l * ls : nullptr; };
             dr.v_q = [qv, ls](int l) { return qv ? qv + l * ls : nullptr; };
         }
@@ -727,6 +772,8 @@ GenResult do_decode(Ctx* c, sgc_model* m, const sgc_kv* kv, const ExtendKeep* ke
         b.pfx_rows = static_cast<int>(kv->rows);
         b.k_pfx = [kv](int l) { return static_cast<const bf16*>(kv->k_layer(l)); };
         b.v_pfx = [kv](int l) { return static_cast<const bf16*>(kv->v_layer(l)); };
+        bf16 *gk = g.gk, *gv = g.gv;
+        const size_t grows = g.grows;
         b.k_loc = [gk, grows, d](int l) { return gk + l * grows * d; };
         b.v_loc = [gv, grows, d](int l) { return gv + l * grows * d; };
         b.dec = &dr;
@@ -734,25 +781,26 @@ GenResult do_decode(Ctx* c, sgc_model* m, const sgc_kv* kv, const ExtendKeep* ke
         b.n_logits = M;
         b.d_logits = d_logits;
         forward_rows(c, m, b);
-        sgc::step_tokens(c, d_tok_out, d_logits, M, d_hint, d_atok, d_aoff, col(11), col(3), bonus);
+        sgc::step_tokens(c, d_tok_out, d_logits, M, g.d_hint, g.d_atok, g.d_aoff, col(11), col(3), bonus);
         cudaEvent_t ev = c->event();
         SGC_CUDA_CHECK(cudaEventRecord(ev, c->stream));
-        r.step_end.push_back(ev);
+        const int32_t ev_idx = static_cast<int32_t>(st.events.size());
+        st.events.push_back(ev);
         std::vector<int32_t> out(M);
         sgc::copy_out(c, out.data(), d_tok_out, M);
         c->sync();
-        r.rows += static_cast<uint64_t>(M);
+        st.rows += static_cast<uint64_t>(M);
         for (int i = 0; i < M; ++i) {
             const int32_t j = act[i];
-            r.tokens[static_cast<size_t>(j) * max_new + t] = out[i];
-            r.count[j] = t + 1;
-            r.last_step[j] = static_cast<int32_t>(t);
+            const uint32_t t = st.count[j];
+            st.tokens[static_cast<size_t>(j) * max_new + t] = out[i];
+            st.count[j] = t + 1;
+            st.last_ev[j] = ev_idx;
             // stop rules after emitting token t (lm_core.cpp:387-389)
             if (out[i] == SGC_EOS || t + 1 == max_new || static_cast<uint64_t>(job.pos0[j]) + t + 1 > max_seq)
-                done[j] = 1;
+                st.done[j] = 1;
         }
     }
-    return r;
 }
 
 // ============================================================ graph-side helpers
@@ -1626,11 +1674,18 @@ int sgc_extend_generate(sgc_ctx* ctx, sgc_model* model, sgc_kv* kv, const uint32
             job.first.push_back(first[j]);
             job.hint.push_back(keep.hint[j]);
         }
-        GenResult r = do_decode(c, model, kv, &keep, job, std::max<uint32_t>(1, max_new), pointer_bonus);
-        for (cudaEvent_t e : r.step_end) c->event_pool.push_back(e);
+        const uint32_t mx = std::max<uint32_t>(1, max_new);
+        for (uint32_t j = 0; j < n; ++j) job.gen_row0.push_back(static_cast<int32_t>(j * mx));
+        GenState st;
+        st.init(job, mx, model->cfg.max_seq_len);
+        GenBuffers gb = gen_buffers(c, model, kv, &keep, job, static_cast<size_t>(n) * mx);
+        std::vector<uint32_t> all(n);
+        std::iota(all.begin(), all.end(), 0u);
+        decode_steps(c, model, gb, job, st, all, 0, pointer_bonus);
+        for (cudaEvent_t e : st.events) c->event_pool.push_back(e);
         if (first_token) sgc::copy_in(c, first_token, first.data(), n);
-        if (tokens) sgc::copy_in(c, tokens, r.tokens.data(), r.tokens.size());
-        if (n_tokens) sgc::copy_in(c, n_tokens, r.count.data(), n);
+        if (tokens) sgc::copy_in(c, tokens, st.tokens.data(), st.tokens.size());
+        if (n_tokens) sgc::copy_in(c, n_tokens, st.count.data(), n);
         c->sync();
     });
 }
@@ -1777,7 +1832,63 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         double pf_ms = 0, ex_ms = 0, dec_ms = 0;
         const uint32_t max_new = b->max_new_tokens;
         const bool gen_on = max_new > 1;
-        std::vector<cudaEvent_t> rt_event(m, nullptr), dec_events;
+        std::vector<int32_t> wave_of_job;  // decode job index -> wave
+        // ---- row budget of every wave: prefill rows (representatives + standalone fallbacks)
+        // and kept question rows; with generation the waves' prefix / question K/V stay resident
+        // until the end so stragglers of every wave decode together (one weight pass per step)
+        std::vector<uint64_t> wave_pf(wave_end.size(), 0), wave_qr(wave_end.size(), 0);
+        {
+            uint32_t w0 = 0;
+            for (uint32_t wv = 0; wv < wave_end.size(); ++wv) {
+                for (uint32_t i = w0; i < wave_end[wv]; ++i) {
+                    const uint64_t plen = reps.prefix_off[i + 1] - reps.prefix_off[i] + (d_soft ? 1 : 0);
+                    wave_pf[wv] += plen;
+                    for (uint32_t q : own_members[i]) {
+                        const uint64_t qn = q_off[q + 1] - q_off[q];
+                        if (plen + qn + lc.max_new_tokens > lc.max_seq_len) {
+                            if (b->own_prefix.count != m) fail(SGC_DOMAIN, "fallback needs own_prefix token lists");
+                            if (oo.empty()) {
+                                oo = to_host(c, b->own_prefix.off, m + 1);
+                                ot = to_host(c, b->own_prefix.tokens, oo[m]);
+                            }
+                            size_t allowed = lc.max_seq_len;
+                            allowed -= std::min<size_t>(allowed, lc.max_new_tokens + (b->soft_prefix ? 1 : 0));
+                            wave_pf[wv] += std::min<uint64_t>(oo[q + 1] - oo[q] + qn, allowed) + (b->soft_prefix ? 1 : 0);
+                        } else {
+                            wave_qr[wv] += qn;
+                        }
+                    }
+                }
+                w0 = wave_end[wv];
+            }
+        }
+        uint64_t pf_total = 0, qr_total = 0, pf_max = 0, qr_max = 0;
+        for (size_t w = 0; w < wave_end.size(); ++w) {
+            pf_total += wave_pf[w];
+            qr_total += wave_qr[w];
+            pf_max = std::max(pf_max, wave_pf[w]);
+            qr_max = std::max(qr_max, wave_qr[w]);
+        }
+        // retain every wave's K/V only when generating and it fits comfortably (C3: ~45 GB)
+        const double kv_row_bytes = 2.0 * model->L * d * sizeof(bf16);
+        const bool retain = gen_on && (pf_total + qr_total + static_cast<double>(m) * max_new) * kv_row_bytes < 96e9;
+        const uint64_t arena_rows = retain ? pf_total : pf_max;
+        ExtendKeep keep_all;
+        if (gen_on) {
+            keep_all.rows = std::max<uint64_t>(1, retain ? qr_total : qr_max);
+            keep_all.k = c->buf<bf16>("ex_keep_k", static_cast<size_t>(model->L) * keep_all.rows * d);
+            keep_all.v = c->buf<bf16>("ex_keep_v", static_cast<size_t>(model->L) * keep_all.rows * d);
+        }
+        // stragglers: a wave stops decoding on its own once fewer than this many of its queries
+        // are still generating; they finish in one shared loop after the last wave
+        const uint32_t defer_pct = retain ? c->decode_defer_pct : 0;
+        GenJob gj;                  // every query served here, in wave order
+        GenState gst;
+        gst.max_new = std::max<uint32_t>(1, max_new);
+        std::vector<uint32_t> gen_q;  // job index -> query
+        sgc_kv kv_all;                // view over the whole arena (the decode's prefix base)
+        kv_all.model = model;
+        uint64_t arena_row0 = 0, keep_row0 = 0;
         uint32_t wb = 0;
         for (uint32_t wv = 0; wv < wave_end.size(); ++wv) {
             const uint32_t we = wave_end[wv];
@@ -1790,9 +1901,10 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             std::vector<uint32_t> mem_seg, mem_q;  // extend members (segment index within the wave)
             std::vector<uint32_t> fb_q;            // fallback queries -> their standalone sequence
             std::vector<uint64_t> fb_seq;
-            GenJob gj;                             // the wave's decode rows (members, then fallbacks)
-            std::vector<uint32_t> gen_q;
-            ExtendKeep keep;
+            const uint32_t job0 = gj.size();  // this wave's decode rows: job0 .. (members, then fallbacks)
+            ExtendKeep keep = keep_all;
+            keep.base = retain ? keep_row0 : 0;
+            if (!retain) arena_row0 = 0;
             for (uint32_t i = wb; i < we; ++i) {
                 seq_tok.insert(seq_tok.end(), rep_tok.begin() + reps.prefix_off[i], rep_tok.begin() + reps.prefix_off[i + 1]);
                 seq_off.push_back(seq_tok.size());
@@ -1815,11 +1927,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             // standalone path for fallbacks (cache_engine.cpp:112-138): own prompt + question, trimmed
             if (!fb_q.empty()) {
                 if (b->own_prefix.count != m) fail(SGC_DOMAIN, "fallback needs own_prefix token lists");
-                if (oo.empty()) {
-                    oo = to_host(c, b->own_prefix.off, m + 1);
-                    ot = to_host(c, b->own_prefix.tokens, oo[m]);
-                    if (b->soft_prefix) emb_h = to_host(c, d_emb, static_cast<size_t>(m) * d);
-                }
+                if (b->soft_prefix && emb_h.empty()) emb_h = to_host(c, d_emb, static_cast<size_t>(m) * d);
                 for (uint32_t q : fb_q) {
                     std::vector<int32_t> full(ot.begin() + oo[q], ot.begin() + oo[q + 1]);
                     full.insert(full.end(), q_tok.begin() + q_off[q], q_tok.begin() + q_off[q + 1]);
@@ -1837,9 +1945,16 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             const uint32_t ns = static_cast<uint32_t>(seq_off.size() - 1);
             std::vector<float> seq_logits(static_cast<size_t>(ns) * SGC_VOCAB);
             sgc_kv* kv = do_prefill(c, model, ns, seq_off.data(), seq_tok.data(), seq_soft_vec.data(),
-                                    seq_soft.data(), seq_logits.data(), /*arena=*/true);
+                                    seq_soft.data(), seq_logits.data(), /*arena=*/true, arena_row0, arena_rows);
             std::unique_ptr<sgc_kv, int (*)(sgc_kv*)> kv_guard(kv, sgc_kv_release);
             prefill_rows += kv->rows;
+            const int32_t pfx_base = static_cast<int32_t>(arena_row0);  // absolute arena row of this wave
+            if (!kv_all.k) {
+                kv_all.k = kv->k - arena_row0 * d;
+                kv_all.v = kv->v - arena_row0 * d;
+                kv_all.rows = arena_rows;
+                kv_all.lstride = arena_rows;
+            }
             const double tw1 = now_ms();
             pf_ms += tw1 - tw0;
             // ---- (5) per-query reuse: every member of the wave's clusters in one cascade pass
@@ -1864,12 +1979,13 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                     if (gen_on) {
                         const int32_t S = static_cast<int32_t>(q_off[q + 1] - q_off[q]);
                         gen_q.push_back(q);
-                        gj.pfx_kv0.push_back(static_cast<int32_t>(kv->off[mem_seg[j]]));
+                        gj.pfx_kv0.push_back(pfx_base + static_cast<int32_t>(kv->off[mem_seg[j]]));
                         gj.pfx_len.push_back(static_cast<int32_t>(kv->len[mem_seg[j]]));
                         gj.q_lo.push_back(keep.q_lo[j]);
                         gj.q_n.push_back(S);
                         gj.pos0.push_back(static_cast<int32_t>(kv->len[mem_seg[j]]) + S);
                         gj.first.push_back(ft[j]);
+                        gj.gen_row0.push_back(static_cast<int32_t>(q * gst.max_new));
                         gj.hint.push_back(keep.hint[j]);
                         if (ans) gj.a_tok.insert(gj.a_tok.end(), a_tok.begin() + a_off[q], a_tok.begin() + a_off[q + 1]);
                         gj.a_off.push_back(gj.a_tok.size());
@@ -1913,12 +2029,13 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 if (o->fallback) o->fallback[q] = 1;
                 if (gen_on) {  // standalone decode continues from its own sealed prompt
                     gen_q.push_back(q);
-                    gj.pfx_kv0.push_back(static_cast<int32_t>(kv->off[s]));
+                    gj.pfx_kv0.push_back(pfx_base + static_cast<int32_t>(kv->off[s]));
                     gj.pfx_len.push_back(static_cast<int32_t>(kv->len[s]));
                     gj.q_lo.push_back(0);
                     gj.q_n.push_back(0);
                     gj.pos0.push_back(static_cast<int32_t>(kv->len[s]));
                     gj.first.push_back(best);
+                    gj.gen_row0.push_back(static_cast<int32_t>(q * gst.max_new));
                     gj.hint.push_back(target >= 0 ? 1 : 0);
                     if (ans) gj.a_tok.insert(gj.a_tok.end(), a_tok.begin() + a_off[q], a_tok.begin() + a_off[q + 1]);
                     gj.a_off.push_back(gj.a_tok.size());
@@ -1929,22 +2046,62 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             ev_wave.push_back(e);
             ex_ms += now_ms() - tw1;
             // ---- (6) batched greedy decode of the wave's queries (RT)
-            if (gen_on && gj.size() > 0) {
+            if (gen_on && gj.size() > job0) {
                 const double td0 = now_ms();
-                GenResult gr = do_decode(c, model, kv, keep.k ? &keep : nullptr, gj, max_new, b->pointer_bonus);
-                decode_rows += gr.rows;
-                for (uint32_t j = 0; j < gj.size(); ++j) {
-                    const uint32_t q = gen_q[j];
-                    if (o->tokens)
-                        std::memcpy(o->tokens + static_cast<size_t>(q) * max_new, gr.tokens.data() + static_cast<size_t>(j) * max_new,
-                                    max_new * sizeof(int32_t));
-                    if (o->n_tokens) o->n_tokens[q] = gr.count[j];
-                    rt_event[q] = gr.last_step[j] > 0 ? gr.step_end[gr.last_step[j] - 1] : e;
+                // new members' state (first token already produced)
+                const uint64_t max_seq = lc.max_seq_len;
+                for (uint32_t j = job0; j < gj.size(); ++j) {
+                    gst.tokens.resize(static_cast<size_t>(j + 1) * gst.max_new, -1);
+                    gst.tokens[static_cast<size_t>(j) * gst.max_new] = gj.first[j];
+                    gst.count.push_back(1);
+                    gst.done.push_back(gst.max_new <= 1 || gj.first[j] == SGC_EOS ||
+                                       static_cast<uint64_t>(gj.pos0[j]) + 1 > max_seq);
+                    gst.last_ev.push_back(-1);
                 }
-                for (cudaEvent_t se : gr.step_end) dec_events.push_back(se);
+                std::vector<uint32_t> sel;
+                for (uint32_t j = job0; j < gj.size(); ++j) sel.push_back(j);
+                const uint32_t min_active = static_cast<uint32_t>((static_cast<uint64_t>(sel.size()) * defer_pct + 99) / 100);
+                sgc_kv wave_view = kv_all;
+                if (!retain) {  // this wave's prefixes only (the arena is reused by the next wave)
+                    wave_view = *kv;
+                    wave_view.off.clear();
+                    wave_view.len.clear();
+                    wave_view.d_tokens = nullptr;
+                    wave_view.d_tok_off = nullptr;
+                    for (uint32_t j = job0; j < gj.size(); ++j) gj.pfx_kv0[j] -= pfx_base;
+                }
+                GenBuffers gb = gen_buffers(c, model, &wave_view, &keep_all, gj, static_cast<size_t>(m) * gst.max_new);
+                decode_steps(c, model, gb, gj, gst, sel, min_active, b->pointer_bonus);
                 dec_ms += now_ms() - td0;
             }
+            for (uint32_t j = job0; j < gj.size(); ++j) wave_of_job.push_back(static_cast<int32_t>(wv));
+            if (retain) {
+                arena_row0 += kv->rows;
+                keep_row0 += wave_qr[wv];
+            }
             wb = we;
+        }
+        // ---- stragglers of every wave, one shared decode loop (retained K/V)
+        if (gen_on && retain) {
+            std::vector<uint32_t> rest;
+            for (uint32_t j = 0; j < gj.size(); ++j)
+                if (!gst.done[j]) rest.push_back(j);
+            if (!rest.empty()) {
+                const double td0 = now_ms();
+                GenBuffers gb = gen_buffers(c, model, &kv_all, &keep_all, gj, static_cast<size_t>(m) * gst.max_new);
+                decode_steps(c, model, gb, gj, gst, rest, 0, b->pointer_bonus);
+                dec_ms += now_ms() - td0;
+            }
+        }
+        if (gen_on) {
+            decode_rows = gst.rows;
+            for (uint32_t j = 0; j < gj.size(); ++j) {
+                const uint32_t q = gen_q[j];
+                if (o->tokens)
+                    std::memcpy(o->tokens + static_cast<size_t>(q) * max_new, gst.tokens.data() + static_cast<size_t>(j) * max_new,
+                                max_new * sizeof(int32_t));
+                if (o->n_tokens) o->n_tokens[q] = gst.count[j];
+            }
         }
         c->sync();
         std::vector<float> wave_ms;
@@ -1954,13 +2111,17 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             wave_ms.push_back(ms);
             c->event_pool.push_back(e);
         }
-        if (o->rt_ms)
-            for (uint32_t q = 0; q < m; ++q) {
-                float ms = -1.0f;
-                if (rt_event[q]) SGC_CUDA_CHECK(cudaEventElapsedTime(&ms, ev_start, rt_event[q]));
-                o->rt_ms[q] = rt_event[q] ? static_cast<float>(t_rep - t_start) + ms : -1.0f;
+        if (o->rt_ms) {
+            for (uint32_t q = 0; q < m; ++q) o->rt_ms[q] = -1.0f;
+            for (uint32_t j = 0; j < gj.size(); ++j) {
+                const uint32_t q = gen_q[j];
+                cudaEvent_t e = gst.last_ev[j] >= 0 ? gst.events[gst.last_ev[j]] : ev_wave[wave_of_job[j]];
+                float ms = 0.f;
+                SGC_CUDA_CHECK(cudaEventElapsedTime(&ms, ev_start, e));
+                o->rt_ms[q] = static_cast<float>(t_rep - t_start) + ms;
             }
-        for (cudaEvent_t e : dec_events) c->event_pool.push_back(e);
+        }
+        for (cudaEvent_t e : gst.events) c->event_pool.push_back(e);
         c->event_pool.push_back(ev_start);
         // TTFT (submission -> first token): batch start to the end of the query's wave; the
         // encode/cluster/represent stages before ev_start are added from the host clock
@@ -2070,8 +2231,8 @@ int sgc_attention_bf16(sgc_ctx* ctx, const void* q, const void* k_pfx, const voi
 
 int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value) {
     return guarded([&] {
-        (void)ctx;
         if (std::string(name) == "gemm_pairs") sgc::gemm_set_pairs(value != 0);
+        else if (std::string(name) == "decode_defer_pct") ctx->c.decode_defer_pct = static_cast<uint32_t>(std::max<int64_t>(0, value));
         else fail(SGC_DOMAIN, std::string("unknown option ") + name);
     });
 }

@@ -411,7 +411,7 @@ void decode_attention_local(Ctx* c, const DecodeAttnParams& p) {
     const int hd = p.d / p.heads;
     const int warps = p.rows * p.heads;
     const dim3 grid((warps + 7) / 8);
-    Ctx::Timed timer(c, "attention");
+    Ctx::Timed timer(c, "attn_decode");
     switch (hd) {
         case 16: decode_local_kernel<16><<<grid, 256, 0, c->stream>>>(p); break;
         case 32: decode_local_kernel<32><<<grid, 256, 0, c->stream>>>(p); break;

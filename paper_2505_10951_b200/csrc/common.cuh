@@ -67,6 +67,9 @@ struct KernelTiming {
 struct Ctx {
     int device = 0;
     int num_sms = 148;
+    // generation: a wave decodes on its own until fewer than this % of its queries are still
+    // generating; the stragglers of all waves then finish in one shared loop
+    uint32_t decode_defer_pct = 25;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     uint64_t launches = 0;

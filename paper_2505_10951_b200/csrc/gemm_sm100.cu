@@ -558,7 +558,16 @@ template <int EPI, int HD>
 void dispatch_bn(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
     // widest tile that divides N (and d, for the QKV section split)
     int lim = EPI == EPI_QKV ? ep.d : N;
-    if (g_gemm_pairs && M >= 2 * BM && N % 256 == 0 && lim % 256 == 0) launch2<EPI, HD>(c, A, B, M, N, K, ep);
+    const int m_tiles = (M + BM - 1) / BM;
+    // few rows (decode steps): the GEMM is weight-bandwidth bound, so spread the weight matrix
+    // over as many CTAs as possible -- the narrowest tile that still yields >= one wave
+    // (the QKV epilogue needs whole heads inside a tile: BN >= head_dim)
+    if (m_tiles * (N / 256) < c->num_sms && N % 64 == 0 && lim % 64 == 0 && HD <= 128) {
+        if ((N % 128 == 0 && lim % 128 == 0 && m_tiles * (N / 128) >= c->num_sms) || HD > 64)
+            launch<128, EPI, HD>(c, A, B, M, N, K, ep);
+        else
+            launch<64, EPI, HD>(c, A, B, M, N, K, ep);
+    } else if (g_gemm_pairs && M >= 2 * BM && N % 256 == 0 && lim % 256 == 0) launch2<EPI, HD>(c, A, B, M, N, K, ep);
     else if (N % 256 == 0 && lim % 256 == 0) launch<256, EPI, HD>(c, A, B, M, N, K, ep);
     else if (N % 128 == 0 && lim % 128 == 0) launch<128, EPI, HD>(c, A, B, M, N, K, ep);
     else if (N % 64 == 0 && lim % 64 == 0) launch<64, EPI, HD>(c, A, B, M, N, K, ep);

@@ -110,46 +110,56 @@ __global__ void rmsnorm_bf16_kernel(__nv_bfloat16* out, const float* x, int d, i
 // final rmsnorm + fp32 head (lm_core.cpp:288-295) for selected rows. CTA = 16 rows x all
 // vocab; the head is stored transposed [d x 260] so a thread per vocab id reads coalesced.
 constexpr int kHeadRows = 16;
-constexpr int kHeadChunk = 512;
-__global__ void __launch_bounds__(288) head_kernel(float* logits, const float* x,
+constexpr int kHeadChunk = 512;  // K slice per CTA: the split is a function of d only, so the
+                                 // summation order (and the logits, bit for bit) never depends
+                                 // on how many rows a call carries
+
+// 1 / sqrt(mean(x^2) + 1e-5) of the logit rows (the final RMSNorm, lm_core.cpp:285-296)
+__global__ void head_norm_kernel(float* inv, const float* x, const int32_t* rows, int n, int d) {
+    const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (r >= n) return;
+    const float* xr = x + static_cast<size_t>(rows[r]) * d;
+    float ss = 0.f;
+    for (int i = lane; i < d; i += 32) ss += xr[i] * xr[i];
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
+    if (lane == 0) inv[r] = 1.0f / sqrtf(ss / static_cast<float>(d) + 1e-5f);
+}
+
+// partial[ks][r][v] = sum over k in slice ks of head[v][k] * x[row r][k] * inv[r]
+__global__ void __launch_bounds__(288) head_kernel(float* partial, const float* x, const float* inv,
                                                    const int32_t* rows, int n, const float* head_t,
                                                    int d) {
     __shared__ float xs[kHeadRows][kHeadChunk];
-    __shared__ float inv[kHeadRows];
-    const int r0 = blockIdx.x * kHeadRows;
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    for (int rr = warp; rr < kHeadRows; rr += blockDim.x / 32) {
-        float ss = 0.f;
-        if (r0 + rr < n) {
-            const float* xr = x + static_cast<size_t>(rows[r0 + rr]) * d;
-            for (int i = lane; i < d; i += 32) ss += xr[i] * xr[i];
-        }
-        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffff, ss, o);
-        if (lane == 0) inv[rr] = 1.0f / sqrtf(ss / static_cast<float>(d) + 1e-5f);
+    const int r0 = blockIdx.x * kHeadRows, k0 = blockIdx.y * kHeadChunk;
+    const int kc = min(kHeadChunk, d - k0);
+    for (int i = threadIdx.x; i < kHeadRows * kc; i += blockDim.x) {
+        const int rr = i / kc, k = i % kc;
+        xs[rr][k] = r0 + rr < n ? x[static_cast<size_t>(rows[r0 + rr]) * d + k0 + k] * inv[r0 + rr] : 0.f;
     }
-    const int v = threadIdx.x;  // vocab id (260 of 288 threads active in the dot)
+    __syncthreads();
+    const int v = threadIdx.x;  // vocab id (260 of 288 threads active)
+    if (v >= SGC_VOCAB) return;
     float acc[kHeadRows];
 #pragma unroll
     for (int i = 0; i < kHeadRows; ++i) acc[i] = 0.f;
-    for (int k0 = 0; k0 < d; k0 += kHeadChunk) {
-        const int kc = min(kHeadChunk, d - k0);
-        __syncthreads();
-        for (int i = threadIdx.x; i < kHeadRows * kc; i += blockDim.x) {
-            int rr = i / kc, k = i % kc;
-            xs[rr][k] = r0 + rr < n ? x[static_cast<size_t>(rows[r0 + rr]) * d + k0 + k] * inv[rr] : 0.f;
-        }
-        __syncthreads();
-        if (v < SGC_VOCAB) {
-            for (int k = 0; k < kc; ++k) {
-                float w = head_t[static_cast<size_t>(k0 + k) * SGC_VOCAB + v];
+    for (int k = 0; k < kc; ++k) {
+        const float w = head_t[static_cast<size_t>(k0 + k) * SGC_VOCAB + v];
 #pragma unroll
-                for (int i = 0; i < kHeadRows; ++i) acc[i] = fmaf(xs[i][k], w, acc[i]);
-            }
-        }
+        for (int i = 0; i < kHeadRows; ++i) acc[i] = fmaf(xs[i][k], w, acc[i]);
     }
-    if (v < SGC_VOCAB)
-        for (int i = 0; i < kHeadRows; ++i)
-            if (r0 + i < n) logits[static_cast<size_t>(r0 + i) * SGC_VOCAB + v] = acc[i];
+    float* out = partial + static_cast<size_t>(blockIdx.y) * n * SGC_VOCAB;
+    for (int i = 0; i < kHeadRows; ++i)
+        if (r0 + i < n) out[static_cast<size_t>(r0 + i) * SGC_VOCAB + v] = acc[i];
+}
+
+// fixed-order reduction of the K slices
+__global__ void head_reduce_kernel(float* logits, const float* partial, int n, int splits) {
+    const size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+    const size_t total = static_cast<size_t>(n) * SGC_VOCAB;
+    if (i >= total) return;
+    float s = partial[i];
+    for (int k = 1; k < splits; ++k) s += partial[k * total + i];
+    logits[i] = s;
 }
 
 // copy pointer (lm_core.cpp:360-374) + first greedy step (:379-385): one CTA per member.
@@ -288,8 +298,17 @@ void head_logits(Ctx* c, float* logits, const float* x, const int32_t* rows, int
                  const float* head_t, int d) {
     if (n <= 0) return;
     Ctx::Timed timer(c, "head");
-    head_kernel<<<ceil_div(n, kHeadRows), 288, 0, c->stream>>>(logits, x, rows, n, head_t, d);
+    const int splits = static_cast<int>(ceil_div(d, kHeadChunk));
+    float* inv = c->buf<float>("head_inv", n);
+    float* partial = splits > 1 ? c->buf<float>("head_partial", static_cast<size_t>(splits) * n * SGC_VOCAB) : logits;
+    head_norm_kernel<<<ceil_div(n, 8), 256, 0, c->stream>>>(inv, x, rows, n, d);
     SGC_LAUNCH_CHECK(c);
+    head_kernel<<<dim3(ceil_div(n, kHeadRows), splits), 288, 0, c->stream>>>(partial, x, inv, rows, n, head_t, d);
+    SGC_LAUNCH_CHECK(c);
+    if (splits > 1) {
+        head_reduce_kernel<<<ceil_div(static_cast<uint64_t>(n) * SGC_VOCAB, 256), 256, 0, c->stream>>>(logits, partial, n, splits);
+        SGC_LAUNCH_CHECK(c);
+    }
 }
 void first_tokens(Ctx* c, int32_t* first, const float* logits, int n, const int32_t* ctx_tokens,
                   const uint64_t* ctx_off, const uint32_t* member_ctx, const int32_t* ans,

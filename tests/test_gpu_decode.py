@@ -142,3 +142,23 @@ def test_decode_members_of_many_segments_match_extend(ctx):
                 assert int(np.argmax(lg[row])) == gen[j][k], (j, k)
                 checked += 1
     assert checked > 300
+
+
+def test_decode_schedule_does_not_change_tokens(ctx):
+    """Deferring a wave's stragglers to the shared loop (or decoding everything after the last
+    wave) only regroups rows; every row's math is independent of its batch, so the generated ids
+    are identical and RT only moves."""
+    w = W.c1_workload(40, 4)
+    pb = host.PreparedBatch(w)
+    pb.al.count = 0  # no copy pointer: plain greedy, decode runs to EOS / max_new
+    lm = host.ToyLm(ctx, host.ToyLmConfig(**w.lm, seed=7))
+    dg = host.DeviceGraph(ctx, w.graph)
+    runs = []
+    for pct in (0, 25, 1000):
+        ctx.set_option("decode_defer_pct", pct)
+        r = host.run_subgcache(ctx, lm, dg, pb, waves=3, max_new=12)
+        runs.append([t.tolist() for t in r.tokens])
+        assert (r.rt_ms >= r.ttft_ms - 1e-3).all()
+    ctx.set_option("decode_defer_pct", 25)
+    assert runs[0] == runs[1] == runs[2]
+    assert max(len(t) for t in runs[0]) > 1
