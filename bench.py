@@ -143,6 +143,8 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     ctx.set_option("gemm_pairs", 0 if args.no_pairs else 1)
+    if args.attn_split is not None:
+        ctx.set_option("attn_split", args.attn_split)
     t0 = time.time()
     lm = host.ToyLm(ctx, host.ToyLmConfig(**w.lm, seed=w.seed))
     dg = host.DeviceGraph(ctx, w.graph)
@@ -442,6 +444,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gen", action="store_true", help="skip the generation (decode) measurement")
+    ap.add_argument("--attn-split", type=int, default=None, help="1: two softmax warpgroups per query tile")
     ap.add_argument("--gen-steps", type=int, default=2)
     ap.add_argument("--no-pairs", action="store_true", help="1-CTA GEMM instead of CTA pairs")
     ap.add_argument("--waves", type=int, default=4,

@@ -157,6 +157,27 @@ public:
             std::copy(lg.begin() + i * SGC_VOCAB, lg.begin() + (i + 1) * SGC_VOCAB, out[i].begin());
         return out;
     }
+    // KVCache::fork + ToyLm::extend + ToyLm::greedy_decode (lm_core.cpp:352-404) per member,
+    // all members batched; returns GenerationResult::token_ids per member
+    std::vector<std::vector<TokenId>> generate(const SealedPrefixes& kv, const std::vector<uint32_t>& segment,
+                                               const std::vector<std::vector<TokenId>>& questions,
+                                               const std::vector<std::vector<TokenId>>* answers = nullptr,
+                                               uint32_t max_new = 0, float bonus = 100.0f) const {
+        const uint32_t mx = max_new ? max_new : cfg_.max_new_tokens;
+        std::vector<uint64_t> qo, ao;
+        std::vector<TokenId> qf, af;
+        sgc_token_lists ql = pack(questions, qo, qf);
+        sgc_token_lists al{};
+        if (answers) al = pack(*answers, ao, af);
+        std::vector<TokenId> toks(questions.size() * mx, -1);
+        std::vector<uint32_t> cnt(questions.size());
+        check(sgc_extend_generate(ctx_.get(), h_.get(), kv.get(), segment.data(), &ql, answers ? &al : nullptr,
+                                  bonus, mx, nullptr, nullptr, toks.data(), cnt.data()));
+        std::vector<std::vector<TokenId>> out(questions.size());
+        for (size_t i = 0; i < questions.size(); ++i)
+            out[i].assign(toks.begin() + i * mx, toks.begin() + i * mx + cnt[i]);
+        return out;
+    }
     sgc_model* get() const { return h_.get(); }
 
 private:

@@ -328,58 +328,85 @@ void cascade_attention(Ctx* c, const AttnParams& p, int n_work, int heads, int h
 }
 
 // ---- decode step: each row's own keys (+ merge with the prefix partial) ------------------
-// One warp per (row, head); lane i holds dims [i*DPL, i*DPL + DPL). Keys are visited in
-// order (prefix when no partial is given, question suffix, generated tokens) with an online
-// softmax in scaled-log2 units, then merged with the tcgen05 prefix partial:
+// One warp per (row, head). Keys are visited 32 at a time, one key per lane: the lane's score
+// is a full dot product (uint4 loads of its key row, q broadcast from shared memory), the chunk
+// is folded into an online softmax in scaled-log2 units, and O += P V with lane i holding dims
+// [i*DPL, i*DPL + DPL) (p_j broadcast by shuffle, V rows read coalesced). Ranges in order:
+// the prefix (only when no tcgen05 partial is given), the question suffix, the generated
+// tokens. Finally merged with the prefix partial:
 //   out = (O1 2^(lse1 - M) + acc 2^(m2 - M)) / (2^(lse1 - M) + l2 2^(m2 - M)).
 namespace {
 template <int HD>
 __global__ void __launch_bounds__(256) decode_local_kernel(DecodeAttnParams p) {
     constexpr int DPL = HD >= 32 ? HD / 32 : 1;
-    const int wg = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
-    const int lane = threadIdx.x & 31;
-    if (wg >= p.rows * p.heads) return;
+    __shared__ float qs[8][HD];
+    const int wib = threadIdx.x / 32, lane = threadIdx.x & 31;
+    const int wg = blockIdx.x * 8 + wib;
+    if (wg >= p.rows * p.heads) return;  // warp-uniform; only __syncwarp below
     const int r = wg / p.heads, h = wg % p.heads;
+    const float sl2 = p.scale * 1.4426950408889634f;
+    const __nv_bfloat16* qrow = p.q + static_cast<size_t>(r) * p.d + h * HD;
+    for (int i = lane; i < HD; i += 32) qs[wib][i] = __bfloat162float(qrow[i]) * sl2;
+    __syncwarp();
     const bool act = lane * DPL < HD;
     const size_t col = static_cast<size_t>(h) * HD + (act ? lane * DPL : 0);
-    const float sl2 = p.scale * 1.4426950408889634f;
-    float q[DPL], acc[DPL];
+    float m = -INFINITY, l = 0.f, acc[DPL];
 #pragma unroll
-    for (int i = 0; i < DPL; ++i) {
-        q[i] = act ? __bfloat162float(p.q[static_cast<size_t>(r) * p.d + col + i]) : 0.f;
-        acc[i] = 0.f;
-    }
-    float m = -INFINITY, l = 0.f;
+    for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
     auto run = [&](const __nv_bfloat16* K, const __nv_bfloat16* V, int lo, int n) {
-        // four keys per round: independent dot products and shuffle trees (ILP)
-        for (int k0 = 0; k0 < n; k0 += 4) {
-            float s[4];
+        for (int k0 = 0; k0 < n; k0 += 32) {
+            const int key = k0 + lane;
+            float sc = -INFINITY;
+            if (key < n) {
+                const uint4* kr = reinterpret_cast<const uint4*>(K + static_cast<size_t>(lo + key) * p.d + h * HD);
+                float a0 = 0.f, a1 = 0.f;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                s[u] = 0.f;
-                if (k0 + u < n && act) {
-                    const __nv_bfloat16* kr = K + static_cast<size_t>(lo + k0 + u) * p.d + col;
+                for (int c = 0; c < HD / 8; ++c) {
+                    const uint4 u = kr[c];
+                    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-                    for (int i = 0; i < DPL; ++i) s[u] = fmaf(q[i], __bfloat162float(kr[i]), s[u]);
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 f = __bfloat1622float2(b2[e]);
+                        a0 = fmaf(qs[wib][c * 8 + 2 * e], f.x, a0);
+                        a1 = fmaf(qs[wib][c * 8 + 2 * e + 1], f.y, a1);
+                    }
+                }
+                sc = a0 + a1;
+            }
+            float cm = sc;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+            const float mn = fmaxf(m, cm);
+            const float alpha = m == -INFINITY ? 0.f : exp2f(m - mn);
+            const float pk = key < n ? exp2f(sc - mn) : 0.f;
+            float ps = pk;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+            l = l * alpha + ps;
+#pragma unroll
+            for (int i = 0; i < DPL; ++i) acc[i] *= alpha;
+            const int nk = min(32, n - k0);
+            const __nv_bfloat16* vb = V + static_cast<size_t>(lo + k0) * p.d + col;
+#pragma unroll 8
+            for (int j = 0; j < nk; ++j) {
+                const float pj = __shfl_sync(0xffffffffu, pk, j);
+                if (act) {
+                    const __nv_bfloat16* vr = vb + static_cast<size_t>(j) * p.d;
+                    if constexpr (DPL == 4) {
+                        const uint2 u = *reinterpret_cast<const uint2*>(vr);
+                        const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+                        const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+                        acc[0] = fmaf(pj, f0.x, acc[0]);
+                        acc[1] = fmaf(pj, f0.y, acc[1]);
+                        acc[2] = fmaf(pj, f1.x, acc[2]);
+                        acc[3] = fmaf(pj, f1.y, acc[3]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < DPL; ++i) acc[i] = fmaf(pj, __bfloat162float(vr[i]), acc[i]);
+                    }
                 }
             }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                for (int u = 0; u < 4; ++u) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (k0 + u >= n) break;
-                const float x = s[u] * sl2;
-                const float mn = fmaxf(m, x);
-                const float a = m == -INFINITY ? 0.f : exp2f(m - mn);
-                const float pk = exp2f(x - mn);
-                l = l * a + pk;
-                const __nv_bfloat16* vr = V + static_cast<size_t>(lo + k0 + u) * p.d + col;
-#pragma unroll
-                for (int i = 0; i < DPL; ++i) acc[i] = acc[i] * a + pk * (act ? __bfloat162float(vr[i]) : 0.f);
-                m = mn;
-            }
+            m = mn;
         }
     };
     if (!p.part_o && p.p_n) run(p.k_p, p.v_p, p.p_lo[r], p.p_n[r]);

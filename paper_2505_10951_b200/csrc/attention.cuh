@@ -38,6 +38,8 @@ void cascade_attention(Ctx* c, const AttnParams& p, int n_work, int heads, int h
 bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, int hd, int q_rows,
                           int pfx_rows, int loc_rows);
 inline bool attention_tc_supported(int hd) { return hd == 64 || hd == 128; }
+// split every S row over two softmax warpgroups, or one thread per row (default)
+void attention_set_split(bool on);
 
 // Decode step (attention.cu): merge the prefix partial (part_o, part_lse from the tcgen05 kernel
 // in partial mode, or none when part_o == nullptr) with each row's own keys: question rows

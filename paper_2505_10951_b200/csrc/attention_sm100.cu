@@ -35,7 +35,8 @@ namespace {
 
 constexpr int BQ = 128;   // rows per query tile (two tiles per unit)
 constexpr int BKV = 128;  // keys per block
-constexpr int kThreads = 320;  // loader, MMA, 2 x 4 softmax warps
+// threads: loader warp, MMA warp, 2 tiles x SPLIT softmax warpgroups (SPLIT = 1: 320, 2: 576)
+bool g_attn_split = false;  // two softmax warpgroups per query tile (sgc_set_option "attn_split"; measured no faster)
 constexpr int kKStages = 3;
 constexpr int kVStages = 2;
 // SGC_POLY_NUM / SGC_POLY_DEN of the exponential pairs run as a polynomial on the FMA pipe
@@ -51,7 +52,8 @@ struct TcCfg {
     static constexpr int kQBytes = BQ * HD * 2;
     static constexpr int kKBytes = BKV * HD * 2;
     static constexpr int kVBytes = BKV * HD * 2;
-    static constexpr int kSmem = 2 * kQBytes + kKStages * kKBytes + kVStages * kVBytes + 256;
+    // + barriers (256 B) + the split-softmax exchange slots [2][2][BQ] fp32
+    static constexpr int kSmem = 2 * kQBytes + kKStages * kKBytes + kVStages * kVBytes + 256 + 2 * 2 * BQ * 4;
     static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kS = 0;    // S_X at column X * 128
     static constexpr uint32_t kO = 256;  // O_X at column 256 + X * 128
@@ -163,8 +165,8 @@ __device__ __forceinline__ UnitPlan plan_unit(const AttnWork& w, const int32_t* 
     return u;
 }
 
-template <int HD>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int HD, int SPLIT>
+__global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKp,
                    const __grid_constant__ CUtensorMap tmVp, const __grid_constant__ CUtensorMap tmKl,
                    const __grid_constant__ CUtensorMap tmVl, TcParams p) {
@@ -185,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* p_full = bars + 16;   // [2] per tile
     uint64_t* o_full = bars + 18;   // [2] per tile
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+    float* xm = reinterpret_cast<float*>(bars + 32);  // [2 tiles][SPLIT][BQ] row max / sum exchange
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int n_items = p.n_work * p.heads;
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&v_full[i], 1);
             ptx::mbar_init(&v_empty[i], 1);
             ptx::mbar_init(&s_full[i], 1);
-            ptx::mbar_init(&p_full[i], 128);
+            ptx::mbar_init(&p_full[i], 128 * SPLIT);
             ptx::mbar_init(&o_full[i], 1);
         }
         ptx::fence_barrier_init();
@@ -324,13 +327,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else {
-        // warps 2-5: tile A, warps 6-9: tile B; a warp may only touch TMEM lanes
-        // 32 * (warp % 4) .. +31, so row = 32 * (warp % 4) + lane
-        const int x = (warp - 2) >> 2;                  // query tile handled by this warpgroup
-        const int r = (warp & 3) * 32 + lane;           // row within the tile == TMEM lane
+        // softmax warps: tile x = 0 (A) / 1 (B); with SPLIT = 2 each tile has two warpgroups,
+        // half 0 owning S columns 0-63 and half 1 columns 64-127 of every row (the row max is
+        // exchanged through shared memory once per block). A warp may only touch TMEM lanes
+        // 32 * (warp % 4) .. +31, so row = 32 * (warp % 4) + lane.
+        constexpr int COLS = BKV / SPLIT;          // S columns per thread
+        constexpr int OCOLS = HD / SPLIT;          // O columns per thread (rescale, epilogue)
+        const int sw = warp - 2;
+        const int x = sw / (4 * SPLIT);            // query tile handled by this warpgroup
+        const int half = (sw / 4) % SPLIT;
+        const int c0 = half * COLS;                // first S column (key) of this thread
+        const int r = (warp & 3) * 32 + lane;      // row within the tile == TMEM lane
         const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
         const uint32_t tS = tmem_base + lane_base + C::kS + x * BQ;
         const uint32_t tO = tmem_base + lane_base + C::kO + x * 128;
+        float* xch = xm + (x * SPLIT) * BQ;        // [SPLIT][BQ] exchange slots of this tile
+        auto tile_sync = [&]() {
+            if constexpr (SPLIT > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(128 * SPLIT) : "memory");
+        };
         uint32_t gs = 0, uit = 0;
 #ifdef SGC_ATTN_PROF
         const bool prof_thr = threadIdx.x == 64;
@@ -370,46 +384,54 @@ __global__ void __launch_bounds__(kThreads, 1)
                     khi = valid ? min(BKV - 1, row - k0) : -1;
                 }
                 // warp-uniform: the tcgen05.ld/st below are .sync.aligned (whole warp, same path)
-                const bool full = __all_sync(0xffffffffu, klo == 0 && khi == BKV - 1);
-                // The whole S row (128 fp32) is loaded into registers with four back-to-back
-                // tcgen05.ld (one wait), reduced to its max, exponentiated in place (P packed as
-                // bf16 pairs over the first 64 registers) and stored over S's first 64 columns.
-                // The row's reference max m is lazy: it only moves when the block max exceeds it
-                // by more than 2^8 (then O is rescaled in place; P <= 2^8 otherwise), so the
-                // common case has no O traffic at all.
+                const bool full = __all_sync(0xffffffffu, klo <= c0 && khi >= c0 + COLS - 1);
+                // This thread's part of the S row (COLS fp32) is loaded into registers with
+                // back-to-back tcgen05.ld (one wait), reduced to its max (with SPLIT = 2 combined
+                // with the other half's through shared memory), exponentiated in place (P packed
+                // as bf16 pairs) and stored over S's first 64 columns. The row's reference max m
+                // is lazy: it only moves when the block max exceeds it by more than 2^8 (then O
+                // is rescaled in place; P <= 2^8 otherwise), so the common case has no O traffic.
                 const float sc = p.scale_log2;
-                uint32_t sv[BKV];
+                uint32_t sv[COLS];
 #pragma unroll
-                for (int c = 0; c < BKV / 32; ++c)
-                    ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
+                for (int c = 0; c < COLS / 32; ++c)
+                    ptx::tmem_ld32(tS + c0 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
                 ptx::tmem_ld_wait();
                 SPROF(7);
-                // visibility bitmap of the block's keys [klo, khi] (4 x 32 bits); masked -> -inf
-                uint32_t vw[BKV / 32];
+                // visibility bitmap of this thread's keys [klo, khi] (COLS / 32 words)
+                uint32_t vw[COLS / 32];
 #pragma unroll
-                for (int w = 0; w < BKV / 32; ++w) {
-                    const int lo = klo - 32 * w, hi = khi - 32 * w;
+                for (int wd = 0; wd < COLS / 32; ++wd) {
+                    const int lo = klo - c0 - 32 * wd, hi = khi - c0 - 32 * wd;
                     const uint32_t mlo = lo <= 0 ? ~0u : (lo >= 32 ? 0u : ~0u << lo);
                     const uint32_t mhi = hi >= 31 ? ~0u : (hi < 0 ? 0u : ~0u >> (31 - hi));
-                    vw[w] = mlo & mhi;
+                    vw[wd] = mlo & mhi;
                 }
                 if (!full) {
 #pragma unroll
-                    for (int j = 0; j < BKV; ++j)
+                    for (int j = 0; j < COLS; ++j)
                         if (!(vw[j / 32] & (1u << (j % 32)))) sv[j] = __float_as_uint(-INFINITY);
                 }
                 float bmax;
                 {
                     // max over RAW scores (scale > 0): 3-input max, four independent chains
-                    float c0 = -INFINITY, c1 = -INFINITY, c2 = -INFINITY, c3 = -INFINITY;
+                    float q0 = -INFINITY, q1 = -INFINITY, q2 = -INFINITY, q3 = -INFINITY;
 #pragma unroll
-                    for (int j = 0; j < BKV; j += 8) {
-                        c0 = fmax3(c0, __uint_as_float(sv[j]), __uint_as_float(sv[j + 1]));
-                        c1 = fmax3(c1, __uint_as_float(sv[j + 2]), __uint_as_float(sv[j + 3]));
-                        c2 = fmax3(c2, __uint_as_float(sv[j + 4]), __uint_as_float(sv[j + 5]));
-                        c3 = fmax3(c3, __uint_as_float(sv[j + 6]), __uint_as_float(sv[j + 7]));
+                    for (int j = 0; j < COLS; j += 8) {
+                        q0 = fmax3(q0, __uint_as_float(sv[j]), __uint_as_float(sv[j + 1]));
+                        q1 = fmax3(q1, __uint_as_float(sv[j + 2]), __uint_as_float(sv[j + 3]));
+                        q2 = fmax3(q2, __uint_as_float(sv[j + 4]), __uint_as_float(sv[j + 5]));
+                        q3 = fmax3(q3, __uint_as_float(sv[j + 6]), __uint_as_float(sv[j + 7]));
                     }
-                    bmax = fmaxf(fmaxf(c0, c1), fmaxf(c2, c3)) * sc;  // scaled-log2 units
+                    bmax = fmaxf(fmaxf(q0, q1), fmaxf(q2, q3));
+                    if constexpr (SPLIT > 1) {
+                        // every S load of the tile is complete once all its threads pass here,
+                        // so P may overwrite S columns owned by the other half afterwards
+                        xch[half * BQ + r] = bmax;
+                        tile_sync();
+                        bmax = fmaxf(bmax, xch[(1 - half) * BQ + r]);
+                    }
+                    bmax *= sc;  // scaled-log2 units
                 }
                 SPROF(8);
                 const float mnew = (m == -INFINITY || bmax > m + 8.f) ? bmax : m;
@@ -419,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint64_t sc2 = f2pack(sc, sc), nm2 = f2pack(nm, nm);
                     uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;  // packed partial row sums
 #pragma unroll
-                    for (int j = 0; j < BKV / 2; ++j) {
+                    for (int j = 0; j < COLS / 2; ++j) {
                         float xa, xc;  // x = raw * scale_log2 - m: one FFMA2 per pair
                         f2unpack(ffma2(f2pack(__uint_as_float(sv[2 * j]), __uint_as_float(sv[2 * j + 1])), sc2, nm2),
                                  xa, xc);
@@ -455,21 +477,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // O is stable here: s_full certified the previous PV of this tile completed
                     alpha = resc ? ex2_approx(m - mnew) : 1.f;
 #pragma unroll 1
-                    for (int c = 0; c < HD / 32; ++c) {
+                    for (int c = 0; c < OCOLS / 32; ++c) {
                         uint32_t o[32];
-                        ptx::tmem_ld32(tO + c * 32, o);
+                        ptx::tmem_ld32(tO + half * OCOLS + c * 32, o);
                         ptx::tmem_ld_wait();
 #pragma unroll
                         for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-                        ptx::tmem_st32(tO + c * 32, o);
+                        ptx::tmem_st32(tO + half * OCOLS + c * 32, o);
                     }
                 }
                 m = mnew;
                 SPROF(3);
-                // P -> TMEM over S's first 64 columns
+                // P -> TMEM over S's first 64 columns (this thread's keys: columns c0/2 ..)
 #pragma unroll
-                for (int c = 0; c < BKV / 32; ++c)
-                    ptx::tmem_st16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&sv[c * 16]));
+                for (int c = 0; c < COLS / 32; ++c)
+                    ptx::tmem_st16(tS + c0 / 2 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&sv[c * 16]));
                 l = l * alpha + rs;
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
@@ -480,23 +502,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(&o_full[x], uit & 1);
             ptx::tc_fence_after();
             SPROF(5);
+            if constexpr (SPLIT > 1) {
+                // every thread of the tile read the last block's max before its p_full arrive,
+                // and o_full follows all of them: the exchange slots are free for the row sums
+                xch[half * BQ + r] = l;
+                tile_sync();
+                l += xch[(1 - half) * BQ + r];
+                tile_sync();  // slots reused by the next item's first block
+            }
             const float il = l > 0.f ? 1.f / l : 0.f;
-            uint32_t o[HD];
+            uint32_t o[OCOLS];
 #pragma unroll
-            for (int c = 0; c < HD / 32; ++c)
-                ptx::tmem_ld32(tO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
+            for (int c = 0; c < OCOLS / 32; ++c)
+                ptx::tmem_ld32(tO + half * OCOLS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
             ptx::tmem_ld_wait();
             if (valid && p.part_o) {
-                float4* dst = reinterpret_cast<float4*>(p.part_o + static_cast<size_t>(row) * p.d + h * HD);
+                float4* dst = reinterpret_cast<float4*>(p.part_o + static_cast<size_t>(row) * p.d + h * HD + half * OCOLS);
 #pragma unroll
-                for (int q = 0; q < HD / 4; ++q)
+                for (int q = 0; q < OCOLS / 4; ++q)
                     dst[q] = make_float4(__uint_as_float(o[4 * q]) * il, __uint_as_float(o[4 * q + 1]) * il,
                                          __uint_as_float(o[4 * q + 2]) * il, __uint_as_float(o[4 * q + 3]) * il);
-                p.part_lse[static_cast<size_t>(row) * p.heads + h] = l > 0.f ? m + __log2f(l) : -INFINITY;
+                if (half == 0) p.part_lse[static_cast<size_t>(row) * p.heads + h] = l > 0.f ? m + __log2f(l) : -INFINITY;
             } else if (valid) {
-                uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(row) * p.d + h * HD);
+                uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(row) * p.d + h * HD + half * OCOLS);
 #pragma unroll
-                for (int q = 0; q < HD / 8; ++q) {
+                for (int q = 0; q < OCOLS / 8; ++q) {
                     uint32_t wv[4];
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
@@ -520,10 +550,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <int HD>
+template <int HD, int SPLIT>
 void launch_tc(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, int pfx_rows, int loc_rows) {
     using Cf = TcCfg<HD>;
-    auto kfn = attn_tc_kernel<HD>;
+    auto kfn = attn_tc_kernel<HD, SPLIT>;
     static bool attr = false;
     if (!attr) {
         SGC_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmem));
@@ -539,7 +569,7 @@ void launch_tc(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, i
     const int items = n_work * heads;
     const int grid = items < c->num_sms ? items : c->num_sms;
     Ctx::Timed timer(c, "attention");
-    kfn<<<grid, kThreads, Cf::kSmem, c->stream>>>(tq, tkp, tvp, tkl, tvl, p);
+    kfn<<<grid, 64 + 256 * SPLIT, Cf::kSmem, c->stream>>>(tq, tkp, tvp, tkl, tvl, p);
     SGC_LAUNCH_CHECK(c);
 }
 
@@ -560,11 +590,20 @@ bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, in
     if (n_work <= 0) return true;
     if (p.loc_kv0 != 0) return false;
     if (p.part_o && !p.part_lse) return false;
+    const bool split = g_attn_split;
     switch (hd) {
-        case 64: launch_tc<64>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows); return true;
-        case 128: launch_tc<128>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows); return true;
+        case 64:
+            if (split) launch_tc<64, 2>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows);
+            else launch_tc<64, 1>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows);
+            return true;
+        case 128:
+            if (split) launch_tc<128, 2>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows);
+            else launch_tc<128, 1>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows);
+            return true;
         default: return false;
     }
 }
+
+void attention_set_split(bool on) { g_attn_split = on; }
 
 }  // namespace sgc

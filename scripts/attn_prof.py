@@ -21,6 +21,8 @@ def main():
     L.sgc_debug_attn_prof.argtypes = [C.POINTER(C.c_ulonglong), C.c_int]
     w = W.c3_workload()
     ctx = host.Context(0)
+    if os.environ.get("SGC_ATTN_SPLIT") is not None:
+        ctx.set_option("attn_split", int(os.environ["SGC_ATTN_SPLIT"]))
     lm = host.ToyLm(ctx, host.ToyLmConfig(**w.lm, seed=w.seed))
     dg = host.DeviceGraph(ctx, w.graph)
     pb = host.PreparedBatch(w)

@@ -54,6 +54,12 @@ int main() {
         threw = true;
     }
     CHECK(threw);
+    // greedy decode with the copy pointer: answer then EOS (lm_core.cpp:376-387)
+    std::vector<TokenId> prompt = {256, 'c', 'o', 'l', 'o', 'r', ':', ' ', 'b', 'l', 'u', 'e', '.'};
+    SealedPrefixes pp = lm.prefill({prompt});
+    std::vector<std::vector<TokenId>> ans = {{'b', 'l', 'u', 'e'}};
+    auto gen = lm.generate(pp, {0}, {{'?', ' '}}, &ans, 8);
+    CHECK((gen[0] == std::vector<TokenId>{'b', 'l', 'u', 'e', SGC_EOS}));
     auto d = pairwise_distances(ctx, {{1.f, 0.f, 0.f}, {-1.f, 0.f, 0.f}});
     CHECK(d[1] == 2.0 && d[2] == 2.0 && d[0] == 0.0);
     std::printf("facade ok (logit gap %.4f)\n", gap);
