@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "per-query TTFT (p50) and queries/s vs CPU ref; fraction of tensor/HBM roofline"
 # every kernel launch of the library is bracketed by CUDA events under one of these names
-KERNEL_GROUPS = ["gemm", "attention", "attn_decode", "rmsnorm", "embed", "head", "first_token", "gnn_encode",
+KERNEL_GROUPS = ["gemm", "gemm_qkv", "gemm_resid", "gemm_tanh", "attention", "attn_decode", "rmsnorm", "embed", "head", "first_token", "gnn_encode",
                  "text_features", "pairwise", "agglomerate", "union_prompt", "prompt_gather"]
 
 
@@ -199,7 +199,8 @@ def run_ours(args, rank, world, local_rank):
     total_ms = ev0.elapsed_time(ev1)
     launches = ctx.launches - launches0
     kt = {k: ctx.kernel_time(k) for k in KERNEL_GROUPS}
-    gemm_ms, gemm_n = kt["gemm"]
+    gemm_ms = sum(v[0] for k, v in kt.items() if k.startswith("gemm"))
+    gemm_n = sum(v[1] for k, v in kt.items() if k.startswith("gemm"))
     attn_ms, attn_n = kt["attention"]
     ctx.set_timing(False)
     if world > 1:
@@ -295,6 +296,14 @@ def run_ours(args, rank, world, local_rank):
                 "flops_per_launch": gemm_f / max(1, gemm_n / args.steps),
                 "avg_launch_ms": gemm_ms / max(1, gemm_n)}
     step_tf = (gemm_f + attn_f + head_f) / (ms_per_step / 1e3) / 1e12
+    # per fused-epilogue GEMM family: algorithmic FLOPs of the step / its event time
+    L, d, f = w.lm["layers"], w.lm["model_dim"], w.lm["ffn_hidden"]
+    rows = sum(prefix_lens) + sum(members_q)
+    fam_f = {"gemm_qkv": rows * 2.0 * L * 3 * d * d, "gemm_resid": rows * 2.0 * L * (d * d + d * f),
+             "gemm_tanh": rows * 2.0 * L * d * f}
+    gemm_families = {k: {"ms_per_step": round(kt[k][0] / args.steps, 3),
+                         "tflops": round(fam_f[k] * args.steps / (kt[k][0] / 1e3) / 1e12, 1)}
+                     for k in fam_f if kt[k][1]}
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
@@ -317,6 +326,7 @@ def run_ours(args, rank, world, local_rank):
         "kernel_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in kt.items() if v[1]},
         "gpu_idle_ms_per_step": round(ms_per_step - sum(v[0] for v in kt.values()) / args.steps, 3),
         "step_tflops": round(step_tf, 2), "step_tensor_frac": round(step_tf / peak, 4),
+        "gemm_families": gemm_families,
         "roofline": roofline,
         "e2e": e2e,
         "generation": gen,

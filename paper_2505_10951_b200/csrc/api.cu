@@ -65,14 +65,28 @@ inline void dfree(Ctx* c, void* p) {
     if (p) cudaFreeAsync(p, c->stream);
 }
 
+// is `p` device (or managed) memory? host pointers are read directly -- no stream sync, so host
+// preparation of the next wave never drains the GPU queue
+inline bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
 // host copy of a possibly-device array
 template <typename T>
 std::vector<T> to_host(Ctx* c, const T* p, size_t n) {
     std::vector<T> v(n);
-    if (n) {
-        SGC_CUDA_CHECK(cudaMemcpyAsync(v.data(), p, n * sizeof(T), cudaMemcpyDefault, c->stream));
-        SGC_CUDA_CHECK(cudaStreamSynchronize(c->stream));
+    if (!n) return v;
+    if (!is_device_ptr(p)) {
+        std::memcpy(v.data(), p, n * sizeof(T));
+        return v;
     }
+    SGC_CUDA_CHECK(cudaMemcpyAsync(v.data(), p, n * sizeof(T), cudaMemcpyDefault, c->stream));
+    SGC_CUDA_CHECK(cudaStreamSynchronize(c->stream));
     return v;
 }
 
@@ -226,14 +240,7 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
     bf16* h = c->buf<bf16>("fwd_h", static_cast<size_t>(M) * m->ffn);
     int* bad = c->buf<int>("fwd_bad", 1);
     const int32_t* kv_row = b.d_kv_row;
-    if (!kv_row) {
-        int32_t* iota = c->buf<int32_t>("fwd_iota", M);
-        std::vector<int32_t> io(M);
-        std::iota(io.begin(), io.end(), 0);
-        sgc::copy_in(c, iota, io.data(), M);
-        SGC_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-        kv_row = iota;
-    }
+    if (!kv_row) kv_row = c->iota(M);
     float* part_o = nullptr;
     float* part_lse = nullptr;
     if (b.dec && sgc::attention_tc_supported(m->hd)) {
@@ -336,10 +343,13 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
         sgc::gemm_bf16(c, h, m->w2[l], M, d, m->ffn, r);
     }
     sgc::head_logits(c, b.d_logits, x, b.d_logit_rows, b.n_logits, m->head_t, d);
-    int hbad = 0;
-    SGC_CUDA_CHECK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    c->sync();
-    if (hbad) fail(SGC_DOMAIN, "token id out of vocab");
+    // the out-of-vocab flag lands in pinned host memory; callers check it after their own sync
+    c->flag_readback(bad);
+}
+
+// after the caller's stream sync: fail if any forward since the last check saw a bad token id
+void check_forward_flags(Ctx* c) {
+    if (c->take_flag()) fail(SGC_DOMAIN, "token id out of vocab");
 }
 
 // tiles of <= 64 rows that never cross a `group` boundary (sequence for prefill, segment
@@ -360,7 +370,7 @@ std::vector<sgc::AttnWork> make_work(const std::vector<int>& group_start, const 
 
 sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in, const int32_t* tok_in,
                    const float* soft, const uint8_t* soft_mask, float* last_logits, bool arena = false,
-                   uint64_t arena_row0 = 0, uint64_t arena_rows = 0) {
+                   uint64_t arena_row0 = 0, uint64_t arena_rows = 0, bool sync = true) {
     std::vector<uint64_t> off = to_host(c, off_in, count + 1);
     std::vector<int32_t> toks = to_host(c, tok_in, off[count]);
     std::vector<uint8_t> smask = soft_mask ? to_host(c, soft_mask, count) : std::vector<uint8_t>(count, 0);
@@ -460,7 +470,10 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
     b.d_logits = d_logits;
     forward_rows(c, m, b);
     sgc::copy_out(c, last_logits, d_logits, static_cast<size_t>(count) * SGC_VOCAB);
-    c->sync();
+    if (sync) {  // else: the caller syncs (last_logits must then be pinned or null)
+        c->sync();
+        check_forward_flags(c);
+    }
     return kv.release();
 }
 
@@ -475,11 +488,20 @@ struct ExtendKeep {
     std::vector<int8_t> hint;   // per member: answer found in the prefix (lm_core.cpp:361-374)
 };
 
+// Deferred outputs of do_extend: logits / first tokens in the extend's row order (members
+// stably sorted by segment) land in PINNED host memory with no stream sync; `order` maps that
+// order back to member indices. The caller syncs once (e.g. at the end of the batch).
+struct ExtendDefer {
+    float* logits = nullptr;   // pinned [n * 260] or null
+    int32_t* first = nullptr;  // pinned [n]
+    std::vector<uint32_t> order;
+};
+
 // members: segment, question tokens, answers; returns logits/first token in member order
 void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg_in,
                const uint64_t* q_off_in, const int32_t* q_in, const uint64_t* a_off_in,
                const int32_t* a_in, float bonus, float* logits_out, int32_t* first_out,
-               ExtendKeep* keep = nullptr, uint64_t max_rows = 1ull << 16) {
+               ExtendKeep* keep = nullptr, ExtendDefer* defer = nullptr, uint64_t max_rows = 1ull << 16) {
     if (n == 0) return;
     const int d = m->d;
     std::vector<uint32_t> seg = to_host(c, seg_in, n);
@@ -609,6 +631,13 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
         sgc::first_tokens(c, d_first, d_logits, nm, kv->d_tokens, kv->d_tok_off, d_mseg, d_atok,
                           a_tok.empty() ? nullptr : d_aoff, bonus, d_hint);
         // scatter back to member order
+        if (defer) {  // no sync: results stay in extend order, copied to pinned host memory
+            if (defer->logits) sgc::copy_out(c, defer->logits + i0 * SGC_VOCAB, d_logits, static_cast<size_t>(nm) * SGC_VOCAB);
+            if (defer->first) sgc::copy_out(c, defer->first + i0, d_first, nm);
+            chunk0 += static_cast<uint64_t>(M);
+            i0 = i1;
+            continue;
+        }
         std::vector<float> lg(logits_out ? static_cast<size_t>(nm) * SGC_VOCAB : 0);
         std::vector<int32_t> ft(nm);
         std::vector<int8_t> hn(keep ? nm : 0);
@@ -616,6 +645,7 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
         sgc::copy_out(c, ft.data(), d_first, ft.size());
         if (keep) sgc::copy_out(c, hn.data(), d_hint, hn.size());
         c->sync();
+        check_forward_flags(c);
         // scatter back to member order (outputs may be host or device memory)
         for (int k = 0; k < nm; ++k) {
             const uint32_t j = order[i0 + k];
@@ -627,6 +657,10 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
         }
         chunk0 += static_cast<uint64_t>(M);
         i0 = i1;
+    }
+    if (defer) {
+        defer->order = order;
+        return;
     }
     if (first_out) sgc::copy_in(c, first_out, first_h.data(), n);
     if (logits_out) sgc::copy_in(c, logits_out, logits_h.data(), logits_h.size());
@@ -789,6 +823,7 @@ void decode_steps(Ctx* c, sgc_model* m, const GenBuffers& g, const GenJob& job, 
         std::vector<int32_t> out(M);
         sgc::copy_out(c, out.data(), d_tok_out, M);
         c->sync();
+        check_forward_flags(c);
         st.rows += static_cast<uint64_t>(M);
         for (int i = 0; i < M; ++i) {
             const int32_t j = act[i];
@@ -1265,6 +1300,8 @@ int sgc_ctx_destroy(sgc_ctx* ctx) {
             g_enc.erase(it);
         }
         for (auto e : c->event_pool) cudaEventDestroy(e);
+        if (c->h_flags) cudaFreeHost(c->h_flags);
+        for (auto& kv : c->pinned_bufs) cudaFreeHost(kv.second.ptr);
         cudaStreamDestroy(c->own_stream);
         delete ctx;
     });
@@ -1819,7 +1856,9 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 acc += wcost[i];
                 const uint32_t w = static_cast<uint32_t>(wave_end.size());
                 const bool last_wave = w + 1 == n_waves;
-                if (!last_wave && acc >= total_cost * (w + 1) / n_waves && nown - (i + 1) >= n_waves - (w + 1))
+                // cut at the cost quantile, or when only one cluster per remaining wave is left
+                const bool must = nown - (i + 1) == n_waves - (w + 1);
+                if (!last_wave && (acc >= total_cost * (w + 1) / n_waves || must) && nown - (i + 1) >= n_waves - (w + 1))
                     wave_end.push_back(i + 1);
             }
             while (wave_end.size() < n_waves) wave_end.push_back(nown);
@@ -1833,6 +1872,11 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         const uint32_t max_new = b->max_new_tokens;
         const bool gen_on = max_new > 1;
         std::vector<int32_t> wave_of_job;  // decode job index -> wave
+        // deferred first-token outputs (first tokens only): pinned, in extend order, + query ids
+        float* def_lg = o->logits ? c->pinned<float>("run_def_lg", static_cast<size_t>(m) * SGC_VOCAB) : nullptr;
+        int32_t* def_ft = c->pinned<int32_t>("run_def_ft", m);
+        std::vector<uint32_t> def_q;
+        uint32_t def_n = 0;
         // ---- row budget of every wave: prefill rows (representatives + standalone fallbacks)
         // and kept question rows; with generation the waves' prefix / question K/V stay resident
         // until the end so stragglers of every wave decode together (one weight pass per step)
@@ -1943,9 +1987,12 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 }
             }
             const uint32_t ns = static_cast<uint32_t>(seq_off.size() - 1);
-            std::vector<float> seq_logits(static_cast<size_t>(ns) * SGC_VOCAB);
+            // representative logits are only read on the host for standalone fallbacks; without
+            // them no sync is needed and the host prepares the next wave while the GPU works
+            std::vector<float> seq_logits(fb_q.empty() ? 0 : static_cast<size_t>(ns) * SGC_VOCAB);
             sgc_kv* kv = do_prefill(c, model, ns, seq_off.data(), seq_tok.data(), seq_soft_vec.data(),
-                                    seq_soft.data(), seq_logits.data(), /*arena=*/true, arena_row0, arena_rows);
+                                    seq_soft.data(), fb_q.empty() ? nullptr : seq_logits.data(), /*arena=*/true,
+                                    arena_row0, arena_rows, /*sync=*/!fb_q.empty());
             std::unique_ptr<sgc_kv, int (*)(sgc_kv*)> kv_guard(kv, sgc_kv_release);
             prefill_rows += kv->rows;
             const int32_t pfx_base = static_cast<int32_t>(arena_row0);  // absolute arena row of this wave
@@ -1969,12 +2016,24 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                     extend_rows += q_off[q + 1] - q_off[q];
                 }
                 const uint32_t nm = static_cast<uint32_t>(mem_q.size());
-                std::vector<float> lg(static_cast<size_t>(nm) * SGC_VOCAB);
-                std::vector<int32_t> ft(nm);
-                do_extend(c, model, kv, nm, mem_seg.data(), mq_off.data(), mq_tok.data(), ans ? ma_off.data() : nullptr,
-                          ans ? ma_tok.data() : nullptr, b->pointer_bonus, lg.data(), ft.data(),
-                          gen_on ? &keep : nullptr);
-                for (uint32_t j = 0; j < nm; ++j) {
+                if (!gen_on) {
+                    // first tokens only: results stay on the stream (pinned host copies), read once
+                    // after the last wave
+                    ExtendDefer dd;
+                    dd.logits = o->logits ? def_lg + static_cast<size_t>(def_n) * SGC_VOCAB : nullptr;
+                    dd.first = def_ft + def_n;
+                    do_extend(c, model, kv, nm, mem_seg.data(), mq_off.data(), mq_tok.data(),
+                              ans ? ma_off.data() : nullptr, ans ? ma_tok.data() : nullptr, b->pointer_bonus,
+                              nullptr, nullptr, nullptr, &dd);
+                    for (uint32_t k = 0; k < nm; ++k) def_q.push_back(mem_q[dd.order[k]]);
+                    def_n += nm;
+                }
+                std::vector<float> lg(gen_on ? static_cast<size_t>(nm) * SGC_VOCAB : 0);
+                std::vector<int32_t> ft(gen_on ? nm : 0);
+                if (gen_on)
+                    do_extend(c, model, kv, nm, mem_seg.data(), mq_off.data(), mq_tok.data(), ans ? ma_off.data() : nullptr,
+                              ans ? ma_tok.data() : nullptr, b->pointer_bonus, lg.data(), ft.data(), &keep);
+                for (uint32_t j = 0; gen_on && j < nm; ++j) {
                     const uint32_t q = mem_q[j];
                     if (gen_on) {
                         const int32_t S = static_cast<int32_t>(q_off[q + 1] - q_off[q]);
@@ -2104,6 +2163,15 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             }
         }
         c->sync();
+        check_forward_flags(c);
+        for (uint32_t k = 0; k < def_n; ++k) {
+            const uint32_t q = def_q[k];
+            if (o->logits)
+                std::memcpy(o->logits + static_cast<size_t>(q) * SGC_VOCAB, def_lg + static_cast<size_t>(k) * SGC_VOCAB,
+                            SGC_VOCAB * sizeof(float));
+            if (o->first_token) o->first_token[q] = def_ft[k];
+            if (o->fallback) o->fallback[q] = 0;
+        }
         std::vector<float> wave_ms;
         for (cudaEvent_t e : ev_wave) {
             float ms = 0;

@@ -8,6 +8,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -139,6 +140,48 @@ struct Ctx {
     void sync() {
         SGC_CUDA_CHECK(cudaStreamSynchronize(stream));
         resolve_timings();
+    }
+    // grow-only PINNED host buffers keyed by name (asynchronous device -> host copies)
+    std::map<std::string, Buffer> pinned_bufs;
+    template <typename T>
+    T* pinned(const std::string& name, size_t count) {
+        Buffer& b = pinned_bufs[name];
+        size_t need = std::max<size_t>(16, count * sizeof(T));
+        if (b.bytes < need) {
+            if (b.ptr) {
+                SGC_CUDA_CHECK(cudaStreamSynchronize(stream));  // no copy may still target it
+                SGC_CUDA_CHECK(cudaFreeHost(b.ptr));
+            }
+            SGC_CUDA_CHECK(cudaMallocHost(&b.ptr, need + need / 8));
+            b.bytes = need + need / 8;
+        }
+        return reinterpret_cast<T*>(b.ptr);
+    }
+    // device [0, 1, ..., n-1] (grown on demand, filled on the device: no host round trip)
+    int32_t* iota(int n);
+    int iota_n = 0;
+    int32_t* iota_ptr = nullptr;
+    // error flags raised by kernels: copied (stream-ordered) into pinned host memory and OR-ed
+    // there; take_flag() is valid after the next stream sync
+    int* h_flags = nullptr;
+    int n_flags = 0;
+    void flag_readback(const int* d_flag) {
+        if (!h_flags) SGC_CUDA_CHECK(cudaMallocHost(&h_flags, 64 * sizeof(int)));
+        if (n_flags == 64) {  // rare: fold the pending flags first
+            sync();
+            int any = 0;
+            for (int i = 0; i < n_flags; ++i) any |= h_flags[i];
+            h_flags[0] = any;
+            n_flags = 1;
+        }
+        SGC_CUDA_CHECK(cudaMemcpyAsync(h_flags + n_flags, d_flag, sizeof(int), cudaMemcpyDeviceToHost, stream));
+        ++n_flags;
+    }
+    bool take_flag() {
+        int any = 0;
+        for (int i = 0; i < n_flags; ++i) any |= h_flags[i];
+        n_flags = 0;
+        return any != 0;
     }
 };
 

@@ -517,6 +517,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 // ---- host side ----------------------------------------------------------------------------
 
+// CUDA-event timing category per fused epilogue (bench.py sums "gemm*" for the roofline)
+constexpr const char* gemm_timer_name(int epi) {
+    return epi == EPI_QKV ? "gemm_qkv" : epi == EPI_RESID ? "gemm_resid" : epi == EPI_TANH ? "gemm_tanh" : "gemm";
+}
+
 template <int BN, int EPI, int HD>
 void launch(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
     using Cf = Cfg<BN>;
@@ -530,7 +535,7 @@ void launch(Ctx* c, const void* A, const void* B, int M, int N, int K, const Gem
     CUtensorMap tb = make_map_2d(B, N, K, BN, BK);
     int tiles = ((M + BM - 1) / BM) * (N / BN);
     int grid = tiles < c->num_sms ? tiles : c->num_sms;
-    Ctx::Timed timer(c, "gemm");
+    Ctx::Timed timer(c, gemm_timer_name(EPI));
     kfn<<<grid, kThreads, Cf::kSmem, c->stream>>>(ta, tb, M, N, K, ep);
     SGC_LAUNCH_CHECK(c);
 }
@@ -547,7 +552,7 @@ void launch2(Ctx* c, const void* A, const void* B, int M, int N, int K, const Ge
     CUtensorMap tb = make_map_2d(B, N, K, BM, BK);
     int tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / 256);
     int grid = 2 * tiles < c->num_sms ? 2 * tiles : (c->num_sms & ~1);
-    Ctx::Timed timer(c, "gemm");
+    Ctx::Timed timer(c, gemm_timer_name(EPI));
     kfn<<<grid, kThreads, Cfg2::kSmem, c->stream>>>(ta, tb, M, N, K, ep);
     SGC_LAUNCH_CHECK(c);
 }

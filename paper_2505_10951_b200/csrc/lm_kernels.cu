@@ -326,6 +326,22 @@ void step_tokens(Ctx* c, int32_t* tok, const float* logits, int n, const int8_t*
     step_token_kernel<<<n, 128, 0, c->stream>>>(tok, logits, n, hint, ans, ans_off, member, step, bonus);
     SGC_LAUNCH_CHECK(c);
 }
+namespace {
+__global__ void iota_kernel(int32_t* p, int n) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
+}
+}  // namespace
+int32_t* Ctx::iota(int n) {
+    int32_t* p = buf<int32_t>("iota", n);
+    const int cap = static_cast<int>(scratch["iota"].bytes / sizeof(int32_t));
+    if (n > iota_n || iota_ptr != p) {
+        iota_kernel<<<grid_for(static_cast<uint64_t>(cap), 256, num_sms), 256, 0, stream>>>(p, cap);
+        SGC_LAUNCH_CHECK(this);
+        iota_n = cap;
+        iota_ptr = p;
+    }
+    return p;
+}
 void head_transpose(Ctx* c, float* out_t, const float* head, int d) {
     transpose_head<<<grid_for((uint64_t)SGC_VOCAB * d, 256, c->num_sms), 256, 0, c->stream>>>(out_t, head, d);
     SGC_LAUNCH_CHECK(c);
