@@ -239,6 +239,12 @@ typedef struct {
     uint32_t* n_tokens;     /* [m] tokens generated (stops on EOS, max_new, full context) */
     float* rt_ms;           /* [m] submission -> last token (QueryOutcome::rt_ms semantics) */
     uint64_t decode_rows;   /* member-steps pushed through the decode forward */
+    /* ledger / report timings (optional, HOST memory; ms since submission like ttft_ms):
+     * seal_ms [c]  the cluster's prefix sealed (its wave's prefill done), -1 if not served here
+     * pftt_ms [m]  QueryOutcome::pftt_ms: the query's own work start (its wave's extend, or its
+     *              standalone prefill for a fallback) -> first token */
+    float* seal_ms;
+    float* pftt_ms;
 } sgc_batch_out;
 
 int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_batch* batch,

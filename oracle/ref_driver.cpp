@@ -386,6 +386,24 @@ json cmd_pipeline(const json& spec) {
 }
 
 // Bounded timing samples of each stage at a model shape (bench.py --impl reference).
+// the reference's whole run() (pipeline.cpp:114-320) -> its subgcache-report-v1 document
+json cmd_run(const json& spec) {
+    RunConfig rc;
+    rc.graph_nodes_path = spec.at("nodes_csv");
+    rc.graph_edges_path = spec.at("edges_csv");
+    rc.queries_path = spec.at("queries_jsonl");
+    rc.undirected = spec.value("undirected", false);
+    rc.retrieval.strategy = retrieval_strategy_from_string(spec.value("retrieval", std::string("ego-topk")));
+    rc.cluster.linkage = linkage_from_string(spec.value("linkage", std::string("ward")));
+    rc.cluster.cluster_count = spec.value("clusters", 4u);
+    rc.seed = spec.value("seed", 7ull);
+    if (spec.contains("lm")) rc.lm = lm_cfg(spec["lm"]);
+    const std::string soft = spec.value("soft_prefix", std::string("auto"));
+    rc.soft_prefix = soft == "on" ? SoftPrefixMode::On : (soft == "off" ? SoftPrefixMode::Off : SoftPrefixMode::Auto);
+    BatchReport r = run(rc);
+    return json::parse(r.to_json());
+}
+
 json cmd_bench(const json& spec) {
     json out;
     ToyLmConfig lc = lm_cfg(spec.at("lm"));
@@ -481,6 +499,7 @@ int main(int argc, char** argv) {
         else if (cmd == "prompt") out = cmd_prompt(spec);
         else if (cmd == "pipeline") out = cmd_pipeline(spec);
         else if (cmd == "bench") out = cmd_bench(spec);
+        else if (cmd == "run") out = cmd_run(spec);
         else if (cmd == "synth") {  // the reference's own synthetic dataset writer
             auto ds = testsupport::write_synth_dataset(spec.at("dir"), spec.at("m").get<size_t>());
             out = json{{"nodes", ds.nodes_path}, {"edges", ds.edges_path}, {"queries", ds.queries_path}};

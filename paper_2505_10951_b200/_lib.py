@@ -89,7 +89,8 @@ class BatchOut(C.Structure):
                 ("stage_ms", C.c_double * 8),
                 ("prefill_rows", C.c_uint64), ("extend_rows", C.c_uint64),
                 ("tokens", C.POINTER(C.c_int32)), ("n_tokens", C.POINTER(C.c_uint32)),
-                ("rt_ms", C.POINTER(C.c_float)), ("decode_rows", C.c_uint64)]
+                ("rt_ms", C.POINTER(C.c_float)), ("decode_rows", C.c_uint64),
+                ("seal_ms", C.POINTER(C.c_float)), ("pftt_ms", C.POINTER(C.c_float))]
 
 
 # every symbol include/sgc_b200.h declares (checked by tests/test_boundary.py)

@@ -1865,7 +1865,8 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         }
         cudaEvent_t ev_start = c->event();
         SGC_CUDA_CHECK(cudaEventRecord(ev_start, c->stream));
-        std::vector<cudaEvent_t> ev_wave;
+        std::vector<cudaEvent_t> ev_wave, ev_seal, ev_wave_start;
+        std::vector<uint8_t> fb_flag(m, 0);
         std::vector<int32_t> wave_of(m, -1);
         uint64_t prefill_rows = 0, extend_rows = 0, decode_rows = 0;
         double pf_ms = 0, ex_ms = 0, dec_ms = 0;
@@ -1938,6 +1939,11 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             const uint32_t we = wave_end[wv];
             if (we <= wb) continue;
             const double tw0 = now_ms();
+            {
+                cudaEvent_t e0 = c->event();
+                SGC_CUDA_CHECK(cudaEventRecord(e0, c->stream));
+                ev_wave_start.push_back(e0);
+            }
             std::vector<uint64_t> seq_off(1, 0);
             std::vector<int32_t> seq_tok;
             std::vector<uint8_t> seq_soft;
@@ -1995,6 +2001,11 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                                     arena_row0, arena_rows, /*sync=*/!fb_q.empty());
             std::unique_ptr<sgc_kv, int (*)(sgc_kv*)> kv_guard(kv, sgc_kv_release);
             prefill_rows += kv->rows;
+            {
+                cudaEvent_t es = c->event();
+                SGC_CUDA_CHECK(cudaEventRecord(es, c->stream));
+                ev_seal.push_back(es);
+            }
             const int32_t pfx_base = static_cast<int32_t>(arena_row0);  // absolute arena row of this wave
             if (!kv_all.k) {
                 kv_all.k = kv->k - arena_row0 * d;
@@ -2086,6 +2097,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 if (o->logits) std::memcpy(o->logits + static_cast<size_t>(q) * SGC_VOCAB, lg, SGC_VOCAB * sizeof(float));
                 if (o->first_token) o->first_token[q] = best;
                 if (o->fallback) o->fallback[q] = 1;
+                fb_flag[q] = 1;
                 if (gen_on) {  // standalone decode continues from its own sealed prompt
                     gen_q.push_back(q);
                     gj.pfx_kv0.push_back(pfx_base + static_cast<int32_t>(kv->off[s]));
@@ -2197,6 +2209,36 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         if (o->ttft_ms)
             for (uint32_t q = 0; q < m; ++q)
                 o->ttft_ms[q] = wave_of[q] >= 0 ? static_cast<float>(pre_ms + wave_ms[wave_of[q]]) : -1.0f;
+        {
+            // ledger / report timings from the per-wave events
+            std::vector<float> seal_w(ev_seal.size()), start_w(ev_wave_start.size());
+            for (size_t w = 0; w < ev_seal.size(); ++w) {
+                SGC_CUDA_CHECK(cudaEventElapsedTime(&seal_w[w], ev_start, ev_seal[w]));
+                SGC_CUDA_CHECK(cudaEventElapsedTime(&start_w[w], ev_start, ev_wave_start[w]));
+            }
+            if (o->seal_ms) {
+                for (uint32_t ci = 0; ci < k; ++ci) o->seal_ms[ci] = -1.0f;
+                uint32_t w0 = 0;
+                for (size_t w = 0; w < wave_end.size() && w < seal_w.size(); ++w) {
+                    for (uint32_t i = w0; i < wave_end[w]; ++i) o->seal_ms[owned[i]] = static_cast<float>(pre_ms + seal_w[w]);
+                    w0 = wave_end[w];
+                }
+            }
+            if (o->pftt_ms)
+                for (uint32_t q = 0; q < m; ++q) {
+                    const int wq = wave_of[q];
+                    if (wq < 0) {
+                        o->pftt_ms[q] = -1.0f;
+                        continue;
+                    }
+                    // members: from their wave's extend (= the seal event); fallbacks: from the
+                    // wave's prefill start (their standalone prefill)
+                    const bool fbq = fb_flag[q] != 0;
+                    o->pftt_ms[q] = wave_ms[wq] - (fbq ? start_w[wq] : seal_w[wq]);
+                }
+            for (cudaEvent_t e : ev_seal) c->event_pool.push_back(e);
+            for (cudaEvent_t e : ev_wave_start) c->event_pool.push_back(e);
+        }
         o->waves = static_cast<uint32_t>(ev_wave.size());
         const double t_pf = t_rep + pf_ms;
         const double t_ext = now_ms();

@@ -474,6 +474,8 @@ class SubgCacheResult:
     rt_ms: np.ndarray | None = None
     decode_ms: float = 0.0
     decode_rows: int = 0
+    seal_ms: np.ndarray | None = None   # [c] cluster prefix sealed (ms since submission)
+    pftt_ms: np.ndarray | None = None   # [m] own work start -> first token
 
 
 class PreparedBatch:
@@ -587,6 +589,10 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     o.logits = _p(logits, C.c_float)
     o.first_token = _p(first, C.c_int32)
     o.fallback = _p(fb, C.c_uint8)
+    seal = np.full(k, -1.0, np.float32)
+    pftt = np.full(m, -1.0, np.float32)
+    o.seal_ms = _p(seal, C.c_float)
+    o.pftt_ms = _p(pftt, C.c_float)
     toks = cnt = rt = None
     if max_new > 1:
         toks = np.full((m, max_new), -1, np.int32)
@@ -599,6 +605,7 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     res = SubgCacheResult(emb, labels, left[: m - k], right[: m - k], dist[: m - k], plen, logits,
                           first, fb, owner, ttft, o.waves, list(o.stage_ms)[:6], o.prefill_rows,
                           o.extend_rows)
+    res.seal_ms, res.pftt_ms = seal, pftt
     if max_new > 1:
         res.tokens = [toks[q, :cnt[q]].copy() for q in range(m)]
         res.rt_ms = rt

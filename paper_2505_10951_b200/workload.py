@@ -70,11 +70,15 @@ class TextualGraph:
     def sorted_node_ids(self) -> np.ndarray:
         return np.array(sorted(self.nodes), dtype=np.uint32)
 
+    quote_node_attrs: bool = False  # tests/support/synth.hpp:38-47 quotes every node attribute
+
     def write_csv(self, node_path: str, edge_path: str) -> None:
         with open(node_path, "wb") as f:
             f.write(b"node id,node attr\n")
             for nid in sorted(self.nodes):
-                f.write(b"%d,%s\n" % (nid, csv_quote(self.nodes[nid])))
+                a = self.nodes[nid]
+                q = b'"' + a.replace(b'"', b'""') + b'"' if self.quote_node_attrs else csv_quote(a)
+                f.write(b"%d,%s\n" % (nid, q))
         with open(edge_path, "wb") as f:
             f.write(b"src,edge attr,dst\n")
             for s, a, d in self.edges:
@@ -166,6 +170,7 @@ def c1_workload(m: int = 64, clusters: int = 4) -> Workload:
     for the engine topic, nodes 8..15 / edges 7..13 for the garden topic); the
     golden fixture pins this against the reference's retrieve()."""
     g, qs = two_star_dataset(m)
+    g.quote_node_attrs = True  # byte-identical to the reference's writer (dataset digest)
     stars = [Subgraph.of(range(0, 8), range(0, 7)), Subgraph.of(range(8, 16), range(7, 14))]
     return Workload("c1-tiny-twostar", g, qs, [stars[j % 2] for j in range(m)], dict(TINY_LM),
                     clusters, seed=7)

@@ -65,6 +65,18 @@ def c1_pipeline(td):
     dump("c1_pipeline.json", out)
 
 
+def c1_report(td):
+    """The reference's whole run() on the C1 dataset: its subgcache-report-v1 (pipeline.cpp:388-452)
+    and the dataset files' digest inputs (the GPU report must reproduce digest, clusters, proxies,
+    generations and correctness exactly; wall times differ)."""
+    d = os.path.join(td, "c1r")
+    ref = oracle.run_ref({"cmd": "synth", "dir": d, "m": 64})
+    out = oracle.run_ref({"cmd": "run", "nodes_csv": ref["nodes"], "edges_csv": ref["edges"],
+                          "queries_jsonl": ref["queries"], "clusters": 4, "linkage": "ward", "seed": 7,
+                          "retrieval": "ego-topk"})
+    dump("c1_report.json", out)
+
+
 def c1_variants(td):
     """Same dataset with c in {2, 64} (c=m degenerates to the baseline, acceptance.cpp:108-124)
     and soft-prefix on (node-edge-topk semantics)."""
@@ -212,6 +224,7 @@ if __name__ == "__main__":
         oracle.build(ref=True)
     with tempfile.TemporaryDirectory() as td:
         c1_pipeline(td)
+        c1_report(td)
         c1_variants(td)
         lm_cases()
         cluster_cases()
