@@ -28,7 +28,27 @@ namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
-constexpr int kThreads = 256;
+// warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4-11 epilogue (two warpgroups,
+// each owning half of the tile's 32-column chunks; a warp may only read TMEM lanes 32*(warp%4))
+constexpr int kThreads = 384;
+constexpr int kEpiThreads = 256;
+// per epilogue warp: a 32 x 33 fp32 staging tile (row-major, padded: conflict-free both ways)
+constexpr int kStageSmem = 8 * 32 * 33 * 4;
+
+// chunk range of epilogue warpgroup `eg` (0/1): halves of the tile, or everything in group 0 when
+// a QKV head (RoPE pairs chunk ch with ch + HD/64) would straddle the halves
+template <int BN, int EPI, int HD>
+__device__ __forceinline__ void epi_chunks(int eg, int& lo, int& hi) {
+    constexpr int NCH = BN / 32;
+    constexpr bool split = NCH % 2 == 0 && !(EPI == EPI_QKV && BN < 2 * HD);
+    if (split) {
+        lo = eg * (NCH / 2);
+        hi = lo + NCH / 2;
+    } else {
+        lo = 0;
+        hi = eg == 0 ? NCH : 0;
+    }
+}
 
 template <int BN>
 struct Cfg {
@@ -37,7 +57,7 @@ struct Cfg {
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
-    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ + kStageSmem;
 };
 
 __device__ __forceinline__ float tanh_fast(float x) {
@@ -84,7 +104,8 @@ __device__ __forceinline__ void rope_pair(float* lo, float* hi, const float* cos
 // this warp's 32 lanes at the tile's first column, `row` is this thread's output row.
 template <int BN, int EPI, int HD>
 __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool valid, int n0,
-                                              const GemmEpi& ep) {
+                                              const GemmEpi& ep, int ch_lo, int ch_hi, float* stage,
+                                              int ep_rows) {
     // fused RMSNorm of the A rows: one scale per accumulator row
     float inv = 1.0f;
     if (ep.in_ss && valid) inv = 1.0f / sqrtf(ep.in_ss[row] / static_cast<float>(ep.norm_dim) + 1e-5f);
@@ -101,7 +122,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
         }
         if (section == 2) {
 #pragma unroll 1
-            for (int ch = 0; ch < BN / 32; ++ch) {
+            for (int ch = ch_lo; ch < ch_hi; ++ch) {
                 uint32_t r[32];
                 ptx::tmem_ld32(tbase + ch * 32, r);
                 ptx::tmem_ld_wait();
@@ -121,20 +142,26 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
             if constexpr (HALF >= 32) {
                 // pairs span two chunks: (ch, ch + HALF/32) within each head
 #pragma unroll 1
-                for (int ch = 0; ch < BN / 32; ++ch) {
+                for (int ch = ch_lo; ch < ch_hi; ++ch) {
                     const int in_head = (ch * 32) % HD;
                     if (in_head >= HALF) continue;
                     const int ch2 = ch + HALF / 32;
+                    // RoPE table rows (128 B aligned) in flight while the accumulator loads
+                    float cs[32], sn[32];
+                    if (valid) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            reinterpret_cast<float4*>(cs)[j] = __ldg(reinterpret_cast<const float4*>(cosp + in_head) + j);
+                            reinterpret_cast<float4*>(sn)[j] = __ldg(reinterpret_cast<const float4*>(sinp + in_head) + j);
+                        }
+                    }
                     uint32_t lo[32], hi[32];
                     ptx::tmem_ld32(tbase + ch * 32, lo);
                     ptx::tmem_ld32(tbase + ch2 * 32, hi);
                     ptx::tmem_ld_wait();
                     if (valid) {
-                        float cs[32], sn[32];
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
-                            cs[j] = __ldg(cosp + in_head + j);
-                            sn[j] = __ldg(sinp + in_head + j);
                             reinterpret_cast<float*>(lo)[j] *= inv;
                             reinterpret_cast<float*>(hi)[j] *= inv;
                         }
@@ -147,7 +174,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
             } else {
                 // whole heads inside one 32-column chunk
 #pragma unroll 1
-                for (int ch = 0; ch < BN / 32; ++ch) {
+                for (int ch = ch_lo; ch < ch_hi; ++ch) {
                     uint32_t r[32];
                     ptx::tmem_ld32(tbase + ch * 32, r);
                     ptx::tmem_ld_wait();
@@ -172,62 +199,81 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
             }
         }
     } else {
+        // Coalesced epilogue: each warp owns a 32-row x 32-column chunk per step; the accumulator
+        // (thread = row) goes through a padded shared-memory tile and leaves along rows: lane l
+        // handles rows 2i + l/16 and the column pair 2(l%16), so every warp instruction moves two
+        // full 128 B (fp32) / 64 B (bf16) row segments instead of touching 32 lines -- the L1TEX
+        // path stays free for the TMA operand loads.
         float ss = 0.f;  // EPI_RESID with out_ss: this row's partial sum of squares of x_new
+        const int lane = threadIdx.x & 31;
+        const int row0 = row - lane;    // the warp's first row
+        const int half = lane >> 4;     // row parity handled by this lane
+        const int c2 = 2 * (lane & 15);  // column pair within the chunk
 #pragma unroll 1
-        for (int ch = 0; ch < BN / 32; ++ch) {
+        for (int ch = ch_lo; ch < ch_hi; ++ch) {
+            const int col = n0 + ch * 32 + c2;
+            // residual inputs (16 row pairs) in flight with the TMEM load
+            float2 xo[16];
+            if constexpr (EPI == EPI_RESID) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int gr = row0 + 2 * i + half;
+                    xo[i] = gr < ep_rows ? *reinterpret_cast<const float2*>(static_cast<const float*>(ep.out) +
+                                                                            static_cast<size_t>(gr) * ep.ldo + col)
+                                         : make_float2(0.f, 0.f);
+                }
+            }
             uint32_t r[32];
             ptx::tmem_ld32(tbase + ch * 32, r);
             ptx::tmem_ld_wait();
-            if (!valid) continue;
             float* v = reinterpret_cast<float*>(r);
-            const int col = n0 + ch * 32;
             if constexpr (EPI != EPI_RESID) {
-                if (ep.in_ss) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] *= inv;
-                }
+                for (int j = 0; j < 32; ++j) v[j] *= inv;
             }
-            if constexpr (EPI == EPI_F32) {
-                float4* dst = reinterpret_cast<float4*>(
-                    static_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ldo + col);
-#pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            } else if constexpr (EPI == EPI_BF16) {
-                store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) +
-                                  static_cast<size_t>(row) * ep.ldo + col,
-                              v);
-            } else if constexpr (EPI == EPI_TANH) {
+            if constexpr (EPI == EPI_TANH) {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = tanh_fast(v[j]);
-                store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) +
-                                  static_cast<size_t>(row) * ep.ldo + col,
-                              v);
-            } else if constexpr (EPI == EPI_RESID) {
-                float4* dst = reinterpret_cast<float4*>(
-                    static_cast<float*>(ep.out) + static_cast<size_t>(row) * ep.ldo + col);
+            }
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    float4 x = dst[q];
-                    x.x += v[4 * q];
-                    x.y += v[4 * q + 1];
-                    x.z += v[4 * q + 2];
-                    x.w += v[4 * q + 3];
-                    dst[q] = x;
-                    v[4 * q] = x.x;
-                    v[4 * q + 1] = x.y;
-                    v[4 * q + 2] = x.z;
-                    v[4 * q + 3] = x.w;
+            for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = v[j];
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int lr = 2 * i + half, gr = row0 + lr;
+                float2 val = make_float2(stage[lr * 33 + c2], stage[lr * 33 + c2 + 1]);
+                const size_t off = static_cast<size_t>(gr) * ep.ldo + col;
+                if constexpr (EPI == EPI_RESID) {
+                    val.x += xo[i].x;
+                    val.y += xo[i].y;
+                    stage[lr * 33 + c2] = val.x;
+                    stage[lr * 33 + c2 + 1] = val.y;
                 }
+                if (gr < ep_rows) {
+                    if constexpr (EPI == EPI_RESID || EPI == EPI_F32) {
+                        *reinterpret_cast<float2*>(static_cast<float*>(ep.out) + off) = val;
+                        if constexpr (EPI == EPI_RESID)
+                            if (ep.out_xb) *reinterpret_cast<__nv_bfloat162*>(ep.out_xb + off) = __floats2bfloat162_rn(val.x, val.y);
+                    } else {
+                        *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(ep.out) + off) =
+                            __floats2bfloat162_rn(val.x, val.y);
+                    }
+                }
+            }
+            __syncwarp();
+            if constexpr (EPI == EPI_RESID) {
                 if (ep.out_xb) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) ss = fmaf(v[j], v[j], ss);
-                    store_bf16x32(ep.out_xb + static_cast<size_t>(row) * ep.ldo + col, v);
+                    for (int j = 0; j < 32; ++j) {
+                        const float xv = stage[lane * 33 + j];
+                        ss = fmaf(xv, xv, ss);
+                    }
                 }
+                __syncwarp();
             }
         }
         if constexpr (EPI == EPI_RESID) {
-            if (ep.out_ss && valid) atomicAdd(ep.out_ss + row, ss);
+            if (ep.out_ss && valid && ch_hi > ch_lo) atomicAdd(ep.out_ss + row, ss);
         }
     }
 }
@@ -268,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 128);
+            ptx::mbar_init(&tempty[a], kEpiThreads);
         }
         ptx::fence_barrier_init();
     }
@@ -340,7 +386,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
+        const int ew = warp & 3;  // TMEM lanes 32*ew .. 32*ew+31
+        int ch_lo, ch_hi;
+        epi_chunks<BN, EPI, HD>((warp - 4) / 4, ch_lo, ch_hi);
+        float* stage = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256) + (warp - 4) * 32 * 33;
         int local = 0;
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
             int m0, n0;
@@ -353,7 +402,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool valid = row < M;
             const uint32_t tbase = tmem_base + ((ew * 32) << 16) + acc * BN;
 
-            epilogue_tile<BN, EPI, HD>(tbase, row, valid, n0, ep);
+            epilogue_tile<BN, EPI, HD>(tbase, row, valid, n0, ep, ch_lo, ch_hi, stage, M);
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);
         }
@@ -376,7 +425,7 @@ struct Cfg2 {
     static constexpr int kABytes = BM * BK * 2;  // this CTA's 128 rows of A
     static constexpr int kBBytes = BM * BK * 2;  // this CTA's 128 rows of B
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kSmem = kStages2 * kStageBytes + 1024 + 256;
+    static constexpr int kSmem = kStages2 * kStageBytes + 1024 + 256 + kStageSmem;
 };
 
 template <int EPI, int HD>
@@ -417,7 +466,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 2 * 128);  // both CTAs' epilogue threads release
+            ptx::mbar_init(&tempty[a], 2 * kEpiThreads);  // both CTAs' epilogue threads release
         }
         ptx::fence_barrier_init();
     }
@@ -490,7 +539,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        const int ew = warp - 4;
+        const int ew = warp & 3;
+        int ch_lo, ch_hi;
+        epi_chunks<BN, EPI, HD>((warp - 4) / 4, ch_lo, ch_hi);
+        float* stage = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256) + (warp - 4) * 32 * 33;
         int local = 0;
         for (int t = pair; t < num_tiles; t += npairs, ++local) {
             int m0, n0;
@@ -501,7 +553,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             const int row = m0 + static_cast<int>(rank) * BM + ew * 32 + lane;
             const uint32_t tbase = tmem_base + ((ew * 32) << 16) + acc * BN;
-            epilogue_tile<BN, EPI, HD>(tbase, row, row < M, n0, ep);
+            epilogue_tile<BN, EPI, HD>(tbase, row, row < M, n0, ep, ch_lo, ch_hi, stage, M);
             ptx::tc_fence_before();
             ptx::mbar_arrive_cluster(&tempty[acc], 0);
         }
