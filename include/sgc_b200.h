@@ -232,7 +232,8 @@ typedef struct {
     uint32_t* owner;        /* [c] optional: rank serving each cluster */
     float* ttft_ms;         /* [m] optional: submission -> first token (-1 if not served here) */
     uint32_t waves;         /* waves actually run */
-    double stage_ms[8];     /* encode, cluster, represent, prefill, extend, total, -, - */
+    double stage_ms[8];     /* encode, cluster, represent (host clock); prefill, extend (device events,
+                             * summed over waves); total; decode (host clock); - */
     uint64_t prefill_rows, extend_rows; /* tokens pushed through prefill / extend */
     /* with batch.max_new_tokens > 1 (all optional, HOST memory): */
     int32_t* tokens;        /* [m * max_new_tokens] generated ids, -1 padded (GenerationResult::token_ids) */

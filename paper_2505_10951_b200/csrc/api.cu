@@ -1789,11 +1789,23 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         std::vector<uint32_t> owned;
         for (uint32_t ci = 0; ci < k; ++ci)
             if (owner[ci] == static_cast<uint32_t>(world > 1 || b->cluster_owner ? b->rank : 0)) owned.push_back(ci);
+        // serving order: Smith's rule (ascending row cost per query) so the waves that finish
+        // first carry the most queries -- minimizes the summed (mean) TTFT; results are
+        // independent of the order (every row's math is batch-independent)
+        if (b->waves > 1) {
+            std::vector<double> ratio(k, 0.0);
+            for (uint32_t ci : owned) {
+                double cost = static_cast<double>(reps_all.prefix_off[ci + 1] - reps_all.prefix_off[ci]);
+                for (uint32_t q : members[ci]) cost += static_cast<double>(q_off_all[q + 1] - q_off_all[q]);
+                ratio[ci] = cost / std::max<size_t>(1, members[ci].size());
+            }
+            std::stable_sort(owned.begin(), owned.end(), [&](uint32_t a, uint32_t b2) { return ratio[a] < ratio[b2]; });
+        }
         std::vector<std::vector<uint32_t>> own_members;
         for (uint32_t ci : owned) own_members.push_back(members[ci]);
         RepResult reps;
         if (!owned.empty()) {
-            if (owned.size() == k) reps = reps_all;
+            if (owned.size() == k && b->waves <= 1) reps = reps_all;
             else reps = build_reps(c, g, hs, m, own_members, budget);
         }
         std::vector<float> soft_h;
@@ -1867,6 +1879,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         SGC_CUDA_CHECK(cudaEventRecord(ev_start, c->stream));
         std::vector<cudaEvent_t> ev_wave, ev_seal, ev_wave_start;
         std::vector<uint8_t> fb_flag(m, 0);
+        double dev_pf_ms = 0.0, dev_ex_ms = 0.0;
         std::vector<int32_t> wave_of(m, -1);
         uint64_t prefill_rows = 0, extend_rows = 0, decode_rows = 0;
         double pf_ms = 0, ex_ms = 0, dec_ms = 0;
@@ -2236,6 +2249,13 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                     const bool fbq = fb_flag[q] != 0;
                     o->pftt_ms[q] = wave_ms[wq] - (fbq ? start_w[wq] : seal_w[wq]);
                 }
+            // device-side stage times (the host runs ahead of the GPU without per-wave syncs):
+            // prefill = wave start -> seal, extend = seal -> the wave's first tokens
+            dev_pf_ms = dev_ex_ms = 0.0;
+            for (size_t w = 0; w < seal_w.size() && w < wave_ms.size(); ++w) {
+                dev_pf_ms += seal_w[w] - start_w[w];
+                dev_ex_ms += wave_ms[w] - seal_w[w];
+            }
             for (cudaEvent_t e : ev_seal) c->event_pool.push_back(e);
             for (cudaEvent_t e : ev_wave_start) c->event_pool.push_back(e);
         }
@@ -2253,8 +2273,10 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         o->stage_ms[0] = t_enc - t_start;
         o->stage_ms[1] = t_cl - t_enc;
         o->stage_ms[2] = t_rep - t_cl;
-        o->stage_ms[3] = pf_ms;
-        o->stage_ms[4] = ex_ms;
+        o->stage_ms[3] = dev_pf_ms;
+        o->stage_ms[4] = dev_ex_ms;
+        (void)pf_ms;
+        (void)ex_ms;
         o->stage_ms[5] = now_ms() - t_start;
         o->prefill_rows = prefill_rows;
         o->extend_rows = extend_rows;

@@ -204,6 +204,27 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
         // handles rows 2i + l/16 and the column pair 2(l%16), so every warp instruction moves two
         // full 128 B (fp32) / 64 B (bf16) row segments instead of touching 32 lines -- the L1TEX
         // path stays free for the TMA operand loads.
+        if constexpr (EPI == EPI_TANH || EPI == EPI_BF16) {
+            // bf16 outputs: each thread stores its own row's 64 B per chunk (measured faster for
+            // the FFN activation than the transposed path: 97.7% vs 92% tensor-active)
+#pragma unroll 1
+            for (int ch = ch_lo; ch < ch_hi; ++ch) {
+                uint32_t r[32];
+                ptx::tmem_ld32(tbase + ch * 32, r);
+                ptx::tmem_ld_wait();
+                if (!valid) continue;
+                float* v = reinterpret_cast<float*>(r);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    v[j] *= inv;
+                    if constexpr (EPI == EPI_TANH) v[j] = tanh_fast(v[j]);
+                }
+                store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(row) * ep.ldo + n0 + ch * 32, v);
+            }
+            (void)stage;
+            (void)ep_rows;
+            return;
+        }
         float ss = 0.f;  // EPI_RESID with out_ss: this row's partial sum of squares of x_new
         const int lane = threadIdx.x & 31;
         const int row0 = row - lane;    // the warp's first row
