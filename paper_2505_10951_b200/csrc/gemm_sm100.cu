@@ -74,6 +74,17 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 }
 
 // store 32 fp32 values as bf16 (64 contiguous bytes)
+__device__ __forceinline__ void store_bf16x32_stream(__nv_bfloat16* dst, const float* v, uint64_t pol) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        uint4 w;
+        w.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
+        w.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
+        w.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
+        w.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
+        ptx::st_global_v4_hint(dst + 8 * q, w, pol);
+    }
+}
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v) {
     uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
@@ -206,7 +217,9 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
         // path stays free for the TMA operand loads.
         if constexpr (EPI == EPI_TANH || EPI == EPI_BF16) {
             // bf16 outputs: each thread stores its own row's 64 B per chunk (measured faster for
-            // the FFN activation than the transposed path: 97.7% vs 92% tensor-active)
+            // the FFN activation than the transposed path: 97.7% vs 92% tensor-active); streamed
+            // with evict_first so they do not push the group's operand tiles out of L2
+            const uint64_t stream_pol = ptx::policy_evict_first();
 #pragma unroll 1
             for (int ch = ch_lo; ch < ch_hi; ++ch) {
                 uint32_t r[32];
@@ -219,7 +232,8 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                     v[j] *= inv;
                     if constexpr (EPI == EPI_TANH) v[j] = tanh_fast(v[j]);
                 }
-                store_bf16x32(static_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(row) * ep.ldo + n0 + ch * 32, v);
+                store_bf16x32_stream(static_cast<__nv_bfloat16*>(ep.out) + static_cast<size_t>(row) * ep.ldo + n0 + ch * 32, v,
+                                     stream_pol);
             }
             (void)stage;
             (void)ep_rows;
@@ -359,14 +373,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            // operands are re-read across the raster group's tiles: keep them in L2 ahead of the
+            // streamed epilogue outputs
+            const uint64_t keep = ptx::policy_evict_last();
             for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
                 int m0, n0;
                 tile_coords(t, m0, n0);
                 for (int kb = 0; kb < num_kb; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     ptx::mbar_expect_tx(&full[stage], C::kStageBytes);
-                    ptx::tma_load_2d(smemA + stage * C::kABytes, &tmA, &full[stage], kb * BK, m0);
-                    ptx::tma_load_2d(smemB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, n0);
+                    ptx::tma_load_2d_hint(smemA + stage * C::kABytes, &tmA, &full[stage], kb * BK, m0, keep);
+                    ptx::tma_load_2d_hint(smemB + stage * C::kBBytes, &tmB, &full[stage], kb * BK, n0, keep);
                     if (++stage == C::kStages) {
                         stage = 0;
                         phase ^= 1;
@@ -512,16 +529,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            const uint64_t keep = ptx::policy_evict_last();  // operands re-read across the group
             for (int t = pair; t < num_tiles; t += npairs) {
                 int m0, n0;
                 tile_coords(t, m0, n0);
                 for (int kb = 0; kb < num_kb; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) ptx::mbar_expect_tx(&full[stage], 2 * Cfg2::kStageBytes);
-                    ptx::tma_load_2d_2sm(smemA + stage * Cfg2::kABytes, &tmA, &full[stage], kb * BK,
-                                         m0 + rank * BM);
-                    ptx::tma_load_2d_2sm(smemB + stage * Cfg2::kBBytes, &tmB, &full[stage], kb * BK,
-                                         n0 + rank * BM);
+                    ptx::tma_load_2d_2sm_hint(smemA + stage * Cfg2::kABytes, &tmA, &full[stage], kb * BK,
+                                              m0 + rank * BM, keep);
+                    ptx::tma_load_2d_2sm_hint(smemB + stage * Cfg2::kBBytes, &tmB, &full[stage], kb * BK,
+                                              n0 + rank * BM, keep);
                     if (++stage == kStages2) {
                         stage = 0;
                         phase ^= 1;
