@@ -328,6 +328,7 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
         r.ldo = d;
         r.out_xb = xb;
         r.out_ss = ss_b;
+        r.splitk_ok = b.dec != nullptr;
         SGC_CUDA_CHECK(cudaMemsetAsync(ss_b, 0, sizeof(float) * M, c->stream));
         sgc::gemm_bf16(c, ao, m->wo[l], M, d, d, r);
 

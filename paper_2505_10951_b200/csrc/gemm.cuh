@@ -31,6 +31,10 @@ struct GemmEpi {
     // row's sum of squares of x_new into out_ss (zeroed by the caller) for the next GEMM
     __nv_bfloat16* out_xb = nullptr;
     float* out_ss = nullptr;
+    // decode steps only: allow the split-K residual path for few rows (changes the fp32
+    // summation order, so prefill / extend rows never take it: their results stay
+    // independent of how rows are grouped into calls)
+    bool splitk_ok = false;
 };
 
 void gemm_bf16(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep);

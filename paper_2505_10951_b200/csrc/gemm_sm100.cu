@@ -316,7 +316,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
 template <int BN, int EPI, int HD>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                int M, int N, int K, GemmEpi ep) {
+                int M, int N, int K, GemmEpi ep, int ksplit) {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -334,8 +334,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int lane = threadIdx.x % 32;
     const int m_tiles = (M + BM - 1) / BM;
     const int n_tiles = N / BN;
-    const int num_tiles = m_tiles * n_tiles;
-    const int num_kb = K / BK;
+    // split-K (few-row decode GEMMs): work item = (output tile, K slice); slice s accumulates
+    // k-blocks [s * num_kb, (s + 1) * num_kb) and the fp32 epilogue writes plane s of `out`
+    const int num_tiles = m_tiles * n_tiles * ksplit;
+    const int num_kb = K / BK / ksplit;
     // grouped raster: GROUP m-tiles sweep all n-tiles before moving on, so both the
     // activation rows and the weight tiles of the concurrently running CTAs stay in L2
     const int GROUP = max(4, min(64, (48 << 20) / (BM * K * 2)));
@@ -360,6 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     auto tile_coords = [&](int t, int& m0, int& n0) {
+        t /= ksplit;
         int per_group = GROUP * n_tiles;
         int g = t / per_group;
         int first_m = g * GROUP;
@@ -379,7 +382,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
                 int m0, n0;
                 tile_coords(t, m0, n0);
-                for (int kb = 0; kb < num_kb; ++kb) {
+                const int kb0 = (t % ksplit) * num_kb;
+                for (int kb = kb0; kb < kb0 + num_kb; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     ptx::mbar_expect_tx(&full[stage], C::kStageBytes);
                     ptx::tma_load_2d_hint(smemA + stage * C::kABytes, &tmA, &full[stage], kb * BK, m0, keep);
@@ -439,8 +443,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int row = m0 + ew * 32 + lane;
             const bool valid = row < M;
             const uint32_t tbase = tmem_base + ((ew * 32) << 16) + acc * BN;
-
-            epilogue_tile<BN, EPI, HD>(tbase, row, valid, n0, ep, ch_lo, ch_hi, stage, M);
+            GemmEpi eps = ep;
+            if (ksplit > 1)  // fp32 partial plane of this K slice
+                eps.out = static_cast<float*>(ep.out) + static_cast<size_t>(t % ksplit) * M * ep.ldo;
+            epilogue_tile<BN, EPI, HD>(tbase, row, valid, n0, eps, ch_lo, ch_hi, stage, M);
             ptx::tc_fence_before();
             ptx::mbar_arrive(&tempty[acc]);
         }
@@ -614,7 +620,7 @@ constexpr const char* gemm_timer_name(int epi) {
 }
 
 template <int BN, int EPI, int HD>
-void launch(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
+void launch(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep, int ksplit = 1) {
     using Cf = Cfg<BN>;
     static bool attr_set = false;  // per-instantiation (per process; single device type)
     auto kfn = gemm_kernel<BN, EPI, HD>;
@@ -624,10 +630,10 @@ void launch(Ctx* c, const void* A, const void* B, int M, int N, int K, const Gem
     }
     CUtensorMap ta = make_map_2d(A, M, K, BM, BK);
     CUtensorMap tb = make_map_2d(B, N, K, BN, BK);
-    int tiles = ((M + BM - 1) / BM) * (N / BN);
+    int tiles = ((M + BM - 1) / BM) * (N / BN) * ksplit;
     int grid = tiles < c->num_sms ? tiles : c->num_sms;
-    Ctx::Timed timer(c, gemm_timer_name(EPI));
-    kfn<<<grid, kThreads, Cf::kSmem, c->stream>>>(ta, tb, M, N, K, ep);
+    Ctx::Timed timer(c, gemm_timer_name(ksplit > 1 ? EPI_RESID : EPI));
+    kfn<<<grid, kThreads, Cf::kSmem, c->stream>>>(ta, tb, M, N, K, ep, ksplit);
     SGC_LAUNCH_CHECK(c);
 }
 
@@ -650,11 +656,68 @@ void launch2(Ctx* c, const void* A, const void* B, int M, int N, int K, const Ge
 
 bool g_gemm_pairs = true;  // CTA-pair kernel for large tiles (sgc_set_gemm_pairs toggles)
 
+// split-K residual for decode-sized GEMMs: x += sum_s partial[s] in a fixed order, then bf16(x)
+// and the row's sum of squares for the next GEMM's fused RMSNorm (one CTA per row)
+__global__ void __launch_bounds__(256) resid_reduce_kernel(float* x, __nv_bfloat16* xb, float* ss_out,
+                                                           const float* partial, int M, int N, int splits) {
+    const int r = blockIdx.x;
+    float ss = 0.f;
+    const size_t plane = static_cast<size_t>(M) * N;
+    for (int c = threadIdx.x * 4; c < N; c += blockDim.x * 4) {
+        const size_t off = static_cast<size_t>(r) * N + c;
+        float4 v = *reinterpret_cast<const float4*>(x + off);
+        for (int s2 = 0; s2 < splits; ++s2) {
+            const float4 p = *reinterpret_cast<const float4*>(partial + s2 * plane + off);
+            v.x += p.x;
+            v.y += p.y;
+            v.z += p.z;
+            v.w += p.w;
+        }
+        *reinterpret_cast<float4*>(x + off) = v;
+        if (xb) {
+            __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+            uint2 pk;
+            pk.x = *reinterpret_cast<uint32_t*>(&a);
+            pk.y = *reinterpret_cast<uint32_t*>(&b);
+            *reinterpret_cast<uint2*>(xb + off) = pk;
+            ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+        }
+    }
+    if (!ss_out) return;
+    __shared__ float red[8];
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < 8; ++w) t += red[w];
+        ss_out[r] = t;
+    }
+}
+
 template <int EPI, int HD>
 void dispatch_bn(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
     // widest tile that divides N (and d, for the QKV section split)
     int lim = EPI == EPI_QKV ? ep.d : N;
     const int m_tiles = (M + BM - 1) / BM;
+    if constexpr (EPI == EPI_RESID) {
+        // decode-sized residual GEMMs (N = d): too few output tiles to stream the weight matrix at
+        // full bandwidth -> 4-way split-K into fp32 planes + a fixed-order reduction
+        constexpr int kSplit = 4;
+        if (ep.splitk_ok && M <= 2 * BM && m_tiles * (N / 64) < c->num_sms && N % 64 == 0 && (K / BK) % kSplit == 0) {
+            float* partial = c->buf<float>("gemm_splitk", static_cast<size_t>(kSplit) * M * N);
+            GemmEpi pe;
+            pe.mode = EPI_F32;
+            pe.out = partial;
+            pe.ldo = N;
+            launch<64, EPI_F32, 0>(c, A, B, M, N, K, pe, kSplit);
+            Ctx::Timed timer(c, "gemm_resid");
+            resid_reduce_kernel<<<M, 256, 0, c->stream>>>(static_cast<float*>(ep.out), ep.out_xb, ep.out_ss, partial, M,
+                                                          N, kSplit);
+            SGC_LAUNCH_CHECK(c);
+            return;
+        }
+    }
     // few rows (decode steps): the GEMM is weight-bandwidth bound, so spread the weight matrix
     // over as many CTAs as possible -- the narrowest tile that still yields >= one wave
     // (the QKV epilogue needs whole heads inside a tile: BN >= head_dim)
