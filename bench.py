@@ -31,6 +31,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "per-query TTFT (p50) and queries/s vs CPU ref; fraction of tensor/HBM roofline"
+COLL_DEV = "cuda"  # device of the tensors handed to torch.distributed collectives
 # every kernel launch of the library is bracketed by CUDA events under one of these names
 KERNEL_GROUPS = ["gemm", "gemm_qkv", "gemm_resid", "gemm_tanh", "attention", "attn_decode", "rmsnorm", "embed", "head", "first_token", "gnn_encode",
                  "text_features", "pairwise", "agglomerate", "union_prompt", "prompt_gather"]
@@ -136,10 +137,10 @@ def run_ours(args, rank, world, local_rank):
 
     from paper_2505_10951_b200 import host
 
-    torch.cuda.set_device(local_rank)
+    torch.cuda.set_device(local_rank % torch.cuda.device_count())
     w = build_workload(args)
     m = len(w.queries)
-    ctx = host.Context(local_rank)
+    ctx = host.Context(torch.cuda.current_device())
     stream = torch.cuda.current_stream()
     ctx.set_stream(stream.cuda_stream)
     ctx.set_option("gemm_pairs", 0 if args.no_pairs else 1)
@@ -165,12 +166,12 @@ def run_ours(args, rank, world, local_rank):
         emb = None
         if world > 1:
             shard = host.encode_subgraphs(ctx, dg, w.retrieved[lo:hi], pb.gnn)
-            emb = D.gather_rows(torch.from_numpy(shard).cuda(), m, world, pg).cpu().numpy()
+            emb = D.gather_rows(torch.from_numpy(shard).to(COLL_DEV), m, world, pg).cpu().numpy()
         res = host.run_subgcache(ctx, lm, dg, pb, embeddings=emb, rank=rank, world_size=world,
                                  want_logits=False, device_inputs=True, waves=args.waves)
         if world > 1:
             res.first_token = D.combine_first_tokens(
-                torch.from_numpy(res.first_token.astype(np.int64)).cuda(), pg)
+                torch.from_numpy(res.first_token.astype(np.int64)).to(COLL_DEV), pg)
         return res
 
     for _ in range(args.warmup):
@@ -183,7 +184,7 @@ def run_ours(args, rank, world, local_rank):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     stage = np.zeros(6)
     ttfts = []
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         if world > 1:
             pg.barrier()
         torch.cuda.synchronize()
@@ -204,7 +205,7 @@ def run_ours(args, rank, world, local_rank):
     attn_ms, attn_n = kt["attention"]
     ctx.set_timing(False)
     if world > 1:
-        t = torch.tensor([total_ms], device="cuda")
+        t = torch.tensor([total_ms], device=COLL_DEV)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
@@ -268,7 +269,7 @@ def run_ours(args, rank, world, local_rank):
 
     if world > 1:
         # every query is served by one rank: its TTFT is that rank's value (others report -1)
-        tt = torch.from_numpy(np.stack(ttfts)).cuda()
+        tt = torch.from_numpy(np.stack(ttfts)).to(COLL_DEV)
         pg.all_reduce(tt, op=pg.ReduceOp.MAX)
         ttfts = list(tt.cpu().numpy())
     allt = np.concatenate(ttfts)
@@ -473,8 +474,17 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        global COLL_DEV
+        # NCCL over NVLink on a real multi-GPU box; SGC_DIST_BACKEND=gloo runs every rank's data
+        # path through the same code with host-side collectives (e.g. N ranks sharing one GPU)
+        backend = os.environ.get("SGC_DIST_BACKEND", "nccl")
+        dev = local_rank % torch.cuda.device_count()
+        torch.cuda.set_device(dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            COLL_DEV = "cpu"
+            dist.init_process_group(backend)
     out = run_ours(args, rank, world, local_rank)
     if rank == 0 and out is not None:
         print(json.dumps(out))
