@@ -112,6 +112,31 @@ int sgc_graph_upload(sgc_ctx* ctx, uint32_t n_nodes, const uint32_t* node_ids,
                      const uint64_t* edge_off, sgc_graph** out);
 int sgc_graph_destroy(sgc_graph* g);
 
+/* ---- (0) retrieval: retrieve() (retrieval.hpp, retrieval.cpp:96-239) ------------------
+ * The step before the hot path: each question is embedded with the
+ * TextEncoder (dim, seed, salt), nodes (and for node-edge-topk edges) are scored by cosine
+ * similarity on the GPU in the reference's exact fp64 order, and the selection -- top-k with
+ * ties toward the smaller index, edge rule, BFS path connection (node-edge-topk) or ego nets
+ * with pooled-feature re-ranking (ego-topk, pooling and scoring on the GPU) -- follows the
+ * reference step for step, so retrieved node/edge sets are bit-identical.
+ * Questions: text q_text[q_off[i] .. q_off[i+1]). Outputs (host or device) CSR:
+ *   node_off [m+1], nodes (ascending ids), edge_off [m+1], edges (ascending indices); SGC_CAPACITY
+ *   if a capacity is too small. DomainError for k < 1, ego_hops < 1, edge_cost < 0, empty graph. */
+enum { SGC_RETRIEVE_NODE_EDGE_TOPK = 0, SGC_RETRIEVE_EGO_TOPK = 1 };
+typedef struct {
+    int strategy;             /* SGC_RETRIEVE_* (RetrievalConfig::strategy) */
+    uint32_t k;               /* RetrievalConfig::k (3) */
+    double edge_cost;         /* RetrievalConfig::edge_cost (0.5) */
+    uint32_t ego_hops;        /* RetrievalConfig::ego_hops (2) */
+    uint32_t ego_entity_cap;  /* RetrievalConfig::ego_entity_cap (10) */
+    uint32_t dim;             /* TextEncoderConfig::dim */
+    uint64_t text_seed;       /* TextEncoderConfig::seed (1) */
+    uint64_t hash_salt;       /* TextEncoderConfig::hash_salt (55) */
+} sgc_retrieval_config;
+int sgc_retrieve(sgc_ctx* ctx, sgc_graph* g, const sgc_retrieval_config* cfg, uint32_t m,
+                 const char* q_text, const uint64_t* q_off, uint64_t* node_off, uint32_t* nodes,
+                 uint64_t node_cap, uint64_t* edge_off, uint32_t* edges, uint64_t edge_cap);
+
 /* ---- (1) subgraph embedding: GnnEncoder::encode (encoders.hpp:61, encoders.cpp:122-186) --
  * Batched over subgraphs; out [count * dim] fp32. DomainError on an empty subgraph. */
 int sgc_encode_subgraphs(sgc_ctx* ctx, sgc_graph* g, const sgc_gnn_config* cfg,

@@ -386,6 +386,30 @@ json cmd_pipeline(const json& spec) {
 }
 
 // Bounded timing samples of each stage at a model shape (bench.py --impl reference).
+// retrieve() (retrieval.cpp:226-239) for a list of questions on a CSV graph
+json cmd_retrieve(const json& spec) {
+    TextualGraph g = graph_of(spec);
+    TextEncoderConfig tc;
+    tc.dim = spec.at("dim");
+    TextEncoder enc(tc);
+    RetrievalConfig rc;
+    rc.strategy = retrieval_strategy_from_string(spec.value("strategy", std::string("ego-topk")));
+    rc.k = spec.value("k", rc.k);
+    rc.edge_cost = spec.value("edge_cost", rc.edge_cost);
+    rc.ego_hops = spec.value("ego_hops", rc.ego_hops);
+    rc.ego_entity_cap = spec.value("ego_entity_cap", rc.ego_entity_cap);
+    json out = json::array();
+    uint64_t qid = 0;
+    for (const json& q : spec.at("questions")) {
+        QueryRecord rec;
+        rec.id = qid++;
+        rec.question = q.get<std::string>();
+        Subgraph s = retrieve(rc, g, rec, enc);
+        out.push_back(subgraph_json(s));
+    }
+    return out;
+}
+
 // the reference's whole run() (pipeline.cpp:114-320) -> its subgcache-report-v1 document
 json cmd_run(const json& spec) {
     RunConfig rc;
@@ -500,6 +524,7 @@ int main(int argc, char** argv) {
         else if (cmd == "pipeline") out = cmd_pipeline(spec);
         else if (cmd == "bench") out = cmd_bench(spec);
         else if (cmd == "run") out = cmd_run(spec);
+        else if (cmd == "retrieve") out = cmd_retrieve(spec);
         else if (cmd == "synth") {  // the reference's own synthetic dataset writer
             auto ds = testsupport::write_synth_dataset(spec.at("dir"), spec.at("m").get<size_t>());
             out = json{{"nodes", ds.nodes_path}, {"edges", ds.edges_path}, {"queries", ds.queries_path}};

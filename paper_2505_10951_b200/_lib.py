@@ -69,6 +69,12 @@ class TokenLists(C.Structure):
                 ("tokens", C.POINTER(C.c_int32))]
 
 
+class RetrievalConfig(C.Structure):
+    _fields_ = [("strategy", C.c_int), ("k", C.c_uint32), ("edge_cost", C.c_double),
+                ("ego_hops", C.c_uint32), ("ego_entity_cap", C.c_uint32), ("dim", C.c_uint32),
+                ("text_seed", C.c_uint64), ("hash_salt", C.c_uint64)]
+
+
 class Batch(C.Structure):
     _fields_ = [("retrieved", Subgraphs), ("questions", TokenLists), ("answers", TokenLists),
                 ("own_prefix", TokenLists), ("clusters", C.c_uint32), ("linkage", C.c_int),
@@ -101,7 +107,7 @@ EXPORTS = [
     "sgc_pairwise_distances", "sgc_agglomerate", "sgc_build_representatives", "sgc_prefill",
     "sgc_kv_release", "sgc_kv_count", "sgc_kv_tokens", "sgc_kv_digest", "sgc_kv_resident_bytes",
     "sgc_kv_read", "sgc_extend", "sgc_run_subgcache", "sgc_gemm_bf16", "sgc_set_timing",
-    "sgc_get_timing", "sgc_lpt_assign", "sgc_set_option", "sgc_attention_bf16", "sgc_extend_generate",
+    "sgc_get_timing", "sgc_lpt_assign", "sgc_set_option", "sgc_attention_bf16", "sgc_extend_generate", "sgc_retrieve",
 ]
 
 _lib = None
@@ -159,6 +165,9 @@ def load() -> C.CDLL:
     L.sgc_run_subgcache.argtypes = [vp, vp, vp, P(Batch), P(BatchOut)]
     L.sgc_gemm_bf16.argtypes = [vp, vp, vp, vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_int]
     L.sgc_set_timing.argtypes = [vp, C.c_int]
+    L.sgc_retrieve.argtypes = [vp, vp, P(RetrievalConfig), C.c_uint32, C.c_char_p, P(C.c_uint64),
+                               P(C.c_uint64), P(C.c_uint32), C.c_uint64, P(C.c_uint64), P(C.c_uint32),
+                               C.c_uint64]
     L.sgc_extend_generate.argtypes = [vp, vp, vp, P(C.c_uint32), P(TokenLists), P(TokenLists), C.c_float,
                                       C.c_uint32, P(C.c_float), P(C.c_int32), P(C.c_int32), P(C.c_uint32)]
     L.sgc_attention_bf16.argtypes = [vp, vp, vp, vp, C.c_uint32, vp, vp, vp, P(C.c_int32), C.c_uint32,

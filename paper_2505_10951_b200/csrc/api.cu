@@ -7,6 +7,8 @@
 //   cache_engine.cpp:140-233 process_cluster / run_batch -> sgc_prefill + sgc_extend
 //   lm_core.cpp:179-297 ToyLm::forward (token-sequential)  -> forward_rows (row-batched)
 #include <algorithm>
+#include <deque>
+#include <set>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -1493,6 +1495,211 @@ int sgc_text_features(sgc_ctx* ctx, sgc_graph* g, uint32_t dim, uint64_t seed, u
         if (dim == 0) fail(SGC_DOMAIN, "text encoder dim must be >= 1");
         float* f = compute_text_features(c, g, dim, seed, salt, nullptr);
         sgc::copy_out(c, out, f, static_cast<size_t>(g->n_nodes + g->n_edges) * dim);
+        c->sync();
+    });
+}
+
+int sgc_retrieve(sgc_ctx* ctx, sgc_graph* g, const sgc_retrieval_config* cfg, uint32_t m,
+                 const char* q_text, const uint64_t* q_off, uint64_t* node_off, uint32_t* nodes,
+                 uint64_t node_cap, uint64_t* edge_off, uint32_t* edges, uint64_t edge_cap) {
+    return guarded([&] {
+        Ctx* c = &ctx->c;
+        // RetrievalConfig::validate (retrieval.cpp:21-25), retrieve() (:226-239)
+        if (cfg->k < 1) fail(SGC_DOMAIN, "retrieval k must be >= 1");
+        if (cfg->ego_hops < 1) fail(SGC_DOMAIN, "ego hops must be >= 1");
+        if (cfg->edge_cost < 0) fail(SGC_DOMAIN, "edge cost must be >= 0");
+        if (cfg->dim == 0) fail(SGC_DOMAIN, "text encoder dim must be >= 1");
+        if (g->n_nodes == 0) fail(SGC_DOMAIN, "retrieve: graph has no nodes");
+        const int N = static_cast<int>(g->n_nodes), E = static_cast<int>(g->n_edges);
+        const int d = static_cast<int>(cfg->dim);
+        const bool ego = cfg->strategy == SGC_RETRIEVE_EGO_TOPK;
+        // element features (nodes then edges) and question features: TextEncoder::embed
+        const float* feat = compute_text_features(c, g, cfg->dim, cfg->text_seed, cfg->hash_salt, nullptr);
+        std::vector<uint64_t> qo = to_host(c, q_off, m + 1);
+        std::vector<char> qt = to_host(c, q_text, qo[m]);
+        std::vector<uint32_t> qb;
+        std::vector<int8_t> qs;
+        std::vector<uint64_t> qtok(1, 0);
+        for (uint32_t i = 0; i < m; ++i) {
+            hash_tokens(qt.data() + qo[i], qo[i + 1] - qo[i], cfg->hash_salt, qb, qs);
+            qtok.push_back(qb.size());
+        }
+        uint32_t* d_qb = c->buf<uint32_t>("ret_qb", std::max<size_t>(1, qb.size()));
+        int8_t* d_qs = c->buf<int8_t>("ret_qs", std::max<size_t>(1, qs.size()));
+        uint64_t* d_qtok = c->buf<uint64_t>("ret_qtok", m + 1);
+        sgc::copy_in(c, d_qb, qb.data(), qb.size());
+        sgc::copy_in(c, d_qs, qs.data(), qs.size());
+        sgc::copy_in(c, d_qtok, qtok.data(), m + 1);
+        float* qf = c->buf<float>("ret_qf", static_cast<size_t>(std::max<uint32_t>(1, m)) * d);
+        sgc::text_features(c, qf, d_qb, d_qs, d_qtok, static_cast<int>(m), g_enc[c].proj_t, d);
+        // cosine scores of every (question, element): exact fp64 sums on the device
+        const int ne = ego ? N : N + E;
+        double* d_dot = c->buf<double>("ret_dot", static_cast<size_t>(std::max<uint32_t>(1, m)) * ne);
+        double* d_qsq = c->buf<double>("ret_qsq", std::max<uint32_t>(1, m));
+        double* d_esq = c->buf<double>("ret_esq", ne);
+        sgc::retrieval_dots(c, d_dot, d_qsq, d_esq, qf, static_cast<int>(m), feat, ne, d);
+        std::vector<double> dot = to_host(c, d_dot, static_cast<size_t>(m) * ne);
+        std::vector<double> qsq = to_host(c, d_qsq, m), esq = to_host(c, d_esq, ne);
+        auto cosine = [](double dt, double na, double nb) {  // encoders.cpp:35-37
+            if (na == 0 || nb == 0) return 0.0;
+            return dt / (std::sqrt(na) * std::sqrt(nb));
+        };
+        // undirected adjacency, neighbours sorted by (node id, edge index) (retrieval.cpp:30-49)
+        std::vector<std::vector<std::pair<uint32_t, uint32_t>>> nb(N);  // (node index, edge)
+        for (int e = 0; e < E; ++e) {
+            nb[g->edge_src_idx[e]].push_back({g->edge_dst_idx[e], static_cast<uint32_t>(e)});
+            nb[g->edge_dst_idx[e]].push_back({g->edge_src_idx[e], static_cast<uint32_t>(e)});
+        }
+        for (auto& v : nb) std::sort(v.begin(), v.end());  // node index order == id order
+        auto top_k = [](const double* sc, int n, uint32_t k) {  // retrieval.cpp:85-93
+            std::vector<uint32_t> o(n);
+            std::iota(o.begin(), o.end(), 0u);
+            std::stable_sort(o.begin(), o.end(), [&](uint32_t a, uint32_t b) { return sc[a] > sc[b]; });
+            if (o.size() > k) o.resize(k);
+            return o;
+        };
+        std::vector<std::set<uint32_t>> out_nodes(m), out_edges(m);  // node indices / edge indices
+        if (!ego) {
+            // node-edge-topk (retrieval.cpp:96-148)
+            for (uint32_t q = 0; q < m; ++q) {
+                std::vector<double> sc(ne);
+                for (int j = 0; j < ne; ++j) sc[j] = cosine(dot[static_cast<size_t>(q) * ne + j], qsq[q], esq[j]);
+                std::set<uint32_t>& sn = out_nodes[q];
+                std::set<uint32_t>& se = out_edges[q];
+                for (uint32_t i : top_k(sc.data(), N, cfg->k)) sn.insert(i);
+                const std::set<uint32_t> seeds = sn;
+                for (uint32_t ei : top_k(sc.data() + N, E, cfg->k)) {
+                    const uint32_t a = g->edge_src_idx[ei], b2 = g->edge_dst_idx[ei];
+                    const bool covered = seeds.count(a) && seeds.count(b2);
+                    if (sc[N + ei] >= cfg->edge_cost || covered) {
+                        se.insert(ei);
+                        sn.insert(a);
+                        sn.insert(b2);
+                    }
+                }
+                for (auto it = seeds.begin(); it != seeds.end(); ++it)
+                    for (auto jt = std::next(it); jt != seeds.end(); ++jt) {
+                        // BFS shortest path, first-discovery parents (retrieval.cpp:54-82)
+                        const uint32_t s0 = *it, t0 = *jt;
+                        std::vector<int64_t> pe(N, -1), pn(N, -1);
+                        std::vector<uint8_t> seen(N, 0);
+                        std::deque<uint32_t> dq{s0};
+                        seen[s0] = 1;
+                        while (!dq.empty()) {
+                            const uint32_t u = dq.front();
+                            dq.pop_front();
+                            if (u == t0) break;
+                            for (const auto& [v, ei] : nb[u]) {
+                                if (seen[v]) continue;
+                                seen[v] = 1;
+                                pe[v] = ei;
+                                pn[v] = u;
+                                dq.push_back(v);
+                            }
+                        }
+                        if (!seen[t0]) continue;
+                        std::vector<uint32_t> path;
+                        for (uint32_t cur = t0; cur != s0; cur = static_cast<uint32_t>(pn[cur]))
+                            path.push_back(static_cast<uint32_t>(pe[cur]));
+                        if (path.empty()) continue;
+                        const double gain = std::max(0.0, sc[s0]) + std::max(0.0, sc[t0]);
+                        if (static_cast<double>(path.size()) * cfg->edge_cost > gain) continue;
+                        for (uint32_t ei : path) {
+                            se.insert(ei);
+                            sn.insert(g->edge_src_idx[ei]);
+                            sn.insert(g->edge_dst_idx[ei]);
+                        }
+                    }
+            }
+        } else {
+            // ego-topk (retrieval.cpp:151-223): ego nets of the top centres on the host, their
+            // pooled features and re-ranking scores on the device
+            struct Ego {
+                uint32_t q, center;
+                std::set<uint32_t> nodes, edges;
+            };
+            std::vector<Ego> egos;
+            std::vector<uint32_t> mem_off(1, 0), mem_idx;
+            std::vector<int32_t> ego_q;
+            for (uint32_t q = 0; q < m; ++q) {
+                std::vector<double> sc(N);
+                for (int j = 0; j < N; ++j) sc[j] = cosine(dot[static_cast<size_t>(q) * N + j], qsq[q], esq[j]);
+                for (uint32_t ci : top_k(sc.data(), N, cfg->ego_entity_cap)) {
+                    Ego eg{q, ci, {ci}, {}};
+                    std::set<uint32_t> visited{ci};
+                    std::deque<std::pair<uint32_t, uint32_t>> dq{{ci, 0u}};
+                    while (!dq.empty()) {
+                        auto [u, depth] = dq.front();
+                        dq.pop_front();
+                        if (depth == cfg->ego_hops) continue;
+                        for (const auto& [v, ei] : nb[u]) {
+                            (void)ei;
+                            if (visited.insert(v).second) {
+                                eg.nodes.insert(v);
+                                dq.push_back({v, depth + 1});
+                            }
+                        }
+                    }
+                    for (uint32_t u : eg.nodes)  // induced edges
+                        for (const auto& [v, ei] : nb[u])
+                            if (eg.nodes.count(v)) eg.edges.insert(ei);
+                    for (uint32_t u : eg.nodes) mem_idx.push_back(u);
+                    for (uint32_t ei : eg.edges) mem_idx.push_back(static_cast<uint32_t>(N) + ei);
+                    mem_off.push_back(static_cast<uint32_t>(mem_idx.size()));
+                    ego_q.push_back(static_cast<int32_t>(q));
+                    egos.push_back(std::move(eg));
+                }
+            }
+            const int n_ego = static_cast<int>(egos.size());
+            std::vector<double> pdot(n_ego), psq(n_ego);
+            if (n_ego) {
+                uint32_t* d_moff = c->buf<uint32_t>("ret_moff", mem_off.size());
+                uint32_t* d_midx = c->buf<uint32_t>("ret_midx", std::max<size_t>(1, mem_idx.size()));
+                int32_t* d_eq = c->buf<int32_t>("ret_eq", n_ego);
+                float* d_pool = c->buf<float>("ret_pool", static_cast<size_t>(n_ego) * d);
+                double* d_pd = c->buf<double>("ret_pd", n_ego);
+                double* d_ps = c->buf<double>("ret_ps", n_ego);
+                sgc::copy_in(c, d_moff, mem_off.data(), mem_off.size());
+                sgc::copy_in(c, d_midx, mem_idx.data(), mem_idx.size());
+                sgc::copy_in(c, d_eq, ego_q.data(), n_ego);
+                sgc::ego_pool_dots(c, d_pool, d_pd, d_ps, feat, d_moff, d_midx, qf, d_eq, n_ego, d);
+                pdot = to_host(c, d_pd, n_ego);
+                psq = to_host(c, d_ps, n_ego);
+            }
+            size_t e0 = 0;
+            for (uint32_t q = 0; q < m; ++q) {
+                size_t e1 = e0;
+                while (e1 < egos.size() && egos[e1].q == q) ++e1;
+                std::vector<std::pair<double, uint32_t>> ranked;  // (score, ego)
+                for (size_t e = e0; e < e1; ++e) ranked.push_back({cosine(pdot[e], qsq[q], psq[e]), static_cast<uint32_t>(e)});
+                std::stable_sort(ranked.begin(), ranked.end(), [&](const auto& a, const auto& b2) {
+                    if (a.first != b2.first) return a.first > b2.first;
+                    return egos[a.second].center < egos[b2.second].center;
+                });
+                if (ranked.size() > cfg->k) ranked.resize(cfg->k);
+                for (const auto& r : ranked) {  // merge_subgraphs: set union
+                    out_nodes[q].insert(egos[r.second].nodes.begin(), egos[r.second].nodes.end());
+                    out_edges[q].insert(egos[r.second].edges.begin(), egos[r.second].edges.end());
+                }
+                e0 = e1;
+            }
+        }
+        // CSR out (node ids ascending == node indices ascending)
+        std::vector<uint64_t> no(1, 0), eo(1, 0);
+        std::vector<uint32_t> nv, ev;
+        for (uint32_t q = 0; q < m; ++q) {
+            for (uint32_t i : out_nodes[q]) nv.push_back(g->ids[i]);
+            for (uint32_t ei : out_edges[q]) ev.push_back(ei);
+            no.push_back(nv.size());
+            eo.push_back(ev.size());
+        }
+        if (nv.size() > node_cap || ev.size() > edge_cap)
+            fail(SGC_CAPACITY, "retrieve: output capacity too small (" + std::to_string(nv.size()) + " nodes, " +
+                                   std::to_string(ev.size()) + " edges needed)");
+        sgc::copy_in(c, node_off, no.data(), no.size());
+        sgc::copy_in(c, edge_off, eo.data(), eo.size());
+        sgc::copy_in(c, nodes, nv.data(), nv.size());
+        sgc::copy_in(c, edges, ev.data(), ev.size());
         c->sync();
     });
 }

@@ -315,4 +315,93 @@ void prompt_gather(Ctx* c, const GatherArgs& a) {
     SGC_LAUNCH_CHECK(c);
 }
 
+// ---- retrieval scoring ----------------------------------------------------------------------
+namespace {
+constexpr int RT = 16;   // pairs per CTA side
+constexpr int RK = 64;   // feature chunk staged in shared memory
+
+// one thread per (i, j) pair of a 16 x 16 tile; the feature axis is walked in order (chunks of
+// 64 staged in smem), so each sum is the reference's sequential double accumulation
+__global__ void __launch_bounds__(256) retrieval_dot_kernel(double* dot, const float* A, int na, const float* B,
+                                                            int nb, int d) {
+    __shared__ float As[RT][RK + 1], Bs[RT][RK + 1];
+    const int i0 = blockIdx.y * RT, j0 = blockIdx.x * RT;
+    const int ti = threadIdx.x / RT, tj = threadIdx.x % RT;
+    double acc = 0.0;
+    for (int k0 = 0; k0 < d; k0 += RK) {
+        const int kc = min(RK, d - k0);
+        for (int t = threadIdx.x; t < RT * RK; t += blockDim.x) {
+            const int r = t / RK, k = t % RK;
+            As[r][k] = (i0 + r < na && k < kc) ? A[static_cast<size_t>(i0 + r) * d + k0 + k] : 0.f;
+            Bs[r][k] = (j0 + r < nb && k < kc) ? B[static_cast<size_t>(j0 + r) * d + k0 + k] : 0.f;
+        }
+        __syncthreads();
+        for (int k = 0; k < kc; ++k)
+            acc = __dadd_rn(acc, __dmul_rn(static_cast<double>(As[ti][k]), static_cast<double>(Bs[tj][k])));
+        __syncthreads();
+    }
+    if (i0 + ti < na && j0 + tj < nb) dot[static_cast<size_t>(i0 + ti) * nb + j0 + tj] = acc;
+}
+
+__global__ void sq_norm_kernel(double* out, const float* A, int n, int d) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double s = 0.0;
+    const float* a = A + static_cast<size_t>(i) * d;
+    for (int k = 0; k < d; ++k) s = __dadd_rn(s, __dmul_rn(static_cast<double>(a[k]), static_cast<double>(a[k])));
+    out[i] = s;
+}
+
+// retrieval.cpp:175-189: pooled = mean of the ego net's node then edge attribute embeddings
+// (double accumulation in member order, one division, cast to float)
+__global__ void ego_pool_kernel(float* pooled, const float* feat, const uint32_t* mem_off,
+                                const uint32_t* mem_idx, int d) {
+    const int e = blockIdx.x;
+    const uint32_t m0 = mem_off[e], m1 = mem_off[e + 1];
+    for (int k = threadIdx.x; k < d; k += blockDim.x) {
+        double s = 0.0;
+        for (uint32_t t = m0; t < m1; ++t) s = __dadd_rn(s, static_cast<double>(feat[static_cast<size_t>(mem_idx[t]) * d + k]));
+        pooled[static_cast<size_t>(e) * d + k] = static_cast<float>(__ddiv_rn(s, static_cast<double>(m1 - m0)));
+    }
+}
+
+__global__ void pair_dot_kernel(double* dot, double* sq, const float* q, const int32_t* qi, const float* p,
+                                int n, int d) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    const float* a = q + static_cast<size_t>(qi[e]) * d;
+    const float* b = p + static_cast<size_t>(e) * d;
+    double s = 0.0, nb2 = 0.0;
+    for (int k = 0; k < d; ++k) {
+        s = __dadd_rn(s, __dmul_rn(static_cast<double>(a[k]), static_cast<double>(b[k])));
+        nb2 = __dadd_rn(nb2, __dmul_rn(static_cast<double>(b[k]), static_cast<double>(b[k])));
+    }
+    dot[e] = s;
+    sq[e] = nb2;
+}
+}  // namespace
+
+void retrieval_dots(Ctx* c, double* dot, double* sq_a, double* sq_b, const float* A, int na, const float* B,
+                    int nb, int d) {
+    if (na <= 0 || nb <= 0) return;
+    Ctx::Timed timer(c, "retrieval");
+    retrieval_dot_kernel<<<dim3(ceil_div(nb, RT), ceil_div(na, RT)), 256, 0, c->stream>>>(dot, A, na, B, nb, d);
+    SGC_LAUNCH_CHECK(c);
+    sq_norm_kernel<<<ceil_div(na, 128), 128, 0, c->stream>>>(sq_a, A, na, d);
+    SGC_LAUNCH_CHECK(c);
+    sq_norm_kernel<<<ceil_div(nb, 128), 128, 0, c->stream>>>(sq_b, B, nb, d);
+    SGC_LAUNCH_CHECK(c);
+}
+
+void ego_pool_dots(Ctx* c, float* pooled, double* pair_dot, double* pair_sq, const float* feat,
+                   const uint32_t* mem_off, const uint32_t* mem_idx, const float* q, const int32_t* qi,
+                   int n_ego, int d) {
+    if (n_ego <= 0) return;
+    Ctx::Timed timer(c, "retrieval");
+    ego_pool_kernel<<<n_ego, 128, 0, c->stream>>>(pooled, feat, mem_off, mem_idx, d);
+    SGC_LAUNCH_CHECK(c);
+    pair_dot_kernel<<<ceil_div(n_ego, 128), 128, 0, c->stream>>>(pair_dot, pair_sq, q, qi, pooled, n_ego, d);
+    SGC_LAUNCH_CHECK(c);
+}
+
 }  // namespace sgc

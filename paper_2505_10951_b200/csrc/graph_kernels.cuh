@@ -10,6 +10,18 @@ void text_features(Ctx* c, float* out, const uint32_t* bucket, const int8_t* sig
 void node_index(Ctx* c, int32_t* out, const uint32_t* ids, uint64_t n, const uint32_t* sorted_ids,
                 int n_nodes);
 
+// retrieval (retrieval.cpp): cosine_similarity's three sums (encoders.cpp:28-38) in the
+// reference's order -- sequential over the feature index, products rounded before the add --
+// so the scores and every top-k decision taken on them are bit-identical.
+// dot[i * nb + j] = sum_k a_i[k] * b_j[k]; sq_a[i] = sum_k a_i[k]^2 (sq_b likewise)
+void retrieval_dots(Ctx* c, double* dot, double* sq_a, double* sq_b, const float* A, int na, const float* B,
+                    int nb, int d);
+// ego nets: pooled[e] = float(mean over members (nodes then edges, given order) of feat rows);
+// then pair_dot[e] = sum_k q[qi[e]][k] * pooled[e][k] and pair_sq[e] = sum_k pooled[e][k]^2
+void ego_pool_dots(Ctx* c, float* pooled, double* pair_dot, double* pair_sq, const float* feat,
+                   const uint32_t* mem_off, const uint32_t* mem_idx, const float* q, const int32_t* qi,
+                   int n_ego, int d);
+
 struct UnionArgs {
     int clusters;
     const int32_t* sub_nodes;  // dense node indices

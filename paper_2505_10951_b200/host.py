@@ -323,6 +323,33 @@ class GnnEncoderConfig:
                               self.text_salt)
 
 
+STRATEGIES = {"node-edge-topk": 0, "g-retriever": 0, "ego-topk": 1, "grag": 1}
+
+
+def retrieve(ctx: Context, g: DeviceGraph, questions, strategy: str = "node-edge-topk", k: int = 3,
+             edge_cost: float = 0.5, ego_hops: int = 2, ego_entity_cap: int = 10, dim: int = 64,
+             text_seed: int = 1, hash_salt: int = 55):
+    """retrieve() (retrieval.cpp:226-239) for every question: list of Subgraph."""
+    if strategy not in STRATEGIES:
+        raise DomainError(f"unknown retrieval strategy: {strategy}")
+    cfg = _lib.RetrievalConfig(STRATEGIES[strategy], k, edge_cost, ego_hops, ego_entity_cap, dim,
+                               text_seed, hash_salt)
+    qs = [q if isinstance(q, bytes) else q.encode() for q in questions]
+    m = len(qs)
+    text = b"".join(qs)
+    off = np.zeros(m + 1, np.uint64)
+    off[1:] = np.cumsum([len(q) for q in qs])
+    cap_n = max(1, m * g.n_nodes)
+    cap_e = max(1, m * max(1, g.n_edges))
+    noff = np.zeros(m + 1, np.uint64)
+    eoff = np.zeros(m + 1, np.uint64)
+    nodes = np.zeros(cap_n, np.uint32)
+    edges = np.zeros(cap_e, np.uint32)
+    check(ctx.lib.sgc_retrieve(ctx.h, g.h, C.byref(cfg), m, text, _p(off, C.c_uint64), _p(noff, C.c_uint64),
+                               _p(nodes, C.c_uint32), cap_n, _p(eoff, C.c_uint64), _p(edges, C.c_uint32), cap_e))
+    return [Subgraph.of(nodes[noff[i]:noff[i + 1]], edges[eoff[i]:eoff[i + 1]]) for i in range(m)]
+
+
 def text_features(ctx: Context, g: DeviceGraph, dim: int, seed: int = 1, salt: int = 55):
     out = np.zeros((g.n_nodes + g.n_edges, dim), np.float32)
     check(ctx.lib.sgc_text_features(ctx.h, g.h, dim, seed, salt, _p(out, C.c_float)))

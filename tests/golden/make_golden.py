@@ -77,6 +77,42 @@ def c1_report(td):
     dump("c1_report.json", out)
 
 
+def retrieval_cases(td):
+    """retrieve() (retrieval.cpp:96-239) of the reference for both strategies on three graphs:
+    the C1 two-star dataset, a seeded community graph (C2-C5 generator, small) and the bundled
+    scene graph with its own queries."""
+    res = {}
+    graphs = []
+    w1 = W.c1_workload(64, 4)
+    graphs.append(("c1", w1.graph, [q.question.decode() for q in w1.queries], 64))
+    wc = W.community_workload("retrieval-comm", dict(W.TINY_LM), 48, 4, 60, 130, 8, 20, 4, seed=777)
+    graphs.append(("comm", wc.graph, [q.question.decode() for q in wc.queries], 128))
+    res["graphs"] = {}
+    for name, g, qs, dim in graphs:
+        d = os.path.join(td, "ret_" + name)
+        os.makedirs(d, exist_ok=True)
+        g.write_csv(os.path.join(d, "nodes.csv"), os.path.join(d, "edges.csv"))
+        res["graphs"][name] = {"graph": graph_json(g), "questions": qs, "dim": dim}
+        for strategy in ("ego-topk", "node-edge-topk"):
+            for cfg in ({}, {"k": 5, "edge_cost": 0.2, "ego_hops": 1, "ego_entity_cap": 6}):
+                spec = {"cmd": "retrieve", "nodes_csv": os.path.join(d, "nodes.csv"),
+                        "edges_csv": os.path.join(d, "edges.csv"), "questions": qs, "dim": dim,
+                        "strategy": strategy}
+                spec.update(cfg)
+                key = f"{name}|{strategy}|{json.dumps(cfg, sort_keys=True)}"
+                res[key] = {"cfg": dict(cfg, strategy=strategy), "out": oracle.run_ref(spec)}
+    # the bundled scene graph (read by the reference's own loader)
+    with open(os.path.join(REF_DATA, "queries.jsonl")) as f:
+        sq = [json.loads(x)["question"] for x in f if x.strip()]
+    for strategy in ("ego-topk", "node-edge-topk"):
+        spec = {"cmd": "retrieve", "nodes_csv": os.path.join(REF_DATA, "nodes.csv"),
+                "edges_csv": os.path.join(REF_DATA, "edges.csv"), "questions": sq, "dim": 64,
+                "strategy": strategy}
+        res[f"scene|{strategy}|{{}}"] = {"cfg": {"strategy": strategy}, "out": oracle.run_ref(spec)}
+    res["graphs"]["scene"] = {"questions": sq, "dim": 64}
+    dump("retrieval.json", res)
+
+
 def c1_variants(td):
     """Same dataset with c in {2, 64} (c=m degenerates to the baseline, acceptance.cpp:108-124)
     and soft-prefix on (node-edge-topk semantics)."""
@@ -225,6 +261,7 @@ if __name__ == "__main__":
     with tempfile.TemporaryDirectory() as td:
         c1_pipeline(td)
         c1_report(td)
+        retrieval_cases(td)
         c1_variants(td)
         lm_cases()
         cluster_cases()
