@@ -267,6 +267,24 @@ def run_ours(args, rank, world, local_rank):
                "semantics": "same batch to EOS / max_new (run() with ToyLmConfig::max_new_tokens); "
                             "rt = submission -> last token"}
 
+    # ---- retrieval (the step before the hot path): retrieve() of every
+    # question on the device, reported beside the metric (the TTFT clock starts after it)
+    retr = None
+    if not args.no_gen and world == 1:
+        qs = [q.question for q in w.queries]
+        host.retrieve(ctx, dg, qs[:8], strategy="ego-topk", dim=d)
+        ev6, ev7 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev6.record(stream)
+        sub = host.retrieve(ctx, dg, qs, strategy="ego-topk", dim=d)
+        ev7.record(stream)
+        torch.cuda.synchronize()
+        r_ms = ev6.elapsed_time(ev7)
+        retr = {"strategy": "ego-topk (k 3, 2 hops, 10 centres)", "queries": m, "ms_per_batch": round(r_ms, 3),
+                "queries_per_s": round(m / (r_ms / 1e3), 1),
+                "mean_nodes": round(float(np.mean([len(s.node_ids) for s in sub])), 2),
+                "graph": {"nodes": len(w.graph.nodes), "edges": len(w.graph.edges)}}
+
     if world > 1:
         # every query is served by one rank: its TTFT is that rank's value (others report -1)
         tt = torch.from_numpy(np.stack(ttfts)).to(COLL_DEV)
@@ -331,6 +349,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roofline,
         "e2e": e2e,
         "generation": gen,
+        "retrieval": retr,
         "gpu_launches": int(launches),
         "setup_s": round(setup_s, 2),
     }
