@@ -168,7 +168,8 @@ def run_ours(args, rank, world, local_rank):
             shard = host.encode_subgraphs(ctx, dg, w.retrieved[lo:hi], pb.gnn)
             emb = D.gather_rows(torch.from_numpy(shard).to(COLL_DEV), m, world, pg).cpu().numpy()
         res = host.run_subgcache(ctx, lm, dg, pb, embeddings=emb, rank=rank, world_size=world,
-                                 want_logits=False, device_inputs=True, waves=args.waves)
+                                 want_logits=False, device_inputs=True, waves=args.waves,
+                                 split_clusters=world > 1 and not args.no_split)
         if world > 1:
             res.first_token = D.combine_first_tokens(
                 torch.from_numpy(res.first_token.astype(np.int64)).to(COLL_DEV), pg)
@@ -474,6 +475,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gen", action="store_true", help="skip the generation (decode) measurement")
+    ap.add_argument("--no-split", action="store_true",
+                    help="N > 1: whole clusters per GPU only (no member-level rebalancing of skewed clusters)")
     ap.add_argument("--attn-split", type=int, default=None, help="1: two softmax warpgroups per query tile")
     ap.add_argument("--gen-steps", type=int, default=2)
     ap.add_argument("--no-pairs", action="store_true", help="1-CTA GEMM instead of CTA pairs")

@@ -242,6 +242,11 @@ typedef struct {
      * every member of a wave): 0 or 1 = first token only; N > 1 = up to N tokens per query
      * (run() uses ToyLmConfig::max_new_tokens, pipeline.cpp:186) */
     uint32_t max_new_tokens;
+    /* world_size > 1: rebalance skewed clusters at member level: after the
+     * cluster LPT, members of the busiest rank's largest cluster move to the idlest rank while that
+     * beats replicating the cluster's prefix there (the receiving rank prefills the identical
+     * representative itself; sgc_balance_members is the plan) */
+    int split_clusters;
 } sgc_batch;
 
 typedef struct {
@@ -280,6 +285,13 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
  * processing time first (descending cost, ties by cluster index) onto the least-loaded rank
  * (ties by rank). Host-only (no device needed). */
 int sgc_lpt_assign(const double* cost, uint32_t clusters, int world_size, uint32_t* owner);
+/* Member-level plan used with sgc_batch.split_clusters: cluster LPT on prefill + member cost, then
+ * members of the busiest rank's largest cluster move to the idlest rank while max load drops even
+ * after paying that rank a prefix replica (prefill_cost). query_owner [m], cluster_owner [c] (the
+ * rank that prefills the cluster first; replicas are implied by query_owner). Host-only. */
+int sgc_balance_members(const double* prefill_cost, uint32_t clusters, const uint32_t* labels,
+                        const double* member_cost, uint32_t m, int world_size, uint32_t* query_owner,
+                        uint32_t* cluster_owner);
 
 /* ---- GEMM building block (exposed for parity tests and the roofline bench) -----------
  * D[M x N] = A[M x K] (bf16, row-major) * B[N x K]^T (bf16, row-major), fp32 accumulate in

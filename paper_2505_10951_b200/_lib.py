@@ -82,7 +82,8 @@ class Batch(C.Structure):
                 ("pointer_bonus", C.c_float), ("gnn", GnnConfig),
                 ("precomputed_embeddings", C.POINTER(C.c_float)),
                 ("cluster_owner", C.POINTER(C.c_uint32)), ("rank", C.c_int),
-                ("world_size", C.c_int), ("waves", C.c_uint32), ("max_new_tokens", C.c_uint32)]
+                ("world_size", C.c_int), ("waves", C.c_uint32), ("max_new_tokens", C.c_uint32),
+                ("split_clusters", C.c_int)]
 
 
 class BatchOut(C.Structure):
@@ -107,7 +108,7 @@ EXPORTS = [
     "sgc_pairwise_distances", "sgc_agglomerate", "sgc_build_representatives", "sgc_prefill",
     "sgc_kv_release", "sgc_kv_count", "sgc_kv_tokens", "sgc_kv_digest", "sgc_kv_resident_bytes",
     "sgc_kv_read", "sgc_extend", "sgc_run_subgcache", "sgc_gemm_bf16", "sgc_set_timing",
-    "sgc_get_timing", "sgc_lpt_assign", "sgc_set_option", "sgc_attention_bf16", "sgc_extend_generate", "sgc_retrieve",
+    "sgc_get_timing", "sgc_lpt_assign", "sgc_set_option", "sgc_attention_bf16", "sgc_extend_generate", "sgc_retrieve", "sgc_balance_members",
 ]
 
 _lib = None
@@ -175,6 +176,8 @@ def load() -> C.CDLL:
     L.sgc_get_timing.argtypes = [vp, C.c_char_p, P(C.c_double), P(C.c_uint64)]
     L.sgc_set_option.argtypes = [vp, C.c_char_p, C.c_int64]
     L.sgc_lpt_assign.argtypes = [P(C.c_double), C.c_uint32, C.c_int, P(C.c_uint32)]
+    L.sgc_balance_members.argtypes = [P(C.c_double), C.c_uint32, P(C.c_uint32), P(C.c_double), C.c_uint32,
+                                      C.c_int, P(C.c_uint32), P(C.c_uint32)]
     _lib = L
     return L
 

@@ -1146,6 +1146,79 @@ std::vector<uint32_t> lpt_assign(const std::vector<double>& cost, int world) {
     return owner;
 }
 
+// Member-level rebalancing on top of the cluster LPT. Whole clusters
+// first go to ranks by LPT on their cost (prefill + members); then, while the busiest rank is
+// ahead of the idlest by more than it costs to replicate one of its clusters' prefix there,
+// members of the busiest rank's largest cluster move over (highest query index first) -- the
+// receiving rank prefills that prefix itself (a replica: same representative, same tokens), so
+// no KV crosses GPUs. Deterministic: every rank computes the same plan from the same labels.
+std::vector<uint32_t> balance_members(const std::vector<double>& prefill_cost,
+                                      const std::vector<std::vector<uint32_t>>& members,
+                                      const std::vector<double>& member_cost, int world,
+                                      std::vector<uint32_t>& cluster_owner) {
+    const size_t k = prefill_cost.size();
+    std::vector<double> cost(k);
+    for (size_t ci = 0; ci < k; ++ci) {
+        cost[ci] = prefill_cost[ci];
+        for (uint32_t q : members[ci]) cost[ci] += member_cost[q];
+    }
+    cluster_owner = lpt_assign(cost, world);
+    std::vector<uint32_t> qown(member_cost.size(), 0);
+    std::vector<double> load(world, 0.0);
+    std::set<std::pair<uint32_t, uint32_t>> replica;  // (cluster, rank) holding its prefix
+    for (size_t ci = 0; ci < k; ++ci) {
+        for (uint32_t q : members[ci]) qown[q] = cluster_owner[ci];
+        load[cluster_owner[ci]] += cost[ci];
+        replica.insert({static_cast<uint32_t>(ci), cluster_owner[ci]});
+    }
+    if (world < 2) return qown;
+    for (size_t iter = 0; iter < member_cost.size(); ++iter) {
+        int rmax = 0, rmin = 0;
+        for (int r = 1; r < world; ++r) {
+            if (load[r] > load[rmax]) rmax = r;
+            if (load[r] < load[rmin]) rmin = r;
+        }
+        // the busiest rank's largest cluster (by the member work it serves), >= 2 members there
+        int best = -1;
+        double best_w = 0.0;
+        for (size_t ci = 0; ci < k; ++ci) {
+            double w = 0.0;
+            int cnt = 0;
+            for (uint32_t q : members[ci])
+                if (qown[q] == static_cast<uint32_t>(rmax)) {
+                    w += member_cost[q];
+                    ++cnt;
+                }
+            if (cnt >= 2 && w > best_w) {
+                best_w = w;
+                best = static_cast<int>(ci);
+            }
+        }
+        if (best < 0) break;
+        bool moved = false;
+        const auto& mem = members[best];
+        int left = 0;
+        for (uint32_t q : mem) left += qown[q] == static_cast<uint32_t>(rmax);
+        for (auto it = mem.rbegin(); it != mem.rend() && left > 1; ++it) {
+            const uint32_t q = *it;
+            if (qown[q] != static_cast<uint32_t>(rmax)) continue;
+            const bool has = replica.count({static_cast<uint32_t>(best), static_cast<uint32_t>(rmin)}) != 0;
+            const double add = member_cost[q] + (has ? 0.0 : prefill_cost[best]);
+            const double before = std::max(load[rmax], load[rmin]);
+            const double after = std::max(load[rmax] - member_cost[q], load[rmin] + add);
+            if (!(after < before * (1.0 - 1e-9))) break;
+            qown[q] = static_cast<uint32_t>(rmin);
+            load[rmax] -= member_cost[q];
+            load[rmin] += add;
+            replica.insert({static_cast<uint32_t>(best), static_cast<uint32_t>(rmin)});
+            --left;
+            moved = true;
+        }
+        if (!moved) break;
+    }
+    return qown;
+}
+
 struct RepResult {
     std::vector<uint64_t> prefix_off;  // [c+1] on host
     int32_t* d_prefix = nullptr;       // device tokens (BOS + bytes)
@@ -1978,25 +2051,34 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         std::vector<uint64_t> q_off_all = to_host(c, b->questions.off, m + 1);
         std::vector<uint32_t> owner(k, 0);
         const int world = b->world_size > 1 ? b->world_size : 1;
+        const uint32_t me = static_cast<uint32_t>(world > 1 || b->cluster_owner ? b->rank : 0);
+        std::vector<uint32_t> qown;  // member-level plan (split_clusters): query -> rank
         if (b->cluster_owner) {
             owner = to_host(c, b->cluster_owner, k);
         } else if (world > 1) {
-            std::vector<double> cost(k, 0.0);
+            std::vector<double> pcost(k, 0.0), mcost(m, 0.0), cost(k, 0.0);
             const double ftok = 2.0 * model->L * (4.0 * d * d + 2.0 * d * model->ffn);
             for (uint32_t ci = 0; ci < k; ++ci) {
                 const double P = static_cast<double>(reps_all.prefix_off[ci + 1] - reps_all.prefix_off[ci]);
-                cost[ci] = P * ftok + 2.0 * d * model->L * P * P;
+                pcost[ci] = P * ftok + 2.0 * d * model->L * P * P;
+                cost[ci] = pcost[ci];
                 for (uint32_t q : members[ci]) {
                     const double S = static_cast<double>(q_off_all[q + 1] - q_off_all[q]);
-                    cost[ci] += S * ftok + 4.0 * d * model->L * S * P;
+                    mcost[q] = S * ftok + 4.0 * d * model->L * S * P;
+                    cost[ci] += mcost[q];
                 }
             }
-            owner = lpt_assign(cost, world);
+            if (b->split_clusters) qown = balance_members(pcost, members, mcost, world, owner);
+            else owner = lpt_assign(cost, world);
         }
         if (o->owner) sgc::copy_out(c, o->owner, owner.data(), k);
         std::vector<uint32_t> owned;
-        for (uint32_t ci = 0; ci < k; ++ci)
-            if (owner[ci] == static_cast<uint32_t>(world > 1 || b->cluster_owner ? b->rank : 0)) owned.push_back(ci);
+        std::vector<std::vector<uint32_t>> served(k);  // members this rank serves, per cluster
+        for (uint32_t ci = 0; ci < k; ++ci) {
+            for (uint32_t q : members[ci])
+                if (qown.empty() ? owner[ci] == me : qown[q] == me) served[ci].push_back(q);
+            if (!served[ci].empty()) owned.push_back(ci);
+        }
         // serving order: Smith's rule (ascending row cost per query) so the waves that finish
         // first carry the most queries -- minimizes the summed (mean) TTFT; results are
         // independent of the order (every row's math is batch-independent)
@@ -2009,12 +2091,17 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             }
             std::stable_sort(owned.begin(), owned.end(), [&](uint32_t a, uint32_t b2) { return ratio[a] < ratio[b2]; });
         }
-        std::vector<std::vector<uint32_t>> own_members;
-        for (uint32_t ci : owned) own_members.push_back(members[ci]);
+        // representatives are built from the FULL membership (a replicated prefix is identical on
+        // every rank serving part of the cluster); own_members are the queries served here
+        std::vector<std::vector<uint32_t>> own_members, rep_members;
+        for (uint32_t ci : owned) {
+            own_members.push_back(served[ci]);
+            rep_members.push_back(members[ci]);
+        }
         RepResult reps;
         if (!owned.empty()) {
             if (owned.size() == k && b->waves <= 1) reps = reps_all;
-            else reps = build_reps(c, g, hs, m, own_members, budget);
+            else reps = build_reps(c, g, hs, m, rep_members, budget);
         }
         std::vector<float> soft_h;
         std::vector<uint8_t> soft_mask;
@@ -2507,6 +2594,24 @@ int sgc_debug_attn_prof(unsigned long long* out, int reset) {
     return 0;
 }
 #endif
+
+int sgc_balance_members(const double* prefill_cost, uint32_t clusters, const uint32_t* labels,
+                        const double* member_cost, uint32_t m, int world_size, uint32_t* query_owner,
+                        uint32_t* cluster_owner) {
+    return guarded([&] {
+        if (world_size < 1) fail(SGC_DOMAIN, "world_size must be >= 1");
+        std::vector<std::vector<uint32_t>> members(clusters);
+        for (uint32_t q = 0; q < m; ++q) {
+            if (labels[q] >= clusters) fail(SGC_DOMAIN, "label out of range");
+            members[labels[q]].push_back(q);
+        }
+        std::vector<uint32_t> co;
+        std::vector<uint32_t> qo = balance_members(std::vector<double>(prefill_cost, prefill_cost + clusters), members,
+                                                   std::vector<double>(member_cost, member_cost + m), world_size, co);
+        std::copy(qo.begin(), qo.end(), query_owner);
+        if (cluster_owner) std::copy(co.begin(), co.end(), cluster_owner);
+    });
+}
 
 int sgc_lpt_assign(const double* cost, uint32_t clusters, int world_size, uint32_t* owner) {
     return guarded([&] {

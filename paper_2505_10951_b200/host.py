@@ -558,7 +558,8 @@ def _device_copy(pb: "PreparedBatch"):
 def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
                   embeddings: np.ndarray | None = None, cluster_owner=None, rank: int = 0,
                   world_size: int = 1, want_logits: bool = True,
-                  device_inputs: bool = False, waves: int = 1, max_new: int = 0) -> SubgCacheResult:
+                  device_inputs: bool = False, waves: int = 1, max_new: int = 0,
+                  split_clusters: bool = False) -> SubgCacheResult:
     """pipeline.cpp:212-293 (SubgCache branch) + cache_engine.cpp:217-233 (run_batch), to the
     first token of every query."""
     w = pb.w
@@ -593,6 +594,7 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     b.world_size = world_size
     b.waves = waves
     b.max_new_tokens = max_new
+    b.split_clusters = int(split_clusters)
     emb = np.zeros((m, d), np.float32)
     labels = np.zeros(m, np.uint32)
     nm = max(m - k, 1)

@@ -88,3 +88,58 @@ def test_two_rank_gloo_matches_single_process():
     assert r0[2] == r1[2]                           # same ownership on every rank
     expected = [(7 * q + 3) % 260 for q in range(m)]
     assert r0[3] == r1[3] == expected               # every query served exactly once
+
+
+def _balance(prefill, labels, mcost, world):
+    import ctypes as C
+
+    from paper_2505_10951_b200 import _lib
+
+    L = _lib.load()
+    pc = np.ascontiguousarray(prefill, np.float64)
+    lb = np.ascontiguousarray(labels, np.uint32)
+    mc = np.ascontiguousarray(mcost, np.float64)
+    qo = np.zeros(len(lb), np.uint32)
+    co = np.zeros(len(pc), np.uint32)
+    _lib.check(L.sgc_balance_members(pc.ctypes.data_as(C.POINTER(C.c_double)), len(pc),
+                                     lb.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                     mc.ctypes.data_as(C.POINTER(C.c_double)), len(lb), world,
+                                     qo.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                     co.ctypes.data_as(C.POINTER(C.c_uint32))))
+    return qo, co
+
+
+def _loads(prefill, labels, mcost, qo, world):
+    load = np.zeros(world)
+    for q, r in enumerate(qo):
+        load[r] += mcost[q]
+    for c in range(len(prefill)):
+        for r in set(int(qo[q]) for q in range(len(labels)) if labels[q] == c):
+            load[r] += prefill[c]  # every rank serving part of a cluster prefills it
+    return load
+
+
+def test_member_balance_splits_skewed_clusters_only():
+    """a dominant cluster is split across ranks (each receiving rank pays
+    a prefix replica); balanced inputs keep whole clusters (the plan degenerates to cluster LPT)."""
+    # skewed: one cluster with 600 members, seven with 20
+    labels = np.array([0] * 600 + [c for c in range(1, 8) for _ in range(20)])
+    prefill = np.full(8, 30.0)
+    mcost = np.ones(len(labels))
+    for world in (2, 4, 8):
+        qo, co = _balance(prefill, labels, mcost, world)
+        assert qo.max() < world
+        lpt = np.zeros(world)
+        cost = prefill + np.bincount(labels, weights=mcost)
+        for c in np.argsort(-cost, kind="stable"):
+            lpt[np.argmin(lpt)] += cost[c]
+        bal = _loads(prefill, labels, mcost, qo, world)
+        assert bal.max() < 0.85 * lpt.max()                  # the 600-member cluster got split
+        assert bal.max() - bal.min() <= prefill.max() + mcost.max()  # ~even after replicas
+        assert len(set(qo[labels == 0].tolist())) >= 2
+        assert np.array_equal(qo, _balance(prefill, labels, mcost, world)[0])  # deterministic
+    # balanced: 16 equal clusters over 8 ranks -> no member moves, two whole clusters per rank
+    labels = np.repeat(np.arange(16), 64)
+    qo, co = _balance(np.full(16, 30.0), labels, np.ones(len(labels)), 8)
+    for c in range(16):
+        assert len(set(qo[labels == c].tolist())) == 1 and qo[labels == c][0] == co[c]

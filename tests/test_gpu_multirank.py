@@ -21,17 +21,33 @@ def _port():
     return p
 
 
-def test_two_ranks_serve_every_query_once(tmp_path):
-    out = tmp_path / "mr.json"
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+def _run(tmp_path, ranks, *extra):
+    out = tmp_path / f"mr{ranks}.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(HERE, "support", "multirank_c1.py"), str(out)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+           os.path.join(HERE, "support", "multirank_c1.py"), str(out), *extra]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
-    got = json.loads(out.read_text())
+    return json.loads(out.read_text())
+
+
+def test_two_ranks_serve_every_query_once(tmp_path):
+    got = _run(tmp_path, 2)
     with open(os.path.join(HERE, "golden", "c1_pipeline.json")) as f:
         G = json.load(f)
     assert got["labels"] == G["labels"]
     assert sorted(set(got["owner"])) == [0, 1]          # both ranks own clusters (LPT)
     assert sum(got["served"]) == 64                      # each query served by exactly one rank
     assert got["first"] == G["run_batch_first_token"]    # == the reference's run_batch
+
+
+def test_split_clusters_member_level_balance(tmp_path):
+    """SURVEY.md 8(f) rank 2 on four ranks: C1's clusters are 32/30/1/1 members, so the two big
+    ones are split (their prefixes replicated on the idle ranks); answers are unchanged."""
+    with open(os.path.join(HERE, "golden", "c1_pipeline.json")) as f:
+        G = json.load(f)
+    got = _run(tmp_path, 4, "split")
+    assert sum(got["served"]) == 64 and min(got["served"]) > 0   # every rank works
+    servers_of_c0 = {got["server"][q] for q in range(64) if got["labels"][q] == 0}
+    assert len(servers_of_c0) >= 2                              # the 32-member cluster was split
+    assert got["first"] == G["run_batch_first_token"]
