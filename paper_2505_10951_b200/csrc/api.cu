@@ -252,13 +252,16 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
     SGC_CUDA_CHECK(cudaMemsetAsync(bad, 0, sizeof(int), c->stream));
     // RMSNorm is fused: every residual GEMM (and the embedding) writes bf16(x) and the row sums
     // of squares; the next GEMM scales its accumulator rows (gemm.cuh GemmEpi::in_ss)
-    float* ss_a = c->buf<float>("fwd_ss_a", M);  // -> QKV
-    float* ss_b = c->buf<float>("fwd_ss_b", M);  // -> W1
+    // row sums of squares as d/32 chunk slots per row (written, never accumulated: deterministic)
+    const int parts = d / 32;
+    float* ss_a = c->buf<float>("fwd_ss_a", static_cast<size_t>(M) * parts);  // -> QKV
+    float* ss_b = c->buf<float>("fwd_ss_b", static_cast<size_t>(M) * parts);  // -> W1
+    float* rs = c->buf<float>("fwd_rscale", M);                                // finalized scales
     sgc::embed(c, x, b.d_tokens, m->tok_emb, b.d_soft, b.d_soft_idx, d, M, bad, xb, ss_a);
     for (int l = 0; l < m->L; ++l) {
         sgc::GemmEpi e;
-        e.in_ss = ss_a;
-        e.norm_dim = d;
+        sgc::rms_scale(c, rs, ss_a, M, l == 0 ? 1 : parts, d);  // the embedding writes one slot per row
+        e.row_scale = rs;
         e.mode = sgc::EPI_QKV;
         e.q_out = q;
         e.k_cache = b.k_loc(l);
@@ -331,18 +334,16 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
         r.out_xb = xb;
         r.out_ss = ss_b;
         r.splitk_ok = b.dec != nullptr;
-        SGC_CUDA_CHECK(cudaMemsetAsync(ss_b, 0, sizeof(float) * M, c->stream));
         sgc::gemm_bf16(c, ao, m->wo[l], M, d, d, r);
 
         sgc::GemmEpi t;
         t.mode = sgc::EPI_TANH;
         t.out = h;
         t.ldo = m->ffn;
-        t.in_ss = ss_b;
-        t.norm_dim = d;
+        sgc::rms_scale(c, rs, ss_b, M, parts, d);
+        t.row_scale = rs;
         sgc::gemm_bf16(c, xb, m->w1[l], M, m->ffn, d, t);
         r.out_ss = ss_a;  // the next layer's QKV input
-        SGC_CUDA_CHECK(cudaMemsetAsync(ss_a, 0, sizeof(float) * M, c->stream));
         sgc::gemm_bf16(c, h, m->w2[l], M, d, m->ffn, r);
     }
     sgc::head_logits(c, b.d_logits, x, b.d_logit_rows, b.n_logits, m->head_t, d);

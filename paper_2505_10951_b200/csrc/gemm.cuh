@@ -24,11 +24,11 @@ struct GemmEpi {
     int d = 0;
     int hd = 0;
     // fused RMSNorm (lm_core.cpp:26-31, no gain): A holds bf16(x) UNnormalized and the epilogue
-    // scales each accumulator row by 1 / sqrt(in_ss[row] / norm_dim + 1e-5) (QKV, TANH, F32, BF16)
-    const float* in_ss = nullptr;
-    int norm_dim = 0;
-    // EPI_RESID producer side: also store bf16(x_new) to out_xb (ld = ldo) and accumulate the
-    // row's sum of squares of x_new into out_ss (zeroed by the caller) for the next GEMM
+    // multiplies each accumulator row by row_scale[row] = 1 / sqrt(mean(x^2) + 1e-5) (QKV, TANH,
+    // F32, BF16), finalized from the producer's per-chunk sums in index order (rms_scale)
+    const float* row_scale = nullptr;
+    // EPI_RESID producer side: also store bf16(x_new) to out_xb (ld = ldo) and, per 32-column
+    // chunk c of the row, its sum of squares of x_new to out_ss[row * (N / 32) + c]
     __nv_bfloat16* out_xb = nullptr;
     float* out_ss = nullptr;
     // decode steps only: allow the split-K residual path for few rows (changes the fp32

@@ -119,7 +119,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                                               int ep_rows) {
     // fused RMSNorm of the A rows: one scale per accumulator row
     float inv = 1.0f;
-    if (ep.in_ss && valid) inv = 1.0f / sqrtf(ep.in_ss[row] / static_cast<float>(ep.norm_dim) + 1e-5f);
+    if (ep.row_scale && valid) inv = ep.row_scale[row];
     if constexpr (EPI == EPI_QKV) {
         // one tile never straddles the q/k/v sections (d % BN == 0)
         const int d = ep.d;
@@ -297,19 +297,19 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
             }
             __syncwarp();
             if constexpr (EPI == EPI_RESID) {
-                if (ep.out_xb) {
+                if (ep.out_ss) {  // this row's sum of squares over the chunk -> its own slot
+                    float cs = 0.f;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         const float xv = stage[lane * 33 + j];
-                        ss = fmaf(xv, xv, ss);
+                        cs = fmaf(xv, xv, cs);
                     }
+                    if (valid) ep.out_ss[static_cast<size_t>(row) * (ep.ldo / 32) + (n0 / 32 + ch)] = cs;
                 }
                 __syncwarp();
             }
         }
-        if constexpr (EPI == EPI_RESID) {
-            if (ep.out_ss && valid && ch_hi > ch_lo) atomicAdd(ep.out_ss + row, ss);
-        }
+        (void)ss;
     }
 }
 
@@ -663,6 +663,9 @@ __global__ void __launch_bounds__(256) resid_reduce_kernel(float* x, __nv_bfloat
     const int r = blockIdx.x;
     float ss = 0.f;
     const size_t plane = static_cast<size_t>(M) * N;
+    // the row's sum of squares leaves as N/32 chunk slots (part 0 = the whole row, the rest 0)
+    if (ss_out)
+        for (int p = threadIdx.x + 1; p < N / 32; p += blockDim.x) ss_out[static_cast<size_t>(r) * (N / 32) + p] = 0.f;
     for (int c = threadIdx.x * 4; c < N; c += blockDim.x * 4) {
         const size_t off = static_cast<size_t>(r) * N + c;
         float4 v = *reinterpret_cast<const float4*>(x + off);
@@ -691,7 +694,7 @@ __global__ void __launch_bounds__(256) resid_reduce_kernel(float* x, __nv_bfloat
     if (threadIdx.x == 0) {
         float t = 0.f;
         for (int w = 0; w < 8; ++w) t += red[w];
-        ss_out[r] = t;
+        ss_out[static_cast<size_t>(r) * (N / 32)] = t;
     }
 }
 

@@ -327,10 +327,36 @@ void step_tokens(Ctx* c, int32_t* tok, const float* logits, int n, const int8_t*
     SGC_LAUNCH_CHECK(c);
 }
 namespace {
+// RMSNorm scale of every row from its chunk sums of squares, summed in index order (the scale
+// never depends on which tile or warp produced a chunk): 1 / sqrt(sum / d + 1e-5), lm_core.cpp:26-31
+__global__ void rms_scale_kernel(float* scale, const float* parts, int rows, int n_parts, int d) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= rows) return;
+    const float4* p4 = reinterpret_cast<const float4*>(parts + static_cast<size_t>(r) * n_parts);
+    float ss = 0.f;
+    if (n_parts % 4 == 0) {
+        for (int i = 0; i < n_parts / 4; ++i) {
+            const float4 v = p4[i];
+            ss += v.x;
+            ss += v.y;
+            ss += v.z;
+            ss += v.w;
+        }
+    } else {
+        for (int i = 0; i < n_parts; ++i) ss += parts[static_cast<size_t>(r) * n_parts + i];
+    }
+    scale[r] = 1.0f / sqrtf(ss / static_cast<float>(d) + 1e-5f);
+}
 __global__ void iota_kernel(int32_t* p, int n) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
 }
 }  // namespace
+void rms_scale(Ctx* c, float* scale, const float* parts, int rows, int n_parts, int d) {
+    if (rows <= 0) return;
+    Ctx::Timed timer(c, "rmsnorm");
+    rms_scale_kernel<<<ceil_div(rows, 256), 256, 0, c->stream>>>(scale, parts, rows, n_parts, d);
+    SGC_LAUNCH_CHECK(c);
+}
 int32_t* Ctx::iota(int n) {
     int32_t* p = buf<int32_t>("iota", n);
     const int cap = static_cast<int>(scratch["iota"].bytes / sizeof(int32_t));

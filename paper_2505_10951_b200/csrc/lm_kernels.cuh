@@ -12,6 +12,8 @@ void embed(Ctx* c, float* x, const int32_t* tokens, const float* tok_emb, const 
            const int32_t* soft_idx, int d, int rows, int* bad, __nv_bfloat16* xb = nullptr,
            float* ss = nullptr);
 void rmsnorm_bf16(Ctx* c, __nv_bfloat16* out, const float* x, int d, int rows);
+// per-row RMSNorm scale from per-chunk sums of squares (n_parts per row), fixed summation order
+void rms_scale(Ctx* c, float* scale, const float* parts, int rows, int n_parts, int d);
 void head_logits(Ctx* c, float* logits, const float* x, const int32_t* rows, int n,
                  const float* head_t, int d);
 void first_tokens(Ctx* c, int32_t* first, const float* logits, int n, const int32_t* ctx_tokens,
