@@ -146,6 +146,8 @@ def run_ours(args, rank, world, local_rank):
     ctx.set_option("gemm_pairs", 0 if args.no_pairs else 1)
     if args.attn_split is not None:
         ctx.set_option("attn_split", args.attn_split)
+    if args.attn_db is not None:
+        ctx.set_option("attn_db", args.attn_db)
     t0 = time.time()
     lm = host.ToyLm(ctx, host.ToyLmConfig(**w.lm, seed=w.seed))
     dg = host.DeviceGraph(ctx, w.graph)
@@ -478,6 +480,8 @@ def main():
     ap.add_argument("--no-split", action="store_true",
                     help="N > 1: whole clusters per GPU only (no member-level rebalancing of skewed clusters)")
     ap.add_argument("--attn-split", type=int, default=None, help="1: two softmax warpgroups per query tile")
+    ap.add_argument("--attn-db", type=int, default=None,
+                    help="1: double-buffered 64-key attention kernel, 0: 128-key single-buffer kernel")
     ap.add_argument("--gen-steps", type=int, default=2)
     ap.add_argument("--no-pairs", action="store_true", help="1-CTA GEMM instead of CTA pairs")
     ap.add_argument("--waves", type=int, default=4,

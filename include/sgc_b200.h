@@ -315,7 +315,10 @@ int sgc_set_timing(sgc_ctx* ctx, int enable);
 /* Tuning knobs: "gemm_pairs" (1 = CTA-pair tcgen05 GEMM for 256-wide tiles, default; 0 = 1-CTA);
  * "decode_defer_pct" (generation: a wave decodes on its own until fewer than this percentage of
  * its queries still generate, the stragglers of every wave then finish in one shared loop;
- * default 25, 0 = each wave to completion, >= 100 = all decoding after the last wave). */
+ * default 25, 0 = each wave to completion, >= 100 = all decoding after the last wave);
+ * "attn_split" (1 = two softmax warpgroups per query tile; default 0);
+ * "attn_db" (1 = double-buffered 64-key attention kernel; default 0, the 128-key kernel is
+ * faster at C3: 141 vs 188 ms/step). Unknown names return SGC_ERR_INVALID. */
 int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value);
 int sgc_get_timing(sgc_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches);
 

@@ -40,6 +40,8 @@ bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, in
 inline bool attention_tc_supported(int hd) { return hd == 64 || hd == 128; }
 // split every S row over two softmax warpgroups, or one thread per row (default)
 void attention_set_split(bool on);
+// double-buffered S with 64-key blocks (default on) or the single-buffered 128-key kernel
+void attention_set_db(bool on);
 
 // Decode step (attention.cu): merge the prefix partial (part_o, part_lse from the tcgen05 kernel
 // in partial mode, or none when part_o == nullptr) with each row's own keys: question rows

@@ -1,6 +1,7 @@
 // sm100_ptx.cuh -- thin inline-PTX wrappers for Blackwell (sm_100a): mbarrier, TMA,
 // tcgen05 (TMEM alloc / MMA / commit / ld) and UMMA descriptors.
 #pragma once
+#include <cstdio>
 #include <cuda.h>
 #include <stdint.h>
 
@@ -26,6 +27,26 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifdef SGC_MBAR_WATCHDOG
+// debug builds: a wait that spins for ~seconds reports (block, thread, barrier, parity) and traps
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    for (long long it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (it == (1ll << 24) && (threadIdx.x & 31) == 0)
+            printf("mbar watchdog: block %d thread %d bar smem+%u parity %u\n", blockIdx.x, threadIdx.x,
+                   smem_u32(bar), parity);
+        if (it == (1ll << 25)) __trap();
+    }
+}
+#else
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -35,6 +56,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+#endif
 
 // ---- TMA ------------------------------------------------------------------------------
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
