@@ -27,6 +27,7 @@
 // sequences (representative prefill).
 #include "attention.cuh"
 #include "common.cuh"
+#include "sched.cuh"
 #include "sm100_ptx.cuh"
 #include "tma.cuh"
 
@@ -54,7 +55,8 @@ struct TcCfg {
     static constexpr int kKBytes = BKV * HD * 2;
     static constexpr int kVBytes = BKV * HD * 2;
     // + barriers (256 B) + the split-softmax exchange slots [2][2][BQ] fp32
-    static constexpr int kSmem = 2 * kQBytes + kKStages * kKBytes + kVStages * kVBytes + 256 + 2 * 2 * BQ * 4;
+    // + barriers (256 B) + the split-softmax exchange slots [2][2][BQ] fp32 + the item ring
+    static constexpr int kSmem = 2 * kQBytes + kKStages * kKBytes + kVStages * kVBytes + 256 + 2 * 2 * BQ * 4 + 128;
     static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kS = 0;    // S_X at column X * 128
     static constexpr uint32_t kO = 256;  // O_X at column 256 + X * 128
@@ -77,7 +79,9 @@ struct TcParams {
     __nv_bfloat16* out;
     int d;
     float scale_log2;
+    uint32_t* sched;  // dynamic item counter (sched.cuh)
 };
+using ItemRing = UnitRing<4>;
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -172,6 +176,7 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                    const __grid_constant__ CUtensorMap tmVp, const __grid_constant__ CUtensorMap tmKl,
                    const __grid_constant__ CUtensorMap tmVl, TcParams p) {
     using C = TcCfg<HD>;
+    static_assert(sizeof(ItemRing) <= 128, "item ring");
     // all shared memory is dynamic (no static arrays), so the base is 1024-byte aligned
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sQ = smem;                                  // [2][BQ x HD]
@@ -189,6 +194,8 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
     uint64_t* o_full = bars + 18;   // [2] per tile
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
     float* xm = reinterpret_cast<float*>(bars + 32);  // [2 tiles][SPLIT][BQ] row max / sum exchange
+    // items (unit x head) claimed by the producer and handed to the MMA and softmax warps
+    ItemRing* ring = reinterpret_cast<ItemRing*>(xm + 2 * 2 * BQ);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int n_items = p.n_work * p.heads;
@@ -212,6 +219,7 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
             ptx::mbar_init(&p_full[i], 128 * SPLIT);
             ptx::mbar_init(&o_full[i], 1);
         }
+        sched::init(ring, 1 + 8 * SPLIT);  // the MMA thread + every softmax warp
         ptx::fence_barrier_init();
     }
     if (warp == 0) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -224,7 +232,10 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
         // TMA loader: Q tiles once per unit, then K_b and V_b per block
         if (lane == 0) {
             uint32_t g = 0, qit[2] = {0, 0};
-            for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+            for (uint32_t k = 0;; ++k) {
+                const uint32_t iu = sched::publish(ring, k, p.sched, n_items, gridDim.x);
+                if (iu >= static_cast<uint32_t>(n_items)) break;
+                const int item = static_cast<int>(iu);
                 const int h = item / p.n_work;
                 const AttnWork w = p.work[item % p.n_work];
                 const UnitPlan u = plan_unit(w, p.seg_lo, p.part_o != nullptr);
@@ -288,8 +299,11 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 }
                 ++gx[x];
             };
-            for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-                const AttnWork w = p.work[item % p.n_work];
+            for (uint32_t k = 0;; ++k) {
+                const uint32_t iu = sched::wait(ring, k);
+                sched::release(ring, k);
+                if (iu >= static_cast<uint32_t>(n_items)) break;
+                const AttnWork w = p.work[iu % p.n_work];
                 const UnitPlan u = plan_unit(w, p.seg_lo, p.part_o != nullptr);
                 const int nbu = max(u.nb[0], u.nb[1]);
                 for (int x = 0; x < 2; ++x)
@@ -359,7 +373,12 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
 #else
 #define SPROF(slot)
 #endif
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t iu = sched::wait(ring, k);
+            __syncwarp();
+            if (lane == 0) sched::release(ring, k);
+            if (iu >= static_cast<uint32_t>(n_items)) break;
+            const int item = static_cast<int>(iu);
             const int h = item / p.n_work;
             const AttnWork w = p.work[item % p.n_work];
             const UnitPlan u = plan_unit(w, p.seg_lo, p.part_o != nullptr);
@@ -929,7 +948,8 @@ void launch_db(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, i
     CUtensorMap tvp = make_map_2d(a.v_pfx, pfx_rows, d, BKD, 64);
     CUtensorMap tkl = make_map_2d(a.k_loc, loc_rows, d, BKD, 64);
     CUtensorMap tvl = make_map_2d(a.v_loc, loc_rows, d, BKD, 64);
-    TcParams p{a.work, n_work, heads, a.part_o, a.part_lse, a.seg_lo, a.out, d, a.scale * 1.4426950408889634f};
+    TcParams p{a.work, n_work, heads, a.part_o, a.part_lse, a.seg_lo, a.out, d, a.scale * 1.4426950408889634f,
+                c->sched_counter()};
     const int items = n_work * heads;
     const int grid = items < c->num_sms ? items : c->num_sms;
     Ctx::Timed timer(c, "attention");
@@ -952,7 +972,8 @@ void launch_tc(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, i
     CUtensorMap tvp = make_map_2d(a.v_pfx, pfx_rows, d, BKV, 64);
     CUtensorMap tkl = make_map_2d(a.k_loc, loc_rows, d, BKV, 64);
     CUtensorMap tvl = make_map_2d(a.v_loc, loc_rows, d, BKV, 64);
-    TcParams p{a.work, n_work, heads, a.part_o, a.part_lse, a.seg_lo, a.out, d, a.scale * 1.4426950408889634f};
+    TcParams p{a.work, n_work, heads, a.part_o, a.part_lse, a.seg_lo, a.out, d, a.scale * 1.4426950408889634f,
+                c->sched_counter()};
     const int items = n_work * heads;
     const int grid = items < c->num_sms ? items : c->num_sms;
     Ctx::Timed timer(c, "attention");

@@ -157,6 +157,16 @@ struct Ctx {
         }
         return reinterpret_cast<T*>(b.ptr);
     }
+    // [next unit, finished fetchers] of the persistent kernels' dynamic scheduler (sched.cuh):
+    // zeroed once, every kernel leaves it zeroed for the next one in the stream
+    uint32_t* sched_ptr = nullptr;
+    uint32_t* sched_counter() {
+        if (!sched_ptr) {
+            sched_ptr = buf<uint32_t>("unit_sched", 4);
+            SGC_CUDA_CHECK(cudaMemsetAsync(sched_ptr, 0, 4 * sizeof(uint32_t), stream));
+        }
+        return sched_ptr;
+    }
     // device [0, 1, ..., n-1] (grown on demand, filled on the device: no host round trip)
     int32_t* iota(int n);
     int iota_n = 0;

@@ -19,6 +19,7 @@
 
 #include "common.cuh"
 #include "gemm.cuh"
+#include "sched.cuh"
 #include "sm100_ptx.cuh"
 #include "tma.cuh"
 
@@ -34,6 +35,11 @@ constexpr int kThreads = 384;
 constexpr int kEpiThreads = 256;
 // per epilogue warp: a 32 x 33 fp32 staging tile (row-major, padded: conflict-free both ways)
 constexpr int kStageSmem = 8 * 32 * 33 * 4;
+// barrier area: stage / accumulator barriers in the first 256 B, the tile ring in the next 256 B
+constexpr int kBarBytes = 512;
+constexpr int kRing = 8;  // claimed tiles in flight between the fetcher and the epilogue
+using TileRing = UnitRing<kRing>;
+static_assert(sizeof(TileRing) <= 256, "tile ring must fit its barrier-area half");
 
 // chunk range of epilogue warpgroup `eg` (0/1): halves of the tile, or everything in group 0 when
 // a QKV head (RoPE pairs chunk ch with ch + HD/64) would straddle the halves
@@ -57,7 +63,7 @@ struct Cfg {
     static constexpr int kBBytes = BN * BK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;
-    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/ + kStageSmem;
+    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + kBarBytes + kStageSmem;
 };
 
 __device__ __forceinline__ float tanh_fast(float x) {
@@ -316,7 +322,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
 template <int BN, int EPI, int HD>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                int M, int N, int K, GemmEpi ep, int ksplit) {
+                int M, int N, int K, GemmEpi ep, int ksplit, uint32_t* sched_ctr) {
     using C = Cfg<BN>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -329,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = bars + 2 * C::kStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    TileRing* ring = reinterpret_cast<TileRing*>(reinterpret_cast<uint8_t*>(bars) + 256);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -353,6 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&tfull[a], 1);
             ptx::mbar_init(&tempty[a], kEpiThreads);
         }
+        sched::init(ring, 1 + kEpiThreads / 32);  // consumers: the MMA thread + 8 epilogue warps
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -379,7 +387,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             // operands are re-read across the raster group's tiles: keep them in L2 ahead of the
             // streamed epilogue outputs
             const uint64_t keep = ptx::policy_evict_last();
-            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            for (uint32_t k = 0;; ++k) {
+                const uint32_t tu = sched::publish(ring, k, sched_ctr, num_tiles, gridDim.x);
+                if (tu >= static_cast<uint32_t>(num_tiles)) break;
+                const int t = static_cast<int>(tu);
                 int m0, n0;
                 tile_coords(t, m0, n0);
                 const int kb0 = (t % ksplit) * num_kb;
@@ -400,8 +411,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN);
             int stage = 0;
             uint32_t phase = 0;
-            int local = 0;
-            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+            for (uint32_t local = 0;; ++local) {
+                const uint32_t tu = sched::wait(ring, local);
+                sched::release(ring, local);
+                if (tu >= static_cast<uint32_t>(num_tiles)) break;
                 const int acc = local & 1;
                 const uint32_t acc_phase = (local >> 1) & 1;
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -431,9 +444,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ew = warp & 3;  // TMEM lanes 32*ew .. 32*ew+31
         int ch_lo, ch_hi;
         epi_chunks<BN, EPI, HD>((warp - 4) / 4, ch_lo, ch_hi);
-        float* stage = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256) + (warp - 4) * 32 * 33;
-        int local = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++local) {
+        float* stage = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes) + (warp - 4) * 32 * 33;
+        for (uint32_t local = 0;; ++local) {
+            const uint32_t tu = sched::wait(ring, local);
+            __syncwarp();
+            if (lane == 0) sched::release(ring, local);
+            if (tu >= static_cast<uint32_t>(num_tiles)) break;
+            const int t = static_cast<int>(tu);
             int m0, n0;
             tile_coords(t, m0, n0);
             const int acc = local & 1;
@@ -469,13 +486,13 @@ struct Cfg2 {
     static constexpr int kABytes = BM * BK * 2;  // this CTA's 128 rows of A
     static constexpr int kBBytes = BM * BK * 2;  // this CTA's 128 rows of B
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kSmem = kStages2 * kStageBytes + 1024 + 256 + kStageSmem;
+    static constexpr int kSmem = kStages2 * kStageBytes + 1024 + kBarBytes + kStageSmem;
 };
 
 template <int EPI, int HD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 int M, int N, int K, GemmEpi ep) {
+                 int M, int N, int K, GemmEpi ep, uint32_t* sched_ctr) {
     constexpr int BN = 256;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -488,11 +505,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* tfull = bars + 2 * kStages2;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    // the leader's producer claims pair-tiles and publishes them to both CTAs' rings
+    TileRing* ring = reinterpret_cast<TileRing*>(reinterpret_cast<uint8_t*>(bars) + 256);
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = ptx::cluster_ctarank();
     const bool leader = rank == 0;
-    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int npairs = gridDim.x >> 1;
     const int m_tiles = (M + 2 * BM - 1) / (2 * BM);
     const int n_tiles = N / BN;
     const int num_tiles = m_tiles * n_tiles;
@@ -512,6 +531,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&tfull[a], 1);
             ptx::mbar_init(&tempty[a], 2 * kEpiThreads);  // both CTAs' epilogue threads release
         }
+        // leader slot consumers: its MMA thread + 8 epilogue warps, the peer's producer + 8
+        // epilogue warps (the peer's own empty barriers are unused)
+        sched::init(ring, 2 + 2 * (kEpiThreads / 32));
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc_2sm<512>(tmem_slot);
@@ -536,7 +558,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             const uint64_t keep = ptx::policy_evict_last();  // operands re-read across the group
-            for (int t = pair; t < num_tiles; t += npairs) {
+            for (uint32_t k = 0;; ++k) {
+                uint32_t tu;
+                if (leader) {
+                    tu = sched::publish_pair(ring, k, sched_ctr, num_tiles, npairs);
+                } else {
+                    tu = sched::wait_remote(ring, k);
+                    sched::release_to(ring, k, 0);
+                }
+                if (tu >= static_cast<uint32_t>(num_tiles)) break;
+                const int t = static_cast<int>(tu);
                 int m0, n0;
                 tile_coords(t, m0, n0);
                 for (int kb = 0; kb < num_kb; ++kb) {
@@ -558,8 +589,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * BM, BN);
             int stage = 0;
             uint32_t phase = 0;
-            int local = 0;
-            for (int t = pair; t < num_tiles; t += npairs, ++local) {
+            for (uint32_t local = 0;; ++local) {
+                const uint32_t tu = sched::wait(ring, local);
+                sched::release(ring, local);
+                if (tu >= static_cast<uint32_t>(num_tiles)) break;
                 const int acc = local & 1;
                 const uint32_t acc_phase = (local >> 1) & 1;
                 ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -587,9 +620,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const int ew = warp & 3;
         int ch_lo, ch_hi;
         epi_chunks<BN, EPI, HD>((warp - 4) / 4, ch_lo, ch_hi);
-        float* stage = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + 256) + (warp - 4) * 32 * 33;
-        int local = 0;
-        for (int t = pair; t < num_tiles; t += npairs, ++local) {
+        float* stage = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes) + (warp - 4) * 32 * 33;
+        for (uint32_t local = 0;; ++local) {
+            uint32_t tu;
+            if (leader) {
+                tu = sched::wait(ring, local);
+                __syncwarp();
+                if (lane == 0) sched::release(ring, local);
+            } else {
+                tu = sched::wait_remote(ring, local);
+                __syncwarp();
+                if (lane == 0) sched::release_to(ring, local, 0);
+            }
+            if (tu >= static_cast<uint32_t>(num_tiles)) break;
+            const int t = static_cast<int>(tu);
             int m0, n0;
             tile_coords(t, m0, n0);
             const int acc = local & 1;
@@ -633,7 +677,7 @@ void launch(Ctx* c, const void* A, const void* B, int M, int N, int K, const Gem
     int tiles = ((M + BM - 1) / BM) * (N / BN) * ksplit;
     int grid = tiles < c->num_sms ? tiles : c->num_sms;
     Ctx::Timed timer(c, gemm_timer_name(ksplit > 1 ? EPI_RESID : EPI));
-    kfn<<<grid, kThreads, Cf::kSmem, c->stream>>>(ta, tb, M, N, K, ep, ksplit);
+    kfn<<<grid, kThreads, Cf::kSmem, c->stream>>>(ta, tb, M, N, K, ep, ksplit, c->sched_counter());
     SGC_LAUNCH_CHECK(c);
 }
 
@@ -650,7 +694,7 @@ void launch2(Ctx* c, const void* A, const void* B, int M, int N, int K, const Ge
     int tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / 256);
     int grid = 2 * tiles < c->num_sms ? 2 * tiles : (c->num_sms & ~1);
     Ctx::Timed timer(c, gemm_timer_name(EPI));
-    kfn<<<grid, kThreads, Cfg2::kSmem, c->stream>>>(ta, tb, M, N, K, ep);
+    kfn<<<grid, kThreads, Cfg2::kSmem, c->stream>>>(ta, tb, M, N, K, ep, c->sched_counter());
     SGC_LAUNCH_CHECK(c);
 }
 
