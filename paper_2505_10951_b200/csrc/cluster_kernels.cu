@@ -95,7 +95,6 @@ __global__ void __launch_bounds__(kAggThreads)
     __shared__ int red_i[32], red_j[32];
     __shared__ int n_rescan;
     __shared__ int s_keep, s_kill;
-    __shared__ double s_best;
 
     const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32, nwarps = blockDim.x / 32;
     for (int i = tid; i < m; i += blockDim.x) {
@@ -109,12 +108,23 @@ __global__ void __launch_bounds__(kAggThreads)
         double bv = INFINITY;
         int bj = 0x7fffffff;
         const double* row = D + static_cast<size_t>(i) * m;
-        for (int j = i + 1 + lane; j < m; j += 32) {
-            if (!alive[j]) continue;
-            double v = row[j];
-            if (better(v, j, bv, bj)) {
-                bv = v;
-                bj = j;
+        // 8 independent L2 loads in flight per lane per round (a rescan was a chain of m/32
+        // dependent round trips); the (value, j) minimum does not depend on the visiting order
+        constexpr int U = 8;
+        for (int j0 = i + 1 + lane; j0 < m; j0 += 32 * U) {
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + 32 * u;
+                v[u] = j < m ? row[j] : INFINITY;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + 32 * u;
+                if (j < m && alive[j] && better(v[u], j, bv, bj)) {
+                    bv = v[u];
+                    bj = j;
+                }
             }
         }
         for (int o = 16; o > 0; o >>= 1) {
@@ -163,19 +173,24 @@ __global__ void __launch_bounds__(kAggThreads)
             red_j[warp] = bj;
         }
         __syncthreads();
-        if (tid == 0) {
-            for (int w = 1; w < nwarps; ++w) {
-                double ov = red_v[w];
-                int oi = red_i[w], oj = red_j[w];
+        if (warp == 0) {
+            bv = lane < nwarps ? red_v[lane] : INFINITY;
+            bi = lane < nwarps ? red_i[lane] : 0x7fffffff;
+            bj = lane < nwarps ? red_j[lane] : 0x7fffffff;
+            for (int o = 16; o > 0; o >>= 1) {
+                double ov = __shfl_xor_sync(0xffffffff, bv, o);
+                int oi = __shfl_xor_sync(0xffffffff, bi, o);
+                int oj = __shfl_xor_sync(0xffffffff, bj, o);
                 if (ov < bv || (ov == bv && (oi < bi || (oi == bi && oj < bj)))) {
                     bv = ov;
                     bi = oi;
                     bj = oj;
                 }
             }
+        }
+        if (tid == 0) {
             s_keep = bi;  // slot index == min member, bi < bj
             s_kill = bj;
-            s_best = bv;
             merge_left[step] = bi;
             merge_right[step] = bj;
             merge_dist[step] = linkage == SGC_WARD ? __ddiv_rn(bv, 2.0)

@@ -329,23 +329,23 @@ void step_tokens(Ctx* c, int32_t* tok, const float* logits, int n, const int8_t*
 namespace {
 // RMSNorm scale of every row from its chunk sums of squares, summed in index order (the scale
 // never depends on which tile or warp produced a chunk): 1 / sqrt(sum / d + 1e-5), lm_core.cpp:26-31
+// one warp per row: lane l sums parts l, l + 32, ... in order, then a fixed xor tree -- the
+// reduction order depends only on n_parts, never on how rows are batched (bit-identical waves)
 __global__ void rms_scale_kernel(float* scale, const float* parts, int rows, int n_parts, int d) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
     if (r >= rows) return;
-    const float4* p4 = reinterpret_cast<const float4*>(parts + static_cast<size_t>(r) * n_parts);
+    const float* pr = parts + static_cast<size_t>(r) * n_parts;
     float ss = 0.f;
-    if (n_parts % 4 == 0) {
-        for (int i = 0; i < n_parts / 4; ++i) {
-            const float4 v = p4[i];
-            ss += v.x;
-            ss += v.y;
-            ss += v.z;
-            ss += v.w;
-        }
+    if (n_parts == 128) {  // d = 4096: one float4 per lane, coalesced
+        const float4 v = reinterpret_cast<const float4*>(pr)[lane];
+        ss = (v.x + v.y) + (v.z + v.w);
     } else {
-        for (int i = 0; i < n_parts; ++i) ss += parts[static_cast<size_t>(r) * n_parts + i];
+        for (int i = lane; i < n_parts; i += 32) ss += pr[i];
     }
-    scale[r] = 1.0f / sqrtf(ss / static_cast<float>(d) + 1e-5f);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) scale[r] = 1.0f / sqrtf(ss / static_cast<float>(d) + 1e-5f);
 }
 __global__ void iota_kernel(int32_t* p, int n) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
@@ -354,7 +354,7 @@ __global__ void iota_kernel(int32_t* p, int n) {
 void rms_scale(Ctx* c, float* scale, const float* parts, int rows, int n_parts, int d) {
     if (rows <= 0) return;
     Ctx::Timed timer(c, "rmsnorm");
-    rms_scale_kernel<<<ceil_div(rows, 256), 256, 0, c->stream>>>(scale, parts, rows, n_parts, d);
+    rms_scale_kernel<<<ceil_div(rows, 8), 256, 0, c->stream>>>(scale, parts, rows, n_parts, d);
     SGC_LAUNCH_CHECK(c);
 }
 int32_t* Ctx::iota(int n) {
