@@ -43,6 +43,9 @@ constexpr int kKStages = 3;
 constexpr int kVStages = 2;
 // SGC_POLY_NUM / SGC_POLY_DEN of the exponential pairs run as a polynomial on the FMA pipe
 // (MUFU.EX2 offload, FA4-style); the rest on MUFU
+#ifndef SGC_ATTN_PINGPONG
+#define SGC_ATTN_PINGPONG 1
+#endif
 #ifndef SGC_POLY_NUM
 #define SGC_POLY_NUM 1
 #define SGC_POLY_DEN 3
@@ -360,6 +363,18 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
         auto tile_sync = [&]() {
             if constexpr (SPLIT > 1) asm volatile("bar.sync %0, %1;" ::"r"(1 + x), "r"(128 * SPLIT) : "memory");
         };
+        // Softmax ping-pong (FA3/FA4-style): while both tiles have block b, the two warpgroups
+        // take turns on the exponentials (A(b), B(b), A(b+1), ...) through named barriers 3/4,
+        // so each runs at the SM's full MUFU/FMA rate while the tensor pipe works on the other
+        // tile's PV + next S, instead of both crawling side by side and stretching the chain
+        // S(b) -> softmax(b) -> PV(b) -> S(b+1) of each tile.
+        constexpr bool kPing = SPLIT == 1 && SGC_ATTN_PINGPONG;
+        auto ping_wait = [&]() {
+            if constexpr (kPing) asm volatile("bar.sync %0, 256;" ::"r"(3 + x) : "memory");
+        };
+        auto ping_pass = [&]() {
+            if constexpr (kPing) asm volatile("bar.arrive %0, 256;" ::"r"(4 - x) : "memory");
+        };
         uint32_t gs = 0, uit = 0;
 #ifdef SGC_ATTN_PROF
         const bool prof_thr = threadIdx.x == 64;
@@ -387,6 +402,9 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
             const bool valid = r < u.nrows[x];
             const int row = w.row0 + x * BQ + r;
             const int seg = valid && !p.part_o ? p.seg_lo[row] : 0x7fffffff;
+            // blocks both tiles have take turns; tile B hands tile A the first turn
+            const int n_ping = min(u.nb[0], u.nb[1]);
+            if (x == 1 && n_ping > 0) ping_pass();
             float m = -INFINITY, l = 0.f;
             for (int b = 0; b < nb; ++b, ++gs) {
                 SPROF(0);
@@ -454,6 +472,9 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                     bmax *= sc;  // scaled-log2 units
                 }
                 SPROF(8);
+                // the turn covers the MUFU-heavy exponentials only: the S load and the max of one
+                // tile overlap the other tile's exponentials
+                if (b < n_ping) ping_wait();
                 const float mnew = (m == -INFINITY || bmax > m + 8.f) ? bmax : m;
                 const float nm = mnew == -INFINITY ? 0.f : -mnew;
                 float rs;
@@ -488,6 +509,8 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                     f2unpack(fadd2(fadd2(r0, r1), fadd2(r2, r3)), x0, x1);
                     rs = x0 + x1;
                 }
+                // A always passes the turn on; B only while A has another shared block
+                if (b < n_ping && (x == 0 || b + 1 < n_ping)) ping_pass();
                 SPROF(2);
                 float alpha = 1.f;
                 // the rescale is a per-row decision, but tcgen05.ld/st are .sync.aligned: the
