@@ -59,7 +59,7 @@ struct TcCfg {
     static constexpr int kVBytes = BKV * HD * 2;
     // + barriers (256 B) + the split-softmax exchange slots [2][2][BQ] fp32
     // + barriers (256 B) + the split-softmax exchange slots [2][2][BQ] fp32 + the item ring
-    static constexpr int kSmem = 2 * kQBytes + kKStages * kKBytes + kVStages * kVBytes + 256 + 2 * 2 * BQ * 4 + 128;
+    static constexpr int kSmem = 2 * kQBytes + kKStages * kKBytes + kVStages * kVBytes + 256 + 2 * 2 * BQ * 4 + 128 + 256;
     static constexpr uint32_t kTmemCols = 512;
     static constexpr uint32_t kS = 0;    // S_X at column X * 128
     static constexpr uint32_t kO = 256;  // O_X at column 256 + X * 128
@@ -85,6 +85,12 @@ struct TcParams {
     uint32_t* sched;  // dynamic item counter (sched.cuh)
 };
 using ItemRing = UnitRing<4>;
+// what the producer resolved for a claimed item (published with the ring slot, so the MMA and
+// softmax warps start an item from shared memory instead of two dependent global loads)
+struct ItemInfo {
+    AttnWork w;
+    int nA, nb0, nb1, nrows0, nrows1, loc_first;
+};
 
 __device__ __forceinline__ float ex2_approx(float x) {
     float y;
@@ -179,7 +185,7 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                    const __grid_constant__ CUtensorMap tmVp, const __grid_constant__ CUtensorMap tmKl,
                    const __grid_constant__ CUtensorMap tmVl, TcParams p) {
     using C = TcCfg<HD>;
-    static_assert(sizeof(ItemRing) <= 128, "item ring");
+    static_assert(sizeof(ItemRing) <= 128 && 4 * sizeof(ItemInfo) <= 256, "item ring");
     // all shared memory is dynamic (no static arrays), so the base is 1024-byte aligned
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sQ = smem;                                  // [2][BQ x HD]
@@ -199,9 +205,25 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
     float* xm = reinterpret_cast<float*>(bars + 32);  // [2 tiles][SPLIT][BQ] row max / sum exchange
     // items (unit x head) claimed by the producer and handed to the MMA and softmax warps
     ItemRing* ring = reinterpret_cast<ItemRing*>(xm + 2 * 2 * BQ);
+    ItemInfo* info = reinterpret_cast<ItemInfo*>(reinterpret_cast<uint8_t*>(ring) + 128);  // [4] per slot
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const int n_items = p.n_work * p.heads;
+    // consumer side: item k's slot -> (item, work, plan) in registers, then release the slot
+    auto take_item = [&](uint32_t k, AttnWork& w, UnitPlan& u) -> uint32_t {
+        const uint32_t iu = sched::wait(ring, k);
+        if (iu < static_cast<uint32_t>(n_items)) {
+            const ItemInfo& f = info[k % 4];
+            w = f.w;
+            u.nA = f.nA;
+            u.nb[0] = f.nb0;
+            u.nb[1] = f.nb1;
+            u.nrows[0] = f.nrows0;
+            u.nrows[1] = f.nrows1;
+            u.loc_first = f.loc_first;
+        }
+        return iu;
+    };
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmQ);
@@ -236,12 +258,21 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
         if (lane == 0) {
             uint32_t g = 0, qit[2] = {0, 0};
             for (uint32_t k = 0;; ++k) {
-                const uint32_t iu = sched::publish(ring, k, p.sched, n_items, gridDim.x);
+                // claim, resolve the item's plan, publish it with the slot
+                const int sl = k % 4;
+                ptx::mbar_wait(&ring->empty[sl], ((k / 4) & 1) ^ 1);
+                const uint32_t iu = sched::claim(p.sched, n_items, gridDim.x, k);
+                ring->unit[sl] = iu;
+                AttnWork w{};
+                UnitPlan u{};
+                if (iu < static_cast<uint32_t>(n_items)) {
+                    w = p.work[iu % p.n_work];
+                    u = plan_unit(w, p.seg_lo, p.part_o != nullptr);
+                    info[sl] = ItemInfo{w, u.nA, u.nb[0], u.nb[1], u.nrows[0], u.nrows[1], u.loc_first};
+                }
+                ptx::mbar_arrive(&ring->full[sl]);
                 if (iu >= static_cast<uint32_t>(n_items)) break;
-                const int item = static_cast<int>(iu);
-                const int h = item / p.n_work;
-                const AttnWork w = p.work[item % p.n_work];
-                const UnitPlan u = plan_unit(w, p.seg_lo, p.part_o != nullptr);
+                const int h = static_cast<int>(iu) / p.n_work;
 #pragma unroll
                 for (int x = 0; x < 2; ++x) {
                     if (!u.nb[x]) continue;
@@ -303,11 +334,11 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 ++gx[x];
             };
             for (uint32_t k = 0;; ++k) {
-                const uint32_t iu = sched::wait(ring, k);
+                AttnWork w;
+                UnitPlan u;
+                const uint32_t iu = take_item(k, w, u);
                 sched::release(ring, k);
                 if (iu >= static_cast<uint32_t>(n_items)) break;
-                const AttnWork w = p.work[iu % p.n_work];
-                const UnitPlan u = plan_unit(w, p.seg_lo, p.part_o != nullptr);
                 const int nbu = max(u.nb[0], u.nb[1]);
                 for (int x = 0; x < 2; ++x)
                     if (u.nb[x]) ptx::mbar_wait(&q_full[x], qit[x] & 1);
@@ -389,14 +420,14 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
 #define SPROF(slot)
 #endif
         for (uint32_t k = 0;; ++k) {
-            const uint32_t iu = sched::wait(ring, k);
+            AttnWork w;
+            UnitPlan u;
+            const uint32_t iu = take_item(k, w, u);
             __syncwarp();
             if (lane == 0) sched::release(ring, k);
             if (iu >= static_cast<uint32_t>(n_items)) break;
             const int item = static_cast<int>(iu);
             const int h = item / p.n_work;
-            const AttnWork w = p.work[item % p.n_work];
-            const UnitPlan u = plan_unit(w, p.seg_lo, p.part_o != nullptr);
             const int nb = u.nb[x];
             if (!nb) continue;
             const bool valid = r < u.nrows[x];
@@ -488,11 +519,10 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                                  xa, xc);
                         float a, cc;
                         if ((j % SGC_POLY_DEN) < SGC_POLY_NUM) {  // share of exponentials on the FMA pipe
+                            // a masked key (-inf) comes out as 2^-125 instead of 0: < 1e-37 of the
+                            // row sum (>= 1), below every fp32 ulp of l and O -- not worth the
+                            // predicated selects in the hot loop
                             ex2_poly2(xa, xc, a, cc);
-                            if (!full) {  // the polynomial maps -inf to 2^-125: zero masked keys
-                                if (!(vw[(2 * j) / 32] & (1u << ((2 * j) % 32)))) a = 0.f;
-                                if (!(vw[(2 * j + 1) / 32] & (1u << ((2 * j + 1) % 32)))) cc = 0.f;
-                            }
                         } else {
                             a = ex2_approx(xa);
                             cc = ex2_approx(xc);
