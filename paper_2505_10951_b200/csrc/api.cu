@@ -1912,6 +1912,9 @@ uint64_t sgc_kv_digest(const sgc_kv* kv, uint32_t i) {
     uint64_t h = 0xcbf29ce484222325ULL;
     try {
         Ctx* c = kv->model->c;
+        // the KV was written on the context's non-blocking stream: a plain cudaMemcpy does not
+        // order after it
+        SGC_CUDA_CHECK(cudaStreamSynchronize(c->stream));
         const size_t d = kv->model->d, n = kv->len[i] * d;
         std::vector<bf16> buf(n);
         for (int l = 0; l < kv->model->L; ++l) {
@@ -1936,6 +1939,7 @@ uint64_t sgc_kv_digest(const sgc_kv* kv, uint32_t i) {
 int sgc_kv_read(const sgc_kv* kv, uint32_t i, uint32_t layer, int is_v, float* out) {
     return guarded([&] {
         if (i >= kv->n || layer >= static_cast<uint32_t>(kv->model->L)) fail(SGC_DOMAIN, "kv_read: out of range");
+        SGC_CUDA_CHECK(cudaStreamSynchronize(kv->model->c->stream));  // see sgc_kv_digest
         const size_t d = kv->model->d, n = kv->len[i] * d;
         std::vector<bf16> buf(n);
         const bf16* src = (is_v ? kv->v_layer(layer) : kv->k_layer(layer)) + kv->off[i] * d;

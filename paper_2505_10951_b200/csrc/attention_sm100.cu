@@ -43,6 +43,11 @@ constexpr int kKStages = 3;
 constexpr int kVStages = 2;
 // SGC_POLY_NUM / SGC_POLY_DEN of the exponential pairs run as a polynomial on the FMA pipe
 // (MUFU.EX2 offload, FA4-style); the rest on MUFU
+// the row's reference max only moves when a block max exceeds it by more than this (log2
+// units): P <= 2^SGC_LAZY_MAX in bf16 (same relative precision at any scale), O rescales rare
+#ifndef SGC_LAZY_MAX
+#define SGC_LAZY_MAX 8.f
+#endif
 #ifndef SGC_ATTN_PINGPONG
 #define SGC_ATTN_PINGPONG 1
 #endif
@@ -258,7 +263,8 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
         if (lane == 0) {
             uint32_t g = 0, qit[2] = {0, 0};
             for (uint32_t k = 0;; ++k) {
-                // claim, resolve the item's plan, publish it with the slot
+                // claim (when the slot frees: items are long, claiming ahead would only skew the
+                // tail), resolve the item's plan, publish it with the slot
                 const int sl = k % 4;
                 ptx::mbar_wait(&ring->empty[sl], ((k / 4) & 1) ^ 1);
                 const uint32_t iu = sched::claim(p.sched, n_items, gridDim.x, k);
@@ -506,7 +512,7 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 // the turn covers the MUFU-heavy exponentials only: the S load and the max of one
                 // tile overlap the other tile's exponentials
                 if (b < n_ping) ping_wait();
-                const float mnew = (m == -INFINITY || bmax > m + 8.f) ? bmax : m;
+                const float mnew = (m == -INFINITY || bmax > m + SGC_LAZY_MAX) ? bmax : m;
                 const float nm = mnew == -INFINITY ? 0.f : -mnew;
                 float rs;
                 {
@@ -887,7 +893,7 @@ __global__ void __launch_bounds__(320, 1)
                     }
                     bmax = fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)) * sc;
                 }
-                const float mnew = (m == -INFINITY || bmax > m + 8.f) ? bmax : m;
+                const float mnew = (m == -INFINITY || bmax > m + SGC_LAZY_MAX) ? bmax : m;
                 const float nm = mnew == -INFINITY ? 0.f : -mnew;
                 float rs;
                 {

@@ -387,9 +387,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             // operands are re-read across the raster group's tiles: keep them in L2 ahead of the
             // streamed epilogue outputs
             const uint64_t keep = ptx::policy_evict_last();
+            uint32_t next = sched::claim(sched_ctr, num_tiles, gridDim.x, 0);
             for (uint32_t k = 0;; ++k) {
-                const uint32_t tu = sched::publish(ring, k, sched_ctr, num_tiles, gridDim.x);
+                const uint32_t tu = next;
+                sched::publish(ring, k, tu);
                 if (tu >= static_cast<uint32_t>(num_tiles)) break;
+                next = sched::claim(sched_ctr, num_tiles, gridDim.x, k + 1);
                 const int t = static_cast<int>(tu);
                 int m0, n0;
                 tile_coords(t, m0, n0);
@@ -558,10 +561,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             const uint64_t keep = ptx::policy_evict_last();  // operands re-read across the group
+            uint32_t next = leader ? sched::claim(sched_ctr, num_tiles, npairs, 0) : 0;
             for (uint32_t k = 0;; ++k) {
                 uint32_t tu;
                 if (leader) {
-                    tu = sched::publish_pair(ring, k, sched_ctr, num_tiles, npairs);
+                    tu = next;
+                    sched::publish_pair(ring, k, tu);
+                    if (tu < static_cast<uint32_t>(num_tiles)) next = sched::claim(sched_ctr, num_tiles, npairs, k + 1);
                 } else {
                     tu = sched::wait_remote(ring, k);
                     sched::release_to(ring, k, 0);

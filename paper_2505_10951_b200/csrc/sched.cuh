@@ -59,31 +59,27 @@ __device__ __forceinline__ void init(UnitRing<R>* r, uint32_t consumers) {
     }
 }
 
-// fetcher, k-th claim of this CTA: wait for the slot, claim, publish (one thread)
+// fetcher: publish unit t (claimed ahead: the next claim's atomic round trip overlaps the
+// current unit's loads instead of stalling the operand pipeline at every unit boundary) as the
+// k-th unit of this CTA (one thread)
 template <int R>
-__device__ __forceinline__ uint32_t publish(UnitRing<R>* r, uint32_t k, uint32_t* ctr, uint32_t n_units,
-                                            uint32_t n_fetchers) {
+__device__ __forceinline__ void publish(UnitRing<R>* r, uint32_t k, uint32_t t) {
     const int s = k % R;
     ptx::mbar_wait(&r->empty[s], ((k / R) & 1) ^ 1);
-    const uint32_t t = claim(ctr, n_units, n_fetchers, k);
     r->unit[s] = t;
     ptx::mbar_arrive(&r->full[s]);
-    return t;
 }
 
 // CTA-pair leader's fetcher: also writes the peer's (rank 1) ring; the slot's empty barrier
 // collects the peer's consumers too, so its wait acquires at cluster scope
 template <int R>
-__device__ __forceinline__ uint32_t publish_pair(UnitRing<R>* r, uint32_t k, uint32_t* ctr, uint32_t n_units,
-                                                 uint32_t n_fetchers) {
+__device__ __forceinline__ void publish_pair(UnitRing<R>* r, uint32_t k, uint32_t t) {
     const int s = k % R;
     ptx::mbar_wait_cluster(&r->empty[s], ((k / R) & 1) ^ 1);
-    const uint32_t t = claim(ctr, n_units, n_fetchers, k);
     r->unit[s] = t;
     ptx::st_cluster_u32(&r->unit[s], 1, t);
     ptx::mbar_arrive(&r->full[s]);
     ptx::mbar_arrive_cluster(&r->full[s], 1);
-    return t;
 }
 
 // consumer: the k-th unit (every thread that calls it gets the value)
