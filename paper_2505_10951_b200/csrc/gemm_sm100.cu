@@ -246,6 +246,9 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
             return;
         }
         float ss = 0.f;  // EPI_RESID with out_ss: this row's partial sum of squares of x_new
+        // the fp32 residual stream is read and written once per launch: evict_first keeps it from
+        // pushing the raster group's operand tiles out of L2
+        const uint64_t resid_pol = ptx::policy_evict_first();
         const int lane = threadIdx.x & 31;
         const int row0 = row - lane;    // the warp's first row
         const int half = lane >> 4;     // row parity handled by this lane
@@ -259,8 +262,9 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
                     const int gr = row0 + 2 * i + half;
-                    xo[i] = gr < ep_rows ? *reinterpret_cast<const float2*>(static_cast<const float*>(ep.out) +
-                                                                            static_cast<size_t>(gr) * ep.ldo + col)
+                    xo[i] = gr < ep_rows ? ptx::ld_global_f2_hint(static_cast<const float*>(ep.out) +
+                                                                      static_cast<size_t>(gr) * ep.ldo + col,
+                                                                  resid_pol)
                                          : make_float2(0.f, 0.f);
                 }
             }
@@ -291,10 +295,11 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                     stage[lr * 33 + c2 + 1] = val.y;
                 }
                 if (gr < ep_rows) {
-                    if constexpr (EPI == EPI_RESID || EPI == EPI_F32) {
+                    if constexpr (EPI == EPI_RESID) {
+                        ptx::st_global_f2_hint(static_cast<float*>(ep.out) + off, val, resid_pol);
+                        if (ep.out_xb) *reinterpret_cast<__nv_bfloat162*>(ep.out_xb + off) = __floats2bfloat162_rn(val.x, val.y);
+                    } else if constexpr (EPI == EPI_F32) {
                         *reinterpret_cast<float2*>(static_cast<float*>(ep.out) + off) = val;
-                        if constexpr (EPI == EPI_RESID)
-                            if (ep.out_xb) *reinterpret_cast<__nv_bfloat162*>(ep.out_xb + off) = __floats2bfloat162_rn(val.x, val.y);
                     } else {
                         *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(ep.out) + off) =
                             __floats2bfloat162_rn(val.x, val.y);
@@ -521,7 +526,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int num_kb = K / BK;
     // pair-tiles of 256 rows per raster group: the group's A rows (GROUP x 256 x K bf16) stay
     // L2-resident (~48 MB) while the group sweeps every n-tile; larger K -> smaller group
-    const int GROUP = max(2, min(32, (48 << 20) / (2 * BM * K * 2)));
+#ifndef SGC_RESID_GROUP_MB
+#define SGC_RESID_GROUP_MB 48
+#endif
+    constexpr int kGroupBytes = (EPI == EPI_RESID ? SGC_RESID_GROUP_MB : 48) << 20;
+    const int GROUP = max(2, min(32, kGroupBytes / (2 * BM * K * 2)));
 
     if (warp == 0 && lane == 0) {
         ptx::tma_prefetch_desc(&tmA);
