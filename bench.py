@@ -258,6 +258,22 @@ def run_ours(args, rank, world, local_rank):
         ctx.set_timing(False)
         g_ms = ev4.elapsed_time(ev5) / args.gen_steps
         rt_all = np.concatenate(rts)
+        # decode-step GEMMs stream every weight once per step (few rows): HBM roofline of the
+        # decode GEMM time (generation batch minus its first-token pass, timed above per step)
+        fams = ("gemm_qkv", "gemm_resid", "gemm_tanh")
+        dec_gemm_ms = sum(gkt[k][0] / args.gen_steps - kt[k][0] / args.steps for k in fams)
+        L_ = w.lm["layers"]
+        dec_steps = (gkt["gemm_qkv"][1] / args.gen_steps - kt["gemm_qkv"][1] / args.steps) / L_
+        w_bytes = L_ * 2 * (4 * d * d + 2 * d * w.lm["ffn_hidden"])
+        dec_roof = None
+        pk_gen, _ = load_peaks()
+        if dec_steps > 0 and dec_gemm_ms > 0:
+            ach = dec_steps * w_bytes / (dec_gemm_ms / 1e3) / 1e9
+            dec_roof = {"bound": "hbm", "kernel": "decode-step GEMMs (weights streamed once per step)",
+                        "decode_steps_per_batch": round(dec_steps, 1), "weight_bytes_per_step": w_bytes,
+                        "gemm_ms_per_batch": round(dec_gemm_ms, 3), "achieved": round(ach, 1),
+                        "peak": pk_gen.get("hbm_gbs"), "unit": "GB/s",
+                        "frac": round(ach / pk_gen["hbm_gbs"], 3) if pk_gen.get("hbm_gbs") else None}
         gen = {"max_new_tokens": mx, "ms_per_batch": round(g_ms, 3),
                "queries_per_s_to_last_token": round(m / (g_ms / 1e3), 3),
                "rt_p50_ms": round(float(np.percentile(rt_all[rt_all >= 0], 50)), 3),
@@ -266,6 +282,8 @@ def run_ours(args, rank, world, local_rank):
                "decode_stage_ms": round(dec_ms / args.gen_steps, 3),
                "decode_rows_per_batch": dec_rows // args.gen_steps,
                "kernel_ms_per_batch": {k: round(v[0] / args.gen_steps, 3) for k, v in gkt.items() if v[1]},
+               "kernel_launches_per_batch": {k: v[1] // args.gen_steps for k, v in gkt.items() if v[1]},
+               "decode_roofline": dec_roof,
                "steps": args.gen_steps,
                "semantics": "same batch to EOS / max_new (run() with ToyLmConfig::max_new_tokens); "
                             "rt = submission -> last token"}
