@@ -40,7 +40,7 @@ def main(path):
         t[1] += 1
     total = sum(v[0] for v in step.values())
     print("# ncu --metrics gpu__time_duration.sum --clock-control none -- bench.py --config c3 --steps 1 --warmup 0 --no-gen")
-    print("# (4 cluster waves). Serialized, cold-cache per-launch timings: compare SHARES, not absolutes.")
+    print("# (2 cluster waves, the bench default). Serialized, cold-cache per-launch timings: compare SHARES, not absolutes.")
     print("       ms launches  share  kernel")
     for k, (ms, n) in sorted(step.items(), key=lambda kv: -kv[1][0]):
         note = NOTES.get(k)
