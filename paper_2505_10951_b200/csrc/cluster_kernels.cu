@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kAggThreads)
     }
     __syncthreads();
 
-    auto scan_row = [&](int i) {  // warp-cooperative: min over alive j > i of (D[i][j], j)
+    auto scan_row = [&](int i, int skip) {  // warp-cooperative: min over alive j > i, j != skip
         double bv = INFINITY;
         int bj = 0x7fffffff;
         const double* row = D + static_cast<size_t>(i) * m;
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kAggThreads)
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int j = j0 + 32 * u;
-                if (j < m && alive[j] && better(v[u], j, bv, bj)) {
+                if (j < m && j != skip && alive[j] && better(v[u], j, bv, bj)) {
                     bv = v[u];
                     bj = j;
                 }
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kAggThreads)
             rj[i] = bj;
         }
     };
-    for (int i = warp; i < m; i += nwarps) scan_row(i);
+    for (int i = warp; i < m; i += nwarps) scan_row(i, -1);
     __syncthreads();
 
     const int steps = m - c;
@@ -204,63 +204,62 @@ __global__ void __launch_bounds__(kAggThreads)
         double* Dk = D + static_cast<size_t>(keep) * m;
         const double* Dl = D + static_cast<size_t>(kill) * m;
         const double dab = Dk[kill];
-        // ---- Lance-Williams update (clustering.cpp:128-148), same operand order, no FMA
+        // ---- one pass per k: Lance-Williams update (clustering.cpp:128-148, same operand order,
+        // no FMA), owner relabel, and row k's cached minimum against its new D[k][keep] (the
+        // value this thread just computed); rows whose cached argmin was keep / kill are rescanned
         for (int k = tid; k < m; k += blockDim.x) {
-            if (!alive[k] || k == keep || k == kill) continue;
-            const double dak = Dk[k], dbk = Dl[k];
-            const double nk = size[k];
-            double v;
-            switch (linkage) {
-                case SGC_SINGLE: v = dak < dbk ? dak : dbk; break;
-                case SGC_COMPLETE: v = dak > dbk ? dak : dbk; break;
-                case SGC_AVERAGE:
-                    v = __ddiv_rn(__dadd_rn(__dmul_rn(na, dak), __dmul_rn(nb, dbk)), __dadd_rn(na, nb));
-                    break;
-                case SGC_CENTROID: {
-                    double s = __dadd_rn(na, nb);
-                    double t1 = __ddiv_rn(__dadd_rn(__dmul_rn(na, dak), __dmul_rn(nb, dbk)), s);
-                    double t2 = __ddiv_rn(__dmul_rn(__dmul_rn(na, nb), dab), __dmul_rn(s, s));
-                    v = __dsub_rn(t1, t2);
-                    break;
+            if (owner[k] == kill) owner[k] = keep;
+            if (!alive[k] || k == kill) continue;
+            double v = 0.0;
+            if (k != keep) {
+                const double dak = Dk[k], dbk = Dl[k];
+                const double nk = size[k];
+                switch (linkage) {
+                    case SGC_SINGLE: v = dak < dbk ? dak : dbk; break;
+                    case SGC_COMPLETE: v = dak > dbk ? dak : dbk; break;
+                    case SGC_AVERAGE:
+                        v = __ddiv_rn(__dadd_rn(__dmul_rn(na, dak), __dmul_rn(nb, dbk)), __dadd_rn(na, nb));
+                        break;
+                    case SGC_CENTROID: {
+                        double s = __dadd_rn(na, nb);
+                        double t1 = __ddiv_rn(__dadd_rn(__dmul_rn(na, dak), __dmul_rn(nb, dbk)), s);
+                        double t2 = __ddiv_rn(__dmul_rn(__dmul_rn(na, nb), dab), __dmul_rn(s, s));
+                        v = __dsub_rn(t1, t2);
+                        break;
+                    }
+                    default: {  // ward
+                        double t = __dadd_rn(__dmul_rn(__dadd_rn(na, nk), dak), __dmul_rn(__dadd_rn(nb, nk), dbk));
+                        t = __dsub_rn(t, __dmul_rn(nk, dab));
+                        v = __ddiv_rn(t, __dadd_rn(__dadd_rn(na, nb), nk));
+                    }
                 }
-                default: {  // ward
-                    double t = __dadd_rn(__dmul_rn(__dadd_rn(na, nk), dak), __dmul_rn(__dadd_rn(nb, nk), dbk));
-                    t = __dsub_rn(t, __dmul_rn(nk, dab));
-                    v = __ddiv_rn(t, __dadd_rn(__dadd_rn(na, nb), nk));
-                }
+                Dk[k] = v;
+                D[static_cast<size_t>(k) * m + keep] = v;
             }
-            Dk[k] = v;
-            D[static_cast<size_t>(k) * m + keep] = v;
+            // row-min maintenance of row k (rows > kill never cached keep or kill)
+            if (k < kill) {
+                bool need = false;
+                if (k == keep) need = true;
+                else if (rj[k] == kill) need = true;
+                else if (k < keep) {
+                    if (rj[k] == keep) need = true;
+                    else if (better(v, keep, rv[k], rj[k])) {
+                        rv[k] = v;
+                        rj[k] = keep;
+                    }
+                }
+                if (need) rescan[atomicAdd(&n_rescan, 1)] = k;
+            }
         }
         __syncthreads();
+        // rescans skip `kill` explicitly: thread 0 retires it concurrently (read again only after
+        // the closing barrier)
         if (tid == 0) {
             alive[kill] = 0;
             size[keep] += size[kill];
         }
-        for (int p = tid; p < m; p += blockDim.x)
-            if (owner[p] == kill) owner[p] = keep;
-        __syncthreads();
-        // ---- row-min maintenance
-        for (int i = tid; i < kill; i += blockDim.x) {
-            if (!alive[i]) continue;
-            bool need = false;
-            if (i == keep) need = true;
-            else if (rj[i] == kill) need = true;
-            else if (i < keep) {
-                if (rj[i] == keep) need = true;
-                else {
-                    double v = D[static_cast<size_t>(i) * m + keep];
-                    if (better(v, keep, rv[i], rj[i])) {
-                        rv[i] = v;
-                        rj[i] = keep;
-                    }
-                }
-            }
-            if (need) rescan[atomicAdd(&n_rescan, 1)] = i;
-        }
-        __syncthreads();
         const int nr = n_rescan;
-        for (int r = warp; r < nr; r += nwarps) scan_row(rescan[r]);
+        for (int r = warp; r < nr; r += nwarps) scan_row(rescan[r], kill);
         __syncthreads();
     }
     // ---- labels by ascending min member (clustering.cpp:162-172): alive slot i == min member
