@@ -95,6 +95,9 @@ __global__ void __launch_bounds__(kAggThreads)
     __shared__ int red_i[32], red_j[32];
     __shared__ int n_rescan;
     __shared__ int s_keep, s_kill;
+    constexpr int kRescanRows = kAggThreads / 32 / 8;  // rows rescanned 8 warps each
+    __shared__ double part_v[kAggThreads / 32];
+    __shared__ int part_j[kAggThreads / 32];
 
     const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32, nwarps = blockDim.x / 32;
     for (int i = tid; i < m; i += blockDim.x) {
@@ -104,24 +107,26 @@ __global__ void __launch_bounds__(kAggThreads)
     }
     __syncthreads();
 
-    auto scan_row = [&](int i, int skip) {  // warp-cooperative: min over alive j > i, j != skip
-        double bv = INFINITY;
-        int bj = 0x7fffffff;
+    // warp-cooperative min over alive j in [j_lo, j_hi), j != skip, of (D[i][j], j); every lane
+    // returns the result. 8 independent L2 loads in flight per lane per round (a rescan was a
+    // chain of m/32 dependent round trips); the (value, j) minimum does not depend on the
+    // visiting order
+    auto scan_range = [&](int i, int j_lo, int j_hi, int skip, double& bv, int& bj) {
+        bv = INFINITY;
+        bj = 0x7fffffff;
         const double* row = D + static_cast<size_t>(i) * m;
-        // 8 independent L2 loads in flight per lane per round (a rescan was a chain of m/32
-        // dependent round trips); the (value, j) minimum does not depend on the visiting order
         constexpr int U = 8;
-        for (int j0 = i + 1 + lane; j0 < m; j0 += 32 * U) {
+        for (int j0 = j_lo + lane; j0 < j_hi; j0 += 32 * U) {
             double v[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int j = j0 + 32 * u;
-                v[u] = j < m ? row[j] : INFINITY;
+                v[u] = j < j_hi ? row[j] : INFINITY;
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int j = j0 + 32 * u;
-                if (j < m && j != skip && alive[j] && better(v[u], j, bv, bj)) {
+                if (j < j_hi && j != skip && alive[j] && better(v[u], j, bv, bj)) {
                     bv = v[u];
                     bj = j;
                 }
@@ -135,6 +140,11 @@ __global__ void __launch_bounds__(kAggThreads)
                 bj = oj;
             }
         }
+    };
+    auto scan_row = [&](int i, int skip) {
+        double bv;
+        int bj;
+        scan_range(i, i + 1, m, skip, bv, bj);
         if (lane == 0) {
             rv[i] = bv;
             rj[i] = bj;
@@ -259,7 +269,37 @@ __global__ void __launch_bounds__(kAggThreads)
             size[keep] += size[kill];
         }
         const int nr = n_rescan;
-        for (int r = warp; r < nr; r += nwarps) scan_row(rescan[r], kill);
+        if (nr <= kRescanRows) {
+            // few rows (the common case): 8 warps per row, one contiguous j segment each, then one
+            // thread per row merges the 8 partial minima -- one L2 round trip instead of m/256
+            const int rr = warp / 8, sg = warp % 8;
+            if (rr < nr) {
+                const int i = rescan[rr];
+                const int len = m - i - 1, seg_len = (len + 7) / 8;
+                const int lo = i + 1 + sg * seg_len, hi = min(m, lo + seg_len);
+                double pv;
+                int pj;
+                scan_range(i, lo, hi, kill, pv, pj);
+                if (lane == 0) {
+                    part_v[warp] = pv;
+                    part_j[warp] = pj;
+                }
+            }
+            __syncthreads();
+            if (tid < nr) {
+                double bv2 = INFINITY;
+                int bj2 = 0x7fffffff;
+                for (int q = 0; q < 8; ++q)
+                    if (better(part_v[tid * 8 + q], part_j[tid * 8 + q], bv2, bj2)) {
+                        bv2 = part_v[tid * 8 + q];
+                        bj2 = part_j[tid * 8 + q];
+                    }
+                rv[rescan[tid]] = bv2;
+                rj[rescan[tid]] = bj2;
+            }
+        } else {
+            for (int r = warp; r < nr; r += nwarps) scan_row(rescan[r], kill);
+        }
         __syncthreads();
     }
     // ---- labels by ascending min member (clustering.cpp:162-172): alive slot i == min member
