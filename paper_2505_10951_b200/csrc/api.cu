@@ -273,6 +273,11 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
         e.d = d;
         e.hd = m->hd;
         sgc::gemm_bf16(c, xb, m->wqkv[l], M, 3 * d, d, e);
+        // last layer: K/V of every row are written now; the rest of the layer only feeds the
+        // head, so rows without logits skip it (values nothing reads: a prefill without logits
+        // stops here, an extend finishes only its members' last rows; decode rows all need logits)
+        const bool last = l == m->L - 1;
+        if (last && !b.dec && b.n_logits == 0) break;
 
         sgc::AttnParams ap;
         ap.q = q;
@@ -334,6 +339,35 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
         r.out_xb = xb;
         r.out_ss = ss_b;
         r.splitk_ok = b.dec != nullptr;
+        if (last && !b.dec && b.n_logits < M) {
+            // the rows the head reads, compacted (per-row GEMM results are independent of M)
+            const int n = b.n_logits;
+            float* cx = c->buf<float>("fwd_cx", static_cast<size_t>(n) * d);
+            bf16* cao = c->buf<bf16>("fwd_cao", static_cast<size_t>(n) * d);
+            bf16* cxb = c->buf<bf16>("fwd_cxb", static_cast<size_t>(n) * d);
+            bf16* ch = c->buf<bf16>("fwd_ch", static_cast<size_t>(n) * m->ffn);
+            float* css = c->buf<float>("fwd_css", static_cast<size_t>(n) * parts);
+            float* crs = c->buf<float>("fwd_crs", n);
+            sgc::gather_rows(c, cx, x, b.d_logit_rows, n, static_cast<size_t>(d) * sizeof(float));
+            sgc::gather_rows(c, cao, ao, b.d_logit_rows, n, static_cast<size_t>(d) * sizeof(bf16));
+            r.out = cx;
+            r.out_xb = cxb;
+            r.out_ss = css;
+            sgc::gemm_bf16(c, cao, m->wo[l], n, d, d, r);
+            sgc::GemmEpi t;
+            t.mode = sgc::EPI_TANH;
+            t.out = ch;
+            t.ldo = m->ffn;
+            sgc::rms_scale(c, crs, css, n, parts, d);
+            t.row_scale = crs;
+            sgc::gemm_bf16(c, cxb, m->w1[l], n, m->ffn, d, t);
+            r.out_xb = nullptr;  // no next layer
+            r.out_ss = nullptr;
+            sgc::gemm_bf16(c, ch, m->w2[l], n, d, m->ffn, r);
+            sgc::head_logits(c, b.d_logits, cx, c->iota(n), n, m->head_t, d);
+            c->flag_readback(bad);
+            return;
+        }
         sgc::gemm_bf16(c, ao, m->wo[l], M, d, d, r);
 
         sgc::GemmEpi t;
@@ -343,7 +377,8 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
         sgc::rms_scale(c, rs, ss_b, M, parts, d);
         t.row_scale = rs;
         sgc::gemm_bf16(c, xb, m->w1[l], M, m->ffn, d, t);
-        r.out_ss = ss_a;  // the next layer's QKV input
+        r.out_ss = last ? nullptr : ss_a;  // the next layer's QKV input
+        if (last) r.out_xb = nullptr;
         sgc::gemm_bf16(c, h, m->w2[l], M, d, m->ffn, r);
     }
     sgc::head_logits(c, b.d_logits, x, b.d_logit_rows, b.n_logits, m->head_t, d);
@@ -470,10 +505,11 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
     b.k_loc = [kvp](int l) { return kvp->k_layer(l); };
     b.v_loc = [kvp](int l) { return kvp->v_layer(l); };
     b.d_logit_rows = d_lr;
-    b.n_logits = static_cast<int>(count);
-    b.d_logits = d_logits;
+    // no logits requested (a representative's prompt): the last layer stops after its K/V
+    b.n_logits = last_logits ? static_cast<int>(count) : 0;
+    b.d_logits = last_logits ? d_logits : nullptr;
     forward_rows(c, m, b);
-    sgc::copy_out(c, last_logits, d_logits, static_cast<size_t>(count) * SGC_VOCAB);
+    if (last_logits) sgc::copy_out(c, last_logits, d_logits, static_cast<size_t>(count) * SGC_VOCAB);
     if (sync) {  // else: the caller syncs (last_logits must then be pinned or null)
         c->sync();
         check_forward_flags(c);

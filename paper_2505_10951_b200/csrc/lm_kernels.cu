@@ -347,6 +347,11 @@ __global__ void rms_scale_kernel(float* scale, const float* parts, int rows, int
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     if (lane == 0) scale[r] = 1.0f / sqrtf(ss / static_cast<float>(d) + 1e-5f);
 }
+__global__ void gather_rows_kernel(uint4* dst, const uint4* src, const int32_t* rows, size_t row_vecs) {
+    const uint4* s = src + static_cast<size_t>(rows[blockIdx.x]) * row_vecs;
+    uint4* o = dst + static_cast<size_t>(blockIdx.x) * row_vecs;
+    for (size_t k = threadIdx.x; k < row_vecs; k += blockDim.x) o[k] = s[k];
+}
 __global__ void iota_kernel(int32_t* p, int n) {
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = i;
 }
@@ -355,6 +360,13 @@ void rms_scale(Ctx* c, float* scale, const float* parts, int rows, int n_parts, 
     if (rows <= 0) return;
     Ctx::Timed timer(c, "rmsnorm");
     rms_scale_kernel<<<ceil_div(rows, 8), 256, 0, c->stream>>>(scale, parts, rows, n_parts, d);
+    SGC_LAUNCH_CHECK(c);
+}
+void gather_rows(Ctx* c, void* dst, const void* src, const int32_t* rows, int n, size_t row_bytes) {
+    if (n <= 0) return;
+    if (row_bytes % 16) fail(SGC_DOMAIN, "gather_rows: row bytes must be a multiple of 16");
+    gather_rows_kernel<<<n, 256, 0, c->stream>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), rows,
+                                                 row_bytes / 16);
     SGC_LAUNCH_CHECK(c);
 }
 int32_t* Ctx::iota(int n) {

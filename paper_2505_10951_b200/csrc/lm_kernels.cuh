@@ -14,6 +14,8 @@ void embed(Ctx* c, float* x, const int32_t* tokens, const float* tok_emb, const 
 void rmsnorm_bf16(Ctx* c, __nv_bfloat16* out, const float* x, int d, int rows);
 // per-row RMSNorm scale from per-chunk sums of squares (n_parts per row), fixed summation order
 void rms_scale(Ctx* c, float* scale, const float* parts, int rows, int n_parts, int d);
+// dst[i] = src[rows[i]] for i < n, rows of row_bytes (a multiple of 16)
+void gather_rows(Ctx* c, void* dst, const void* src, const int32_t* rows, int n, size_t row_bytes);
 void head_logits(Ctx* c, float* logits, const float* x, const int32_t* rows, int n,
                  const float* head_t, int d);
 void first_tokens(Ctx* c, int32_t* first, const float* logits, int n, const int32_t* ctx_tokens,
