@@ -84,6 +84,8 @@ const char* sgc_version(void);
 
 /* ---- context ------------------------------------------------------------------ */
 int sgc_ctx_create(int device, sgc_ctx** out);
+/* Release every handle created on the context (sgc_kv, then sgc_model / sgc_graph) first:
+ * their destructors free device memory on the context's stream. */
 int sgc_ctx_destroy(sgc_ctx* ctx);
 /* Use an external cudaStream_t (e.g. torch's current stream); NULL restores the own stream. */
 int sgc_ctx_set_stream(sgc_ctx* ctx, void* stream);

@@ -27,6 +27,10 @@ namespace sgc {
 
 namespace {
 
+// decode-sized GEMMs (129-256 rows) on CTA pairs (1) or 1-CTA 128-row tiles (0)
+#ifndef SGC_DECODE_PAIRS
+#define SGC_DECODE_PAIRS 1
+#endif
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
 // warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4-11 epilogue (two warpgroups,
@@ -500,7 +504,7 @@ struct Cfg2 {
 template <int EPI, int HD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 int M, int N, int K, GemmEpi ep, uint32_t* sched_ctr) {
+                 int M, int N, int K, GemmEpi ep, int ksplit, uint32_t* sched_ctr) {
     constexpr int BN = 256;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -522,8 +526,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int npairs = gridDim.x >> 1;
     const int m_tiles = (M + 2 * BM - 1) / (2 * BM);
     const int n_tiles = N / BN;
-    const int num_tiles = m_tiles * n_tiles;
-    const int num_kb = K / BK;
+    // split-K (decode residual GEMMs): work item = (pair-tile, K slice); the fp32 epilogue writes
+    // plane `slice` of `out`, a fixed-order reduction adds the planes
+    const int num_tiles = m_tiles * n_tiles * ksplit;
+    const int num_kb = K / BK / ksplit;
     // pair-tiles of 256 rows per raster group: the group's A rows (GROUP x 256 x K bf16) stay
     // L2-resident (~48 MB) while the group sweeps every n-tile; larger K -> smaller group
 #ifndef SGC_RESID_GROUP_MB
@@ -556,6 +562,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tmem_base = *tmem_slot;
 
     auto tile_coords = [&](int t, int& m0, int& n0) {
+        t /= ksplit;
         int per_group = GROUP * n_tiles;
         int g = t / per_group;
         int first_m = g * GROUP;
@@ -585,7 +592,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int t = static_cast<int>(tu);
                 int m0, n0;
                 tile_coords(t, m0, n0);
-                for (int kb = 0; kb < num_kb; ++kb) {
+                const int kb0 = (t % ksplit) * num_kb;
+                for (int kb = kb0; kb < kb0 + num_kb; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) ptx::mbar_expect_tx(&full[stage], 2 * Cfg2::kStageBytes);
                     ptx::tma_load_2d_2sm_hint(smemA + stage * Cfg2::kABytes, &tmA, &full[stage], kb * BK,
@@ -657,7 +665,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             const int row = m0 + static_cast<int>(rank) * BM + ew * 32 + lane;
             const uint32_t tbase = tmem_base + ((ew * 32) << 16) + acc * BN;
-            epilogue_tile<BN, EPI, HD>(tbase, row, row < M, n0, ep, ch_lo, ch_hi, stage, M);
+            GemmEpi eps = ep;
+            if (ksplit > 1)  // fp32 partial plane of this K slice
+                eps.out = static_cast<float*>(ep.out) + static_cast<size_t>(t % ksplit) * M * ep.ldo;
+            epilogue_tile<BN, EPI, HD>(tbase, row, row < M, n0, eps, ch_lo, ch_hi, stage, M);
             ptx::tc_fence_before();
             ptx::mbar_arrive_cluster(&tempty[acc], 0);
         }
@@ -697,7 +708,7 @@ void launch(Ctx* c, const void* A, const void* B, int M, int N, int K, const Gem
 }
 
 template <int EPI, int HD>
-void launch2(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
+void launch2(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep, int ksplit = 1) {
     static bool attr_set = false;
     auto kfn = gemm2_kernel<EPI, HD>;
     if (!attr_set) {
@@ -706,10 +717,10 @@ void launch2(Ctx* c, const void* A, const void* B, int M, int N, int K, const Ge
     }
     CUtensorMap ta = make_map_2d(A, M, K, BM, BK);
     CUtensorMap tb = make_map_2d(B, N, K, BM, BK);
-    int tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / 256);
+    int tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / 256) * ksplit;
     int grid = 2 * tiles < c->num_sms ? 2 * tiles : (c->num_sms & ~1);
-    Ctx::Timed timer(c, gemm_timer_name(EPI));
-    kfn<<<grid, kThreads, Cfg2::kSmem, c->stream>>>(ta, tb, M, N, K, ep, c->sched_counter());
+    Ctx::Timed timer(c, gemm_timer_name(ksplit > 1 ? EPI_RESID : EPI));
+    kfn<<<grid, kThreads, Cfg2::kSmem, c->stream>>>(ta, tb, M, N, K, ep, ksplit, c->sched_counter());
     SGC_LAUNCH_CHECK(c);
 }
 
@@ -772,13 +783,24 @@ void dispatch_bn(Ctx* c, const void* A, const void* B, int M, int N, int K, cons
             pe.mode = EPI_F32;
             pe.out = partial;
             pe.ldo = N;
-            launch<64, EPI_F32, 0>(c, A, B, M, N, K, pe, kSplit);
+            // 129-256 rows: one CTA pair per 256-column tile reads each weight tile once and
+            // every activation row once per 256 columns (the 1-CTA 64-column tiles re-read all
+            // rows 4x as often); same K slices, so the same partial sums
+            if (SGC_DECODE_PAIRS && g_gemm_pairs && M > BM && N % 256 == 0) launch2<EPI_F32, 0>(c, A, B, M, N, K, pe, kSplit);
+            else launch<64, EPI_F32, 0>(c, A, B, M, N, K, pe, kSplit);
             Ctx::Timed timer(c, "gemm_resid");
             resid_reduce_kernel<<<M, 256, 0, c->stream>>>(static_cast<float*>(ep.out), ep.out_xb, ep.out_ss, partial, M,
                                                           N, kSplit);
             SGC_LAUNCH_CHECK(c);
             return;
         }
+    }
+    // 129-256 rows (decode steps of ~150 members): one CTA pair covers all rows, so every weight
+    // tile is read once (two 128-row m-tiles would each stream it) and a wide N fits one wave
+    if (SGC_DECODE_PAIRS && g_gemm_pairs && EPI != EPI_RESID && M > BM && M <= 2 * BM && N % 256 == 0 &&
+        lim % 256 == 0 && 2 * (N / 256) >= c->num_sms / 2) {
+        launch2<EPI, HD>(c, A, B, M, N, K, ep);
+        return;
     }
     // few rows (decode steps): the GEMM is weight-bandwidth bound, so spread the weight matrix
     // over as many CTAs as possible -- the narrowest tile that still yields >= one wave

@@ -24,6 +24,7 @@ from __future__ import annotations
 
 import ctypes as C
 import dataclasses
+import weakref
 
 import numpy as np
 
@@ -46,16 +47,30 @@ def splitmix64_once(x: int) -> int:
 
 
 class Context:
-    """One CUDA device + stream (sgc_ctx)."""
+    """One CUDA device + stream (sgc_ctx). Handles created on it (KV batches, models, graphs)
+    are released before the context itself, whatever order Python collects them in -- their
+    native destructors free device memory on the context's stream."""
 
     def __init__(self, device: int = 0):
         self.lib = _lib.load()
         h = C.c_void_p()
         check(self.lib.sgc_ctx_create(device, C.byref(h)))
         self.h = h
+        self._children = weakref.WeakSet()
+
+    def _adopt(self, child):
+        self._children.add(child)
+
+    @property
+    def alive(self) -> bool:
+        return bool(getattr(self, "h", None))
 
     def close(self):
         if getattr(self, "h", None):
+            kids = list(getattr(self, "_children", ()))
+            # KV batches reference their model: release them first
+            for k in sorted(kids, key=lambda o: 0 if isinstance(o, KVBatch) else 1):
+                k.close()
             self.lib.sgc_ctx_destroy(self.h)
             self.h = None
 
@@ -148,11 +163,16 @@ class KVBatch:
     def __init__(self, lm: "ToyLm", h):
         self.lm, self.h = lm, h
         self.lib = lm.lib
+        lm.ctx._adopt(self)
 
     def release(self):
         if getattr(self, "h", None):
-            self.lib.sgc_kv_release(self.h)
+            if self.lm.ctx.alive and getattr(self.lm, "h", None):  # else freed with its context
+                self.lib.sgc_kv_release(self.h)
             self.h = None
+
+    def close(self):
+        self.release()
 
     def __del__(self):
         self.release()
@@ -189,10 +209,12 @@ class ToyLm:
         c = self.cfg.c()
         check(self.lib.sgc_model_create(ctx.h, C.byref(c), C.byref(h)))
         self.h = h
+        ctx._adopt(self)
 
     def close(self):
         if getattr(self, "h", None):
-            self.lib.sgc_model_destroy(self.h)
+            if self.ctx.alive:
+                self.lib.sgc_model_destroy(self.h)
             self.h = None
 
     def __del__(self):
@@ -297,10 +319,12 @@ class DeviceGraph:
                                         _p(eoff, C.c_uint64), C.byref(h)))
         self.h = h
         self.n_nodes, self.n_edges = len(ids), len(g.edges)
+        ctx._adopt(self)
 
     def close(self):
         if getattr(self, "h", None):
-            self.lib.sgc_graph_destroy(self.h)
+            if self.ctx.alive:
+                self.lib.sgc_graph_destroy(self.h)
             self.h = None
 
     def __del__(self):
