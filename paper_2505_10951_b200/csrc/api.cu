@@ -2222,6 +2222,32 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             }
             while (wave_end.size() < n_waves) wave_end.push_back(nown);
         }
+        {
+            // memory cap: a wave's prefill K/V (+ its forward activations) must fit beside the
+            // weights -- split any wave whose prefix rows exceed ~45% of the device (C4 with 256
+            // clusters in 2 waves would need ~125 GB of K/V per wave)
+            size_t free_b = 0, total_b = 0;
+            SGC_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+            const double row_bytes = 2.0 * model->L * d * sizeof(bf16)                      // K/V, all layers
+                                     + d * (4.0 + 2 * 4) + 2.0 * model->ffn + 4.0 * d / 32;  // x, xb, q, ao, h, ss
+            const uint64_t cap = std::max<uint64_t>(1, static_cast<uint64_t>(0.45 * total_b / row_bytes));
+            std::vector<uint32_t> split;
+            uint32_t w0 = 0;
+            for (uint32_t e : wave_end) {
+                uint64_t rows = 0;
+                for (uint32_t i = w0; i < e; ++i) {
+                    const uint64_t pr = reps.prefix_off[i + 1] - reps.prefix_off[i] + 1;
+                    if (rows > 0 && rows + pr > cap) {
+                        split.push_back(i);
+                        rows = 0;
+                    }
+                    rows += pr;
+                }
+                split.push_back(e);
+                w0 = e;
+            }
+            wave_end.swap(split);
+        }
         cudaEvent_t ev_start = c->event();
         SGC_CUDA_CHECK(cudaEventRecord(ev_start, c->stream));
         std::vector<cudaEvent_t> ev_wave, ev_seal, ev_wave_start;
