@@ -232,19 +232,43 @@ def run_ours(args, rank, world, local_rank):
     # ---- e2e: same batch through the C ABI with host buffers, rank-local inputs copied in and
     # first tokens copied out every step (run_subgcache takes host numpy arrays)
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e:
+        def step_e2e():
+            emb = None
+            if world > 1:
+                shard = host.encode_subgraphs(ctx, dg, w.retrieved[lo:hi], pb.gnn)
+                emb = D.gather_rows(torch.from_numpy(shard).to(COLL_DEV), m, world, pg).cpu().numpy()
+            r = host.run_subgcache(ctx, lm, dg, pb, embeddings=emb, rank=rank, world_size=world,
+                                   want_logits=True, waves=args.waves,
+                                   split_clusters=world > 1 and not args.no_split)
+            if world > 1:
+                r.first_token = D.combine_first_tokens(
+                    torch.from_numpy(r.first_token.astype(np.int64)).to(COLL_DEV), pg)
+            return r
+
         ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            pg.barrier()
         torch.cuda.synchronize()
         ev2.record(stream)
         for _ in range(args.steps):
-            r2 = host.run_subgcache(ctx, lm, dg, pb, want_logits=True, waves=args.waves)
+            r2 = step_e2e()
         ev3.record(stream)
+        if world > 1:
+            pg.barrier()
         torch.cuda.synchronize()
         e2e_ms = ev2.elapsed_time(ev3) / args.steps
+        if world > 1:  # max over ranks, like the device-resident number
+            t = torch.tensor([e2e_ms], device=COLL_DEV)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            e2e_ms = float(t.item())
         h2d = int(sum(a.nbytes for a in pb._ks) + sum(a.nbytes for a in pb._kq) +
                   (sum(a.nbytes for a in pb._ka) if pb._ka else 0) +
                   (sum(a.nbytes for a in pb._ko) if pb._ko else 0))
-        d2h = int(r2.first_token.nbytes + r2.logits.nbytes + r2.labels.nbytes + r2.embeddings.nbytes)
+        def nb(a):
+            return 0 if a is None else int(a.nbytes) if hasattr(a, "nbytes") else int(a.numel() * a.element_size())
+
+        d2h = nb(r2.first_token) + nb(r2.logits) + nb(r2.labels) + nb(r2.embeddings)
         e2e = {"value": m / (e2e_ms / 1000.0), "unit": "queries/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
