@@ -1049,13 +1049,6 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
         sub_off.push_back(static_cast<uint32_t>(inst_node.size()));
     }
     const size_t n_inst = inst_node.size();
-    struct KeyHash {
-        size_t operator()(const std::vector<uint32_t>& v) const {
-            uint64_t h = 0x9e3779b97f4a7c15ULL;
-            for (uint32_t x : v) h = sgc::mix64(h ^ x);
-            return static_cast<size_t>(h);
-        }
-    };
     // layer 0 groups = distinct nodes
     std::vector<uint32_t> gid(n_inst), g0_node;
     {
@@ -1074,29 +1067,53 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
     };
     std::vector<LayerHost> lh(cfg.layers);
     size_t max_groups = g0_node.size();
+    // open-addressing table over (signature hash -> group); a group's signature is read back
+    // from its own plan rows (self_row, in_src, in_gate), so no key copies are stored. Groups are
+    // numbered in order of first appearance, exactly as before.
+    size_t cap = 16;
+    while (cap < 2 * n_inst + 16) cap <<= 1;
+    std::vector<uint32_t> table(cap);
+    std::vector<uint64_t> ghash;
     for (uint32_t l = 0; l < cfg.layers; ++l) {
-        std::unordered_map<std::vector<uint32_t>, uint32_t, KeyHash> groups;
+        std::fill(table.begin(), table.end(), UINT32_MAX);
+        ghash.clear();
         std::vector<uint32_t> next(n_inst);
         LayerHost& L = lh[l];
-        std::vector<uint32_t> key;
         for (size_t v = 0; v < n_inst; ++v) {
-            key.assign(1, gid[v]);
-            for (auto& pr : inst_in[v]) {
-                key.push_back(pr.first);
-                key.push_back(gid[pr.second]);
+            const auto& in = inst_in[v];
+            uint64_t h = sgc::mix64(0x9e3779b97f4a7c15ULL ^ gid[v]);
+            for (auto& pr : in) {
+                h = sgc::mix64(h ^ pr.first);
+                h = sgc::mix64(h ^ gid[pr.second]);
             }
-            auto it = groups.find(key);
-            if (it == groups.end()) {
-                uint32_t ng = static_cast<uint32_t>(L.self_row.size());
-                it = groups.emplace(key, ng).first;
+            size_t pos = static_cast<size_t>(h) & (cap - 1);
+            uint32_t found = UINT32_MAX;
+            for (; table[pos] != UINT32_MAX; pos = (pos + 1) & (cap - 1)) {
+                const uint32_t ng = table[pos];
+                if (ghash[ng] != h || L.self_row[ng] != gid[v] || L.in_off[ng + 1] - L.in_off[ng] != in.size())
+                    continue;
+                bool eq = true;
+                for (size_t k = 0; k < in.size() && eq; ++k) {
+                    const uint32_t o = L.in_off[ng] + static_cast<uint32_t>(k);
+                    eq = L.in_gate[o] == g->n_nodes + in[k].first && L.in_src[o] == gid[in[k].second];
+                }
+                if (eq) {
+                    found = ng;
+                    break;
+                }
+            }
+            if (found == UINT32_MAX) {
+                found = static_cast<uint32_t>(L.self_row.size());
+                table[pos] = found;
+                ghash.push_back(h);
                 L.self_row.push_back(gid[v]);
-                for (auto& pr : inst_in[v]) {
+                for (auto& pr : in) {
                     L.in_src.push_back(gid[pr.second]);
                     L.in_gate.push_back(g->n_nodes + pr.first);
                 }
                 L.in_off.push_back(static_cast<uint32_t>(L.in_src.size()));
             }
-            next[v] = it->second;
+            next[v] = found;
         }
         gid.swap(next);
         max_groups = std::max(max_groups, L.self_row.size());
