@@ -596,24 +596,27 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 ptx::tmem_ld32(tO + half * OCOLS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
             ptx::tmem_ld_wait();
             if (valid && p.part_o) {
-                float4* dst = reinterpret_cast<float4*>(p.part_o + static_cast<size_t>(row) * p.d + h * HD + half * OCOLS);
+                float* dst = p.part_o + static_cast<size_t>(row) * p.d + h * HD + half * OCOLS;
 #pragma unroll
-                for (int q = 0; q < OCOLS / 4; ++q)
-                    dst[q] = make_float4(__uint_as_float(o[4 * q]) * il, __uint_as_float(o[4 * q + 1]) * il,
-                                         __uint_as_float(o[4 * q + 2]) * il, __uint_as_float(o[4 * q + 3]) * il);
+                for (int q = 0; q < OCOLS / 8; ++q) {  // 32 B per store (STG.256)
+                    uint32_t wv[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) wv[e] = __float_as_uint(__uint_as_float(o[8 * q + e]) * il);
+                    ptx::st_global_v8(dst + 8 * q, wv);
+                }
                 if (half == 0) p.part_lse[static_cast<size_t>(row) * p.heads + h] = l > 0.f ? m + __log2f(l) : -INFINITY;
             } else if (valid) {
-                uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(row) * p.d + h * HD + half * OCOLS);
+                __nv_bfloat16* dst = p.out + static_cast<size_t>(row) * p.d + h * HD + half * OCOLS;
 #pragma unroll
-                for (int q = 0; q < OCOLS / 8; ++q) {
-                    uint32_t wv[4];
+                for (int q = 0; q < OCOLS / 16; ++q) {  // 32 B per store (STG.256)
+                    uint32_t wv[8];
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        __nv_bfloat162 bv = __floats2bfloat162_rn(__uint_as_float(o[8 * q + 2 * e]) * il,
-                                                                  __uint_as_float(o[8 * q + 2 * e + 1]) * il);
+                    for (int e = 0; e < 8; ++e) {
+                        __nv_bfloat162 bv = __floats2bfloat162_rn(__uint_as_float(o[16 * q + 2 * e]) * il,
+                                                                  __uint_as_float(o[16 * q + 2 * e + 1]) * il);
                         wv[e] = *reinterpret_cast<uint32_t*>(&bv);
                     }
-                    dst[q] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
+                    ptx::st_global_v8(dst + 16 * q, wv);
                 }
             }
             ptx::tc_fence_before();

@@ -86,25 +86,20 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // store 32 fp32 values as bf16 (64 contiguous bytes)
 __device__ __forceinline__ void store_bf16x32_stream(__nv_bfloat16* dst, const float* v, uint64_t pol) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        uint4 w;
-        w.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
-        w.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
-        w.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
-        w.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
-        ptx::st_global_v4_hint(dst + 8 * q, w, pol);
+    for (int q = 0; q < 2; ++q) {  // 2 x 32 B (STG.256)
+        uint32_t w[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) w[e] = pack_bf16(v[16 * q + 2 * e], v[16 * q + 2 * e + 1]);
+        ptx::st_global_v8_hint(dst + 16 * q, w, pol);
     }
 }
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v) {
-    uint4* d4 = reinterpret_cast<uint4*>(dst);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        uint4 w;
-        w.x = pack_bf16(v[8 * q + 0], v[8 * q + 1]);
-        w.y = pack_bf16(v[8 * q + 2], v[8 * q + 3]);
-        w.z = pack_bf16(v[8 * q + 4], v[8 * q + 5]);
-        w.w = pack_bf16(v[8 * q + 6], v[8 * q + 7]);
-        d4[q] = w;
+    for (int q = 0; q < 2; ++q) {
+        uint32_t w[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) w[e] = pack_bf16(v[16 * q + 2 * e], v[16 * q + 2 * e + 1]);
+        ptx::st_global_v8(dst + 16 * q, w);
     }
 }
 
