@@ -31,6 +31,10 @@ namespace {
 #ifndef SGC_DECODE_PAIRS
 #define SGC_DECODE_PAIRS 1
 #endif
+// A/B switch: residual epilogue with 32-byte loads/stores (1) or 8-byte column pairs (0)
+#ifndef SGC_RESID_V8
+#define SGC_RESID_V8 1
+#endif
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle row
 // warps: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 3 idle, 4-11 epilogue (two warpgroups,
@@ -244,6 +248,75 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
             (void)ep_rows;
             return;
         }
+#if SGC_RESID_V8
+        if constexpr (EPI == EPI_RESID) {
+            // transposed residual epilogue with 32-byte accesses: lane = (row 8i + lane/4,
+            // columns 8*(lane%4)..+7) of the warp's 32 x 32 chunk; stage reads conflict-free
+            // (bank = row + column mod 32 covers all 32 banks)
+            const uint64_t resid_pol = ptx::policy_evict_first();
+            const int lane = threadIdx.x & 31;
+            const int row0 = row - lane;
+            const int rsub = lane >> 2, cq = (lane & 3) * 8;
+#pragma unroll 1
+            for (int ch = ch_lo; ch < ch_hi; ++ch) {
+                const int col = n0 + ch * 32 + cq;
+                float xo[4][8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int gr = row0 + 8 * i + rsub;
+                    if (gr < ep_rows)
+                        ptx::ld_global_f8_hint(static_cast<const float*>(ep.out) + static_cast<size_t>(gr) * ep.ldo + col,
+                                               xo[i], resid_pol);
+                    else {
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) xo[i][e] = 0.f;
+                    }
+                }
+                uint32_t r[32];
+                ptx::tmem_ld32(tbase + ch * 32, r);
+                ptx::tmem_ld_wait();
+                float* v = reinterpret_cast<float*>(r);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = v[j];
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int lr = 8 * i + rsub, gr = row0 + lr;
+                    float val[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        val[e] = stage[lr * 33 + cq + e] + xo[i][e];
+                        stage[lr * 33 + cq + e] = val[e];
+                    }
+                    if (gr < ep_rows) {
+                        const size_t off = static_cast<size_t>(gr) * ep.ldo + col;
+                        ptx::st_global_v8_hint(static_cast<float*>(ep.out) + off, *reinterpret_cast<uint32_t(*)[8]>(val),
+                                               resid_pol);
+                        if (ep.out_xb) {
+                            uint4 w;
+                            w.x = pack_bf16(val[0], val[1]);
+                            w.y = pack_bf16(val[2], val[3]);
+                            w.z = pack_bf16(val[4], val[5]);
+                            w.w = pack_bf16(val[6], val[7]);
+                            *reinterpret_cast<uint4*>(ep.out_xb + off) = w;
+                        }
+                    }
+                }
+                __syncwarp();
+                if (ep.out_ss) {  // this row's sum of squares over the chunk -> its own slot
+                    float cs = 0.f;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float xv = stage[lane * 33 + j];
+                        cs = fmaf(xv, xv, cs);
+                    }
+                    if (valid) ep.out_ss[static_cast<size_t>(row) * (ep.ldo / 32) + (n0 / 32 + ch)] = cs;
+                }
+                __syncwarp();
+            }
+            return;
+        }
+#endif
         float ss = 0.f;  // EPI_RESID with out_ss: this row's partial sum of squares of x_new
         // the fp32 residual stream is read and written once per launch: evict_first keeps it from
         // pushing the raster group's operand tiles out of L2

@@ -255,6 +255,11 @@ __device__ __forceinline__ void st_global_v8_hint(void* ptr, const uint32_t (&w)
                  "l"(policy)
                  : "memory");
 }
+__device__ __forceinline__ void ld_global_f8_hint(const void* ptr, float (&v)[8], uint64_t policy) {
+    asm volatile("ld.global.L2::cache_hint.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(ptr), "l"(policy));
+}
 __device__ __forceinline__ float2 ld_global_f2_hint(const void* ptr, uint64_t policy) {
     float2 v;
     asm volatile("ld.global.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(ptr), "l"(policy));
