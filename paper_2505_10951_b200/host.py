@@ -229,10 +229,11 @@ class ToyLm:
                                         _p(out, C.c_float), n))
         return out
 
-    def prefill_batch(self, seqs, softs=None):
+    def prefill_batch(self, seqs, softs=None, want_logits=True):
         """ToyLm::prefill + KVCache::seal for many prompts in one batched pass.
 
-        softs: optional list (per sequence) of a model_dim vector or None."""
+        softs: optional list (per sequence) of a model_dim vector or None. want_logits=False
+        returns (kv, None): the library then stops the last layer after its K/V."""
         tl, keep = pack_tokens(seqs)
         n = len(seqs)
         soft = mask = None
@@ -247,7 +248,7 @@ class ToyLm:
                         raise DomainError("soft prefix length must equal model_dim")
                     soft[i] = s
                     mask[i] = 1
-        logits = np.zeros((n, VOCAB), np.float32)
+        logits = np.zeros((n, VOCAB), np.float32) if want_logits else None
         h = C.c_void_p()
         check(self.lib.sgc_prefill(self.ctx.h, self.h, C.byref(tl), _p(soft, C.c_float),
                                    _p(mask, C.c_uint8), C.byref(h), _p(logits, C.c_float)))

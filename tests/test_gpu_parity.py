@@ -141,6 +141,34 @@ def test_prefill_split_equivalence_batched(ctx):
     assert np.abs(lg_full - lg_split).max() < 0.05
 
 
+@pytest.mark.parametrize("hd_cfg", [dict(max_seq_len=512),
+                                    dict(layers=2, heads=2, model_dim=256, ffn_hidden=512, max_seq_len=512)])
+def test_dead_last_layer_work_changes_nothing(ctx, hd_cfg):
+    """A prefill without logits stops its last layer after the K/V (forward_rows); an extend runs
+    the rest of the last layer only for its members' last rows. Every K/V byte and every member
+    logit must equal the full computation's."""
+    lm = host.ToyLm(ctx, host.ToyLmConfig(**hd_cfg))
+    rng = np.random.default_rng(5)
+    seqs = [rng.integers(0, 256, int(rng.integers(40, 300))).tolist() for _ in range(6)]
+    kv_full, lg_full = lm.prefill_batch(seqs)
+    kv_kv, none = lm.prefill_batch(seqs, want_logits=False)
+    assert none is None
+    for i in range(len(seqs)):
+        assert kv_full.prefix_digest(i) == kv_kv.prefix_digest(i)
+    # logits of a prefill that does request them: the compacted last rows vs a per-sequence run
+    for i in (0, 3):
+        _, lg1 = lm.prefill_batch([seqs[i]])
+        assert np.array_equal(lg1[0], lg_full[i])
+    qs = [rng.integers(0, 256, int(rng.integers(5, 60))).tolist() for _ in range(10)]
+    segs = [int(rng.integers(0, len(seqs))) for _ in qs]
+    lg_a, ft_a = lm.extend_members(kv_full, segs, qs)
+    lg_b, ft_b = lm.extend_members(kv_kv, segs, qs)
+    assert np.array_equal(lg_a, lg_b) and np.array_equal(ft_a, ft_b)
+    # one member alone (its last row is the only row) == the same member in the batch
+    lg_1, _ = lm.extend_members(kv_kv, [segs[0]], [qs[0]])
+    assert np.abs(lg_1[0] - lg_a[0]).max() < 0.05
+
+
 def test_many_members_share_one_prefix(ctx):
     """Cascade attention: members of several segments, interleaved order, vs the oracle."""
     cfg = host.ToyLmConfig(layers=2, heads=4, model_dim=256, ffn_hidden=512, max_seq_len=600, seed=9)
