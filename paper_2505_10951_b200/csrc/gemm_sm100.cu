@@ -118,6 +118,31 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float* v
 
 // RoPE on a pair of 32-column chunks (lo = cols i, hi = cols i+half), reference op order
 // (lm_core.cpp:231-238) without FMA contraction.
+#ifndef SGC_ROPE_PACKED
+#define SGC_ROPE_PACKED 1
+#endif
+// packed fp32x2 helpers (FMUL2 / FFMA2 on sm_100a)
+__device__ __forceinline__ uint64_t f2pack_g(float a, float b) {
+    uint64_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void f2unpack_g(uint64_t v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t fmul2_g(uint64_t a, uint64_t b) {
+    uint64_t r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ uint64_t ffma2_g(uint64_t a, uint64_t b, uint64_t c) {
+    uint64_t r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+__device__ __forceinline__ uint64_t fneg2_g(uint64_t a) {
+    return a ^ 0x8000000080000000ull;
+}
 __device__ __forceinline__ void rope_pair(float* lo, float* hi, const float* cosp,
                                           const float* sinp) {
 #pragma unroll
@@ -189,6 +214,28 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                     ptx::tmem_ld32(tbase + ch2 * 32, hi);
                     ptx::tmem_ld_wait();
                     if (valid) {
+#if SGC_ROPE_PACKED
+                        // RMSNorm scale + RoPE on packed fp32 pairs (FMUL2 / FFMA2): the epilogue's
+                        // issue slots, not the tensor pipe, were the QKV GEMM's margin
+                        const uint64_t inv2 = f2pack_g(inv, inv);
+#pragma unroll
+                        for (int j = 0; j < 32; j += 2) {
+                            const uint64_t c2 = f2pack_g(cs[j], cs[j + 1]);
+                            const uint64_t a2 = fmul2_g(f2pack_g(__uint_as_float(lo[j]), __uint_as_float(lo[j + 1])), inv2);
+                            const uint64_t b2 = fmul2_g(f2pack_g(__uint_as_float(hi[j]), __uint_as_float(hi[j + 1])), inv2);
+                            const uint64_t sp = f2pack_g(sn[j], sn[j + 1]);
+                            // lo' = a c - b s ; hi' = b c + a s
+                            const uint64_t l2 = ffma2_g(a2, c2, fmul2_g(b2, fneg2_g(sp)));
+                            const uint64_t h2 = ffma2_g(b2, c2, fmul2_g(a2, sp));
+                            float x0, x1, y0, y1;
+                            f2unpack_g(l2, x0, x1);
+                            f2unpack_g(h2, y0, y1);
+                            reinterpret_cast<float*>(lo)[j] = x0;
+                            reinterpret_cast<float*>(lo)[j + 1] = x1;
+                            reinterpret_cast<float*>(hi)[j] = y0;
+                            reinterpret_cast<float*>(hi)[j + 1] = y1;
+                        }
+#else
 #pragma unroll
                         for (int j = 0; j < 32; ++j) {
                             reinterpret_cast<float*>(lo)[j] *= inv;
@@ -196,6 +243,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                         }
                         rope_pair(reinterpret_cast<float*>(lo), reinterpret_cast<float*>(hi),
                                   cs, sn);
+#endif
                         store_bf16x32(dst + c0 + ch * 32, reinterpret_cast<float*>(lo));
                         store_bf16x32(dst + c0 + ch2 * 32, reinterpret_cast<float*>(hi));
                     }
