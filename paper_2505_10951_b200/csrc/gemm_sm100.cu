@@ -332,18 +332,31 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                 uint32_t r[32];
                 ptx::tmem_ld32(tbase + ch * 32, r);
                 ptx::tmem_ld_wait();
-                float* v = reinterpret_cast<float*>(r);
+                // 16-byte staging with an XOR swizzle of the 4-float groups (row r's group k at
+                // k ^ (r & 7)): STS.128 / LDS.128, conflict-free on both sides, no padding
+                float4* st4 = reinterpret_cast<float4*>(stage);
 #pragma unroll
-                for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = v[j];
+                for (int k = 0; k < 8; ++k)
+                    st4[lane * 8 + (k ^ (lane & 7))] = make_float4(__uint_as_float(r[4 * k]), __uint_as_float(r[4 * k + 1]),
+                                                                   __uint_as_float(r[4 * k + 2]), __uint_as_float(r[4 * k + 3]));
                 __syncwarp();
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int lr = 8 * i + rsub, gr = row0 + lr;
                     float val[8];
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        val[e] = stage[lr * 33 + cq + e] + xo[i][e];
-                        stage[lr * 33 + cq + e] = val[e];
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        const float4 a = st4[lr * 8 + ((cq / 4 + h2) ^ (lr & 7))];
+                        val[4 * h2 + 0] = a.x;
+                        val[4 * h2 + 1] = a.y;
+                        val[4 * h2 + 2] = a.z;
+                        val[4 * h2 + 3] = a.w;
+                    }
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) val[e] += xo[i][e];
+                    if (ep.out_ss) {  // keep x_new for the row sums below
+                        st4[lr * 8 + ((cq / 4) ^ (lr & 7))] = make_float4(val[0], val[1], val[2], val[3]);
+                        st4[lr * 8 + ((cq / 4 + 1) ^ (lr & 7))] = make_float4(val[4], val[5], val[6], val[7]);
                     }
                     if (gr < ep_rows) {
                         const size_t off = static_cast<size_t>(gr) * ep.ldo + col;
@@ -360,12 +373,15 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                     }
                 }
                 __syncwarp();
-                if (ep.out_ss) {  // this row's sum of squares over the chunk -> its own slot
+                if (ep.out_ss) {  // this row's sum of squares over the chunk, columns in order
                     float cs = 0.f;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const float xv = stage[lane * 33 + j];
-                        cs = fmaf(xv, xv, cs);
+                    for (int k = 0; k < 8; ++k) {
+                        const float4 a = st4[lane * 8 + (k ^ (lane & 7))];
+                        cs = fmaf(a.x, a.x, cs);
+                        cs = fmaf(a.y, a.y, cs);
+                        cs = fmaf(a.z, a.z, cs);
+                        cs = fmaf(a.w, a.w, cs);
                     }
                     if (valid) ep.out_ss[static_cast<size_t>(row) * (ep.ldo / 32) + (n0 / 32 + ch)] = cs;
                 }
