@@ -204,9 +204,9 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                     float cs[32], sn[32];
                     if (valid) {
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            reinterpret_cast<float4*>(cs)[j] = __ldg(reinterpret_cast<const float4*>(cosp + in_head) + j);
-                            reinterpret_cast<float4*>(sn)[j] = __ldg(reinterpret_cast<const float4*>(sinp + in_head) + j);
+                        for (int j = 0; j < 4; ++j) {  // LDG.256
+                            ptx::ld_nc_f8(cosp + in_head + 8 * j, cs + 8 * j);
+                            ptx::ld_nc_f8(sinp + in_head + 8 * j, sn + 8 * j);
                         }
                     }
                     uint32_t lo[32], hi[32];

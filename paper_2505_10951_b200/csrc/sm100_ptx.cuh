@@ -255,6 +255,12 @@ __device__ __forceinline__ void st_global_v8_hint(void* ptr, const uint32_t (&w)
                  "l"(policy)
                  : "memory");
 }
+// 256-bit read-only load (LDG.256.CONSTANT)
+__device__ __forceinline__ void ld_nc_f8(const float* ptr, float* v) {
+    asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(ptr));
+}
 __device__ __forceinline__ void ld_global_f8_hint(const void* ptr, float (&v)[8], uint64_t policy) {
     asm volatile("ld.global.L2::cache_hint.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8], %9;"
                  : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
