@@ -676,7 +676,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #ifndef SGC_RESID_GROUP_MB
 #define SGC_RESID_GROUP_MB 48
 #endif
-    constexpr int kGroupBytes = (EPI == EPI_RESID ? SGC_RESID_GROUP_MB : 48) << 20;
+// raster-group budget (A rows of a group kept L2-resident while it sweeps the n-tiles):
+// measured at C3, 24-32 MB beats 48 (~0.7% GEMM time) and 96 (-4%)
+#ifndef SGC_GROUP_MB
+#define SGC_GROUP_MB 32
+#endif
+    constexpr int kGroupBytes = (EPI == EPI_RESID ? SGC_RESID_GROUP_MB : SGC_GROUP_MB) << 20;
     const int GROUP = max(2, min(32, kGroupBytes / (2 * BM * K * 2)));
 
     if (warp == 0 && lane == 0) {
