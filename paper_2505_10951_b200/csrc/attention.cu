@@ -14,6 +14,7 @@
 // with cp.async (zero-filled out of range) in a double-buffered smem ring.
 #include "attention.cuh"
 #include "common.cuh"
+#include "sm100_ptx.cuh"
 
 namespace sgc {
 namespace {
@@ -358,17 +359,19 @@ __global__ void __launch_bounds__(256) decode_local_kernel(DecodeAttnParams p) {
             const int key = k0 + lane;
             float sc = -INFINITY;
             if (key < n) {
-                const uint4* kr = reinterpret_cast<const uint4*>(K + static_cast<size_t>(lo + key) * p.d + h * HD);
+                const __nv_bfloat16* kr = K + static_cast<size_t>(lo + key) * p.d + h * HD;
                 float a0 = 0.f, a1 = 0.f;
+                // the key row in 32-byte loads (LDG.256): all of them in flight before the math
+                uint32_t u[HD / 16][8];
 #pragma unroll
-                for (int c = 0; c < HD / 8; ++c) {
-                    const uint4 u = kr[c];
-                    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+                for (int c = 0; c < HD / 16; ++c) ptx::ld_nc_u8(kr + 16 * c, u[c]);
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 f = __bfloat1622float2(b2[e]);
-                        a0 = fmaf(qs[wib][c * 8 + 2 * e], f.x, a0);
-                        a1 = fmaf(qs[wib][c * 8 + 2 * e + 1], f.y, a1);
+                for (int c = 0; c < HD / 16; ++c) {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u[c][e]));
+                        a0 = fmaf(qs[wib][c * 16 + 2 * e], f.x, a0);
+                        a1 = fmaf(qs[wib][c * 16 + 2 * e + 1], f.y, a1);
                     }
                 }
                 sc = a0 + a1;

@@ -255,6 +255,12 @@ __device__ __forceinline__ void st_global_v8_hint(void* ptr, const uint32_t (&w)
                  "l"(policy)
                  : "memory");
 }
+// 256-bit read-only load of 8 words (LDG.256.CONSTANT)
+__device__ __forceinline__ void ld_nc_u8(const void* ptr, uint32_t (&v)[8]) {
+    asm volatile("ld.global.nc.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "l"(ptr));
+}
 // 256-bit read-only load (LDG.256.CONSTANT)
 __device__ __forceinline__ void ld_nc_f8(const float* ptr, float* v) {
     asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
