@@ -1430,6 +1430,10 @@ int sgc_ctx_destroy(sgc_ctx* ctx) {
             g_enc.erase(it);
         }
         for (auto e : c->event_pool) cudaEventDestroy(e);
+        for (auto& pe : c->pending) {
+            cudaEventDestroy(pe.second.first);
+            cudaEventDestroy(pe.second.second);
+        }
         if (c->h_flags) cudaFreeHost(c->h_flags);
         for (auto& kv : c->pinned_bufs) cudaFreeHost(kv.second.ptr);
         cudaStreamDestroy(c->own_stream);
@@ -2782,6 +2786,7 @@ int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value) {
 int sgc_set_timing(sgc_ctx* ctx, int enable) {
     return guarded([&] {
         ctx->c.sync();
+        ctx->c.resolve_timings();  // recycle the pending pairs; the totals restart
         ctx->c.timing = enable != 0;
         ctx->c.timings.clear();
     });
@@ -2790,6 +2795,7 @@ int sgc_set_timing(sgc_ctx* ctx, int enable) {
 int sgc_get_timing(sgc_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches) {
     return guarded([&] {
         ctx->c.sync();
+        ctx->c.resolve_timings();
         auto it = ctx->c.timings.find(kernel);
         *total_ms = it == ctx->c.timings.end() ? 0.0 : it->second.ms;
         *launches = it == ctx->c.timings.end() ? 0 : it->second.launches;

@@ -77,7 +77,7 @@ struct Ctx {
     std::map<std::string, Buffer> scratch;
     bool timing = false;
     std::map<std::string, KernelTiming> timings;
-    // pending (name, start, stop) event triples, resolved at the next sync point
+    // pending (name, start, stop) event triples, resolved when the timings are read
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> event_pool;
 
@@ -137,9 +137,11 @@ struct Ctx {
         }
         pending.clear();
     }
+    // pending event pairs are resolved when the timings are read (or the list grows large), not
+    // at every sync: resolving ~1000 pairs right after a sync kept the GPU idle for milliseconds
     void sync() {
         SGC_CUDA_CHECK(cudaStreamSynchronize(stream));
-        resolve_timings();
+        if (pending.size() > 16384) resolve_timings();
     }
     // grow-only PINNED host buffers keyed by name (asynchronous device -> host copies)
     std::map<std::string, Buffer> pinned_bufs;
