@@ -545,9 +545,9 @@ def main():
     ap.add_argument("--attn-db", type=int, default=None,
                     help="1: double-buffered 64-key attention kernel, 0: 128-key single-buffer kernel")
     ap.add_argument("--gen-steps", type=int, default=2)
-    ap.add_argument("--gen-waves", type=int, default=4,
-                    help="waves of the generation run (RT: more, smaller waves finish the median "
-                         "query's decode earlier; the TTFT metric uses --waves)")
+    ap.add_argument("--gen-waves", type=int, default=2,
+                    help="waves of the generation run (cost-balanced cuts; scripts/defer_probe.py: "
+                         "2 waves gave the shortest batch and RT p50 at C3, 4 the lowest RT mean)")
     ap.add_argument("--no-pairs", action="store_true", help="1-CTA GEMM instead of CTA pairs")
     ap.add_argument("--waves", type=int, default=2,
                     help="serve clusters in this many waves (lower TTFT p50); 1 = one pass")
