@@ -8,6 +8,7 @@
 //
 // Usage: ref_driver <spec.json> <out.json>. The spec's "cmd" selects:
 //   lm        ToyLm::prefill / seal / fork / extend / prefill_collect_logits / greedy_decode
+//   lm_cluster prefill + seal per cluster, fork + extend per member (threaded), any shape
 //   cluster   pairwise_distances + agglomerate (+ naive oracle from tests/support)
 //   gnn       TextEncoder::embed + GnnEncoder::encode over a CSV graph and subgraph lists
 //   prompt    merge_subgraphs + build_prompt + Tokenizer over a CSV graph
@@ -135,12 +136,76 @@ json cmd_lm(const json& spec) {
     return out;
 }
 
+
+// process_cluster's KV lifecycle (cache_engine.cpp:140-215) at an arbitrary model shape, for
+// the full-width parity fixtures: prefill each cluster's prefix, seal, then fork + extend every
+// member (answer lookup off: plain greedy_argmax). Clusters prefill concurrently and members
+// extend concurrently (ToyLm const methods are safe on distinct forks, lm_core.hpp:118-121),
+// bounded by "threads"; the arithmetic is the reference's own.
+json cmd_lm_cluster(const json& spec) {
+    ToyLm lm(lm_cfg(spec.at("cfg")));
+    const json& cl = spec.at("clusters");
+    size_t threads = std::max<size_t>(1, spec.value("threads", std::thread::hardware_concurrency()));
+    size_t nc = cl.size();
+    std::vector<KVCache> shared(nc);
+    std::vector<json> out(nc);
+    auto run_bounded = [&](size_t n, auto&& fn) {
+        for (size_t b = 0; b < n; b += threads) {
+            std::vector<std::future<void>> fs;
+            for (size_t i = b; i < std::min(n, b + threads); ++i)
+                fs.push_back(std::async(std::launch::async, [&, i] { fn(i); }));
+            for (auto& f : fs) f.get();
+        }
+    };
+    auto t0 = Clock::now();
+    run_bounded(nc, [&](size_t c) {
+        shared[c] = lm.prefill(toks(cl[c].at("prefix")));
+        out[c]["prefix_logits"] = shared[c].last_logits();
+        shared[c].seal();
+        out[c]["prefix_digest"] = std::to_string(shared[c].prefix_digest());
+        out[c]["prefix_tokens"] = shared[c].token_count();
+    });
+    double prefill_ms = ms_since(t0);
+    std::vector<std::pair<size_t, size_t>> work;
+    for (size_t c = 0; c < nc; ++c) {
+        out[c]["members"] = json::array();
+        for (size_t j = 0; j < cl[c].at("members").size(); ++j) {
+            work.emplace_back(c, j);
+            out[c]["members"].push_back(nullptr);
+        }
+    }
+    std::vector<json> res(work.size());
+    t0 = Clock::now();
+    run_bounded(work.size(), [&](size_t w) {
+        auto [c, j] = work[w];
+        KVCache f = shared[c].fork();
+        std::vector<float> lg = lm.extend(f, toks(cl[c]["members"][j]));
+        std::vector<float> s = lg;
+        std::sort(s.begin(), s.end());
+        res[w] = json{{"logits", lg}, {"margin", s[s.size() - 1] - s[s.size() - 2]},
+                      {"argmax", greedy_argmax(lg)}};
+    });
+    double extend_ms = ms_since(t0);
+    for (size_t w = 0; w < work.size(); ++w) out[work[w].first]["members"][work[w].second] = res[w];
+    return json{{"clusters", out}, {"prefill_ms", prefill_ms}, {"extend_ms", extend_ms},
+                {"threads", threads}};
+}
+
 Linkage linkage_of(const json& spec) { return linkage_from_string(spec.value("linkage", "ward")); }
 
 json cmd_cluster(const json& spec) {
     json out = json::array();
     for (const json& c : spec.at("cases")) {
-        std::vector<EmbeddingVec> emb = c.at("embeddings").get<std::vector<EmbeddingVec>>();
+        std::vector<EmbeddingVec> emb;
+        if (c.contains("embeddings_f32")) {  // raw row-major float32 [m x d] (large fixtures)
+            size_t m = c.at("m"), d = c.at("d");
+            std::ifstream bin(c["embeddings_f32"].get<std::string>(), std::ios::binary);
+            emb.assign(m, EmbeddingVec(d));
+            for (auto& e : emb) bin.read(reinterpret_cast<char*>(e.data()), d * sizeof(float));
+            if (!bin) throw std::runtime_error("short embeddings_f32 file");
+        } else {
+            emb = c.at("embeddings").get<std::vector<EmbeddingVec>>();
+        }
         json r;
         try {
             if (c.value("pairwise", false)) r["pairwise"] = pairwise_distances(emb);
@@ -518,6 +583,7 @@ int main(int argc, char** argv) {
     json out;
     try {
         if (cmd == "lm") out = cmd_lm(spec);
+        else if (cmd == "lm_cluster") out = cmd_lm_cluster(spec);
         else if (cmd == "cluster") out = cmd_cluster(spec);
         else if (cmd == "gnn") out = cmd_gnn(spec);
         else if (cmd == "prompt") out = cmd_prompt(spec);

@@ -51,6 +51,15 @@ int guarded(F&& f) {
     }
 }
 
+// every ABI entry that touches the device makes the context's device current first: a process
+// may hold contexts on several GPUs and call them from any thread
+Ctx* current(Ctx* c) {
+    int cur = -1;
+    SGC_CUDA_CHECK(cudaGetDevice(&cur));
+    if (cur != c->device) SGC_CUDA_CHECK(cudaSetDevice(c->device));
+    return c;
+}
+
 double now_ms() {
     return std::chrono::duration<double, std::milli>(
                std::chrono::steady_clock::now().time_since_epoch())
@@ -1354,13 +1363,8 @@ RepResult build_reps(Ctx* c, sgc_graph* g, const HostSubs& hs, uint32_t count,
     r.d_prefix = c->buf<int32_t>("rep_prefix", r.prefix_off.back());
     r.d_prefix_off = c->buf<uint64_t>("rep_prefix_off", k + 1);
     sgc::copy_in(c, r.d_prefix_off, r.prefix_off.data(), k + 1);
-    static bool headers_set = false;
-    if (!headers_set) {
-        std::string h = std::string(kHeader) + kNodeHdr + "\n";
-        std::string eh = std::string(kEdgeHdr) + "\n";
-        sgc::set_prompt_headers(h.data(), static_cast<int>(h.size()), eh.data(), static_cast<int>(eh.size()));
-        headers_set = true;
-    }
+    const std::string h = std::string(kHeader) + kNodeHdr + "\n";
+    const std::string eh = std::string(kEdgeHdr) + "\n";
     sgc::GatherArgs ga;
     ga.clusters = static_cast<int>(k);
     ga.max_tokens = maxp;
@@ -1379,6 +1383,8 @@ RepResult build_reps(Ctx* c, sgc_graph* g, const HostSubs& hs, uint32_t count,
     ga.n_edges = static_cast<int>(g->n_edges);
     ga.head_len = static_cast<int>(head_len);
     ga.ehead_len = static_cast<int>(ehead_len);
+    ga.head = h.data();
+    ga.ehead = eh.data();
     sgc::prompt_gather(c, ga);
     return r;
 }
@@ -1420,7 +1426,7 @@ int sgc_ctx_create(int device, sgc_ctx** out) {
 int sgc_ctx_destroy(sgc_ctx* ctx) {
     return guarded([&] {
         if (!ctx) return;
-        Ctx* c = &ctx->c;
+        Ctx* c = current(&ctx->c);
         cudaStreamSynchronize(c->stream);
         for (auto& kv : c->scratch) cudaFree(kv.second.ptr);
         auto it = g_enc.find(c);
@@ -1452,7 +1458,7 @@ uint64_t sgc_ctx_launch_count(const sgc_ctx* ctx) { return ctx ? ctx->c.launches
 
 int sgc_model_create(sgc_ctx* ctx, const sgc_lm_config* cfg, sgc_model** out) {
     return guarded([&] {
-        Ctx* c = &ctx->c;
+        Ctx* c = current(&ctx->c);
         check_lm_cfg(*cfg);
         auto m = std::make_unique<sgc_model>();
         m->c = c;
@@ -1508,7 +1514,7 @@ int sgc_model_create(sgc_ctx* ctx, const sgc_lm_config* cfg, sgc_model** out) {
 int sgc_model_destroy(sgc_model* m) {
     return guarded([&] {
         if (!m) return;
-        Ctx* c = m->c;
+        Ctx* c = current(m->c);
         dfree(c, m->tok_emb);
         dfree(c, m->head);
         dfree(c, m->head_t);
@@ -1522,7 +1528,7 @@ int sgc_model_destroy(sgc_model* m) {
 
 int sgc_model_weight(sgc_model* m, int which, uint32_t layer, int fp32, float* out, size_t n) {
     return guarded([&] {
-        Ctx* c = m->c;
+        Ctx* c = current(m->c);
         const size_t d = m->d, ffn = m->ffn;
         if (which < 2) {
             if (n != SGC_VOCAB * d) fail(SGC_DOMAIN, "size mismatch");
@@ -1558,7 +1564,7 @@ int sgc_graph_upload(sgc_ctx* ctx, uint32_t n_nodes, const uint32_t* node_ids, c
                      const uint32_t* edge_dst, const char* edge_text, const uint64_t* edge_off,
                      sgc_graph** out) {
     return guarded([&] {
-        Ctx* c = &ctx->c;
+        Ctx* c = current(&ctx->c);
         auto g = std::make_unique<sgc_graph>();
         g->c = c;
         g->n_nodes = n_nodes;
@@ -1610,7 +1616,7 @@ int sgc_graph_upload(sgc_ctx* ctx, uint32_t n_nodes, const uint32_t* node_ids, c
 int sgc_graph_destroy(sgc_graph* g) {
     return guarded([&] {
         if (!g) return;
-        Ctx* c = g->c;
+        Ctx* c = current(g->c);
         for (void* p : {(void*)g->d_ids, (void*)g->d_node_rows, (void*)g->d_node_row_off,
                         (void*)g->d_node_row_len, (void*)g->d_edge_rows, (void*)g->d_edge_row_off,
                         (void*)g->d_edge_row_len, (void*)g->d_bucket, (void*)g->d_sign, (void*)g->d_tok_off})
@@ -1622,7 +1628,7 @@ int sgc_graph_destroy(sgc_graph* g) {
 
 int sgc_text_features(sgc_ctx* ctx, sgc_graph* g, uint32_t dim, uint64_t seed, uint64_t salt, float* out) {
     return guarded([&] {
-        Ctx* c = &ctx->c;
+        Ctx* c = current(&ctx->c);
         if (dim == 0) fail(SGC_DOMAIN, "text encoder dim must be >= 1");
         float* f = compute_text_features(c, g, dim, seed, salt, nullptr);
         sgc::copy_out(c, out, f, static_cast<size_t>(g->n_nodes + g->n_edges) * dim);
@@ -1634,7 +1640,7 @@ int sgc_retrieve(sgc_ctx* ctx, sgc_graph* g, const sgc_retrieval_config* cfg, ui
                  const char* q_text, const uint64_t* q_off, uint64_t* node_off, uint32_t* nodes,
                  uint64_t node_cap, uint64_t* edge_off, uint32_t* edges, uint64_t edge_cap) {
     return guarded([&] {
-        Ctx* c = &ctx->c;
+        Ctx* c = current(&ctx->c);
         // RetrievalConfig::validate (retrieval.cpp:21-25), retrieve() (:226-239)
         if (cfg->k < 1) fail(SGC_DOMAIN, "retrieval k must be >= 1");
         if (cfg->ego_hops < 1) fail(SGC_DOMAIN, "ego hops must be >= 1");
@@ -1838,7 +1844,7 @@ int sgc_retrieve(sgc_ctx* ctx, sgc_graph* g, const sgc_retrieval_config* cfg, ui
 int sgc_encode_subgraphs(sgc_ctx* ctx, sgc_graph* g, const sgc_gnn_config* cfg,
                          const sgc_subgraphs* subs, float* out) {
     return guarded([&] {
-        Ctx* c = &ctx->c;
+        Ctx* c = current(&ctx->c);
         HostSubs hs = host_subs(c, subs);
         float* d_out = c->buf<float>("enc_out", static_cast<size_t>(subs->count) * cfg->dim);
         encode_subgraphs(c, g, *cfg, hs, subs->count, d_out);
@@ -1849,7 +1855,7 @@ int sgc_encode_subgraphs(sgc_ctx* ctx, sgc_graph* g, const sgc_gnn_config* cfg,
 
 int sgc_pairwise_distances(sgc_ctx* ctx, const float* emb, uint32_t m, uint32_t dim, double* out) {
     return guarded([&] {
-        Ctx* c = &ctx->c;
+        Ctx* c = current(&ctx->c);
         if (m == 0) fail(SGC_DOMAIN, "pairwise_distances: need at least one embedding");
         float* e = c->buf<float>("pw_emb", static_cast<size_t>(m) * dim);
         sgc::copy_in(c, e, emb, static_cast<size_t>(m) * dim);
@@ -1864,7 +1870,7 @@ int sgc_agglomerate(sgc_ctx* ctx, const float* emb, uint32_t m, uint32_t dim, in
                     uint32_t* labels, uint32_t* merge_left, uint32_t* merge_right, double* merge_dist,
                     uint64_t* op_count) {
     return guarded([&] {
-        Ctx* c = &ctx->c;
+        Ctx* c = current(&ctx->c);
         if (k < 1) fail(SGC_DOMAIN, "cluster count must be >= 1");
         if (k > m) fail(SGC_DOMAIN, "cluster count " + std::to_string(k) + " exceeds point count " + std::to_string(m));
         float* e = c->buf<float>("ag_emb", static_cast<size_t>(m) * dim);
@@ -1889,7 +1895,7 @@ int sgc_build_representatives(sgc_ctx* ctx, sgc_graph* g, const sgc_subgraphs* s
                               uint64_t rep_edge_cap, uint64_t* prefix_off, int32_t* prefix, uint64_t prefix_cap,
                               uint32_t* dropped) {
     return guarded([&] {
-        Ctx* c = &ctx->c;
+        Ctx* c = current(&ctx->c);
         HostSubs hs = host_subs(c, subs);
         std::vector<uint32_t> lab = to_host(c, labels, subs->count);
         std::vector<std::vector<uint32_t>> members(k);
@@ -1939,21 +1945,23 @@ int sgc_prefill(sgc_ctx* ctx, sgc_model* model, const sgc_token_lists* seqs, con
                 const uint8_t* soft_mask, sgc_kv** out, float* last_logits) {
     return guarded([&] {
         if (seqs->count == 0) fail(SGC_DOMAIN, "prefill: no sequences");
-        *out = do_prefill(&ctx->c, model, seqs->count, seqs->off, seqs->tokens, soft, soft_mask, last_logits);
+        *out = do_prefill(current(&ctx->c), model, seqs->count, seqs->off, seqs->tokens, soft, soft_mask, last_logits);
     });
 }
 
 int sgc_kv_release(sgc_kv* kv) {
     return guarded([&] {
         if (!kv) return;
-        Ctx* c = kv->model->c;
+        Ctx* c = current(kv->model->c);
         if (kv->owns_kv) {
             dfree(c, kv->k);
             dfree(c, kv->v);
         }
         dfree(c, kv->d_tokens);
         dfree(c, kv->d_tok_off);
-        c->sync();
+        // frees are stream-ordered; an arena view (batch-internal, owns no K/V) releases without
+        // draining the stream so the host keeps preparing the next wave while the GPU works
+        if (kv->owns_kv) c->sync();
         delete kv;
     });
 }
@@ -1968,7 +1976,7 @@ uint64_t sgc_kv_digest(const sgc_kv* kv, uint32_t i) {
     if (!kv || i >= kv->n) return 0;
     uint64_t h = 0xcbf29ce484222325ULL;
     try {
-        Ctx* c = kv->model->c;
+        Ctx* c = current(kv->model->c);
         // the KV was written on the context's non-blocking stream: a plain cudaMemcpy does not
         // order after it
         SGC_CUDA_CHECK(cudaStreamSynchronize(c->stream));
@@ -2014,7 +2022,7 @@ int sgc_extend(sgc_ctx* ctx, sgc_model* model, sgc_kv* kv, const uint32_t* membe
         if (kv->model != model) fail(SGC_DOMAIN, "KV cache does not belong to this model");
         const bool ans = answers && answers->count > 0;
         if (ans && answers->count != questions->count) fail(SGC_DOMAIN, "answers/questions count mismatch");
-        do_extend(&ctx->c, model, kv, questions->count, member_seg, questions->off, questions->tokens,
+        do_extend(current(&ctx->c), model, kv, questions->count, member_seg, questions->off, questions->tokens,
                   ans ? answers->off : nullptr, ans ? answers->tokens : nullptr, pointer_bonus, logits,
                   first_token);
     });
@@ -2026,7 +2034,7 @@ int sgc_extend_generate(sgc_ctx* ctx, sgc_model* model, sgc_kv* kv, const uint32
                         int32_t* tokens, uint32_t* n_tokens) {
     return guarded([&] {
         if (kv->model != model) fail(SGC_DOMAIN, "KV cache does not belong to this model");
-        Ctx* c = &ctx->c;
+        Ctx* c = current(&ctx->c);
         const uint32_t n = questions->count;
         const bool ans = answers && answers->count > 0;
         if (ans && answers->count != n) fail(SGC_DOMAIN, "answers/questions count mismatch");
@@ -2072,7 +2080,7 @@ int sgc_extend_generate(sgc_ctx* ctx, sgc_model* model, sgc_kv* kv, const uint32
 
 int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_batch* b, sgc_batch_out* o) {
     return guarded([&] {
-        Ctx* c = &ctx->c;
+        Ctx* c = current(&ctx->c);
         const double t_start = now_ms();
         const uint32_t m = b->retrieved.count;
         const uint32_t d = model->d;
@@ -2323,7 +2331,16 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         }
         // retain every wave's K/V only when generating and it fits comfortably (C3: ~45 GB)
         const double kv_row_bytes = 2.0 * model->L * d * sizeof(bf16);
-        const bool retain = gen_on && (pf_total + qr_total + static_cast<double>(m) * max_new) * kv_row_bytes < 96e9;
+        // (against what the device has free now, weights and scratch already allocated, keeping
+        // 20% headroom for the forward activations)
+        size_t free_now = 0, total_now = 0;
+        SGC_CUDA_CHECK(cudaMemGetInfo(&free_now, &total_now));
+        for (const char* nm : {"kv_arena_k", "kv_arena_v", "ex_keep_k", "ex_keep_v"}) {
+            auto it = c->scratch.find(nm);  // grow-only buffers this batch re-uses (or regrows)
+            if (it != c->scratch.end()) free_now += it->second.bytes;
+        }
+        const bool retain = gen_on && (pf_total + qr_total + static_cast<double>(m) * max_new) * kv_row_bytes <
+                                          0.8 * static_cast<double>(free_now);
         const uint64_t arena_rows = retain ? pf_total : pf_max;
         ExtendKeep keep_all;
         if (gen_on) {
@@ -2479,9 +2496,10 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 const uint32_t q = fb_q[f];
                 const uint64_t s = fb_seq[f];
                 const float* lg = seq_logits.data() + s * SGC_VOCAB;
-                const uint64_t ctx_len = seq_off[s + 1] - seq_off[s] + (b->soft_prefix ? 1 : 0);
-                const uint64_t qn = std::min<uint64_t>(q_off[q + 1] - q_off[q], ctx_len);
-                const uint64_t limit = ctx_len - qn;
+                // CopyPointerHint::search_limit of the standalone path (cache_engine.cpp:82-85,
+                // :124-129): token_count minus the TRIMMED question = the kept prompt prefix (+ soft)
+                const uint64_t full_len = seq_off[s + 1] - seq_off[s];
+                const uint64_t limit = std::min<uint64_t>(oo[q + 1] - oo[q], full_len) + (b->soft_prefix ? 1 : 0);
                 int target = -1;
                 if (ans && a_off[q + 1] > a_off[q]) {
                     std::vector<int32_t> ctxv;
@@ -2727,7 +2745,7 @@ int sgc_gemm_bf16(sgc_ctx* ctx, const void* a, const void* b, void* d, uint32_t 
         e.out = d;
         e.ldo = static_cast<int>(N);
         if (epi == sgc::EPI_QKV) fail(SGC_DOMAIN, "QKV epilogue is internal");
-        sgc::gemm_bf16(&ctx->c, a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e);
+        sgc::gemm_bf16(current(&ctx->c), a, b, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K), e);
         ctx->c.sync();
     });
 }
@@ -2740,7 +2758,7 @@ int sgc_attention_bf16(sgc_ctx* ctx, const void* q, const void* k_pfx, const voi
         if (heads == 0 || d % heads != 0) fail(SGC_DOMAIN, "attention: d must be a multiple of heads");
         const int hd = static_cast<int>(d / heads);
         const int tile = attn_tile(hd);
-        Ctx* c = &ctx->c;
+        Ctx* c = current(&ctx->c);
         std::vector<sgc::AttnWork> w(n_work);
         for (uint32_t i = 0; i < n_work; ++i) {
             w[i] = {work[4 * i], work[4 * i + 1], work[4 * i + 2], work[4 * i + 3]};

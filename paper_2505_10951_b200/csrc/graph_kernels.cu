@@ -1,5 +1,7 @@
 // graph_kernels.cu -- text features (TextEncoder::embed), representative union
 // (merge_subgraphs) and prompt construction (build_prompt + tokenize) on the device.
+#include <cstring>
+
 #include "common.cuh"
 #include "graph_kernels.cuh"
 
@@ -209,8 +211,12 @@ __global__ void __launch_bounds__(1024)
     }
 }
 
-__constant__ char c_header[128];  // header + node csv header + '\n'
-__constant__ char c_edge_header[32];
+// prompt headers travel as a by-value kernel parameter (no per-device constant state: a
+// context on another device launches with the same bytes)
+struct PromptHeaders {
+    char head[128];  // header + node csv header + '\n'
+    char edge[32];   // edge csv header + '\n'
+};
 
 // tokenize (tokenizer.cpp:5-11) of the truncated prompt: BOS + bytes, as int32 tokens.
 __global__ void prompt_gather_kernel(int32_t* tokens, const uint64_t* tok_off,
@@ -219,7 +225,7 @@ __global__ void prompt_gather_kernel(int32_t* tokens, const uint64_t* tok_off,
                                      const uint32_t* edge_pre, const char* node_text,
                                      const uint64_t* node_text_off, const char* edge_text,
                                      const uint64_t* edge_text_off, int n_nodes, int n_edges,
-                                     int head_len, int ehead_len) {
+                                     int head_len, int ehead_len, const PromptHeaders hdr) {
     const int k = blockIdx.y;
     const uint32_t* st = stats + static_cast<size_t>(k) * 6;
     const uint32_t kn = st[2], ke = st[3], nb = st[4], eb = st[5];
@@ -238,7 +244,7 @@ __global__ void prompt_gather_kernel(int32_t* tokens, const uint64_t* tok_off,
         uint32_t q = static_cast<uint32_t>(j - 1);
         unsigned char ch;
         if (q < static_cast<uint32_t>(head_len)) {
-            ch = c_header[q];
+            ch = hdr.head[q];
         } else if ((q -= head_len) < nb) {
             int lo = 0, hi = kn - 1;  // last row with np[row] <= q
             while (lo < hi) {
@@ -251,7 +257,7 @@ __global__ void prompt_gather_kernel(int32_t* tokens, const uint64_t* tok_off,
             uint64_t len = node_text_off[node + 1] - node_text_off[node];
             ch = o < len ? node_text[node_text_off[node] + o] : '\n';
         } else if ((q -= nb) < static_cast<uint32_t>(ehead_len)) {
-            ch = c_edge_header[q];
+            ch = hdr.edge[q];
         } else {
             q -= ehead_len;
             int lo = 0, hi = ke - 1;
@@ -301,17 +307,17 @@ void union_prompt(Ctx* c, const UnionArgs& a) {
     SGC_LAUNCH_CHECK(c);
 }
 
-void set_prompt_headers(const char* head, int head_len, const char* ehead, int ehead_len) {
-    SGC_CUDA_CHECK(cudaMemcpyToSymbol(c_header, head, head_len));
-    SGC_CUDA_CHECK(cudaMemcpyToSymbol(c_edge_header, ehead, ehead_len));
-}
-
 void prompt_gather(Ctx* c, const GatherArgs& a) {
+    PromptHeaders hdr{};
+    if (a.head_len > static_cast<int>(sizeof(hdr.head)) || a.ehead_len > static_cast<int>(sizeof(hdr.edge)))
+        fail(SGC_LOGIC, "prompt header too long");
+    std::memcpy(hdr.head, a.head, a.head_len);
+    std::memcpy(hdr.edge, a.ehead, a.ehead_len);
     Ctx::Timed timer(c, "prompt_gather");
     dim3 grid(ceil_div(a.max_tokens, 256), a.clusters);
     prompt_gather_kernel<<<grid, 256, 0, c->stream>>>(
         a.tokens, a.tok_off, a.stats, a.sel_nodes, a.sel_edges, a.node_pre, a.edge_pre, a.node_text,
-        a.node_text_off, a.edge_text, a.edge_text_off, a.n_nodes, a.n_edges, a.head_len, a.ehead_len);
+        a.node_text_off, a.edge_text, a.edge_text_off, a.n_nodes, a.n_edges, a.head_len, a.ehead_len, hdr);
     SGC_LAUNCH_CHECK(c);
 }
 

@@ -62,7 +62,8 @@ struct GatherArgs {
     const uint64_t* edge_text_off;
     int n_nodes, n_edges;
     int head_len, ehead_len;
+    const char* head;   // host bytes: header + node csv header + '\n' (build_prompt, cache_engine.cpp:29-71)
+    const char* ehead;  // host bytes: edge csv header + '\n'
 };
-void set_prompt_headers(const char* head, int head_len, const char* ehead, int ehead_len);
 void prompt_gather(Ctx* c, const GatherArgs& a);
 }  // namespace sgc
