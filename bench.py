@@ -113,7 +113,7 @@ def build_workload(args):
     return w
 
 
-def lm_flops(w, prefix_lens, members_q, labels):
+def lm_flops(w, prefix_lens, members_q, labels, all_prefix=None):
     """FLOPs of one batch as executed (SURVEY.md 8(d)): F_tok = 2 L (4 d^2 + 2 d ffn);
     prefill P F_tok + 2 d L P (P+1); member S F_tok + 4 d L (S P + S (S+1)/2); + heads -- minus
     the last layer's dead work the library skips (api.cu forward_rows): after the last layer's
@@ -132,7 +132,7 @@ def lm_flops(w, prefix_lens, members_q, labels):
         skipped_rows += P
         attn -= 2.0 * d * P * (P + 1)  # the last layer's attention
     for S, c in zip(members_q, labels):
-        P = prefix_lens[c]
+        P = (all_prefix or prefix_lens)[c]
         gemm += S * ftok
         attn += 4.0 * d * L * (S * P + S * (S + 1) / 2)
         skipped_rows += S - 1
@@ -170,27 +170,21 @@ def run_ours(args, rank, world, local_rank):
     setup_s = time.time() - t0
     d = w.lm["model_dim"]
     pg = None
+    from paper_2505_10951_b200 import dist as D
+
     if world > 1:
         import torch.distributed as dist
 
         pg = dist
-    from paper_2505_10951_b200 import dist as D
-
-    # this rank's encode shard (contiguous query ranges)
-    lo, hi = D.shard_range(m, world, rank)
+        # the library does the path's exchanges itself: NCCL over NVLink (or the gloo host
+        # transport when ranks share a GPU): sharded encode + embedding all-gather, split
+        # clusters' sealed prefixes point to point, outputs gathered to rank 0
+        D.init_library_comm(ctx, dist, "nccl" if COLL_DEV == "cuda" else "gloo")
+    split = world > 1 and not args.no_split
 
     def step():
-        emb = None
-        if world > 1:
-            shard = host.encode_subgraphs(ctx, dg, w.retrieved[lo:hi], pb.gnn)
-            emb = D.gather_rows(torch.from_numpy(shard).to(COLL_DEV), m, world, pg).cpu().numpy()
-        res = host.run_subgcache(ctx, lm, dg, pb, embeddings=emb, rank=rank, world_size=world,
-                                 want_logits=False, device_inputs=True, waves=args.waves,
-                                 split_clusters=world > 1 and not args.no_split)
-        if world > 1:
-            res.first_token = D.combine_first_tokens(
-                torch.from_numpy(res.first_token.astype(np.int64)).to(COLL_DEV), pg)
-        return res
+        return host.run_subgcache(ctx, lm, dg, pb, want_logits=False, device_inputs=True, waves=args.waves,
+                                  split_clusters=split, transfer_prefix=not args.replica_prefill)
 
     for _ in range(args.warmup):
         res = step()
@@ -234,17 +228,8 @@ def run_ours(args, rank, world, local_rank):
     e2e = None
     if not args.no_e2e:
         def step_e2e():
-            emb = None
-            if world > 1:
-                shard = host.encode_subgraphs(ctx, dg, w.retrieved[lo:hi], pb.gnn)
-                emb = D.gather_rows(torch.from_numpy(shard).to(COLL_DEV), m, world, pg).cpu().numpy()
-            r = host.run_subgcache(ctx, lm, dg, pb, embeddings=emb, rank=rank, world_size=world,
-                                   want_logits=True, waves=args.waves,
-                                   split_clusters=world > 1 and not args.no_split)
-            if world > 1:
-                r.first_token = D.combine_first_tokens(
-                    torch.from_numpy(r.first_token.astype(np.int64)).to(COLL_DEV), pg)
-            return r
+            return host.run_subgcache(ctx, lm, dg, pb, want_logits=True, waves=args.waves,
+                                      split_clusters=split, transfer_prefix=not args.replica_prefill)
 
         ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
@@ -350,21 +335,34 @@ def run_ours(args, rank, world, local_rank):
                 "mean_nodes": round(float(np.mean([len(s.node_ids) for s in sub])), 2),
                 "graph": {"nodes": len(w.graph.nodes), "edges": len(w.graph.edges)}}
 
-    if world > 1:
-        # every query is served by one rank: its TTFT is that rank's value (others report -1)
-        tt = torch.from_numpy(np.stack(ttfts)).to(COLL_DEV)
-        pg.all_reduce(tt, op=pg.ReduceOp.MAX)
-        ttfts = list(tt.cpu().numpy())
+    # rank 0 holds every query's TTFT (the library gathers outputs to rank 0)
     allt = np.concatenate(ttfts)
     allt = allt[allt >= 0]
     ttft_p50, ttft_p90 = float(np.percentile(allt, 50)), float(np.percentile(allt, 90))
-    if rank != 0:
-        return None
-    # ---- roofline of the dominant kernel (the tcgen05 GEMM, tensor-bound)
+    # ---- roofline of the dominant kernel (the tcgen05 GEMM, tensor-bound): FLOPs this rank
+    # executed (the representatives it prefilled -- a replica counts once per prefilling rank, a
+    # received prefix not at all -- and the members it served) over this rank's GEMM time; at
+    # N > 1 both are summed over ranks (the per-GPU average rate)
     labels = res.labels
     prefix_lens = [int(x) for x in res.prefix_len]
     members_q = [len(q) for q in pb.q]
-    gemm_f, attn_f, head_f, fam_f = lm_flops(w, prefix_lens, members_q, labels)
+    mine_c = [c for c in range(len(prefix_lens)) if res.prefilled[c]]
+    mine_q = [q for q in range(m) if res.query_rank[q] == rank]
+    gemm_f, attn_f, head_f, fam_f = lm_flops(w, [prefix_lens[c] for c in mine_c],
+                                             [members_q[q] for q in mine_q], [labels[q] for q in mine_q],
+                                             all_prefix=prefix_lens)
+    fam_ms = {k: kt[k][0] for k in fam_f}
+    if world > 1:
+        keys = sorted(fam_f)
+        t = torch.tensor([gemm_f, attn_f, head_f, gemm_ms, float(gemm_n)] + [fam_f[k] for k in keys] +
+                         [fam_ms[k] for k in keys], dtype=torch.float64, device=COLL_DEV)
+        pg.all_reduce(t)
+        v = t.cpu().tolist()
+        gemm_f, attn_f, head_f, gemm_ms, gemm_n = v[:5]
+        fam_f = dict(zip(keys, v[5:5 + len(keys)]))
+        fam_ms = dict(zip(keys, v[5 + len(keys):]))
+    if rank != 0:
+        return None
     peaks, pk_kind = load_peaks()
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     gemm_tf = (gemm_f * args.steps) / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0.0
@@ -381,13 +379,13 @@ def run_ours(args, rank, world, local_rank):
                 "traffic": prof,
                 "flops_per_launch": gemm_f / max(1, gemm_n / args.steps),
                 "avg_launch_ms": gemm_ms / max(1, gemm_n)}
-    step_tf = (gemm_f + attn_f + head_f) / (ms_per_step / 1e3) / 1e12
+    step_tf = (gemm_f + attn_f + head_f) / (ms_per_step / 1e3) / 1e12 / world  # per GPU
     # per fused-epilogue GEMM family: algorithmic FLOPs of the step / its event time
     L, d, f = w.lm["layers"], w.lm["model_dim"], w.lm["ffn_hidden"]
     rows = sum(prefix_lens) + sum(members_q)
-    gemm_families = {k: {"ms_per_step": round(kt[k][0] / args.steps, 3),
-                         "tflops": round(fam_f[k] * args.steps / (kt[k][0] / 1e3) / 1e12, 1)}
-                     for k in fam_f if kt[k][1]}
+    gemm_families = {k: {"ms_per_step": round(fam_ms[k] / args.steps / world, 3),
+                         "tflops": round(fam_f[k] * args.steps / (fam_ms[k] / 1e3) / 1e12, 1)}
+                     for k in fam_f if fam_ms[k] > 0}
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "queries/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3),
@@ -549,6 +547,9 @@ def main():
                     help="waves of the generation run (cost-balanced cuts; scripts/defer_probe.py: "
                          "2 waves gave the shortest batch and RT p50 at C3, 4 the lowest RT mean)")
     ap.add_argument("--no-pairs", action="store_true", help="1-CTA GEMM instead of CTA pairs")
+    ap.add_argument("--replica-prefill", action="store_true",
+                    help="N > 1: split clusters' helper ranks prefill a replica instead of receiving the "
+                         "sealed prefix point to point")
     ap.add_argument("--waves", type=int, default=2,
                     help="serve clusters in this many waves (lower TTFT p50); 1 = one pass")
     args = ap.parse_args()
@@ -557,6 +558,25 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N`: launch the N ranks ourselves (one process per GPU)
+        if args.impl == "ours" and os.environ.get("SGC_DIST_BACKEND", "nccl") == "nccl":
+            import torch
+
+            have = torch.cuda.device_count()
+            if have < args.gpus:
+                raise SystemExit(f"--gpus {args.gpus} but only {have} CUDA device(s) are visible")
+        import socket
+
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        raise SystemExit(subprocess.call(cmd))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
     if args.impl == "reference":
         if rank == 0:
             print(json.dumps(run_reference(args)))

@@ -92,6 +92,32 @@ int sgc_ctx_set_stream(sgc_ctx* ctx, void* stream);
 /* Number of kernel launches issued by this context since creation (bench evidence). */
 uint64_t sgc_ctx_launch_count(const sgc_ctx* ctx);
 
+/* ---- multi-GPU transport -----------------------------------------------
+ * A context joins a group of `world` ranks (one process or thread per GPU); sgc_run_subgcache
+ * then does the path's only exchanges itself: the all-gather of subgraph embeddings before
+ * clustering, the point-to-point copy of a split cluster's sealed prefix K/V to the ranks serving
+ * the rest of its members (instead of a replica prefill; the reference's fork shares the sealed
+ * prefix by pointer, cache_engine.cpp:183), and the gather of per-query outputs to rank 0.
+ * NCCL (NVLink / NVSwitch): rank 0 makes an id with sgc_comm_unique_id, every rank passes the same
+ * 128 bytes to sgc_comm_init_nccl (libnccl.so.2 is resolved at run time). Host transport: C
+ * callbacks over HOST buffers (e.g. torch.distributed gloo, or in-process ranks); both return
+ * 0 on success. */
+typedef struct {
+    void* user;
+    /* recv[world * bytes] <- every rank's send[bytes], in rank order */
+    int (*allgather)(void* user, const void* send, void* recv, size_t bytes);
+    /* post every send and receive of this rank together, return when all completed */
+    int (*exchange)(void* user, int n_send, const void* const* send_buf, const size_t* send_bytes,
+                    const int* send_peer, int n_recv, void* const* recv_buf, const size_t* recv_bytes,
+                    const int* recv_peer);
+} sgc_host_transport;
+int sgc_comm_unique_id(uint8_t id[128]);
+int sgc_comm_init_nccl(sgc_ctx* ctx, const uint8_t id[128], int world, int rank);
+int sgc_comm_init_host(sgc_ctx* ctx, const sgc_host_transport* t, int world, int rank);
+int sgc_comm_destroy(sgc_ctx* ctx);
+/* 1 if the context has a transport with world > 1 (out: world, rank, kind 0 none / 1 nccl / 2 host) */
+int sgc_comm_info(const sgc_ctx* ctx, int* world, int* rank, int* kind);
+
 /* ---- model: ToyLm::ToyLm (lm_core.cpp:122-161) -------------------------------------
  * Weights are generated ON DEVICE from the seed, element-for-element identical to the
  * reference's fp32 SplitMix64 streams, then stored as bf16 (GEMM operands) and fp32
@@ -235,8 +261,8 @@ typedef struct {
      * own. cluster_owner (optional) forces the assignment. */
     const float* precomputed_embeddings; /* [m * dim] (all-gathered) or NULL to encode here */
     const uint32_t* cluster_owner;       /* [c] or NULL = LPT over world_size */
-    int rank;
-    int world_size;                      /* 0 or 1 = single GPU */
+    int rank;                            /* ignored when the context has a transport (its rank) */
+    int world_size;                      /* 0 or 1 = single GPU; with a transport: 0 or its world */
     /* clusters are served in `waves` groups of balanced cost (index order): members of an early
      * wave get their first token before later waves run (lower TTFT); 0/1 = one pass */
     uint32_t waves;
@@ -249,6 +275,11 @@ typedef struct {
      * beats replicating the cluster's prefix there (the receiving rank prefills the identical
      * representative itself; sgc_balance_members is the plan) */
     int split_clusters;
+    /* split clusters with a context transport: 1 = the rank that prefilled the representative
+     * sends its sealed K/V to the other serving ranks (point to point) when the copy costs less
+     * than a prefill (bytes over NVLink vs FLOPs on the tensor cores), else they prefill an
+     * identical replica; 2 = always send; 0 = always replicate. Ignored without a transport. */
+    int transfer_prefix;
 } sgc_batch;
 
 typedef struct {
@@ -278,6 +309,13 @@ typedef struct {
      *              standalone prefill for a fallback) -> first token */
     float* seal_ms;
     float* pftt_ms;
+    /* multi-GPU bookkeeping (optional, HOST memory): query_rank [m] = rank that served each query;
+     * prefilled [c] = 1 if THIS rank ran the representative's prefill (0 for a received copy).
+     * With a context transport, logits / first_token / fallback / ttft_ms / pftt_ms / tokens /
+     * n_tokens / rt_ms of every query are gathered to rank 0 (other ranks hold their own). */
+    uint32_t* query_rank;
+    uint8_t* prefilled;
+    uint64_t prefix_bytes_sent, prefix_bytes_received; /* sealed K/V moved point to point */
 } sgc_batch_out;
 
 int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_batch* batch,

@@ -83,7 +83,7 @@ class Batch(C.Structure):
                 ("precomputed_embeddings", C.POINTER(C.c_float)),
                 ("cluster_owner", C.POINTER(C.c_uint32)), ("rank", C.c_int),
                 ("world_size", C.c_int), ("waves", C.c_uint32), ("max_new_tokens", C.c_uint32),
-                ("split_clusters", C.c_int)]
+                ("split_clusters", C.c_int), ("transfer_prefix", C.c_int)]
 
 
 class BatchOut(C.Structure):
@@ -97,7 +97,49 @@ class BatchOut(C.Structure):
                 ("prefill_rows", C.c_uint64), ("extend_rows", C.c_uint64),
                 ("tokens", C.POINTER(C.c_int32)), ("n_tokens", C.POINTER(C.c_uint32)),
                 ("rt_ms", C.POINTER(C.c_float)), ("decode_rows", C.c_uint64),
-                ("seal_ms", C.POINTER(C.c_float)), ("pftt_ms", C.POINTER(C.c_float))]
+                ("seal_ms", C.POINTER(C.c_float)), ("pftt_ms", C.POINTER(C.c_float)),
+                ("query_rank", C.POINTER(C.c_uint32)), ("prefilled", C.POINTER(C.c_uint8)),
+                ("prefix_bytes_sent", C.c_uint64), ("prefix_bytes_received", C.c_uint64)]
+
+
+# sgc_host_transport callbacks (include/sgc_b200.h)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
+                          C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p), C.POINTER(C.c_size_t),
+                          C.POINTER(C.c_int))
+
+
+class HostTransport(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allgather", ALLGATHER_FN), ("exchange", EXCHANGE_FN)]
+
+
+def make_host_transport(t):
+    """sgc_host_transport whose callbacks call t.allgather / t.exchange (see host.Context);
+    returns (struct, callbacks) -- keep both alive while the context uses them."""
+
+    def _allgather(user, send, recv, nbytes):
+        try:
+            out = t.allgather(C.string_at(send, nbytes), nbytes)
+            C.memmove(recv, out, len(out))
+            return 0
+        except Exception as e:  # noqa: BLE001 -- reported as a status to the C side
+            print("host transport allgather failed:", e)
+            return 1
+
+    def _exchange(user, ns, sbuf, sbytes, speer, nr, rbuf, rbytes, rpeer):
+        try:
+            sends = [(C.string_at(sbuf[i], sbytes[i]), speer[i]) for i in range(ns)]
+            recvs = [(rbytes[i], rpeer[i]) for i in range(nr)]
+            got = t.exchange(sends, recvs)
+            for i in range(nr):
+                C.memmove(rbuf[i], got[i], rbytes[i])
+            return 0
+        except Exception as e:  # noqa: BLE001
+            print("host transport exchange failed:", e)
+            return 1
+
+    cbs = (ALLGATHER_FN(_allgather), EXCHANGE_FN(_exchange))
+    return HostTransport(None, cbs[0], cbs[1]), cbs
 
 
 # every symbol include/sgc_b200.h declares (checked by tests/test_boundary.py)
@@ -109,6 +151,7 @@ EXPORTS = [
     "sgc_kv_release", "sgc_kv_count", "sgc_kv_tokens", "sgc_kv_digest", "sgc_kv_resident_bytes",
     "sgc_kv_read", "sgc_extend", "sgc_run_subgcache", "sgc_gemm_bf16", "sgc_set_timing",
     "sgc_get_timing", "sgc_lpt_assign", "sgc_set_option", "sgc_attention_bf16", "sgc_extend_generate", "sgc_retrieve", "sgc_balance_members",
+    "sgc_comm_unique_id", "sgc_comm_init_nccl", "sgc_comm_init_host", "sgc_comm_destroy", "sgc_comm_info",
 ]
 
 _lib = None
@@ -178,6 +221,11 @@ def load() -> C.CDLL:
     L.sgc_lpt_assign.argtypes = [P(C.c_double), C.c_uint32, C.c_int, P(C.c_uint32)]
     L.sgc_balance_members.argtypes = [P(C.c_double), C.c_uint32, P(C.c_uint32), P(C.c_double), C.c_uint32,
                                       C.c_int, P(C.c_uint32), P(C.c_uint32)]
+    L.sgc_comm_unique_id.argtypes = [P(C.c_uint8)]
+    L.sgc_comm_init_nccl.argtypes = [vp, P(C.c_uint8), C.c_int, C.c_int]
+    L.sgc_comm_init_host.argtypes = [vp, P(HostTransport), C.c_int, C.c_int]
+    L.sgc_comm_destroy.argtypes = [vp]
+    L.sgc_comm_info.argtypes = [vp, P(C.c_int), P(C.c_int), P(C.c_int)]
     _lib = L
     return L
 

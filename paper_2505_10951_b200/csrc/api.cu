@@ -416,9 +416,12 @@ std::vector<sgc::AttnWork> make_work(const std::vector<int>& group_start, const 
 
 // ============================================================ prefill / extend
 
+// n_remote: the last n_remote sequences are laid out (segments, context tokens, arena rows) but not
+// computed -- their sealed K/V arrive point to point from the rank that prefilled them; the
+// forward covers the leading local rows only (last_logits: local sequences only).
 sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in, const int32_t* tok_in,
                    const float* soft, const uint8_t* soft_mask, float* last_logits, bool arena = false,
-                   uint64_t arena_row0 = 0, uint64_t arena_rows = 0, bool sync = true) {
+                   uint64_t arena_row0 = 0, uint64_t arena_rows = 0, bool sync = true, uint32_t n_remote = 0) {
     std::vector<uint64_t> off = to_host(c, off_in, count + 1);
     std::vector<int32_t> toks = to_host(c, tok_in, off[count]);
     std::vector<uint8_t> smask = soft_mask ? to_host(c, soft_mask, count) : std::vector<uint8_t>(count, 0);
@@ -458,6 +461,9 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
     }
     const int M = static_cast<int>(rows_tok.size());
     kv->rows = M;
+    if (n_remote > count) fail(SGC_LOGIC, "prefill: more remote sequences than sequences");
+    const uint32_t n_local = count - n_remote;
+    const int M_local = n_local < count ? static_cast<int>(kv->off[n_local]) : M;
     if (arena) {
         // batch-internal sealed prefixes: one grow-only arena [L][arena_rows][d] holding every
         // wave's prefixes at row offsets (arena_rows == 0: just this call's rows)
@@ -488,8 +494,8 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
         d_soft = c->buf<float>("pf_soft", static_cast<size_t>(count) * d);
         sgc::copy_in(c, d_soft, soft, static_cast<size_t>(count) * d);
     }
-    std::vector<int> gs, gr, z(count, 0);
-    for (uint32_t s = 0; s < count; ++s) {
+    std::vector<int> gs, gr, z(n_local, 0);
+    for (uint32_t s = 0; s < n_local; ++s) {
         gs.push_back(static_cast<int>(kv->off[s]));
         gr.push_back(static_cast<int>(kv->len[s]));
     }
@@ -502,7 +508,7 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
     sgc::copy_in(c, d_work, work.data(), work.size());
 
     FwdBatch b;
-    b.M = M;
+    b.M = M_local;
     b.d_tokens = kv->d_tokens;
     b.d_soft = d_soft;
     b.d_soft_idx = any_soft ? d_sidx : nullptr;
@@ -515,10 +521,10 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
     b.v_loc = [kvp](int l) { return kvp->v_layer(l); };
     b.d_logit_rows = d_lr;
     // no logits requested (a representative's prompt): the last layer stops after its K/V
-    b.n_logits = last_logits ? static_cast<int>(count) : 0;
+    b.n_logits = last_logits ? static_cast<int>(n_local) : 0;
     b.d_logits = last_logits ? d_logits : nullptr;
-    forward_rows(c, m, b);
-    if (last_logits) sgc::copy_out(c, last_logits, d_logits, static_cast<size_t>(count) * SGC_VOCAB);
+    if (M_local > 0) forward_rows(c, m, b);
+    if (last_logits && n_local) sgc::copy_out(c, last_logits, d_logits, static_cast<size_t>(n_local) * SGC_VOCAB);
     if (sync) {  // else: the caller syncs (last_logits must then be pinned or null)
         c->sync();
         check_forward_flags(c);
@@ -979,6 +985,18 @@ HostSubs host_subs(Ctx* c, const sgc_subgraphs* s) {
     return h;
 }
 
+// subgraphs [lo, hi) of a CSR batch
+HostSubs slice_subs(const HostSubs& h, uint32_t lo, uint32_t hi) {
+    HostSubs s;
+    for (uint32_t i = lo; i <= hi; ++i) {
+        s.noff.push_back(h.noff[i] - h.noff[lo]);
+        s.eoff.push_back(h.eoff[i] - h.eoff[lo]);
+    }
+    s.nodes.assign(h.nodes.begin() + h.noff[lo], h.nodes.begin() + h.noff[hi]);
+    s.edges.assign(h.edges.begin() + h.eoff[lo], h.edges.begin() + h.eoff[hi]);
+    return s;
+}
+
 uint32_t dense_index(const sgc_graph* g, uint32_t id) {
     auto it = std::lower_bound(g->ids.begin(), g->ids.end(), id);
     if (it == g->ids.end() || *it != id)
@@ -1215,10 +1233,13 @@ std::vector<uint32_t> lpt_assign(const std::vector<double>& cost, int world) {
 // members of the busiest rank's largest cluster move over (highest query index first) -- the
 // receiving rank prefills that prefix itself (a replica: same representative, same tokens), so
 // no KV crosses GPUs. Deterministic: every rank computes the same plan from the same labels.
+// replica_cost (optional): what another serving rank pays to hold the prefix (default: its
+// prefill; with a transport, the point-to-point copy of the sealed K/V).
 std::vector<uint32_t> balance_members(const std::vector<double>& prefill_cost,
                                       const std::vector<std::vector<uint32_t>>& members,
                                       const std::vector<double>& member_cost, int world,
-                                      std::vector<uint32_t>& cluster_owner) {
+                                      std::vector<uint32_t>& cluster_owner,
+                                      const std::vector<double>* replica_cost = nullptr) {
     const size_t k = prefill_cost.size();
     std::vector<double> cost(k);
     for (size_t ci = 0; ci < k; ++ci) {
@@ -1266,7 +1287,7 @@ std::vector<uint32_t> balance_members(const std::vector<double>& prefill_cost,
             const uint32_t q = *it;
             if (qown[q] != static_cast<uint32_t>(rmax)) continue;
             const bool has = replica.count({static_cast<uint32_t>(best), static_cast<uint32_t>(rmin)}) != 0;
-            const double add = member_cost[q] + (has ? 0.0 : prefill_cost[best]);
+            const double add = member_cost[q] + (has ? 0.0 : (replica_cost ? (*replica_cost)[best] : prefill_cost[best]));
             const double before = std::max(load[rmax], load[rmin]);
             const double after = std::max(load[rmax] - member_cost[q], load[rmin] + add);
             if (!(after < before * (1.0 - 1e-9))) break;
@@ -1428,6 +1449,7 @@ int sgc_ctx_destroy(sgc_ctx* ctx) {
         if (!ctx) return;
         Ctx* c = current(&ctx->c);
         cudaStreamSynchronize(c->stream);
+        ctx->comm.reset();
         for (auto& kv : c->scratch) cudaFree(kv.second.ptr);
         auto it = g_enc.find(c);
         if (it != g_enc.end()) {
@@ -1455,6 +1477,40 @@ int sgc_ctx_set_stream(sgc_ctx* ctx, void* stream) {
 }
 
 uint64_t sgc_ctx_launch_count(const sgc_ctx* ctx) { return ctx ? ctx->c.launches : 0; }
+
+int sgc_comm_unique_id(uint8_t id[128]) {
+    return guarded([&] { sgc::nccl_unique_id(id); });
+}
+
+int sgc_comm_init_nccl(sgc_ctx* ctx, const uint8_t id[128], int world, int rank) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world) fail(SGC_DOMAIN, "comm: rank must lie in [0, world)");
+        Ctx* c = current(&ctx->c);
+        ctx->comm.reset(sgc::comm_nccl(c, id, world, rank));
+    });
+}
+
+int sgc_comm_init_host(sgc_ctx* ctx, const sgc_host_transport* t, int world, int rank) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world) fail(SGC_DOMAIN, "comm: rank must lie in [0, world)");
+        ctx->comm.reset(sgc::comm_host(t, world, rank));
+    });
+}
+
+int sgc_comm_destroy(sgc_ctx* ctx) {
+    return guarded([&] {
+        current(&ctx->c)->sync();
+        ctx->comm.reset();
+    });
+}
+
+int sgc_comm_info(const sgc_ctx* ctx, int* world, int* rank, int* kind) {
+    const sgc::Comm* cm = ctx ? ctx->comm.get() : nullptr;
+    if (world) *world = cm ? cm->world : 1;
+    if (rank) *rank = cm ? cm->rank : 0;
+    if (kind) *kind = cm ? (std::string(cm->kind()) == "nccl" ? 1 : 2) : 0;
+    return cm && cm->world > 1 ? 1 : 0;
+}
 
 int sgc_model_create(sgc_ctx* ctx, const sgc_lm_config* cfg, sgc_model** out) {
     return guarded([&] {
@@ -2082,6 +2138,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
     return guarded([&] {
         Ctx* c = current(&ctx->c);
         const double t_start = now_ms();
+        o->prefix_bytes_sent = o->prefix_bytes_received = 0;
         const uint32_t m = b->retrieved.count;
         const uint32_t d = model->d;
         if (m == 0) fail(SGC_DOMAIN, "no queries to run");
@@ -2093,10 +2150,37 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         const uint32_t budget = reserved >= lc.max_seq_len ? 0 : lc.max_seq_len - reserved;
         if (budget <= 1) fail(SGC_DOMAIN, "max_seq too small for the question budget and generation cap");
         HostSubs hs = host_subs(c, &b->retrieved);
+        // ---- multi-GPU: the context's transport (comm.cuh) or a caller-driven plan
+        sgc::Comm* comm = ctx->comm.get();
+        const bool use_comm = comm && comm->world > 1;
+        if (use_comm && b->world_size > 1 && b->world_size != comm->world)
+            fail(SGC_DOMAIN, "batch world_size differs from the context transport's");
+        const int world = use_comm ? comm->world : (b->world_size > 1 ? b->world_size : 1);
+        const uint32_t me = use_comm ? static_cast<uint32_t>(comm->rank)
+                                     : static_cast<uint32_t>(world > 1 || b->cluster_owner ? b->rank : 0);
         // ---- (1) embeddings
         float* d_emb = c->buf<float>("run_emb", static_cast<size_t>(m) * d);
         if (b->precomputed_embeddings) {
             sgc::copy_in(c, d_emb, b->precomputed_embeddings, static_cast<size_t>(m) * d);
+        } else if (use_comm) {
+            // data-parallel encode: rank r embeds the contiguous shard [r m / W, (r + 1) m / W),
+            // then ONE all-gather (NCCL over NVLink) assembles [m x d] in query order on every rank
+            auto lo_of = [&](int r) { return static_cast<uint32_t>(static_cast<uint64_t>(r) * m / world); };
+            uint32_t mx = 1;
+            for (int r = 0; r < world; ++r) mx = std::max(mx, lo_of(r + 1) - lo_of(r));
+            const uint32_t lo = lo_of(static_cast<int>(me)), hi = lo_of(static_cast<int>(me) + 1);
+            const size_t shard_elems = static_cast<size_t>(mx) * d;
+            float* shard = c->buf<float>("run_emb_shard", shard_elems);
+            SGC_CUDA_CHECK(cudaMemsetAsync(shard, 0, shard_elems * sizeof(float), c->stream));
+            sgc_gnn_config gc = b->gnn;
+            gc.dim = d;
+            if (hi > lo) encode_subgraphs(c, g, gc, slice_subs(hs, lo, hi), hi - lo, shard);
+            float* all = c->buf<float>("run_emb_all", shard_elems * world);
+            comm->allgather(c, shard, all, shard_elems * sizeof(float));
+            for (int r = 0; r < world; ++r)
+                SGC_CUDA_CHECK(cudaMemcpyAsync(d_emb + static_cast<size_t>(lo_of(r)) * d, all + shard_elems * r,
+                                               static_cast<size_t>(lo_of(r + 1) - lo_of(r)) * d * sizeof(float),
+                                               cudaMemcpyDeviceToDevice, c->stream));
         } else {
             sgc_gnn_config gc = b->gnn;
             gc.dim = d;
@@ -2120,17 +2204,19 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         RepResult reps_all = build_reps(c, g, hs, m, members, budget);
         std::vector<uint64_t> q_off_all = to_host(c, b->questions.off, m + 1);
         std::vector<uint32_t> owner(k, 0);
-        const int world = b->world_size > 1 ? b->world_size : 1;
-        const uint32_t me = static_cast<uint32_t>(world > 1 || b->cluster_owner ? b->rank : 0);
         std::vector<uint32_t> qown;  // member-level plan (split_clusters): query -> rank
-        if (b->cluster_owner) {
-            owner = to_host(c, b->cluster_owner, k);
-        } else if (world > 1) {
-            std::vector<double> pcost(k, 0.0), mcost(m, 0.0), cost(k, 0.0);
+        // split clusters' sealed prefixes travel point to point (instead of replica prefills)
+        const bool transfer = use_comm && b->split_clusters && b->transfer_prefix;
+        // cost model (FLOPs): a representative's prefill, each member's extend, and the copy of a
+        // sealed prefix over NVLink in FLOP-equivalents (bytes x sustained tensor FLOP/s / link B/s)
+        std::vector<double> pcost(k, 0.0), mcost(m, 0.0), cost(k, 0.0), xcost(k, 0.0);
+        {
             const double ftok = 2.0 * model->L * (4.0 * d * d + 2.0 * d * model->ffn);
+            constexpr double kFlopPerLinkByte = 1.35e15 / 6.0e11;
             for (uint32_t ci = 0; ci < k; ++ci) {
                 const double P = static_cast<double>(reps_all.prefix_off[ci + 1] - reps_all.prefix_off[ci]);
                 pcost[ci] = P * ftok + 2.0 * d * model->L * P * P;
+                xcost[ci] = P * 2.0 * model->L * d * sizeof(bf16) * kFlopPerLinkByte;
                 cost[ci] = pcost[ci];
                 for (uint32_t q : members[ci]) {
                     const double S = static_cast<double>(q_off_all[q + 1] - q_off_all[q]);
@@ -2138,16 +2224,50 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                     cost[ci] += mcost[q];
                 }
             }
-            if (b->split_clusters) qown = balance_members(pcost, members, mcost, world, owner);
-            else owner = lpt_assign(cost, world);
         }
+        // a split cluster's other serving ranks receive the sealed K/V when the copy is cheaper
+        // than prefilling a replica (C3: 1.1 GB ~ 2.4 TFLOP-eq vs a 25 TFLOP prefill; the tiny C1
+        // model: replicas), or always with transfer_prefix == 2
+        std::vector<uint8_t> xfer(k, 0);
+        for (uint32_t ci = 0; ci < k; ++ci)
+            xfer[ci] = transfer && (b->transfer_prefix == 2 || xcost[ci] < pcost[ci]) ? 1 : 0;
+        if (b->cluster_owner) {
+            owner = to_host(c, b->cluster_owner, k);
+        } else if (world > 1) {
+            if (b->split_clusters) {
+                std::vector<double> rcost(k, 0.0);
+                for (uint32_t ci = 0; ci < k; ++ci) rcost[ci] = xfer[ci] ? std::min(pcost[ci], xcost[ci]) : pcost[ci];
+                qown = balance_members(pcost, members, mcost, world, owner, &rcost);
+            } else {
+                owner = lpt_assign(cost, world);
+            }
+        }
+        // every rank knows who serves what (the plan is deterministic)
+        std::vector<uint32_t> qrank(m, 0);
+        for (uint32_t i = 0; i < m; ++i) qrank[i] = qown.empty() ? owner[labels[i]] : qown[i];
+        if (o->query_rank) std::memcpy(o->query_rank, qrank.data(), m * sizeof(uint32_t));
+        // a split cluster is served by more than one rank; with `transfer` its owner prefills it
+        // and sends the sealed K/V to the other serving ranks
+        std::vector<std::vector<uint32_t>> peers(k);  // serving ranks other than the owner
+        for (uint32_t ci = 0; ci < k; ++ci) {
+            std::set<uint32_t> rs;
+            for (uint32_t q : members[ci])
+                if (qrank[q] != owner[ci]) rs.insert(qrank[q]);
+            peers[ci].assign(rs.begin(), rs.end());
+        }
+        auto is_split = [&](uint32_t ci) { return xfer[ci] && !peers[ci].empty(); };
+        // representative prompt lengths of every cluster (deterministic on every rank)
+        if (o->prefix_len)
+            for (uint32_t ci = 0; ci < k; ++ci)
+                o->prefix_len[ci] = reps_all.prefix_off[ci + 1] - reps_all.prefix_off[ci] + (b->soft_prefix ? 1 : 0);
         if (o->owner) sgc::copy_out(c, o->owner, owner.data(), k);
         std::vector<uint32_t> owned;
         std::vector<std::vector<uint32_t>> served(k);  // members this rank serves, per cluster
         for (uint32_t ci = 0; ci < k; ++ci) {
             for (uint32_t q : members[ci])
-                if (qown.empty() ? owner[ci] == me : qown[q] == me) served[ci].push_back(q);
-            if (!served[ci].empty()) owned.push_back(ci);
+                if (qrank[q] == me) served[ci].push_back(q);
+            // the owner of a split cluster prefills it even when all its members moved away
+            if (!served[ci].empty() || (is_split(ci) && owner[ci] == me)) owned.push_back(ci);
         }
         // serving order: Smith's rule (ascending row cost per query) so the waves that finish
         // first carry the most queries -- minimizes the summed (mean) TTFT; results are
@@ -2161,6 +2281,13 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             }
             std::stable_sort(owned.begin(), owned.end(), [&](uint32_t a, uint32_t b2) { return ratio[a] < ratio[b2]; });
         }
+        // split clusters first: all of them are served in wave 0, where their K/V are exchanged
+        std::stable_partition(owned.begin(), owned.end(), [&](uint32_t ci) { return is_split(ci); });
+        uint32_t n_split = 0;
+        for (uint32_t ci : owned) n_split += is_split(ci) ? 1 : 0;
+        auto is_remote = [&](uint32_t ci) { return is_split(ci) && owner[ci] != me; };
+        if (o->prefilled)
+            for (uint32_t ci = 0; ci < k; ++ci) o->prefilled[ci] = 0;
         // representatives are built from the FULL membership (a replicated prefix is identical on
         // every rank serving part of the cluster); own_members are the queries served here
         std::vector<std::vector<uint32_t>> own_members, rep_members;
@@ -2170,7 +2297,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         }
         RepResult reps;
         if (!owned.empty()) {
-            if (owned.size() == k && b->waves <= 1) reps = reps_all;
+            if (owned.size() == k && b->waves <= 1 && n_split == 0) reps = reps_all;
             else reps = build_reps(c, g, hs, m, rep_members, budget);
         }
         std::vector<float> soft_h;
@@ -2276,6 +2403,12 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 w0 = e;
             }
             wave_end.swap(split);
+            if (n_split > 0) {  // wave 0 holds every split cluster (one exchange point)
+                std::vector<uint32_t> we2{std::max(wave_end.front(), n_split)};
+                for (uint32_t e : wave_end)
+                    if (e > we2.back()) we2.push_back(e);
+                wave_end.swap(we2);
+            }
         }
         cudaEvent_t ev_start = c->event();
         SGC_CUDA_CHECK(cudaEventRecord(ev_start, c->stream));
@@ -2379,21 +2512,28 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             ExtendKeep keep = keep_all;
             keep.base = retain ? keep_row0 : 0;
             if (!retain) arena_row0 = 0;
-            for (uint32_t i = wb; i < we; ++i) {
+            // sequences of the wave: local representatives, standalone fallbacks, then the split
+            // clusters' representatives whose sealed K/V arrive from their owner (not computed here)
+            std::vector<uint32_t> seq_of(we - wb, 0), remote_i, mem_cl;
+            auto push_rep = [&](uint32_t i) {
+                seq_of[i - wb] = static_cast<uint32_t>(seq_off.size() - 1);
                 seq_tok.insert(seq_tok.end(), rep_tok.begin() + reps.prefix_off[i], rep_tok.begin() + reps.prefix_off[i + 1]);
                 seq_off.push_back(seq_tok.size());
                 seq_soft.push_back(d_soft ? 1 : 0);
                 if (d_soft) seq_soft_vec.insert(seq_soft_vec.end(), soft_all.begin() + static_cast<size_t>(i) * d, soft_all.begin() + static_cast<size_t>(i + 1) * d);
                 else seq_soft_vec.insert(seq_soft_vec.end(), d, 0.f);
+            };
+            for (uint32_t i = wb; i < we; ++i) {
+                if (is_remote(owned[i])) remote_i.push_back(i);
+                else push_rep(i);
                 const uint64_t plen = reps.prefix_off[i + 1] - reps.prefix_off[i] + (d_soft ? 1 : 0);
-                if (o->prefix_len) o->prefix_len[owned[i]] = plen;
                 for (uint32_t q : own_members[i]) {
                     const uint64_t qn = q_off[q + 1] - q_off[q];
                     wave_of[q] = static_cast<int32_t>(wv);
                     if (plen + qn + lc.max_new_tokens > lc.max_seq_len) {  // cache_engine.cpp:171
                         fb_q.push_back(q);
                     } else {
-                        mem_seg.push_back(i - wb);
+                        mem_cl.push_back(i);
                         mem_q.push_back(q);
                     }
                 }
@@ -2416,15 +2556,50 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                     else seq_soft_vec.insert(seq_soft_vec.end(), d, 0.f);
                 }
             }
+            for (uint32_t i : remote_i) push_rep(i);  // trailing: laid out, not computed
+            for (size_t j = 0; j < mem_q.size(); ++j) mem_seg.push_back(seq_of[mem_cl[j] - wb]);
             const uint32_t ns = static_cast<uint32_t>(seq_off.size() - 1);
+            const uint32_t n_remote = static_cast<uint32_t>(remote_i.size());
             // representative logits are only read on the host for standalone fallbacks; without
             // them no sync is needed and the host prepares the next wave while the GPU works
             std::vector<float> seq_logits(fb_q.empty() ? 0 : static_cast<size_t>(ns) * SGC_VOCAB);
             sgc_kv* kv = do_prefill(c, model, ns, seq_off.data(), seq_tok.data(), seq_soft_vec.data(),
                                     seq_soft.data(), fb_q.empty() ? nullptr : seq_logits.data(), /*arena=*/true,
-                                    arena_row0, arena_rows, /*sync=*/!fb_q.empty());
+                                    arena_row0, arena_rows, /*sync=*/!fb_q.empty(), n_remote);
             std::unique_ptr<sgc_kv, int (*)(sgc_kv*)> kv_guard(kv, sgc_kv_release);
-            prefill_rows += kv->rows;
+            prefill_rows += kv->rows - (n_remote ? kv->rows - kv->off[ns - n_remote] : 0);
+            for (uint32_t i = wb; i < we; ++i)
+                if (o->prefilled && !is_remote(owned[i])) o->prefilled[owned[i]] = 1;
+            if (wv == 0 && n_split > 0) {
+                // the split clusters' sealed K/V, owner -> other serving ranks, all layers; both
+                // sides walk clusters in ascending index order, so every pair posts its messages
+                // in the same order (one grouped exchange per rank)
+                std::vector<std::pair<uint32_t, uint32_t>> mine;  // (cluster, wave-local index)
+                for (uint32_t i = wb; i < we; ++i)
+                    if (is_split(owned[i])) mine.push_back({owned[i], i});
+                std::sort(mine.begin(), mine.end());
+                std::vector<sgc::P2P> sends, recvs;
+                for (auto [ci, i] : mine) {
+                    const uint32_t s = seq_of[i - wb];
+                    const size_t bytes = static_cast<size_t>(kv->len[s]) * d * sizeof(bf16);
+                    for (int l = 0; l < model->L; ++l) {
+                        bf16* kp = kv->k_layer(l) + static_cast<size_t>(kv->off[s]) * d;
+                        bf16* vp = kv->v_layer(l) + static_cast<size_t>(kv->off[s]) * d;
+                        if (owner[ci] == me) {
+                            for (uint32_t p : peers[ci]) {
+                                sends.push_back({kp, bytes, static_cast<int>(p)});
+                                sends.push_back({vp, bytes, static_cast<int>(p)});
+                                o->prefix_bytes_sent += 2 * bytes;
+                            }
+                        } else {
+                            recvs.push_back({kp, bytes, static_cast<int>(owner[ci])});
+                            recvs.push_back({vp, bytes, static_cast<int>(owner[ci])});
+                            o->prefix_bytes_received += 2 * bytes;
+                        }
+                    }
+                }
+                comm->exchange(c, sends, recvs);
+            }
             {
                 cudaEvent_t es = c->event();
                 SGC_CUDA_CHECK(cudaEventRecord(es, c->stream));
@@ -2682,6 +2857,70 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         if (o->merge_right) sgc::copy_out(c, o->merge_right, d_right, m - k);
         if (o->merge_dist) sgc::copy_out(c, o->merge_dist, d_dist, m - k);
         c->sync();
+        if (use_comm) {
+            // gather every query's outputs to rank 0: one fixed-size record per
+            // served query, in ascending query order per rank (rank 0 knows every rank's list).
+            // Every rank passes the same set of optional outputs.
+            const size_t gen_w = (gen_on && o->tokens) ? max_new : 0, lg_w = o->logits ? SGC_VOCAB : 0;
+            const size_t W = 6 + gen_w + lg_w;  // 4-byte words per record
+            auto pack = [&](uint32_t q, uint32_t* r) {
+                int32_t ft = o->first_token ? o->first_token[q] : -1;
+                std::memcpy(&r[0], &ft, 4);
+                r[1] = o->fallback ? o->fallback[q] : 0;
+                float f3[3] = {o->ttft_ms ? o->ttft_ms[q] : -1.f, o->pftt_ms ? o->pftt_ms[q] : -1.f,
+                               o->rt_ms ? o->rt_ms[q] : -1.f};
+                std::memcpy(&r[2], f3, 12);
+                r[5] = o->n_tokens ? o->n_tokens[q] : 0;
+                if (gen_w) std::memcpy(&r[6], o->tokens + static_cast<size_t>(q) * max_new, gen_w * 4);
+                if (lg_w) std::memcpy(&r[6 + gen_w], o->logits + static_cast<size_t>(q) * SGC_VOCAB, lg_w * 4);
+            };
+            auto unpack = [&](uint32_t q, const uint32_t* r) {
+                if (o->first_token) std::memcpy(&o->first_token[q], &r[0], 4);
+                if (o->fallback) o->fallback[q] = static_cast<uint8_t>(r[1]);
+                float f3[3];
+                std::memcpy(f3, &r[2], 12);
+                if (o->ttft_ms) o->ttft_ms[q] = f3[0];
+                if (o->pftt_ms) o->pftt_ms[q] = f3[1];
+                if (o->rt_ms) o->rt_ms[q] = f3[2];
+                if (o->n_tokens) o->n_tokens[q] = r[5];
+                if (gen_w) std::memcpy(o->tokens + static_cast<size_t>(q) * max_new, &r[6], gen_w * 4);
+                if (lg_w) std::memcpy(o->logits + static_cast<size_t>(q) * SGC_VOCAB, &r[6 + gen_w], lg_w * 4);
+            };
+            std::vector<std::vector<uint32_t>> by_rank(world);
+            for (uint32_t q = 0; q < m; ++q) by_rank[qrank[q]].push_back(q);
+            std::vector<sgc::P2P> sends, recvs;
+            std::vector<uint32_t> hbuf;
+            uint32_t* dbuf = nullptr;
+            if (me != 0 && !by_rank[me].empty()) {
+                hbuf.resize(by_rank[me].size() * W);
+                for (size_t j = 0; j < by_rank[me].size(); ++j) pack(by_rank[me][j], &hbuf[j * W]);
+                dbuf = c->buf<uint32_t>("gather_out", hbuf.size());
+                sgc::copy_in(c, dbuf, hbuf.data(), hbuf.size());
+                sends.push_back({dbuf, hbuf.size() * 4, 0});
+            } else if (me == 0) {
+                size_t tot = 0;
+                for (int r = 1; r < world; ++r) tot += by_rank[r].size() * W;
+                dbuf = c->buf<uint32_t>("gather_out", std::max<size_t>(tot, 1));
+                size_t off = 0;
+                for (int r = 1; r < world; ++r) {
+                    if (!by_rank[r].empty()) recvs.push_back({dbuf + off, by_rank[r].size() * W * 4, r});
+                    off += by_rank[r].size() * W;
+                }
+                hbuf.resize(tot);
+            }
+            comm->exchange(c, sends, recvs);
+            if (me == 0 && !hbuf.empty()) {
+                sgc::copy_out(c, hbuf.data(), dbuf, hbuf.size());
+                c->sync();
+                size_t off = 0;
+                for (int r = 1; r < world; ++r)
+                    for (uint32_t q : by_rank[r]) {
+                        unpack(q, &hbuf[off]);
+                        off += W;
+                    }
+            }
+            c->sync();
+        }
         o->stage_ms[0] = t_enc - t_start;
         o->stage_ms[1] = t_cl - t_enc;
         o->stage_ms[2] = t_rep - t_cl;

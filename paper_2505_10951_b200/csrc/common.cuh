@@ -10,11 +10,13 @@
 #include <cstdlib>
 #include <algorithm>
 #include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
 #include "sgc_b200.h"
+#include "comm.cuh"
 
 namespace sgc {
 
@@ -214,4 +216,5 @@ inline unsigned ceil_div(uint64_t a, uint64_t b) { return static_cast<unsigned>(
 // opaque handle definitions
 struct sgc_ctx {
     sgc::Ctx c;
+    std::unique_ptr<sgc::Comm> comm;  // multi-GPU transport (comm.cuh), null = single GPU
 };

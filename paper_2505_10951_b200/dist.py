@@ -40,6 +40,55 @@ def combine_first_tokens(first, dist):
     return t.cpu().numpy().astype(np.int32)
 
 
+class GlooTransport:
+    """Host transport for the library's multi-rank path (sgc_comm_init_host) over a
+    torch.distributed process group on CPU (gloo): the CPU tests and ranks sharing one GPU."""
+
+    def __init__(self, dist, group=None):
+        self.dist, self.group = dist, group
+
+    def allgather(self, send: bytes, nbytes: int) -> bytes:
+        import torch
+
+        t = torch.frombuffer(bytearray(send), dtype=torch.uint8) if nbytes else torch.zeros(0, dtype=torch.uint8)
+        parts = [torch.zeros(nbytes, dtype=torch.uint8) for _ in range(self.dist.get_world_size(self.group))]
+        self.dist.all_gather(parts, t, group=self.group)
+        return b"".join(p.numpy().tobytes() for p in parts)
+
+    def exchange(self, sends, recvs):
+        import torch
+
+        reqs, outs = [], []
+        for data, peer in sends:
+            reqs.append(self.dist.isend(torch.frombuffer(bytearray(data), dtype=torch.uint8), peer, group=self.group))
+        for nbytes, peer in recvs:
+            buf = torch.zeros(nbytes, dtype=torch.uint8)
+            outs.append(buf)
+            reqs.append(self.dist.irecv(buf, peer, group=self.group))
+        for r in reqs:
+            r.wait()
+        return [b.numpy().tobytes() for b in outs]
+
+
+def init_library_comm(ctx, dist, backend: str):
+    """Join the library context to the process group: NCCL (rank 0's unique id broadcast over
+    the group) or the gloo host transport."""
+    import torch
+
+    world, rank = dist.get_world_size(), dist.get_rank()
+    if backend == "nccl":
+        from . import host
+
+        uid = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            uid = torch.frombuffer(bytearray(host.comm_unique_id()), dtype=torch.uint8)
+        obj = [uid.numpy().tobytes()]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.init_comm_nccl(obj[0], world, rank)
+    else:
+        ctx.init_comm_host(GlooTransport(dist), world, rank)
+
+
 def lpt_assign(costs, world: int) -> np.ndarray:
     from . import _lib
 

@@ -46,6 +46,14 @@ def splitmix64_once(x: int) -> int:
     return s(x)
 
 
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0 makes it, every rank passes it on)."""
+    L = _lib.load()
+    buf = (C.c_uint8 * 128)()
+    check(L.sgc_comm_unique_id(buf))
+    return bytes(buf)
+
+
 class Context:
     """One CUDA device + stream (sgc_ctx). Handles created on it (KV batches, models, graphs)
     are released before the context itself, whatever order Python collects them in -- their
@@ -94,6 +102,27 @@ class Context:
         ms, n = C.c_double(), C.c_uint64()
         check(self.lib.sgc_get_timing(self.h, name.encode(), C.byref(ms), C.byref(n)))
         return ms.value, n.value
+
+    # ---- multi-GPU transport (sgc_comm_*): the library then all-gathers embeddings, moves split
+    # clusters' sealed prefixes point to point and gathers outputs to rank 0 itself
+    def init_comm_nccl(self, unique_id: bytes, world: int, rank: int):
+        uid = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        check(self.lib.sgc_comm_init_nccl(self.h, uid, world, rank))
+
+    def init_comm_host(self, transport, world: int, rank: int):
+        """transport: an object with allgather(send: bytes-like, nbytes) -> bytes (rank order) and
+        exchange(sends [(memoryview, peer)], recvs [(memoryview, peer)]) -- e.g. dist.GlooTransport."""
+        self._transport = _lib.make_host_transport(transport)
+        check(self.lib.sgc_comm_init_host(self.h, C.byref(self._transport[0]), world, rank))
+
+    def comm_info(self):
+        w, r, k = C.c_int(), C.c_int(), C.c_int()
+        self.lib.sgc_comm_info(self.h, C.byref(w), C.byref(r), C.byref(k))
+        return w.value, r.value, {0: None, 1: "nccl", 2: "host"}[k.value]
+
+    def close_comm(self):
+        check(self.lib.sgc_comm_destroy(self.h))
+        self._transport = None
 
     def gemm(self, a_ptr: int, b_ptr: int, d_ptr: int, M: int, N: int, K: int, epi: int):
         check(self.lib.sgc_gemm_bf16(self.h, C.c_void_p(a_ptr), C.c_void_p(b_ptr),
@@ -528,6 +557,10 @@ class SubgCacheResult:
     decode_rows: int = 0
     seal_ms: np.ndarray | None = None   # [c] cluster prefix sealed (ms since submission)
     pftt_ms: np.ndarray | None = None   # [m] own work start -> first token
+    query_rank: np.ndarray | None = None  # [m] rank serving each query
+    prefilled: np.ndarray | None = None   # [c] 1 if this rank ran the representative's prefill
+    prefix_bytes_sent: int = 0            # split clusters' sealed K/V moved point to point
+    prefix_bytes_received: int = 0
 
 
 class PreparedBatch:
@@ -584,7 +617,7 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
                   embeddings: np.ndarray | None = None, cluster_owner=None, rank: int = 0,
                   world_size: int = 1, want_logits: bool = True,
                   device_inputs: bool = False, waves: int = 1, max_new: int = 0,
-                  split_clusters: bool = False) -> SubgCacheResult:
+                  split_clusters: bool = False, transfer_prefix: int = 1) -> SubgCacheResult:
     """pipeline.cpp:212-293 (SubgCache branch) + cache_engine.cpp:217-233 (run_batch), to the
     first token of every query."""
     w = pb.w
@@ -620,6 +653,7 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     b.waves = waves
     b.max_new_tokens = max_new
     b.split_clusters = int(split_clusters)
+    b.transfer_prefix = int(transfer_prefix)
     emb = np.zeros((m, d), np.float32)
     labels = np.zeros(m, np.uint32)
     nm = max(m - k, 1)
@@ -647,6 +681,10 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     pftt = np.full(m, -1.0, np.float32)
     o.seal_ms = _p(seal, C.c_float)
     o.pftt_ms = _p(pftt, C.c_float)
+    qrank = np.zeros(m, np.uint32)
+    prefilled = np.zeros(k, np.uint8)
+    o.query_rank = _p(qrank, C.c_uint32)
+    o.prefilled = _p(prefilled, C.c_uint8)
     toks = cnt = rt = None
     if max_new > 1:
         toks = np.full((m, max_new), -1, np.int32)
@@ -660,6 +698,8 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
                           first, fb, owner, ttft, o.waves, list(o.stage_ms)[:6], o.prefill_rows,
                           o.extend_rows)
     res.seal_ms, res.pftt_ms = seal, pftt
+    res.query_rank, res.prefilled = qrank, prefilled
+    res.prefix_bytes_sent, res.prefix_bytes_received = o.prefix_bytes_sent, o.prefix_bytes_received
     if max_new > 1:
         res.tokens = [toks[q, :cnt[q]].copy() for q in range(m)]
         res.rt_ms = rt
