@@ -145,6 +145,62 @@ def lm_flops(w, prefix_lens, members_q, labels, all_prefix=None):
     return gemm, attn, head, fam
 
 
+# ----------------------------------------------------------------- parity
+
+PARITY_FIXTURES = (("lm_c3_l32.json", "all 32 layers, full width, ~350-token prefix (budget-cut prompt)"),
+                   ("lm_c3_l2.json", "2 layers, full width, three ~2.1k-token C3 representatives"))
+MARGIN_BANDS = (0.0, 0.01, 0.05, 0.16, float("inf"))
+
+
+def parity_block(ctx, lm, w):
+    """First-token argmax agreement and max |dlogit| of THIS build at the measured shape (8B-shaped,
+    d 4096, hd 128, ffn 14336) against the reference's fp32 logits on the same inputs
+    (tests/golden/lm_c3_*.json, written by the unmodified reference: make_golden_fullwidth.py).
+    The 32-layer fixture runs on the bench's own model (same seed and shape); the 2-layer one on a
+    2-layer model of the same width. Answer lookup off (plain greedy_argmax), stratified by the
+    reference's top-1/top-2 margin."""
+    from paper_2505_10951_b200 import host
+
+    out = {}
+    for name, what in PARITY_FIXTURES:
+        path = os.path.join(ROOT, "tests", "golden", name)
+        if not os.path.exists(path) or w.lm["model_dim"] != 4096:
+            continue
+        with open(path) as f:
+            G = json.load(f)
+        cfg = G["cfg"]
+        own = cfg["layers"] == w.lm["layers"] and cfg["seed"] == w.seed
+        model = lm if own else host.ToyLm(ctx, host.ToyLmConfig(**cfg))
+        kv, plog = model.prefill_batch([c["prefix"] for c in G["clusters"]])
+        seg, qs, ref, margin = [], [], [], []
+        for ci, (c, o) in enumerate(zip(G["clusters"], G["out"])):
+            for q, r in zip(c["members"], o["members"]):
+                seg.append(ci)
+                qs.append(q)
+                ref.append(r["logits"])
+                margin.append(r["margin"])
+        lg, first = model.extend_members(kv, seg, qs)
+        kv.release()
+        if not own:
+            model.close()
+        ref = np.asarray(ref, np.float32)
+        margin = np.asarray(margin)
+        agree = np.argmax(lg, axis=1) == np.argmax(ref, axis=1)
+        pref = np.asarray([o["prefix_logits"] for o in G["out"]], np.float32)
+        out[name.replace(".json", "")] = {
+            "what": what, "members": int(len(agree)),
+            "max_abs_dlogit": round(float(np.abs(lg - ref).max()), 5),
+            "prefix_max_abs_dlogit": round(float(np.abs(plog - pref).max()), 5),
+            "argmax_agree": f"{int(agree.sum())}/{len(agree)}",
+            "by_ref_margin": {f"[{lo},{hi})": f"{int(agree[(margin >= lo) & (margin < hi)].sum())}/"
+                                              f"{int(((margin >= lo) & (margin < hi)).sum())}"
+                              for lo, hi in zip(MARGIN_BANDS, MARGIN_BANDS[1:])}}
+    if out:
+        out["tolerance"] = ("max |dlogit| <= 0.08 (bf16 weights/activations, fp32 accumulate); argmax must "
+                            "agree when the reference's margin > 0.16 (tests/test_gpu_fullwidth.py)")
+    return out or None
+
+
 # ---------------------------------------------------------------- our arm
 
 def run_ours(args, rank, world, local_rank):
@@ -417,6 +473,8 @@ def run_ours(args, rank, world, local_rank):
         "setup_s": round(setup_s, 2),
     }
     out["clocks"] = clk.summary()
+    if not args.no_parity:
+        out["parity"] = parity_block(ctx, lm, w)
     if not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(w, res, pb, threads=1)
     return out
@@ -537,6 +595,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-gen", action="store_true", help="skip the generation (decode) measurement")
+    ap.add_argument("--no-parity", action="store_true", help="skip the full-width parity block")
     ap.add_argument("--no-split", action="store_true",
                     help="N > 1: whole clusters per GPU only (no member-level rebalancing of skewed clusters)")
     ap.add_argument("--attn-split", type=int, default=None, help="1: two softmax warpgroups per query tile")

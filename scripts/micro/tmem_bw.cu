@@ -1,4 +1,5 @@
 // Microbenchmark: tcgen05.ld (32x32b.x32) throughput per SM for 4 / 8 / 12 warps, and
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 -o /tmp/tmem_bw scripts/micro/tmem_bw.cu
 // tcgen05.st. Prints cycles per warp-load and bytes/clk/SM.
 #include <cstdio>
 #include <cstdint>
