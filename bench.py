@@ -240,7 +240,8 @@ def run_ours(args, rank, world, local_rank):
 
     def step():
         return host.run_subgcache(ctx, lm, dg, pb, want_logits=False, device_inputs=True, waves=args.waves,
-                                  split_clusters=split, transfer_prefix=not args.replica_prefill)
+                                  split_clusters=split, transfer_prefix=0 if args.replica_prefill else 1,
+                                  verify_prefix=not args.no_verify_prefix)
 
     for _ in range(args.warmup):
         res = step()
@@ -285,7 +286,8 @@ def run_ours(args, rank, world, local_rank):
     if not args.no_e2e:
         def step_e2e():
             return host.run_subgcache(ctx, lm, dg, pb, want_logits=True, waves=args.waves,
-                                      split_clusters=split, transfer_prefix=not args.replica_prefill)
+                                      split_clusters=split, transfer_prefix=0 if args.replica_prefill else 1,
+                                      verify_prefix=not args.no_verify_prefix)
 
         ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:
@@ -606,6 +608,8 @@ def main():
                     help="waves of the generation run (cost-balanced cuts; scripts/defer_probe.py: "
                          "2 waves gave the shortest batch and RT p50 at C3, 4 the lowest RT mean)")
     ap.add_argument("--no-pairs", action="store_true", help="1-CTA GEMM instead of CTA pairs")
+    ap.add_argument("--no-verify-prefix", action="store_true",
+                    help="skip the sealed-prefix digest check after serving (cache_engine.cpp:210)")
     ap.add_argument("--replica-prefill", action="store_true",
                     help="N > 1: split clusters' helper ranks prefill a replica instead of receiving the "
                          "sealed prefix point to point")

@@ -200,8 +200,8 @@ int sgc_build_representatives(sgc_ctx* ctx, sgc_graph* g, const sgc_subgraphs* s
                               uint32_t* dropped);
 
 /* ---- (4) KV precompute: ToyLm::prefill + KVCache::seal (lm_core.cpp:299-327, :60-80) --
- * Prefills `seqs.count` sequences in one batched pass (varlen causal attention) into a
- * paged bf16 KV pool and seals them. soft (optional) [count * model_dim] with
+ * Prefills `seqs.count` sequences in one batched pass (varlen causal attention) into the
+ * model's paged bf16 KV pool (128-token pages, one block table per sequence) and seals them. soft (optional) [count * model_dim] with
  * soft_mask[i] != 0 selecting sequences that carry a GRAPH_SOFT_SLOT at position 0.
  * last_logits (optional) [count * 260]. CapacityError if a sequence exceeds max_seq_len. */
 int sgc_prefill(sgc_ctx* ctx, sgc_model* model, const sgc_token_lists* seqs, const float* soft,
@@ -210,10 +210,16 @@ int sgc_kv_release(sgc_kv* kv);
 uint32_t sgc_kv_count(const sgc_kv* kv);
 /* KVCache::token_count of sealed segment i */
 uint64_t sgc_kv_tokens(const sgc_kv* kv, uint32_t i);
-/* KVCache::prefix_digest analogue: FNV-1a over segment i's bf16 K/V bytes, layer-major */
+/* KVCache::prefix_digest analogue (lm_core.cpp:108-116) over the bf16 pages: FNV-1a over each
+ * row's 64-bit words, those row digests folded per (layer, K|V) in row order, the folds folded in
+ * layer order (K before V) -- computed on the device. The reference hashes fp32 bytes, so the
+ * values are this library's own; equality before / after serving is what the path checks. */
 uint64_t sgc_kv_digest(const sgc_kv* kv, uint32_t i);
-/* KVCache::resident_kv_bytes analogue for the whole handle (bf16 storage) */
+/* KVCache::resident_kv_bytes analogue for the whole handle: its pages (K + V, all layers, bf16) */
 uint64_t sgc_kv_resident_bytes(const sgc_kv* kv);
+/* Paged KV cache: the block table of segment i (page ids of the model's pool; token t of the
+ * segment is row t % 128 of page pages[t / 128]). Returns the page count; pages may be NULL. */
+uint32_t sgc_kv_pages(const sgc_kv* kv, uint32_t i, int32_t* pages);
 /* Copy segment i, layer l, K (is_v=0) or V as fp32 [tokens * model_dim] (test hook). */
 int sgc_kv_read(const sgc_kv* kv, uint32_t i, uint32_t layer, int is_v, float* out);
 
@@ -280,6 +286,9 @@ typedef struct {
      * than a prefill (bytes over NVLink vs FLOPs on the tensor cores), else they prefill an
      * identical replica; 2 = always send; 0 = always replicate. Ignored without a transport. */
     int transfer_prefix;
+    /* KVCache::prefix_digest at seal and again after the cluster's members are served
+     * (cache_engine.cpp:189, :210): SGC_LOGIC if the sealed K/V changed. 0 = skip the check. */
+    int verify_prefix;
 } sgc_batch;
 
 typedef struct {
@@ -316,6 +325,10 @@ typedef struct {
     uint32_t* query_rank;
     uint8_t* prefilled;
     uint64_t prefix_bytes_sent, prefix_bytes_received; /* sealed K/V moved point to point */
+    /* paged KV cache: [c] digest of each sealed prefix this rank held (0 otherwise; see
+     * sgc_kv_digest), peak pages in use during the batch, bytes per page (K + V, all layers) */
+    uint64_t* prefix_digest;
+    uint64_t kv_pages_peak, kv_page_bytes;
 } sgc_batch_out;
 
 int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_batch* batch,
@@ -356,9 +369,8 @@ int sgc_set_timing(sgc_ctx* ctx, int enable);
  * "decode_defer_pct" (generation: a wave decodes on its own until fewer than this percentage of
  * its queries still generate, the stragglers of every wave then finish in one shared loop;
  * default 25, 0 = each wave to completion, >= 100 = all decoding after the last wave);
- * "attn_split" (1 = two softmax warpgroups per query tile; default 0);
- * "attn_db" (1 = double-buffered 64-key attention kernel; default 0, the 128-key kernel is
- * faster at C3: 141 vs 188 ms/step). Unknown names return SGC_ERR_INVALID. */
+ * "attn_split" (1 = two softmax warpgroups per query tile; default 0).
+ * Unknown names return SGC_DOMAIN. */
 int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value);
 int sgc_get_timing(sgc_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches);
 

@@ -83,7 +83,8 @@ class Batch(C.Structure):
                 ("precomputed_embeddings", C.POINTER(C.c_float)),
                 ("cluster_owner", C.POINTER(C.c_uint32)), ("rank", C.c_int),
                 ("world_size", C.c_int), ("waves", C.c_uint32), ("max_new_tokens", C.c_uint32),
-                ("split_clusters", C.c_int), ("transfer_prefix", C.c_int)]
+                ("split_clusters", C.c_int), ("transfer_prefix", C.c_int),
+                ("verify_prefix", C.c_int)]
 
 
 class BatchOut(C.Structure):
@@ -99,7 +100,9 @@ class BatchOut(C.Structure):
                 ("rt_ms", C.POINTER(C.c_float)), ("decode_rows", C.c_uint64),
                 ("seal_ms", C.POINTER(C.c_float)), ("pftt_ms", C.POINTER(C.c_float)),
                 ("query_rank", C.POINTER(C.c_uint32)), ("prefilled", C.POINTER(C.c_uint8)),
-                ("prefix_bytes_sent", C.c_uint64), ("prefix_bytes_received", C.c_uint64)]
+                ("prefix_bytes_sent", C.c_uint64), ("prefix_bytes_received", C.c_uint64),
+                ("prefix_digest", C.POINTER(C.c_uint64)), ("kv_pages_peak", C.c_uint64),
+                ("kv_page_bytes", C.c_uint64)]
 
 
 # sgc_host_transport callbacks (include/sgc_b200.h)
@@ -151,7 +154,7 @@ EXPORTS = [
     "sgc_kv_release", "sgc_kv_count", "sgc_kv_tokens", "sgc_kv_digest", "sgc_kv_resident_bytes",
     "sgc_kv_read", "sgc_extend", "sgc_run_subgcache", "sgc_gemm_bf16", "sgc_set_timing",
     "sgc_get_timing", "sgc_lpt_assign", "sgc_set_option", "sgc_attention_bf16", "sgc_extend_generate", "sgc_retrieve", "sgc_balance_members",
-    "sgc_comm_unique_id", "sgc_comm_init_nccl", "sgc_comm_init_host", "sgc_comm_destroy", "sgc_comm_info",
+    "sgc_kv_pages", "sgc_comm_unique_id", "sgc_comm_init_nccl", "sgc_comm_init_host", "sgc_comm_destroy", "sgc_comm_info",
 ]
 
 _lib = None
@@ -204,6 +207,8 @@ def load() -> C.CDLL:
     L.sgc_kv_resident_bytes.argtypes = [vp]
     L.sgc_kv_resident_bytes.restype = C.c_uint64
     L.sgc_kv_read.argtypes = [vp, C.c_uint32, C.c_uint32, C.c_int, P(C.c_float)]
+    L.sgc_kv_pages.argtypes = [vp, C.c_uint32, P(C.c_int32)]
+    L.sgc_kv_pages.restype = C.c_uint32
     L.sgc_extend.argtypes = [vp, vp, vp, P(C.c_uint32), P(TokenLists), P(TokenLists), C.c_float,
                              P(C.c_float), P(C.c_int32)]
     L.sgc_run_subgcache.argtypes = [vp, vp, vp, P(Batch), P(BatchOut)]

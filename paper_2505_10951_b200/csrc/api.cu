@@ -145,8 +145,24 @@ const char kEdgeHdr[] = "src,edge attr,dst";
 
 // ====================================================================== handles
 
+// ---- paged bf16 KV cache --------------------------------------------------------------------
+// One page pool per model: K and V are [L][pages][128][d] bf16 (layer-major, so one layer's pages
+// form a [pages * 128 x d] matrix for the attention's TMA descriptors). A sealed prefix segment
+// owns a list of pages (its block table); pages come from a free list and go back to it when the
+// handle is released (KVCache::release_suffix / the shared prefix dropped, lm_core.hpp:35-92). The
+// pool grows like a vector (new buffers, live pages copied, indices unchanged); new memory is
+// zeroed once, so a page's unused tail rows always hold finite values (masked keys read 0 * V).
+struct KvPool {
+    bf16* k = nullptr;
+    bf16* v = nullptr;
+    uint32_t pages = 0;
+    std::vector<int32_t> free_pages;  // sorted descending: pop_back hands out ascending ids
+    uint32_t live() const { return pages - static_cast<uint32_t>(free_pages.size()); }
+};
+
 struct sgc_model {
     Ctx* c = nullptr;
+    KvPool pool;
     sgc_lm_config cfg{};
     int d = 0, hd = 0, H = 0, L = 0, ffn = 0;
     float* tok_emb = nullptr;  // fp32 [260 x d]
@@ -182,20 +198,82 @@ struct sgc_graph {
 struct sgc_kv {
     sgc_model* model = nullptr;
     uint32_t n = 0;
-    std::vector<uint64_t> off, len;  // rows per segment in the KV region
-    uint64_t rows = 0;
-    bf16* k = nullptr;  // [L][rows x d]
-    bf16* v = nullptr;
-    int32_t* d_tokens = nullptr;  // context token ids (prefix, incl. soft slot)
+    std::vector<uint64_t> len;       // tokens per sealed segment
+    std::vector<uint32_t> bt_off;    // segment s's pages: pages[bt_off[s] ..]
+    std::vector<int32_t> pages;      // block table (host copy)
+    int32_t* d_bt = nullptr;         // block table (device)
+    uint64_t rows = 0;               // tokens of all segments
+    int32_t* d_tokens = nullptr;     // context token ids (prefix, incl. soft slot), segments back to back
     uint64_t* d_tok_off = nullptr;
-    bool owns_kv = true;          // false: K/V live in the context's reusable KV arena
-    uint64_t lstride = 0;         // rows per layer of the underlying buffer (0: rows)
-    size_t layer_elems() const { return static_cast<size_t>(lstride ? lstride : rows) * model->d; }
-    bf16* k_layer(int l) const { return k + l * layer_elems(); }
-    bf16* v_layer(int l) const { return v + l * layer_elems(); }
+    size_t layer_elems() const { return static_cast<size_t>(model->pool.pages) * sgc::kPageTokens * model->d; }
+    bf16* k_layer(int l) const { return model->pool.k + l * layer_elems(); }
+    bf16* v_layer(int l) const { return model->pool.v + l * layer_elems(); }
+    int pool_rows() const { return static_cast<int>(model->pool.pages * sgc::kPageTokens); }
+    uint32_t seg_pages(uint32_t s) const { return static_cast<uint32_t>((len[s] + sgc::kPageTokens - 1) / sgc::kPageTokens); }
 };
 
 namespace {
+
+// ============================================================ KV page pool
+
+size_t page_bytes(const sgc_model* m) {
+    return static_cast<size_t>(m->L) * 2 * sgc::kPageTokens * m->d * sizeof(bf16);  // K + V, all layers
+}
+
+// grow the pool to at least `need` pages (x1.5 when memory allows): new zeroed buffers, live pages
+// copied (page ids unchanged), old buffers freed in stream order
+void pool_grow(Ctx* c, sgc_model* m, uint32_t need) {
+    KvPool& p = m->pool;
+    if (need <= p.pages) return;
+    size_t free_b = 0, total_b = 0;
+    SGC_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t pb = page_bytes(m);
+    const size_t headroom = std::max<size_t>(static_cast<size_t>(0.04 * total_b), 2ull << 30);
+    const size_t avail = free_b > headroom ? free_b - headroom : 0;  // new buffers coexist with the old
+    uint32_t want = std::max<uint32_t>(need, p.pages + p.pages / 2);
+    if (static_cast<size_t>(want) * pb > avail) want = need;
+    if (static_cast<size_t>(want) * pb > avail)
+        fail(SGC_CAPACITY, "KV page pool: " + std::to_string(want) + " pages (" +
+                               std::to_string((static_cast<size_t>(want) * pb) >> 20) +
+                               " MiB) do not fit in free device memory");
+    const size_t row_elems = static_cast<size_t>(sgc::kPageTokens) * m->d;
+    bf16 *nk = nullptr, *nv = nullptr;
+    const size_t bytes = static_cast<size_t>(want) * row_elems * m->L * sizeof(bf16);
+    SGC_CUDA_CHECK(cudaMallocAsync(&nk, bytes, c->stream));
+    SGC_CUDA_CHECK(cudaMallocAsync(&nv, bytes, c->stream));
+    SGC_CUDA_CHECK(cudaMemsetAsync(nk, 0, bytes, c->stream));
+    SGC_CUDA_CHECK(cudaMemsetAsync(nv, 0, bytes, c->stream));
+    if (p.pages) {
+        const size_t src_pitch = static_cast<size_t>(p.pages) * row_elems * sizeof(bf16);
+        const size_t dst_pitch = static_cast<size_t>(want) * row_elems * sizeof(bf16);
+        SGC_CUDA_CHECK(cudaMemcpy2DAsync(nk, dst_pitch, p.k, src_pitch, src_pitch, m->L, cudaMemcpyDeviceToDevice, c->stream));
+        SGC_CUDA_CHECK(cudaMemcpy2DAsync(nv, dst_pitch, p.v, src_pitch, src_pitch, m->L, cudaMemcpyDeviceToDevice, c->stream));
+        SGC_CUDA_CHECK(cudaFreeAsync(p.k, c->stream));
+        SGC_CUDA_CHECK(cudaFreeAsync(p.v, c->stream));
+    }
+    for (uint32_t i = p.pages; i < want; ++i) p.free_pages.push_back(static_cast<int32_t>(i));
+    std::sort(p.free_pages.begin(), p.free_pages.end(), std::greater<int32_t>());
+    p.k = nk;
+    p.v = nv;
+    p.pages = want;
+}
+
+std::vector<int32_t> pool_alloc(Ctx* c, sgc_model* m, uint32_t n) {
+    KvPool& p = m->pool;
+    if (p.free_pages.size() < n) pool_grow(c, m, p.live() + n);
+    std::vector<int32_t> out(p.free_pages.end() - n, p.free_pages.end());
+    p.free_pages.resize(p.free_pages.size() - n);
+    std::reverse(out.begin(), out.end());
+    return out;
+}
+
+// pages return to the free list; stream order makes the reuse safe (one stream per context)
+void pool_release(sgc_model* m, const std::vector<int32_t>& pages) {
+    if (pages.empty()) return;
+    KvPool& p = m->pool;
+    p.free_pages.insert(p.free_pages.end(), pages.begin(), pages.end());
+    std::sort(p.free_pages.begin(), p.free_pages.end(), std::greater<int32_t>());
+}
 
 // ============================================================ model weights
 
@@ -222,6 +300,8 @@ struct FwdBatch {
     const sgc::AttnWork* d_work = nullptr;  // tiles of <= attn_tile(hd) rows
     int n_work = 0;
     int pfx_rows = 0;  // rows of the prefix KV region (TMA bounds)
+    int loc_rows = 0;  // rows of the k_loc / v_loc region (TMA bounds; 0 = M, contiguous batch rows)
+    const int32_t* d_bt = nullptr;  // block table of the pages the work items reference
     // KV written by this batch: row r -> loc row r of (k_loc_layer(l), v_loc_layer(l))
     std::function<bf16*(int)> k_loc, v_loc;
     std::function<const bf16*(int)> k_pfx, v_pfx;
@@ -298,6 +378,7 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
         ap.loc_kv0 = 0;
         ap.seg_lo = b.d_seg_lo;
         ap.work = b.d_work;
+        ap.bt = b.d_bt;
         ap.d = d;
         ap.scale = 1.0f / std::sqrt(static_cast<float>(m->hd));
         if (b.dec) {
@@ -317,6 +398,7 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
             dp.q_n = b.dec->q_n;
             dp.g_lo = b.dec->g_lo;
             dp.g_n = b.dec->g_n;
+            dp.p_bt = b.d_bt;
             dp.out = ao;
             dp.rows = M;
             dp.d = d;
@@ -336,7 +418,8 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
             }
             sgc::decode_attention_local(c, dp);
         } else if (sgc::attention_tc_supported(m->hd)) {
-            sgc::cascade_attention_tc(c, ap, b.n_work, m->H, m->hd, M, b.k_pfx ? b.pfx_rows : M, M);
+            const int loc_rows = b.loc_rows ? b.loc_rows : M;
+            sgc::cascade_attention_tc(c, ap, b.n_work, m->H, m->hd, M, b.k_pfx ? b.pfx_rows : loc_rows, loc_rows);
         } else {
             sgc::cascade_attention(c, ap, b.n_work, m->H, m->hd);
         }
@@ -400,37 +483,43 @@ void check_forward_flags(Ctx* c) {
     if (c->take_flag()) fail(SGC_DOMAIN, "token id out of vocab");
 }
 
-// tiles of <= 64 rows that never cross a `group` boundary (sequence for prefill, segment
-// for extend); rows of one group are contiguous
+// tiles of <= attn_tile rows that never cross a `group` boundary (sequence for prefill, segment
+// for extend); rows of one group are contiguous. loc_bt: per group, the block-table offset of the
+// group's own pages (paged prefill) or -1 (own keys in contiguous scratch rows)
 int attn_tile(int hd) { return sgc::attention_tc_supported(hd) ? 256 : 64; }
 
 std::vector<sgc::AttnWork> make_work(const std::vector<int>& group_start, const std::vector<int>& group_rows,
-                                     const std::vector<int>& pfx_kv0, const std::vector<int>& pfx_len,
-                                     int tile) {
+                                     const std::vector<int>& pfx_off, const std::vector<int>& pfx_len,
+                                     const std::vector<int>& loc_bt, int tile) {
     std::vector<sgc::AttnWork> w;
     for (size_t g = 0; g < group_start.size(); ++g)
         for (int r = 0; r < group_rows[g]; r += tile)
-            w.push_back({group_start[g] + r, std::min(tile, group_rows[g] - r), pfx_kv0[g], pfx_len[g]});
+            w.push_back({group_start[g] + r, std::min(tile, group_rows[g] - r), pfx_off[g], pfx_len[g], loc_bt[g]});
     return w;
 }
 
 // ============================================================ prefill / extend
 
-// n_remote: the last n_remote sequences are laid out (segments, context tokens, arena rows) but not
-// computed -- their sealed K/V arrive point to point from the rank that prefilled them; the
-// forward covers the leading local rows only (last_logits: local sequences only).
+// ToyLm::prefill + KVCache::seal (lm_core.cpp:299-327, :60-80) for `count` sequences in one
+// handle. Every sequence gets its own 128-token pages from the model's pool (its block table);
+// the forward runs over chunks of whole sequences (<= max_rows rows: bounded activations), the QKV
+// GEMM epilogue writes each row's K/V straight into its page slot, and the attention reads each
+// sequence's own keys through its pages.
+// n_remote: the last n_remote sequences get pages and context tokens but are not computed -- their
+// sealed K/V arrive point to point from the rank that prefilled them (last_logits: local ones).
 sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in, const int32_t* tok_in,
-                   const float* soft, const uint8_t* soft_mask, float* last_logits, bool arena = false,
-                   uint64_t arena_row0 = 0, uint64_t arena_rows = 0, bool sync = true, uint32_t n_remote = 0) {
+                   const float* soft, const uint8_t* soft_mask, float* last_logits, bool sync = true,
+                   uint32_t n_remote = 0, uint64_t max_rows = 1ull << 16) {
     std::vector<uint64_t> off = to_host(c, off_in, count + 1);
     std::vector<int32_t> toks = to_host(c, tok_in, off[count]);
     std::vector<uint8_t> smask = soft_mask ? to_host(c, soft_mask, count) : std::vector<uint8_t>(count, 0);
     const int d = m->d;
+    if (n_remote > count) fail(SGC_LOGIC, "prefill: more remote sequences than sequences");
     auto kv = std::make_unique<sgc_kv>();
     kv->model = m;
     kv->n = count;
-    std::vector<int32_t> rows_tok, pos, seg_lo, soft_idx, logit_rows;
-    std::vector<uint64_t> ctx_off(1, 0);
+    std::vector<int32_t> rows_tok, soft_idx;
+    std::vector<uint64_t> ctx_off(1, 0), seq_row0;
     bool any_soft = false;
     for (uint32_t s = 0; s < count; ++s) {
         uint64_t n = off[s + 1] - off[s];
@@ -441,8 +530,7 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
             fail(SGC_CAPACITY, "prompt of " + std::to_string(total) + " tokens exceeds max " +
                                    std::to_string(m->cfg.max_seq_len));
         if (total == 0) fail(SGC_DOMAIN, "prefill: empty sequence");
-        int start = static_cast<int>(rows_tok.size());
-        kv->off.push_back(start);
+        seq_row0.push_back(rows_tok.size());
         kv->len.push_back(total);
         if (has_soft) {
             rows_tok.push_back(259);
@@ -452,78 +540,84 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
             rows_tok.push_back(toks[off[s] + i]);
             soft_idx.push_back(-1);
         }
-        for (uint64_t i = 0; i < total; ++i) {
-            pos.push_back(static_cast<int32_t>(i));
-            seg_lo.push_back(start);
-        }
-        logit_rows.push_back(static_cast<int32_t>(rows_tok.size() - 1));
         ctx_off.push_back(rows_tok.size());
     }
-    const int M = static_cast<int>(rows_tok.size());
+    const uint64_t M = rows_tok.size();
     kv->rows = M;
-    if (n_remote > count) fail(SGC_LOGIC, "prefill: more remote sequences than sequences");
-    const uint32_t n_local = count - n_remote;
-    const int M_local = n_local < count ? static_cast<int>(kv->off[n_local]) : M;
-    if (arena) {
-        // batch-internal sealed prefixes: one grow-only arena [L][arena_rows][d] holding every
-        // wave's prefixes at row offsets (arena_rows == 0: just this call's rows)
-        const uint64_t total = arena_rows ? arena_rows : static_cast<uint64_t>(M);
-        if (arena_row0 + static_cast<uint64_t>(M) > total) fail(SGC_LOGIC, "KV arena overflow");
-        bf16* ak = c->buf<bf16>("kv_arena_k", static_cast<size_t>(m->L) * total * d);
-        bf16* av = c->buf<bf16>("kv_arena_v", static_cast<size_t>(m->L) * total * d);
-        kv->k = ak + arena_row0 * d;
-        kv->v = av + arena_row0 * d;
-        kv->lstride = total;
-        kv->owns_kv = false;
-    } else {
-        kv->k = dalloc<bf16>(c, static_cast<size_t>(m->L) * M * d);
-        kv->v = dalloc<bf16>(c, static_cast<size_t>(m->L) * M * d);
+    // pages: one block table for the handle, segment s at bt_off[s]
+    uint32_t npages = 0;
+    for (uint32_t s = 0; s < count; ++s) {
+        kv->bt_off.push_back(npages);
+        npages += kv->seg_pages(s);
     }
+    kv->pages = pool_alloc(c, m, npages);
+    kv->d_bt = dalloc<int32_t>(c, npages);
+    sgc::copy_in(c, kv->d_bt, kv->pages.data(), npages);
     kv->d_tokens = dalloc<int32_t>(c, M);
     kv->d_tok_off = dalloc<uint64_t>(c, count + 1);
     sgc::copy_in(c, kv->d_tokens, rows_tok.data(), M);
     sgc::copy_in(c, kv->d_tok_off, ctx_off.data(), count + 1);
-
-    int32_t* d_pos = c->buf<int32_t>("pf_pos", M);
-    int32_t* d_seg = c->buf<int32_t>("pf_seg", M);
-    int32_t* d_sidx = c->buf<int32_t>("pf_sidx", M);
-    int32_t* d_lr = c->buf<int32_t>("pf_lrows", count);
-    float* d_logits = c->buf<float>("pf_logits", static_cast<size_t>(count) * SGC_VOCAB);
     float* d_soft = nullptr;
     if (any_soft) {
         d_soft = c->buf<float>("pf_soft", static_cast<size_t>(count) * d);
         sgc::copy_in(c, d_soft, soft, static_cast<size_t>(count) * d);
     }
-    std::vector<int> gs, gr, z(n_local, 0);
-    for (uint32_t s = 0; s < n_local; ++s) {
-        gs.push_back(static_cast<int>(kv->off[s]));
-        gr.push_back(static_cast<int>(kv->len[s]));
-    }
-    std::vector<sgc::AttnWork> work = make_work(gs, gr, z, z, attn_tile(m->hd));
-    sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("pf_work", work.size());
-    sgc::copy_in(c, d_pos, pos.data(), M);
-    sgc::copy_in(c, d_seg, seg_lo.data(), M);
-    sgc::copy_in(c, d_sidx, soft_idx.data(), M);
-    sgc::copy_in(c, d_lr, logit_rows.data(), count);
-    sgc::copy_in(c, d_work, work.data(), work.size());
-
-    FwdBatch b;
-    b.M = M_local;
-    b.d_tokens = kv->d_tokens;
-    b.d_soft = d_soft;
-    b.d_soft_idx = any_soft ? d_sidx : nullptr;
-    b.d_pos = d_pos;
-    b.d_seg_lo = d_seg;
-    b.d_work = d_work;
-    b.n_work = static_cast<int>(work.size());
+    const uint32_t n_local = count - n_remote;
+    float* d_logits = c->buf<float>("pf_logits", static_cast<size_t>(std::max<uint32_t>(1, n_local)) * SGC_VOCAB);
     sgc_kv* kvp = kv.get();
-    b.k_loc = [kvp](int l) { return kvp->k_layer(l); };
-    b.v_loc = [kvp](int l) { return kvp->v_layer(l); };
-    b.d_logit_rows = d_lr;
-    // no logits requested (a representative's prompt): the last layer stops after its K/V
-    b.n_logits = last_logits ? static_cast<int>(n_local) : 0;
-    b.d_logits = last_logits ? d_logits : nullptr;
-    if (M_local > 0) forward_rows(c, m, b);
+    // the forward, one chunk of whole local sequences at a time
+    for (uint32_t s0 = 0; s0 < n_local;) {
+        uint32_t s1 = s0 + 1;
+        uint64_t rows = kv->len[s0];
+        while (s1 < n_local && rows + kv->len[s1] <= max_rows) rows += kv->len[s1++];
+        const uint64_t R0 = seq_row0[s0];
+        std::vector<int32_t> pos, seg_lo, sidx, kvrow, lrows;
+        std::vector<int> gs, gr, z, lb;
+        for (uint32_t s = s0; s < s1; ++s) {
+            const int start = static_cast<int>(seq_row0[s] - R0);
+            gs.push_back(start);
+            gr.push_back(static_cast<int>(kv->len[s]));
+            z.push_back(0);
+            lb.push_back(static_cast<int>(kv->bt_off[s]));
+            for (uint64_t t = 0; t < kv->len[s]; ++t) {
+                pos.push_back(static_cast<int32_t>(t));
+                seg_lo.push_back(start);
+                sidx.push_back(soft_idx[seq_row0[s] + t]);
+                kvrow.push_back(kv->pages[kv->bt_off[s] + t / sgc::kPageTokens] * sgc::kPageTokens +
+                                static_cast<int32_t>(t % sgc::kPageTokens));
+            }
+            lrows.push_back(static_cast<int32_t>(start + kv->len[s] - 1));
+        }
+        std::vector<sgc::AttnWork> work = make_work(gs, gr, z, z, lb, attn_tile(m->hd));
+        const int Mc = static_cast<int>(rows);
+        int32_t* d_arr = c->buf<int32_t>("pf_rows", static_cast<size_t>(Mc) * 4 + (s1 - s0));
+        std::vector<int32_t> packed;
+        packed.reserve(static_cast<size_t>(Mc) * 4 + (s1 - s0));
+        for (auto* v : {&pos, &seg_lo, &sidx, &kvrow, &lrows}) packed.insert(packed.end(), v->begin(), v->end());
+        sgc::copy_in(c, d_arr, packed.data(), packed.size());
+        sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("pf_work", work.size());
+        sgc::copy_in(c, d_work, work.data(), work.size());
+        FwdBatch b;
+        b.M = Mc;
+        b.d_tokens = kv->d_tokens + R0;
+        b.d_soft = d_soft;
+        b.d_soft_idx = any_soft ? d_arr + 2 * static_cast<size_t>(Mc) : nullptr;
+        b.d_pos = d_arr;
+        b.d_seg_lo = d_arr + Mc;
+        b.d_kv_row = d_arr + 3 * static_cast<size_t>(Mc);
+        b.d_work = d_work;
+        b.n_work = static_cast<int>(work.size());
+        b.k_loc = [kvp](int l) { return kvp->k_layer(l); };
+        b.v_loc = [kvp](int l) { return kvp->v_layer(l); };
+        b.loc_rows = kv->pool_rows();
+        b.d_bt = kv->d_bt;
+        b.d_logit_rows = d_arr + 4 * static_cast<size_t>(Mc);
+        // no logits requested (a representative's prompt): the last layer stops after its K/V
+        b.n_logits = last_logits ? static_cast<int>(s1 - s0) : 0;
+        b.d_logits = last_logits ? d_logits + static_cast<size_t>(s0) * SGC_VOCAB : nullptr;
+        forward_rows(c, m, b);
+        s0 = s1;
+    }
     if (last_logits && n_local) sgc::copy_out(c, last_logits, d_logits, static_cast<size_t>(n_local) * SGC_VOCAB);
     if (sync) {  // else: the caller syncs (last_logits must then be pinned or null)
         c->sync();
@@ -608,7 +702,7 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
         }
         const int M = static_cast<int>(rows);
         std::vector<int32_t> toks, pos, seg_lo, lrows;
-        std::vector<int> gs, gr, pk, pl;
+        std::vector<int> gs, gr, pk, pl, lb;
         std::vector<uint32_t> mseg;
         std::vector<uint64_t> a_off(1, 0);
         std::vector<int32_t> a_tok;
@@ -620,8 +714,9 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
             if (gs.empty() || mseg.back() != s) {
                 gs.push_back(start);
                 gr.push_back(0);
-                pk.push_back(static_cast<int>(kv->off[s]));
+                pk.push_back(static_cast<int>(kv->bt_off[s]));  // the sealed prefix's pages
                 pl.push_back(static_cast<int>(kv->len[s]));
+                lb.push_back(-1);                                // own keys: contiguous scratch
             }
             gr.back() += static_cast<int>(qn);
             mseg.push_back(s);
@@ -637,7 +732,7 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
             }
             a_off.push_back(a_tok.size());
         }
-        std::vector<sgc::AttnWork> work = make_work(gs, gr, pk, pl, attn_tile(m->hd));
+        std::vector<sgc::AttnWork> work = make_work(gs, gr, pk, pl, lb, attn_tile(m->hd));
         const int nm = static_cast<int>(i1 - i0);
         int32_t* d_tok = c->buf<int32_t>("ex_tok", M);
         int32_t* d_pos = c->buf<int32_t>("ex_pos", M);
@@ -677,8 +772,9 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
             b.v_loc = [vl](int) { return vl; };
         }
         b.k_pfx = [kv](int l) { return static_cast<const bf16*>(kv->k_layer(l)); };
-        b.pfx_rows = static_cast<int>(kv->rows);
+        b.pfx_rows = kv->pool_rows();
         b.v_pfx = [kv](int l) { return static_cast<const bf16*>(kv->v_layer(l)); };
+        b.d_bt = kv->d_bt;
         b.d_logit_rows = d_lr;
         b.n_logits = nm;
         b.d_logits = d_logits;
@@ -730,7 +826,7 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
 // extend). Stops per member on EOS, after max_new tokens, or when the context is full; the
 // copy pointer biases answer[t] (then EOS) when the answer occurs in the prefix.
 struct GenJob {
-    std::vector<int32_t> pfx_kv0, pfx_len, q_lo, q_n, pos0, first, gen_row0;
+    std::vector<int32_t> pfx_bt, pfx_len, q_lo, q_n, pos0, first, gen_row0;  // pfx_bt: block-table offset
     std::vector<int8_t> hint;
     std::vector<uint64_t> a_off{0};
     std::vector<int32_t> a_tok;
@@ -758,10 +854,12 @@ struct GenState {
         }
     }
 };
-// Decode buffers shared by every step of a batch: the prefix KV view (all sealed prefixes the
-// job's pfx_kv0 index), the kept question K/V and the generated-token K/V, each [L][rows][d].
+// Decode buffers shared by every step of a batch: the block table of every sealed prefix the job's
+// pfx_bt offsets index (pages of the model's pool), the kept question K/V and the generated-token
+// K/V, each [L][rows][d].
 struct GenBuffers {
-    const sgc_kv* pfx = nullptr;
+    sgc_model* model = nullptr;
+    int32_t* d_bt = nullptr;
     const ExtendKeep* keep = nullptr;
     bf16 *gk = nullptr, *gv = nullptr;
     size_t grows = 0;
@@ -770,10 +868,12 @@ struct GenBuffers {
     int32_t* d_atok = nullptr;
 };
 
-GenBuffers gen_buffers(Ctx* c, sgc_model* m, const sgc_kv* pfx, const ExtendKeep* keep, const GenJob& job,
-                       size_t gen_rows) {
+GenBuffers gen_buffers(Ctx* c, sgc_model* m, const std::vector<int32_t>& block_table, const ExtendKeep* keep,
+                       const GenJob& job, size_t gen_rows) {
     GenBuffers g;
-    g.pfx = pfx;
+    g.model = m;
+    g.d_bt = c->buf<int32_t>("dec_bt", std::max<size_t>(1, block_table.size()));
+    sgc::copy_in(c, g.d_bt, block_table.data(), block_table.size());
     g.keep = keep;
     g.grows = std::max<size_t>(1, gen_rows);
     g.gk = c->buf<bf16>("dec_gk", static_cast<size_t>(m->L) * g.grows * m->d);
@@ -796,7 +896,6 @@ void decode_steps(Ctx* c, sgc_model* m, const GenBuffers& g, const GenJob& job, 
     const uint32_t max_new = st.max_new;
     const uint64_t max_seq = m->cfg.max_seq_len;
     const int tile = attn_tile(m->hd);
-    const sgc_kv* kv = g.pfx;
     for (;;) {
         std::vector<int32_t> act;
         for (uint32_t j : sel)
@@ -815,14 +914,14 @@ void decode_steps(Ctx* c, sgc_model* m, const GenBuffers& g, const GenJob& job, 
             kvr[i] = job.gen_row0[j] + t - 1;
             step[i] = t;
             lrow[i] = i;
-            plo[i] = job.pfx_kv0[j];
+            plo[i] = job.pfx_bt[j];
             pn[i] = job.pfx_len[j];
             qlo[i] = job.q_lo[j];
             qn[i] = job.q_n[j];
             glo[i] = job.gen_row0[j];
             gn[i] = t;
-            if (work.empty() || work.back().pfx_kv0 != plo[i] || work.back().nrows == tile)
-                work.push_back({i, 0, plo[i], pn[i]});
+            if (work.empty() || work.back().pfx_off != plo[i] || work.back().nrows == tile)
+                work.push_back({i, 0, plo[i], pn[i], -1});
             work.back().nrows++;
         }
         int32_t* d_arr = c->buf<int32_t>("dec_rows", static_cast<size_t>(M) * 12);
@@ -858,9 +957,12 @@ void decode_steps(Ctx* c, sgc_model* m, const GenBuffers& g, const GenJob& job, 
         b.d_seg_lo = col(4);  // unused by the decode attention (own keys come from DecodeRows)
         b.d_work = d_work;
         b.n_work = static_cast<int>(work.size());
-        b.pfx_rows = static_cast<int>(kv->rows);
-        b.k_pfx = [kv](int l) { return static_cast<const bf16*>(kv->k_layer(l)); };
-        b.v_pfx = [kv](int l) { return static_cast<const bf16*>(kv->v_layer(l)); };
+        const KvPool* pool = &m->pool;
+        const size_t pls = static_cast<size_t>(pool->pages) * sgc::kPageTokens * d;
+        b.pfx_rows = static_cast<int>(pool->pages * sgc::kPageTokens);
+        b.k_pfx = [pool, pls](int l) { return static_cast<const bf16*>(pool->k + l * pls); };
+        b.v_pfx = [pool, pls](int l) { return static_cast<const bf16*>(pool->v + l * pls); };
+        b.d_bt = g.d_bt;
         bf16 *gk = g.gk, *gv = g.gv;
         const size_t grows = g.grows;
         b.k_loc = [gk, grows, d](int l) { return gk + l * grows * d; };
@@ -1465,6 +1567,7 @@ int sgc_ctx_destroy(sgc_ctx* ctx) {
         if (c->h_flags) cudaFreeHost(c->h_flags);
         for (auto& kv : c->pinned_bufs) cudaFreeHost(kv.second.ptr);
         cudaStreamDestroy(c->own_stream);
+        if (c->side) cudaStreamDestroy(c->side);
         delete ctx;
     });
 }
@@ -1577,6 +1680,8 @@ int sgc_model_destroy(sgc_model* m) {
         dfree(c, m->weights);
         dfree(c, m->rope_cos);
         dfree(c, m->rope_sin);
+        dfree(c, m->pool.k);
+        dfree(c, m->pool.v);
         c->sync();
         delete m;
     });
@@ -2009,15 +2114,12 @@ int sgc_kv_release(sgc_kv* kv) {
     return guarded([&] {
         if (!kv) return;
         Ctx* c = current(kv->model->c);
-        if (kv->owns_kv) {
-            dfree(c, kv->k);
-            dfree(c, kv->v);
-        }
+        // pages back to the model's pool and frees in stream order: no drain, so the host keeps
+        // preparing the next wave while the GPU still reads these pages
+        pool_release(kv->model, kv->pages);
+        dfree(c, kv->d_bt);
         dfree(c, kv->d_tokens);
         dfree(c, kv->d_tok_off);
-        // frees are stream-ordered; an arena view (batch-internal, owns no K/V) releases without
-        // draining the stream so the host keeps preparing the next wave while the GPU works
-        if (kv->owns_kv) c->sync();
         delete kv;
     });
 }
@@ -2025,46 +2127,67 @@ int sgc_kv_release(sgc_kv* kv) {
 uint32_t sgc_kv_count(const sgc_kv* kv) { return kv ? kv->n : 0; }
 uint64_t sgc_kv_tokens(const sgc_kv* kv, uint32_t i) { return kv && i < kv->n ? kv->len[i] : 0; }
 uint64_t sgc_kv_resident_bytes(const sgc_kv* kv) {
-    return kv ? kv->rows * static_cast<uint64_t>(kv->model->L) * 2 * kv->model->d * sizeof(bf16) : 0;
+    // resident pages (KVCache::resident_kv_bytes counts tokens; pages round up to 128 tokens)
+    return kv ? kv->pages.size() * page_bytes(kv->model) : 0;
 }
+uint32_t sgc_kv_pages(const sgc_kv* kv, uint32_t i, int32_t* pages) {
+    if (!kv || i >= kv->n) return 0;
+    const uint32_t n = kv->seg_pages(i);
+    if (pages) std::copy(kv->pages.begin() + kv->bt_off[i], kv->pages.begin() + kv->bt_off[i] + n, pages);
+    return n;
+}
+
+namespace {
+// device digests of segments `segs` of a handle (kv_digest kernel) into out[0 ..) (device), on
+// `stream`; meta / rows: scratch of >= 2 |segs| words and |segs| x 2 L x max len words
+void kv_digests(Ctx* c, cudaStream_t stream, const sgc_kv* kv, const std::vector<uint32_t>& segs, uint64_t* out,
+                uint32_t* d_meta, uint64_t* d_rows) {
+    const uint32_t n = static_cast<uint32_t>(segs.size());
+    if (!n) return;
+    std::vector<uint32_t> meta(2 * n);
+    uint32_t mx = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+        meta[i] = kv->bt_off[segs[i]];
+        meta[n + i] = static_cast<uint32_t>(kv->len[segs[i]]);
+        mx = std::max(mx, meta[n + i]);
+    }
+    SGC_CUDA_CHECK(cudaMemcpyAsync(d_meta, meta.data(), meta.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+    sgc::kv_digest(c, stream, out, d_rows, kv->model->pool.k, kv->model->pool.v, kv->layer_elems(), kv->d_bt, d_meta,
+                   d_meta + n, static_cast<int>(n), static_cast<int>(mx), kv->model->L, kv->model->d);
+}
+}  // namespace
 
 uint64_t sgc_kv_digest(const sgc_kv* kv, uint32_t i) {
     if (!kv || i >= kv->n) return 0;
-    uint64_t h = 0xcbf29ce484222325ULL;
     try {
         Ctx* c = current(kv->model->c);
-        // the KV was written on the context's non-blocking stream: a plain cudaMemcpy does not
-        // order after it
-        SGC_CUDA_CHECK(cudaStreamSynchronize(c->stream));
-        const size_t d = kv->model->d, n = kv->len[i] * d;
-        std::vector<bf16> buf(n);
-        for (int l = 0; l < kv->model->L; ++l) {
-            for (int which = 0; which < 2; ++which) {
-                const bf16* src = (which ? kv->v_layer(l) : kv->k_layer(l)) + kv->off[i] * d;
-                SGC_CUDA_CHECK(cudaMemcpy(buf.data(), src, n * sizeof(bf16), cudaMemcpyDeviceToHost));
-                const unsigned char* p = reinterpret_cast<const unsigned char*>(buf.data());
-                for (size_t b = 0; b < n * sizeof(bf16); ++b) {
-                    h ^= p[b];
-                    h *= 0x100000001b3ULL;
-                }
-            }
-        }
-        (void)c;
+        uint64_t* d_out = c->buf<uint64_t>("kv_digest_out", 1);
+        uint32_t* d_meta = c->buf<uint32_t>("kv_digest_meta", 2);
+        uint64_t* d_rows = c->buf<uint64_t>("kv_digest_rows", 2ull * kv->model->L * std::max<uint64_t>(1, kv->len[i]));
+        kv_digests(c, c->stream, kv, {i}, d_out, d_meta, d_rows);
+        uint64_t h = 0;
+        sgc::copy_out(c, &h, d_out, 1);
+        c->sync();
+        return h;
     } catch (const std::exception& e) {
         g_last_error = e.what();
         return 0;
     }
-    return h;
 }
 
 int sgc_kv_read(const sgc_kv* kv, uint32_t i, uint32_t layer, int is_v, float* out) {
     return guarded([&] {
         if (i >= kv->n || layer >= static_cast<uint32_t>(kv->model->L)) fail(SGC_DOMAIN, "kv_read: out of range");
-        SGC_CUDA_CHECK(cudaStreamSynchronize(kv->model->c->stream));  // see sgc_kv_digest
+        Ctx* c = current(kv->model->c);
         const size_t d = kv->model->d, n = kv->len[i] * d;
+        // gather the segment's rows of every layer through its pages, keep the requested layer
+        const int L = kv->model->L;
+        bf16* packed = c->buf<bf16>("kv_read_pack", static_cast<size_t>(L) * n);
+        sgc::kv_pages_pack(c, packed, is_v ? kv->model->pool.v : kv->model->pool.k, kv->layer_elems(),
+                           kv->d_bt + kv->bt_off[i], static_cast<int>(kv->len[i]), L, static_cast<int>(d), true);
         std::vector<bf16> buf(n);
-        const bf16* src = (is_v ? kv->v_layer(layer) : kv->k_layer(layer)) + kv->off[i] * d;
-        SGC_CUDA_CHECK(cudaMemcpy(buf.data(), src, n * sizeof(bf16), cudaMemcpyDeviceToHost));
+        sgc::copy_out(c, buf.data(), packed + static_cast<size_t>(layer) * n, n);
+        c->sync();
         std::vector<float> f(n);
         for (size_t t = 0; t < n; ++t) f[t] = __bfloat162float(buf[t]);
         SGC_CUDA_CHECK(cudaMemcpy(out, f.data(), n * sizeof(float), cudaMemcpyDefault));
@@ -2110,7 +2233,7 @@ int sgc_extend_generate(sgc_ctx* ctx, sgc_model* model, sgc_kv* kv, const uint32
         }
         for (uint32_t j = 0; j < n; ++j) {
             const int32_t S = static_cast<int32_t>(qo[j + 1] - qo[j]);
-            job.pfx_kv0.push_back(static_cast<int32_t>(kv->off[seg[j]]));
+            job.pfx_bt.push_back(static_cast<int32_t>(kv->bt_off[seg[j]]));
             job.pfx_len.push_back(static_cast<int32_t>(kv->len[seg[j]]));
             job.q_lo.push_back(keep.q_lo[j]);
             job.q_n.push_back(S);
@@ -2122,7 +2245,7 @@ int sgc_extend_generate(sgc_ctx* ctx, sgc_model* model, sgc_kv* kv, const uint32
         for (uint32_t j = 0; j < n; ++j) job.gen_row0.push_back(static_cast<int32_t>(j * mx));
         GenState st;
         st.init(job, mx, model->cfg.max_seq_len);
-        GenBuffers gb = gen_buffers(c, model, kv, &keep, job, static_cast<size_t>(n) * mx);
+        GenBuffers gb = gen_buffers(c, model, kv->pages, &keep, job, static_cast<size_t>(n) * mx);
         std::vector<uint32_t> all(n);
         std::iota(all.begin(), all.end(), 0u);
         decode_steps(c, model, gb, job, st, all, 0, pointer_bonus);
@@ -2379,25 +2502,30 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             while (wave_end.size() < n_waves) wave_end.push_back(nown);
         }
         {
-            // memory cap: a wave's prefill K/V (+ its forward activations) must fit beside the
-            // weights -- split any wave whose prefix rows exceed ~45% of the device (C4 with 256
-            // clusters in 2 waves would need ~125 GB of K/V per wave)
+            // KV page budget: a wave's representatives take whole 128-token pages of the model's
+            // pool, which may grow into the free device memory minus a reserve for the forward's
+            // activations (prefill runs in row chunks of <= 64k rows) and the extend scratch; split
+            // any wave whose pages exceed it (C4 with 256 clusters: ~137 GB of K/V in each of 2 waves)
             size_t free_b = 0, total_b = 0;
             SGC_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-            const double row_bytes = 2.0 * model->L * d * sizeof(bf16)                      // K/V, all layers
-                                     + d * (4.0 + 2 * 4) + 2.0 * model->ffn + 4.0 * d / 32;  // x, xb, q, ao, h, ss
-            const uint64_t cap = std::max<uint64_t>(1, static_cast<uint64_t>(0.45 * total_b / row_bytes));
+            const double act_row = d * (4.0 + 2 * 4) + 2.0 * model->ffn + 4.0 * d / 32;  // x, xb, q, ao, h, ss
+            const double reserve = 2.0 * 65536.0 * act_row + 0.06 * static_cast<double>(total_b);
+            const double pb = static_cast<double>(page_bytes(model));
+            const double budget = static_cast<double>(model->pool.free_pages.size()) * pb +
+                                  std::max(0.0, static_cast<double>(free_b) - reserve);
+            const uint64_t cap = std::max<uint64_t>(1, static_cast<uint64_t>(budget / pb));
             std::vector<uint32_t> split;
             uint32_t w0 = 0;
             for (uint32_t e : wave_end) {
-                uint64_t rows = 0;
+                uint64_t pages = 0;
                 for (uint32_t i = w0; i < e; ++i) {
-                    const uint64_t pr = reps.prefix_off[i + 1] - reps.prefix_off[i] + 1;
-                    if (rows > 0 && rows + pr > cap) {
+                    const uint64_t pr = (reps.prefix_off[i + 1] - reps.prefix_off[i] + 1 + sgc::kPageTokens - 1) /
+                                        sgc::kPageTokens;
+                    if (pages > 0 && pages + pr > cap) {
                         split.push_back(i);
-                        rows = 0;
+                        pages = 0;
                     }
-                    rows += pr;
+                    pages += pr;
                 }
                 split.push_back(e);
                 w0 = e;
@@ -2429,13 +2557,15 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         // ---- row budget of every wave: prefill rows (representatives + standalone fallbacks)
         // and kept question rows; with generation the waves' prefix / question K/V stay resident
         // until the end so stragglers of every wave decode together (one weight pass per step)
-        std::vector<uint64_t> wave_pf(wave_end.size(), 0), wave_qr(wave_end.size(), 0);
+        std::vector<uint64_t> wave_pf(wave_end.size(), 0), wave_qr(wave_end.size(), 0), wave_pg(wave_end.size(), 0);
+        auto pages_of = [](uint64_t rows) { return (rows + sgc::kPageTokens - 1) / sgc::kPageTokens; };
         {
             uint32_t w0 = 0;
             for (uint32_t wv = 0; wv < wave_end.size(); ++wv) {
                 for (uint32_t i = w0; i < wave_end[wv]; ++i) {
                     const uint64_t plen = reps.prefix_off[i + 1] - reps.prefix_off[i] + (d_soft ? 1 : 0);
                     wave_pf[wv] += plen;
+                    wave_pg[wv] += pages_of(plen);
                     for (uint32_t q : own_members[i]) {
                         const uint64_t qn = q_off[q + 1] - q_off[q];
                         if (plen + qn + lc.max_new_tokens > lc.max_seq_len) {
@@ -2446,7 +2576,9 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                             }
                             size_t allowed = lc.max_seq_len;
                             allowed -= std::min<size_t>(allowed, lc.max_new_tokens + (b->soft_prefix ? 1 : 0));
-                            wave_pf[wv] += std::min<uint64_t>(oo[q + 1] - oo[q] + qn, allowed) + (b->soft_prefix ? 1 : 0);
+                            const uint64_t fl = std::min<uint64_t>(oo[q + 1] - oo[q] + qn, allowed) + (b->soft_prefix ? 1 : 0);
+                            wave_pf[wv] += fl;
+                            wave_pg[wv] += pages_of(fl);
                         } else {
                             wave_qr[wv] += qn;
                         }
@@ -2455,26 +2587,34 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 w0 = wave_end[wv];
             }
         }
-        uint64_t pf_total = 0, qr_total = 0, pf_max = 0, qr_max = 0;
+        uint64_t pf_total = 0, qr_total = 0, pg_total = 0, pg_max = 0, qr_max = 0;
         for (size_t w = 0; w < wave_end.size(); ++w) {
             pf_total += wave_pf[w];
             qr_total += wave_qr[w];
-            pf_max = std::max(pf_max, wave_pf[w]);
+            pg_total += wave_pg[w];
+            pg_max = std::max(pg_max, wave_pg[w]);
             qr_max = std::max(qr_max, wave_qr[w]);
         }
-        // retain every wave's K/V only when generating and it fits comfortably (C3: ~45 GB)
+        // retain every wave's K/V only when generating and it fits comfortably (C3: ~45 GB):
+        // pages of every wave + kept question rows + generated rows, against the free device
+        // memory (weights and scratch already allocated; the pool's free pages and the re-used
+        // keep buffers count as free), 20% headroom for the forward activations
         const double kv_row_bytes = 2.0 * model->L * d * sizeof(bf16);
-        // (against what the device has free now, weights and scratch already allocated, keeping
-        // 20% headroom for the forward activations)
         size_t free_now = 0, total_now = 0;
         SGC_CUDA_CHECK(cudaMemGetInfo(&free_now, &total_now));
-        for (const char* nm : {"kv_arena_k", "kv_arena_v", "ex_keep_k", "ex_keep_v"}) {
+        double avail_now = static_cast<double>(free_now) +
+                           static_cast<double>(model->pool.free_pages.size()) * page_bytes(model);
+        for (const char* nm : {"ex_keep_k", "ex_keep_v"}) {
             auto it = c->scratch.find(nm);  // grow-only buffers this batch re-uses (or regrows)
-            if (it != c->scratch.end()) free_now += it->second.bytes;
+            if (it != c->scratch.end()) avail_now += static_cast<double>(it->second.bytes);
         }
-        const bool retain = gen_on && (pf_total + qr_total + static_cast<double>(m) * max_new) * kv_row_bytes <
-                                          0.8 * static_cast<double>(free_now);
-        const uint64_t arena_rows = retain ? pf_total : pf_max;
+        const bool retain = gen_on && static_cast<double>(pg_total) * page_bytes(model) +
+                                              (qr_total + static_cast<double>(m) * max_new) * kv_row_bytes <
+                                          0.8 * avail_now;
+        // grow the pool once up front (a mid-batch growth would copy the live pages)
+        pool_grow(c, model, model->pool.live() + static_cast<uint32_t>(retain ? pg_total : pg_max));
+        o->kv_pages_peak = 0;
+        o->kv_page_bytes = page_bytes(model);
         ExtendKeep keep_all;
         if (gen_on) {
             keep_all.rows = std::max<uint64_t>(1, retain ? qr_total : qr_max);
@@ -2488,9 +2628,48 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         GenState gst;
         gst.max_new = std::max<uint32_t>(1, max_new);
         std::vector<uint32_t> gen_q;  // job index -> query
-        sgc_kv kv_all;                // view over the whole arena (the decode's prefix base)
-        kv_all.model = model;
-        uint64_t arena_row0 = 0, keep_row0 = 0;
+        // retained waves' sealed prefixes (generation) and the block table over all of them
+        std::vector<std::unique_ptr<sgc_kv, int (*)(sgc_kv*)>> held;
+        std::vector<int32_t> gen_bt;
+        // sealed-prefix digests (KVCache::prefix_digest at seal, re-checked once the members are
+        // served, cache_engine.cpp:189, :210): device slots [seal | end] per served cluster
+        // The digests run on a side stream: the seal digest overlaps the members' extend (which only
+        // reads the prefix pages), the end digest follows the wave's last use of them and the main
+        // stream waits for it before those pages can be reused. Scratch is sized once up front.
+        const bool verify = b->verify_prefix != 0;
+        const uint32_t dig_cap = static_cast<uint32_t>(owned.size());
+        uint64_t* d_dig = verify ? c->buf<uint64_t>("run_digests", 2 * static_cast<size_t>(dig_cap) + 2) : nullptr;
+        uint32_t* d_dig_meta[2] = {nullptr, nullptr};
+        uint64_t* d_dig_rows[2] = {nullptr, nullptr};
+        if (verify) {  // two sets: the seal digest of wave w+1 may overlap the end digest of wave w
+            for (int t = 0; t < 2; ++t) {
+                d_dig_meta[t] = c->buf<uint32_t>(t ? "run_dig_meta1" : "run_dig_meta0", 2 * static_cast<size_t>(dig_cap) + 2);
+                d_dig_rows[t] = c->buf<uint64_t>(t ? "run_dig_rows1" : "run_dig_rows0",
+                                                 static_cast<size_t>(dig_cap) * 2 * model->L * lc.max_seq_len + 1);
+            }
+        }
+        std::vector<std::pair<uint32_t, uint32_t>> dig_slot;  // (cluster, seal slot); end slot = seal + dig_cap
+        uint32_t dig_n = 0;
+        std::vector<std::pair<uint32_t, std::vector<uint32_t>>> dig_wave;  // held waves: (first slot, segments)
+        // digest of segments `segs` of `kv` into slots slot0.. after everything on the main stream so far
+        auto digest_wave = [&](const sgc_kv* kv, const std::vector<uint32_t>& segs, uint32_t slot0, bool end) {
+            cudaStream_t side = c->side_stream();
+            cudaEvent_t e = c->event();
+            SGC_CUDA_CHECK(cudaEventRecord(e, c->stream));
+            SGC_CUDA_CHECK(cudaStreamWaitEvent(side, e, 0));
+            // the seal (end) digests of consecutive waves alternate scratch sets 0 / 1 -- both
+            // run on the one side stream, so a set is never overwritten while in use
+            const int t = end ? 1 : 0;
+            kv_digests(c, side, kv, segs, d_dig + slot0 + (end ? dig_cap : 0), d_dig_meta[t], d_dig_rows[t]);
+            if (end) {  // the pages go back to the pool after this: the main stream waits for it
+                cudaEvent_t e2 = c->event();
+                SGC_CUDA_CHECK(cudaEventRecord(e2, side));
+                SGC_CUDA_CHECK(cudaStreamWaitEvent(c->stream, e2, 0));
+                c->event_pool.push_back(e2);
+            }
+            c->event_pool.push_back(e);
+        };
+        uint64_t keep_row0 = 0;
         uint32_t wb = 0;
         for (uint32_t wv = 0; wv < wave_end.size(); ++wv) {
             const uint32_t we = wave_end[wv];
@@ -2511,7 +2690,6 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             const uint32_t job0 = gj.size();  // this wave's decode rows: job0 .. (members, then fallbacks)
             ExtendKeep keep = keep_all;
             keep.base = retain ? keep_row0 : 0;
-            if (!retain) arena_row0 = 0;
             // sequences of the wave: local representatives, standalone fallbacks, then the split
             // clusters' representatives whose sealed K/V arrive from their owner (not computed here)
             std::vector<uint32_t> seq_of(we - wb, 0), remote_i, mem_cl;
@@ -2564,10 +2742,15 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             // them no sync is needed and the host prepares the next wave while the GPU works
             std::vector<float> seq_logits(fb_q.empty() ? 0 : static_cast<size_t>(ns) * SGC_VOCAB);
             sgc_kv* kv = do_prefill(c, model, ns, seq_off.data(), seq_tok.data(), seq_soft_vec.data(),
-                                    seq_soft.data(), fb_q.empty() ? nullptr : seq_logits.data(), /*arena=*/true,
-                                    arena_row0, arena_rows, /*sync=*/!fb_q.empty(), n_remote);
+                                    seq_soft.data(), fb_q.empty() ? nullptr : seq_logits.data(),
+                                    /*sync=*/!fb_q.empty(), n_remote);
             std::unique_ptr<sgc_kv, int (*)(sgc_kv*)> kv_guard(kv, sgc_kv_release);
-            prefill_rows += kv->rows - (n_remote ? kv->rows - kv->off[ns - n_remote] : 0);
+            for (uint32_t s = 0; s < ns - n_remote; ++s) prefill_rows += kv->len[s];
+            o->kv_pages_peak = std::max<uint64_t>(o->kv_pages_peak, model->pool.live());
+            // decode jobs index prefix pages through one block table: every retained wave's pages
+            // back to back (generation), or this wave's own
+            const int32_t bt_base = retain ? static_cast<int32_t>(gen_bt.size()) : 0;
+            if (retain) gen_bt.insert(gen_bt.end(), kv->pages.begin(), kv->pages.end());
             for (uint32_t i = wb; i < we; ++i)
                 if (o->prefilled && !is_remote(owned[i])) o->prefilled[owned[i]] = 1;
             if (wv == 0 && n_split > 0) {
@@ -2578,39 +2761,60 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 for (uint32_t i = wb; i < we; ++i)
                     if (is_split(owned[i])) mine.push_back({owned[i], i});
                 std::sort(mine.begin(), mine.end());
+                // pages differ between ranks: the owner packs a segment's rows of every layer
+                // ([L][len][d] for K, then V) into a staging buffer, the receiver unpacks into its pages
                 std::vector<sgc::P2P> sends, recvs;
+                size_t stage_elems = 0;
+                for (auto [ci, i] : mine) stage_elems += 2ull * model->L * kv->len[seq_of[i - wb]] * d;
+                bf16* stage = c->buf<bf16>("xfer_stage", std::max<size_t>(1, stage_elems));
+                std::vector<std::pair<uint32_t, size_t>> unpack;  // (sequence, staging offset)
+                size_t so = 0;
                 for (auto [ci, i] : mine) {
                     const uint32_t s = seq_of[i - wb];
-                    const size_t bytes = static_cast<size_t>(kv->len[s]) * d * sizeof(bf16);
-                    for (int l = 0; l < model->L; ++l) {
-                        bf16* kp = kv->k_layer(l) + static_cast<size_t>(kv->off[s]) * d;
-                        bf16* vp = kv->v_layer(l) + static_cast<size_t>(kv->off[s]) * d;
-                        if (owner[ci] == me) {
-                            for (uint32_t p : peers[ci]) {
-                                sends.push_back({kp, bytes, static_cast<int>(p)});
-                                sends.push_back({vp, bytes, static_cast<int>(p)});
-                                o->prefix_bytes_sent += 2 * bytes;
-                            }
-                        } else {
-                            recvs.push_back({kp, bytes, static_cast<int>(owner[ci])});
-                            recvs.push_back({vp, bytes, static_cast<int>(owner[ci])});
-                            o->prefix_bytes_received += 2 * bytes;
+                    const size_t n = static_cast<size_t>(model->L) * kv->len[s] * d, bytes = n * sizeof(bf16);
+                    bf16 *ks = stage + so, *vs = stage + so + n;
+                    if (owner[ci] == me) {
+                        sgc::kv_pages_pack(c, ks, model->pool.k, kv->layer_elems(), kv->d_bt + kv->bt_off[s],
+                                           static_cast<int>(kv->len[s]), model->L, d, true);
+                        sgc::kv_pages_pack(c, vs, model->pool.v, kv->layer_elems(), kv->d_bt + kv->bt_off[s],
+                                           static_cast<int>(kv->len[s]), model->L, d, true);
+                        for (uint32_t p : peers[ci]) {
+                            sends.push_back({ks, bytes, static_cast<int>(p)});
+                            sends.push_back({vs, bytes, static_cast<int>(p)});
+                            o->prefix_bytes_sent += 2 * bytes;
                         }
+                    } else {
+                        recvs.push_back({ks, bytes, static_cast<int>(owner[ci])});
+                        recvs.push_back({vs, bytes, static_cast<int>(owner[ci])});
+                        o->prefix_bytes_received += 2 * bytes;
+                        unpack.push_back({s, so});
                     }
+                    so += 2 * n;
                 }
                 comm->exchange(c, sends, recvs);
+                for (auto [s, off] : unpack) {
+                    const size_t n = static_cast<size_t>(model->L) * kv->len[s] * d;
+                    sgc::kv_pages_pack(c, stage + off, model->pool.k, kv->layer_elems(), kv->d_bt + kv->bt_off[s],
+                                       static_cast<int>(kv->len[s]), model->L, d, false);
+                    sgc::kv_pages_pack(c, stage + off + n, model->pool.v, kv->layer_elems(), kv->d_bt + kv->bt_off[s],
+                                       static_cast<int>(kv->len[s]), model->L, d, false);
+                }
             }
             {
                 cudaEvent_t es = c->event();
                 SGC_CUDA_CHECK(cudaEventRecord(es, c->stream));
                 ev_seal.push_back(es);
             }
-            const int32_t pfx_base = static_cast<int32_t>(arena_row0);  // absolute arena row of this wave
-            if (!kv_all.k) {
-                kv_all.k = kv->k - arena_row0 * d;
-                kv_all.v = kv->v - arena_row0 * d;
-                kv_all.rows = arena_rows;
-                kv_all.lstride = arena_rows;
+            uint32_t dig0 = 0;
+            std::vector<uint32_t> dig_segs;  // the wave's representatives (fallbacks are private)
+            if (verify) {  // sealed: digest every representative of the wave (after the exchange)
+                dig0 = dig_n;
+                for (uint32_t i = wb; i < we; ++i) {
+                    dig_slot.push_back({owned[i], dig0 + static_cast<uint32_t>(dig_segs.size())});
+                    dig_segs.push_back(seq_of[i - wb]);
+                }
+                digest_wave(kv, dig_segs, dig0, false);
+                dig_n += static_cast<uint32_t>(dig_segs.size());
             }
             const double tw1 = now_ms();
             pf_ms += tw1 - tw0;
@@ -2648,7 +2852,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                     if (gen_on) {
                         const int32_t S = static_cast<int32_t>(q_off[q + 1] - q_off[q]);
                         gen_q.push_back(q);
-                        gj.pfx_kv0.push_back(pfx_base + static_cast<int32_t>(kv->off[mem_seg[j]]));
+                        gj.pfx_bt.push_back(bt_base + static_cast<int32_t>(kv->bt_off[mem_seg[j]]));
                         gj.pfx_len.push_back(static_cast<int32_t>(kv->len[mem_seg[j]]));
                         gj.q_lo.push_back(keep.q_lo[j]);
                         gj.q_n.push_back(S);
@@ -2700,7 +2904,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 fb_flag[q] = 1;
                 if (gen_on) {  // standalone decode continues from its own sealed prompt
                     gen_q.push_back(q);
-                    gj.pfx_kv0.push_back(pfx_base + static_cast<int32_t>(kv->off[s]));
+                    gj.pfx_bt.push_back(bt_base + static_cast<int32_t>(kv->bt_off[s]));
                     gj.pfx_len.push_back(static_cast<int32_t>(kv->len[s]));
                     gj.q_lo.push_back(0);
                     gj.q_n.push_back(0);
@@ -2732,23 +2936,18 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 std::vector<uint32_t> sel;
                 for (uint32_t j = job0; j < gj.size(); ++j) sel.push_back(j);
                 const uint32_t min_active = static_cast<uint32_t>((static_cast<uint64_t>(sel.size()) * defer_pct + 99) / 100);
-                sgc_kv wave_view = kv_all;
-                if (!retain) {  // this wave's prefixes only (the arena is reused by the next wave)
-                    wave_view = *kv;
-                    wave_view.off.clear();
-                    wave_view.len.clear();
-                    wave_view.d_tokens = nullptr;
-                    wave_view.d_tok_off = nullptr;
-                    for (uint32_t j = job0; j < gj.size(); ++j) gj.pfx_kv0[j] -= pfx_base;
-                }
-                GenBuffers gb = gen_buffers(c, model, &wave_view, &keep_all, gj, static_cast<size_t>(m) * gst.max_new);
+                GenBuffers gb = gen_buffers(c, model, retain ? gen_bt : kv->pages, &keep_all, gj,
+                                            static_cast<size_t>(m) * gst.max_new);
                 decode_steps(c, model, gb, gj, gst, sel, min_active, b->pointer_bonus);
                 dec_ms += now_ms() - td0;
             }
             for (uint32_t j = job0; j < gj.size(); ++j) wave_of_job.push_back(static_cast<int32_t>(wv));
             if (retain) {
-                arena_row0 += kv->rows;
                 keep_row0 += wave_qr[wv];
+                held.push_back(std::move(kv_guard));  // its pages stay until the stragglers are done
+                dig_wave.push_back({dig0, dig_segs});
+            } else if (verify) {
+                digest_wave(kv, dig_segs, dig0, true);  // served: re-check before the pages are released
             }
             wb = we;
         }
@@ -2759,11 +2958,13 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 if (!gst.done[j]) rest.push_back(j);
             if (!rest.empty()) {
                 const double td0 = now_ms();
-                GenBuffers gb = gen_buffers(c, model, &kv_all, &keep_all, gj, static_cast<size_t>(m) * gst.max_new);
+                GenBuffers gb = gen_buffers(c, model, gen_bt, &keep_all, gj, static_cast<size_t>(m) * gst.max_new);
                 decode_steps(c, model, gb, gj, gst, rest, 0, b->pointer_bonus);
                 dec_ms += now_ms() - td0;
             }
         }
+        if (verify)
+            for (size_t w = 0; w < held.size(); ++w) digest_wave(held[w].get(), dig_wave[w].second, dig_wave[w].first, true);
         if (gen_on) {
             decode_rows = gst.rows;
             for (uint32_t j = 0; j < gj.size(); ++j) {
@@ -2776,6 +2977,20 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         }
         c->sync();
         check_forward_flags(c);
+        if (o->prefix_digest)
+            for (uint32_t ci = 0; ci < k; ++ci) o->prefix_digest[ci] = 0;
+        if (verify && dig_n) {
+            // the sealed prefix must be byte-identical after serving its members (cache_engine.cpp:210)
+            std::vector<uint64_t> dg(2 * static_cast<size_t>(dig_cap) + 2);
+            sgc::copy_out(c, dg.data(), d_dig, dg.size());
+            c->sync();
+            for (auto [ci, slot] : dig_slot) {
+                if (dg[slot] != dg[slot + dig_cap])
+                    fail(SGC_LOGIC, "sealed prefix KV bytes changed while serving members (cluster " +
+                                        std::to_string(ci) + ")");
+                if (o->prefix_digest) o->prefix_digest[ci] = dg[slot];
+            }
+        }
         for (uint32_t k = 0; k < def_n; ++k) {
             const uint32_t q = def_q[k];
             if (o->logits)
@@ -3000,10 +3215,10 @@ int sgc_attention_bf16(sgc_ctx* ctx, const void* q, const void* k_pfx, const voi
         Ctx* c = current(&ctx->c);
         std::vector<sgc::AttnWork> w(n_work);
         for (uint32_t i = 0; i < n_work; ++i) {
-            w[i] = {work[4 * i], work[4 * i + 1], work[4 * i + 2], work[4 * i + 3]};
+            w[i] = {work[4 * i], work[4 * i + 1], work[4 * i + 2], work[4 * i + 3], -1};  // contiguous rows
             if (w[i].nrows < 1 || w[i].nrows > tile || w[i].row0 < 0 ||
                 static_cast<uint32_t>(w[i].row0 + w[i].nrows) > rows ||
-                static_cast<uint32_t>(w[i].pfx_kv0 + w[i].pfx_len) > pfx_rows)
+                static_cast<uint32_t>(w[i].pfx_off + w[i].pfx_len) > pfx_rows)
                 fail(SGC_DOMAIN, "attention: work unit out of range");
         }
         sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("dbg_attn_work", n_work);
@@ -3034,7 +3249,6 @@ int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value) {
     return guarded([&] {
         if (std::string(name) == "gemm_pairs") sgc::gemm_set_pairs(value != 0);
         else if (std::string(name) == "attn_split") sgc::attention_set_split(value != 0);
-        else if (std::string(name) == "attn_db") sgc::attention_set_db(value != 0);
         else if (std::string(name) == "decode_defer_pct") ctx->c.decode_defer_pct = static_cast<uint32_t>(std::max<int64_t>(0, value));
         else fail(SGC_DOMAIN, std::string("unknown option ") + name);
     });

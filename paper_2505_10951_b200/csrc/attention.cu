@@ -141,15 +141,17 @@ __global__ void __launch_bounds__(kThreads)
 
     auto issue = [&](int b, int buf) {
         if (b < nA) {
-            int k0 = b * TK;
+            int k0 = b * TK;  // a 64-key block never straddles a 128-token page
             int nv = min(TK, w.pfx_len - k0);
-            load_block<HD>(sK(buf), p.k_pfx, d, c0, w.pfx_kv0 + k0, nv);
-            load_block<HD>(sV(buf), p.v_pfx, d, c0, w.pfx_kv0 + k0, nv);
+            const int row = kv_row_of(p.bt, w.pfx_off, k0);
+            load_block<HD>(sK(buf), p.k_pfx, d, c0, row, nv);
+            load_block<HD>(sV(buf), p.v_pfx, d, c0, row, nv);
         } else {
             int k0 = loc_first + (b - nA) * TK;
             int nv = min(TK, loc_last + 1 - k0);
-            load_block<HD>(sK(buf), p.k_loc, d, c0, p.loc_kv0 + k0, nv);
-            load_block<HD>(sV(buf), p.v_loc, d, c0, p.loc_kv0 + k0, nv);
+            const int row = w.loc_bt >= 0 ? kv_row_of(p.bt, w.loc_bt, (b - nA) * TK) : p.loc_kv0 + k0;
+            load_block<HD>(sK(buf), p.k_loc, d, c0, row, nv);
+            load_block<HD>(sV(buf), p.v_loc, d, c0, row, nv);
         }
         cp_commit();
     };
@@ -354,12 +356,15 @@ __global__ void __launch_bounds__(256) decode_local_kernel(DecodeAttnParams p) {
     float m = -INFINITY, l = 0.f, acc[DPL];
 #pragma unroll
     for (int i = 0; i < DPL; ++i) acc[i] = 0.f;
-    auto run = [&](const __nv_bfloat16* K, const __nv_bfloat16* V, int lo, int n) {
+    // keys [0, n) of a range at rows lo.. (bt == nullptr) or through the block table bt at offset
+    // lo; a 32-key chunk never straddles a 128-token page
+    auto run = [&](const __nv_bfloat16* K, const __nv_bfloat16* V, int lo, int n, const int32_t* bt) {
         for (int k0 = 0; k0 < n; k0 += 32) {
             const int key = k0 + lane;
+            const int row0 = kv_row_of(bt, lo, k0);
             float sc = -INFINITY;
             if (key < n) {
-                const __nv_bfloat16* kr = K + static_cast<size_t>(lo + key) * p.d + h * HD;
+                const __nv_bfloat16* kr = K + static_cast<size_t>(row0 + lane) * p.d + h * HD;
                 float a0 = 0.f, a1 = 0.f;
                 // the key row in 32-byte loads (LDG.256): all of them in flight before the math
                 uint32_t u[HD / 16][8];
@@ -389,7 +394,7 @@ __global__ void __launch_bounds__(256) decode_local_kernel(DecodeAttnParams p) {
 #pragma unroll
             for (int i = 0; i < DPL; ++i) acc[i] *= alpha;
             const int nk = min(32, n - k0);
-            const __nv_bfloat16* vb = V + static_cast<size_t>(lo + k0) * p.d + col;
+            const __nv_bfloat16* vb = V + static_cast<size_t>(row0) * p.d + col;
 #pragma unroll 8
             for (int j = 0; j < nk; ++j) {
                 const float pj = __shfl_sync(0xffffffffu, pk, j);
@@ -412,9 +417,9 @@ __global__ void __launch_bounds__(256) decode_local_kernel(DecodeAttnParams p) {
             m = mn;
         }
     };
-    if (!p.part_o && p.p_n) run(p.k_p, p.v_p, p.p_lo[r], p.p_n[r]);
-    if (p.q_n) run(p.k_q, p.v_q, p.q_lo[r], p.q_n[r]);
-    if (p.g_n) run(p.k_g, p.v_g, p.g_lo[r], p.g_n[r]);
+    if (!p.part_o && p.p_n) run(p.k_p, p.v_p, p.p_lo[r], p.p_n[r], p.p_bt);
+    if (p.q_n) run(p.k_q, p.v_q, p.q_lo[r], p.q_n[r], nullptr);
+    if (p.g_n) run(p.k_g, p.v_g, p.g_lo[r], p.g_n[r], nullptr);
     float o1[DPL], w1 = 0.f, w2 = 1.f, den = l;
 #pragma unroll
     for (int i = 0; i < DPL; ++i) o1[i] = 0.f;

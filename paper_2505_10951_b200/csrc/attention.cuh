@@ -7,11 +7,21 @@ namespace sgc {
 
 struct Ctx;
 
-// A tile of <= 64 consecutive query rows that share one sealed prefix.
+// KV pages: 128 tokens (= the tcgen05 kernel's key block). A key sequence is read through a
+// block table: key j of a sequence whose pages start at table offset `off` lives at pool row
+// bt[off + j / 128] * 128 + j % 128 (bt == nullptr: contiguous rows, key j at row off + j).
+constexpr int kPageTokens = 128;
+__host__ __device__ inline int kv_row_of(const int32_t* bt, int off, int j) {
+    return bt ? bt[off + j / kPageTokens] * kPageTokens + j % kPageTokens : off + j;
+}
+
+// A tile of consecutive query rows that share one sealed prefix.
 struct AttnWork {
     int row0, nrows;
-    int pfx_kv0;  // first KV-pool row of the shared prefix
+    int pfx_off;  // prefix: block-table offset of the sealed prefix's pages (bt) or its first row
     int pfx_len;  // prefix keys (0 for representative prefill)
+    int loc_bt;   // own keys: -1 = contiguous batch rows of k_loc / v_loc; >= 0 = block-table
+                  // offset of the sequence's pages in k_loc / v_loc (paged prefill)
 };
 
 struct AttnParams {
@@ -24,6 +34,7 @@ struct AttnParams {
     int loc_kv0;
     const int32_t* seg_lo;  // [rows] first row of the row's own sequence (causal window start)
     const AttnWork* work;
+    const int32_t* bt = nullptr;  // block table of the pages the work items reference (device)
     int d;
     float scale;  // 1/sqrt(head_dim) (lm_core.cpp:188)
     // partial mode (tcgen05 kernel only): prefix keys only, fp32 normalized O + log2-sum-exp
@@ -40,8 +51,6 @@ bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, in
 inline bool attention_tc_supported(int hd) { return hd == 64 || hd == 128; }
 // split every S row over two softmax warpgroups, or one thread per row (default)
 void attention_set_split(bool on);
-// double-buffered S with 64-key blocks (default on) or the single-buffered 128-key kernel
-void attention_set_db(bool on);
 
 // Decode step (attention.cu): merge the prefix partial (part_o, part_lse from the tcgen05 kernel
 // in partial mode, or none when part_o == nullptr) with each row's own keys: question rows
@@ -50,8 +59,10 @@ void attention_set_db(bool on);
 struct DecodeAttnParams {
     const __nv_bfloat16* q;
     const __nv_bfloat16 *k_p, *v_p, *k_q, *v_q, *k_g, *v_g;
-    // prefix range [p_lo, p_lo + p_n) of (k_p, v_p): read here only when part_o == nullptr
+    // prefix keys [0, p_n) of (k_p, v_p) through the block table p_bt at offset p_lo (p_bt ==
+    // nullptr: rows p_lo ..): read here only when part_o == nullptr
     const int32_t *p_lo, *p_n, *q_lo, *q_n, *g_lo, *g_n;
+    const int32_t* p_bt = nullptr;
     const float* part_o;
     const float* part_lse;
     __nv_bfloat16* out;

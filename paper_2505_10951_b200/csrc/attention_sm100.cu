@@ -25,6 +25,8 @@
 //
 // Persistent: CTAs loop over (unit, head) items; units never straddle clusters (members) or
 // sequences (representative prefill).
+#include <atomic>
+
 #include "attention.cuh"
 #include "common.cuh"
 #include "sched.cuh"
@@ -38,7 +40,6 @@ constexpr int BQ = 128;   // rows per query tile (two tiles per unit)
 constexpr int BKV = 128;  // keys per block
 // threads: loader warp, MMA warp, 2 tiles x SPLIT softmax warpgroups (SPLIT = 1: 320, 2: 576)
 bool g_attn_split = false;  // two softmax warpgroups per query tile (sgc_set_option "attn_split"; measured no faster)
-bool g_attn_db = false;     // double-buffered 64-key variant (sgc_set_option "attn_db")
 constexpr int kKStages = 3;
 constexpr int kVStages = 2;
 // SGC_POLY_NUM / SGC_POLY_DEN of the exponential pairs run as a polynomial on the FMA pipe
@@ -88,6 +89,7 @@ struct TcParams {
     int d;
     float scale_log2;
     uint32_t* sched;  // dynamic item counter (sched.cuh)
+    const int32_t* bt;  // block table (AttnParams::bt)
 };
 using ItemRing = UnitRing<4>;
 // what the producer resolved for a claimed item (published with the ring slot, so the MMA and
@@ -293,7 +295,11 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 const int nbu = max(u.nb[0], u.nb[1]);
                 for (int b = 0; b < nbu; ++b, ++g) {
                     const bool pfx = b < u.nA;
-                    const int row = pfx ? w.pfx_kv0 + b * BKV : u.loc_first + (b - u.nA) * BKV;
+                    // 128-key block == one page: prefix pages / the sequence's own pages
+                    // (paged prefill) through the block table, or contiguous scratch rows
+                    const int row = pfx ? kv_row_of(p.bt, w.pfx_off, b * BKV)
+                                        : (w.loc_bt >= 0 ? kv_row_of(p.bt, w.loc_bt, (b - u.nA) * BKV)
+                                                         : u.loc_first + (b - u.nA) * BKV);
                     const int ks = g % kKStages;
                     ptx::mbar_wait(&k_empty[ks], ((g / kKStages) & 1) ^ 1);
                     ptx::mbar_expect_tx(&k_full[ks], C::kKBytes);
@@ -632,401 +638,14 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
     }
 }
 
-// ============================================================================================
-// Double-buffered variant: 64-key blocks and TWO S buffers per query tile (TMEM: S_A0 S_A1 S_B0
-// S_B1 (64 columns each) | O_A | O_B), so the MMA warp computes S(j+2) while the softmax still
-// works on block j+1 -- the softmax never waits on the QK^T of its next block, only on its own
-// work, and the tensor pipe always has the other tile's and the next block's MMAs queued.
-//   MMA warp, per block j (both tiles): O_X += P_X(j) V_j (after the tile's softmax of block j),
-//     then S_X(j+2) = Q_X K_{j+2}^T into the buffer P_X(j) just left (tcgen05 ops of one thread run
-//     in order); pv_done_X is committed after every PV so a softmax that must rescale O (its lazy
-//     max moved) first waits for the previous PV of its tile.
-constexpr int BKD = 64;   // keys per block
-constexpr int kKStD = 5;  // K ring stages (16 KB each at hd 128)
-constexpr int kVStD = 5;  // V ring stages
-
-template <int HD>
-struct DbCfg {
-    static constexpr int kSub = HD / 64;
-    static constexpr int kQBytes = BQ * HD * 2;
-    static constexpr int kKBytes = BKD * HD * 2;
-    static constexpr int kVBytes = BKD * HD * 2;
-    static constexpr int kSmem = 2 * kQBytes + kKStD * kKBytes + kVStD * kVBytes + 512;
-    static constexpr uint32_t kO = 256;  // O_X at column 256 + X * 128; S_Xb at X * 128 + b * 64
-};
-
-__device__ __forceinline__ UnitPlan plan_unit_db(const AttnWork& w, const int32_t* seg_lo, bool partial) {
-    UnitPlan u;
-    u.nA = (w.pfx_len + BKD - 1) / BKD;
-    u.loc_first = partial ? 0 : seg_lo[w.row0];
-#pragma unroll
-    for (int x = 0; x < 2; ++x) {
-        u.nrows[x] = min(BQ, max(0, w.nrows - x * BQ));
-        const int last = w.row0 + x * BQ + u.nrows[x] - 1;
-        u.nb[x] = u.nrows[x] <= 0 ? 0 : (partial ? u.nA : u.nA + (last - u.loc_first + BKD) / BKD);
-    }
-    return u;
-}
-
-template <int HD>
-__global__ void __launch_bounds__(320, 1)
-    attn_db_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKp,
-                   const __grid_constant__ CUtensorMap tmVp, const __grid_constant__ CUtensorMap tmKl,
-                   const __grid_constant__ CUtensorMap tmVl, TcParams p) {
-    using C = DbCfg<HD>;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* sQ = smem;
-    uint8_t* sK = sQ + 2 * C::kQBytes;
-    uint8_t* sV = sK + kKStD * C::kKBytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVStD * C::kVBytes);
-    uint64_t* q_full = bars + 0;     // [2]
-    uint64_t* q_empty = bars + 2;    // [2]
-    uint64_t* k_full = bars + 4;     // [5]
-    uint64_t* k_empty = bars + 9;    // [5]
-    uint64_t* v_full = bars + 14;    // [5]
-    uint64_t* v_empty = bars + 19;   // [5]
-    uint64_t* s_full = bars + 24;    // [2 tiles][2 buffers]
-    // p_full is per S buffer like s_full: S(b) and S(b+1) are both in flight, so the softmax can
-    // finish two blocks before the MMA observes the first -- one barrier would skip a phase
-    uint64_t* p_full = bars + 28;    // [2 tiles][2 buffers]
-    uint64_t* o_full = bars + 32;    // [2]
-    uint64_t* pv_done = bars + 34;   // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 36);
-
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    const int n_items = p.n_work * p.heads;
-    const bool partial = p.part_o != nullptr;
-
-    if (warp == 0 && lane == 0) {
-        ptx::tma_prefetch_desc(&tmQ);
-        ptx::tma_prefetch_desc(&tmKp);
-        ptx::tma_prefetch_desc(&tmVp);
-        ptx::tma_prefetch_desc(&tmKl);
-        ptx::tma_prefetch_desc(&tmVl);
-        for (int i = 0; i < kKStD; ++i) {
-            ptx::mbar_init(&k_full[i], 1);
-            ptx::mbar_init(&k_empty[i], 1);
-            ptx::mbar_init(&v_full[i], 1);
-            ptx::mbar_init(&v_empty[i], 1);
-        }
-        for (int i = 0; i < 2; ++i) {
-            ptx::mbar_init(&q_full[i], 1);
-            ptx::mbar_init(&q_empty[i], 1);
-            ptx::mbar_init(&p_full[2 * i], 128);
-            ptx::mbar_init(&p_full[2 * i + 1], 128);
-            ptx::mbar_init(&o_full[i], 1);
-            ptx::mbar_init(&pv_done[i], 1);
-            ptx::mbar_init(&s_full[2 * i], 1);
-            ptx::mbar_init(&s_full[2 * i + 1], 1);
-        }
-        ptx::fence_barrier_init();
-    }
-    if (warp == 0) ptx::tmem_alloc<512>(tmem_slot);
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            uint32_t g = 0, qit[2] = {0, 0};
-            for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-                const int h = item / p.n_work;
-                const AttnWork w = p.work[item % p.n_work];
-                const UnitPlan u = plan_unit_db(w, p.seg_lo, partial);
-#pragma unroll
-                for (int x = 0; x < 2; ++x) {
-                    if (!u.nb[x]) continue;
-                    ptx::mbar_wait(&q_empty[x], (qit[x] & 1) ^ 1);
-                    ptx::mbar_expect_tx(&q_full[x], C::kQBytes);
-#pragma unroll
-                    for (int sI = 0; sI < C::kSub; ++sI)
-                        ptx::tma_load_2d(sQ + x * C::kQBytes + sI * (BQ * 128), &tmQ, &q_full[x], h * HD + sI * 64,
-                                         w.row0 + x * BQ);
-                    ++qit[x];
-                }
-                const int nbu = max(u.nb[0], u.nb[1]);
-                for (int b = 0; b < nbu; ++b, ++g) {
-                    const bool pfx = b < u.nA;
-                    const int row = pfx ? w.pfx_kv0 + b * BKD : u.loc_first + (b - u.nA) * BKD;
-                    const int st = g % kKStD;
-                    const uint32_t ph = ((g / kKStD) & 1) ^ 1;
-                    ptx::mbar_wait(&k_empty[st], ph);
-                    ptx::mbar_expect_tx(&k_full[st], C::kKBytes);
-#pragma unroll
-                    for (int sI = 0; sI < C::kSub; ++sI)
-                        ptx::tma_load_2d(sK + st * C::kKBytes + sI * (BKD * 128), pfx ? &tmKp : &tmKl, &k_full[st],
-                                         h * HD + sI * 64, row);
-                    ptx::mbar_wait(&v_empty[st], ph);
-                    ptx::mbar_expect_tx(&v_full[st], C::kVBytes);
-#pragma unroll
-                    for (int sI = 0; sI < C::kSub; ++sI)
-                        ptx::tma_load_2d(sV + st * C::kVBytes + sI * (BKD * 128), pfx ? &tmVp : &tmVl, &v_full[st],
-                                         h * HD + sI * 64, row);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idS = ptx::idesc_bf16_f32(BQ, BKD);
-            constexpr uint32_t idO = ptx::idesc_bf16_f32_bmn(BQ, HD);
-            // gx[x]: blocks of tile x issued so far (all items): the S buffer of a block is the
-            // parity of its tile-global index, matching the softmax's own counter
-            uint32_t g = 0, gx[2] = {0, 0}, qit[2] = {0, 0}, bx[2] = {0, 0};
-            auto s_col = [&](int x, uint32_t j) { return tmem_base + x * 128 + ((bx[x] + j) & 1) * 64; };
-            auto issue_s = [&](int x, uint32_t kg, uint32_t j) {  // S_X(j) = Q_X K_kg^T
-                const uint32_t q_addr = ptx::smem_u32(sQ + x * C::kQBytes);
-                const uint32_t k_addr = ptx::smem_u32(sK + (kg % kKStD) * C::kKBytes);
-#pragma unroll
-                for (int kc = 0; kc < HD / 16; ++kc) {
-                    uint64_t ad = ptx::umma_desc_sw128(q_addr + (kc / 4) * (BQ * 128) + (kc % 4) * 32);
-                    uint64_t bd = ptx::umma_desc_sw128(k_addr + (kc / 4) * (BKD * 128) + (kc % 4) * 32);
-                    ptx::mma_bf16(s_col(x, j), ad, bd, idS, kc > 0 ? 1u : 0u);
-                }
-                ptx::mma_commit(&s_full[2 * x + ((bx[x] + j) & 1)]);
-            };
-            for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-                const AttnWork w = p.work[item % p.n_work];
-                const UnitPlan u = plan_unit_db(w, p.seg_lo, partial);
-                const int nbu = max(u.nb[0], u.nb[1]);
-                for (int x = 0; x < 2; ++x) {
-                    if (u.nb[x]) ptx::mbar_wait(&q_full[x], qit[x] & 1);
-                    bx[x] = gx[x];
-                }
-                // prologue: S(0) and S(1) of both tiles
-                for (int j = 0; j < 2 && j < nbu; ++j) {
-                    const uint32_t kg = g + j;
-                    ptx::mbar_wait(&k_full[kg % kKStD], (kg / kKStD) & 1);
-                    ptx::tc_fence_after();
-                    for (int x = 0; x < 2; ++x)
-                        if (j < u.nb[x]) issue_s(x, kg, j);
-                    ptx::mma_commit(&k_empty[kg % kKStD]);
-                }
-                for (int j = 0; j < nbu; ++j) {
-                    const uint32_t kg = g + j;
-                    ptx::mbar_wait(&v_full[kg % kKStD], (kg / kKStD) & 1);
-                    bool waited_k = false;
-                    for (int x = 0; x < 2; ++x) {
-                        if (j >= u.nb[x]) continue;
-                        // O_X += P_X(j) V_j, P read from TMEM (buffer j & 1, packed bf16 pairs)
-                        ptx::mbar_wait(&p_full[2 * x + (gx[x] & 1)], (gx[x] >> 1) & 1);
-                        ptx::tc_fence_after();
-                        const uint32_t v_addr = ptx::smem_u32(sV + (kg % kVStD) * C::kVBytes);
-#pragma unroll
-                        for (int kk = 0; kk < BKD / 16; ++kk) {
-                            uint64_t bd = ptx::umma_desc_sw128_lbo(v_addr + kk * 16 * 128, BKD * 128, 1024);
-                            ptx::mma_bf16_ts(tmem_base + C::kO + x * 128, s_col(x, j) + kk * 8, bd, idO,
-                                             (j > 0 || kk > 0) ? 1u : 0u);
-                        }
-                        ptx::mma_commit(&pv_done[x]);
-                        ++gx[x];
-                        if (j + 2 < u.nb[x]) {
-                            if (!waited_k) {
-                                ptx::mbar_wait(&k_full[(kg + 2) % kKStD], ((kg + 2) / kKStD) & 1);
-                                ptx::tc_fence_after();
-                                waited_k = true;
-                            }
-                            issue_s(x, kg + 2, j + 2);
-                        }
-                        if (j + 1 == u.nb[x]) {
-                            ptx::mma_commit(&o_full[x]);
-                            ptx::mma_commit(&q_empty[x]);
-                        }
-                    }
-                    ptx::mma_commit(&v_empty[kg % kVStD]);
-                    if (j + 2 < nbu) ptx::mma_commit(&k_empty[(kg + 2) % kKStD]);
-                }
-                g += nbu;
-                for (int x = 0; x < 2; ++x)
-                    if (u.nb[x]) ++qit[x];
-            }
-        }
-    } else {
-        // softmax: warps 2-5 tile A, 6-9 tile B; thread = query row = TMEM lane
-        const int x = (warp - 2) >> 2;
-        const int r = (warp & 3) * 32 + lane;
-        const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
-        const uint32_t tSx = tmem_base + lane_base + x * 128;
-        const uint32_t tO = tmem_base + lane_base + C::kO + x * 128;
-        uint32_t gs = 0, uit = 0;  // blocks / items of this tile processed by this CTA
-        for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-            const int h = item / p.n_work;
-            const AttnWork w = p.work[item % p.n_work];
-            const UnitPlan u = plan_unit_db(w, p.seg_lo, partial);
-            const int nb = u.nb[x];
-            if (!nb) continue;
-            const bool valid = r < u.nrows[x];
-            const int row = w.row0 + x * BQ + r;
-            const int seg = valid && !partial ? p.seg_lo[row] : 0x7fffffff;
-            float m = -INFINITY, l = 0.f;
-            for (int b = 0; b < nb; ++b, ++gs) {
-                // buffer b & 1 completes once every two blocks of this tile
-                ptx::mbar_wait(&s_full[2 * x + (gs & 1)], (gs >> 1) & 1);
-                ptx::tc_fence_after();
-                const uint32_t tS = tSx + (gs & 1) * 64;
-                int klo, khi;
-                if (b < u.nA) {
-                    klo = 0;
-                    khi = valid ? min(BKD, w.pfx_len - b * BKD) - 1 : -1;
-                } else {
-                    const int k0 = u.loc_first + (b - u.nA) * BKD;
-                    klo = max(0, seg - k0);
-                    khi = valid ? min(BKD - 1, row - k0) : -1;
-                }
-                const bool full = __all_sync(0xffffffffu, klo == 0 && khi == BKD - 1);
-                const float sc = p.scale_log2;
-                uint32_t sv[BKD];
-                ptx::tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
-                ptx::tmem_ld32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
-                ptx::tmem_ld_wait();
-                if (!full) {
-#pragma unroll
-                    for (int j = 0; j < BKD; ++j)
-                        if (j < klo || j > khi) sv[j] = __float_as_uint(-INFINITY);
-                }
-                float bmax;
-                {
-                    float q0 = -INFINITY, q1 = -INFINITY, q2 = -INFINITY, q3 = -INFINITY;
-#pragma unroll
-                    for (int j = 0; j < BKD; j += 8) {
-                        q0 = fmax3(q0, __uint_as_float(sv[j]), __uint_as_float(sv[j + 1]));
-                        q1 = fmax3(q1, __uint_as_float(sv[j + 2]), __uint_as_float(sv[j + 3]));
-                        q2 = fmax3(q2, __uint_as_float(sv[j + 4]), __uint_as_float(sv[j + 5]));
-                        q3 = fmax3(q3, __uint_as_float(sv[j + 6]), __uint_as_float(sv[j + 7]));
-                    }
-                    bmax = fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)) * sc;
-                }
-                const float mnew = (m == -INFINITY || bmax > m + SGC_LAZY_MAX) ? bmax : m;
-                const float nm = mnew == -INFINITY ? 0.f : -mnew;
-                float rs;
-                {
-                    const uint64_t sc2 = f2pack(sc, sc), nm2 = f2pack(nm, nm);
-                    uint64_t r0 = 0, r1 = 0;
-#pragma unroll
-                    for (int j = 0; j < BKD / 2; ++j) {
-                        float xa, xc;
-                        f2unpack(ffma2(f2pack(__uint_as_float(sv[2 * j]), __uint_as_float(sv[2 * j + 1])), sc2, nm2),
-                                 xa, xc);
-                        float a, cc;
-                        if ((j % SGC_POLY_DEN) < SGC_POLY_NUM) {
-                            ex2_poly2(xa, xc, a, cc);
-                            if (!full) {
-                                if (2 * j < klo || 2 * j > khi) a = 0.f;
-                                if (2 * j + 1 < klo || 2 * j + 1 > khi) cc = 0.f;
-                            }
-                        } else {
-                            a = ex2_approx(xa);
-                            cc = ex2_approx(xc);
-                        }
-                        if (j & 1) r1 = fadd2(r1, f2pack(a, cc));
-                        else r0 = fadd2(r0, f2pack(a, cc));
-                        __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
-                        sv[j] = *reinterpret_cast<uint32_t*>(&bv);
-                    }
-                    float x0, x1;
-                    f2unpack(fadd2(r0, r1), x0, x1);
-                    rs = x0 + x1;
-                }
-                float alpha = 1.f;
-                const bool resc = m != -INFINITY && mnew > m;
-                if (__any_sync(0xffffffffu, resc)) {
-                    // O must be stable: wait for the previous PV of this tile (block b-1)
-                    if (b > 0) {
-                        ptx::mbar_wait(&pv_done[x], (gs - 1) & 1);
-                        ptx::tc_fence_after();
-                    }
-                    alpha = resc ? ex2_approx(m - mnew) : 1.f;
-#pragma unroll 1
-                    for (int c = 0; c < HD / 32; ++c) {
-                        uint32_t o[32];
-                        ptx::tmem_ld32(tO + c * 32, o);
-                        ptx::tmem_ld_wait();
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
-                        ptx::tmem_st32(tO + c * 32, o);
-                    }
-                }
-                m = mnew;
-                // P -> TMEM over the buffer's first 32 columns
-                ptx::tmem_st16(tS, *reinterpret_cast<uint32_t(*)[16]>(&sv[0]));
-                ptx::tmem_st16(tS + 16, *reinterpret_cast<uint32_t(*)[16]>(&sv[16]));
-                l = l * alpha + rs;
-                ptx::tmem_st_wait();
-                ptx::tc_fence_before();
-                ptx::mbar_arrive(&p_full[2 * x + (gs & 1)]);
-            }
-            ptx::mbar_wait(&o_full[x], uit & 1);
-            ptx::tc_fence_after();
-            const float il = l > 0.f ? 1.f / l : 0.f;
-            uint32_t o[HD];
-#pragma unroll
-            for (int c = 0; c < HD / 32; ++c)
-                ptx::tmem_ld32(tO + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
-            ptx::tmem_ld_wait();
-            if (valid && partial) {
-                float4* dst = reinterpret_cast<float4*>(p.part_o + static_cast<size_t>(row) * p.d + h * HD);
-#pragma unroll
-                for (int q = 0; q < HD / 4; ++q)
-                    dst[q] = make_float4(__uint_as_float(o[4 * q]) * il, __uint_as_float(o[4 * q + 1]) * il,
-                                         __uint_as_float(o[4 * q + 2]) * il, __uint_as_float(o[4 * q + 3]) * il);
-                p.part_lse[static_cast<size_t>(row) * p.heads + h] = l > 0.f ? m + __log2f(l) : -INFINITY;
-            } else if (valid) {
-                uint4* dst = reinterpret_cast<uint4*>(p.out + static_cast<size_t>(row) * p.d + h * HD);
-#pragma unroll
-                for (int q = 0; q < HD / 8; ++q) {
-                    uint32_t wv[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        __nv_bfloat162 bv = __floats2bfloat162_rn(__uint_as_float(o[8 * q + 2 * e]) * il,
-                                                                  __uint_as_float(o[8 * q + 2 * e + 1]) * il);
-                        wv[e] = *reinterpret_cast<uint32_t*>(&bv);
-                    }
-                    dst[q] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-                }
-            }
-            ptx::tc_fence_before();
-            ++uit;
-        }
-    }
-    __syncthreads();
-    if (warp == 0) {
-        ptx::tc_fence_after();
-        ptx::tmem_dealloc<512>(tmem_base);
-    }
-}
-
-template <int HD>
-void launch_db(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, int pfx_rows, int loc_rows) {
-    using Cf = DbCfg<HD>;
-    auto kfn = attn_db_kernel<HD>;
-    static bool attr = false;
-    if (!attr) {
-        SGC_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmem));
-        attr = true;
-    }
-    const int d = a.d;
-    CUtensorMap tq = make_map_2d(a.q, q_rows, d, BQ, 64);
-    CUtensorMap tkp = make_map_2d(a.k_pfx, pfx_rows, d, BKD, 64);
-    CUtensorMap tvp = make_map_2d(a.v_pfx, pfx_rows, d, BKD, 64);
-    CUtensorMap tkl = make_map_2d(a.k_loc, loc_rows, d, BKD, 64);
-    CUtensorMap tvl = make_map_2d(a.v_loc, loc_rows, d, BKD, 64);
-    TcParams p{a.work, n_work, heads, a.part_o, a.part_lse, a.seg_lo, a.out, d, a.scale * 1.4426950408889634f,
-                c->sched_counter()};
-    const int items = n_work * heads;
-    const int grid = items < c->num_sms ? items : c->num_sms;
-    Ctx::Timed timer(c, "attention");
-    kfn<<<grid, 320, Cf::kSmem, c->stream>>>(tq, tkp, tvp, tkl, tvl, p);
-    SGC_LAUNCH_CHECK(c);
-}
-
 template <int HD, int SPLIT>
 void launch_tc(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, int pfx_rows, int loc_rows) {
     using Cf = TcCfg<HD>;
     auto kfn = attn_tc_kernel<HD, SPLIT>;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr_devices{0};  // function attributes are per device
+    if (!(attr_devices.load() >> c->device & 1)) {
         SGC_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmem));
-        attr = true;
+        attr_devices |= 1ull << c->device;
     }
     const int d = a.d;
     CUtensorMap tq = make_map_2d(a.q, q_rows, d, BQ, 64);
@@ -1035,7 +654,7 @@ void launch_tc(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, i
     CUtensorMap tkl = make_map_2d(a.k_loc, loc_rows, d, BKV, 64);
     CUtensorMap tvl = make_map_2d(a.v_loc, loc_rows, d, BKV, 64);
     TcParams p{a.work, n_work, heads, a.part_o, a.part_lse, a.seg_lo, a.out, d, a.scale * 1.4426950408889634f,
-                c->sched_counter()};
+                c->sched_counter(), a.bt};
     const int items = n_work * heads;
     const int grid = items < c->num_sms ? items : c->num_sms;
     Ctx::Timed timer(c, "attention");
@@ -1061,13 +680,6 @@ bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, in
     if (p.loc_kv0 != 0) return false;
     if (p.part_o && !p.part_lse) return false;
     const bool split = g_attn_split;
-    if (g_attn_db && !split) {
-        switch (hd) {
-            case 64: launch_db<64>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows); return true;
-            case 128: launch_db<128>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows); return true;
-            default: return false;
-        }
-    }
     switch (hd) {
         case 64:
             if (split) launch_tc<64, 2>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows);
@@ -1082,6 +694,5 @@ bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, in
 }
 
 void attention_set_split(bool on) { g_attn_split = on; }
-void attention_set_db(bool on) { g_attn_db = on; }
 
 }  // namespace sgc

@@ -74,6 +74,11 @@ struct Ctx {
     // generating; the stragglers of all waves then finish in one shared loop
     uint32_t decode_defer_pct = 25;
     cudaStream_t own_stream = nullptr;
+    cudaStream_t side = nullptr;  // overlapped side work (sealed-prefix digests), created on first use
+    cudaStream_t side_stream() {
+        if (!side) SGC_CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        return side;
+    }
     cudaStream_t stream = nullptr;
     uint64_t launches = 0;
     std::map<std::string, Buffer> scratch;

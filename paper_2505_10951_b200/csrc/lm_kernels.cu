@@ -380,6 +380,89 @@ int32_t* Ctx::iota(int n) {
     }
     return p;
 }
+namespace {
+__global__ void kv_pages_pack_kernel(uint4* packed, uint4* pool, size_t layer_vecs, const int32_t* bt, int len,
+                                     int row_vecs, bool pack) {
+    const int j = blockIdx.x, l = blockIdx.y;  // row j of layer l
+    const size_t prow = static_cast<size_t>(bt[j / 128]) * 128 + j % 128;
+    uint4* pp = pool + l * layer_vecs + prow * row_vecs;
+    uint4* qq = packed + (static_cast<size_t>(l) * len + j) * row_vecs;
+    for (int k = threadIdx.x; k < row_vecs; k += blockDim.x) {
+        if (pack) qq[k] = pp[k];
+        else pp[k] = qq[k];
+    }
+}
+
+constexpr uint64_t kFnvBasis = 0xcbf29ce484222325ULL, kFnvPrime = 0x100000001b3ULL;
+// level 1: one warp per (segment, layer, K|V, row): lane l hashes the row's 16-byte vectors
+// l, l + 32, ... (FNV-1a over 64-bit words, coalesced loads), then the 32 lane digests are folded
+// in lane order -- the row digest
+__global__ void kv_row_digest_kernel(uint64_t* rowh, const __nv_bfloat16* kp, const __nv_bfloat16* vp,
+                                     size_t layer_stride, const int32_t* bt, const uint32_t* bt_off,
+                                     const uint32_t* len, int max_len, int layers, int d) {
+    const int s = blockIdx.z, lw = blockIdx.y;  // lw = 2 l + which
+    const int lane = threadIdx.x & 31;
+    const int j = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (j >= static_cast<int>(len[s])) return;  // warp-uniform
+    const int l = lw >> 1;
+    const __nv_bfloat16* base = ((lw & 1) ? vp : kp) + l * layer_stride;
+    const size_t prow = static_cast<size_t>(bt[bt_off[s] + j / 128]) * 128 + j % 128;
+    const uint4* r = reinterpret_cast<const uint4*>(base + prow * d);
+    uint64_t h = kFnvBasis;
+    for (int v = lane; v < d / 8; v += 32) {
+        const uint4 u = __ldg(r + v);
+        h = (h ^ (static_cast<uint64_t>(u.y) << 32 | u.x)) * kFnvPrime;
+        h = (h ^ (static_cast<uint64_t>(u.w) << 32 | u.z)) * kFnvPrime;
+    }
+    uint64_t row = kFnvBasis;
+    for (int t = 0; t < 32; ++t) row = (row ^ __shfl_sync(0xffffffffu, h, t)) * kFnvPrime;
+    if (lane == 0) rowh[(static_cast<size_t>(s) * layers * 2 + lw) * max_len + j] = row;
+}
+// level 2: fold row digests per (segment, layer, K|V) in row order; level 3: fold those in order
+__global__ void kv_fold_kernel(uint64_t* out, const uint64_t* rowh, const uint32_t* len, int max_len, int layers) {
+    const int s = blockIdx.x;
+    __shared__ uint64_t part[256];
+    const int n = static_cast<int>(len[s]);
+    for (int lw = threadIdx.x; lw < 2 * layers; lw += blockDim.x) {
+        const uint64_t* r = rowh + (static_cast<size_t>(s) * layers * 2 + lw) * max_len;
+        uint64_t h = kFnvBasis;
+        for (int j = 0; j < n; ++j) h = (h ^ r[j]) * kFnvPrime;
+        part[lw] = h;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t h = kFnvBasis;
+        for (int lw = 0; lw < 2 * layers; ++lw) h = (h ^ part[lw]) * kFnvPrime;
+        out[s] = h;
+    }
+}
+}  // namespace
+
+void kv_pages_pack(Ctx* c, __nv_bfloat16* packed, __nv_bfloat16* pool, size_t layer_stride, const int32_t* bt,
+                   int len, int layers, int d, bool pack) {
+    if (len <= 0 || layers <= 0) return;
+    if (d % 8) fail(SGC_DOMAIN, "kv_pages_pack: d must be a multiple of 8");
+    const dim3 grid(len, layers);
+    kv_pages_pack_kernel<<<grid, 128, 0, c->stream>>>(reinterpret_cast<uint4*>(packed), reinterpret_cast<uint4*>(pool),
+                                                      layer_stride / 8, bt, len, d / 8, pack);
+    SGC_LAUNCH_CHECK(c);
+}
+
+void kv_digest(Ctx* c, cudaStream_t stream, uint64_t* out, uint64_t* rowh, const __nv_bfloat16* k_pool,
+               const __nv_bfloat16* v_pool, size_t layer_stride, const int32_t* bt, const uint32_t* bt_off,
+               const uint32_t* len, int n, int max_len, int layers, int d) {
+    if (n <= 0) return;
+    if (2 * layers > 256) fail(SGC_DOMAIN, "kv_digest: at most 128 layers");
+    if (max_len > 0) {
+        const dim3 grid(ceil_div(max_len, 8), 2 * layers, n);
+        kv_row_digest_kernel<<<grid, 256, 0, stream>>>(rowh, k_pool, v_pool, layer_stride, bt, bt_off, len,
+                                                       max_len, layers, d);
+        SGC_LAUNCH_CHECK(c);
+    }
+    kv_fold_kernel<<<n, 64, 0, stream>>>(out, rowh, len, max_len, layers);
+    SGC_LAUNCH_CHECK(c);
+}
+
 void head_transpose(Ctx* c, float* out_t, const float* head, int d) {
     transpose_head<<<grid_for((uint64_t)SGC_VOCAB * d, 256, c->num_sms), 256, 0, c->stream>>>(out_t, head, d);
     SGC_LAUNCH_CHECK(c);

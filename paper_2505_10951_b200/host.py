@@ -220,6 +220,13 @@ class KVBatch:
     def resident_kv_bytes(self) -> int:
         return self.lib.sgc_kv_resident_bytes(self.h)
 
+    def pages(self, i: int = 0) -> np.ndarray:
+        """Block table of segment i: page ids of the model's paged KV pool (128 tokens per page)."""
+        n = self.lib.sgc_kv_pages(self.h, i, None)
+        out = np.zeros(max(n, 1), np.int32)
+        self.lib.sgc_kv_pages(self.h, i, _p(out, C.c_int32))
+        return out[:n]
+
     def read(self, i: int, layer: int, is_v: bool) -> np.ndarray:
         out = np.zeros(self.token_count(i) * self.lm.cfg.model_dim, np.float32)
         check(self.lib.sgc_kv_read(self.h, i, layer, int(is_v), _p(out, C.c_float)))
@@ -561,6 +568,9 @@ class SubgCacheResult:
     prefilled: np.ndarray | None = None   # [c] 1 if this rank ran the representative's prefill
     prefix_bytes_sent: int = 0            # split clusters' sealed K/V moved point to point
     prefix_bytes_received: int = 0
+    prefix_digest: np.ndarray | None = None  # [c] sealed-prefix digest (verified after serving)
+    kv_pages_peak: int = 0                   # paged KV: peak pages in use, bytes per page
+    kv_page_bytes: int = 0
 
 
 class PreparedBatch:
@@ -617,7 +627,8 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
                   embeddings: np.ndarray | None = None, cluster_owner=None, rank: int = 0,
                   world_size: int = 1, want_logits: bool = True,
                   device_inputs: bool = False, waves: int = 1, max_new: int = 0,
-                  split_clusters: bool = False, transfer_prefix: int = 1) -> SubgCacheResult:
+                  split_clusters: bool = False, transfer_prefix: int = 1,
+                  verify_prefix: bool = True) -> SubgCacheResult:
     """pipeline.cpp:212-293 (SubgCache branch) + cache_engine.cpp:217-233 (run_batch), to the
     first token of every query."""
     w = pb.w
@@ -654,6 +665,7 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     b.max_new_tokens = max_new
     b.split_clusters = int(split_clusters)
     b.transfer_prefix = int(transfer_prefix)
+    b.verify_prefix = int(verify_prefix)
     emb = np.zeros((m, d), np.float32)
     labels = np.zeros(m, np.uint32)
     nm = max(m - k, 1)
@@ -685,6 +697,8 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     prefilled = np.zeros(k, np.uint8)
     o.query_rank = _p(qrank, C.c_uint32)
     o.prefilled = _p(prefilled, C.c_uint8)
+    digest = np.zeros(k, np.uint64)
+    o.prefix_digest = _p(digest, C.c_uint64)
     toks = cnt = rt = None
     if max_new > 1:
         toks = np.full((m, max_new), -1, np.int32)
@@ -700,6 +714,8 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     res.seal_ms, res.pftt_ms = seal, pftt
     res.query_rank, res.prefilled = qrank, prefilled
     res.prefix_bytes_sent, res.prefix_bytes_received = o.prefix_bytes_sent, o.prefix_bytes_received
+    res.prefix_digest = digest
+    res.kv_pages_peak, res.kv_page_bytes = o.kv_pages_peak, o.kv_page_bytes
     if max_new > 1:
         res.tokens = [toks[q, :cnt[q]].copy() for q in range(m)]
         res.rt_ms = rt
