@@ -46,6 +46,7 @@ typedef struct sgc_ctx sgc_ctx;     /* one CUDA device + stream + scratch arena 
 typedef struct sgc_model sgc_model; /* ToyLm weights, bf16 in HBM (lm_core.hpp:114-171) */
 typedef struct sgc_graph sgc_graph; /* TextualGraph pre-rendered rows + text features */
 typedef struct sgc_kv sgc_kv;       /* sealed prefix segments (KVCache::seal, lm_core.cpp:60-80) */
+typedef struct sgc_fork sgc_fork;   /* KVCache::fork of one sealed segment + private suffix */
 
 /* lm_core.hpp:16-27 ToyLmConfig */
 typedef struct {
@@ -222,6 +223,24 @@ uint64_t sgc_kv_resident_bytes(const sgc_kv* kv);
 uint32_t sgc_kv_pages(const sgc_kv* kv, uint32_t i, int32_t* pages);
 /* Copy segment i, layer l, K (is_v=0) or V as fp32 [tokens * model_dim] (test hook). */
 int sgc_kv_read(const sgc_kv* kv, uint32_t i, uint32_t layer, int is_v, float* out);
+
+/* ---- fork handles: the KVCache object model (lm_core.hpp:35-92, lm_core.cpp:82-99) --------
+ * A fork shares sealed segment `seg` of `kv` (the segment stays alive while forks use it, like the
+ * reference's shared_ptr prefix; sgc_kv_release only drops the handle's reference) and owns a
+ * private suffix in pages of the same pool. sgc_fork_extend = ToyLm::extend (lm_core.cpp:329-339)
+ * on n forks in one batched pass: fork j appends tokens[j]; logits [n * 260] (optional) are the
+ * last-position logits (also kept per fork). CapacityError past max_seq_len. truncate: SGC_LOGIC
+ * into the sealed prefix (std::logic_error in the reference), SGC_DOMAIN beyond the token count. */
+int sgc_kv_fork(sgc_kv* kv, uint32_t seg, sgc_fork** out);
+int sgc_fork_fork(const sgc_fork* f, sgc_fork** out); /* deep copy of the private suffix */
+int sgc_fork_extend(sgc_ctx* ctx, sgc_model* model, sgc_fork* const* forks, uint32_t n,
+                    const sgc_token_lists* tokens, float* logits);
+uint64_t sgc_fork_tokens(const sgc_fork* f);        /* KVCache::token_count */
+uint64_t sgc_fork_prefix_tokens(const sgc_fork* f); /* KVCache::prefix_token_count */
+int sgc_fork_last_logits(const sgc_fork* f, float* out);
+int sgc_fork_truncate(sgc_fork* f, uint64_t tokens);  /* KVCache::truncate_to */
+int sgc_fork_release_suffix(sgc_fork* f);             /* KVCache::release_suffix */
+int sgc_fork_destroy(sgc_fork* f);
 
 /* ---- (5) per-query reuse: KVCache::fork + ToyLm::extend + first greedy token ----------
  * (lm_core.cpp:82-90, :329-339, :352-390; cache_engine.cpp:183-189)

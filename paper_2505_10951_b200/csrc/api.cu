@@ -205,6 +205,7 @@ struct sgc_kv {
     uint64_t rows = 0;               // tokens of all segments
     int32_t* d_tokens = nullptr;     // context token ids (prefix, incl. soft slot), segments back to back
     uint64_t* d_tok_off = nullptr;
+    int refs = 1;                    // the handle + live forks (the prefix outlives its forks' users)
     size_t layer_elems() const { return static_cast<size_t>(model->pool.pages) * sgc::kPageTokens * model->d; }
     bf16* k_layer(int l) const { return model->pool.k + l * layer_elems(); }
     bf16* v_layer(int l) const { return model->pool.v + l * layer_elems(); }
@@ -2110,17 +2111,16 @@ int sgc_prefill(sgc_ctx* ctx, sgc_model* model, const sgc_token_lists* seqs, con
     });
 }
 
+namespace {
+void kv_drop_ref(sgc_kv* kv);
+}
+
 int sgc_kv_release(sgc_kv* kv) {
     return guarded([&] {
         if (!kv) return;
-        Ctx* c = current(kv->model->c);
-        // pages back to the model's pool and frees in stream order: no drain, so the host keeps
-        // preparing the next wave while the GPU still reads these pages
-        pool_release(kv->model, kv->pages);
-        dfree(c, kv->d_bt);
-        dfree(c, kv->d_tokens);
-        dfree(c, kv->d_tok_off);
-        delete kv;
+        // pages back to the model's pool and frees in stream order once no fork shares them: no
+        // drain, so the host keeps preparing the next wave while the GPU still reads these pages
+        kv_drop_ref(kv);
     });
 }
 
@@ -2193,6 +2193,232 @@ int sgc_kv_read(const sgc_kv* kv, uint32_t i, uint32_t layer, int is_v, float* o
         SGC_CUDA_CHECK(cudaMemcpy(out, f.data(), n * sizeof(float), cudaMemcpyDefault));
     });
 }
+
+}  // extern "C"
+
+// ---- fork handles: KVCache::fork / extend / truncate_to / release_suffix (lm_core.hpp:35-92) ----
+// A fork shares one sealed segment of an sgc_kv (refcounted, as the reference's shared_ptr to the
+// prefix Segment) and owns a private suffix stored in pages of the same pool. Extending a batch of
+// forks runs one forward over their new tokens: every row attends to its segment's prefix pages and,
+// causally, to its fork's suffix pages (earlier extends included) -- the own-key window starts at
+// a virtual row `suffix tokens` before the fork's first new row, so the kernels' causal masks are
+// unchanged and only the block table says where the keys live.
+struct sgc_fork {
+    sgc_kv* kv = nullptr;
+    uint32_t seg = 0;
+    std::vector<int32_t> pages;  // suffix pages (block table)
+    uint64_t suffix = 0;         // suffix tokens
+    std::vector<float> last_logits;
+    uint64_t prefix_tokens() const { return kv->len[seg]; }
+};
+
+namespace {
+void kv_drop_ref(sgc_kv* kv) {
+    if (--kv->refs == 0) {
+        Ctx* c = current(kv->model->c);
+        pool_release(kv->model, kv->pages);
+        dfree(c, kv->d_bt);
+        dfree(c, kv->d_tokens);
+        dfree(c, kv->d_tok_off);
+        delete kv;
+    }
+}
+
+void fork_reserve(Ctx* c, sgc_fork* f, uint64_t tokens) {
+    const uint32_t need = static_cast<uint32_t>((tokens + sgc::kPageTokens - 1) / sgc::kPageTokens);
+    if (need > f->pages.size()) {
+        std::vector<int32_t> more = pool_alloc(c, f->kv->model, need - static_cast<uint32_t>(f->pages.size()));
+        f->pages.insert(f->pages.end(), more.begin(), more.end());
+    }
+}
+
+void fork_trim(sgc_fork* f) {
+    const size_t keep = (f->suffix + sgc::kPageTokens - 1) / sgc::kPageTokens;
+    if (f->pages.size() > keep) {
+        pool_release(f->kv->model, std::vector<int32_t>(f->pages.begin() + keep, f->pages.end()));
+        f->pages.resize(keep);
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int sgc_kv_fork(sgc_kv* kv, uint32_t seg, sgc_fork** out) {
+    return guarded([&] {
+        if (!kv || seg >= kv->n) fail(SGC_DOMAIN, "fork: unknown sealed segment");
+        auto* f = new sgc_fork();
+        f->kv = kv;
+        f->seg = seg;
+        ++kv->refs;
+        *out = f;
+    });
+}
+
+int sgc_fork_fork(const sgc_fork* src, sgc_fork** out) {
+    return guarded([&] {
+        Ctx* c = current(src->kv->model->c);
+        sgc_model* m = src->kv->model;
+        auto f = std::make_unique<sgc_fork>();
+        f->kv = src->kv;
+        f->seg = src->seg;
+        f->last_logits = src->last_logits;
+        f->suffix = src->suffix;
+        fork_reserve(c, f.get(), src->suffix);  // deep copy of the private suffix (lm_core.cpp:82-90)
+        if (src->suffix) {
+            const int n = static_cast<int>(src->suffix);
+            int32_t* bt = c->buf<int32_t>("fork_copy_bt", 2 * f->pages.size());
+            sgc::copy_in(c, bt, src->pages.data(), src->pages.size());
+            sgc::copy_in(c, bt + f->pages.size(), f->pages.data(), f->pages.size());
+            bf16* stage = c->buf<bf16>("fork_copy_stage", static_cast<size_t>(m->L) * n * m->d);
+            const size_t ls = static_cast<size_t>(m->pool.pages) * sgc::kPageTokens * m->d;
+            for (bf16* pool : {m->pool.k, m->pool.v}) {
+                sgc::kv_pages_pack(c, stage, pool, ls, bt, n, m->L, m->d, true);
+                sgc::kv_pages_pack(c, stage, pool, ls, bt + f->pages.size(), n, m->L, m->d, false);
+            }
+        }
+        ++f->kv->refs;
+        *out = f.release();
+    });
+}
+
+uint64_t sgc_fork_tokens(const sgc_fork* f) { return f ? f->prefix_tokens() + f->suffix : 0; }
+uint64_t sgc_fork_prefix_tokens(const sgc_fork* f) { return f ? f->prefix_tokens() : 0; }
+
+int sgc_fork_last_logits(const sgc_fork* f, float* out) {
+    return guarded([&] {
+        const std::vector<float>& lg = f->last_logits;
+        if (lg.empty()) fail(SGC_DOMAIN, "fork: no logits yet (extend first)");
+        std::memcpy(out, lg.data(), lg.size() * sizeof(float));
+    });
+}
+
+int sgc_fork_truncate(sgc_fork* f, uint64_t n) {
+    return guarded([&] {
+        const uint64_t p = f->prefix_tokens();
+        if (n < p) fail(SGC_LOGIC, "KVCache: cannot truncate into the sealed prefix segment");
+        if (n - p > f->suffix) fail(SGC_DOMAIN, "KVCache: truncate_to beyond current token count");
+        f->suffix = n - p;
+        fork_trim(f);
+    });
+}
+
+int sgc_fork_release_suffix(sgc_fork* f) { return sgc_fork_truncate(f, f->prefix_tokens()); }
+
+int sgc_fork_destroy(sgc_fork* f) {
+    return guarded([&] {
+        if (!f) return;
+        current(f->kv->model->c);
+        pool_release(f->kv->model, f->pages);
+        kv_drop_ref(f->kv);
+        delete f;
+    });
+}
+
+// ToyLm::extend (lm_core.cpp:329-339) on n forks at once: fork j appends tokens[j] to its suffix
+int sgc_fork_extend(sgc_ctx* ctx, sgc_model* model, sgc_fork* const* forks, uint32_t n,
+                    const sgc_token_lists* tokens, float* logits) {
+    return guarded([&] {
+        Ctx* c = current(&ctx->c);
+        if (tokens->count != n) fail(SGC_DOMAIN, "fork_extend: one token list per fork");
+        if (n == 0) return;
+        std::vector<uint64_t> off = to_host(c, tokens->off, n + 1);
+        std::vector<int32_t> toks = to_host(c, tokens->tokens, off[n]);
+        const int d = model->d;
+        // one block table for the call: every involved sealed segment's pages, then every fork's suffix pages
+        std::vector<int32_t> bt;
+        std::map<std::pair<const sgc_kv*, uint32_t>, int> pfx_at;
+        std::vector<int> suf_at(n);
+        for (uint32_t j = 0; j < n; ++j) {
+            sgc_fork* f = forks[j];
+            if (f->kv->model != model) fail(SGC_DOMAIN, "fork does not belong to this model");
+            const uint64_t sn = off[j + 1] - off[j];
+            if (sn == 0) fail(SGC_DOMAIN, "extend: empty token list");
+            if (f->prefix_tokens() + f->suffix + sn > model->cfg.max_seq_len)
+                fail(SGC_CAPACITY, "sequence length " + std::to_string(f->prefix_tokens() + f->suffix + sn) +
+                                       " exceeds max " + std::to_string(model->cfg.max_seq_len));
+            for (uint32_t i = 0; i < j; ++i)
+                if (forks[i] == f) fail(SGC_DOMAIN, "fork_extend: a fork appears twice");
+        }
+        for (uint32_t j = 0; j < n; ++j) fork_reserve(c, forks[j], forks[j]->suffix + off[j + 1] - off[j]);
+        for (uint32_t j = 0; j < n; ++j) {
+            sgc_fork* f = forks[j];
+            auto key = std::make_pair(static_cast<const sgc_kv*>(f->kv), f->seg);
+            if (!pfx_at.count(key)) {
+                pfx_at[key] = static_cast<int>(bt.size());
+                bt.insert(bt.end(), f->kv->pages.begin() + f->kv->bt_off[f->seg],
+                          f->kv->pages.begin() + f->kv->bt_off[f->seg] + f->kv->seg_pages(f->seg));
+            }
+        }
+        for (uint32_t j = 0; j < n; ++j) {
+            suf_at[j] = static_cast<int>(bt.size());
+            bt.insert(bt.end(), forks[j]->pages.begin(), forks[j]->pages.end());
+        }
+        const int M = static_cast<int>(off[n]);
+        std::vector<int32_t> pos, seg_lo, kvrow, lrows;
+        std::vector<int> gs, gr, pk, pl, lb;
+        for (uint32_t j = 0; j < n; ++j) {
+            sgc_fork* f = forks[j];
+            const int start = static_cast<int>(off[j]);
+            const int sn = static_cast<int>(off[j + 1] - off[j]);
+            gs.push_back(start);
+            gr.push_back(sn);
+            pk.push_back(pfx_at[{f->kv, f->seg}]);
+            pl.push_back(static_cast<int>(f->prefix_tokens()));
+            lb.push_back(suf_at[j]);
+            for (int i = 0; i < sn; ++i) {
+                const uint64_t t = f->suffix + i;  // suffix-relative token index
+                pos.push_back(static_cast<int32_t>(f->prefix_tokens() + t));
+                seg_lo.push_back(start - static_cast<int>(f->suffix));  // virtual: earlier suffix keys
+                kvrow.push_back(f->pages[t / sgc::kPageTokens] * sgc::kPageTokens + static_cast<int32_t>(t % sgc::kPageTokens));
+            }
+            lrows.push_back(start + sn - 1);
+        }
+        std::vector<sgc::AttnWork> work = make_work(gs, gr, pk, pl, lb, attn_tile(model->hd));
+        int32_t* d_arr = c->buf<int32_t>("fk_rows", static_cast<size_t>(M) * 4 + n + bt.size());
+        std::vector<int32_t> packed;
+        for (auto* v : {&toks, &pos, &seg_lo, &kvrow, &lrows, &bt}) packed.insert(packed.end(), v->begin(), v->end());
+        sgc::copy_in(c, d_arr, packed.data(), packed.size());
+        sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("fk_work", work.size());
+        sgc::copy_in(c, d_work, work.data(), work.size());
+        float* d_logits = c->buf<float>("fk_logits", static_cast<size_t>(n) * SGC_VOCAB);
+        const KvPool* pool = &model->pool;
+        const size_t pls = static_cast<size_t>(pool->pages) * sgc::kPageTokens * d;
+        FwdBatch b;
+        b.M = M;
+        b.d_tokens = d_arr;
+        b.d_pos = d_arr + M;
+        b.d_seg_lo = d_arr + 2 * static_cast<size_t>(M);
+        b.d_kv_row = d_arr + 3 * static_cast<size_t>(M);
+        b.d_logit_rows = d_arr + 4 * static_cast<size_t>(M);
+        b.d_bt = d_arr + 4 * static_cast<size_t>(M) + n;
+        b.d_work = d_work;
+        b.n_work = static_cast<int>(work.size());
+        b.k_loc = [pool, pls](int l) { return pool->k + l * pls; };
+        b.v_loc = [pool, pls](int l) { return pool->v + l * pls; };
+        b.loc_rows = static_cast<int>(pool->pages * sgc::kPageTokens);
+        b.k_pfx = [pool, pls](int l) { return static_cast<const bf16*>(pool->k + l * pls); };
+        b.v_pfx = [pool, pls](int l) { return static_cast<const bf16*>(pool->v + l * pls); };
+        b.pfx_rows = b.loc_rows;
+        b.n_logits = static_cast<int>(n);
+        b.d_logits = d_logits;
+        forward_rows(c, model, b);
+        std::vector<float> lg(static_cast<size_t>(n) * SGC_VOCAB);
+        sgc::copy_out(c, lg.data(), d_logits, lg.size());
+        c->sync();
+        check_forward_flags(c);
+        for (uint32_t j = 0; j < n; ++j) {
+            forks[j]->suffix += off[j + 1] - off[j];
+            forks[j]->last_logits.assign(lg.begin() + static_cast<size_t>(j) * SGC_VOCAB,
+                                         lg.begin() + static_cast<size_t>(j + 1) * SGC_VOCAB);
+        }
+        if (logits) sgc::copy_in(c, logits, lg.data(), lg.size());
+        c->sync();
+    });
+}
+
+}  // extern "C"
+
+extern "C" {
 
 int sgc_extend(sgc_ctx* ctx, sgc_model* model, sgc_kv* kv, const uint32_t* member_seg,
                const sgc_token_lists* questions, const sgc_token_lists* answers, float pointer_bonus,

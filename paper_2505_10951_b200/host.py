@@ -76,8 +76,8 @@ class Context:
     def close(self):
         if getattr(self, "h", None):
             kids = list(getattr(self, "_children", ()))
-            # KV batches reference their model: release them first
-            for k in sorted(kids, key=lambda o: 0 if isinstance(o, KVBatch) else 1):
+            # forks reference their KV batch, KV batches their model: release them first
+            for k in sorted(kids, key=lambda o: 0 if isinstance(o, KVFork) else 1 if isinstance(o, KVBatch) else 2):
                 k.close()
             self.lib.sgc_ctx_destroy(self.h)
             self.h = None
@@ -233,6 +233,46 @@ class KVBatch:
         return out
 
 
+class KVFork:
+    """KVCache after fork() (lm_core.cpp:82-90): shares one sealed segment, private suffix in pages."""
+
+    def __init__(self, lm: "ToyLm", h):
+        self.lm, self.h, self.lib = lm, h, lm.lib
+        lm.ctx._adopt(self)
+
+    def close(self):
+        if getattr(self, "h", None):
+            if self.lm.ctx.alive:
+                self.lib.sgc_fork_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def token_count(self) -> int:
+        return self.lib.sgc_fork_tokens(self.h)
+
+    def prefix_token_count(self) -> int:
+        return self.lib.sgc_fork_prefix_tokens(self.h)
+
+    @property
+    def last_logits(self) -> np.ndarray:
+        out = np.zeros(VOCAB, np.float32)
+        check(self.lib.sgc_fork_last_logits(self.h, _p(out, C.c_float)))
+        return out
+
+    def fork(self) -> "KVFork":
+        h = C.c_void_p()
+        check(self.lib.sgc_fork_fork(self.h, C.byref(h)))
+        return KVFork(self.lm, h)
+
+    def truncate_to(self, n: int):
+        check(self.lib.sgc_fork_truncate(self.h, n))
+
+    def release_suffix(self):
+        check(self.lib.sgc_fork_release_suffix(self.h))
+
+
 class ToyLm:
     """ToyLm (lm_core.hpp:114-171) with device-generated, bit-exact seeded weights (bf16)."""
 
@@ -326,6 +366,21 @@ class ToyLm:
                                            _p(logits, C.c_float), _p(first, C.c_int32),
                                            _p(toks, C.c_int32), _p(cnt, C.c_uint32)))
         return logits, first, [toks[j, :cnt[j]].copy() for j in range(n)]
+
+    def fork(self, kv: KVBatch, seg: int = 0) -> KVFork:
+        """KVCache::fork of sealed segment `seg`."""
+        h = C.c_void_p()
+        check(self.lib.sgc_kv_fork(kv.h, seg, C.byref(h)))
+        return KVFork(self, h)
+
+    def extend_forks(self, forks, token_lists) -> np.ndarray:
+        """ToyLm::extend on every fork at once (fork j appends token_lists[j]); last logits [n x 260]."""
+        tl, keep = pack_tokens(token_lists)
+        n = len(forks)
+        arr = (C.c_void_p * max(n, 1))(*[f.h for f in forks])
+        logits = np.zeros((n, VOCAB), np.float32)
+        check(self.lib.sgc_fork_extend(self.ctx.h, self.h, arr, n, C.byref(tl), _p(logits, C.c_float)))
+        return logits
 
     def extend(self, kv: KVBatch, tokens, seg: int = 0):
         """ToyLm::extend on a fork of sealed segment `seg`; returns the last logits."""
