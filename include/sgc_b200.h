@@ -348,6 +348,11 @@ typedef struct {
      * sgc_kv_digest), peak pages in use during the batch, bytes per page (K + V, all layers) */
     uint64_t* prefix_digest;
     uint64_t kv_pages_peak, kv_page_bytes;
+    /* [m] optional, HOST: the reference's TTFT semantics (QueryOutcome::ttft_ms, cache_engine.cpp:
+     * 149, 169, 97-100): cluster dequeue -> first token. A cluster is dequeued when its wave starts
+     * (its representative's prefill), so this excludes encode / cluster / represent and earlier
+     * waves; -1 if not served here. ttft_ms above is the paper's submission -> first token. */
+    float* ttft_dequeue_ms;
 } sgc_batch_out;
 
 int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_batch* batch,
@@ -382,13 +387,20 @@ int sgc_attention_bf16(sgc_ctx* ctx, const void* q, const void* k_pfx, const voi
                        uint32_t pfx_rows, const void* k_loc, const void* v_loc, const int32_t* seg_lo,
                        const int32_t* work, uint32_t n_work, uint32_t rows, uint32_t d, uint32_t heads,
                        void* out);
+/* Measured FP64 FMA throughput of the context's device (TFLOP/s): the GNN layer map's roofline
+ * denominator (bench.py). */
+int sgc_probe_fp64_tflops(sgc_ctx* ctx, double* tflops);
+/* Work of the context's last GNN encode: unique node states computed over all layers (identical
+ * in-neighbourhood signatures are computed once) and the reference's node instances x layers. */
+int sgc_gnn_stats(const sgc_ctx* ctx, uint64_t* state_rows, uint64_t* node_instances);
 /* Enable/disable per-kernel CUDA-event timing; sgc_get_timing reads the accumulated totals. */
 int sgc_set_timing(sgc_ctx* ctx, int enable);
 /* Tuning knobs: "gemm_pairs" (1 = CTA-pair tcgen05 GEMM for 256-wide tiles, default; 0 = 1-CTA);
  * "decode_defer_pct" (generation: a wave decodes on its own until fewer than this percentage of
  * its queries still generate, the stragglers of every wave then finish in one shared loop;
  * default 25, 0 = each wave to completion, >= 100 = all decoding after the last wave);
- * "attn_split" (1 = two softmax warpgroups per query tile; default 0).
+ * "attn_split" (1 = two softmax warpgroups per query tile; default 0);
+ * "gnn_tile" (GNN layer-map FP64 GEMM tile: 0 = 64x64, 1 = 64x128 (default), 2 = 128x128).
  * Unknown names return SGC_DOMAIN. */
 int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value);
 int sgc_get_timing(sgc_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches);

@@ -489,8 +489,13 @@ json cmd_run(const json& spec) {
     if (spec.contains("lm")) rc.lm = lm_cfg(spec["lm"]);
     const std::string soft = spec.value("soft_prefix", std::string("auto"));
     rc.soft_prefix = soft == "on" ? SoftPrefixMode::On : (soft == "off" ? SoftPrefixMode::Off : SoftPrefixMode::Auto);
+    rc.parallel_queries = spec.value("parallel_queries", false);       // --parallel-queries
+    if (spec.value("mode", std::string("subgcache")) == "baseline") rc.mode = RunMode::Baseline;
+    auto t0 = Clock::now();
     BatchReport r = run(rc);
-    return json::parse(r.to_json());
+    json out = json::parse(r.to_json());
+    out["wall_ms"] = ms_since(t0);  // the whole run(): load, retrieve, encode, cluster, serve
+    return out;
 }
 
 json cmd_bench(const json& spec) {
@@ -555,6 +560,60 @@ json cmd_bench(const json& spec) {
         t0 = Clock::now();
         gnn.encode(enc, full_subgraph(g));
         out["gnn_encode_ms"] = ms_since(t0);
+    }
+    // attention cost per context key, measured at a small width with the real head_dim and the
+    // real prefix length (the full-width per-token cost above covers the matvecs): extend of n
+    // tokens on a P-token prefix minus the same on an 8-token prefix, per key and token
+    if (spec.contains("attn_calib")) {
+        const json& a = spec["attn_calib"];
+        ToyLmConfig sc;
+        sc.layers = 1;
+        sc.heads = a.value("heads", 2u);
+        sc.model_dim = a.value("d", 256u);
+        sc.ffn_hidden = a.value("ffn", 4 * sc.model_dim);
+        const uint32_t P = a.at("P"), n = a.value("n", 8u);
+        sc.max_seq_len = P + n + 8;
+        ToyLm small(sc);
+        KVCache longp = small.prefill(rand_toks(P));
+        longp.seal();
+        KVCache shortp = small.prefill(rand_toks(8));
+        shortp.seal();
+        std::vector<TokenId> q = rand_toks(n);
+        double best_long = 1e30, best_short = 1e30;
+        for (int rep = 0; rep < 3; ++rep) {
+            KVCache f1 = longp.fork();
+            t0 = Clock::now();
+            small.extend(f1, q);
+            best_long = std::min(best_long, ms_since(t0));
+            KVCache f2 = shortp.fork();
+            t0 = Clock::now();
+            small.extend(f2, q);
+            best_short = std::min(best_short, ms_since(t0));
+        }
+        out["attn_ms_per_key_token"] = std::max(0.0, best_long - best_short) / (static_cast<double>(n) * (P - 8));
+        out["attn_calib_d"] = sc.model_dim;
+    }
+    // GNN encode of real subgraphs of the workload's graph (CSV) at the model width
+    if (spec.contains("gnn_subgraphs")) {
+        TextualGraph g = graph_of(spec);
+        TextEncoderConfig tc;
+        tc.dim = lc.model_dim;
+        TextEncoder enc(tc);
+        GnnEncoderConfig gc;
+        gc.dim = lc.model_dim;
+        gc.seed = spec.value("gnn_seed", gc.seed);
+        GnnEncoder gnn(gc);
+        double ms = 0;
+        uint64_t nodes = 0;
+        for (const json& sj : spec["gnn_subgraphs"]) {
+            Subgraph sub = subgraph_of(g, sj);
+            nodes += sub.node_ids.size();
+            t0 = Clock::now();
+            gnn.encode(enc, sub);
+            ms += ms_since(t0);
+        }
+        out["gnn_sample_ms"] = ms;
+        out["gnn_sample_nodes"] = nodes;
     }
     if (spec.contains("agglomerate_m")) {
         uint32_t m = spec["agglomerate_m"], d = spec.value("agglomerate_d", lc.model_dim);

@@ -102,7 +102,7 @@ class BatchOut(C.Structure):
                 ("query_rank", C.POINTER(C.c_uint32)), ("prefilled", C.POINTER(C.c_uint8)),
                 ("prefix_bytes_sent", C.c_uint64), ("prefix_bytes_received", C.c_uint64),
                 ("prefix_digest", C.POINTER(C.c_uint64)), ("kv_pages_peak", C.c_uint64),
-                ("kv_page_bytes", C.c_uint64)]
+                ("kv_page_bytes", C.c_uint64), ("ttft_dequeue_ms", C.POINTER(C.c_float))]
 
 
 # sgc_host_transport callbacks (include/sgc_b200.h)
@@ -154,7 +154,7 @@ EXPORTS = [
     "sgc_kv_release", "sgc_kv_count", "sgc_kv_tokens", "sgc_kv_digest", "sgc_kv_resident_bytes",
     "sgc_kv_read", "sgc_extend", "sgc_run_subgcache", "sgc_gemm_bf16", "sgc_set_timing",
     "sgc_get_timing", "sgc_lpt_assign", "sgc_set_option", "sgc_attention_bf16", "sgc_extend_generate", "sgc_retrieve", "sgc_balance_members",
-    "sgc_kv_pages", "sgc_kv_fork", "sgc_fork_fork", "sgc_fork_extend", "sgc_fork_tokens",
+    "sgc_kv_pages", "sgc_probe_fp64_tflops", "sgc_gnn_stats", "sgc_kv_fork", "sgc_fork_fork", "sgc_fork_extend", "sgc_fork_tokens",
     "sgc_fork_prefix_tokens", "sgc_fork_last_logits", "sgc_fork_truncate", "sgc_fork_release_suffix",
     "sgc_fork_destroy", "sgc_comm_unique_id", "sgc_comm_init_nccl", "sgc_comm_init_host", "sgc_comm_destroy", "sgc_comm_info",
 ]
@@ -212,6 +212,8 @@ def load() -> C.CDLL:
     L.sgc_kv_pages.argtypes = [vp, C.c_uint32, P(C.c_int32)]
     L.sgc_kv_pages.restype = C.c_uint32
     L.sgc_kv_fork.argtypes = [vp, C.c_uint32, P(vp)]
+    L.sgc_probe_fp64_tflops.argtypes = [vp, P(C.c_double)]
+    L.sgc_gnn_stats.argtypes = [vp, P(C.c_uint64), P(C.c_uint64)]
     L.sgc_fork_fork.argtypes = [vp, P(vp)]
     L.sgc_fork_extend.argtypes = [vp, vp, P(vp), C.c_uint32, P(TokenLists), P(C.c_float)]
     L.sgc_fork_tokens.argtypes = [vp]

@@ -1285,6 +1285,11 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
     float* uniq_out = c->buf<float>("gnn_uniq_out", static_cast<size_t>(nu) * d);
     p.out = uniq_out;
     sgc::gnn_encode_layers(c, p);
+    // work accounting (bench.py's embedding roofline): unique node states computed per layer vs
+    // the reference's node instances (every subgraph's nodes, every layer)
+    c->gnn_state_rows = 0;
+    for (uint32_t l = 0; l < cfg.layers; ++l) c->gnn_state_rows += lh[l].self_row.size();
+    c->gnn_node_instances = static_cast<uint64_t>(hs.nodes.size()) * cfg.layers;
     // unique subgraph embeddings -> every subgraph
     uint32_t* d_uo = c->buf<uint32_t>("gnn_uniq_of", count);
     sgc::copy_in(c, d_uo, uniq_of.data(), count);
@@ -3265,6 +3270,9 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                     w0 = wave_end[w];
                 }
             }
+            if (o->ttft_dequeue_ms)
+                for (uint32_t q = 0; q < m; ++q)
+                    o->ttft_dequeue_ms[q] = wave_of[q] >= 0 ? wave_ms[wave_of[q]] - start_w[wave_of[q]] : -1.0f;
             if (o->pftt_ms)
                 for (uint32_t q = 0; q < m; ++q) {
                     const int wq = wave_of[q];
@@ -3303,7 +3311,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             // served query, in ascending query order per rank (rank 0 knows every rank's list).
             // Every rank passes the same set of optional outputs.
             const size_t gen_w = (gen_on && o->tokens) ? max_new : 0, lg_w = o->logits ? SGC_VOCAB : 0;
-            const size_t W = 6 + gen_w + lg_w;  // 4-byte words per record
+            const size_t W = 7 + gen_w + lg_w;  // 4-byte words per record
             auto pack = [&](uint32_t q, uint32_t* r) {
                 int32_t ft = o->first_token ? o->first_token[q] : -1;
                 std::memcpy(&r[0], &ft, 4);
@@ -3312,8 +3320,10 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                                o->rt_ms ? o->rt_ms[q] : -1.f};
                 std::memcpy(&r[2], f3, 12);
                 r[5] = o->n_tokens ? o->n_tokens[q] : 0;
-                if (gen_w) std::memcpy(&r[6], o->tokens + static_cast<size_t>(q) * max_new, gen_w * 4);
-                if (lg_w) std::memcpy(&r[6 + gen_w], o->logits + static_cast<size_t>(q) * SGC_VOCAB, lg_w * 4);
+                const float td = o->ttft_dequeue_ms ? o->ttft_dequeue_ms[q] : -1.f;
+                std::memcpy(&r[6], &td, 4);
+                if (gen_w) std::memcpy(&r[7], o->tokens + static_cast<size_t>(q) * max_new, gen_w * 4);
+                if (lg_w) std::memcpy(&r[7 + gen_w], o->logits + static_cast<size_t>(q) * SGC_VOCAB, lg_w * 4);
             };
             auto unpack = [&](uint32_t q, const uint32_t* r) {
                 if (o->first_token) std::memcpy(&o->first_token[q], &r[0], 4);
@@ -3324,8 +3334,9 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 if (o->pftt_ms) o->pftt_ms[q] = f3[1];
                 if (o->rt_ms) o->rt_ms[q] = f3[2];
                 if (o->n_tokens) o->n_tokens[q] = r[5];
-                if (gen_w) std::memcpy(o->tokens + static_cast<size_t>(q) * max_new, &r[6], gen_w * 4);
-                if (lg_w) std::memcpy(o->logits + static_cast<size_t>(q) * SGC_VOCAB, &r[6 + gen_w], lg_w * 4);
+                if (o->ttft_dequeue_ms) std::memcpy(&o->ttft_dequeue_ms[q], &r[6], 4);
+                if (gen_w) std::memcpy(o->tokens + static_cast<size_t>(q) * max_new, &r[7], gen_w * 4);
+                if (lg_w) std::memcpy(o->logits + static_cast<size_t>(q) * SGC_VOCAB, &r[7 + gen_w], lg_w * 4);
             };
             std::vector<std::vector<uint32_t>> by_rank(world);
             for (uint32_t q = 0; q < m; ++q) by_rank[qrank[q]].push_back(q);
@@ -3475,9 +3486,20 @@ int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value) {
     return guarded([&] {
         if (std::string(name) == "gemm_pairs") sgc::gemm_set_pairs(value != 0);
         else if (std::string(name) == "attn_split") sgc::attention_set_split(value != 0);
+        else if (std::string(name) == "gnn_tile") ctx->c.gnn_tile = static_cast<int>(value);
         else if (std::string(name) == "decode_defer_pct") ctx->c.decode_defer_pct = static_cast<uint32_t>(std::max<int64_t>(0, value));
         else fail(SGC_DOMAIN, std::string("unknown option ") + name);
     });
+}
+
+int sgc_gnn_stats(const sgc_ctx* ctx, uint64_t* state_rows, uint64_t* node_instances) {
+    if (state_rows) *state_rows = ctx->c.gnn_state_rows;
+    if (node_instances) *node_instances = ctx->c.gnn_node_instances;
+    return SGC_OK;
+}
+
+int sgc_probe_fp64_tflops(sgc_ctx* ctx, double* tflops) {
+    return guarded([&] { *tflops = sgc::fp64_probe_tflops(current(&ctx->c)); });
 }
 
 int sgc_set_timing(sgc_ctx* ctx, int enable) {

@@ -73,6 +73,9 @@ struct Ctx {
     // generation: a wave decodes on its own until fewer than this % of its queries are still
     // generating; the stragglers of all waves then finish in one shared loop
     uint32_t decode_defer_pct = 25;
+    // last GNN encode: unique node states computed (all layers) / the reference's node instances
+    uint64_t gnn_state_rows = 0, gnn_node_instances = 0;
+    int gnn_tile = 1;  // GNN layer-map GEMM tile: 0 = 64x64, 1 = 64x128 (measured best at C3), 2 = 128x128
     cudaStream_t own_stream = nullptr;
     cudaStream_t side = nullptr;  // overlapped side work (sealed-prefix digests), created on first use
     cudaStream_t side_stream() {

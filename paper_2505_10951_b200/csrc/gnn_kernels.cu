@@ -31,8 +31,10 @@ __global__ void gen_wbar_kernel(double* wbar, int layers, int heads, int d, uint
     }
 }
 
-// one CTA per output group; threads over the feature dim. The group's self row and in-edge
-// list (ascending edge index) index the previous layer's unique states.
+// one CTA per output group; each thread owns two adjacent features (16-byte double2 state loads,
+// 8-byte float2 gate loads, coalesced across the CTA). The group's self row and in-edge list
+// (ascending edge index) index the previous layer's unique states; per feature the operand order
+// is the reference's (self, then each message in edge order; mul and add rounded separately).
 __global__ void gnn_aggregate_kernel(double* agg, const double* state, const uint32_t* self_row,
                                      const uint32_t* in_off, const uint32_t* in_src,
                                      const uint32_t* in_gate, const float* feat, int d) {
@@ -40,14 +42,16 @@ __global__ void gnn_aggregate_kernel(double* agg, const double* state, const uin
     const uint32_t e0 = in_off[v], e1 = in_off[v + 1];
     const double inv = __ddiv_rn(1.0, static_cast<double>(1 + (e1 - e0)));
     const size_t self = self_row[v];
-    for (int k = threadIdx.x; k < d; k += blockDim.x) {
-        double a = state[self * d + k];
+    const int d2 = d / 2;
+    for (int k2 = threadIdx.x; k2 < d2; k2 += blockDim.x) {
+        double2 a = reinterpret_cast<const double2*>(state + self * d)[k2];
         for (uint32_t e = e0; e < e1; ++e) {
-            double s = state[static_cast<size_t>(in_src[e]) * d + k];
-            double g = static_cast<double>(feat[static_cast<size_t>(in_gate[e]) * d + k]);
-            a = __dadd_rn(a, __dmul_rn(s, g));
+            const double2 s = reinterpret_cast<const double2*>(state + static_cast<size_t>(in_src[e]) * d)[k2];
+            const float2 g = __ldg(reinterpret_cast<const float2*>(feat + static_cast<size_t>(in_gate[e]) * d) + k2);
+            a.x = __dadd_rn(a.x, __dmul_rn(s.x, static_cast<double>(g.x)));
+            a.y = __dadd_rn(a.y, __dmul_rn(s.y, static_cast<double>(g.y)));
         }
-        agg[static_cast<size_t>(v) * d + k] = __dmul_rn(a, inv);
+        reinterpret_cast<double2*>(agg + static_cast<size_t>(v) * d)[k2] = make_double2(__dmul_rn(a.x, inv), __dmul_rn(a.y, inv));
     }
 }
 
@@ -62,42 +66,80 @@ __global__ void gnn_init_kernel(double* state, const uint32_t* inst_feat, const 
     }
 }
 
-constexpr int GM = 64, GN = 64, GK = 16;
-// out[v][r] = tanh(sum_c W[r][c] * A[v][c] * inv_heads); 256 threads, 4x4 outputs each
+// out[v][r] = tanh(sum_c W[r][c] * A[v][c] * inv_heads): FP64 SIMT GEMM, TM x TN tile per CTA,
+// 256 threads x a (TM/16) x (TN/16) register tile (the half-warp's A operand is a broadcast, B
+// 16 consecutive doubles: conflict-free shared loads; padded rows keep the staging stores at the
+// 2-wavefront minimum), k tiles of 8 double-buffered through registers. DFMA (fused) accumulation in ascending c per output.
+constexpr int GK = 8;
+template <int TM, int TN>
 __global__ void __launch_bounds__(256)
     gnn_layer_gemm(double* out, const double* A, const double* W, int n_inst, int d,
                    double inv_heads) {
-    __shared__ double As[GK][GM + 1];
-    __shared__ double Bs[GK][GN + 1];
-    const int v0 = blockIdx.x * GM, r0 = blockIdx.y * GN;
+    constexpr int PM = TM / 16, PN = TN / 16, LA = TM * GK / 256, LB = TN * GK / 256;
+    // rows padded by 4 doubles: the staging stores (8 k x 4 rows per warp) land 2 per bank pair
+    __shared__ double As[2][GK][TM + 4];
+    __shared__ double Bs[2][GK][TN + 4];
+    const int v0 = blockIdx.x * TM, r0 = blockIdx.y * TN;
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    double acc[4][4] = {};
-    for (int k0 = 0; k0 < d; k0 += GK) {
-        for (int idx = threadIdx.x; idx < GM * GK; idx += 256) {
-            int r = idx / GK, kk = idx % GK;
-            As[kk][r] = v0 + r < n_inst ? A[static_cast<size_t>(v0 + r) * d + k0 + kk] : 0.0;
-            Bs[kk][r] = r0 + r < d ? W[static_cast<size_t>(r0 + r) * d + k0 + kk] : 0.0;
+    double acc[PM][PN];
+#pragma unroll
+    for (int p = 0; p < PM; ++p)
+#pragma unroll
+        for (int q = 0; q < PN; ++q) acc[p][q] = 0.0;
+    double ra[LA], rb[LB];
+    auto load = [&](int k0) {
+#pragma unroll
+        for (int t = 0; t < LA; ++t) {
+            const int idx = threadIdx.x + 256 * t, r = idx / GK, kk = idx % GK;
+            ra[t] = v0 + r < n_inst ? A[static_cast<size_t>(v0 + r) * d + k0 + kk] : 0.0;
         }
-        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < LB; ++t) {
+            const int idx = threadIdx.x + 256 * t, r = idx / GK, kk = idx % GK;
+            rb[t] = r0 + r < d ? W[static_cast<size_t>(r0 + r) * d + k0 + kk] : 0.0;
+        }
+    };
+    auto store = [&](int buf) {
+#pragma unroll
+        for (int t = 0; t < LA; ++t) {
+            const int idx = threadIdx.x + 256 * t;
+            As[buf][idx % GK][idx / GK] = ra[t];
+        }
+#pragma unroll
+        for (int t = 0; t < LB; ++t) {
+            const int idx = threadIdx.x + 256 * t;
+            Bs[buf][idx % GK][idx / GK] = rb[t];
+        }
+    };
+    load(0);
+    store(0);
+    __syncthreads();
+    int buf = 0;
+    for (int k0 = 0; k0 < d; k0 += GK) {
+        const bool more = k0 + GK < d;
+        if (more) load(k0 + GK);  // in flight during the math
 #pragma unroll
         for (int kk = 0; kk < GK; ++kk) {
-            double a[4], b[4];
+            double a[PM], b[PN];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                a[q] = As[kk][ty + 16 * q];
-                b[q] = Bs[kk][tx + 16 * q];
-            }
+            for (int p = 0; p < PM; ++p) a[p] = As[buf][kk][ty + 16 * p];
 #pragma unroll
-            for (int p = 0; p < 4; ++p)
+            for (int q = 0; q < PN; ++q) b[q] = Bs[buf][kk][tx + 16 * q];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+            for (int p = 0; p < PM; ++p)
+#pragma unroll
+                for (int q = 0; q < PN; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
         }
-        __syncthreads();
+        if (more) {
+            store(buf ^ 1);
+            __syncthreads();
+            buf ^= 1;
+        }
     }
 #pragma unroll
-    for (int p = 0; p < 4; ++p)
+    for (int p = 0; p < PM; ++p)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < PN; ++q) {
             int v = v0 + ty + 16 * p, r = r0 + tx + 16 * q;
             if (v < n_inst && r < d) out[static_cast<size_t>(v) * d + r] = tanh(acc[p][q] * inv_heads);
         }
@@ -127,6 +169,22 @@ __global__ void gnn_pool_kernel(float* out, const double* state, const uint32_t*
     const double nrm = norm_s;
     for (int k = threadIdx.x; k < d; k += blockDim.x)
         out[static_cast<size_t>(u) * d + k] = nrm > 0.0 ? static_cast<float>(__ddiv_rn(pooled[k], nrm)) : 0.0f;
+}
+
+// FP64 FMA throughput probe (the GNN layer map's roofline denominator; MEASURED_PEAKS.json has no
+// FP64 figure): 8 independent DFMA chains per thread, no memory traffic
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double* sink, int iters) {
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = 1.0 + 1e-9 * (threadIdx.x + i);
+    const double a = 0.999999999, b = 1e-9;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += x[i];
+    if (s == 12345.0) sink[0] = s;  // never true: keeps the chains live
 }
 
 __global__ void gather_rows_kernel(float* out, const float* src, const uint32_t* idx, int d) {
@@ -161,9 +219,23 @@ void gnn_encode_layers(Ctx* c, const GnnPlan& p) {
         gnn_aggregate_kernel<<<L.n_out, threads, 0, c->stream>>>(p.agg, prev, L.self_row, L.in_off, L.in_src,
                                                                  L.in_gate, p.feat, d);
         SGC_LAUNCH_CHECK(c);
-        dim3 grid(ceil_div(L.n_out, GM), ceil_div(d, GN));
-        gnn_layer_gemm<<<grid, 256, 0, c->stream>>>(next, p.agg, p.wbar + static_cast<size_t>(l) * d * d,
-                                                     L.n_out, d, 1.0 / p.heads);
+        const double* wl = p.wbar + static_cast<size_t>(l) * d * d;
+        switch (c->gnn_tile) {
+            case 2: {
+                dim3 grid(ceil_div(L.n_out, 128), ceil_div(d, 128));
+                gnn_layer_gemm<128, 128><<<grid, 256, 0, c->stream>>>(next, p.agg, wl, L.n_out, d, 1.0 / p.heads);
+                break;
+            }
+            case 1: {
+                dim3 grid(ceil_div(L.n_out, 64), ceil_div(d, 128));
+                gnn_layer_gemm<64, 128><<<grid, 256, 0, c->stream>>>(next, p.agg, wl, L.n_out, d, 1.0 / p.heads);
+                break;
+            }
+            default: {
+                dim3 grid(ceil_div(L.n_out, 64), ceil_div(d, 64));
+                gnn_layer_gemm<64, 64><<<grid, 256, 0, c->stream>>>(next, p.agg, wl, L.n_out, d, 1.0 / p.heads);
+            }
+        }
         SGC_LAUNCH_CHECK(c);
     }
     size_t smem = static_cast<size_t>(d) * sizeof(double);
@@ -173,6 +245,28 @@ void gnn_encode_layers(Ctx* c, const GnnPlan& p) {
     gnn_pool_kernel<<<p.n_sub, threads, smem, c->stream>>>(p.out, p.state[p.layers & 1], p.sub_off,
                                                           p.sub_rows, d);
     SGC_LAUNCH_CHECK(c);
+}
+
+double fp64_probe_tflops(Ctx* c) {
+    double* sink = c->buf<double>("fp64_probe", 1);
+    const int blocks = c->num_sms * 8, iters = 4096;
+    cudaEvent_t e0 = c->event(), e1 = c->event();
+    fp64_probe_kernel<<<blocks, 256, 0, c->stream>>>(sink, iters);  // warm-up (clocks up)
+    SGC_LAUNCH_CHECK(c);
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        SGC_CUDA_CHECK(cudaEventRecord(e0, c->stream));
+        fp64_probe_kernel<<<blocks, 256, 0, c->stream>>>(sink, iters);
+        SGC_LAUNCH_CHECK(c);
+        SGC_CUDA_CHECK(cudaEventRecord(e1, c->stream));
+        SGC_CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0;
+        SGC_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+        best = std::min(best, ms);
+    }
+    c->event_pool.push_back(e0);
+    c->event_pool.push_back(e1);
+    return 2.0 * blocks * 256.0 * iters * 8 / (best * 1e-3) / 1e12;
 }
 
 void gather_rows(Ctx* c, float* out, const float* src, const uint32_t* idx, int n, int d) {

@@ -35,4 +35,6 @@ struct GnnPlan {
 void gnn_gen_wbar(Ctx* c, double* wbar, int layers, int heads, int d, uint64_t state0, float scale);
 void gnn_encode_layers(Ctx* c, const GnnPlan& p);
 void gather_rows(Ctx* c, float* out, const float* src, const uint32_t* idx, int n, int d);
+// measured FP64 FMA throughput of this device (TFLOP/s, best of 5 short launches)
+double fp64_probe_tflops(Ctx* c);
 }  // namespace sgc

@@ -124,6 +124,18 @@ class Context:
         check(self.lib.sgc_comm_destroy(self.h))
         self._transport = None
 
+    def fp64_tflops(self) -> float:
+        """Measured FP64 FMA throughput of this device (sgc_probe_fp64_tflops)."""
+        v = C.c_double()
+        check(self.lib.sgc_probe_fp64_tflops(self.h, C.byref(v)))
+        return v.value
+
+    def gnn_stats(self):
+        """(unique node states computed, the reference's node instances) of the last GNN encode."""
+        a, b = C.c_uint64(), C.c_uint64()
+        check(self.lib.sgc_gnn_stats(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def gemm(self, a_ptr: int, b_ptr: int, d_ptr: int, M: int, N: int, K: int, epi: int):
         check(self.lib.sgc_gemm_bf16(self.h, C.c_void_p(a_ptr), C.c_void_p(b_ptr),
                                      C.c_void_p(d_ptr), M, N, K, epi))
@@ -626,6 +638,7 @@ class SubgCacheResult:
     prefix_digest: np.ndarray | None = None  # [c] sealed-prefix digest (verified after serving)
     kv_pages_peak: int = 0                   # paged KV: peak pages in use, bytes per page
     kv_page_bytes: int = 0
+    ttft_dequeue_ms: np.ndarray | None = None  # [m] reference semantics: cluster dequeue -> first token
 
 
 class PreparedBatch:
@@ -754,6 +767,8 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     o.prefilled = _p(prefilled, C.c_uint8)
     digest = np.zeros(k, np.uint64)
     o.prefix_digest = _p(digest, C.c_uint64)
+    ttft_dq = np.full(m, -1.0, np.float32)
+    o.ttft_dequeue_ms = _p(ttft_dq, C.c_float)
     toks = cnt = rt = None
     if max_new > 1:
         toks = np.full((m, max_new), -1, np.int32)
@@ -770,6 +785,7 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     res.query_rank, res.prefilled = qrank, prefilled
     res.prefix_bytes_sent, res.prefix_bytes_received = o.prefix_bytes_sent, o.prefix_bytes_received
     res.prefix_digest = digest
+    res.ttft_dequeue_ms = ttft_dq
     res.kv_pages_peak, res.kv_page_bytes = o.kv_pages_peak, o.kv_page_bytes
     if max_new > 1:
         res.tokens = [toks[q, :cnt[q]].copy() for q in range(m)]
