@@ -266,3 +266,7 @@ if __name__ == "__main__":
         lm_cases()
         cluster_cases()
         scene_graph_cases(td)
+    # the bundled scene graph's queries (acceptance criterion 11 runs in a data dir written from
+    # scene_graph.json + this file: tests/test_dropin.py)
+    with open(os.path.join(REF_DATA, "queries.jsonl")) as f:
+        dump("scene_graph_queries.json", [json.loads(x) for x in f if x.strip()])
