@@ -217,8 +217,8 @@ def run_ours(args, rank, world, local_rank):
     ctx.set_option("gemm_pairs", 0 if args.no_pairs else 1)
     if args.attn_split is not None:
         ctx.set_option("attn_split", args.attn_split)
-    if args.attn_db is not None:
-        ctx.set_option("attn_db", args.attn_db)
+    if args.attn_kernel is not None:
+        ctx.set_option("attn_kernel", args.attn_kernel)
     t0 = time.time()
     lm = host.ToyLm(ctx, host.ToyLmConfig(**w.lm, seed=w.seed))
     dg = host.DeviceGraph(ctx, w.graph)
@@ -729,8 +729,8 @@ def main():
     ap.add_argument("--no-split", action="store_true",
                     help="N > 1: whole clusters per GPU only (no member-level rebalancing of skewed clusters)")
     ap.add_argument("--attn-split", type=int, default=None, help="1: two softmax warpgroups per query tile")
-    ap.add_argument("--attn-db", type=int, default=None,
-                    help="1: double-buffered 64-key attention kernel, 0: 128-key single-buffer kernel")
+    ap.add_argument("--attn-kernel", type=int, default=None,
+                    help="0: two-tile attention kernel, 1/2: double-buffered S with one/two softmax warpgroups")
     ap.add_argument("--gen-steps", type=int, default=2)
     ap.add_argument("--gen-waves", type=int, default=2,
                     help="waves of the generation run (cost-balanced cuts; scripts/defer_probe.py: "

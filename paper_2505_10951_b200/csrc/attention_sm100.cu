@@ -49,6 +49,9 @@ constexpr int kVStages = 2;
 #ifndef SGC_LAZY_MAX
 #define SGC_LAZY_MAX 8.f
 #endif
+#ifndef SGC_S3_TOKEN_LATE
+#define SGC_S3_TOKEN_LATE 0
+#endif
 #ifndef SGC_ATTN_PINGPONG
 #define SGC_ATTN_PINGPONG 1
 #endif
@@ -74,7 +77,7 @@ struct TcCfg {
 // Compile with -DSGC_ATTN_PROF to accumulate per-phase clock64() cycles into a global
 // [148][16] counter array (debug builds only; see scripts/attn_prof.py).
 #ifdef SGC_ATTN_PROF
-__device__ unsigned long long g_attn_prof[148 * 16];
+__device__ unsigned long long g_attn_prof[148 * 32];
 #endif
 
 struct TcParams {
@@ -425,7 +428,7 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
 #define SPROF(slot)                                                                            \
     if (prof_thr) {                                                                            \
         long long _n = clock64();                                                              \
-        atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 16 + (slot)], (unsigned long long)(_n - _pt)); \
+        atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 32 + (slot)], (unsigned long long)(_n - _pt)); \
         _pt = _n;                                                                              \
     }
 #else
@@ -638,6 +641,565 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
     }
 }
 
+// =============================================================================================
+// attn_s3_kernel -- one 128-row query tile per item; S triple-buffered in TMEM; two softmax
+// warpgroups taking alternate key blocks of the same rows.
+//
+// The two-tile kernel above runs two dependency chains S(b) -> softmax(b) -> PV(b) -> S(b+1) per
+// CTA (P lives in S's columns, so S(b+1) of a tile waits for PV(b) of that tile) and shares the
+// SM sub-partitions between the two tiles' softmaxes: the chain per block is softmax + S + PV +
+// latencies (~3.7k cycles against 2 x 1024 of tensor work; 54% tensor-active, the softmax
+// waiting a third of its time for its next S, scripts/attn_prof.py). Here:
+//   * the MMA warp runs three blocks ahead: S(g+3) goes into buffer g % 3 as soon as PV(g) is
+//     issued, so a block's S is ready long before its softmax starts;
+//   * softmax warpgroup w takes the blocks g with g % 2 == w, so two blocks' softmaxes overlap
+//     (one's exponentials on MUFU while the other loads S from TMEM / reduces its max) and each
+//     warpgroup has two block periods per block;
+//   * the rows' running max is shared (smem, lazy: it only moves when a block overshoots it by
+//     more than 2^8): block g+1 reads the max block g decided (named-barrier token passed
+//     between the warpgroups, after both computed their block max) before its exponentials;
+//     each warpgroup keeps its own row sum relative to the max it last saw; the rare O rescale
+//     waits for the previous PV; the epilogue combines the two row sums.
+//
+//   warp 0      TMEM allocator + TMA producer: claims tiles (skipping empty ones), Q per tile,
+//               K blocks two ahead of V blocks in the global block stream
+//   warp 10     S issuer: S(g) into buffer g % 3 once PV(g-3) read that buffer's P
+//   warp 1      PV issuer: O += P(g) V(g) (one thread issuing both ran ~1.4k cycles per block
+//               of 1024 tensor cycles: ~17 instructions per tcgen05.mma)
+//   warps 2-5   softmax warpgroup 0 (even blocks), warps 6-9 warpgroup 1 (odd blocks)
+//   TMEM: S_0 | S_1 | S_2 | O   (columns 0, 128, 256, 384)
+// =============================================================================================
+template <int HD>
+struct S3Cfg {
+    static constexpr int kSub = HD / 64;
+    static constexpr int kQBytes = BQ * HD * 2;
+    static constexpr int kKBytes = BKV * HD * 2;
+    static constexpr int kVBytes = BKV * HD * 2;
+    static constexpr int kQStages = 2, kKStages = 2, kVStages = 3;
+    static constexpr int kTiles = kQStages * kQBytes + kKStages * kKBytes + kVStages * kVBytes;
+    // + barriers (256 B) + shared row max and row-sum hand-over [2 tile parities][BQ] + item ring
+    static constexpr int kSmem = kTiles + 256 + 2 * BQ * 4 + 2 * BQ * 4 + 160 + 8 * 44;
+    static constexpr uint32_t kTmemCols = 512;
+    static constexpr uint32_t kS = 0;    // S buffer s at column s * 128
+    static constexpr uint32_t kO = 384;  // O (HD columns)
+};
+
+// a claimed 128-row tile, resolved by the producer and published with its ring slot
+struct TileInfo {
+    AttnWork w;
+    int h, x, nA, nb, nrows, loc_first;
+};
+// eight slots: the MMA warp holds the tiles from its PV cursor to its S cursor (up to four
+// one-block tiles) while the producer claims ahead
+constexpr int kTileRing = 8;
+using TileRing = UnitRing<kTileRing>;
+
+__device__ __forceinline__ TileInfo plan_tile(const AttnWork& w, int h, int x, const int32_t* seg_lo, bool partial) {
+    TileInfo t;
+    t.w = w;
+    t.h = h;
+    t.x = x;
+    t.nA = (w.pfx_len + BKV - 1) / BKV;
+    t.nrows = min(BQ, max(0, w.nrows - x * BQ));
+    if (partial) {
+        t.loc_first = 0;
+        t.nb = t.nrows > 0 ? t.nA : 0;
+        return t;
+    }
+    // own keys: contiguous batch rows start at the tile's first member (keys before it are
+    // never visible to the tile); paged sequences are read page by page from their start
+    t.loc_first = t.nrows > 0 ? seg_lo[w.loc_bt >= 0 ? w.row0 : w.row0 + x * BQ] : 0;
+    const int last = w.row0 + x * BQ + t.nrows - 1;
+    t.nb = t.nrows > 0 ? t.nA + (last - t.loc_first + BKV) / BKV : 0;
+    return t;
+}
+
+template <int HD>
+__global__ void __launch_bounds__(352, 1)
+    attn_s3_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKp,
+                   const __grid_constant__ CUtensorMap tmVp, const __grid_constant__ CUtensorMap tmKl,
+                   const __grid_constant__ CUtensorMap tmVl, TcParams p) {
+    using C = S3Cfg<HD>;
+    static_assert(sizeof(TileRing) <= 160 && sizeof(TileInfo) <= 44, "tile ring");
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* sQ = smem;                                  // [2][BQ x HD]
+    uint8_t* sK = sQ + C::kQStages * C::kQBytes;         // [2][BKV x HD]
+    uint8_t* sV = sK + C::kKStages * C::kKBytes;         // [3][BKV x HD]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + C::kVStages * C::kVBytes);
+    uint64_t* q_full = bars + 0;    // [2]
+    uint64_t* q_empty = bars + 2;   // [2]
+    uint64_t* k_full = bars + 4;    // [2]
+    uint64_t* k_empty = bars + 6;   // [2]
+    uint64_t* v_full = bars + 8;    // [3]
+    uint64_t* v_empty = bars + 11;  // [3]
+    uint64_t* s_full = bars + 14;   // [3] per S buffer
+    uint64_t* p_full = bars + 17;   // [3] per S buffer (P is written over S)
+    uint64_t* o_full = bars + 20;   // the tile's last PV completed
+    uint64_t* o_free = bars + 21;   // the tile's epilogue read O (the next tile's first PV may run)
+    uint64_t* pv_done = bars + 22;  // [2] PV(g) completed, by block parity (the rare O rescale)
+    uint64_t* s_free = bars + 24;   // [3] PV read the buffer's P: the next S may overwrite it
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
+    float* m_sh = reinterpret_cast<float*>(bars + 32);  // [2 tile parities][BQ] the rows' running max
+    float* lx = m_sh + 2 * BQ;                          // [2 tile parities][BQ] row-sum hand-over
+    TileRing* ring = reinterpret_cast<TileRing*>(lx + 2 * BQ);
+    TileInfo* info = reinterpret_cast<TileInfo*>(reinterpret_cast<uint8_t*>(ring) + 160);  // [kTileRing]
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int n_items = 2 * p.n_work * p.heads;  // (head, unit, tile) with the tile fastest
+    const bool partial = p.part_o != nullptr;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmQ);
+        ptx::tma_prefetch_desc(&tmKp);
+        ptx::tma_prefetch_desc(&tmVp);
+        ptx::tma_prefetch_desc(&tmKl);
+        ptx::tma_prefetch_desc(&tmVl);
+        for (int i = 0; i < 3; ++i) {
+            ptx::mbar_init(&v_full[i], 1);
+            ptx::mbar_init(&v_empty[i], 1);
+            ptx::mbar_init(&s_full[i], 1);
+            ptx::mbar_init(&p_full[i], 128);
+            ptx::mbar_init(&s_free[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            ptx::mbar_init(&q_full[i], 1);
+            ptx::mbar_init(&q_empty[i], 1);
+            ptx::mbar_init(&k_full[i], 1);
+            ptx::mbar_init(&k_empty[i], 1);
+            ptx::mbar_init(&pv_done[i], 1);
+        }
+        ptx::mbar_init(o_full, 1);
+        ptx::mbar_init(o_free, 128);
+        sched::init(ring, 2 + 8);  // the two MMA threads + every softmax warp
+        ptx::fence_barrier_init();
+    }
+    if (warp == 0) ptx::tmem_alloc<C::kTmemCols>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+#ifdef SGC_ATTN_PROF
+    // cycles the producer / MMA threads spend in each wait (slots 16..)
+    auto pwait = [&](uint64_t* bar, uint32_t par, int slot) {
+        const long long t0 = clock64();
+        ptx::mbar_wait_park(bar, par);
+        atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 32 + slot], (unsigned long long)(clock64() - t0));
+    };
+#else
+    auto pwait = [&](uint64_t* bar, uint32_t par, int) { ptx::mbar_wait_park(bar, par); };
+#endif
+    // key row of block b of tile t: prefix pages, the sequence's own pages (paged prefill) or
+    // contiguous scratch rows
+    auto block_row = [&](const TileInfo& t, int b) -> int {
+        if (b < t.nA) return kv_row_of(p.bt, t.w.pfx_off, b * BKV);
+        return t.w.loc_bt >= 0 ? kv_row_of(p.bt, t.w.loc_bt, (b - t.nA) * BKV) : t.loc_first + (b - t.nA) * BKV;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // two cursors over the global block stream: K runs two blocks ahead of V
+            uint32_t gk = 0, gv = 0;
+            int ki = -1, kb = 0, knb = 0, vi = 0, vb = 0;
+            bool kend = false;
+            auto next_k = [&]() -> bool {
+                if (kend) return false;
+                while (kb >= knb) {
+                    ++ki;
+                    const int sl = ki % kTileRing;
+                    pwait(&ring->empty[sl], ((ki / kTileRing) & 1) ^ 1, 27);
+                    uint32_t iu;
+                    TileInfo t{};
+                    for (;;) {  // claim the next non-empty tile (one claim past the end per CTA)
+                        iu = sched::claim(p.sched, n_items, gridDim.x, ki);
+                        if (iu >= static_cast<uint32_t>(n_items)) break;
+                        const int per_head = 2 * p.n_work;
+                        const int h = static_cast<int>(iu) / per_head, rem = static_cast<int>(iu) % per_head;
+                        t = plan_tile(p.work[rem >> 1], h, rem & 1, p.seg_lo, partial);
+                        if (t.nb > 0) break;
+                    }
+                    ring->unit[sl] = iu;
+                    if (iu < static_cast<uint32_t>(n_items)) info[sl] = t;
+                    ptx::mbar_arrive(&ring->full[sl]);
+                    if (iu >= static_cast<uint32_t>(n_items)) {
+                        kend = true;
+                        return false;
+                    }
+                    knb = t.nb;
+                    kb = 0;
+                    const int qs = ki & 1;
+                    pwait(&q_empty[qs], ((ki >> 1) & 1) ^ 1, 26);
+                    ptx::mbar_expect_tx(&q_full[qs], C::kQBytes);
+#pragma unroll
+                    for (int s = 0; s < C::kSub; ++s)
+                        ptx::tma_load_2d(sQ + qs * C::kQBytes + s * (BQ * 128), &tmQ, &q_full[qs], t.h * HD + s * 64,
+                                         t.w.row0 + t.x * BQ);
+                }
+                const TileInfo& t = info[ki % kTileRing];
+                const bool pfx = kb < t.nA;
+                const int row = block_row(t, kb);
+                const int ks = gk % C::kKStages;
+                pwait(&k_empty[ks], ((gk / C::kKStages) & 1) ^ 1, 24);
+                ptx::mbar_expect_tx(&k_full[ks], C::kKBytes);
+#pragma unroll
+                for (int s = 0; s < C::kSub; ++s)
+                    ptx::tma_load_2d(sK + ks * C::kKBytes + s * (BKV * 128), pfx ? &tmKp : &tmKl, &k_full[ks],
+                                     t.h * HD + s * 64, row);
+                ++kb;
+                ++gk;
+                return true;
+            };
+            auto next_v = [&]() {
+                while (vb >= info[vi % kTileRing].nb) {  // the K cursor already claimed item vi (<= ki)
+                    ++vi;
+                    vb = 0;
+                }
+                const TileInfo& t = info[vi % kTileRing];
+                const bool pfx = vb < t.nA;
+                const int row = block_row(t, vb);
+                const int vs = gv % C::kVStages;
+                pwait(&v_empty[vs], ((gv / C::kVStages) & 1) ^ 1, 25);
+                ptx::mbar_expect_tx(&v_full[vs], C::kVBytes);
+#pragma unroll
+                for (int s = 0; s < C::kSub; ++s)
+                    ptx::tma_load_2d(sV + vs * C::kVBytes + s * (BKV * 128), pfx ? &tmVp : &tmVl, &v_full[vs],
+                                     t.h * HD + s * 64, row);
+                ++vb;
+                ++gv;
+            };
+            bool more = next_k() && next_k();
+            while (more || gv < gk) {
+                if (more) more = next_k();
+                if (gv < gk) next_v();
+            }
+        }
+    } else if (warp == 1 || warp == 10) {
+        // two MMA issuers (a single thread spends ~17 instructions per tcgen05.mma and was the
+        // bottleneck issuing 16 MMAs per 1024 tensor cycles): warp 10 issues S, warp 1 PV.
+        // S(g) overwrites buffer g % 3 only after PV(g - 3) read P(g - 3) from it (s_free).
+        if (lane == 0 && warp == 10) {
+            constexpr uint32_t idS = ptx::idesc_bf16_f32(BQ, BKV);
+            uint32_t g = 0;
+            for (uint32_t k = 0;; ++k) {
+                const uint32_t iu = sched::wait(ring, k);
+                const int nb = iu < static_cast<uint32_t>(n_items) ? info[k % kTileRing].nb : 0;
+                sched::release(ring, k);
+                if (iu >= static_cast<uint32_t>(n_items)) break;
+                pwait(&q_full[k & 1], (k >> 1) & 1, 20);
+                const uint64_t qd = ptx::umma_desc_sw128(ptx::smem_u32(sQ + (k & 1) * C::kQBytes));
+                for (int b = 0; b < nb; ++b, ++g) {
+                    const int ks = g % C::kKStages;
+                    const int sbuf = g % 3;
+                    if (g >= 3) pwait(&s_free[sbuf], ((g - 3) / 3) & 1, 21);
+                    pwait(&k_full[ks], (g / C::kKStages) & 1, 16);
+                    ptx::tc_fence_after();
+                    const uint64_t kd = ptx::umma_desc_sw128(ptx::smem_u32(sK + ks * C::kKBytes));
+                    const uint32_t dS = tmem_base + C::kS + sbuf * 128;
+#pragma unroll
+                    for (int kc = 0; kc < HD / 16; ++kc) {
+                        // descriptor start address field: bytes >> 4
+                        const uint64_t ad = qd + (((kc / 4) * (BQ * 128) + (kc % 4) * 32) >> 4);
+                        const uint64_t bd = kd + (((kc / 4) * (BKV * 128) + (kc % 4) * 32) >> 4);
+                        ptx::mma_bf16(dS, ad, bd, idS, kc > 0 ? 1u : 0u);
+                    }
+                    ptx::mma_commit(&s_full[sbuf]);
+                    ptx::mma_commit(&k_empty[ks]);
+                    if (b == nb - 1) ptx::mma_commit(&q_empty[k & 1]);
+                }
+            }
+        } else if (lane == 0) {
+            constexpr uint32_t idO = ptx::idesc_bf16_f32_bmn(BQ, HD);
+            uint32_t g = 0;
+            for (uint32_t k = 0;; ++k) {
+                const uint32_t iu = sched::wait(ring, k);
+                const int nb = iu < static_cast<uint32_t>(n_items) ? info[k % kTileRing].nb : 0;
+                sched::release(ring, k);
+                if (iu >= static_cast<uint32_t>(n_items)) break;
+                if (k > 0) pwait(o_free, (k - 1) & 1, 19);  // the previous tile's epilogue read O
+                for (int b = 0; b < nb; ++b, ++g) {
+                    const int vs = g % C::kVStages;
+                    const int pbuf = g % 3;
+                    pwait(&v_full[vs], (g / C::kVStages) & 1, 17);
+                    pwait(&p_full[pbuf], (g / 3) & 1, 18);
+                    ptx::tc_fence_after();
+                    const uint64_t vd = ptx::umma_desc_sw128_lbo(ptx::smem_u32(sV + vs * C::kVBytes), BKV * 128, 1024);
+                    const uint32_t aP = tmem_base + C::kS + pbuf * 128;
+#pragma unroll
+                    for (int kk = 0; kk < BKV / 16; ++kk)
+                        ptx::mma_bf16_ts(tmem_base + C::kO, aP + kk * 8, vd + ((kk * 16 * 128) >> 4), idO,
+                                         (b > 0 || kk > 0) ? 1u : 0u);
+                    ptx::mma_commit(&v_empty[vs]);
+                    ptx::mma_commit(&pv_done[g & 1]);
+                    ptx::mma_commit(&s_free[pbuf]);
+                    if (b == nb - 1) ptx::mma_commit(o_full);
+                }
+            }
+        }
+    } else {
+        const int wg = (warp - 2) / 4;            // softmax warpgroup: blocks with g % 2 == wg
+        const int r = (warp & 3) * 32 + lane;     // row within the tile == TMEM lane
+        const uint32_t lane_base = static_cast<uint32_t>((warp & 3) * 32) << 16;
+        const uint32_t tO = tmem_base + lane_base + C::kO;
+        // decision token (this warpgroup -> the other): named barriers 3 + wg / 4 - wg for even
+        // tiles, 5 + wg / 6 - wg for odd ones (a warpgroup starts the next tile without waiting
+        // for the other, so a tile's last token may still be pending when the next tile's first
+        // is posted)
+        uint32_t G = 0, uit = 0;  // first global block of the current tile, tiles done
+#ifdef SGC_ATTN_PROF
+        const bool prof_thr = threadIdx.x == 64 || threadIdx.x == 192;
+        long long _pt = clock64();
+#define SPROF(slot)                                                                                        \
+    if (prof_thr) {                                                                                        \
+        long long _n = clock64();                                                                          \
+        atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 32 + wg * 8 + (slot)], (unsigned long long)(_n - _pt)); \
+        _pt = _n;                                                                                          \
+    }
+#else
+#define SPROF(slot)
+#endif
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t iu = sched::wait(ring, k);
+            TileInfo t;
+            if (iu < static_cast<uint32_t>(n_items)) t = info[k % kTileRing];
+            __syncwarp();
+            if (lane == 0) sched::release(ring, k);
+            if (iu >= static_cast<uint32_t>(n_items)) break;
+            const bool valid = r < t.nrows;
+            const int row = t.w.row0 + t.x * BQ + r;
+            const int seg = valid && !partial ? p.seg_lo[row] : 0x7fffffff;
+            float m_w = -INFINITY, l_w = 0.f;  // this warpgroup's row sum, relative to m_w
+            float m_prev = -INFINITY;            // the max the tile's last block started from
+            float* m_shk = m_sh + (uit & 1) * BQ;
+            const int bar_post = 3 + wg + 2 * (uit & 1), bar_take = 4 - wg + 2 * (uit & 1);
+            for (int b = (static_cast<int>(G) + wg) & 1 ? 1 : 0; b < t.nb; b += 2) {
+                const uint32_t g = G + b;
+                const int sbuf = g % 3;
+                const uint32_t tS = tmem_base + lane_base + C::kS + sbuf * 128;
+                SPROF(0);
+                ptx::mbar_wait(&s_full[sbuf], (g / 3) & 1);
+                ptx::tc_fence_after();
+                SPROF(1);
+                int k0, klo, khi;  // visible key window [klo, khi] in block-local index
+                if (b < t.nA) {
+                    k0 = b * BKV;
+                    klo = 0;
+                    khi = valid ? min(BKV, t.w.pfx_len - k0) - 1 : -1;
+                } else {
+                    k0 = t.loc_first + (b - t.nA) * BKV;
+                    klo = max(0, seg - k0);
+                    khi = valid ? min(BKV - 1, row - k0) : -1;
+                }
+                const bool full = __all_sync(0xffffffffu, klo <= 0 && khi >= BKV - 1);
+                const float sc = p.scale_log2;
+                uint32_t sv[BKV];
+#pragma unroll
+                for (int c = 0; c < BKV / 32; ++c)
+                    ptx::tmem_ld32(tS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
+                ptx::tmem_ld_wait();
+                if (!full) {
+                    uint32_t vw[BKV / 32];
+#pragma unroll
+                    for (int wd = 0; wd < BKV / 32; ++wd) {
+                        const int lo = klo - 32 * wd, hi = khi - 32 * wd;
+                        const uint32_t mlo = lo <= 0 ? ~0u : (lo >= 32 ? 0u : ~0u << lo);
+                        const uint32_t mhi = hi >= 31 ? ~0u : (hi < 0 ? 0u : ~0u >> (31 - hi));
+                        vw[wd] = mlo & mhi;
+                    }
+#pragma unroll
+                    for (int j = 0; j < BKV; ++j)
+                        if (!(vw[j / 32] & (1u << (j % 32)))) sv[j] = __float_as_uint(-INFINITY);
+                }
+                float bmax;
+                {
+                    float q0 = -INFINITY, q1 = -INFINITY, q2 = -INFINITY, q3 = -INFINITY;
+#pragma unroll
+                    for (int j = 0; j < BKV; j += 8) {
+                        q0 = fmax3(q0, __uint_as_float(sv[j]), __uint_as_float(sv[j + 1]));
+                        q1 = fmax3(q1, __uint_as_float(sv[j + 2]), __uint_as_float(sv[j + 3]));
+                        q2 = fmax3(q2, __uint_as_float(sv[j + 4]), __uint_as_float(sv[j + 5]));
+                        q3 = fmax3(q3, __uint_as_float(sv[j + 6]), __uint_as_float(sv[j + 7]));
+                    }
+                    bmax = fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)) * sc;  // scaled-log2 units
+                }
+                SPROF(2);
+                // the running max as the previous block of this tile left it (the other
+                // warpgroup's decision, handed over through a named barrier)
+                float m_cur = -INFINITY;
+                if (b > 0) {
+                    asm volatile("bar.sync %0, 256;" ::"r"(bar_take) : "memory");
+                    m_cur = m_shk[r];
+                }
+                m_prev = m_cur;
+                if (m_cur != m_w) {  // the other warpgroup moved the max: re-base this row sum
+                    l_w = m_w == -INFINITY ? 0.f : l_w * ex2_approx(m_w - m_cur);
+                    m_w = m_cur;
+                }
+                const float mnew = (m_cur == -INFINITY || bmax > m_cur + SGC_LAZY_MAX) ? bmax : m_cur;
+                if (b == 0 || mnew != m_cur) m_shk[r] = mnew;
+#if !SGC_S3_TOKEN_LATE
+                if (b + 1 < t.nb) asm volatile("bar.arrive %0, 256;" ::"r"(bar_post) : "memory");
+#endif
+                const float nm = mnew == -INFINITY ? 0.f : -mnew;
+                SPROF(3);
+                float rs;
+                {
+                    const uint64_t sc2 = f2pack(sc, sc), nm2 = f2pack(nm, nm);
+                    uint64_t r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+#pragma unroll
+                    for (int j = 0; j < BKV / 2; ++j) {
+                        float xa, xc;
+                        f2unpack(ffma2(f2pack(__uint_as_float(sv[2 * j]), __uint_as_float(sv[2 * j + 1])), sc2, nm2),
+                                 xa, xc);
+                        float a, cc;
+                        if ((j % SGC_POLY_DEN) < SGC_POLY_NUM) {
+                            ex2_poly2(xa, xc, a, cc);
+                        } else {
+                            a = ex2_approx(xa);
+                            cc = ex2_approx(xc);
+                        }
+                        const uint64_t pr = f2pack(a, cc);
+                        if ((j & 3) == 0) r0 = fadd2(r0, pr);
+                        else if ((j & 3) == 1) r1 = fadd2(r1, pr);
+                        else if ((j & 3) == 2) r2 = fadd2(r2, pr);
+                        else r3 = fadd2(r3, pr);
+                        __nv_bfloat162 bv = __floats2bfloat162_rn(a, cc);
+                        sv[j] = *reinterpret_cast<uint32_t*>(&bv);
+                    }
+                    float x0, x1;
+                    f2unpack(fadd2(fadd2(r0, r1), fadd2(r2, r3)), x0, x1);
+                    rs = x0 + x1;
+                }
+#if SGC_S3_TOKEN_LATE
+                // hand the token on after the exponentials: the next block's exponentials start
+                // when these end (the two warpgroups take turns on MUFU)
+                if (b + 1 < t.nb) asm volatile("bar.arrive %0, 256;" ::"r"(bar_post) : "memory");
+#endif
+                SPROF(4);
+                const bool resc = m_cur != -INFINITY && mnew > m_cur;
+                if (__any_sync(0xffffffffu, resc)) {
+                    // O holds PV(0 .. g-1) relative to m_cur: rescale once PV(g-1) completed
+                    // (s_full(g) certified PV(g-3); pv_done alternates by block parity)
+                    ptx::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+                    ptx::tc_fence_after();
+                    const float alpha = resc ? ex2_approx(m_cur - mnew) : 1.f;
+                    l_w *= alpha;
+#pragma unroll 1
+                    for (int c = 0; c < HD / 32; ++c) {
+                        uint32_t o[32];
+                        ptx::tmem_ld32(tO + c * 32, o);
+                        ptx::tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+                        ptx::tmem_st32(tO + c * 32, o);
+                    }
+                }
+                m_w = mnew;
+                l_w += rs;
+                // P -> TMEM over the buffer's first 64 columns
+#pragma unroll
+                for (int c = 0; c < BKV / 32; ++c)
+                    ptx::tmem_st16(tS + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&sv[c * 16]));
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                ptx::mbar_arrive(&p_full[sbuf]);
+                SPROF(5);
+            }
+            const int last_wg = (G + t.nb - 1) & 1;  // the warpgroup of the tile's last block
+            G += t.nb;
+            // epilogue by the warpgroup of the tile's last block alone: the other hands over its
+            // row sum (relative to the max the last block started from) and goes on with the next
+            // tile's first block while this one waits for the last PV, reads O and frees it
+            float* lxk = lx + (uit & 1) * BQ;
+            const int bar_epi = 1 + (uit & 1);
+            if (wg != last_wg) {
+                lxk[r] = l_w;
+                asm volatile("bar.arrive %0, 256;" ::"r"(bar_epi) : "memory");
+            } else {
+                asm volatile("bar.sync %0, 256;" ::"r"(bar_epi) : "memory");
+                const float m_fin = m_w;
+                const float lo = lxk[r];
+                const float l = l_w + (m_prev == -INFINITY ? 0.f : lo * ex2_approx(m_prev - m_fin));
+                ptx::mbar_wait(o_full, uit & 1);
+                ptx::tc_fence_after();
+                const float il = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll 1
+                for (int hh = 0; hh < 2; ++hh) {  // two halves of the row (register budget)
+                    constexpr int OCOLS = HD / 2;
+                    uint32_t o[OCOLS];
+#pragma unroll
+                    for (int c = 0; c < OCOLS / 32; ++c)
+                        ptx::tmem_ld32(tO + hh * OCOLS + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
+                    ptx::tmem_ld_wait();
+                    if (hh == 1) {
+                        ptx::tc_fence_before();
+                        ptx::mbar_arrive(o_free);
+                    }
+                    if (valid && partial) {
+                        float* dst = p.part_o + static_cast<size_t>(row) * p.d + t.h * HD + hh * OCOLS;
+#pragma unroll
+                        for (int q = 0; q < OCOLS / 8; ++q) {
+                            uint32_t wv[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) wv[e] = __float_as_uint(__uint_as_float(o[8 * q + e]) * il);
+                            ptx::st_global_v8(dst + 8 * q, wv);
+                        }
+                    } else if (valid) {
+                        __nv_bfloat16* dst = p.out + static_cast<size_t>(row) * p.d + t.h * HD + hh * OCOLS;
+#pragma unroll
+                        for (int q = 0; q < OCOLS / 16; ++q) {
+                            uint32_t wv[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                __nv_bfloat162 bv = __floats2bfloat162_rn(__uint_as_float(o[16 * q + 2 * e]) * il,
+                                                                          __uint_as_float(o[16 * q + 2 * e + 1]) * il);
+                                wv[e] = *reinterpret_cast<uint32_t*>(&bv);
+                            }
+                            ptx::st_global_v8(dst + 16 * q, wv);
+                        }
+                    }
+                }
+                if (valid && partial)
+                    p.part_lse[static_cast<size_t>(row) * p.heads + t.h] = l > 0.f ? m_fin + __log2f(l) : -INFINITY;
+            }
+            ++uit;
+            SPROF(6);
+        }
+#undef SPROF
+    }
+    __syncthreads();
+    if (warp == 0) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<C::kTmemCols>(tmem_base);
+    }
+}
+
+// 0: two-tile kernel (attn_tc_kernel), 1: attn_s3_kernel (sgc_set_option "attn_kernel")
+int g_attn_kernel = 1;
+
+template <int HD>
+void launch_s3(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, int pfx_rows, int loc_rows) {
+    using Cf = S3Cfg<HD>;
+    auto kfn = attn_s3_kernel<HD>;
+    static std::atomic<uint64_t> attr_devices{0};
+    if (!(attr_devices.load() >> c->device & 1)) {
+        SGC_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::kSmem));
+        attr_devices |= 1ull << c->device;
+    }
+    const int d = a.d;
+    CUtensorMap tq = make_map_2d(a.q, q_rows, d, BQ, 64);
+    CUtensorMap tkp = make_map_2d(a.k_pfx, pfx_rows, d, BKV, 64);
+    CUtensorMap tvp = make_map_2d(a.v_pfx, pfx_rows, d, BKV, 64);
+    CUtensorMap tkl = make_map_2d(a.k_loc, loc_rows, d, BKV, 64);
+    CUtensorMap tvl = make_map_2d(a.v_loc, loc_rows, d, BKV, 64);
+    TcParams p{a.work, n_work, heads, a.part_o, a.part_lse, a.seg_lo, a.out, d, a.scale * 1.4426950408889634f,
+               c->sched_counter(), a.bt};
+    const int items = 2 * n_work * heads;
+    const int grid = items < c->num_sms ? items : c->num_sms;
+    Ctx::Timed timer(c, "attention");
+    kfn<<<grid, 352, Cf::kSmem, c->stream>>>(tq, tkp, tvp, tkl, tvl, p);
+    SGC_LAUNCH_CHECK(c);
+}
+
 template <int HD, int SPLIT>
 void launch_tc(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, int pfx_rows, int loc_rows) {
     using Cf = TcCfg<HD>;
@@ -666,10 +1228,10 @@ void launch_tc(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, i
 
 #ifdef SGC_ATTN_PROF
 void attn_prof_read(unsigned long long* out) {
-    cudaMemcpyFromSymbol(out, g_attn_prof, sizeof(unsigned long long) * 148 * 16);
+    cudaMemcpyFromSymbol(out, g_attn_prof, sizeof(unsigned long long) * 148 * 32);
 }
 void attn_prof_reset() {
-    static unsigned long long z[148 * 16] = {};
+    static unsigned long long z[148 * 32] = {};
     cudaMemcpyToSymbol(g_attn_prof, z, sizeof(z));
 }
 #endif
@@ -679,6 +1241,13 @@ bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, in
     if (n_work <= 0) return true;
     if (p.loc_kv0 != 0) return false;
     if (p.part_o && !p.part_lse) return false;
+    if (g_attn_kernel == 1) {
+        switch (hd) {
+            case 64: launch_s3<64>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows); return true;
+            case 128: launch_s3<128>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows); return true;
+            default: return false;
+        }
+    }
     const bool split = g_attn_split;
     switch (hd) {
         case 64:
@@ -694,5 +1263,6 @@ bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, in
 }
 
 void attention_set_split(bool on) { g_attn_split = on; }
+void attention_set_kernel(int k) { g_attn_kernel = k; }
 
 }  // namespace sgc
