@@ -219,6 +219,8 @@ def run_ours(args, rank, world, local_rank):
         ctx.set_option("attn_split", args.attn_split)
     if args.attn_kernel is not None:
         ctx.set_option("attn_kernel", args.attn_kernel)
+    if args.gemm_raster is not None:
+        ctx.set_option("gemm_raster", args.gemm_raster)
     t0 = time.time()
     lm = host.ToyLm(ctx, host.ToyLmConfig(**w.lm, seed=w.seed))
     dg = host.DeviceGraph(ctx, w.graph)
@@ -729,6 +731,8 @@ def main():
     ap.add_argument("--no-split", action="store_true",
                     help="N > 1: whole clusters per GPU only (no member-level rebalancing of skewed clusters)")
     ap.add_argument("--attn-split", type=int, default=None, help="1: two softmax warpgroups per query tile")
+    ap.add_argument("--gemm-raster", type=int, default=None,
+                    help="CTA-pair GEMM raster: 0 M-groups (default), 1 by estimated DRAM bytes, 2 N-groups")
     ap.add_argument("--attn-kernel", type=int, default=None,
                     help="0: two-tile attention kernel, 1/2: double-buffered S with one/two softmax warpgroups")
     ap.add_argument("--gen-steps", type=int, default=2)

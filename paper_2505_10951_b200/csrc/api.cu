@@ -3485,6 +3485,7 @@ int sgc_attention_bf16(sgc_ctx* ctx, const void* q, const void* k_pfx, const voi
 int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value) {
     return guarded([&] {
         if (std::string(name) == "gemm_pairs") sgc::gemm_set_pairs(value != 0);
+        else if (std::string(name) == "gemm_raster") sgc::gemm_set_raster(static_cast<int>(value));
         else if (std::string(name) == "attn_split") sgc::attention_set_split(value != 0);
         else if (std::string(name) == "attn_kernel") sgc::attention_set_kernel(static_cast<int>(value));
         else if (std::string(name) == "gnn_tile") ctx->c.gnn_tile = static_cast<int>(value);

@@ -40,5 +40,7 @@ struct GemmEpi {
 void gemm_bf16(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep);
 // use the CTA-pair (cta_group::2) kernel for 256-wide tiles when M >= 256 (default on)
 void gemm_set_pairs(bool on);
+// CTA-pair GEMM raster: 0 M-groups (default), 1 chosen by estimated DRAM bytes, 2 N-groups
+void gemm_set_raster(int mode);
 
 }  // namespace sgc

@@ -645,7 +645,7 @@ struct Cfg2 {
 template <int EPI, int HD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 int M, int N, int K, GemmEpi ep, int ksplit, uint32_t* sched_ctr) {
+                 int M, int N, int K, GemmEpi ep, int ksplit, uint32_t* sched_ctr, int ngroup) {
     constexpr int BN = 256;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
@@ -709,6 +709,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
     auto tile_coords = [&](int t, int& m0, int& n0) {
         t /= ksplit;
+        if (ngroup > 0) {
+            // N-group raster (host-chosen when it moves fewer DRAM bytes): `ngroup` n-tiles of
+            // the weights stay L2-resident while the group sweeps every m-tile, so the weights
+            // are read once and the activations once per group
+            int per_group = ngroup * m_tiles;
+            int g = t / per_group;
+            int first_n = g * ngroup;
+            int gsize = min(ngroup, n_tiles - first_n);
+            int r = t % per_group;
+            n0 = (first_n + r % gsize) * BN;
+            m0 = (r / gsize) * 2 * BM;
+            return;
+        }
         int per_group = GROUP * n_tiles;
         int g = t / per_group;
         int first_m = g * GROUP;
@@ -853,6 +866,13 @@ void launch(Ctx* c, const void* A, const void* B, int M, int N, int K, const Gem
     SGC_LAUNCH_CHECK(c);
 }
 
+// 0: M-group raster (default), 1: by estimated operand DRAM bytes, 2: N-groups (sgc_set_option
+// "gemm_raster"). Measured at C3 (scripts/gpu_raster_ab.sh): N-groups cut the residual GEMMs' DRAM
+// reads 4.88 -> 3.76 GB per launch but raise QKV / W1 reads 1.54 -> 3.45 GB (the activation rows of
+// the slab's m-tiles do not survive in L2 next to a 64 MB weight slab) and every family ran 1-2%
+// slower, so the M-group raster stays the default.
+int g_gemm_raster = 0;
+
 template <int EPI, int HD>
 void launch2(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep, int ksplit = 1) {
     static bool attr_set = false;
@@ -863,10 +883,25 @@ void launch2(Ctx* c, const void* A, const void* B, int M, int N, int K, const Ge
     }
     CUtensorMap ta = make_map_2d(A, M, K, BM, BK);
     CUtensorMap tb = make_map_2d(B, N, K, BM, BK);
-    int tiles = ((M + 2 * BM - 1) / (2 * BM)) * (N / 256) * ksplit;
+    const int m_tiles = (M + 2 * BM - 1) / (2 * BM), n_tiles = N / 256;
+    int tiles = m_tiles * n_tiles * ksplit;
     int grid = 2 * tiles < c->num_sms ? 2 * tiles : (c->num_sms & ~1);
+    // raster orientation by estimated DRAM bytes for the operands: M-groups (the group's
+    // activation rows resident, weights re-read once per group) or N-groups (a weight slab of
+    // ~kNGroupBytes resident, activations re-read once per slab)
+    int ngroup = 0;
+    if (g_gemm_raster != 0 && m_tiles > 1) {
+        constexpr double kNGroupBytes = 64.0 * (1 << 20);
+        const int mgroup = std::max(2, std::min(32, ((EPI == EPI_RESID ? 48 : 32) << 20) / (2 * BM * K * 2)));
+        const double a = 2.0 * M * K, b = 2.0 * N * K;
+        const int m_groups = (m_tiles + mgroup - 1) / mgroup;
+        const int ng = std::max(1, static_cast<int>(kNGroupBytes / (256.0 * K * 2)));
+        const int n_groups = (n_tiles + ng - 1) / ng;
+        const double traffic_m = a + b * m_groups, traffic_n = a * n_groups + b;
+        if (g_gemm_raster == 2 || traffic_n < 0.9 * traffic_m) ngroup = ng;
+    }
     Ctx::Timed timer(c, gemm_timer_name(ksplit > 1 ? EPI_RESID : EPI));
-    kfn<<<grid, kThreads, Cfg2::kSmem, c->stream>>>(ta, tb, M, N, K, ep, ksplit, c->sched_counter());
+    kfn<<<grid, kThreads, Cfg2::kSmem, c->stream>>>(ta, tb, M, N, K, ep, ksplit, c->sched_counter(), ngroup);
     SGC_LAUNCH_CHECK(c);
 }
 
@@ -966,6 +1001,7 @@ void dispatch_bn(Ctx* c, const void* A, const void* B, int M, int N, int K, cons
 }  // namespace
 
 void gemm_set_pairs(bool on) { g_gemm_pairs = on; }
+void gemm_set_raster(int mode) { g_gemm_raster = mode; }
 
 void gemm_bf16(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
     if (M <= 0) return;
