@@ -159,7 +159,8 @@ def build_report(w, pb, res, paths: dict, cfg_extra: dict | None = None) -> dict
                        "release_ms": float(release),
                        "resident_kv_bytes": plen[c] * L * 2 * d * 2,  # bf16 K/V of the sealed prefix
                        "prefix_tokens": plen[c], "prefix_flop_proxy": proxy(0, plen[c]),
-                       "prefix_digest": 0, "hits": hits[c], "fallbacks": fbs[c]})
+                       "prefix_digest": int(res.prefix_digest[c]) if res.prefix_digest is not None else 0,
+                       "hits": hits[c], "fallbacks": fbs[c]})
         total_prefill += plen[c]
         total_proxy += proxy(0, plen[c])
     n = float(m)
@@ -182,17 +183,16 @@ def build_report(w, pb, res, paths: dict, cfg_extra: dict | None = None) -> dict
     from . import workload as W
 
     config = {"graph_nodes": paths["nodes"], "graph_edges": paths["edges"], "queries": paths["queries"],
-              "undirected": True, "mode": "subgcache", "batch_size": m,
-              "retrieval": {"strategy": "ego-topk", "k": 3, "edge_cost": 0.5, "ego_hops": 2,
-                            "ego_entity_cap": 10},
+              "undirected": bool(w.undirected), "mode": "subgcache", "batch_size": m,
+              "retrieval": dict(w.retrieval),
               "cluster": {"linkage": w.linkage, "count": k},
               "lm": {"layers": L, "heads": H, "model_dim": d, "ffn_hidden": ffn, "max_seq": mx_seq,
                      "max_new": mx_new},
               "effective_seeds": {"lm": w.seed, "gnn": W.splitmix64_once(w.seed ^ 0x62),
-                                  "text_encoder": 1, "hash_salt": 55},
+                                  "text_encoder": w.text_encoder_seed, "hash_salt": w.hash_salt},
               "question_budget": w.question_budget, "seed": w.seed,
-              "soft_prefix": "on" if w.soft_prefix else "off", "answer_lookup": True,
-              "parallel_queries": False, "kernel_backend": "b200-sm100a"}
+              "soft_prefix": "on" if w.soft_prefix else "off", "answer_lookup": bool(w.answer_lookup),
+              "parallel_queries": False, "kernel_backend": "b200-sm100a"}  # one batched GPU pass
     if cfg_extra:
         config.update(cfg_extra)
     return {"schema": "subgcache-report-v1", "mode": "subgcache",

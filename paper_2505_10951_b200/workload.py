@@ -121,6 +121,13 @@ class Workload:
     question_budget: int = 128
     soft_prefix: bool = False
     answer_lookup: bool = True
+    # run settings the reference's report echoes (defaults: RetrievalConfig retrieval.hpp:17-25,
+    # TextEncoder seed / hash_salt encoders.hpp:17-21)
+    retrieval: dict = dataclasses.field(default_factory=lambda: {
+        "strategy": "ego-topk", "k": 3, "edge_cost": 0.5, "ego_hops": 2, "ego_entity_cap": 10})
+    text_encoder_seed: int = 1
+    hash_salt: int = 55
+    undirected: bool = True
 
     def write_dataset(self, d: str):
         os.makedirs(d, exist_ok=True)

@@ -75,6 +75,9 @@ def test_c1_report_matches_reference_run(ctx, tmp_path):
         for k in ("cluster_id", "prefix_tokens", "prefix_flop_proxy", "hits", "fallbacks"):
             assert a[k] == b[k], k
         assert 0 <= a["seal_ms"] <= a["release_ms"]
+        # the sealed prefix's digest (this library's bf16 pages, re-verified after serving)
+        if a["hits"] > 0:
+            assert a["prefix_digest"] != 0
     for k in ("encode_ops", "cluster_ops", "merge_ops"):
         assert rep["cluster_processing"][k] == G["cluster_processing"][k], k
     s = R.compare(G, rep)  # the reference's compare semantics: CPU report vs GPU report
