@@ -736,8 +736,8 @@ __global__ void __launch_bounds__(352, 1)
     uint64_t* p_full = bars + 17;   // [3] per S buffer (P is written over S)
     uint64_t* o_full = bars + 20;   // the tile's last PV completed
     uint64_t* o_free = bars + 21;   // the tile's epilogue read O (the next tile's first PV may run)
-    uint64_t* pv_done = bars + 22;  // [2] PV(g) completed, by block parity (the rare O rescale)
-    uint64_t* s_free = bars + 24;   // [3] PV read the buffer's P: the next S may overwrite it
+    uint64_t* s_free = bars + 24;   // [3] PV(g) completed: S(g+3) may overwrite the buffer's P
+                                    // (also what the rare O rescale of block g+1 waits for)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 28);
     float* m_sh = reinterpret_cast<float*>(bars + 32);  // [2 tile parities][BQ] the rows' running max
     float* lx = m_sh + 2 * BQ;                          // [2 tile parities][BQ] row-sum hand-over
@@ -766,7 +766,6 @@ __global__ void __launch_bounds__(352, 1)
             ptx::mbar_init(&q_empty[i], 1);
             ptx::mbar_init(&k_full[i], 1);
             ptx::mbar_init(&k_empty[i], 1);
-            ptx::mbar_init(&pv_done[i], 1);
         }
         ptx::mbar_init(o_full, 1);
         ptx::mbar_init(o_free, 128);
@@ -929,7 +928,6 @@ __global__ void __launch_bounds__(352, 1)
                         ptx::mma_bf16_ts(tmem_base + C::kO, aP + kk * 8, vd + ((kk * 16 * 128) >> 4), idO,
                                          (b > 0 || kk > 0) ? 1u : 0u);
                     ptx::mma_commit(&v_empty[vs]);
-                    ptx::mma_commit(&pv_done[g & 1]);
                     ptx::mma_commit(&s_free[pbuf]);
                     if (b == nb - 1) ptx::mma_commit(o_full);
                 }
@@ -1077,9 +1075,11 @@ __global__ void __launch_bounds__(352, 1)
                 SPROF(4);
                 const bool resc = m_cur != -INFINITY && mnew > m_cur;
                 if (__any_sync(0xffffffffu, resc)) {
-                    // O holds PV(0 .. g-1) relative to m_cur: rescale once PV(g-1) completed
-                    // (s_full(g) certified PV(g-3); pv_done alternates by block parity)
-                    ptx::mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+                    // O holds PV(0 .. g-1) relative to m_cur: rescale once PV(g-1) completed.
+                    // s_free[(g-1) % 3] phase (g-1)/3: its previous phase (PV(g-4)) is certified
+                    // by s_full(g) (S(g) was issued after PV(g-3)), its next (PV(g+2)) needs this
+                    // warpgroup's P(g+2) -- the parity is unambiguous
+                    ptx::mbar_wait(&s_free[(g - 1) % 3], ((g - 1) / 3) & 1);
                     ptx::tc_fence_after();
                     const float alpha = resc ? ex2_approx(m_cur - mnew) : 1.f;
                     l_w *= alpha;
