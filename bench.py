@@ -504,6 +504,24 @@ def run_ours(args, rank, world, local_rank):
                             "note": "executed = unique states x 2 d^2 (identical in-neighbourhood signatures computed "
                                     "once, the 4 heads folded into one W); reference = every node instance x 4 "
                                     "heads x 2 d^2 (what the CPU reference computes)"}
+        # the same encode with the dedup off (every node instance computed, as on a graph whose
+        # subgraphs share no structure): outside the timed steps, results bit-identical
+        ctx.set_option("gnn_dedup", 0)
+        ctx.set_timing(True)
+        k0 = ctx.kernel_time("gnn_encode")
+        emb_nd = host.encode_subgraphs(ctx, dg, w.retrieved, pb.gnn)
+        torch.cuda.synchronize()
+        k1 = ctx.kernel_time("gnn_encode")
+        rows_nd, _ = ctx.gnn_stats()
+        ctx.set_timing(False)
+        ctx.set_option("gnn_dedup", 1)
+        nd_ms = k1[0] - k0[0]
+        nd_fl = rows_nd * 2.0 * d * d
+        out["embedding"]["dedup_off"] = {
+            "ms": round(nd_ms, 3), "state_rows": rows_nd, "executed_tflop": round(nd_fl / 1e12, 3),
+            "achieved_tflops": round(nd_fl / (nd_ms / 1e3) / 1e12, 2) if nd_ms else None,
+            "frac": round(nd_fl / (nd_ms / 1e3) / 1e12 / fp64, 3) if nd_ms else None,
+            "bit_identical": bool(np.array_equal(emb_nd, host.encode_subgraphs(ctx, dg, w.retrieved, pb.gnn)))}
     except Exception as e:  # noqa: BLE001 -- evidence block only
         out["embedding"] = {"error": str(e)}
     if not args.no_parity:

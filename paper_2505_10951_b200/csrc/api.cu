@@ -1129,6 +1129,7 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
         auto& cand = seen[h];
         uint32_t found = UINT32_MAX;
         for (uint32_t u : cand) {
+            if (!c->gnn_dedup) break;
             uint32_t f = uniq_first[u];
             if (hs.noff[f + 1] - hs.noff[f] == nn && hs.eoff[f + 1] - hs.eoff[f] == ne &&
                 std::equal(hs.nodes.begin() + hs.noff[i], hs.nodes.begin() + hs.noff[i + 1],
@@ -1184,9 +1185,9 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
     {
         std::unordered_map<uint32_t, uint32_t> m0;
         for (size_t v = 0; v < n_inst; ++v) {
-            auto it = m0.find(inst_node[v]);
+            auto it = c->gnn_dedup ? m0.find(inst_node[v]) : m0.end();
             if (it == m0.end()) {
-                it = m0.emplace(inst_node[v], static_cast<uint32_t>(g0_node.size())).first;
+                it = m0.insert_or_assign(inst_node[v], static_cast<uint32_t>(g0_node.size())).first;
                 g0_node.push_back(inst_node[v]);
             }
             gid[v] = it->second;
@@ -1218,7 +1219,7 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
             }
             size_t pos = static_cast<size_t>(h) & (cap - 1);
             uint32_t found = UINT32_MAX;
-            for (; table[pos] != UINT32_MAX; pos = (pos + 1) & (cap - 1)) {
+            for (; c->gnn_dedup && table[pos] != UINT32_MAX; pos = (pos + 1) & (cap - 1)) {
                 const uint32_t ng = table[pos];
                 if (ghash[ng] != h || L.self_row[ng] != gid[v] || L.in_off[ng + 1] - L.in_off[ng] != in.size())
                     continue;
@@ -3489,6 +3490,7 @@ int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value) {
         else if (std::string(name) == "attn_split") sgc::attention_set_split(value != 0);
         else if (std::string(name) == "attn_kernel") sgc::attention_set_kernel(static_cast<int>(value));
         else if (std::string(name) == "gnn_tile") ctx->c.gnn_tile = static_cast<int>(value);
+        else if (std::string(name) == "gnn_dedup") ctx->c.gnn_dedup = value != 0 ? 1 : 0;
         else if (std::string(name) == "decode_defer_pct") ctx->c.decode_defer_pct = static_cast<uint32_t>(std::max<int64_t>(0, value));
         else fail(SGC_DOMAIN, std::string("unknown option ") + name);
     });

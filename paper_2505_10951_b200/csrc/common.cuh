@@ -76,6 +76,10 @@ struct Ctx {
     // last GNN encode: unique node states computed (all layers) / the reference's node instances
     uint64_t gnn_state_rows = 0, gnn_node_instances = 0;
     int gnn_tile = 1;  // GNN layer-map GEMM tile: 0 = 64x64, 1 = 64x128 (measured best at C3), 2 = 128x128
+    // GNN node-state dedup (identical subgraphs / identical per-layer in-neighbourhood signatures
+    // computed once; exact): 0 computes every node instance as the reference does (bench.py
+    // reports the embedding stage both ways)
+    int gnn_dedup = 1;
     cudaStream_t own_stream = nullptr;
     cudaStream_t side = nullptr;  // overlapped side work (sealed-prefix digests), created on first use
     cudaStream_t side_stream() {

@@ -288,6 +288,25 @@ def test_text_features_and_gnn_vs_reference(ctx, scene, dim):
     assert np.abs(emb - exp).max() <= 1e-6
 
 
+def test_gnn_dedup_is_exact(ctx, scene):
+    """The node-state dedup (identical subgraphs / per-layer signatures computed once) changes no
+    bit of the embeddings: every node instance computed (gnn_dedup 0) gives the same floats, and
+    computes more state rows."""
+    G, g, dg = scene
+    subs = [sub_of(s) for s in G["subgraphs"][:30]] * 2  # duplicates on purpose
+    cfg = host.GnnEncoderConfig(2, 4, 128, 11)
+    on = host.encode_subgraphs(ctx, dg, subs, cfg)
+    rows_on, inst = ctx.gnn_stats()
+    ctx.set_option("gnn_dedup", 0)
+    try:
+        off = host.encode_subgraphs(ctx, dg, subs, cfg)
+        rows_off, inst_off = ctx.gnn_stats()
+    finally:
+        ctx.set_option("gnn_dedup", 1)
+    assert np.array_equal(on, off)
+    assert inst_off == inst and rows_off == inst and rows_on < rows_off
+
+
 def test_gnn_empty_subgraph_is_domain_error(ctx, scene):
     G, g, dg = scene
     with pytest.raises(host.DomainError):
