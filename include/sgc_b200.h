@@ -387,8 +387,9 @@ int sgc_attention_bf16(sgc_ctx* ctx, const void* q, const void* k_pfx, const voi
                        uint32_t pfx_rows, const void* k_loc, const void* v_loc, const int32_t* seg_lo,
                        const int32_t* work, uint32_t n_work, uint32_t rows, uint32_t d, uint32_t heads,
                        void* out);
-/* Measured FP64 FMA throughput of the context's device (TFLOP/s): the GNN layer map's roofline
- * denominator (bench.py). */
+/* Measured FP64 throughput of the context's device (TFLOP/s): the larger of the FMA pipe (DFMA
+ * chains) and the FP64 tensor pipe (DMMA chains) -- the GNN layer map's roofline denominator
+ * (bench.py). */
 int sgc_probe_fp64_tflops(sgc_ctx* ctx, double* tflops);
 /* Work of the context's last GNN encode: unique node states computed over all layers (identical
  * in-neighbourhood signatures are computed once) and the reference's node instances x layers. */

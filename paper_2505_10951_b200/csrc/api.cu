@@ -3503,7 +3503,10 @@ int sgc_gnn_stats(const sgc_ctx* ctx, uint64_t* state_rows, uint64_t* node_insta
 }
 
 int sgc_probe_fp64_tflops(sgc_ctx* ctx, double* tflops) {
-    return guarded([&] { *tflops = sgc::fp64_probe_tflops(current(&ctx->c)); });
+    return guarded([&] {
+        sgc::Ctx* c = current(&ctx->c);
+        *tflops = std::max(sgc::fp64_probe_tflops(c), sgc::dmma_probe_tflops(c));
+    });
 }
 
 int sgc_set_timing(sgc_ctx* ctx, int enable) {

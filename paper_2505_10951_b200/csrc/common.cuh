@@ -75,7 +75,7 @@ struct Ctx {
     uint32_t decode_defer_pct = 25;
     // last GNN encode: unique node states computed (all layers) / the reference's node instances
     uint64_t gnn_state_rows = 0, gnn_node_instances = 0;
-    int gnn_tile = 1;  // GNN layer-map GEMM tile: 0 = 64x64, 1 = 64x128 (measured best at C3), 2 = 128x128
+    int gnn_tile = 3;  // GNN layer-map GEMM: DFMA register tiles 0 = 64x64, 1 = 64x128, 2 = 128x128; 3 = DMMA (FP64 tensor pipe)
     // GNN node-state dedup (identical subgraphs / identical per-layer in-neighbourhood signatures
     // computed once; exact): 0 computes every node instance as the reference does (bench.py
     // reports the embedding stage both ways)

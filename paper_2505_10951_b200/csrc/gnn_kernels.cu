@@ -8,6 +8,8 @@
 //   layer map : s'[v] = tanh((Wbar . agg[v]) / heads), Wbar = sum_h W_h folded once in fp64
 //               (register-tiled DFMA GEMM over [instances x dim] . [dim x dim]^T)
 //   pool      : mean over v (ascending node id), L2 normalize (sequential), cast to float
+#include <atomic>
+
 #include "common.cuh"
 #include "gnn_kernels.cuh"
 #include "rng.cuh"
@@ -145,6 +147,122 @@ __global__ void __launch_bounds__(256)
         }
 }
 
+// ---- the layer map on the FP64 tensor cores (DMMA, mma.sync m16n8k4 .f64): one instruction is
+// 512 FMAs instead of DFMA's 32, so the operand traffic and the issue slots per FLOP drop 16x.
+// CTA tile 64 instances x 128 outputs, 8 warps of 32 x 32 (2 m16 x 4 n8 accumulators, 32 doubles
+// per thread); K in chunks of 16 through a 3-stage cp.async ring, rows padded to 20 doubles so the
+// fragment loads (8 rows x 4 k per half warp) hit 32 distinct banks. Accumulation per output in
+// ascending k (fp64 fused multiply-add), then tanh(acc / heads) as in the DFMA kernel.
+constexpr int DM_TM = 64, DM_TN = 128, DM_KC = 16, DM_LD = 20, DM_STAGES = 3;
+constexpr int DM_STAGE_DOUBLES = (DM_TM + DM_TN) * DM_LD;
+constexpr int DM_SMEM = DM_STAGES * DM_STAGE_DOUBLES * 8;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void dmma_16x8x4(double (&c)[4], double a0, double a1, double b0) {
+    asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                 : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+                 : "d"(a0), "d"(a1), "d"(b0));
+}
+
+__global__ void __launch_bounds__(256, 2)
+    gnn_layer_dmma(double* out, const double* A, const double* W, int n_inst, int d, double inv_heads) {
+    extern __shared__ __align__(16) double dsm[];
+    const int v0 = blockIdx.x * DM_TM, r0 = blockIdx.y * DM_TN;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const int wm = warp / 4, wn = warp % 4;  // warp tile rows [wm*32, +32), cols [wn*32, +32)
+    const int g = lane / 4, t = lane % 4;
+    double acc[2][4][4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+    const int nk = d / DM_KC;
+    // stage s: A rows [0, 64) then W rows [64, 192), each DM_LD doubles (16 used)
+    auto load = [&](int kc, int st) {
+        double* base = dsm + st * DM_STAGE_DOUBLES;
+        const int k0 = kc * DM_KC;
+        // 192 rows x 8 16-byte chunks = 1536 chunks over 256 threads
+#pragma unroll
+        for (int it = 0; it < 6; ++it) {
+            const int ch = threadIdx.x + 256 * it;
+            const int row = ch / 8, part = ch % 8;
+            if (row < DM_TM) {
+                const int v = v0 + row;
+                const bool ok = v < n_inst;
+                cp_async16(base + row * DM_LD + part * 2, A + static_cast<size_t>(ok ? v : 0) * d + k0 + part * 2, ok);
+            } else {
+                const int r = r0 + row - DM_TM;
+                const bool ok = r < d;
+                cp_async16(base + row * DM_LD + part * 2, W + static_cast<size_t>(ok ? r : 0) * d + k0 + part * 2, ok);
+            }
+        }
+    };
+#pragma unroll
+    for (int s2 = 0; s2 < DM_STAGES - 1; ++s2) {
+        if (s2 < nk) load(s2, s2);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    for (int kc = 0; kc < nk; ++kc) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(DM_STAGES - 2) : "memory");
+        __syncthreads();
+        if (kc + DM_STAGES - 1 < nk) load(kc + DM_STAGES - 1, (kc + DM_STAGES - 1) % DM_STAGES);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const double* As = dsm + (kc % DM_STAGES) * DM_STAGE_DOUBLES;
+        const double* Bs = As + DM_TM * DM_LD;
+#pragma unroll
+        for (int k4 = 0; k4 < DM_KC; k4 += 4) {
+            double a[2][2], b[4];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                a[i][0] = As[(wm * 32 + i * 16 + g) * DM_LD + k4 + t];
+                a[i][1] = As[(wm * 32 + i * 16 + g + 8) * DM_LD + k4 + t];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Bs[(wn * 32 + j * 8 + g) * DM_LD + k4 + t];
+#pragma unroll
+            for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_16x8x4(acc[i][j], a[i][0], a[i][1], b[j]);
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    // C fragment: element e of tile (i, j) is row g + 8 (e / 2), col 2 t + (e % 2)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int v = v0 + wm * 32 + i * 16 + g + 8 * (e / 2);
+                const int r = r0 + wn * 32 + j * 8 + 2 * t + (e % 2);
+                if (v < n_inst && r < d) out[static_cast<size_t>(v) * d + r] = tanh(acc[i][j][e] * inv_heads);
+            }
+}
+
+// FP64 tensor (DMMA) throughput probe: independent m16n8k4 chains, no memory traffic
+__global__ void __launch_bounds__(256) dmma_probe_kernel(double* sink, int iters) {
+    double c[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c[i][e] = 1e-9 * (threadIdx.x + i + e);
+    const double a0 = 0.999999999, a1 = 1e-9, b = 0.5;
+    for (int it = 0; it < iters; ++it)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) dmma_16x8x4(c[i], a0, a1, b);
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s += c[i][e];
+    if (s == 12345.0) sink[0] = s;
+}
+
 // mean-pool over the subgraph's node states (ascending node id), sequential L2 norm, cast
 // (encoders.cpp:170-185); rows index the last layer's unique states
 __global__ void gnn_pool_kernel(float* out, const double* state, const uint32_t* sub_off,
@@ -221,6 +339,16 @@ void gnn_encode_layers(Ctx* c, const GnnPlan& p) {
         SGC_LAUNCH_CHECK(c);
         const double* wl = p.wbar + static_cast<size_t>(l) * d * d;
         switch (c->gnn_tile) {
+            case 3: {
+                static std::atomic<uint64_t> attr_devices{0};
+                if (!(attr_devices.load() >> c->device & 1)) {
+                    SGC_CUDA_CHECK(cudaFuncSetAttribute(gnn_layer_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, DM_SMEM));
+                    attr_devices |= 1ull << c->device;
+                }
+                dim3 grid(ceil_div(L.n_out, DM_TM), ceil_div(d, DM_TN));
+                gnn_layer_dmma<<<grid, 256, DM_SMEM, c->stream>>>(next, p.agg, wl, L.n_out, d, 1.0 / p.heads);
+                break;
+            }
             case 2: {
                 dim3 grid(ceil_div(L.n_out, 128), ceil_div(d, 128));
                 gnn_layer_gemm<128, 128><<<grid, 256, 0, c->stream>>>(next, p.agg, wl, L.n_out, d, 1.0 / p.heads);
@@ -267,6 +395,29 @@ double fp64_probe_tflops(Ctx* c) {
     c->event_pool.push_back(e0);
     c->event_pool.push_back(e1);
     return 2.0 * blocks * 256.0 * iters * 8 / (best * 1e-3) / 1e12;
+}
+
+double dmma_probe_tflops(Ctx* c) {
+    double* sink = c->buf<double>("fp64_probe", 1);
+    const int blocks = c->num_sms * 8, iters = 2048;
+    cudaEvent_t e0 = c->event(), e1 = c->event();
+    dmma_probe_kernel<<<blocks, 256, 0, c->stream>>>(sink, iters);  // warm-up (clocks up)
+    SGC_LAUNCH_CHECK(c);
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        SGC_CUDA_CHECK(cudaEventRecord(e0, c->stream));
+        dmma_probe_kernel<<<blocks, 256, 0, c->stream>>>(sink, iters);
+        SGC_LAUNCH_CHECK(c);
+        SGC_CUDA_CHECK(cudaEventRecord(e1, c->stream));
+        SGC_CUDA_CHECK(cudaEventSynchronize(e1));
+        float ms = 0;
+        SGC_CUDA_CHECK(cudaEventElapsedTime(&ms, e0, e1));
+        best = std::min(best, ms);
+    }
+    c->event_pool.push_back(e0);
+    c->event_pool.push_back(e1);
+    // 4 chains x m16n8k4 (512 FMA = 1024 FLOP) per warp per iteration
+    return 1024.0 * 4 * (blocks * 256.0 / 32) * iters / (best * 1e-3) / 1e12;
 }
 
 void gather_rows(Ctx* c, float* out, const float* src, const uint32_t* idx, int n, int d) {

@@ -37,4 +37,6 @@ void gnn_encode_layers(Ctx* c, const GnnPlan& p);
 void gather_rows(Ctx* c, float* out, const float* src, const uint32_t* idx, int n, int d);
 // measured FP64 FMA throughput of this device (TFLOP/s, best of 5 short launches)
 double fp64_probe_tflops(Ctx* c);
+// the same for the FP64 tensor pipe (DMMA m16n8k4 chains)
+double dmma_probe_tflops(Ctx* c);
 }  // namespace sgc
