@@ -431,7 +431,7 @@ def run_ours(args, rank, world, local_rank):
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     gemm_tf = (gemm_f * args.steps) / (gemm_ms / 1e3) / 1e12 if gemm_ms else 0.0
     prof = None
-    prof_path = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
+    prof_path = os.path.join(ROOT, "profiles", "r02_gemm_traffic.json")
     if os.path.exists(prof_path):
         with open(prof_path) as f:
             prof = json.load(f).get(args.config)
