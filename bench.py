@@ -416,15 +416,16 @@ def run_ours(args, rank, world, local_rank):
                                              [members_q[q] for q in mine_q], [labels[q] for q in mine_q],
                                              all_prefix=prefix_lens)
     fam_ms = {k: kt[k][0] for k in fam_f}
+    attn_tot_ms = kt["attention"][0]
     if world > 1:
         keys = sorted(fam_f)
-        t = torch.tensor([gemm_f, attn_f, head_f, gemm_ms, float(gemm_n)] + [fam_f[k] for k in keys] +
+        t = torch.tensor([gemm_f, attn_f, head_f, gemm_ms, float(gemm_n), attn_tot_ms] + [fam_f[k] for k in keys] +
                          [fam_ms[k] for k in keys], dtype=torch.float64, device=COLL_DEV)
         pg.all_reduce(t)
         v = t.cpu().tolist()
-        gemm_f, attn_f, head_f, gemm_ms, gemm_n = v[:5]
-        fam_f = dict(zip(keys, v[5:5 + len(keys)]))
-        fam_ms = dict(zip(keys, v[5 + len(keys):]))
+        gemm_f, attn_f, head_f, gemm_ms, gemm_n, attn_tot_ms = v[:6]
+        fam_f = dict(zip(keys, v[6:6 + len(keys)]))
+        fam_ms = dict(zip(keys, v[6 + len(keys):]))
     if rank != 0:
         return None
     peaks, pk_kind = load_peaks()
@@ -475,6 +476,13 @@ def run_ours(args, rank, world, local_rank):
         "kernel_ms_per_step": {k: round(v[0] / args.steps, 3) for k, v in kt.items() if v[1]},
         "gpu_idle_ms_per_step": round(ms_per_step - sum(v[0] for v in kt.values()) / args.steps, 3),
         "step_tflops": round(step_tf, 2), "step_tensor_frac": round(step_tf / peak, 4),
+        # the second kernel family: member / representative attention (tcgen05), algorithmic FLOPs
+        # (4 d (S P + S(S+1)/2) per member per layer, 2 d P(P+1) per representative) over its time
+        "attention_roofline": ({"achieved": round(attn_f * args.steps / (attn_tot_ms / 1e3) / 1e12, 2),
+                                "peak": peak, "unit": "TFLOP/s",
+                                "frac": round(attn_f * args.steps / (attn_tot_ms / 1e3) / 1e12 / peak, 4),
+                                "kernel": "attn_s3_kernel (tcgen05)", "ms_per_step": round(attn_tot_ms / args.steps, 3)}
+                               if attn_tot_ms else None),
         "gemm_families": gemm_families,
         "roofline": roofline,
         "e2e": e2e,

@@ -962,6 +962,7 @@ __global__ void __launch_bounds__(352, 1)
             __syncwarp();
             if (lane == 0) sched::release(ring, k);
             if (iu >= static_cast<uint32_t>(n_items)) break;
+            SPROF(7);
             const bool valid = r < t.nrows;
             const int row = t.w.row0 + t.x * BQ + r;
             const int seg = valid && !partial ? p.seg_lo[row] : 0x7fffffff;

@@ -38,10 +38,10 @@ def main():
     per = buf.reshape(148, 32).astype(np.float64).mean(0)
     if os.environ.get("SGC_ATTN_KERNEL", "1") == "1":
         names = ["top / item", "wait s_full", "S ld + mask + max", "token wait + decision", "exponentials",
-                 "rescale + P store + arrive", "epilogue"]
+                 "rescale + P store + arrive", "epilogue", "tile ring wait"]
         print(f"attention {ctx.kernel_time('attention')[0]:.1f} ms; mean cycles per CTA:")
         for w in range(2):
-            print(f"  warpgroup {w}: sum {per[8 * w:8 * w + 7].sum() / 1e6:.2f} Mcyc")
+            print(f"  warpgroup {w}: sum {per[8 * w:8 * w + 8].sum() / 1e6:.2f} Mcyc")
             for i, nm in enumerate(names):
                 print(f"    {nm:28s} {per[8 * w + i] / 1e6:10.2f} Mcyc")
         for i, nm in zip(range(16, 28), ["mma: k_full", "mma: v_full", "mma: p_full", "mma: o_free", "mma: q_full", "mma: s_free", "-", "-",
