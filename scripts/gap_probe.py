@@ -22,9 +22,14 @@ def main():
         host.run_subgcache(ctx, lm, dg, pb, want_logits=False, device_inputs=True, waves=2)
     torch.cuda.synchronize()
     from torch.profiler import ProfilerActivity, profile
-    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         host.run_subgcache(ctx, lm, dg, pb, want_logits=False, device_inputs=True, waves=2)
         torch.cuda.synchronize()
+    api = sorted(((e.time_range.end - e.time_range.start, e.name) for e in prof.events()
+                  if e.device_type.name == "CPU" and e.name.startswith("cuda")), reverse=True)
+    print("longest CUDA runtime calls (host):")
+    for dur, nm in api[:12]:
+        print(f"  {dur / 1e3:8.3f} ms  {nm}")
     ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
     ks = sorted(((e.time_range.start, e.time_range.end, e.name) for e in ev), key=lambda t: t[0])
     print("events", len(ks))
