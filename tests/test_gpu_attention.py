@@ -114,6 +114,29 @@ def test_cascade_attention_vs_torch_fp32(ctx, hd, heads, clusters, prefill):
     assert bad == 0, f"{bad} elements out of tolerance, max |d| {err.max().item():.4f}"
 
 
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_both_tcgen05_kernels_agree(ctx, kernel):
+    """attn_kernel 0 (two 128-row tiles per item) and 1 (one tile, S triple-buffered; the default)
+    against the same fp32 reference on a C3-like member case."""
+    hd, heads, clusters = 128, 8, 4
+    rng = np.random.default_rng(99)
+    pfx = [int(x) for x in rng.integers(1500, 2200, size=clusters)]
+    members = [int(x) for x in rng.integers(20, 60, size=clusters)]
+    (q, kp, vp, kl, vl), seg, groups, rows, pfx_rows, d = _case(11, heads, hd, clusters, pfx, members, (30, 64), False)
+    work = _units(groups, 256)
+    out = torch.zeros(rows, d, device="cuda", dtype=torch.bfloat16)
+    ctx.set_option("attn_kernel", kernel)
+    try:
+        torch.cuda.synchronize()
+        ctx.attention(q.data_ptr(), kp.data_ptr(), vp.data_ptr(), pfx_rows, kl.data_ptr(), vl.data_ptr(),
+                      seg.data_ptr(), work, rows, d, heads, out.data_ptr())
+    finally:
+        ctx.set_option("attn_kernel", 1)
+    ref = _reference(q, kp, vp, kl, vl, seg, groups, heads)
+    err = (out.float() - ref).abs()
+    assert (err > 2e-2 + 2e-2 * ref.abs()).sum().item() == 0, f"max |d| {err.max().item():.4f}"
+
+
 def test_cascade_attention_work_validation(ctx):
     from paper_2505_10951_b200._lib import DomainError
 
