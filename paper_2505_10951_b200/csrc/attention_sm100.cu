@@ -49,6 +49,9 @@ constexpr int kVStages = 2;
 #ifndef SGC_LAZY_MAX
 #define SGC_LAZY_MAX 8.f
 #endif
+#ifndef SGC_S3_VFIRST
+#define SGC_S3_VFIRST 0
+#endif
 #ifndef SGC_S3_TOKEN_LATE
 #define SGC_S3_TOKEN_LATE 0
 #endif
@@ -866,10 +869,17 @@ __global__ void __launch_bounds__(352, 1)
                 ++vb;
                 ++gv;
             };
+            // K(0), K(1), then K(g+2), V(g) (SGC_S3_VFIRST=1: V(g) first -- V(g) is due at PV(g),
+            // K(g+2) at S(g+2); measured slower at C3, scripts/gpu_attn_ab.sh)
             bool more = next_k() && next_k();
             while (more || gv < gk) {
+#if SGC_S3_VFIRST
+                if (gv < gk) next_v();
+                if (more) more = next_k();
+#else
                 if (more) more = next_k();
                 if (gv < gk) next_v();
+#endif
             }
         }
     } else if (warp == 1 || warp == 10) {
