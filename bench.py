@@ -481,7 +481,7 @@ def run_ours(args, rank, world, local_rank):
         "attention_roofline": ({"achieved": round(attn_f * args.steps / (attn_tot_ms / 1e3) / 1e12, 2),
                                 "peak": peak, "unit": "TFLOP/s",
                                 "frac": round(attn_f * args.steps / (attn_tot_ms / 1e3) / 1e12 / peak, 4),
-                                "kernel": "attn_s3_kernel (tcgen05)", "ms_per_step": round(attn_tot_ms / args.steps, 3)}
+                                "kernel": "attn_tc_kernel (tcgen05)", "ms_per_step": round(attn_tot_ms / args.steps, 3)}
                                if attn_tot_ms else None),
         "gemm_families": gemm_families,
         "roofline": roofline,
@@ -760,7 +760,7 @@ def main():
     ap.add_argument("--gemm-raster", type=int, default=None,
                     help="CTA-pair GEMM raster: 0 M-groups (default), 1 by estimated DRAM bytes, 2 N-groups")
     ap.add_argument("--attn-kernel", type=int, default=None,
-                    help="0: two-tile attention kernel, 1/2: double-buffered S with one/two softmax warpgroups")
+                    help="0: two-tile attention kernel (default), 1: one-tile kernel with S triple-buffered")
     ap.add_argument("--gen-steps", type=int, default=2)
     ap.add_argument("--gen-waves", type=int, default=2,
                     help="waves of the generation run (cost-balanced cuts; scripts/defer_probe.py: "

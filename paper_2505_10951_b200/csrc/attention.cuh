@@ -51,8 +51,8 @@ bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, in
 inline bool attention_tc_supported(int hd) { return hd == 64 || hd == 128; }
 // split every S row over two softmax warpgroups, or one thread per row (default)
 void attention_set_split(bool on);
-// 0: two 128-row tiles per item (attn_tc_kernel); 1: one tile, S triple-buffered, two softmax
-// warpgroups on alternate key blocks (attn_s3_kernel, default)
+// 0: two 128-row tiles per item (attn_tc_kernel, default); 1: one tile, S triple-buffered, two
+// softmax warpgroups on alternate key blocks (attn_s3_kernel)
 void attention_set_kernel(int k);
 
 // Decode step (attention.cu): merge the prefix partial (part_o, part_lse from the tcgen05 kernel

@@ -325,30 +325,43 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
         }
     } else if (warp == 1) {
         if (lane == 0) {
+#ifdef SGC_ATTN_PROF
+            // MMA thread: cycles in each wait (slots 16..19) and in total (slot 22)
+            const long long t_mma0 = clock64();
+            auto mwait = [&](uint64_t* bar, uint32_t par, int slot) {
+                const long long t0 = clock64();
+                ptx::mbar_wait(bar, par);
+                atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 32 + slot], (unsigned long long)(clock64() - t0));
+            };
+#else
+            auto mwait = [&](uint64_t* bar, uint32_t par, int) { ptx::mbar_wait(bar, par); };
+#endif
             constexpr uint32_t idS = ptx::idesc_bf16_f32(BQ, BKV);
             constexpr uint32_t idO = ptx::idesc_bf16_f32_bmn(BQ, HD);
             uint32_t g = 0, gx[2] = {0, 0}, qit[2] = {0, 0};
+            // descriptors built once per operand tile, then advanced by constants (the start
+            // address field is bytes >> 4): fewer dependent instructions per tcgen05.mma for the
+            // single issuing thread, which was busy ~70% of the kernel (scripts/attn_prof.py)
             auto issue_s = [&](int x, uint32_t kg) {  // S_X = Q_X K^T
-                const uint32_t q_addr = ptx::smem_u32(sQ + x * C::kQBytes);
-                const uint32_t k_addr = ptx::smem_u32(sK + (kg % kKStages) * C::kKBytes);
+                const uint64_t qd = ptx::umma_desc_sw128(ptx::smem_u32(sQ + x * C::kQBytes));
+                const uint64_t kd = ptx::umma_desc_sw128(ptx::smem_u32(sK + (kg % kKStages) * C::kKBytes));
+                const uint32_t dS = tmem_base + C::kS + x * BQ;
 #pragma unroll
                 for (int kc = 0; kc < HD / 16; ++kc) {
-                    uint64_t ad = ptx::umma_desc_sw128(q_addr + (kc / 4) * (BQ * 128) + (kc % 4) * 32);
-                    uint64_t bd = ptx::umma_desc_sw128(k_addr + (kc / 4) * (BKV * 128) + (kc % 4) * 32);
-                    ptx::mma_bf16(tmem_base + C::kS + x * BQ, ad, bd, idS, kc > 0 ? 1u : 0u);
+                    const uint64_t ad = qd + (((kc / 4) * (BQ * 128) + (kc % 4) * 32) >> 4);
+                    const uint64_t bd = kd + (((kc / 4) * (BKV * 128) + (kc % 4) * 32) >> 4);
+                    ptx::mma_bf16(dS, ad, bd, idS, kc > 0 ? 1u : 0u);
                 }
                 ptx::mma_commit(&s_full[x]);
             };
             auto issue_pv = [&](int x, uint32_t kg, bool first) {  // O_X += P_X V
-                ptx::mbar_wait(&p_full[x], gx[x] & 1);
+                mwait(&p_full[x], gx[x] & 1, 18);
                 ptx::tc_fence_after();
-                const uint32_t v_addr = ptx::smem_u32(sV + (kg & 1) * C::kVBytes);
+                const uint64_t vd = ptx::umma_desc_sw128_lbo(ptx::smem_u32(sV + (kg & 1) * C::kVBytes), BKV * 128, 1024);
+                const uint32_t dO = tmem_base + C::kO + x * 128, aP = tmem_base + C::kS + x * BQ;
 #pragma unroll
-                for (int kk = 0; kk < BKV / 16; ++kk) {
-                    uint64_t bd = ptx::umma_desc_sw128_lbo(v_addr + kk * 16 * 128, BKV * 128, 1024);
-                    ptx::mma_bf16_ts(tmem_base + C::kO + x * 128, tmem_base + C::kS + x * BQ + kk * 8, bd,
-                                     idO, (!first || kk > 0) ? 1u : 0u);
-                }
+                for (int kk = 0; kk < BKV / 16; ++kk)
+                    ptx::mma_bf16_ts(dO, aP + kk * 8, vd + ((kk * 16 * 128) >> 4), idO, (!first || kk > 0) ? 1u : 0u);
                 ++gx[x];
             };
             for (uint32_t k = 0;; ++k) {
@@ -359,23 +372,23 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 if (iu >= static_cast<uint32_t>(n_items)) break;
                 const int nbu = max(u.nb[0], u.nb[1]);
                 for (int x = 0; x < 2; ++x)
-                    if (u.nb[x]) ptx::mbar_wait(&q_full[x], qit[x] & 1);
+                    if (u.nb[x]) mwait(&q_full[x], qit[x] & 1, 19);
                 // prologue: S(0) of both tiles
-                ptx::mbar_wait(&k_full[g % kKStages], (g / kKStages) & 1);
+                mwait(&k_full[g % kKStages], (g / kKStages) & 1, 16);
                 ptx::tc_fence_after();
                 for (int x = 0; x < 2; ++x)
                     if (u.nb[x]) issue_s(x, g);
                 ptx::mma_commit(&k_empty[g % kKStages]);
                 for (int j = 0; j < nbu; ++j) {
                     const uint32_t kg = g + j;
-                    ptx::mbar_wait(&v_full[kg & 1], (kg >> 1) & 1);
+                    mwait(&v_full[kg & 1], (kg >> 1) & 1, 17);
                     bool waited_next_k = false;
                     for (int x = 0; x < 2; ++x) {
                         if (j >= u.nb[x]) continue;
                         issue_pv(x, kg, j == 0);
                         if (j + 1 < u.nb[x]) {
                             if (!waited_next_k) {
-                                ptx::mbar_wait(&k_full[(kg + 1) % kKStages], ((kg + 1) / kKStages) & 1);
+                                mwait(&k_full[(kg + 1) % kKStages], ((kg + 1) / kKStages) & 1, 16);
                                 ptx::tc_fence_after();
                                 waited_next_k = true;
                             }
@@ -392,6 +405,9 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 for (int x = 0; x < 2; ++x)
                     if (u.nb[x]) ++qit[x];
             }
+#ifdef SGC_ATTN_PROF
+            atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 32 + 22], (unsigned long long)(clock64() - t_mma0));
+#endif
         }
     } else {
         // softmax warps: tile x = 0 (A) / 1 (B); with SPLIT = 2 each tile has two warpgroups,
@@ -1184,8 +1200,10 @@ __global__ void __launch_bounds__(352, 1)
     }
 }
 
-// 0: two-tile kernel (attn_tc_kernel), 1: attn_s3_kernel (sgc_set_option "attn_kernel")
-int g_attn_kernel = 1;
+// 0: two-tile kernel (attn_tc_kernel, default), 1: attn_s3_kernel (sgc_set_option "attn_kernel").
+// Same-box A/B at C3 (scripts/gpu_attn_ab.sh): 112.4 / 112.3 vs 115.8 / 115.8 ms per step once the
+// two-tile kernel's MMA thread built its descriptors once per operand tile (it was 115.6-118)
+int g_attn_kernel = 0;
 
 template <int HD>
 void launch_s3(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, int pfx_rows, int loc_rows) {

@@ -49,6 +49,8 @@ def main():
             if nm != "-":
                 print(f"  {nm:30s} {per[i] / 1e6:10.2f} Mcyc")
         return
+    for i, nm in zip((16, 17, 18, 19, 22), ("mma: k_full", "mma: v_full", "mma: p_full", "mma: q_full", "mma: loop total")):
+        print(f"  {nm:26s} {per[i] / 1e6:10.2f} Mcyc")
     tot = per[:9].sum()
     print(f"attention {ms:.1f} ms over {n} launches; mean cycles per CTA (all launches):")
     for i, nm in enumerate(NAMES):

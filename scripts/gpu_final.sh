@@ -14,7 +14,7 @@ B="python bench.py --steps 1 --warmup 0 --no-cpu --no-e2e --no-gen --no-parity -
 timeout -s KILL 900 ncu $N -k regex:'gemm2_kernel<.int.3' -s 32 -c 1 -o gpurun_out/prof_tanh $B > /dev/null 2>&1; echo "tanh rc=$?"
 timeout -s KILL 900 ncu $N -k regex:'gemm2_kernel<.int.4' -s 32 -c 1 -o gpurun_out/prof_qkv $B > /dev/null 2>&1; echo "qkv rc=$?"
 timeout -s KILL 900 ncu $N -k regex:'gemm2_kernel<.int.2' -s 64 -c 1 -o gpurun_out/prof_resid $B > /dev/null 2>&1; echo "resid rc=$?"
-timeout -s KILL 900 ncu $N -k regex:attn_s3 -s 40 -c 1 -o gpurun_out/prof_attn_k1 $B > /dev/null 2>&1; echo "attn rc=$?"
+timeout -s KILL 900 ncu $N -k regex:attn_tc -s 40 -c 1 -o gpurun_out/prof_attn_k1 $B > /dev/null 2>&1; echo "attn rc=$?"
 timeout -s KILL 600 ncu $N -k regex:gnn_layer_dmma -s 1 -c 1 -o gpurun_out/prof_gnn_dmma python scripts/prof_embed.py > /dev/null 2>&1; echo "gnn rc=$?"
 python - <<'P'
 import json
