@@ -7,6 +7,7 @@
 //   cache_engine.cpp:140-233 process_cluster / run_batch -> sgc_prefill + sgc_extend
 //   lm_core.cpp:179-297 ToyLm::forward (token-sequential)  -> forward_rows (row-batched)
 #include <algorithm>
+#include <cstdlib>
 #include <deque>
 #include <set>
 #include <chrono>
@@ -238,6 +239,8 @@ void pool_grow(Ctx* c, sgc_model* m, uint32_t need) {
                                std::to_string((static_cast<size_t>(want) * pb) >> 20) +
                                " MiB) do not fit in free device memory");
     const size_t row_elems = static_cast<size_t>(sgc::kPageTokens) * m->d;
+    static const bool trace = std::getenv("SGC_TRACE_POOL") != nullptr;
+    if (trace) std::fprintf(stderr, "[sgc] KV pool grow: %u -> %u pages (need %u, %zu MiB per page)\n", p.pages, want, need, pb >> 20);
     bf16 *nk = nullptr, *nv = nullptr;
     const size_t bytes = static_cast<size_t>(want) * row_elems * m->L * sizeof(bf16);
     SGC_CUDA_CHECK(cudaMallocAsync(&nk, bytes, c->stream));

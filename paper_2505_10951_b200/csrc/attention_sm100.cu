@@ -324,14 +324,16 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
+        // the whole warp runs the issue loop (warp-uniform operands -> uniform datapath); one
+        // elected lane issues each tcgen05.mma / commit
+        {
 #ifdef SGC_ATTN_PROF
             // MMA thread: cycles in each wait (slots 16..19) and in total (slot 22)
             const long long t_mma0 = clock64();
             auto mwait = [&](uint64_t* bar, uint32_t par, int slot) {
                 const long long t0 = clock64();
                 ptx::mbar_wait(bar, par);
-                atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 32 + slot], (unsigned long long)(clock64() - t0));
+                if (lane == 0) atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 32 + slot], (unsigned long long)(clock64() - t0));
             };
 #else
             auto mwait = [&](uint64_t* bar, uint32_t par, int) { ptx::mbar_wait(bar, par); };
@@ -350,9 +352,9 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 for (int kc = 0; kc < HD / 16; ++kc) {
                     const uint64_t ad = qd + (((kc / 4) * (BQ * 128) + (kc % 4) * 32) >> 4);
                     const uint64_t bd = kd + (((kc / 4) * (BKV * 128) + (kc % 4) * 32) >> 4);
-                    ptx::mma_bf16(dS, ad, bd, idS, kc > 0 ? 1u : 0u);
+                    ptx::mma_bf16_elect(dS, ad, bd, idS, kc > 0 ? 1u : 0u);
                 }
-                ptx::mma_commit(&s_full[x]);
+                ptx::mma_commit_elect(&s_full[x]);
             };
             auto issue_pv = [&](int x, uint32_t kg, bool first) {  // O_X += P_X V
                 mwait(&p_full[x], gx[x] & 1, 18);
@@ -361,14 +363,15 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 const uint32_t dO = tmem_base + C::kO + x * 128, aP = tmem_base + C::kS + x * BQ;
 #pragma unroll
                 for (int kk = 0; kk < BKV / 16; ++kk)
-                    ptx::mma_bf16_ts(dO, aP + kk * 8, vd + ((kk * 16 * 128) >> 4), idO, (!first || kk > 0) ? 1u : 0u);
+                    ptx::mma_bf16_ts_elect(dO, aP + kk * 8, vd + ((kk * 16 * 128) >> 4), idO, (!first || kk > 0) ? 1u : 0u);
                 ++gx[x];
             };
             for (uint32_t k = 0;; ++k) {
                 AttnWork w;
                 UnitPlan u;
                 const uint32_t iu = take_item(k, w, u);
-                sched::release(ring, k);
+                __syncwarp();
+                if (lane == 0) sched::release(ring, k);
                 if (iu >= static_cast<uint32_t>(n_items)) break;
                 const int nbu = max(u.nb[0], u.nb[1]);
                 for (int x = 0; x < 2; ++x)
@@ -378,7 +381,7 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 ptx::tc_fence_after();
                 for (int x = 0; x < 2; ++x)
                     if (u.nb[x]) issue_s(x, g);
-                ptx::mma_commit(&k_empty[g % kKStages]);
+                ptx::mma_commit_elect(&k_empty[g % kKStages]);
                 for (int j = 0; j < nbu; ++j) {
                     const uint32_t kg = g + j;
                     mwait(&v_full[kg & 1], (kg >> 1) & 1, 17);
@@ -394,19 +397,19 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                             }
                             issue_s(x, kg + 1);
                         } else {
-                            ptx::mma_commit(&o_full[x]);
-                            ptx::mma_commit(&q_empty[x]);
+                            ptx::mma_commit_elect(&o_full[x]);
+                            ptx::mma_commit_elect(&q_empty[x]);
                         }
                     }
-                    ptx::mma_commit(&v_empty[kg & 1]);
-                    if (j + 1 < nbu) ptx::mma_commit(&k_empty[(kg + 1) % kKStages]);
+                    ptx::mma_commit_elect(&v_empty[kg & 1]);
+                    if (j + 1 < nbu) ptx::mma_commit_elect(&k_empty[(kg + 1) % kKStages]);
                 }
                 g += nbu;
                 for (int x = 0; x < 2; ++x)
                     if (u.nb[x]) ++qit[x];
             }
 #ifdef SGC_ATTN_PROF
-            atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 32 + 22], (unsigned long long)(clock64() - t_mma0));
+            if (lane == 0) atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 32 + 22], (unsigned long long)(clock64() - t_mma0));
 #endif
         }
     } else {
@@ -802,7 +805,8 @@ __global__ void __launch_bounds__(352, 1)
     auto pwait = [&](uint64_t* bar, uint32_t par, int slot) {
         const long long t0 = clock64();
         ptx::mbar_wait_park(bar, par);
-        atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 32 + slot], (unsigned long long)(clock64() - t0));
+        if ((threadIdx.x & 31) == 0)
+            atomicAdd(&g_attn_prof[(blockIdx.x % 148) * 32 + slot], (unsigned long long)(clock64() - t0));
     };
 #else
     auto pwait = [&](uint64_t* bar, uint32_t par, int) { ptx::mbar_wait_park(bar, par); };
@@ -902,13 +906,15 @@ __global__ void __launch_bounds__(352, 1)
         // two MMA issuers (a single thread spends ~17 instructions per tcgen05.mma and was the
         // bottleneck issuing 16 MMAs per 1024 tensor cycles): warp 10 issues S, warp 1 PV.
         // S(g) overwrites buffer g % 3 only after PV(g - 3) read P(g - 3) from it (s_free).
-        if (lane == 0 && warp == 10) {
+        // each issuer warp runs its loop convergently; one elected lane issues (uniform datapath)
+        if (warp == 10) {
             constexpr uint32_t idS = ptx::idesc_bf16_f32(BQ, BKV);
             uint32_t g = 0;
             for (uint32_t k = 0;; ++k) {
                 const uint32_t iu = sched::wait(ring, k);
                 const int nb = iu < static_cast<uint32_t>(n_items) ? info[k % kTileRing].nb : 0;
-                sched::release(ring, k);
+                __syncwarp();
+                if (lane == 0) sched::release(ring, k);
                 if (iu >= static_cast<uint32_t>(n_items)) break;
                 pwait(&q_full[k & 1], (k >> 1) & 1, 20);
                 const uint64_t qd = ptx::umma_desc_sw128(ptx::smem_u32(sQ + (k & 1) * C::kQBytes));
@@ -925,20 +931,21 @@ __global__ void __launch_bounds__(352, 1)
                         // descriptor start address field: bytes >> 4
                         const uint64_t ad = qd + (((kc / 4) * (BQ * 128) + (kc % 4) * 32) >> 4);
                         const uint64_t bd = kd + (((kc / 4) * (BKV * 128) + (kc % 4) * 32) >> 4);
-                        ptx::mma_bf16(dS, ad, bd, idS, kc > 0 ? 1u : 0u);
+                        ptx::mma_bf16_elect(dS, ad, bd, idS, kc > 0 ? 1u : 0u);
                     }
-                    ptx::mma_commit(&s_full[sbuf]);
-                    ptx::mma_commit(&k_empty[ks]);
-                    if (b == nb - 1) ptx::mma_commit(&q_empty[k & 1]);
+                    ptx::mma_commit_elect(&s_full[sbuf]);
+                    ptx::mma_commit_elect(&k_empty[ks]);
+                    if (b == nb - 1) ptx::mma_commit_elect(&q_empty[k & 1]);
                 }
             }
-        } else if (lane == 0) {
+        } else {
             constexpr uint32_t idO = ptx::idesc_bf16_f32_bmn(BQ, HD);
             uint32_t g = 0;
             for (uint32_t k = 0;; ++k) {
                 const uint32_t iu = sched::wait(ring, k);
                 const int nb = iu < static_cast<uint32_t>(n_items) ? info[k % kTileRing].nb : 0;
-                sched::release(ring, k);
+                __syncwarp();
+                if (lane == 0) sched::release(ring, k);
                 if (iu >= static_cast<uint32_t>(n_items)) break;
                 if (k > 0) pwait(o_free, (k - 1) & 1, 19);  // the previous tile's epilogue read O
                 for (int b = 0; b < nb; ++b, ++g) {
@@ -951,11 +958,11 @@ __global__ void __launch_bounds__(352, 1)
                     const uint32_t aP = tmem_base + C::kS + pbuf * 128;
 #pragma unroll
                     for (int kk = 0; kk < BKV / 16; ++kk)
-                        ptx::mma_bf16_ts(tmem_base + C::kO, aP + kk * 8, vd + ((kk * 16 * 128) >> 4), idO,
+                        ptx::mma_bf16_ts_elect(tmem_base + C::kO, aP + kk * 8, vd + ((kk * 16 * 128) >> 4), idO,
                                          (b > 0 || kk > 0) ? 1u : 0u);
-                    ptx::mma_commit(&v_empty[vs]);
-                    ptx::mma_commit(&s_free[pbuf]);
-                    if (b == nb - 1) ptx::mma_commit(o_full);
+                    ptx::mma_commit_elect(&v_empty[vs]);
+                    ptx::mma_commit_elect(&s_free[pbuf]);
+                    if (b == nb - 1) ptx::mma_commit_elect(o_full);
                 }
             }
         }
