@@ -12,22 +12,25 @@
 namespace sgc {
 namespace {
 
-constexpr int PT = 64;   // pair tile
 constexpr int PK = 16;   // k chunk
 
-// encoders.cpp:40-48 euclidean_distance for all i<j (one thread = 4x4 pairs, k sequential)
+// encoders.cpp:40-48 euclidean_distance for all i<j (thread = PP x PP pairs, k sequential).
+// PT = 32 (2 x 2 pairs per thread): at m = 1024 that is 528 tiles instead of the 136 of a
+// 64-pair tile, so every SM gets several CTAs; the per-pair arithmetic and order are unchanged.
+template <int PT>
 __global__ void __launch_bounds__(256)
     pairwise_kernel(double* D, const float* emb, int m, int dim, const int2* tiles, int squared) {
+    constexpr int PP = PT / 16;
     __shared__ float As[PK][PT + 1];
     __shared__ float Bs[PK][PT + 1];
     const int2 tile = tiles[blockIdx.x];
     const int i0 = tile.x * PT, j0 = tile.y * PT;
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    double acc[4][4];
+    double acc[PP][PP];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < PP; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+        for (int b = 0; b < PP; ++b) acc[a][b] = 0.0;
     for (int k0 = 0; k0 < dim; k0 += PK) {
         for (int idx = threadIdx.x; idx < PT * PK; idx += 256) {
             int r = idx / PK, kk = idx % PK;
@@ -38,16 +41,16 @@ __global__ void __launch_bounds__(256)
         __syncthreads();
         const int kn = min(PK, dim - k0);
         for (int kk = 0; kk < kn; ++kk) {
-            double a[4], b[4];
+            double a[PP], b[PP];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
+            for (int q = 0; q < PP; ++q) {
                 a[q] = static_cast<double>(As[kk][ty + 16 * q]);
                 b[q] = static_cast<double>(Bs[kk][tx + 16 * q]);
             }
 #pragma unroll
-            for (int p = 0; p < 4; ++p)
+            for (int p = 0; p < PP; ++p)
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
+                for (int q = 0; q < PP; ++q) {
                     double v = __dsub_rn(a[p], b[q]);
                     acc[p][q] = __dadd_rn(acc[p][q], __dmul_rn(v, v));
                 }
@@ -55,9 +58,9 @@ __global__ void __launch_bounds__(256)
         __syncthreads();
     }
 #pragma unroll
-    for (int p = 0; p < 4; ++p)
+    for (int p = 0; p < PP; ++p)
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < PP; ++q) {
             int i = i0 + ty + 16 * p, j = j0 + tx + 16 * q;
             if (i < m && j < m && i <= j) {
                 double v = i == j ? 0.0 : __dsqrt_rn(acc[p][q]);
@@ -315,6 +318,7 @@ __global__ void __launch_bounds__(kAggThreads)
 }  // namespace
 
 void pairwise_distances(Ctx* c, double* D, const float* emb, int m, int dim, bool squared) {
+    constexpr int PT = 32;
     int nt = (m + PT - 1) / PT;
     std::vector<int2> tiles;
     for (int a = 0; a < nt; ++a)
@@ -322,7 +326,7 @@ void pairwise_distances(Ctx* c, double* D, const float* emb, int m, int dim, boo
     int2* dt = c->buf<int2>("pairwise_tiles", tiles.size());
     copy_in(c, dt, tiles.data(), tiles.size());
     Ctx::Timed timer(c, "pairwise");
-    pairwise_kernel<<<tiles.size(), 256, 0, c->stream>>>(D, emb, m, dim, dt, squared ? 1 : 0);
+    pairwise_kernel<PT><<<tiles.size(), 256, 0, c->stream>>>(D, emb, m, dim, dt, squared ? 1 : 0);
     SGC_LAUNCH_CHECK(c);
     // keep `tiles` alive until the async copy has consumed it
     SGC_CUDA_CHECK(cudaStreamSynchronize(c->stream));
