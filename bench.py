@@ -219,6 +219,8 @@ def run_ours(args, rank, world, local_rank):
         ctx.set_option("attn_split", args.attn_split)
     if args.attn_kernel is not None:
         ctx.set_option("attn_kernel", args.attn_kernel)
+    if args.attn_kernel_partial is not None:
+        ctx.set_option("attn_kernel_partial", args.attn_kernel_partial)
     if args.gemm_raster is not None:
         ctx.set_option("gemm_raster", args.gemm_raster)
     t0 = time.time()
@@ -757,6 +759,8 @@ def main():
     ap.add_argument("--no-split", action="store_true",
                     help="N > 1: whole clusters per GPU only (no member-level rebalancing of skewed clusters)")
     ap.add_argument("--attn-split", type=int, default=None, help="1: two softmax warpgroups per query tile")
+    ap.add_argument("--attn-kernel-partial", type=int, default=None,
+                    help="decode steps' prefix attention: 1 one-tile kernel (default), 0 two-tile kernel")
     ap.add_argument("--gemm-raster", type=int, default=None,
                     help="CTA-pair GEMM raster: 0 M-groups (default), 1 by estimated DRAM bytes, 2 N-groups")
     ap.add_argument("--attn-kernel", type=int, default=None,

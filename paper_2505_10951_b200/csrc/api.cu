@@ -3492,6 +3492,7 @@ int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value) {
         else if (std::string(name) == "gemm_raster") sgc::gemm_set_raster(static_cast<int>(value));
         else if (std::string(name) == "attn_split") sgc::attention_set_split(value != 0);
         else if (std::string(name) == "attn_kernel") sgc::attention_set_kernel(static_cast<int>(value));
+        else if (std::string(name) == "attn_kernel_partial") sgc::attention_set_kernel_partial(static_cast<int>(value));
         else if (std::string(name) == "gnn_tile") ctx->c.gnn_tile = static_cast<int>(value);
         else if (std::string(name) == "gnn_dedup") ctx->c.gnn_dedup = value != 0 ? 1 : 0;
         else if (std::string(name) == "decode_defer_pct") ctx->c.decode_defer_pct = static_cast<uint32_t>(std::max<int64_t>(0, value));

@@ -54,6 +54,8 @@ void attention_set_split(bool on);
 // 0: two 128-row tiles per item (attn_tc_kernel, default); 1: one tile, S triple-buffered, two
 // softmax warpgroups on alternate key blocks (attn_s3_kernel)
 void attention_set_kernel(int k);
+// the same for partial mode (decode): default 1
+void attention_set_kernel_partial(int k);
 
 // Decode step (attention.cu): merge the prefix partial (part_o, part_lse from the tcgen05 kernel
 // in partial mode, or none when part_o == nullptr) with each row's own keys: question rows

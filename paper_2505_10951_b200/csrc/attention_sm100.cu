@@ -1211,6 +1211,8 @@ __global__ void __launch_bounds__(352, 1)
 // Same-box A/B at C3 (scripts/gpu_attn_ab.sh): 112.4 / 112.3 vs 115.8 / 115.8 ms per step once the
 // two-tile kernel's MMA thread built its descriptors once per operand tile (it was 115.6-118)
 int g_attn_kernel = 0;
+// the same choice for partial mode (decode steps: prefix keys only), sgc_set_option "attn_kernel_partial"
+int g_attn_kernel_partial = 1;
 
 template <int HD>
 void launch_s3(Ctx* c, const AttnParams& a, int n_work, int heads, int q_rows, int pfx_rows, int loc_rows) {
@@ -1277,7 +1279,11 @@ bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, in
     if (n_work <= 0) return true;
     if (p.loc_kv0 != 0) return false;
     if (p.part_o && !p.part_lse) return false;
-    if (g_attn_kernel == 1) {
+    // decode (partial mode): a cluster's generating members rarely fill one 128-row tile, so the
+    // two-tile kernel runs one tile per item with no second chain to overlap its softmax; the
+    // one-tile kernel keeps two warpgroups busy on alternate key blocks of that tile
+    const int kern = p.part_o ? g_attn_kernel_partial : g_attn_kernel;
+    if (kern == 1) {
         switch (hd) {
             case 64: launch_s3<64>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows); return true;
             case 128: launch_s3<128>(c, p, n_work, heads, q_rows, pfx_rows, loc_rows); return true;
@@ -1300,5 +1306,6 @@ bool cascade_attention_tc(Ctx* c, const AttnParams& p, int n_work, int heads, in
 
 void attention_set_split(bool on) { g_attn_split = on; }
 void attention_set_kernel(int k) { g_attn_kernel = k; }
+void attention_set_kernel_partial(int k) { g_attn_kernel_partial = k; }
 
 }  // namespace sgc
