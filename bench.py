@@ -463,6 +463,11 @@ def run_ours(args, rank, world, local_rank):
                    "queries": m, "clusters": w.clusters, "layers": w.lm["layers"],
                    "model_dim": w.lm["model_dim"], "ffn_hidden": w.lm["ffn_hidden"],
                    "prefix_tokens_mean": float(np.mean(prefix_lens)),
+                   # prefill tokens without the cache (every query's own prompt) over with it (one
+                   # representative per cluster + every question): Aggregate.total_prefill_tokens
+                   "reuse_ratio": (round(float(sum(len(o) + len(qq) for o, qq in zip(pb.own, pb.q)) /
+                                               (sum(prefix_lens) + sum(len(qq) for qq in pb.q))), 3)
+                                   if pb.own else None),
                    "question_tokens_mean": float(np.mean(members_q)),
                    "parallelism": f"clusters sharded over {world} GPU(s)" if world > 1 else "1 GPU",
                    "l2": "inputs larger than L2 (11 GiB bf16 weights + prefix KV streamed every step)"},
