@@ -231,7 +231,17 @@ void pool_grow(Ctx* c, sgc_model* m, uint32_t need) {
     SGC_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
     const size_t pb = page_bytes(m);
     const size_t headroom = std::max<size_t>(static_cast<size_t>(0.04 * total_b), 2ull << 30);
-    const size_t avail = free_b > headroom ? free_b - headroom : 0;  // new buffers coexist with the old
+    size_t avail = free_b > headroom ? free_b - headroom : 0;  // new buffers coexist with the old
+    if (p.pages && p.live() == 0) {
+        // nothing to carry over: hand the old buffers back (stream order) before allocating, so a
+        // pool sized for an earlier, smaller batch does not have to coexist with its replacement
+        SGC_CUDA_CHECK(cudaFreeAsync(p.k, c->stream));
+        SGC_CUDA_CHECK(cudaFreeAsync(p.v, c->stream));
+        avail += static_cast<size_t>(p.pages) * pb;
+        p.k = p.v = nullptr;
+        p.pages = 0;
+        p.free_pages.clear();
+    }
     uint32_t want = std::max<uint32_t>(need, p.pages + p.pages / 2);
     if (static_cast<size_t>(want) * pb > avail) want = need;
     if (static_cast<size_t>(want) * pb > avail)
