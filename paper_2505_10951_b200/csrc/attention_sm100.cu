@@ -55,8 +55,11 @@ constexpr int kVStages = 2;
 #ifndef SGC_S3_TOKEN_LATE
 #define SGC_S3_TOKEN_LATE 0
 #endif
+// softmax ping-pong between the two tiles (named barriers around the exponentials): it helped
+// while the MMA thread was the slow resource; with the convergent-warp MMA issue it costs ~1.3%
+// (same box, 3 alternating runs: 108.1-108.6 vs 109.7-110.0 ms per C3 step), so it is off
 #ifndef SGC_ATTN_PINGPONG
-#define SGC_ATTN_PINGPONG 1
+#define SGC_ATTN_PINGPONG 0
 #endif
 #ifndef SGC_POLY_NUM
 #define SGC_POLY_NUM 1
