@@ -58,6 +58,13 @@ constexpr int kVStages = 2;
 // softmax ping-pong between the two tiles (named barriers around the exponentials): it helped
 // while the MMA thread was the slow resource; with the convergent-warp MMA issue it costs ~1.3%
 // (same box, 3 alternating runs: 108.1-108.6 vs 109.7-110.0 ms per C3 step), so it is off
+// SGC_ATTN_SPLIT_S=1: S(j+1) issued in two N = 64 halves around PV(j) (the lower half as soon as
+// the softmax has loaded S(j), P written over S's upper half) to shorten the per-tile chain;
+// measured slower at C3 (114.5 vs 107.7 ms per step, same box): N = 64 QK^T MMAs re-read Q
+#ifndef SGC_ATTN_SPLIT_S
+#define SGC_ATTN_SPLIT_S 0
+#endif
+constexpr uint32_t kPCol = SGC_ATTN_SPLIT_S ? 64 : 0;  // TMEM column of P within a tile's S
 #ifndef SGC_ATTN_PINGPONG
 #define SGC_ATTN_PINGPONG 0
 #endif
@@ -217,7 +224,8 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
     uint64_t* s_full = bars + 14;   // [2] per tile
     uint64_t* p_full = bars + 16;   // [2] per tile
     uint64_t* o_full = bars + 18;   // [2] per tile
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+    uint64_t* s_read = bars + 20;   // [2] per tile: the softmax loaded S (its lower half may be reused)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
     float* xm = reinterpret_cast<float*>(bars + 32);  // [2 tiles][SPLIT][BQ] row max / sum exchange
     // items (unit x head) claimed by the producer and handed to the MMA and softmax warps
     ItemRing* ring = reinterpret_cast<ItemRing*>(xm + 2 * 2 * BQ);
@@ -259,6 +267,7 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
             ptx::mbar_init(&s_full[i], 1);
             ptx::mbar_init(&p_full[i], 128 * SPLIT);
             ptx::mbar_init(&o_full[i], 1);
+            ptx::mbar_init(&s_read[i], 128 * SPLIT);
         }
         sched::init(ring, 1 + 8 * SPLIT);  // the MMA thread + every softmax warp
         ptx::fence_barrier_init();
@@ -359,11 +368,28 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 }
                 ptx::mma_commit_elect(&s_full[x]);
             };
+#if SGC_ATTN_SPLIT_S
+            // S(j+1) in two N = 64 halves: the lower half (columns 0-63) as soon as the softmax has
+            // loaded S(j) -- P(j) lives in columns 64-127 -- and the upper half after PV(j) read P(j)
+            constexpr uint32_t idS64 = ptx::idesc_bf16_f32(BQ, 64);
+            uint32_t sr[2] = {0, 0};
+            auto issue_s_half = [&](int x, uint32_t kg, int half) {
+                const uint64_t qd = ptx::umma_desc_sw128(ptx::smem_u32(sQ + x * C::kQBytes));
+                const uint64_t kd = ptx::umma_desc_sw128(ptx::smem_u32(sK + (kg % kKStages) * C::kKBytes));
+                const uint32_t dS = tmem_base + C::kS + x * BQ + half * 64;
+#pragma unroll
+                for (int kc = 0; kc < HD / 16; ++kc) {
+                    const uint64_t ad = qd + (((kc / 4) * (BQ * 128) + (kc % 4) * 32) >> 4);
+                    const uint64_t bd = kd + (((kc / 4) * (BKV * 128) + (kc % 4) * 32 + half * 64 * 128) >> 4);
+                    ptx::mma_bf16_elect(dS, ad, bd, idS64, kc > 0 ? 1u : 0u);
+                }
+            };
+#endif
             auto issue_pv = [&](int x, uint32_t kg, bool first) {  // O_X += P_X V
                 mwait(&p_full[x], gx[x] & 1, 18);
                 ptx::tc_fence_after();
                 const uint64_t vd = ptx::umma_desc_sw128_lbo(ptx::smem_u32(sV + (kg & 1) * C::kVBytes), BKV * 128, 1024);
-                const uint32_t dO = tmem_base + C::kO + x * 128, aP = tmem_base + C::kS + x * BQ;
+                const uint32_t dO = tmem_base + C::kO + x * 128, aP = tmem_base + C::kS + x * BQ + kPCol;
 #pragma unroll
                 for (int kk = 0; kk < BKV / 16; ++kk)
                     ptx::mma_bf16_ts_elect(dO, aP + kk * 8, vd + ((kk * 16 * 128) >> 4), idO, (!first || kk > 0) ? 1u : 0u);
@@ -389,6 +415,19 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                     const uint32_t kg = g + j;
                     mwait(&v_full[kg & 1], (kg >> 1) & 1, 17);
                     bool waited_next_k = false;
+#if SGC_ATTN_SPLIT_S
+                    for (int x = 0; x < 2; ++x) {
+                        if (j + 1 >= u.nb[x]) continue;
+                        if (!waited_next_k) {
+                            mwait(&k_full[(kg + 1) % kKStages], ((kg + 1) / kKStages) & 1, 16);
+                            waited_next_k = true;
+                        }
+                        mwait(&s_read[x], sr[x] & 1, 16);
+                        ++sr[x];
+                        ptx::tc_fence_after();
+                        issue_s_half(x, kg + 1, 0);
+                    }
+#endif
                     for (int x = 0; x < 2; ++x) {
                         if (j >= u.nb[x]) continue;
                         issue_pv(x, kg, j == 0);
@@ -398,7 +437,12 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                                 ptx::tc_fence_after();
                                 waited_next_k = true;
                             }
+#if SGC_ATTN_SPLIT_S
+                            issue_s_half(x, kg + 1, 1);
+                            ptx::mma_commit_elect(&s_full[x]);
+#else
                             issue_s(x, kg + 1);
+#endif
                         } else {
                             ptx::mma_commit_elect(&o_full[x]);
                             ptx::mma_commit_elect(&q_empty[x]);
@@ -506,6 +550,12 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 for (int c = 0; c < COLS / 32; ++c)
                     ptx::tmem_ld32(tS + c0 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[c * 32]));
                 ptx::tmem_ld_wait();
+#if SGC_ATTN_SPLIT_S
+                if (b + 1 < nb) {  // S(b) is in registers: the MMA may compute S(b+1)'s lower half
+                    ptx::tc_fence_before();
+                    ptx::mbar_arrive(&s_read[x]);
+                }
+#endif
                 SPROF(7);
                 // visibility bitmap of this thread's keys [klo, khi] (COLS / 32 words)
                 uint32_t vw[COLS / 32];
@@ -604,7 +654,7 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 // P -> TMEM over S's first 64 columns (this thread's keys: columns c0/2 ..)
 #pragma unroll
                 for (int c = 0; c < COLS / 32; ++c)
-                    ptx::tmem_st16(tS + c0 / 2 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&sv[c * 16]));
+                    ptx::tmem_st16(tS + kPCol + c0 / 2 + c * 16, *reinterpret_cast<uint32_t(*)[16]>(&sv[c * 16]));
                 l = l * alpha + rs;
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
