@@ -245,7 +245,7 @@ def run_ours(args, rank, world, local_rank):
     def step():
         return host.run_subgcache(ctx, lm, dg, pb, want_logits=False, device_inputs=True, waves=args.waves,
                                   split_clusters=split, transfer_prefix=0 if args.replica_prefill else 1,
-                                  verify_prefix=not args.no_verify_prefix)
+                                  verify_prefix=not args.no_verify_prefix, want_embeddings=False)
 
     for _ in range(args.warmup):
         res = step()
@@ -292,7 +292,7 @@ def run_ours(args, rank, world, local_rank):
         def step_e2e():
             return host.run_subgcache(ctx, lm, dg, pb, want_logits=True, waves=args.waves,
                                       split_clusters=split, transfer_prefix=0 if args.replica_prefill else 1,
-                                      verify_prefix=not args.no_verify_prefix)
+                                      verify_prefix=not args.no_verify_prefix, want_embeddings=False)
 
         ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if world > 1:

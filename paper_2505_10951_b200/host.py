@@ -696,7 +696,7 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
                   world_size: int = 1, want_logits: bool = True,
                   device_inputs: bool = False, waves: int = 1, max_new: int = 0,
                   split_clusters: bool = False, transfer_prefix: int = 1,
-                  verify_prefix: bool = True) -> SubgCacheResult:
+                  verify_prefix: bool = True, want_embeddings: bool = True) -> SubgCacheResult:
     """pipeline.cpp:212-293 (SubgCache branch) + cache_engine.cpp:217-233 (run_batch), to the
     first token of every query."""
     w = pb.w
@@ -734,7 +734,7 @@ def run_subgcache(ctx: Context, model: ToyLm, g: DeviceGraph, pb: PreparedBatch,
     b.split_clusters = int(split_clusters)
     b.transfer_prefix = int(transfer_prefix)
     b.verify_prefix = int(verify_prefix)
-    emb = np.zeros((m, d), np.float32)
+    emb = np.zeros((m, d), np.float32) if want_embeddings else None  # an intermediate: optional
     labels = np.zeros(m, np.uint32)
     nm = max(m - k, 1)
     left, right = np.zeros(nm, np.uint32), np.zeros(nm, np.uint32)
