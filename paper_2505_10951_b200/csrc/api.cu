@@ -67,6 +67,12 @@ double now_ms() {
         .count();
 }
 
+// SGC_TRACE_HOST=1: host wall-clock marks inside sgc_run_subgcache (stderr), to locate host stalls
+void host_mark(const char* what, double t0) {
+    static const bool on = std::getenv("SGC_TRACE_HOST") != nullptr;
+    if (on) std::fprintf(stderr, "[sgc host] %-24s %9.3f ms\n", what, now_ms() - t0);
+}
+
 template <typename T>
 T* dalloc(Ctx* c, size_t n) {
     void* p = nullptr;
@@ -228,7 +234,7 @@ void pool_grow(Ctx* c, sgc_model* m, uint32_t need) {
     KvPool& p = m->pool;
     if (need <= p.pages) return;
     size_t free_b = 0, total_b = 0;
-    SGC_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    c->mem_info(&free_b, &total_b);
     const size_t pb = page_bytes(m);
     const size_t headroom = std::max<size_t>(static_cast<size_t>(0.04 * total_b), 2ull << 30);
     size_t avail = free_b > headroom ? free_b - headroom : 0;  // new buffers coexist with the old
@@ -270,6 +276,7 @@ void pool_grow(Ctx* c, sgc_model* m, uint32_t need) {
     p.k = nk;
     p.v = nv;
     p.pages = want;
+    c->mem_changed();
 }
 
 std::vector<int32_t> pool_alloc(Ctx* c, sgc_model* m, uint32_t n) {
@@ -2518,6 +2525,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         const uint32_t budget = reserved >= lc.max_seq_len ? 0 : lc.max_seq_len - reserved;
         if (budget <= 1) fail(SGC_DOMAIN, "max_seq too small for the question budget and generation cap");
         HostSubs hs = host_subs(c, &b->retrieved);
+        host_mark("host_subs", t_start);
         // ---- multi-GPU: the context's transport (comm.cuh) or a caller-driven plan
         sgc::Comm* comm = ctx->comm.get();
         const bool use_comm = comm && comm->world > 1;
@@ -2556,6 +2564,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         }
         c->sync();
         const double t_enc = now_ms();
+        host_mark("encoded", t_start);
         // ---- (2) clustering
         uint32_t* d_lab = c->buf<uint32_t>("run_labels", m);
         uint32_t* d_left = c->buf<uint32_t>("run_left", m);
@@ -2564,6 +2573,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         cluster_device(c, d_emb, m, d, b->linkage, b->clusters, d_lab, d_left, d_right, d_dist);
         std::vector<uint32_t> labels = to_host(c, d_lab, m);
         const double t_cl = now_ms();
+        host_mark("clustered", t_start);
         const uint32_t k = b->clusters;
         // ---- (3) jobs (pipeline.cpp:249-261) + representatives for the clusters served here
         std::vector<std::vector<uint32_t>> members(k);
@@ -2692,6 +2702,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         }
         c->sync();
         const double t_rep = now_ms();
+        host_mark("represented", t_start);
         // ---- (4) KV precompute: representative prompts (+ standalone fallbacks) in one batch
         std::vector<uint64_t> q_off = to_host(c, b->questions.off, m + 1);
         std::vector<int32_t> q_tok = to_host(c, b->questions.tokens, q_off[m]);
@@ -2752,7 +2763,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             // activations (prefill runs in row chunks of <= 64k rows) and the extend scratch; split
             // any wave whose pages exceed it (C4 with 256 clusters: ~137 GB of K/V in each of 2 waves)
             size_t free_b = 0, total_b = 0;
-            SGC_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+            c->mem_info(&free_b, &total_b);
             const double act_row = d * (4.0 + 2 * 4) + 2.0 * model->ffn + 4.0 * d / 32;  // x, xb, q, ao, h, ss
             const double reserve = 2.0 * 65536.0 * act_row + 0.06 * static_cast<double>(total_b);
             const double pb = static_cast<double>(page_bytes(model));
@@ -2783,6 +2794,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
                 wave_end.swap(we2);
             }
         }
+        host_mark("waves planned", t_start);
         cudaEvent_t ev_start = c->event();
         SGC_CUDA_CHECK(cudaEventRecord(ev_start, c->stream));
         std::vector<cudaEvent_t> ev_wave, ev_seal, ev_wave_start;
@@ -2846,7 +2858,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         // keep buffers count as free), 20% headroom for the forward activations
         const double kv_row_bytes = 2.0 * model->L * d * sizeof(bf16);
         size_t free_now = 0, total_now = 0;
-        SGC_CUDA_CHECK(cudaMemGetInfo(&free_now, &total_now));
+        c->mem_info(&free_now, &total_now);
         double avail_now = static_cast<double>(free_now) +
                            static_cast<double>(model->pool.free_pages.size()) * page_bytes(model);
         for (const char* nm : {"ex_keep_k", "ex_keep_v"}) {
@@ -2920,6 +2932,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
             const uint32_t we = wave_end[wv];
             if (we <= wb) continue;
             const double tw0 = now_ms();
+            host_mark("wave start", t_start);
             {
                 cudaEvent_t e0 = c->event();
                 SGC_CUDA_CHECK(cudaEventRecord(e0, c->stream));
@@ -3312,6 +3325,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         o->waves = static_cast<uint32_t>(ev_wave.size());
         const double t_pf = t_rep + pf_ms;
         const double t_ext = now_ms();
+        host_mark("waves done", t_start);
         (void)t_pf;
         (void)t_ext;
         if (o->embeddings) sgc::copy_out(c, o->embeddings, d_emb, static_cast<size_t>(m) * d);
@@ -3395,6 +3409,7 @@ int sgc_run_subgcache(sgc_ctx* ctx, sgc_model* model, sgc_graph* g, const sgc_ba
         (void)pf_ms;
         (void)ex_ms;
         o->stage_ms[5] = now_ms() - t_start;
+        host_mark("end", t_start);
         o->prefill_rows = prefill_rows;
         o->extend_rows = extend_rows;
         o->decode_rows = decode_rows;

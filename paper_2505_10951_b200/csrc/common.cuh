@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <chrono>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -94,6 +95,25 @@ struct Ctx {
     // pending (name, start, stop) event triples, resolved when the timings are read
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> event_pool;
+
+    // device free / total memory for the planners, cached: cudaMemGetInfo takes a driver lock
+    // that an nvidia-smi / NVML poller holds now and then, and a step that called it stalled its
+    // host planning for 10-65 ms (scripts/host_trace.py). Refreshed after a minute or when the
+    // KV page pool (the one large allocator) changed size.
+    size_t mem_free = 0, mem_total = 0;
+    std::chrono::steady_clock::time_point mem_at{};
+    bool mem_valid = false;
+    void mem_info(size_t* free_b, size_t* total_b) {
+        const auto now = std::chrono::steady_clock::now();
+        if (!mem_valid || now - mem_at > std::chrono::seconds(60)) {
+            SGC_CUDA_CHECK(cudaMemGetInfo(&mem_free, &mem_total));
+            mem_at = now;
+            mem_valid = true;
+        }
+        *free_b = mem_free;
+        *total_b = mem_total;
+    }
+    void mem_changed() { mem_valid = false; }
 
     template <typename T>
     T* buf(const std::string& name, size_t count) {
