@@ -573,11 +573,11 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
     }
     kv->pages = pool_alloc(c, m, npages);
     kv->d_bt = dalloc<int32_t>(c, npages);
-    sgc::copy_in(c, kv->d_bt, kv->pages.data(), npages);
+    sgc::copy_in_staged(c, kv->d_bt, kv->pages.data(), npages);
     kv->d_tokens = dalloc<int32_t>(c, M);
     kv->d_tok_off = dalloc<uint64_t>(c, count + 1);
-    sgc::copy_in(c, kv->d_tokens, rows_tok.data(), M);
-    sgc::copy_in(c, kv->d_tok_off, ctx_off.data(), count + 1);
+    sgc::copy_in_staged(c, kv->d_tokens, rows_tok.data(), M);
+    sgc::copy_in_staged(c, kv->d_tok_off, ctx_off.data(), count + 1);
     float* d_soft = nullptr;
     if (any_soft) {
         d_soft = c->buf<float>("pf_soft", static_cast<size_t>(count) * d);
@@ -615,9 +615,9 @@ sgc_kv* do_prefill(Ctx* c, sgc_model* m, uint32_t count, const uint64_t* off_in,
         std::vector<int32_t> packed;
         packed.reserve(static_cast<size_t>(Mc) * 4 + (s1 - s0));
         for (auto* v : {&pos, &seg_lo, &sidx, &kvrow, &lrows}) packed.insert(packed.end(), v->begin(), v->end());
-        sgc::copy_in(c, d_arr, packed.data(), packed.size());
+        sgc::copy_in_staged(c, d_arr, packed.data(), packed.size());
         sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("pf_work", work.size());
-        sgc::copy_in(c, d_work, work.data(), work.size());
+        sgc::copy_in_staged(c, d_work, work.data(), work.size());
         FwdBatch b;
         b.M = Mc;
         b.d_tokens = kv->d_tokens + R0;
@@ -766,14 +766,14 @@ void do_extend(Ctx* c, sgc_model* m, sgc_kv* kv, uint32_t n, const uint32_t* seg
         float* d_logits = c->buf<float>("ex_logits", static_cast<size_t>(nm) * SGC_VOCAB);
         int32_t* d_first = c->buf<int32_t>("ex_first", nm);
         int8_t* d_hint = keep ? c->buf<int8_t>("ex_hint", nm) : nullptr;
-        sgc::copy_in(c, d_tok, toks.data(), M);
-        sgc::copy_in(c, d_pos, pos.data(), M);
-        sgc::copy_in(c, d_seg, seg_lo.data(), M);
-        sgc::copy_in(c, d_lr, lrows.data(), nm);
-        sgc::copy_in(c, d_mseg, mseg.data(), nm);
-        sgc::copy_in(c, d_aoff, a_off.data(), nm + 1);
-        sgc::copy_in(c, d_atok, a_tok.data(), a_tok.size());
-        sgc::copy_in(c, d_work, work.data(), work.size());
+        sgc::copy_in_staged(c, d_tok, toks.data(), M);
+        sgc::copy_in_staged(c, d_pos, pos.data(), M);
+        sgc::copy_in_staged(c, d_seg, seg_lo.data(), M);
+        sgc::copy_in_staged(c, d_lr, lrows.data(), nm);
+        sgc::copy_in_staged(c, d_mseg, mseg.data(), nm);
+        sgc::copy_in_staged(c, d_aoff, a_off.data(), nm + 1);
+        sgc::copy_in_staged(c, d_atok, a_tok.data(), a_tok.size());
+        sgc::copy_in_staged(c, d_work, work.data(), work.size());
         FwdBatch b;
         b.M = M;
         b.d_tokens = d_tok;
@@ -894,7 +894,7 @@ GenBuffers gen_buffers(Ctx* c, sgc_model* m, const std::vector<int32_t>& block_t
     GenBuffers g;
     g.model = m;
     g.d_bt = c->buf<int32_t>("dec_bt", std::max<size_t>(1, block_table.size()));
-    sgc::copy_in(c, g.d_bt, block_table.data(), block_table.size());
+    sgc::copy_in_staged(c, g.d_bt, block_table.data(), block_table.size());
     g.keep = keep;
     g.grows = std::max<size_t>(1, gen_rows);
     g.gk = c->buf<bf16>("dec_gk", static_cast<size_t>(m->L) * g.grows * m->d);
@@ -903,9 +903,9 @@ GenBuffers gen_buffers(Ctx* c, sgc_model* m, const std::vector<int32_t>& block_t
     g.d_hint = c->buf<int8_t>("dec_hint", n);
     g.d_aoff = c->buf<uint64_t>("dec_aoff", n + 1);
     g.d_atok = c->buf<int32_t>("dec_atok", std::max<size_t>(1, job.a_tok.size()));
-    sgc::copy_in(c, g.d_hint, job.hint.data(), n);
-    sgc::copy_in(c, g.d_aoff, job.a_off.data(), n + 1);
-    sgc::copy_in(c, g.d_atok, job.a_tok.data(), job.a_tok.size());
+    sgc::copy_in_staged(c, g.d_hint, job.hint.data(), n);
+    sgc::copy_in_staged(c, g.d_aoff, job.a_off.data(), n + 1);
+    sgc::copy_in_staged(c, g.d_atok, job.a_tok.data(), job.a_tok.size());
     return g;
 }
 
@@ -950,10 +950,10 @@ void decode_steps(Ctx* c, sgc_model* m, const GenBuffers& g, const GenJob& job, 
         packed.reserve(static_cast<size_t>(M) * 12);
         for (auto* v : {&tok, &pos, &kvr, &step, &lrow, &plo, &pn, &qlo, &qn, &glo, &gn, &act})
             packed.insert(packed.end(), v->begin(), v->end());
-        sgc::copy_in(c, d_arr, packed.data(), packed.size());
+        sgc::copy_in_staged(c, d_arr, packed.data(), packed.size());
         auto col = [&](int k) { return d_arr + static_cast<size_t>(k) * M; };
         sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("dec_work", work.size());
-        sgc::copy_in(c, d_work, work.data(), work.size());
+        sgc::copy_in_staged(c, d_work, work.data(), work.size());
         float* d_logits = c->buf<float>("dec_logits", static_cast<size_t>(M) * SGC_VOCAB);
         int32_t* d_tok_out = c->buf<int32_t>("dec_tok", M);
         DecodeRows dr;
@@ -1033,9 +1033,9 @@ void ensure_hashes(Ctx* c, sgc_graph* g, uint64_t salt) {
     g->d_bucket = dalloc<uint32_t>(c, b.size());
     g->d_sign = dalloc<int8_t>(c, s.size());
     g->d_tok_off = dalloc<uint64_t>(c, off.size());
-    sgc::copy_in(c, g->d_bucket, b.data(), b.size());
-    sgc::copy_in(c, g->d_sign, s.data(), s.size());
-    sgc::copy_in(c, g->d_tok_off, off.data(), off.size());
+    sgc::copy_in_staged(c, g->d_bucket, b.data(), b.size());
+    sgc::copy_in_staged(c, g->d_sign, s.data(), s.size());
+    sgc::copy_in_staged(c, g->d_tok_off, off.data(), off.size());
     c->sync();
     g->hash_salt = salt;
 }
@@ -1275,7 +1275,7 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
     p.d = d;
     p.n0 = static_cast<int>(g0_node.size());
     uint32_t* d_g0 = c->buf<uint32_t>("gnn_g0", g0_node.size());
-    sgc::copy_in(c, d_g0, g0_node.data(), g0_node.size());
+    sgc::copy_in_staged(c, d_g0, g0_node.data(), g0_node.size());
     p.g0_node = d_g0;
     if (cfg.layers > 8) fail(SGC_DOMAIN, "gnn encoder supports at most 8 layers on this backend");
     for (uint32_t l = 0; l < cfg.layers; ++l) {
@@ -1285,17 +1285,17 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
         uint32_t* io = c->buf<uint32_t>(t + "_off", L.in_off.size());
         uint32_t* is = c->buf<uint32_t>(t + "_src", L.in_src.size());
         uint32_t* ig = c->buf<uint32_t>(t + "_gate", L.in_gate.size());
-        sgc::copy_in(c, sr, L.self_row.data(), L.self_row.size());
-        sgc::copy_in(c, io, L.in_off.data(), L.in_off.size());
-        sgc::copy_in(c, is, L.in_src.data(), L.in_src.size());
-        sgc::copy_in(c, ig, L.in_gate.data(), L.in_gate.size());
+        sgc::copy_in_staged(c, sr, L.self_row.data(), L.self_row.size());
+        sgc::copy_in_staged(c, io, L.in_off.data(), L.in_off.size());
+        sgc::copy_in_staged(c, is, L.in_src.data(), L.in_src.size());
+        sgc::copy_in_staged(c, ig, L.in_gate.data(), L.in_gate.size());
         p.layer[l] = {static_cast<int>(L.self_row.size()), sr, io, is, ig};
     }
     p.n_sub = static_cast<int>(nu);
     uint32_t* d_so = c->buf<uint32_t>("gnn_sub_off", sub_off.size());
     uint32_t* d_sr = c->buf<uint32_t>("gnn_sub_rows", gid.size());
-    sgc::copy_in(c, d_so, sub_off.data(), sub_off.size());
-    sgc::copy_in(c, d_sr, gid.data(), gid.size());
+    sgc::copy_in_staged(c, d_so, sub_off.data(), sub_off.size());
+    sgc::copy_in_staged(c, d_sr, gid.data(), gid.size());
     p.sub_off = d_so;
     p.sub_rows = d_sr;
     p.feat = feat;
@@ -1313,7 +1313,7 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
     c->gnn_node_instances = static_cast<uint64_t>(hs.nodes.size()) * cfg.layers;
     // unique subgraph embeddings -> every subgraph
     uint32_t* d_uo = c->buf<uint32_t>("gnn_uniq_of", count);
-    sgc::copy_in(c, d_uo, uniq_of.data(), count);
+    sgc::copy_in_staged(c, d_uo, uniq_of.data(), count);
     sgc::gather_rows(c, out_dev, uniq_out, d_uo, static_cast<int>(count), d);
     c->sync();
 }
@@ -1452,10 +1452,10 @@ RepResult build_reps(Ctx* c, sgc_graph* g, const HostSubs& hs, uint32_t count,
     uint64_t* d_noff = c->buf<uint64_t>("rep_noff", count + 1);
     uint32_t* d_edges = c->buf<uint32_t>("rep_edges_in", hs.eoff[count]);
     uint64_t* d_eoff = c->buf<uint64_t>("rep_eoff", count + 1);
-    sgc::copy_in(c, d_ids, hs.nodes.data(), total_nodes);
-    sgc::copy_in(c, d_noff, hs.noff.data(), count + 1);
-    sgc::copy_in(c, d_edges, hs.edges.data(), hs.eoff[count]);
-    sgc::copy_in(c, d_eoff, hs.eoff.data(), count + 1);
+    sgc::copy_in_staged(c, d_ids, hs.nodes.data(), total_nodes);
+    sgc::copy_in_staged(c, d_noff, hs.noff.data(), count + 1);
+    sgc::copy_in_staged(c, d_edges, hs.edges.data(), hs.eoff[count]);
+    sgc::copy_in_staged(c, d_eoff, hs.eoff.data(), count + 1);
     sgc::node_index(c, d_idx, d_ids, total_nodes, g->d_ids, static_cast<int>(g->n_nodes));
     std::vector<uint32_t> mem;
     std::vector<uint64_t> moff(1, 0);
@@ -1466,8 +1466,8 @@ RepResult build_reps(Ctx* c, sgc_graph* g, const HostSubs& hs, uint32_t count,
     }
     uint32_t* d_mem = c->buf<uint32_t>("rep_members", mem.size());
     uint64_t* d_moff = c->buf<uint64_t>("rep_moff", moff.size());
-    sgc::copy_in(c, d_mem, mem.data(), mem.size());
-    sgc::copy_in(c, d_moff, moff.data(), moff.size());
+    sgc::copy_in_staged(c, d_mem, mem.data(), mem.size());
+    sgc::copy_in_staged(c, d_moff, moff.data(), moff.size());
     const int nw = static_cast<int>((g->n_nodes + 31) / 32), ew = static_cast<int>((g->n_edges + 31) / 32);
     sgc::UnionArgs a;
     a.clusters = static_cast<int>(k);
@@ -1512,7 +1512,7 @@ RepResult build_reps(Ctx* c, sgc_graph* g, const HostSubs& hs, uint32_t count,
     }
     r.d_prefix = c->buf<int32_t>("rep_prefix", r.prefix_off.back());
     r.d_prefix_off = c->buf<uint64_t>("rep_prefix_off", k + 1);
-    sgc::copy_in(c, r.d_prefix_off, r.prefix_off.data(), k + 1);
+    sgc::copy_in_staged(c, r.d_prefix_off, r.prefix_off.data(), k + 1);
     const std::string h = std::string(kHeader) + kNodeHdr + "\n";
     const std::string eh = std::string(kEdgeHdr) + "\n";
     sgc::GatherArgs ga;
@@ -1592,6 +1592,8 @@ int sgc_ctx_destroy(sgc_ctx* ctx) {
             cudaEventDestroy(pe.second.second);
         }
         if (c->h_flags) cudaFreeHost(c->h_flags);
+        if (c->ring_base) cudaFreeHost(c->ring_base);
+        for (auto e : c->ring_ev) if (e) cudaEventDestroy(e);
         for (auto& kv : c->pinned_bufs) cudaFreeHost(kv.second.ptr);
         cudaStreamDestroy(c->own_stream);
         if (c->side) cudaStreamDestroy(c->side);
@@ -1852,9 +1854,9 @@ int sgc_retrieve(sgc_ctx* ctx, sgc_graph* g, const sgc_retrieval_config* cfg, ui
         uint32_t* d_qb = c->buf<uint32_t>("ret_qb", std::max<size_t>(1, qb.size()));
         int8_t* d_qs = c->buf<int8_t>("ret_qs", std::max<size_t>(1, qs.size()));
         uint64_t* d_qtok = c->buf<uint64_t>("ret_qtok", m + 1);
-        sgc::copy_in(c, d_qb, qb.data(), qb.size());
-        sgc::copy_in(c, d_qs, qs.data(), qs.size());
-        sgc::copy_in(c, d_qtok, qtok.data(), m + 1);
+        sgc::copy_in_staged(c, d_qb, qb.data(), qb.size());
+        sgc::copy_in_staged(c, d_qs, qs.data(), qs.size());
+        sgc::copy_in_staged(c, d_qtok, qtok.data(), m + 1);
         float* qf = c->buf<float>("ret_qf", static_cast<size_t>(std::max<uint32_t>(1, m)) * d);
         sgc::text_features(c, qf, d_qb, d_qs, d_qtok, static_cast<int>(m), g_enc[c].proj_t, d);
         // cosine scores of every (question, element): exact fp64 sums on the device
@@ -1984,9 +1986,9 @@ int sgc_retrieve(sgc_ctx* ctx, sgc_graph* g, const sgc_retrieval_config* cfg, ui
                 float* d_pool = c->buf<float>("ret_pool", static_cast<size_t>(n_ego) * d);
                 double* d_pd = c->buf<double>("ret_pd", n_ego);
                 double* d_ps = c->buf<double>("ret_ps", n_ego);
-                sgc::copy_in(c, d_moff, mem_off.data(), mem_off.size());
-                sgc::copy_in(c, d_midx, mem_idx.data(), mem_idx.size());
-                sgc::copy_in(c, d_eq, ego_q.data(), n_ego);
+                sgc::copy_in_staged(c, d_moff, mem_off.data(), mem_off.size());
+                sgc::copy_in_staged(c, d_midx, mem_idx.data(), mem_idx.size());
+                sgc::copy_in_staged(c, d_eq, ego_q.data(), n_ego);
                 sgc::ego_pool_dots(c, d_pool, d_pd, d_ps, feat, d_moff, d_midx, qf, d_eq, n_ego, d);
                 pdot = to_host(c, d_pd, n_ego);
                 psq = to_host(c, d_ps, n_ego);
@@ -2293,8 +2295,8 @@ int sgc_fork_fork(const sgc_fork* src, sgc_fork** out) {
         if (src->suffix) {
             const int n = static_cast<int>(src->suffix);
             int32_t* bt = c->buf<int32_t>("fork_copy_bt", 2 * f->pages.size());
-            sgc::copy_in(c, bt, src->pages.data(), src->pages.size());
-            sgc::copy_in(c, bt + f->pages.size(), f->pages.data(), f->pages.size());
+            sgc::copy_in_staged(c, bt, src->pages.data(), src->pages.size());
+            sgc::copy_in_staged(c, bt + f->pages.size(), f->pages.data(), f->pages.size());
             bf16* stage = c->buf<bf16>("fork_copy_stage", static_cast<size_t>(m->L) * n * m->d);
             const size_t ls = static_cast<size_t>(m->pool.pages) * sgc::kPageTokens * m->d;
             for (bf16* pool : {m->pool.k, m->pool.v}) {
@@ -2403,9 +2405,9 @@ int sgc_fork_extend(sgc_ctx* ctx, sgc_model* model, sgc_fork* const* forks, uint
         int32_t* d_arr = c->buf<int32_t>("fk_rows", static_cast<size_t>(M) * 4 + n + bt.size());
         std::vector<int32_t> packed;
         for (auto* v : {&toks, &pos, &seg_lo, &kvrow, &lrows, &bt}) packed.insert(packed.end(), v->begin(), v->end());
-        sgc::copy_in(c, d_arr, packed.data(), packed.size());
+        sgc::copy_in_staged(c, d_arr, packed.data(), packed.size());
         sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("fk_work", work.size());
-        sgc::copy_in(c, d_work, work.data(), work.size());
+        sgc::copy_in_staged(c, d_work, work.data(), work.size());
         float* d_logits = c->buf<float>("fk_logits", static_cast<size_t>(n) * SGC_VOCAB);
         const KvPool* pool = &model->pool;
         const size_t pls = static_cast<size_t>(pool->pages) * sgc::kPageTokens * d;
@@ -3488,7 +3490,7 @@ int sgc_attention_bf16(sgc_ctx* ctx, const void* q, const void* k_pfx, const voi
                 fail(SGC_DOMAIN, "attention: work unit out of range");
         }
         sgc::AttnWork* d_work = c->buf<sgc::AttnWork>("dbg_attn_work", n_work);
-        sgc::copy_in(c, d_work, w.data(), n_work);
+        sgc::copy_in_staged(c, d_work, w.data(), n_work);
         sgc::AttnParams ap;
         ap.q = static_cast<const bf16*>(q);
         ap.out = static_cast<bf16*>(out);

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <chrono>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -193,6 +194,43 @@ struct Ctx {
         }
         return reinterpret_cast<T*>(b.ptr);
     }
+    // Pinned staging ring for host -> device plan uploads (row maps, block tables, work lists):
+    // cudaMemcpyAsync from pageable memory synchronizes the stream first, so every per-wave /
+    // per-decode-step upload used to drain the GPU while the host kept planning. Copies out of the
+    // ring are truly asynchronous. The ring is 4 segments; an event recorded when the head leaves
+    // a segment guards its reuse, so the host only ever waits for copies enqueued a lap ago.
+    static constexpr int kRingSegs = 4;
+    uint8_t* ring_base = nullptr;
+    size_t ring_seg = 0, ring_head = 0;  // segment bytes; head offset in the whole ring
+    cudaEvent_t ring_ev[kRingSegs] = {};
+    bool ring_ev_live[kRingSegs] = {};
+    void* stage(const void* src, size_t bytes) {
+        const size_t need = (bytes + 255) & ~size_t(255);
+        if (need > ring_seg) {  // (re)allocate: nothing may still read the old ring
+            SGC_CUDA_CHECK(cudaStreamSynchronize(stream));
+            if (ring_base) SGC_CUDA_CHECK(cudaFreeHost(ring_base));
+            ring_seg = std::max<size_t>(need, 16ull << 20);
+            SGC_CUDA_CHECK(cudaMallocHost(&ring_base, ring_seg * kRingSegs));
+            for (int i = 0; i < kRingSegs; ++i) {
+                if (!ring_ev[i]) SGC_CUDA_CHECK(cudaEventCreateWithFlags(&ring_ev[i], cudaEventDisableTiming));
+                ring_ev_live[i] = false;
+            }
+            ring_head = 0;
+        }
+        const int seg = static_cast<int>(ring_head / ring_seg);
+        if (ring_head + need > static_cast<size_t>(seg + 1) * ring_seg) {  // move to the next segment
+            SGC_CUDA_CHECK(cudaEventRecord(ring_ev[seg], stream));
+            ring_ev_live[seg] = true;
+            const int nxt = (seg + 1) % kRingSegs;
+            if (ring_ev_live[nxt]) SGC_CUDA_CHECK(cudaEventSynchronize(ring_ev[nxt]));
+            ring_ev_live[nxt] = false;
+            ring_head = static_cast<size_t>(nxt) * ring_seg;
+        }
+        void* dst = ring_base + ring_head;
+        std::memcpy(dst, src, bytes);
+        ring_head += need;
+        return dst;
+    }
     // [next unit, finished fetchers] of the persistent kernels' dynamic scheduler (sched.cuh):
     // zeroed once, every kernel leaves it zeroed for the next one in the stream
     uint32_t* sched_ptr = nullptr;
@@ -235,6 +273,13 @@ struct Ctx {
 template <typename T>
 inline void copy_in(Ctx* c, T* dst_dev, const T* src, size_t n) {
     if (n) SGC_CUDA_CHECK(cudaMemcpyAsync(dst_dev, src, n * sizeof(T), cudaMemcpyDefault, c->stream));
+}
+// host (pageable) -> device through the context's pinned staging ring: no stream drain
+template <typename T>
+inline void copy_in_staged(Ctx* c, T* dst_dev, const T* src_host, size_t n) {
+    if (n)
+        SGC_CUDA_CHECK(cudaMemcpyAsync(dst_dev, c->stage(src_host, n * sizeof(T)), n * sizeof(T),
+                                       cudaMemcpyDefault, c->stream));
 }
 template <typename T>
 inline void copy_out(Ctx* c, T* dst, const T* src_dev, size_t n) {
