@@ -223,6 +223,8 @@ def run_ours(args, rank, world, local_rank):
         ctx.set_option("attn_kernel_partial", args.attn_kernel_partial)
     if args.gemm_raster is not None:
         ctx.set_option("gemm_raster", args.gemm_raster)
+    if args.gemm_streamk is not None:
+        ctx.set_option("gemm_streamk", args.gemm_streamk)
     t0 = time.time()
     lm = host.ToyLm(ctx, host.ToyLmConfig(**w.lm, seed=w.seed))
     dg = host.DeviceGraph(ctx, w.graph)
@@ -766,6 +768,8 @@ def main():
     ap.add_argument("--attn-split", type=int, default=None, help="1: two softmax warpgroups per query tile")
     ap.add_argument("--attn-kernel-partial", type=int, default=None,
                     help="decode steps' prefix attention: 1 one-tile kernel (default), 0 two-tile kernel")
+    ap.add_argument("--gemm-streamk", type=int, default=None,
+                    help="decode-step GEMMs on the stream-K pair kernel (A/B; library default 1)")
     ap.add_argument("--gemm-raster", type=int, default=None,
                     help="CTA-pair GEMM raster: 0 M-groups (default), 1 by estimated DRAM bytes, 2 N-groups")
     ap.add_argument("--attn-kernel", type=int, default=None,

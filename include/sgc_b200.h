@@ -373,7 +373,8 @@ int sgc_balance_members(const double* prefill_cost, uint32_t clusters, const uin
 /* ---- GEMM building block (exposed for parity tests and the roofline bench) -----------
  * D[M x N] = A[M x K] (bf16, row-major) * B[N x K]^T (bf16, row-major), fp32 accumulate in
  * TMEM via tcgen05.mma; epi 0 = store fp32 D, 1 = store bf16 D, 2 = D += into fp32 `d`,
- * 3 = bf16(tanh(D)). All pointers device. K % 64 == 0, N % 64 == 0. */
+ * 3 = bf16(tanh(D)); epi | 256 = a decode-step GEMM (few rows: the stream-K / split-K kernels
+ * may run, fp32 summation order differs). All pointers device. K % 64 == 0, N % 64 == 0. */
 int sgc_gemm_bf16(sgc_ctx* ctx, const void* a, const void* b, void* d, uint32_t M, uint32_t N,
                   uint32_t K, int epi);
 /* ---- cascade attention building block (parity tests at full size; lm_core.cpp:246-274) ----
@@ -396,12 +397,20 @@ int sgc_probe_fp64_tflops(sgc_ctx* ctx, double* tflops);
 int sgc_gnn_stats(const sgc_ctx* ctx, uint64_t* state_rows, uint64_t* node_instances);
 /* Enable/disable per-kernel CUDA-event timing; sgc_get_timing reads the accumulated totals. */
 int sgc_set_timing(sgc_ctx* ctx, int enable);
-/* Tuning knobs: "gemm_pairs" (1 = CTA-pair tcgen05 GEMM for 256-wide tiles, default; 0 = 1-CTA);
+/* Tuning knobs (A/B switches; the defaults are the measured best):
+ * "gemm_pairs" (1 = CTA-pair tcgen05 GEMM for 256-wide tiles, default; 0 = 1-CTA);
+ * "gemm_raster" (CTA-pair raster: 0 = M-groups, default; 1 = by estimated DRAM bytes; 2 = N-groups);
+ * "gemm_streamk" (decode-step GEMMs on the stream-K CTA-pair kernel: 1 = where measured faster,
+ * default; 2 = every decode shape; 0 = off);
  * "decode_defer_pct" (generation: a wave decodes on its own until fewer than this percentage of
  * its queries still generate, the stragglers of every wave then finish in one shared loop;
  * default 25, 0 = each wave to completion, >= 100 = all decoding after the last wave);
  * "attn_split" (1 = two softmax warpgroups per query tile; default 0);
- * "gnn_tile" (GNN layer-map FP64 GEMM tile: 0 = 64x64, 1 = 64x128 (default), 2 = 128x128).
+ * "attn_kernel" / "attn_kernel_partial" (tcgen05 attention for prefill / extend and for the
+ * decode prefix partials: 0 = two-tile kernel, 1 = one-tile S-triple-buffered kernel; defaults
+ * 0 / 1);
+ * "gnn_tile" (GNN layer-map FP64 GEMM: 0 = 64x64, 1 = 64x128, 2 = 128x128 DFMA tiles, 3 = DMMA
+ * tensor pipe, default); "gnn_dedup" (1 = identical node states computed once, default).
  * Unknown names return SGC_DOMAIN. */
 int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value);
 int sgc_get_timing(sgc_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches);

@@ -382,6 +382,7 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
         e.rope_sin = m->rope_sin;
         e.d = d;
         e.hd = m->hd;
+        e.splitk_ok = b.dec != nullptr;  // decode step: stream-K / split-K allowed
         sgc::gemm_bf16(c, xb, m->wqkv[l], M, 3 * d, d, e);
         // last layer: K/V of every row are written now; the rest of the layer only feeds the
         // head, so rows without logits skip it (values nothing reads: a prefill without logits
@@ -489,6 +490,7 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
         t.ldo = m->ffn;
         sgc::rms_scale(c, rs, ss_b, M, parts, d);
         t.row_scale = rs;
+        t.splitk_ok = b.dec != nullptr;
         sgc::gemm_bf16(c, xb, m->w1[l], M, m->ffn, d, t);
         r.out_ss = last ? nullptr : ss_a;  // the next layer's QKV input
         if (last) r.out_xb = nullptr;
@@ -3463,6 +3465,8 @@ int sgc_lpt_assign(const double* cost, uint32_t clusters, int world_size, uint32
 int sgc_gemm_bf16(sgc_ctx* ctx, const void* a, const void* b, void* d, uint32_t M, uint32_t N, uint32_t K, int epi) {
     return guarded([&] {
         sgc::GemmEpi e;
+        e.splitk_ok = (epi & 256) != 0;  // decode-step GEMM: stream-K / split-K allowed
+        epi &= 255;
         e.mode = epi;
         e.out = d;
         e.ldo = static_cast<int>(N);
@@ -3517,6 +3521,7 @@ int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value) {
     return guarded([&] {
         if (std::string(name) == "gemm_pairs") sgc::gemm_set_pairs(value != 0);
         else if (std::string(name) == "gemm_raster") sgc::gemm_set_raster(static_cast<int>(value));
+        else if (std::string(name) == "gemm_streamk") sgc::gemm_set_streamk(static_cast<int>(value));
         else if (std::string(name) == "attn_split") sgc::attention_set_split(value != 0);
         else if (std::string(name) == "attn_kernel") sgc::attention_set_kernel(static_cast<int>(value));
         else if (std::string(name) == "attn_kernel_partial") sgc::attention_set_kernel_partial(static_cast<int>(value));

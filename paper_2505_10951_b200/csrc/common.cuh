@@ -241,6 +241,10 @@ struct Ctx {
         }
         return sched_ptr;
     }
+    // stream-K GEMM ready flags (one per CTA of the largest grid, zeroed once) and the launch
+    // sequence number they are compared against
+    uint32_t* sk_flags = nullptr;
+    uint32_t sk_seq = 0;
     // device [0, 1, ..., n-1] (grown on demand, filled on the device: no host round trip)
     int32_t* iota(int n);
     int iota_n = 0;

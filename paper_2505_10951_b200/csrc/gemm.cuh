@@ -35,6 +35,11 @@ struct GemmEpi {
     // summation order, so prefill / extend rows never take it: their results stay
     // independent of how rows are grouped into calls)
     bool splitk_ok = false;
+    // stream-K (set by the dispatcher): fp32 partial slots of the pairs, their ready flags and
+    // this launch's sequence number
+    float* sk_ws = nullptr;
+    uint32_t* sk_flags = nullptr;
+    uint32_t sk_seq = 0;
 };
 
 void gemm_bf16(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep);
@@ -42,5 +47,8 @@ void gemm_bf16(Ctx* c, const void* A, const void* B, int M, int N, int K, const 
 void gemm_set_pairs(bool on);
 // CTA-pair GEMM raster: 0 M-groups (default), 1 chosen by estimated DRAM bytes, 2 N-groups
 void gemm_set_raster(int mode);
+// decode-step GEMMs (splitk_ok) on a stream-K CTA-pair kernel: 1 = on (default), 0 = split-K
+// residual planes / 1-wave tiles
+void gemm_set_streamk(int mode);
 
 }  // namespace sgc

@@ -154,12 +154,59 @@ __device__ __forceinline__ void rope_pair(float* lo, float* hi, const float* cos
     }
 }
 
+// stream-K (decode GEMMs): earlier K segments of this tile, written by other CTA pairs as fp32
+// slots laid out [column / 4][128 rows of the CTA][4] (a warp moves 512 contiguous bytes per
+// 16-byte access, thread = row); the tile's last segment adds them, in pair order, before its
+// fused epilogue
+struct PartIn {
+    const float* base = nullptr;  // slot of the first contributing pair, this CTA's half
+    int n = 0;                    // contributing pairs
+    int stride = 0;               // floats between consecutive pairs' slots
+};
+constexpr int kSkSlot = 128 * 256;  // floats per CTA per slot (128 rows x BN 256)
+__device__ __forceinline__ const float4* sk_at(const float* slot, int ch, int j4, int rr) {
+    return reinterpret_cast<const float4*>(slot) + (ch * 8 + j4) * 128 + rr;
+}
+__device__ __forceinline__ void add_parts(const PartIn& pin, uint32_t* r, int ch) {
+    if (pin.n == 0) return;
+    const int rr = ((threadIdx.x >> 5) & 3) * 32 + (threadIdx.x & 31);
+    for (int q = 0; q < pin.n; q += 2) {  // two contributors' loads in flight, added in order
+        const bool two = q + 1 < pin.n;
+        float4 v0[8], v1[8];
+        const float* s0 = pin.base + static_cast<size_t>(q) * pin.stride;
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) v0[j4] = __ldcg(sk_at(s0, ch, j4, rr));
+        if (two) {
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) v1[j4] = __ldcg(sk_at(s0 + pin.stride, ch, j4, rr));
+        }
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+            float* f = reinterpret_cast<float*>(r + 4 * j4);
+            f[0] += v0[j4].x;
+            f[1] += v0[j4].y;
+            f[2] += v0[j4].z;
+            f[3] += v0[j4].w;
+        }
+        if (two) {
+#pragma unroll
+            for (int j4 = 0; j4 < 8; ++j4) {
+                float* f = reinterpret_cast<float*>(r + 4 * j4);
+                f[0] += v1[j4].x;
+                f[1] += v1[j4].y;
+                f[2] += v1[j4].z;
+                f[3] += v1[j4].w;
+            }
+        }
+    }
+}
+
 // Epilogue of one 128 x BN accumulator tile held in TMEM (lanes = rows): `tbase` addresses
 // this warp's 32 lanes at the tile's first column, `row` is this thread's output row.
 template <int BN, int EPI, int HD>
 __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool valid, int n0,
                                               const GemmEpi& ep, int ch_lo, int ch_hi, float* stage,
-                                              int ep_rows) {
+                                              int ep_rows, const PartIn& pin = PartIn{}) {
     // fused RMSNorm of the A rows: one scale per accumulator row
     float inv = 1.0f;
     if (ep.row_scale && valid) inv = ep.row_scale[row];
@@ -180,6 +227,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                 uint32_t r[32];
                 ptx::tmem_ld32(tbase + ch * 32, r);
                 ptx::tmem_ld_wait();
+                add_parts(pin, r, ch);
                 if (valid) {
                     float* v = reinterpret_cast<float*>(r);
 #pragma unroll
@@ -213,6 +261,8 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                     ptx::tmem_ld32(tbase + ch * 32, lo);
                     ptx::tmem_ld32(tbase + ch2 * 32, hi);
                     ptx::tmem_ld_wait();
+                    add_parts(pin, lo, ch);
+                    add_parts(pin, hi, ch2);
                     if (valid) {
 #if SGC_ROPE_PACKED
                         // RMSNorm scale + RoPE on packed fp32 pairs (FMUL2 / FFMA2): the epilogue's
@@ -255,6 +305,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                     uint32_t r[32];
                     ptx::tmem_ld32(tbase + ch * 32, r);
                     ptx::tmem_ld_wait();
+                    add_parts(pin, r, ch);
                     if (valid) {
                         float* v = reinterpret_cast<float*>(r);
 #pragma unroll
@@ -291,6 +342,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                 uint32_t r[32];
                 ptx::tmem_ld32(tbase + ch * 32, r);
                 ptx::tmem_ld_wait();
+                add_parts(pin, r, ch);
                 if (!valid) continue;
                 float* v = reinterpret_cast<float*>(r);
 #pragma unroll
@@ -332,6 +384,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
                 uint32_t r[32];
                 ptx::tmem_ld32(tbase + ch * 32, r);
                 ptx::tmem_ld_wait();
+                add_parts(pin, r, ch);
                 // 16-byte staging with an XOR swizzle of the 4-float groups (row r's group k at
                 // k ^ (r & 7)): STS.128 / LDS.128, conflict-free on both sides, no padding
                 float4* st4 = reinterpret_cast<float4*>(stage);
@@ -416,6 +469,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
             uint32_t r[32];
             ptx::tmem_ld32(tbase + ch * 32, r);
             ptx::tmem_ld_wait();
+            add_parts(pin, r, ch);
             float* v = reinterpret_cast<float*>(r);
             if constexpr (EPI != EPI_RESID) {
 #pragma unroll
@@ -841,6 +895,264 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
 }
 
+// ---- stream-K CTA-pair variant (decode steps) ----------------------------------------------
+// A decode step has few rows (M <= 512), so the pair-tiles (48 for the QKV weights) cannot fill
+// the 74 SM pairs and every weight byte is streamed by only 2/3 of the SMs. Here the
+// (tile, k-block) space is cut into one equal contiguous range per pair: a pair's range is a run
+// of segments (tile, k-block range). The tile's LAST segment owns the fused epilogue; every
+// earlier segment of that tile (at most one per pair: the one that ends its range) stores its
+// fp32 accumulator to the pair's workspace slot and raises a flag (this launch's sequence
+// number). Each pair processes that partial segment FIRST, so no flag depends on another wait:
+// all pairs are resident (grid <= SM pairs) and the owners' waits always resolve. The owner adds
+// the partials in pair order (deterministic for a given shape) before the usual epilogue.
+struct SkRange {
+    int lo, hi;  // [lo, hi) over the tiles x k-blocks space
+};
+__device__ __forceinline__ SkRange sk_range(int p, int P, int W) {
+    return {static_cast<int>(static_cast<int64_t>(p) * W / P), static_cast<int>(static_cast<int64_t>(p + 1) * W / P)};
+}
+struct SkSeg {
+    int t, kb0, kb1;  // tile, k-blocks [kb0, kb1) within the tile
+    int kind;         // 0 whole tile, 1 partial (ends before the tile does), 2 owner (adds partials)
+    int q0;           // owner: first contributing pair (contributors q0 .. p-1)
+};
+__device__ __forceinline__ int sk_nseg(const SkRange& r, int KB) { return (r.hi - 1) / KB - r.lo / KB + 1; }
+// i-th segment in PROCESSING order: the range's trailing partial (if any) first
+__device__ __forceinline__ SkSeg sk_seg(int p, int P, int W, int KB, const SkRange& r, int i) {
+    const int n = sk_nseg(r, KB);
+    const bool tail_partial = r.hi % KB != 0;
+    const int nat = tail_partial ? (i == 0 ? n - 1 : i - 1) : i;
+    const int t = r.lo / KB + nat;
+    const int a = max(r.lo, t * KB), b = min(r.hi, (t + 1) * KB);
+    SkSeg s;
+    s.t = t;
+    s.kb0 = a - t * KB;
+    s.kb1 = b - t * KB;
+    s.q0 = p;
+    if (b < (t + 1) * KB) s.kind = 1;
+    else if (a > t * KB) {
+        s.kind = 2;
+        int q = p - 1;  // ranges are non-empty (P <= W): walk back to the pair holding k-block t*KB
+        while (q > 0 && sk_range(q, P, W).lo > t * KB) --q;
+        s.q0 = q;
+    } else s.kind = 0;
+    return s;
+}
+
+#ifdef SGC_SK_PROF  // A/B builds only: per-CTA phase cycles of the stream-K kernel (scripts/sk_prof.py)
+}  // namespace
+__device__ unsigned long long g_sk_prof[148 * 32];
+namespace {
+#define SK_T0(v) const long long v = clock64()
+#define SK_ACC(slot, t0) atomicAdd(&g_sk_prof[(blockIdx.x % 148) * 32 + (slot)], (unsigned long long)(clock64() - (t0)))
+#else
+#define SK_T0(v)
+#define SK_ACC(slot, t0)
+#endif
+template <int EPI, int HD>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2_sk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    int M, int N, int K, GemmEpi ep) {
+    constexpr int BN = 256;
+    SK_T0(t_start);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* smemA = smem;
+    uint8_t* smemB = smem + kStages2 * Cfg2::kABytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages2 * Cfg2::kStageBytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kStages2;
+    uint64_t* tfull = bars + 2 * kStages2;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const int P = gridDim.x >> 1, p = blockIdx.x >> 1;
+    const int m_tiles = (M + 2 * BM - 1) / (2 * BM);
+    const int n_tiles = N / BN;
+    const int KB = K / BK;
+    const int W = m_tiles * n_tiles * KB;
+    const SkRange rg = sk_range(p, P, W);
+    const int nseg = sk_nseg(rg, KB);
+    // tile t -> (m0, n0): m-tiles of one weight tile adjacent (its second read hits L2)
+    auto tile_coords = [&](int t, int& m0, int& n0) {
+        m0 = (t % m_tiles) * 2 * BM;
+        n0 = (t / m_tiles) * BN;
+    };
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+        for (int s = 0; s < kStages2; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 2 * kEpiThreads);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc_2sm<512>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 128) SK_ACC(0, t_start);
+    SK_T0(t_main);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint64_t keep = ptx::policy_evict_last();  // A is re-read by every pair
+            const uint64_t stream = ptx::policy_evict_first();  // each weight byte is read once
+            for (int i = 0; i < nseg; ++i) {
+                const SkSeg sg = sk_seg(p, P, W, KB, rg, i);
+                int m0, n0;
+                tile_coords(sg.t, m0, n0);
+                for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
+                    SK_T0(t_w);
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    SK_ACC(8, t_w);
+#ifdef SGC_SK_NOLOAD  // A/B builds only: the MMA side alone
+                    if (leader) ptx::mbar_arrive(&full[stage]);
+                    (void)keep;
+                    (void)stream;
+#else
+                    if (leader) ptx::mbar_expect_tx(&full[stage], 2 * Cfg2::kStageBytes);
+                    ptx::tma_load_2d_2sm_hint(smemA + stage * Cfg2::kABytes, &tmA, &full[stage], kb * BK,
+                                              m0 + rank * BM, keep);
+                    ptx::tma_load_2d_2sm_hint(smemB + stage * Cfg2::kBBytes, &tmB, &full[stage], kb * BK,
+                                              n0 + rank * BM, m_tiles > 1 ? keep : stream);
+#endif
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_bf16_f32(2 * BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int i = 0; i < nseg; ++i) {
+                const SkSeg sg = sk_seg(p, P, W, KB, rg, i);
+                const int acc = i & 1;
+                const uint32_t acc_phase = (i >> 1) & 1;
+                ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t tmem_d = tmem_base + acc * BN;
+                for (int kb = sg.kb0; kb < sg.kb1; ++kb) {
+                    SK_T0(t_w);
+                    ptx::mbar_wait(&full[stage], phase);
+                    SK_ACC(6, t_w);
+                    ptx::tc_fence_after();
+                    const uint32_t a_addr = ptx::smem_u32(smemA + stage * Cfg2::kABytes);
+                    const uint32_t b_addr = ptx::smem_u32(smemB + stage * Cfg2::kBBytes);
+#ifndef SGC_SK_NOMMA  // A/B builds only: the operand stream alone
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        ptx::mma_bf16_2sm(tmem_d, ptx::umma_desc_sw128(a_addr + k * 32),
+                                          ptx::umma_desc_sw128(b_addr + k * 32), idesc, (kb != sg.kb0) | (k != 0));
+#else
+                    (void)a_addr;
+                    (void)b_addr;
+                    (void)idesc;
+#endif
+                    ptx::mma_commit_2sm(&empty[stage], 0x3);
+                    if (++stage == kStages2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                ptx::mma_commit_2sm(&tfull[acc], 0x3);
+            }
+            SK_ACC(7, t_main);
+        }
+    } else if (warp >= 4) {
+        const int ew = warp & 3, eg = (warp - 4) / 4;
+        int ch_lo, ch_hi;
+        epi_chunks<BN, EPI, HD>(eg, ch_lo, ch_hi);
+        float* stage = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars) + kBarBytes) + (warp - 4) * 32 * 33;
+        const int rr = ew * 32 + lane;  // this thread's row within the CTA's 128
+        for (int i = 0; i < nseg; ++i) {
+            const SkSeg sg = sk_seg(p, P, W, KB, rg, i);
+            int m0, n0;
+            tile_coords(sg.t, m0, n0);
+            const int acc = i & 1;
+            const uint32_t acc_phase = (i >> 1) & 1;
+            SK_T0(t_w);
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            if (threadIdx.x == 128) SK_ACC(1, t_w);
+            SK_T0(t_e);
+            ptx::tc_fence_after();
+            const uint32_t tbase = tmem_base + ((ew * 32) << 16) + acc * BN;
+            if (sg.kind == 1) {
+                // partial: raw fp32 accumulator -> this pair's slot (both warpgroups, 4 chunks each)
+                float* slot = ep.sk_ws + static_cast<size_t>(2 * p + rank) * kSkSlot;
+#pragma unroll 1
+                for (int ch = eg * 4; ch < eg * 4 + 4; ++ch) {
+                    uint32_t r[32];
+                    ptx::tmem_ld32(tbase + ch * 32, r);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; ++j4)
+                        __stcg(const_cast<float4*>(sk_at(slot, ch, j4, rr)),
+                               make_float4(__uint_as_float(r[4 * j4]), __uint_as_float(r[4 * j4 + 1]),
+                                           __uint_as_float(r[4 * j4 + 2]), __uint_as_float(r[4 * j4 + 3])));
+                }
+                ptx::tc_fence_before();
+                ptx::mbar_arrive_cluster(&tempty[acc], 0);
+                // every epilogue thread of this CTA stored -> publish (release, GPU scope)
+                __threadfence();
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+                if (warp == 4 && lane == 0) {
+                    __threadfence();
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ep.sk_flags + 2 * p + rank), "r"(ep.sk_seq)
+                                 : "memory");
+                }
+                if (threadIdx.x == 128) SK_ACC(4, t_e);
+                continue;
+            }
+            PartIn pin;
+            if (sg.kind == 2) {
+                for (int q = sg.q0; q < p; ++q) {
+                    const uint32_t* f = ep.sk_flags + 2 * q + rank;
+                    uint32_t v;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+                    } while (v != ep.sk_seq);
+                }
+                pin.base = ep.sk_ws + static_cast<size_t>(2 * sg.q0 + rank) * kSkSlot;
+                pin.n = p - sg.q0;
+                pin.stride = 2 * kSkSlot;
+                if (threadIdx.x == 128) SK_ACC(2, t_e);
+            }
+            SK_T0(t_ep);
+            const int row = m0 + static_cast<int>(rank) * BM + rr;
+            epilogue_tile<BN, EPI, HD>(tbase, row, row < M, n0, ep, ch_lo, ch_hi, stage, M, pin);
+            ptx::tc_fence_before();
+            ptx::mbar_arrive_cluster(&tempty[acc], 0);
+            if (threadIdx.x == 128) SK_ACC(sg.kind == 2 ? 3 : 9, t_ep);
+        }
+        if (threadIdx.x == 128) SK_ACC(5, t_main);
+    }
+
+    __syncthreads();
+    ptx::cluster_sync();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_2sm<512>(tmem_base);
+    }
+}
+
 // ---- host side ----------------------------------------------------------------------------
 
 // CUDA-event timing category per fused epilogue (bench.py sums "gemm*" for the roofline)
@@ -906,6 +1218,60 @@ void launch2(Ctx* c, const void* A, const void* B, int M, int N, int K, const Ge
 }
 
 bool g_gemm_pairs = true;  // CTA-pair kernel for large tiles (sgc_set_gemm_pairs toggles)
+int g_gemm_streamk = 1;    // decode GEMMs on the stream-K pair kernel (sgc_set_option "gemm_streamk"; 2 = every decode shape)
+
+// decode-step GEMM on the stream-K pair kernel: one equal (tile, k-block) range per SM pair
+template <int EPI, int HD>
+void launch2_sk(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
+    static bool attr_set = false;
+    auto kfn = gemm2_sk_kernel<EPI, HD>;
+    if (!attr_set) {
+        SGC_CUDA_CHECK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg2::kSmem));
+        attr_set = true;
+    }
+    CUtensorMap ta = make_map_2d(A, M, K, BM, BK);
+    CUtensorMap tb = make_map_2d(B, N, K, BM, BK);
+    // one pair per co-resident cluster slot: a pair launched only after others retire would
+    // serialize its owners' waits behind a second wave (the GPCs' SM counts are not all even,
+    // so fewer than num_sms / 2 pairs fit at once)
+    static int max_pairs = 0;
+    if (!max_pairs) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr;
+        attr.id = cudaLaunchAttributeClusterDimension;
+        attr.val.clusterDim.x = 2;
+        attr.val.clusterDim.y = 1;
+        attr.val.clusterDim.z = 1;
+        cfg.gridDim = dim3(c->num_sms & ~1);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = Cfg2::kSmem;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        SGC_CUDA_CHECK(cudaOccupancyMaxActiveClusters(&n, kfn, &cfg));
+        max_pairs = std::max(1, std::min(n, c->num_sms / 2));
+        if (std::getenv("SGC_TRACE_SK")) std::fprintf(stderr, "stream-K: %d co-resident CTA pairs\n", n);
+    }
+    const int m_tiles = (M + 2 * BM - 1) / (2 * BM);
+    const int W = m_tiles * (N / 256) * (K / BK);
+    const int P = std::min(max_pairs, W);
+    if (!c->sk_flags) {
+        c->sk_flags = c->buf<uint32_t>("gemm_sk_flags", 512);
+        SGC_CUDA_CHECK(cudaMemsetAsync(c->sk_flags, 0, 512 * sizeof(uint32_t), c->stream));
+    }
+    if (2 * P > 512) fail(SGC_DOMAIN, "gemm: stream-K grid exceeds its flag array");
+    GemmEpi e = ep;
+    e.sk_ws = c->buf<float>("gemm_sk_ws", static_cast<size_t>(2 * P) * kSkSlot);
+    e.sk_flags = c->sk_flags;
+    e.sk_seq = ++c->sk_seq;
+    if (e.sk_seq == 0) e.sk_seq = ++c->sk_seq;  // 0 is the flags' initial value
+    if (std::getenv("SGC_TRACE_SK"))
+        std::fprintf(stderr, "stream-K launch: M %d N %d K %d W %d P %d seq %u ws %p flags %p\n", M, N, K, W, P, e.sk_seq,
+                     (void*)e.sk_ws, (void*)e.sk_flags);
+    Ctx::Timed timer(c, gemm_timer_name(EPI));
+    kfn<<<2 * P, kThreads, Cfg2::kSmem, c->stream>>>(ta, tb, M, N, K, e);
+    SGC_LAUNCH_CHECK(c);
+}
 
 // split-K residual for decode-sized GEMMs: x += sum_s partial[s] in a fixed order, then bf16(x)
 // and the row's sum of squares for the next GEMM's fused RMSNorm (one CTA per row)
@@ -954,6 +1320,17 @@ void dispatch_bn(Ctx* c, const void* A, const void* B, int M, int N, int K, cons
     // widest tile that divides N (and d, for the QKV section split)
     int lim = EPI == EPI_QKV ? ep.d : N;
     const int m_tiles = (M + BM - 1) / BM;
+    // decode steps: stream-K over all SM pairs where it measured faster in the C3 generation run
+    // (scripts/decode_probe.py): the FFN activation GEMM at <= 128 and 257-512 rows, the residual
+    // GEMMs at 257-512 rows (<= 256 rows keep their split-K planes, whose fixed-order reduction
+    // beats a 4-5-way stream-K fixup); never the QKV GEMM, whose RoPE / K-V scatter epilogue then
+    // runs on the owners' critical path over a 256-column tile (57 vs 40 us per launch)
+    const bool sk_rows = EPI != EPI_QKV && (M > 2 * BM || (M <= BM && EPI != EPI_RESID));
+    if (g_gemm_streamk && ep.splitk_ok && g_gemm_pairs && (sk_rows || g_gemm_streamk == 2) && M <= 4 * BM && N % 256 == 0 && lim % 256 == 0 &&
+        N >= 2048 && K >= 1024 && HD <= 128) {
+        launch2_sk<EPI, HD>(c, A, B, M, N, K, ep);
+        return;
+    }
     if constexpr (EPI == EPI_RESID) {
         // decode-sized residual GEMMs (N = d): too few output tiles to stream the weight matrix at
         // full bandwidth -> 4-way split-K into fp32 planes + a fixed-order reduction
@@ -1002,6 +1379,7 @@ void dispatch_bn(Ctx* c, const void* A, const void* B, int M, int N, int K, cons
 
 void gemm_set_pairs(bool on) { g_gemm_pairs = on; }
 void gemm_set_raster(int mode) { g_gemm_raster = mode; }
+void gemm_set_streamk(int mode) { g_gemm_streamk = mode; }
 
 void gemm_bf16(Ctx* c, const void* A, const void* B, int M, int N, int K, const GemmEpi& ep) {
     if (M <= 0) return;
@@ -1023,3 +1401,15 @@ void gemm_bf16(Ctx* c, const void* A, const void* B, int M, int N, int K, const 
 }
 
 }  // namespace sgc
+
+#ifdef SGC_SK_PROF
+extern "C" int sgc_debug_sk_prof(unsigned long long* out, int reset) {
+    if (reset) {
+        static unsigned long long z[148 * 32] = {};
+        cudaMemcpyToSymbol(sgc::g_sk_prof, z, sizeof(z));
+    } else {
+        cudaMemcpyFromSymbol(out, sgc::g_sk_prof, sizeof(unsigned long long) * 148 * 32);
+    }
+    return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
+}
+#endif

@@ -80,6 +80,39 @@ def test_gemm_tcgen05_vs_torch(ctx, M, N, K, epi, pairs):
     assert rel <= tol, f"rel err {rel}"
 
 
+@pytest.mark.parametrize("M", [1, 77, 128, 200, 256, 300, 512])
+@pytest.mark.parametrize("N,K", [(12288, 4096), (4096, 4096), (2048, 14336)])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_gemm_decode_streamk_vs_torch(ctx, M, N, K, epi):
+    """Decode-step GEMMs (epi | 256) on the stream-K CTA-pair kernel: partial K segments of a tile
+    written by other SM pairs are added by the tile's owner before the fused epilogue. Checked
+    against an fp32 torch product and, bit for bit, against a second run (the decomposition is
+    fixed for a shape, so the result is deterministic)."""
+    torch = pytest.importorskip("torch")
+    g = torch.Generator(device="cuda").manual_seed(M * 13 + N + K + epi)
+    a = (torch.randn(M, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    b = (torch.randn(N, K, device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    ref = a.float() @ b.float().t()
+    dt = torch.float32 if epi in (0, 2) else torch.bfloat16
+    base = torch.randn(M, N, device="cuda", generator=g) if epi == 2 else torch.zeros(M, N, device="cuda")
+    if epi == 2:
+        ref = ref + base
+    if epi == 3:
+        ref = torch.tanh(ref)
+    outs = []
+    for _ in range(2):
+        d = base.clone().to(dt)
+        torch.cuda.synchronize()  # the context's stream is not torch's
+        ctx.gemm(a.data_ptr(), b.data_ptr(), d.data_ptr(), M, N, K, epi | 256)
+        torch.cuda.synchronize()
+        outs.append(d.float())
+    got = outs[0]
+    tol = 2e-2 if epi in (1, 3) else 1e-3 * max(1.0, (K / 64) ** 0.5)
+    rel = (got - ref).abs().max().item() / max(1.0, ref.abs().max().item())
+    assert rel <= tol, f"rel err {rel}"
+    assert torch.equal(outs[0], outs[1]), "stream-K result not deterministic"
+
+
 # ------------------------------------------------------------------------ weights
 
 def test_weights_bit_exact_vs_oracle(ctx):
