@@ -162,13 +162,14 @@ struct PartIn {
     const float* base = nullptr;  // slot of the first contributing pair, this CTA's half
     int n = 0;                    // contributing pairs
     int stride = 0;               // floats between consecutive pairs' slots
+    bool valid = true;            // this thread's row exists (rows past M were never stored)
 };
 constexpr int kSkSlot = 128 * 256;  // floats per CTA per slot (128 rows x BN 256)
 __device__ __forceinline__ const float4* sk_at(const float* slot, int ch, int j4, int rr) {
     return reinterpret_cast<const float4*>(slot) + (ch * 8 + j4) * 128 + rr;
 }
 __device__ __forceinline__ void add_parts(const PartIn& pin, uint32_t* r, int ch) {
-    if (pin.n == 0) return;
+    if (pin.n == 0 || !pin.valid) return;
     const int rr = ((threadIdx.x >> 5) & 3) * 32 + (threadIdx.x & 31);
     for (int q = 0; q < pin.n; q += 2) {  // two contributors' loads in flight, added in order
         const bool two = q + 1 < pin.n;
@@ -1095,13 +1096,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::tc_fence_after();
             const uint32_t tbase = tmem_base + ((ew * 32) << 16) + acc * BN;
             if (sg.kind == 1) {
-                // partial: raw fp32 accumulator -> this pair's slot (both warpgroups, 4 chunks each)
+                // partial: raw fp32 accumulator -> this pair's slot (both warpgroups, 4 chunks each);
+                // rows past M are neither stored nor read back
                 float* slot = ep.sk_ws + static_cast<size_t>(2 * p + rank) * kSkSlot;
+                const bool row_ok = m0 + static_cast<int>(rank) * BM + rr < M;
 #pragma unroll 1
                 for (int ch = eg * 4; ch < eg * 4 + 4; ++ch) {
                     uint32_t r[32];
                     ptx::tmem_ld32(tbase + ch * 32, r);
                     ptx::tmem_ld_wait();
+                    if (!row_ok) continue;
 #pragma unroll
                     for (int j4 = 0; j4 < 8; ++j4)
                         __stcg(const_cast<float4*>(sk_at(slot, ch, j4, rr)),
@@ -1133,6 +1137,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 pin.base = ep.sk_ws + static_cast<size_t>(2 * sg.q0 + rank) * kSkSlot;
                 pin.n = p - sg.q0;
                 pin.stride = 2 * kSkSlot;
+                pin.valid = m0 + static_cast<int>(rank) * BM + rr < M;
                 if (threadIdx.x == 128) SK_ACC(2, t_e);
             }
             SK_T0(t_ep);
