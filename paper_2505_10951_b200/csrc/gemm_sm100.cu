@@ -967,6 +967,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t* tfull = bars + 2 * kStages2;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* pub = tempty + 3;  // this CTA's epilogue threads stored the pair's partial
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     const uint32_t rank = ptx::cluster_ctarank();
@@ -995,6 +996,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&tfull[a], 1);
             ptx::mbar_init(&tempty[a], 2 * kEpiThreads);
         }
+        ptx::mbar_init(pub, kEpiThreads);  // one phase: a pair stores at most one partial per launch
         ptx::fence_barrier_init();
     }
     if (warp == 2) ptx::tmem_alloc_2sm<512>(tmem_slot);
@@ -1116,8 +1118,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 ptx::mbar_arrive_cluster(&tempty[acc], 0);
                 // every epilogue thread of this CTA stored -> publish (release, GPU scope)
                 __threadfence();
-                asm volatile("bar.sync 1, 256;" ::: "memory");
+                ptx::mbar_arrive(pub);
                 if (warp == 4 && lane == 0) {
+                    ptx::mbar_wait(pub, 0);
                     __threadfence();
                     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ep.sk_flags + 2 * p + rank), "r"(ep.sk_seq)
                                  : "memory");
