@@ -339,8 +339,11 @@ void cascade_attention(Ctx* c, const AttnParams& p, int n_work, int heads, int h
 // tokens. Finally merged with the prefix partial:
 //   out = (O1 2^(lse1 - M) + acc 2^(m2 - M)) / (2^(lse1 - M) + l2 2^(m2 - M)).
 namespace {
+#ifndef SGC_DECODE_LOCAL_MINB
+#define SGC_DECODE_LOCAL_MINB 1
+#endif
 template <int HD>
-__global__ void __launch_bounds__(256) decode_local_kernel(DecodeAttnParams p) {
+__global__ void __launch_bounds__(256, SGC_DECODE_LOCAL_MINB) decode_local_kernel(DecodeAttnParams p) {
     constexpr int DPL = HD >= 32 ? HD / 32 : 1;
     __shared__ float qs[8][HD];
     const int wib = threadIdx.x / 32, lane = threadIdx.x & 31;
