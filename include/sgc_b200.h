@@ -410,7 +410,9 @@ int sgc_set_timing(sgc_ctx* ctx, int enable);
  * decode prefix partials: 0 = two-tile kernel, 1 = one-tile S-triple-buffered kernel; defaults
  * 0 / 1);
  * "gnn_tile" (GNN layer-map FP64 GEMM: 0 = 64x64, 1 = 64x128, 2 = 128x128 DFMA tiles, 3 = DMMA
- * tensor pipe, default); "gnn_dedup" (1 = identical node states computed once, default).
+ * tensor pipe, default); "gnn_dedup" (1 = identical node states computed once, default);
+ * "agglomerate_global" (1 = the merge loop keeps its per-row state in global memory at any m, as
+ * it always does above ~8k points; default 0).
  * Unknown names return SGC_DOMAIN. */
 int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value);
 int sgc_get_timing(sgc_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches);

@@ -3522,6 +3522,7 @@ int sgc_set_option(sgc_ctx* ctx, const char* name, int64_t value) {
         if (std::string(name) == "gemm_pairs") sgc::gemm_set_pairs(value != 0);
         else if (std::string(name) == "gemm_raster") sgc::gemm_set_raster(static_cast<int>(value));
         else if (std::string(name) == "gemm_streamk") sgc::gemm_set_streamk(static_cast<int>(value));
+        else if (std::string(name) == "agglomerate_global") sgc::agglomerate_set_global(value != 0);
         else if (std::string(name) == "attn_split") sgc::attention_set_split(value != 0);
         else if (std::string(name) == "attn_kernel") sgc::attention_set_kernel(static_cast<int>(value));
         else if (std::string(name) == "attn_kernel_partial") sgc::attention_set_kernel_partial(static_cast<int>(value));

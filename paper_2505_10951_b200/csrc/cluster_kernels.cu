@@ -84,10 +84,13 @@ constexpr int kAggThreads = 1024;
 // One CTA runs the whole merge loop. Per alive row i a cached (value, j) minimum over alive
 // j > i is maintained; after a merge only rows whose cached argmin touched keep/kill (or row
 // keep itself) are rescanned, every other row gets an O(1) update against the new D[i][keep].
+// The per-row state (25 B per point) lives in shared memory up to m ~ 8k points; larger batches
+// (`state` != nullptr) keep it in global memory (L1/L2-resident, same code and results).
 __global__ void __launch_bounds__(kAggThreads)
     agglomerate_kernel(double* D, int m, int c, int linkage, uint32_t* labels, uint32_t* merge_left,
-                       uint32_t* merge_right, double* merge_dist) {
-    extern __shared__ uint8_t sm[];
+                       uint32_t* merge_right, double* merge_dist, uint8_t* state) {
+    extern __shared__ uint8_t smem_state[];
+    uint8_t* sm = state ? state : smem_state;
     double* rv = reinterpret_cast<double*>(sm);                 // [m] row-min value
     int* rj = reinterpret_cast<int*>(rv + m);                   // [m] row-min column
     int* size = rj + m;                                         // [m]
@@ -324,25 +327,28 @@ void pairwise_distances(Ctx* c, double* D, const float* emb, int m, int dim, boo
     for (int a = 0; a < nt; ++a)
         for (int b = a; b < nt; ++b) tiles.push_back(make_int2(a, b));
     int2* dt = c->buf<int2>("pairwise_tiles", tiles.size());
-    copy_in(c, dt, tiles.data(), tiles.size());
+    copy_in_staged(c, dt, tiles.data(), tiles.size());  // pinned staging: no stream drain
     Ctx::Timed timer(c, "pairwise");
     pairwise_kernel<PT><<<tiles.size(), 256, 0, c->stream>>>(D, emb, m, dim, dt, squared ? 1 : 0);
     SGC_LAUNCH_CHECK(c);
-    // keep `tiles` alive until the async copy has consumed it
-    SGC_CUDA_CHECK(cudaStreamSynchronize(c->stream));
 }
 
 size_t agglomerate_smem(int m) { return static_cast<size_t>(m) * (8 + 4 * 4 + 1) + 16; }
+// tests: force the global-memory row state at any m (the large-batch path)
+bool g_agglomerate_global = false;
+void agglomerate_set_global(bool on) { g_agglomerate_global = on; }
 
 void agglomerate(Ctx* c, double* D, int m, int clusters, int linkage, uint32_t* labels,
                  uint32_t* merge_left, uint32_t* merge_right, double* merge_dist) {
-    size_t smem = agglomerate_smem(m);
-    if (smem > 200 * 1024) fail(SGC_DOMAIN, "agglomerate: m too large for the on-chip merge loop");
-    SGC_CUDA_CHECK(cudaFuncSetAttribute(agglomerate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)));
+    const size_t bytes = agglomerate_smem(m);
+    const bool on_chip = bytes <= 200 * 1024 && !g_agglomerate_global;
+    uint8_t* state = on_chip ? nullptr : c->buf<uint8_t>("agglomerate_state", bytes);
+    const int smem = on_chip ? static_cast<int>(bytes) : 0;
+    if (on_chip)
+        SGC_CUDA_CHECK(cudaFuncSetAttribute(agglomerate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     Ctx::Timed timer(c, "agglomerate");
     agglomerate_kernel<<<1, kAggThreads, smem, c->stream>>>(D, m, clusters, linkage, labels, merge_left,
-                                                            merge_right, merge_dist);
+                                                            merge_right, merge_dist, state);
     SGC_LAUNCH_CHECK(c);
 }
 

@@ -9,4 +9,6 @@ void pairwise_distances(Ctx* c, double* D, const float* emb, int m, int dim, boo
 // merge loop over D (destroyed); outputs are device pointers
 void agglomerate(Ctx* c, double* D, int m, int clusters, int linkage, uint32_t* labels,
                  uint32_t* merge_left, uint32_t* merge_right, double* merge_dist);
+// tests: keep the merge loop's per-row state in global memory at any m (the > ~8k-point path)
+void agglomerate_set_global(bool on);
 }  // namespace sgc

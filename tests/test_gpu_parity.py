@@ -297,6 +297,41 @@ def test_agglomerate_bit_exact_vs_restatement_large(ctx, m, d, linkage):
         assert np.array_equal(host.pairwise_distances(ctx, emb), oracle.pairwise(emb))
 
 
+@pytest.mark.parametrize("m,d,linkage", [(1024, 256, "ward"), (700, 32, "single"), (400, 48, "centroid")])
+def test_agglomerate_global_state_bit_exact(ctx, m, d, linkage):
+    """The large-batch merge loop (per-row state in global memory, used above ~8k points) gives
+    the on-chip loop's exact merges."""
+    rng = np.random.default_rng(m * 3 + d)
+    emb = rng.normal(size=(m, d)).astype(np.float32)
+    emb[m // 2: m // 2 + 10] = emb[:10]
+    c = max(1, m // 40)
+    labels, left, right, dist, ops = oracle.agglomerate(emb, linkage, c)
+    ctx.set_option("agglomerate_global", 1)
+    try:
+        a = host.agglomerate(ctx, emb, linkage, c)
+    finally:
+        ctx.set_option("agglomerate_global", 0)
+    assert np.array_equal(a.labels, labels)
+    assert np.array_equal(a.merge_left, left) and np.array_equal(a.merge_right, right)
+    assert np.array_equal(a.merge_dist, dist)
+    assert a.op_count == ops
+
+
+def test_agglomerate_beyond_on_chip_limit(ctx):
+    """m = 8400 points (past the ~8k on-chip limit that used to raise DomainError): the first 40
+    merges, labels and op count equal the restatement's."""
+    m, d = 8400, 8
+    rng = np.random.default_rng(84)
+    emb = rng.normal(size=(m, d)).astype(np.float32)
+    c = m - 40
+    labels, left, right, dist, ops = oracle.agglomerate(emb, "average", c)
+    a = host.agglomerate(ctx, emb, "average", c)
+    assert np.array_equal(a.labels, labels)
+    assert np.array_equal(a.merge_left, left) and np.array_equal(a.merge_right, right)
+    assert np.array_equal(a.merge_dist, dist)
+    assert a.op_count == ops
+
+
 # -------------------------------------------------------- graph: features / GNN / prompts
 
 @pytest.fixture(scope="module")
