@@ -1329,12 +1329,12 @@ void dispatch_bn(Ctx* c, const void* A, const void* B, int M, int N, int K, cons
     int lim = EPI == EPI_QKV ? ep.d : N;
     const int m_tiles = (M + BM - 1) / BM;
     // decode steps: stream-K over all SM pairs where it measured faster in the C3 generation run
-    // (scripts/decode_probe.py): the FFN activation GEMM at <= 128 and 257-512 rows, the residual
-    // GEMMs at 257-512 rows (<= 256 rows keep their split-K planes, whose fixed-order reduction
+    // (scripts/decode_probe.py): the FFN activation GEMM at <= 128 and 257-1024 rows, the residual
+    // GEMMs at 257-1024 rows (W2 at 513-1024 rows: 130 -> 68-85 us; <= 256 rows keep their split-K planes, whose fixed-order reduction
     // beats a 4-5-way stream-K fixup); never the QKV GEMM, whose RoPE / K-V scatter epilogue then
     // runs on the owners' critical path over a 256-column tile (57 vs 40 us per launch)
     const bool sk_rows = EPI != EPI_QKV && (M > 2 * BM || (M <= BM && EPI != EPI_RESID));
-    if (g_gemm_streamk && ep.splitk_ok && g_gemm_pairs && (sk_rows || g_gemm_streamk == 2) && M <= 4 * BM && N % 256 == 0 && lim % 256 == 0 &&
+    if (g_gemm_streamk && ep.splitk_ok && g_gemm_pairs && (sk_rows || g_gemm_streamk == 2) && M <= 8 * BM && N % 256 == 0 && lim % 256 == 0 &&
         N >= 2048 && K >= 1024 && HD <= 128) {
         launch2_sk<EPI, HD>(c, A, B, M, N, K, ep);
         return;

@@ -80,7 +80,7 @@ def test_gemm_tcgen05_vs_torch(ctx, M, N, K, epi, pairs):
     assert rel <= tol, f"rel err {rel}"
 
 
-@pytest.mark.parametrize("M", [1, 77, 128, 200, 256, 300, 512])
+@pytest.mark.parametrize("M", [1, 77, 128, 200, 256, 300, 512, 800])
 @pytest.mark.parametrize("N,K", [(12288, 4096), (4096, 4096), (2048, 14336)])
 @pytest.mark.parametrize("epi", [0, 1, 2, 3])
 def test_gemm_decode_streamk_vs_torch(ctx, M, N, K, epi):
