@@ -31,6 +31,10 @@ namespace {
 #ifndef SGC_DECODE_PAIRS
 #define SGC_DECODE_PAIRS 1
 #endif
+// decode residual split-K at <= 128 rows on CTA pairs (1) or 1-CTA 64-column tiles (0)
+#ifndef SGC_RESID_SPLIT_PAIRS_SMALL
+#define SGC_RESID_SPLIT_PAIRS_SMALL 0
+#endif
 // A/B switch: residual epilogue with 32-byte loads/stores (1) or 8-byte column pairs (0)
 #ifndef SGC_RESID_V8
 #define SGC_RESID_V8 1
@@ -1352,7 +1356,10 @@ void dispatch_bn(Ctx* c, const void* A, const void* B, int M, int N, int K, cons
             // 129-256 rows: one CTA pair per 256-column tile reads each weight tile once and
             // every activation row once per 256 columns (the 1-CTA 64-column tiles re-read all
             // rows 4x as often); same K slices, so the same partial sums
-            if (SGC_DECODE_PAIRS && g_gemm_pairs && M > BM && N % 256 == 0) launch2<EPI_F32, 0>(c, A, B, M, N, K, pe, kSplit);
+            // <= 128 rows: pairs for the long-K W2 (40.7 -> 34.4 us at 64 rows), 64-column 1-CTA
+            // tiles for Wo (18.5 vs 21 us on pairs; scripts/decode_gemm_sweep.py)
+            if (SGC_DECODE_PAIRS && g_gemm_pairs && (M > BM || K >= 2 * N || SGC_RESID_SPLIT_PAIRS_SMALL) && N % 256 == 0)
+                launch2<EPI_F32, 0>(c, A, B, M, N, K, pe, kSplit);
             else launch<64, EPI_F32, 0>(c, A, B, M, N, K, pe, kSplit);
             Ctx::Timed timer(c, "gemm_resid");
             resid_reduce_kernel<<<M, 256, 0, c->stream>>>(static_cast<float*>(ep.out), ep.out_xb, ep.out_ss, partial, M,
