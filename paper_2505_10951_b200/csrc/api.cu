@@ -370,8 +370,14 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
     sgc::embed(c, x, b.d_tokens, m->tok_emb, b.d_soft, b.d_soft_idx, d, M, bad, xb, ss_a);
     for (int l = 0; l < m->L; ++l) {
         sgc::GemmEpi e;
-        sgc::rms_scale(c, rs, ss_a, M, l == 0 ? 1 : parts, d);  // the embedding writes one slot per row
-        e.row_scale = rs;
+        if (b.dec) {  // decode step: the GEMM epilogue finalizes the row scales (no rms_scale launch)
+            e.ss_parts = ss_a;
+            e.ss_n = l == 0 ? 1 : parts;  // the embedding writes one slot per row
+            e.ss_d = d;
+        } else {
+            sgc::rms_scale(c, rs, ss_a, M, l == 0 ? 1 : parts, d);  // the embedding writes one slot per row
+            e.row_scale = rs;
+        }
         e.mode = sgc::EPI_QKV;
         e.q_out = q;
         e.k_cache = b.k_loc(l);
@@ -488,8 +494,14 @@ void forward_rows(Ctx* c, sgc_model* m, const FwdBatch& b) {
         t.mode = sgc::EPI_TANH;
         t.out = h;
         t.ldo = m->ffn;
-        sgc::rms_scale(c, rs, ss_b, M, parts, d);
-        t.row_scale = rs;
+        if (b.dec) {
+            t.ss_parts = ss_b;
+            t.ss_n = parts;
+            t.ss_d = d;
+        } else {
+            sgc::rms_scale(c, rs, ss_b, M, parts, d);
+            t.row_scale = rs;
+        }
         t.splitk_ok = b.dec != nullptr;
         sgc::gemm_bf16(c, xb, m->w1[l], M, m->ffn, d, t);
         r.out_ss = last ? nullptr : ss_a;  // the next layer's QKV input

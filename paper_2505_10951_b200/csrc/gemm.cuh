@@ -27,6 +27,12 @@ struct GemmEpi {
     // multiplies each accumulator row by row_scale[row] = 1 / sqrt(mean(x^2) + 1e-5) (QKV, TANH,
     // F32, BF16), finalized from the producer's per-chunk sums in index order (rms_scale)
     const float* row_scale = nullptr;
+    // decode steps: the epilogue finalizes the row scale itself from the producer's per-chunk
+    // sums of squares (ss_parts[row * ss_n ..], rms_scale's exact summation tree) instead of a
+    // separate rms_scale launch; ss_d = model dim
+    const float* ss_parts = nullptr;
+    int ss_n = 0;
+    int ss_d = 0;
     // EPI_RESID producer side: also store bf16(x_new) to out_xb (ld = ldo) and, per 32-column
     // chunk c of the row, its sum of squares of x_new to out_ss[row * (N / 32) + c]
     __nv_bfloat16* out_xb = nullptr;

@@ -206,6 +206,32 @@ __device__ __forceinline__ void add_parts(const PartIn& pin, uint32_t* r, int ch
     }
 }
 
+// 1 / sqrt(mean(x^2) + 1e-5) of one row from its d/32 chunk sums, in rms_scale_kernel's exact
+// order (lm_kernels.cu: lane l's sum of parts l, l+32, .. -- 4 contiguous parts per lane when
+// n = 128 -- then the xor butterfly lane 0 ends with), so the scale is bit-identical to the
+// separate launch it replaces
+__device__ __forceinline__ float rms_inv_row(const float* pr, int n, int d) {
+    float s[32];
+    if (n == 128) {
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(pr) + l);
+            s[l] = (v.x + v.y) + (v.z + v.w);
+        }
+    } else {
+#pragma unroll
+        for (int l = 0; l < 32; ++l) s[l] = 0.f;
+        for (int i = 0; i < n; ++i) s[i % 32] += __ldg(pr + i);
+    }
+    // butterfly: after the step with offset o, lane l holds (its value) + (lane l^o's value)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int l = 0; l < o; ++l) s[l] = s[l] + s[l + o];
+    }
+    return 1.0f / sqrtf(s[0] / static_cast<float>(d) + 1e-5f);
+}
+
 // Epilogue of one 128 x BN accumulator tile held in TMEM (lanes = rows): `tbase` addresses
 // this warp's 32 lanes at the tile's first column, `row` is this thread's output row.
 template <int BN, int EPI, int HD>
@@ -215,6 +241,7 @@ __device__ __forceinline__ void epilogue_tile(uint32_t tbase, int row, bool vali
     // fused RMSNorm of the A rows: one scale per accumulator row
     float inv = 1.0f;
     if (ep.row_scale && valid) inv = ep.row_scale[row];
+    else if (ep.ss_parts && valid) inv = rms_inv_row(ep.ss_parts + static_cast<size_t>(row) * ep.ss_n, ep.ss_n, ep.ss_d);
     if constexpr (EPI == EPI_QKV) {
         // one tile never straddles the q/k/v sections (d % BN == 0)
         const int d = ep.d;
