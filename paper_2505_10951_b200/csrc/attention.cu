@@ -342,12 +342,18 @@ namespace {
 #ifndef SGC_DECODE_LOCAL_MINB
 #define SGC_DECODE_LOCAL_MINB 1
 #endif
+// warps per CTA of the own-key decode attention (consecutive heads of one row: a CTA reads
+// SGC_DECODE_WPB x head_dim contiguous bytes of every key row). 32 = a whole 4096-wide key row
+// per CTA at C3: 106-108 -> 88-90 ms per generation batch vs 8 (scripts/gpu_lib_gen_ab.sh)
+#ifndef SGC_DECODE_WPB
+#define SGC_DECODE_WPB 32
+#endif
 template <int HD>
-__global__ void __launch_bounds__(256, SGC_DECODE_LOCAL_MINB) decode_local_kernel(DecodeAttnParams p) {
+__global__ void __launch_bounds__(32 * SGC_DECODE_WPB, SGC_DECODE_LOCAL_MINB) decode_local_kernel(DecodeAttnParams p) {
     constexpr int DPL = HD >= 32 ? HD / 32 : 1;
-    __shared__ float qs[8][HD];
+    __shared__ float qs[SGC_DECODE_WPB][HD];
     const int wib = threadIdx.x / 32, lane = threadIdx.x & 31;
-    const int wg = blockIdx.x * 8 + wib;
+    const int wg = blockIdx.x * SGC_DECODE_WPB + wib;
     if (wg >= p.rows * p.heads) return;  // warp-uniform; only __syncwarp below
     const int r = wg / p.heads, h = wg % p.heads;
     const float sl2 = p.scale * 1.4426950408889634f;
@@ -448,13 +454,13 @@ void decode_attention_local(Ctx* c, const DecodeAttnParams& p) {
     if (p.rows <= 0) return;
     const int hd = p.d / p.heads;
     const int warps = p.rows * p.heads;
-    const dim3 grid((warps + 7) / 8);
+    const dim3 grid((warps + SGC_DECODE_WPB - 1) / SGC_DECODE_WPB);
     Ctx::Timed timer(c, "attn_decode");
     switch (hd) {
-        case 16: decode_local_kernel<16><<<grid, 256, 0, c->stream>>>(p); break;
-        case 32: decode_local_kernel<32><<<grid, 256, 0, c->stream>>>(p); break;
-        case 64: decode_local_kernel<64><<<grid, 256, 0, c->stream>>>(p); break;
-        case 128: decode_local_kernel<128><<<grid, 256, 0, c->stream>>>(p); break;
+        case 16: decode_local_kernel<16><<<grid, 32 * SGC_DECODE_WPB, 0, c->stream>>>(p); break;
+        case 32: decode_local_kernel<32><<<grid, 32 * SGC_DECODE_WPB, 0, c->stream>>>(p); break;
+        case 64: decode_local_kernel<64><<<grid, 32 * SGC_DECODE_WPB, 0, c->stream>>>(p); break;
+        case 128: decode_local_kernel<128><<<grid, 32 * SGC_DECODE_WPB, 0, c->stream>>>(p); break;
         default: fail(SGC_DOMAIN, "decode attention: head_dim must be 16, 32, 64 or 128");
     }
     SGC_LAUNCH_CHECK(c);
