@@ -1186,13 +1186,17 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
     // encoders.cpp:142-162), then per-layer signature dedup: an instance's state after layer
     // l+1 is a function of (its state after l, [(edge, source state after l)] in ascending edge
     // order), so instances with equal signatures share one computed state -- bit-identically
+    // in-edges per instance as CSR (in_off / in_e / in_s), each instance's list in ascending
+    // edge order (the subgraph's edge list order, as the reference aggregates)
     std::vector<uint32_t> inst_node, sub_off(1, 0);
-    std::vector<std::vector<std::pair<uint32_t, uint32_t>>> inst_in;  // (edge, src instance)
+    std::vector<std::pair<uint32_t, uint32_t>> edge_dst;  // (dst instance, (edge, src) index) per edge
+    std::vector<uint32_t> tmp_e, tmp_s;
+    std::vector<uint32_t> local_dense;
     for (uint32_t u = 0; u < nu; ++u) {
         uint32_t i = uniq_first[u];
         const uint32_t base = static_cast<uint32_t>(inst_node.size());
         const uint64_t n0 = hs.noff[i], n1 = hs.noff[i + 1];
-        std::vector<uint32_t> local_dense;
+        local_dense.clear();
         for (uint64_t k = n0; k < n1; ++k) {
             if (k > n0 && hs.nodes[k] <= hs.nodes[k - 1])
                 fail(SGC_DOMAIN, "subgraph node ids must be ascending and unique");
@@ -1200,7 +1204,6 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
             local_dense.push_back(di);
             inst_node.push_back(di);
         }
-        inst_in.resize(inst_node.size());
         for (uint64_t k = hs.eoff[i]; k < hs.eoff[i + 1]; ++k) {
             uint32_t e = hs.edges[k];
             if (e >= g->n_edges) fail(SGC_INTEGRITY, "subgraph edge index " + std::to_string(e) + " out of range");
@@ -1209,22 +1212,35 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
             if (ls == local_dense.end() || *ls != g->edge_src_idx[e] || ld == local_dense.end() ||
                 *ld != g->edge_dst_idx[e])
                 fail(SGC_INTEGRITY, "subgraph edge " + std::to_string(e) + " violates closure: endpoint missing");
-            inst_in[base + (ld - local_dense.begin())].push_back({e, base + static_cast<uint32_t>(ls - local_dense.begin())});
+            edge_dst.push_back({base + static_cast<uint32_t>(ld - local_dense.begin()), static_cast<uint32_t>(tmp_e.size())});
+            tmp_e.push_back(e);
+            tmp_s.push_back(base + static_cast<uint32_t>(ls - local_dense.begin()));
         }
         sub_off.push_back(static_cast<uint32_t>(inst_node.size()));
     }
     const size_t n_inst = inst_node.size();
+    std::vector<uint32_t> in_off(n_inst + 1, 0), in_e(tmp_e.size()), in_s(tmp_e.size());
+    for (const auto& ed : edge_dst) ++in_off[ed.first + 1];
+    for (size_t v = 0; v < n_inst; ++v) in_off[v + 1] += in_off[v];
+    {
+        std::vector<uint32_t> fill(in_off.begin(), in_off.end() - 1);
+        for (const auto& ed : edge_dst) {  // stable: per instance in subgraph edge order
+            const uint32_t o = fill[ed.first]++;
+            in_e[o] = tmp_e[ed.second];
+            in_s[o] = tmp_s[ed.second];
+        }
+    }
     // layer 0 groups = distinct nodes
     std::vector<uint32_t> gid(n_inst), g0_node;
     {
-        std::unordered_map<uint32_t, uint32_t> m0;
+        std::vector<uint32_t> m0(g->n_nodes, UINT32_MAX);  // dense node -> group
         for (size_t v = 0; v < n_inst; ++v) {
-            auto it = c->gnn_dedup ? m0.find(inst_node[v]) : m0.end();
-            if (it == m0.end()) {
-                it = m0.insert_or_assign(inst_node[v], static_cast<uint32_t>(g0_node.size())).first;
+            uint32_t& slot = m0[inst_node[v]];
+            if (!c->gnn_dedup || slot == UINT32_MAX) {
+                slot = static_cast<uint32_t>(g0_node.size());
                 g0_node.push_back(inst_node[v]);
             }
-            gid[v] = it->second;
+            gid[v] = slot;
         }
     }
     struct LayerHost {
@@ -1245,22 +1261,22 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
         std::vector<uint32_t> next(n_inst);
         LayerHost& L = lh[l];
         for (size_t v = 0; v < n_inst; ++v) {
-            const auto& in = inst_in[v];
+            const uint32_t i0 = in_off[v], i1 = in_off[v + 1], n_in = i1 - i0;
             uint64_t h = sgc::mix64(0x9e3779b97f4a7c15ULL ^ gid[v]);
-            for (auto& pr : in) {
-                h = sgc::mix64(h ^ pr.first);
-                h = sgc::mix64(h ^ gid[pr.second]);
+            for (uint32_t k = i0; k < i1; ++k) {
+                h = sgc::mix64(h ^ in_e[k]);
+                h = sgc::mix64(h ^ gid[in_s[k]]);
             }
             size_t pos = static_cast<size_t>(h) & (cap - 1);
             uint32_t found = UINT32_MAX;
             for (; c->gnn_dedup && table[pos] != UINT32_MAX; pos = (pos + 1) & (cap - 1)) {
                 const uint32_t ng = table[pos];
-                if (ghash[ng] != h || L.self_row[ng] != gid[v] || L.in_off[ng + 1] - L.in_off[ng] != in.size())
+                if (ghash[ng] != h || L.self_row[ng] != gid[v] || L.in_off[ng + 1] - L.in_off[ng] != n_in)
                     continue;
                 bool eq = true;
-                for (size_t k = 0; k < in.size() && eq; ++k) {
-                    const uint32_t o = L.in_off[ng] + static_cast<uint32_t>(k);
-                    eq = L.in_gate[o] == g->n_nodes + in[k].first && L.in_src[o] == gid[in[k].second];
+                for (uint32_t k = 0; k < n_in && eq; ++k) {
+                    const uint32_t o = L.in_off[ng] + k;
+                    eq = L.in_gate[o] == g->n_nodes + in_e[i0 + k] && L.in_src[o] == gid[in_s[i0 + k]];
                 }
                 if (eq) {
                     found = ng;
@@ -1272,9 +1288,9 @@ void encode_subgraphs(Ctx* c, sgc_graph* g, const sgc_gnn_config& cfg, const Hos
                 table[pos] = found;
                 ghash.push_back(h);
                 L.self_row.push_back(gid[v]);
-                for (auto& pr : in) {
-                    L.in_src.push_back(gid[pr.second]);
-                    L.in_gate.push_back(g->n_nodes + pr.first);
+                for (uint32_t k = i0; k < i1; ++k) {
+                    L.in_src.push_back(gid[in_s[k]]);
+                    L.in_gate.push_back(g->n_nodes + in_e[k]);
                 }
                 L.in_off.push_back(static_cast<uint32_t>(L.in_src.size()));
             }
