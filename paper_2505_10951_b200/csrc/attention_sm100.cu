@@ -68,9 +68,12 @@ constexpr uint32_t kPCol = SGC_ATTN_SPLIT_S ? 64 : 0;  // TMEM column of P withi
 #ifndef SGC_ATTN_PINGPONG
 #define SGC_ATTN_PINGPONG 0
 #endif
+// share of the exponentials on the FMA pipe (pairs j with j % DEN < NUM): measured at C3 with the
+// final kernels (scripts/gpu_lib_ab.sh, attention ms/step): 0 121, 1/8 113, 1/6 113, 1/5 109,
+// 1/4 105-107, 1/3 107-108, 2/5 110, 1/2 120
 #ifndef SGC_POLY_NUM
 #define SGC_POLY_NUM 1
-#define SGC_POLY_DEN 3
+#define SGC_POLY_DEN 4
 #endif
 
 template <int HD>
