@@ -758,7 +758,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int num_tiles = m_tiles * n_tiles * ksplit;
     const int num_kb = K / BK / ksplit;
     // pair-tiles of 256 rows per raster group: the group's A rows (GROUP x 256 x K bf16) stay
-    // L2-resident (~48 MB) while the group sweeps every n-tile; larger K -> smaller group
+    // L2-resident (~32 MB) while the group sweeps every n-tile; larger K -> smaller group
 // residual GEMMs' raster group (scripts/gpu_lib_gemm_ab.sh, final kernels, gemm_resid ms/step):
 // 24 MB 293-296, 32 MB 294-295, 48 MB 296, 64 MB 297-299
 #ifndef SGC_RESID_GROUP_MB
