@@ -765,7 +765,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #define SGC_RESID_GROUP_MB 32
 #endif
 // raster-group budget (A rows of a group kept L2-resident while it sweeps the n-tiles):
-// measured at C3, 24-32 MB beats 48 (~0.7% GEMM time) and 96 (-4%)
+// measured at C3, 24-32 MB beats 48 (~0.7% GEMM time) and 96 (-4%); re-swept on the final
+// kernels: 16 MB 201 / 227 ms (QKV / W1 per step), 24 and 40 MB within noise of 32 (198-199 / 225)
 #ifndef SGC_GROUP_MB
 #define SGC_GROUP_MB 32
 #endif
