@@ -40,8 +40,12 @@ constexpr int BQ = 128;   // rows per query tile (two tiles per unit)
 constexpr int BKV = 128;  // keys per block
 // threads: loader warp, MMA warp, 2 tiles x SPLIT softmax warpgroups (SPLIT = 1: 320, 2: 576)
 bool g_attn_split = false;  // two softmax warpgroups per query tile (sgc_set_option "attn_split"; measured no faster)
-constexpr int kKStages = 3;
-constexpr int kVStages = 2;
+#ifndef SGC_ATTN_KSTAGES
+#define SGC_ATTN_KSTAGES 3
+#endif
+constexpr int kKStages = SGC_ATTN_KSTAGES;
+constexpr int kVStages = 5 - SGC_ATTN_KSTAGES;  // the K + V rings share 5 stages of shared memory
+// (K 3 / V 2 and K 2 / V 3 measured equal on the final kernel: 105.3-105.9 vs 105.2-106.0 ms per C3 step)
 // SGC_POLY_NUM / SGC_POLY_DEN of the exponential pairs run as a polynomial on the FMA pipe
 // (MUFU.EX2 offload, FA4-style); the rest on MUFU
 // the row's reference max only moves when a block max exceeds it by more than this (log2
@@ -220,10 +224,10 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sV + kVStages * C::kVBytes);
     uint64_t* q_full = bars + 0;    // [2]
     uint64_t* q_empty = bars + 2;   // [2]
-    uint64_t* k_full = bars + 4;    // [3]
-    uint64_t* k_empty = bars + 7;   // [3]
-    uint64_t* v_full = bars + 10;   // [2]
-    uint64_t* v_empty = bars + 12;  // [2]
+    uint64_t* k_full = bars + 4;                // [kKStages]
+    uint64_t* k_empty = k_full + kKStages;      // [kKStages]
+    uint64_t* v_full = k_empty + kKStages;      // [kVStages]
+    uint64_t* v_empty = v_full + kVStages;      // [kVStages] (ends at bars + 14)
     uint64_t* s_full = bars + 14;   // [2] per tile
     uint64_t* p_full = bars + 16;   // [2] per tile
     uint64_t* o_full = bars + 18;   // [2] per tile
@@ -262,11 +266,13 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
             ptx::mbar_init(&k_full[i], 1);
             ptx::mbar_init(&k_empty[i], 1);
         }
+        for (int i = 0; i < kVStages; ++i) {
+            ptx::mbar_init(&v_full[i], 1);
+            ptx::mbar_init(&v_empty[i], 1);
+        }
         for (int i = 0; i < 2; ++i) {
             ptx::mbar_init(&q_full[i], 1);
             ptx::mbar_init(&q_empty[i], 1);
-            ptx::mbar_init(&v_full[i], 1);
-            ptx::mbar_init(&v_empty[i], 1);
             ptx::mbar_init(&s_full[i], 1);
             ptx::mbar_init(&p_full[i], 128 * SPLIT);
             ptx::mbar_init(&o_full[i], 1);
@@ -328,8 +334,8 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                     for (int s = 0; s < C::kSub; ++s)
                         ptx::tma_load_2d(sK + ks * C::kKBytes + s * (BKV * 128), pfx ? &tmKp : &tmKl,
                                          &k_full[ks], h * HD + s * 64, row);
-                    const int vs = g & 1;
-                    ptx::mbar_wait(&v_empty[vs], ((g >> 1) & 1) ^ 1);
+                    const int vs = g % kVStages;
+                    ptx::mbar_wait(&v_empty[vs], ((g / kVStages) & 1) ^ 1);
                     ptx::mbar_expect_tx(&v_full[vs], C::kVBytes);
 #pragma unroll
                     for (int s = 0; s < C::kSub; ++s)
@@ -391,7 +397,7 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
             auto issue_pv = [&](int x, uint32_t kg, bool first) {  // O_X += P_X V
                 mwait(&p_full[x], gx[x] & 1, 18);
                 ptx::tc_fence_after();
-                const uint64_t vd = ptx::umma_desc_sw128_lbo(ptx::smem_u32(sV + (kg & 1) * C::kVBytes), BKV * 128, 1024);
+                const uint64_t vd = ptx::umma_desc_sw128_lbo(ptx::smem_u32(sV + (kg % kVStages) * C::kVBytes), BKV * 128, 1024);
                 const uint32_t dO = tmem_base + C::kO + x * 128, aP = tmem_base + C::kS + x * BQ + kPCol;
 #pragma unroll
                 for (int kk = 0; kk < BKV / 16; ++kk)
@@ -416,7 +422,7 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                 ptx::mma_commit_elect(&k_empty[g % kKStages]);
                 for (int j = 0; j < nbu; ++j) {
                     const uint32_t kg = g + j;
-                    mwait(&v_full[kg & 1], (kg >> 1) & 1, 17);
+                    mwait(&v_full[kg % kVStages], (kg / kVStages) & 1, 17);
                     bool waited_next_k = false;
 #if SGC_ATTN_SPLIT_S
                     for (int x = 0; x < 2; ++x) {
@@ -451,7 +457,7 @@ __global__ void __launch_bounds__(64 + 256 * SPLIT, 1)
                             ptx::mma_commit_elect(&q_empty[x]);
                         }
                     }
-                    ptx::mma_commit_elect(&v_empty[kg & 1]);
+                    ptx::mma_commit_elect(&v_empty[kg % kVStages]);
                     if (j + 1 < nbu) ptx::mma_commit_elect(&k_empty[(kg + 1) % kKStages]);
                 }
                 g += nbu;
