@@ -113,6 +113,19 @@ def test_gemm_decode_streamk_vs_torch(ctx, M, N, K, epi):
     assert torch.equal(outs[0], outs[1]), "stream-K result not deterministic"
 
 
+def test_tuning_options_roundtrip(ctx):
+    """Every documented sgc_set_option knob accepts its default (include/sgc_b200.h); an unknown
+    name is a DomainError, as the header states."""
+    from paper_2505_10951_b200 import _lib
+    defaults = {"gemm_pairs": 1, "gemm_raster": 0, "gemm_streamk": 1, "attn_split": 0, "attn_kernel": 0,
+                "attn_kernel_partial": 1, "gnn_tile": 3, "gnn_dedup": 1, "agglomerate_global": 0,
+                "decode_defer_pct": 25}
+    for name, value in defaults.items():
+        ctx.set_option(name, value)
+    with pytest.raises(_lib.DomainError):
+        ctx.set_option("no_such_option", 1)
+
+
 # ------------------------------------------------------------------------ weights
 
 def test_weights_bit_exact_vs_oracle(ctx):
